@@ -1,0 +1,42 @@
+"""P1: oracle (sparse KKT + LU) vs dense brute force (quadrature + null-space method) on tiny
+grids, levels 1 and 2 (BASELINE north_star "dense brute-force solves on
+8×8 grids must agree")."""
+import numpy as np
+import pytest
+
+from mch_inputs import random_medium
+from oracle import Oracle
+from tests.bruteforce import BruteForce
+
+
+def _find_medium(d, n, M, N, seed0):
+    # every continuum must be present in every K_p (reading R13); scan seeds deterministically
+    for seed in range(seed0, seed0 + 50):
+        kap, ids = random_medium(d, n, N, seed=seed)
+        try:
+            o = Oracle(d, n, M, 1, 2, N, kap, ids)
+            for k in o.plan.all_vertices():
+                o.local_system(k)
+            return kap, ids
+        except RuntimeError:
+            continue
+    raise AssertionError("no admissible medium")
+
+
+@pytest.mark.parametrize("d,n,M,L,N", [(2, 16, 4, 1, 2), (2, 16, 4, 2, 2), (2, 32, 4, 2, 3),
+                                       (3, 16, 4, 2, 2)])
+def test_oracle_equals_dense_bruteforce(d, n, M, L, N):
+    kap, ids = _find_medium(d, n, M, N, seed0=10 * d + N)
+    o = Oracle(d, n, M, L, 2, N, kap, ids)
+    bf = BruteForce(d, n, M, L, 2, N, kap, ids)
+    pts = list(o.plan.all_vertices())
+    if d == 3:  # corner, edge, face, interior points of both levels (parents solved on demand)
+        pts = [(0, 0, 0), (1, 0, 0), (1, 1, 0), (2, 2, 2), (1, 1, 1), (3, 2, 1), (4, 4, 4)]
+    for k in pts:
+        ro = o.solve(k)
+        rb = bf.solve(k)
+        Go, Gb = ro["G"], rb["G"]
+        scale = np.sqrt(np.outer(np.diag(Gb), np.diag(Gb))) + 1e-300
+        assert np.max(np.abs(Go - Gb) / np.maximum(np.abs(Gb), scale)) < 1e-10, k
+        po = ro["phi"].reshape(o.n_rhs, -1).T
+        assert np.abs(po - rb["phi"]).max() / np.abs(rb["phi"]).max() < 1e-10, k

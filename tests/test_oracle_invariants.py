@@ -1,0 +1,242 @@
+"""Pins P2-P9 of the oracle against closed forms, exact reductions and invariants
+(SURVEY.md §8(c)).  Every expected value below is computed here by an independent route
+(1D brute force, cell summation), never by re-calling the oracle's own arithmetic."""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+from mch_inputs import layered_medium, periodic_medium, random_medium
+from oracle import Oracle
+
+
+# ---------------------------------------------------------------------------------------
+# independent 1D discrete constrained minimisation (dense, null-space method)
+def kkt1d(kappa_cells, h, rows):
+    """min Σ_e κ_e ∫_e g'^2  s.t.  Σ_e w_re ∫_e g = t_r  for Q1 g on len(kappa_cells) cells.
+    rows: list of (cell weight array w_r (per cell), target t_r).  Returns (g nodes, energy/cell)."""
+    ne = len(kappa_cells)
+    A = np.zeros((ne + 1, ne + 1))
+    for e in range(ne):
+        A[e:e + 2, e:e + 2] += kappa_cells[e] / h * np.array([[1, -1], [-1, 1]])
+    C = np.zeros((len(rows), ne + 1))
+    t = np.zeros(len(rows))
+    for r, (w, tr) in enumerate(rows):
+        for e in range(ne):
+            C[r, e:e + 2] += w[e] * h / 2
+        t[r] = tr
+    keep = np.abs(C).sum(axis=1) > 0
+    C, t = C[keep], t[keep]
+    xp = np.linalg.lstsq(C, t, rcond=None)[0]
+    Z = sla.null_space(C)
+    y = np.linalg.solve(Z.T @ A @ Z, -Z.T @ A @ xp)
+    g = xp + Z @ y
+    dg = np.diff(g) / h
+    return g, kappa_cells * dg ** 2 * h
+
+
+def subcell_ranges(k, c, n, l=1):
+    """global fine-cell ranges of the subcells (dual blocks) along one axis, window order"""
+    out = []
+    for v in range(k - l, k + l + 1):
+        if 0 <= v <= n // c:
+            out.append((max(0, v * c - c // 2), min(n, v * c + c // 2)))
+    return out
+
+
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("k", [(2, 2), (0, 2), (1, 3)])
+def test_P2_constant_kappa_single_continuum(k):
+    """Constant κ, N = 1: φ_0 ≡ 1 (G_00 = 0) and the gradient block is κ·s·|K_p|·I with s from
+    the 1D discrete constrained problem on the same (clipped) window (tensor reduction)."""
+    n, M, kap0 = 64, 4, 2.5
+    c, h = n // M, 1.0 / n
+    kappa = np.full((n, n), kap0)
+    ids = np.zeros((n, n), dtype=np.uint8)
+    o = Oracle(2, n, M, 1, 2, 1, kappa, ids)
+    G = o.solve(k)["G"]
+    assert abs(G[0, 0]) < 1e-10 and np.abs(G[0, 1:]).max() < 1e-10
+    for m in range(2):
+        rng_ = subcell_ranges(k[m], c, n)
+        lo, hi = rng_[0][0], rng_[-1][1]
+        kp = (max(0, k[m] * c - c // 2), min(n, k[m] * c + c // 2))
+        cen = 0.5 * (kp[0] + kp[1]) * h
+        rows = []
+        xs = (np.arange(lo, hi) + 0.5) * h
+        for (a, b) in rng_:
+            w = ((np.arange(lo, hi) >= a) & (np.arange(lo, hi) < b)).astype(float)
+            rows.append((w, float(np.sum(w * (xs - cen)) * h)))
+        g, en = kkt1d(np.ones(hi - lo), h, rows)
+        inkp = (np.arange(lo, hi) >= kp[0]) & (np.arange(lo, hi) < kp[1])
+        s_len = en[inkp].sum()               # ∫_{K_p,x} g'^2
+        other = (min(n, k[1 - m] * c + c // 2) - max(0, k[1 - m] * c - c // 2)) * h
+        assert abs(G[1 + m, 1 + m] - kap0 * s_len * other) < 1e-11 * G[1 + m, 1 + m]
+    assert abs(G[1, 2]) < 1e-10 * G[1, 1]
+
+
+def test_P2_closed_form_limit_1p44():
+    """Continuum limit of the 1D l = 1 problem: φ = a·x on K_p, a = 6/5 (odd, C¹, natural BC,
+    ∫_{R_q} φ = ∫_{R_q} x) ⇒ s = a² = 1.44; the discrete s converges to it at O(h²)."""
+    errs = []
+    for c in (8, 16, 32, 64):
+        h = 1.0 / c
+        lo, hi = -3 * c // 2, 3 * c // 2
+        cells = np.arange(lo, hi)
+        xs = (cells + 0.5) * h
+        rows = []
+        for v in (-1, 0, 1):
+            w = ((cells >= v * c - c // 2) & (cells < v * c + c // 2)).astype(float)
+            rows.append((w, float(np.sum(w * xs) * h)))
+        g, en = kkt1d(np.ones(len(cells)), h, rows)
+        s = en[(cells >= -c // 2) & (cells < c // 2)].sum()
+        errs.append(s - 1.44)
+    assert abs(errs[-1]) < 1e-4
+    for a, b in zip(errs, errs[1:]):
+        assert 3.5 < a / b < 4.5
+
+
+@pytest.mark.parametrize("L", [1, 2])
+def test_P3_partition_of_unity_and_P6_symmetry(L):
+    """Σ_i φ_i ≡ 1 (natural BC, Σ_t c_t = 1), so Σ_i B_ji = 0 and Σ_j B^m_ji = 0; G = Gᵀ."""
+    kap, ids = random_medium(2, 32, 2, seed=11)
+    o = Oracle(2, 32, 4, L, 2, 2, kap, ids)
+    for k in o.plan.all_vertices():
+        r = o.solve(k)
+        phi, G = r["phi"], r["G"]
+        assert np.abs(phi[0] + phi[1] - 1.0).max() < 1e-12
+        sc = np.abs(G).max()
+        assert np.abs(G[:, :2].sum(axis=1)).max() < 1e-11 * sc
+        assert np.abs(G - G.T).max() < 1e-12 * sc
+
+
+def test_P4_layered_media_1d_reductions():
+    """Layers normal to x_2 (κ = 50 / 1): along-layer energy = κ̄_{K_p}·∫g'^2 (1D spline in x);
+    across-layer combination Σ_iφ_i^1 + Σ_j c_1j φ_j = 1D KKT in x_2 with per-(subcell,
+    continuum) constraints and targets ∫ x_2 ψ_j."""
+    n, M = 64, 4
+    c, h = n // M, 1.0 / n
+    kap, ids = layered_medium(2, n, 8, [50.0, 1.0], [3, 5])
+    o = Oracle(2, n, M, 1, 2, 2, kap, ids)
+    N, d = 2, 2
+    for k in [(2, 2), (1, 0), (4, 3)]:
+        G = o.solve(k)["G"]
+        kp = [(max(0, k[i] * c - c // 2), min(n, k[i] * c + c // 2)) for i in range(2)]
+        # along x
+        rx = subcell_ranges(k[0], c, n)
+        lo, hi = rx[0][0], rx[-1][1]
+        cells = np.arange(lo, hi)
+        xs = (cells + 0.5) * h
+        cen = 0.5 * (kp[0][0] + kp[0][1]) * h
+        rows = [(((cells >= a) & (cells < b)).astype(float), 0.0) for a, b in rx]
+        rows = [(w, float(np.sum(w * (xs - cen)) * h)) for w, _ in rows]
+        g, en = kkt1d(np.ones(len(cells)), h, rows)
+        sx = en[(cells >= kp[0][0]) & (cells < kp[0][1])].sum()
+        kbar_int = kap[kp[1][0]:kp[1][1], kp[0][0]].sum() * h  # ∫_{K_p,y} κ dy (κ = κ(y))
+        along = sum(G[N + i * d, N + ii * d] for i in range(N) for ii in range(N))
+        assert abs(along - sx * kbar_int) < 1e-10 * along
+        # across (y)
+        ry = subcell_ranges(k[1], c, n)
+        lo, hi = ry[0][0], ry[-1][1]
+        cells = np.arange(lo, hi)
+        ys = (cells + 0.5) * h
+        col = kap[lo:hi, 0]
+        idc = ids[lo:hi, 0]
+        rows = []
+        for a, b in ry:
+            for j in range(N):
+                w = ((cells >= a) & (cells < b) & (idc == j)).astype(float)
+                rows.append((w, float(np.sum(w * ys) * h)))
+        g, en = kkt1d(col, h, rows)
+        e1 = en[(cells >= kp[1][0]) & (cells < kp[1][1])].sum() * (kp[0][1] - kp[0][0]) * h
+        cyj = []
+        for j in range(N):
+            sel = idc[(cells >= kp[1][0]) & (cells < kp[1][1])] == j
+            cyj.append(ys[(cells >= kp[1][0]) & (cells < kp[1][1])][sel].mean())
+        e = np.zeros(N * (1 + d))
+        for i in range(N):
+            e[N + i * d + 1] = 1.0
+            e[i] = cyj[i]
+        across = e @ G @ e
+        assert abs(across - e1) < 1e-9 * across
+
+
+def test_P5_periodic_translation_and_exact_hierarchy():
+    """Periodic aligned medium (period H/2): interior G identical (translation invariance);
+    L = 2 interior children with interior parents have ξ ≡ 0 and G^hier = G^{L=1}."""
+    n, M = 128, 8
+    kap, ids = periodic_medium(2, n, 8, 0.3, 1.0, 20.0)
+    o1 = Oracle(2, n, M, 1, 2, 2, kap, ids)
+    o2 = Oracle(2, n, M, 2, 2, 2, kap, ids)
+    ref = o1.solve((4, 4))["G"]
+    sc = np.abs(ref).max()
+    for k in [(2, 2), (3, 5), (6, 4), (5, 5)]:
+        assert np.abs(o1.solve(k)["G"] - ref).max() < 1e-11 * sc
+    for k in [(3, 3), (3, 4), (5, 4), (3, 5), (5, 5)]:
+        r = o2.solve(k)
+        assert r["level"] == 2
+        assert np.abs(r["xi"]).max() < 1e-10
+        assert np.abs(r["G"] - o1.solve(k)["G"]).max() < 1e-11 * sc
+
+
+def test_P7_constraints_and_P8_energy():
+    """Combined fine φ meets the ORIGINAL Eq. 3/4 targets (cell-summed here); window energy of
+    the hierarchical φ ≥ the L = 1 energy at the same point; null-space perturbations raise it."""
+    n, M, N, d = 32, 4, 2, 2
+    c, h = n // M, 1.0 / n
+    kap, ids = random_medium(2, n, N, seed=11)
+    o1 = Oracle(2, n, M, 1, 2, N, kap, ids)
+    o2 = Oracle(2, n, M, 2, 2, N, kap, ids)
+    for k in [(1, 2), (3, 3), (2, 1), (1, 1)]:
+        r = o2.solve(k)
+        assert r["level"] == 2
+        lo, hi = r["lo"], r["hi"]
+        phi = r["phi"]  # (n_rhs, ny+1, nx+1)
+        cellavg = 0.25 * (phi[:, :-1, :-1] + phi[:, 1:, :-1] + phi[:, :-1, 1:] + phi[:, 1:, 1:])
+        kb = kap[lo[1]:hi[1], lo[0]:hi[0]]
+        ib = ids[lo[1]:hi[1], lo[0]:hi[0]]
+        X = (np.arange(lo[0], hi[0]) + 0.5) * h
+        Y = (np.arange(lo[1], hi[1]) + 0.5) * h
+        XX, YY = np.meshgrid(X, Y)
+        kpmask = (np.abs(XX - k[0] / M) < 0.5 / M) & (np.abs(YY - k[1] / M) < 0.5 / M)
+        cm = [[(XX if m == 0 else YY)[kpmask & (ib == j)].mean() for j in range(N)] for m in range(d)]
+        for vx in range(k[0] - 1, k[0] + 2):
+            for vy in range(k[1] - 1, k[1] + 2):
+                if not (0 <= vx <= M and 0 <= vy <= M):
+                    continue
+                qm = (np.abs(XX - vx / M) < 0.5 / M) & (np.abs(YY - vy / M) < 0.5 / M)
+                for j in range(N):
+                    sel = qm & (ib == j)
+                    meas = sel.sum() * h * h
+                    for a in range(N * (1 + d)):
+                        got = (cellavg[a][sel]).sum() * h * h
+                        if a < N:
+                            want = meas if a == j else 0.0
+                        else:
+                            i, m = divmod(a - N, d)
+                            want = ((XX if m == 0 else YY)[sel] - cm[m][j]).sum() * h * h if i == j else 0.0
+                        assert abs(got - want) < 1e-12 * max(meas, 1e-3 * h * h), (k, a, j)
+        # energies over the window
+        def energy(f):
+            gx = (f[1:, 1:] - f[1:, :-1] + f[:-1, 1:] - f[:-1, :-1]) / (2 * h)
+            gy = (f[1:, 1:] - f[:-1, 1:] + f[1:, :-1] - f[:-1, :-1]) / (2 * h)
+            # exact Q1 energy: ∫|∇f|² over a cell = h²[(gx²+gy²) + (dxy² terms)/12·...]; use the
+            # element matrix via Gauss points instead of closed form
+            gp = [0.5 - 0.5 / np.sqrt(3), 0.5 + 0.5 / np.sqrt(3)]
+            tot = np.zeros_like(kb)
+            f00, f10, f01, f11 = f[:-1, :-1], f[:-1, 1:], f[1:, :-1], f[1:, 1:]
+            for s in gp:
+                for t in gp:
+                    dx = ((f10 - f00) * (1 - t) + (f11 - f01) * t) / h
+                    dy = ((f01 - f00) * (1 - s) + (f11 - f10) * s) / h
+                    tot += 0.25 * h * h * (dx ** 2 + dy ** 2)
+            return float((kb * tot).sum())
+        r1 = o1.solve(k)
+        for a in range(N * (1 + d)):
+            assert energy(phi[a]) >= energy(r1["phi"][a]) - 1e-12 * energy(r1["phi"][a])
+
+
+def test_P9_level1_points_equal_plain_method():
+    kap, ids = random_medium(2, 32, 2, seed=11)
+    o1 = Oracle(2, 32, 4, 1, 2, 2, kap, ids)
+    o2 = Oracle(2, 32, 4, 2, 2, 2, kap, ids)
+    for k in o2.plan.S(1):
+        assert np.array_equal(o2.solve(k)["G"], o1.solve(k)["G"])
