@@ -1,0 +1,131 @@
+/*
+ * mch.h — C ABI of the B200-native hot path of hierarchical multicontinuum
+ * homogenization (arXiv 2503.01276).
+ *
+ * The library computes, for every macropoint x_p of every level n of the
+ * hierarchy, the constrained local cell problems of Eqs. (3)/(4) (level 1) and
+ * the correction problems of Eqs. (12)/(13) (levels n >= 2) on the level-n FE
+ * grid of mesh h*eta^(n-1), after the linear interpolation of preceding-level
+ * solutions (Eq. 11), followed by the energy reductions of Eq. (7):
+ *
+ *   PAPER.md:147-170 (Eqs. 3-4), 171 (c_mj), 211-224 (Eq. 7),
+ *   249-266 (Algorithm 1), 270-294 (S_n, Eq. 10), 366-374 (V_n),
+ *   382-419 (Eqs. 11-13).
+ *
+ * Readings of the paper: vertex-centred
+ * macropoints x_p = H*k, k in {0..M}^d (R1); R_p^+ = x_p +- (l+1/2)H clipped to
+ * Omega, subcells = dual blocks of the vertices within l*H (R2); natural BC on
+ * the window (R3); c_mj from K_p used in every R_q (R8); local-coordinate
+ * transport of parents (R9); d-linear parents on T_{n-1} (R10); exact Galerkin
+ * level operators (R11); Eq. (7) with prefactor 1 over K_p (R12); zero-measure
+ * constraint rows dropped (R13).
+ *
+ * All entry points return 0 (MCH_OK) or a negative MCH_E* code; they never
+ * throw.  mch_last_error() returns a message for the last failing call on the
+ * context (or the last failed mch_create when ctx is NULL).  All device work is
+ * ordered on params.stream (NULL = legacy default stream).
+ */
+#ifndef MCH_H_
+#define MCH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCH_OK             0
+#define MCH_EINVAL        -1  /* bad argument: d, N, n, M, L, eta, kappa <= 0 / non-finite, id >= N, sizes */
+#define MCH_EDIVISIBILITY -2  /* M does not divide n; H/(2h) or H/(2h eta^(L-1)) not integer; eta^(L-1) does not divide M */
+#define MCH_ERANK         -3  /* a continuum is absent from some K_p (c_mj undefined) */
+#define MCH_ENOCONV       -4  /* projected PCG did not reach the tolerance within max_iter */
+#define MCH_EORDER        -5  /* levels must be solved 1..L in order; coefficients need all levels */
+#define MCH_ECUDA         -6  /* CUDA runtime failure */
+#define MCH_ENOMEM        -7  /* device allocation failed */
+#define MCH_EPLAN         -8  /* hierarchy cannot be built (no covering parent, reading R9) */
+
+typedef struct mch_ctx mch_ctx;
+
+typedef struct {
+  int      d;              /* 2 or 3 */
+  int64_t  n;              /* fine cells per dimension; Omega = [0,1]^d, h = 1/n */
+  int      num_continua;   /* N, 1..4 (continuum ids are 0..N-1) */
+  int64_t  M;              /* macro cells per dimension, H = 1/M; (M+1)^d vertex macropoints */
+  int      levels;         /* L >= 1 */
+  int      eta;            /* coarsening factor >= 2 */
+  int      oversample;     /* l >= 1: R_p^+ = x_p +- (l+1/2)H (BASELINE: 1, i.e. a 3H window) */
+  double   rtol;           /* projected-residual tolerance of the PCG (default 1e-12 if <= 0) */
+  int      max_iter;       /* PCG iteration cap (default 20000 if <= 0) */
+  int      rank, world;    /* macropoint sharding across processes: this context solves the
+                              macropoints of each S_n whose position in S_n is congruent to
+                              rank mod world (world <= 1: all) */
+  int      keep_all;       /* 1: keep every macropoint's fine local solution (for
+                              mch_local_solution); 0: keep only parents (T_{L-1}) */
+  void*    stream;         /* cudaStream_t */
+} mch_params;
+
+typedef struct {
+  int64_t  macropoints;    /* macropoints of this level solved by this context */
+  int64_t  problems;       /* macropoints * N(1+d) right-hand sides */
+  int64_t  iters_total;    /* sum of PCG iterations over problems */
+  int64_t  iters_max;
+  int64_t  unknowns_level; /* sum over macropoints of level-n nodes of the window */
+  int64_t  cells_level;    /* sum over macropoints of level-n cells of the window */
+  double   relres_max;     /* max final projected relative residual */
+  double   ms_total;       /* device time of mch_solve_level(level) */
+  double   ms_pcg;         /* device time of the PCG kernels */
+  double   ms_setup;       /* device time of targets, operators, transport and projector setup */
+  double   ms_gram;        /* device time of combine + Eq. (7) reductions */
+  double   pcg_bytes;      /* algorithmic bytes moved by the PCG: see DESIGN.md §6 */
+} mch_level_stats;
+
+/* Validate params and inputs, copy kappa (float64, n^d, x fastest) and
+ * continuum ids (uint8, n^d, x fastest) into library-owned device memory, build
+ * the hierarchy.  inputs_on_device: 1 if the pointers are device pointers.
+ * The caller keeps ownership of its buffers.  *out is NULL on error. */
+int mch_create(const mch_params* params, const double* kappa, const uint8_t* continuum_id,
+               int inputs_on_device, mch_ctx** out);
+
+/* Algorithm 1 lines 4-7 for level `level` (1..L, strictly in order): solve the
+ * N(1+d) constrained problems of every macropoint of S_level owned by this
+ * context and compute their Eq. (7) Gram matrices.  Stream-ordered; returns
+ * after the level's device work is complete. */
+int mch_solve_level(mch_ctx* ctx, int level);
+
+/* Copy the Eq. (7) coefficients of all (M+1)^d macropoints into out,
+ * layout [(M+1)^d][n_rhs][n_rhs] with n_rhs = N(1+d), macropoints in
+ * lexicographic vertex order (x fastest); G[a][b] = int_{K_p} kappa grad(Phi_a).grad(Phi_b)
+ * with Phi = (phi_0..phi_{N-1}, phi_0^0..phi_0^{d-1}, .., phi_{N-1}^{d-1}), i.e.
+ * B_ji = G[j][i], B^m_ji = G[j][N+i*d+m], Bbar^n_ji = G[N+j*d+n][i],
+ * B^{mn}_ji = G[N+j*d+n][N+i*d+m].  Entries of macropoints owned by other ranks
+ * are left as 0 (the Python layer all-gathers them).  Requires all levels. */
+int mch_effective_coeffs(mch_ctx* ctx, double* out, size_t out_len, int out_on_device);
+
+/* |S_level| (all ranks). */
+int mch_num_macropoints(const mch_ctx* ctx, int level, int64_t* count);
+
+/* Fine-grid combined local solution phi_p (Eq. 11) of macropoint `macropoint`
+ * (lexicographic vertex index) for right-hand side `rhs` on its clipped window,
+ * x fastest; ext receives the node counts per dimension.  Available for
+ * parents (T_{L-1}) or, with keep_all, for every solved macropoint. */
+int mch_local_solution(mch_ctx* ctx, int64_t macropoint, int rhs, double* out, size_t out_len,
+                       int64_t ext[3]);
+
+int mch_get_level_stats(const mch_ctx* ctx, int level, mch_level_stats* out);
+
+/* Parent-pool layout for the multi-GPU exchange (one process per GPU): device
+ * pointer of the pool of fine parent solutions, and for macropoint index m its
+ * element offset and length (-1, 0 if not stored). */
+int mch_pool_info(const mch_ctx* ctx, double** pool, int64_t* pool_len);
+int mch_pool_slot(const mch_ctx* ctx, int64_t macropoint, int64_t* offset, int64_t* length);
+/* device pointer of the [(M+1)^d][n_rhs][n_rhs] coefficient array */
+int mch_coeffs_device(const mch_ctx* ctx, double** G);
+
+const char* mch_last_error(const mch_ctx* ctx);
+void mch_destroy(mch_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCH_H_ */

@@ -1,0 +1,79 @@
+"""ctypes binding of include/mch.h (argument marshalling only; every step runs in libmch.so).
+
+There is no fallback: if the CUDA library is missing or fails to load, importing this
+module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libmch.so")
+
+MCH_OK = 0
+ERRORS = {-1: "MCH_EINVAL", -2: "MCH_EDIVISIBILITY", -3: "MCH_ERANK", -4: "MCH_ENOCONV",
+          -5: "MCH_EORDER", -6: "MCH_ECUDA", -7: "MCH_ENOMEM", -8: "MCH_EPLAN"}
+
+# every symbol include/mch.h declares
+SYMBOLS = ["mch_create", "mch_solve_level", "mch_effective_coeffs", "mch_num_macropoints",
+           "mch_local_solution", "mch_get_level_stats", "mch_pool_info", "mch_pool_slot",
+           "mch_coeffs_device", "mch_last_error", "mch_destroy"]
+
+
+class MchParams(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int), ("n", ctypes.c_int64), ("num_continua", ctypes.c_int),
+                ("M", ctypes.c_int64), ("levels", ctypes.c_int), ("eta", ctypes.c_int),
+                ("oversample", ctypes.c_int), ("rtol", ctypes.c_double), ("max_iter", ctypes.c_int),
+                ("rank", ctypes.c_int), ("world", ctypes.c_int), ("keep_all", ctypes.c_int),
+                ("stream", ctypes.c_void_p)]
+
+
+class MchLevelStats(ctypes.Structure):
+    _fields_ = [("macropoints", ctypes.c_int64), ("problems", ctypes.c_int64),
+                ("iters_total", ctypes.c_int64), ("iters_max", ctypes.c_int64),
+                ("unknowns_level", ctypes.c_int64), ("cells_level", ctypes.c_int64),
+                ("relres_max", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("ms_pcg", ctypes.c_double), ("ms_setup", ctypes.c_double),
+                ("ms_gram", ctypes.c_double), ("pcg_bytes", ctypes.c_double)]
+
+
+class MchError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"CUDA library {LIB_PATH} is not built: run "
+                          "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    lib.mch_create.argtypes = [P(MchParams), vp, vp, i32, P(vp)]
+    lib.mch_solve_level.argtypes = [vp, i32]
+    lib.mch_effective_coeffs.argtypes = [vp, vp, ctypes.c_size_t, i32]
+    lib.mch_num_macropoints.argtypes = [vp, i32, P(i64)]
+    lib.mch_local_solution.argtypes = [vp, i64, i32, vp, ctypes.c_size_t, P(i64)]
+    lib.mch_get_level_stats.argtypes = [vp, i32, P(MchLevelStats)]
+    lib.mch_pool_info.argtypes = [vp, P(vp), P(i64)]
+    lib.mch_pool_slot.argtypes = [vp, i64, P(i64), P(i64)]
+    lib.mch_coeffs_device.argtypes = [vp, P(vp)]
+    lib.mch_last_error.argtypes = [vp]
+    lib.mch_last_error.restype = ctypes.c_char_p
+    lib.mch_destroy.argtypes = [vp]
+    lib.mch_destroy.restype = None
+    for name in SYMBOLS:
+        if name not in ("mch_last_error", "mch_destroy"):
+            getattr(lib, name).restype = i32
+    return lib
+
+
+lib = _load()
+
+
+def check(rc, ctx=None):
+    if rc != MCH_OK:
+        msg = lib.mch_last_error(ctx)
+        raise MchError(rc, msg.decode() if msg else "")

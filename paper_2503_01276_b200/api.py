@@ -1,0 +1,168 @@
+"""Thin Python API over the C ABI (include/mch.h).
+
+Names follow the ABI: ``mch_create`` / ``mch_solve_level`` / ``mch_effective_coeffs`` wrap
+the C calls one-to-one; :class:`Homogenizer` bundles them.  Inputs may be host numpy
+arrays or CUDA torch tensors; PyTorch is only used for device memory and the stream.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from ._native import MchLevelStats, MchParams, check, lib
+
+
+def _ptr(a):
+    """(pointer, on_device) of a numpy array or torch tensor (must be contiguous)."""
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data, 0
+    import torch
+    if isinstance(a, torch.Tensor):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr(), int(a.is_cuda)
+    raise TypeError(type(a))
+
+
+def _current_stream():
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_stream().cuda_stream
+    except Exception:  # pragma: no cover
+        pass
+    return None
+
+
+def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversample=1, rtol=1e-12,
+               max_iter=20000, rank=0, world=1, keep_all=False, stream=None):
+    """Returns an opaque context handle (ctypes.c_void_p)."""
+    if isinstance(kappa, np.ndarray):
+        kappa = np.ascontiguousarray(kappa, dtype=np.float64)
+        continuum_id = np.ascontiguousarray(continuum_id, dtype=np.uint8)
+    kp, kdev = _ptr(kappa)
+    ip, idev = _ptr(continuum_id)
+    if kdev != idev:
+        raise ValueError("kappa and continuum_id must both be host or both be device buffers")
+    p = MchParams(d=d, n=n, num_continua=num_continua, M=M, levels=levels, eta=eta,
+                  oversample=oversample, rtol=rtol, max_iter=max_iter, rank=rank, world=world,
+                  keep_all=int(keep_all), stream=stream if stream is not None else _current_stream())
+    ctx = ctypes.c_void_p()
+    check(lib.mch_create(ctypes.byref(p), kp, ip, kdev, ctypes.byref(ctx)), None)
+    return ctx
+
+
+def mch_solve_level(ctx, level):
+    check(lib.mch_solve_level(ctx, level), ctx)
+
+
+def mch_effective_coeffs(ctx, out):
+    op, odev = _ptr(out)
+    n = out.numel() if hasattr(out, "numel") else out.size
+    check(lib.mch_effective_coeffs(ctx, op, n, odev), ctx)
+    return out
+
+
+def mch_destroy(ctx):
+    lib.mch_destroy(ctx)
+
+
+class Homogenizer:
+    """Hierarchical multicontinuum homogenization hot path on one GPU (or one rank's shard)."""
+
+    def __init__(self, d, n, N, M, L, eta, kappa, ids, l=1, rtol=1e-12, max_iter=20000, rank=0,
+                 world=1, keep_all=False, stream=None):
+        self.d, self.n, self.N, self.M, self.L, self.eta, self.l = d, n, N, M, L, eta, l
+        self.n_rhs = N * (1 + d)
+        self.num_macropoints = (M + 1) ** d
+        self.ctx = mch_create(d, n, N, M, L, eta, kappa, ids, oversample=l, rtol=rtol,
+                              max_iter=max_iter, rank=rank, world=world, keep_all=keep_all,
+                              stream=stream)
+        self.solved = 0
+
+    @classmethod
+    def from_config(cls, cfg, kappa, ids, **kw):
+        return cls(cfg.d, cfg.n, cfg.N, cfg.M, cfg.L, cfg.eta, kappa, ids, l=cfg.l, **kw)
+
+    def solve_level(self, level):
+        mch_solve_level(self.ctx, level)
+        self.solved = level
+
+    def solve_all(self):
+        for lev in range(self.solved + 1, self.L + 1):
+            self.solve_level(lev)
+
+    def effective_coeffs(self, out=None):
+        if out is None:
+            out = np.zeros((self.num_macropoints, self.n_rhs, self.n_rhs))
+        return mch_effective_coeffs(self.ctx, out)
+
+    def coeffs_device_ptr(self):
+        p = ctypes.c_void_p()
+        check(lib.mch_coeffs_device(self.ctx, ctypes.byref(p)), self.ctx)
+        return p.value
+
+    def pool_info(self):
+        p = ctypes.c_void_p()
+        n = ctypes.c_int64()
+        check(lib.mch_pool_info(self.ctx, ctypes.byref(p), ctypes.byref(n)), self.ctx)
+        return p.value, n.value
+
+    def pool_slot(self, mp):
+        o = ctypes.c_int64()
+        n = ctypes.c_int64()
+        check(lib.mch_pool_slot(self.ctx, mp, ctypes.byref(o), ctypes.byref(n)), self.ctx)
+        return o.value, n.value
+
+    def linear_index(self, k):
+        idx = 0
+        for i in reversed(range(self.d)):
+            idx = idx * (self.M + 1) + int(k[i])
+        return idx
+
+    def local_solution(self, k, rhs):
+        """fine φ_p (Eq. 11) for macropoint k (tuple or linear index), shape [z][y][x] nodes"""
+        mp = k if isinstance(k, (int, np.integer)) else self.linear_index(k)
+        ext = (ctypes.c_int64 * 3)()
+        cap = 1
+        for _ in range(self.d):
+            cap *= (2 * self.l + 1) * (self.n // self.M) + 1
+        out = np.zeros(cap)
+        check(lib.mch_local_solution(self.ctx, mp, rhs, out.ctypes.data, cap, ext), self.ctx)
+        shape = tuple(ext[i] for i in reversed(range(self.d)))
+        return out[: int(np.prod(shape))].reshape(shape).copy()
+
+    def level_stats(self, level):
+        s = MchLevelStats()
+        check(lib.mch_get_level_stats(self.ctx, level, ctypes.byref(s)), self.ctx)
+        return {f: getattr(s, f) for f, _ in MchLevelStats._fields_}
+
+    def num_macropoints_level(self, level):
+        c = ctypes.c_int64()
+        check(lib.mch_num_macropoints(self.ctx, level, ctypes.byref(c)), self.ctx)
+        return c.value
+
+    def close(self):
+        if self.ctx is not None and self.ctx.value:
+            mch_destroy(self.ctx)
+        self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+__all__ = ["Homogenizer", "mch_create", "mch_solve_level", "mch_effective_coeffs", "mch_destroy",
+           "_native"]

@@ -1,0 +1,676 @@
+// Hot-path kernels of hierarchical multicontinuum homogenization (sm_100a).
+//
+//  k_level_ops   exact Galerkin level-n element data from fine kappa/psi (PAPER.md:369-371,
+//                reading R11): operator weights W and constraint weights m_{E,j,a}.
+//  k_targets     c_mj and the targets of Eqs. (3)/(4).
+//  k_transport   I_p = sum_t c_t phi_t(x_t + .) (Eq. 11, readings R9/R10),
+//                b = -P^T A_1 I_p and g = g0 - C_1 I_p (Eqs. 12/13, R5).
+//  k_proj_setup  Jacobi D^-1 and the projector's S^-1 = (C D^-1 C^T)^-1 per macropoint.
+//  k_pcg         projected preconditioned CG per (macropoint, rhs) for
+//                min 1/2 x^T A x - b^T x  s.t. C x = g  (Eqs. 3/4 at n = 1, 12/13 at n >= 2).
+//  k_combine     phi_p = P_n xi + I_p at fine resolution (Eq. 11).
+//  k_gram        G_p[a][b] = int_{K_p} kappa grad Phi_a . grad Phi_b (Eq. 7).
+#include <cuda_runtime.h>
+#include "device_common.cuh"
+#include "kernels.h"
+
+// ---------------------------------------------------------------------------------------
+// level-n element data (levels >= 2), one thread per global level-n cell
+__device__ __forceinline__ double int_pair(int t, double t0, double t1) {
+  // int_{t0}^{t1} lhat_a lhat_b, lhat_0 = 1-t, lhat_1 = t; type t = a+b
+  if (t == 0) return ((1 - t0) * (1 - t0) * (1 - t0) - (1 - t1) * (1 - t1) * (1 - t1)) / 3.0;
+  if (t == 1) return (t1 * t1 / 2 - t1 * t1 * t1 / 3) - (t0 * t0 / 2 - t0 * t0 * t0 / 3);
+  return (t1 * t1 * t1 - t0 * t0 * t0) / 3.0;
+}
+
+template <int D>
+__global__ void k_level_ops(LevelArgs A) {
+  const int64_t ncell = (D == 2) ? (int64_t)A.gn * A.gn : (int64_t)A.gn * A.gn * A.gn;
+  const int64_t gc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gc >= ncell) return;
+  int cc[3] = {(int)(gc % A.gn), (int)((gc / A.gn) % A.gn), (D == 3) ? (int)(gc / ((int64_t)A.gn * A.gn)) : 0};
+  const int s = A.s;
+  const double Hc = A.h * s;
+  double W[DimC<D>::NW];
+  double Mc[4 * (1 << D)];
+  for (int i = 0; i < DimC<D>::NW; i++) W[i] = 0.0;
+  for (int i = 0; i < 4 * (1 << D); i++) Mc[i] = 0.0;
+  const double hd = (D == 2) ? A.h * A.h : A.h * A.h * A.h;
+  const double wscale = A.h * ((D == 2) ? 1.0 / Hc : 1.0);  // h Hc^(D-3)
+  const int sz = (D == 3) ? s : 1;
+  for (int iz = 0; iz < sz; iz++)
+    for (int iy = 0; iy < s; iy++)
+      for (int ix = 0; ix < s; ix++) {
+        const int ii[3] = {ix, iy, iz};
+        int64_t f = 0;
+        for (int i = D - 1; i >= 0; i--) f = f * A.n + (cc[i] * s + ii[i]);
+        const double kap = A.kappa[f];
+        const int id = A.ids[f];
+        double I[3][3];  // I[dim][type]
+        double Lc[3][2]; // lhat at cell centre
+        for (int i = 0; i < D; i++) {
+          const double t0 = (double)ii[i] / s, t1 = (double)(ii[i] + 1) / s, tc = (ii[i] + 0.5) / s;
+          for (int t = 0; t < 3; t++) I[i][t] = int_pair(t, t0, t1);
+          Lc[i][0] = 1.0 - tc;
+          Lc[i][1] = tc;
+        }
+        for (int k = 0; k < D; k++) {
+          if (D == 2) {
+            const int o = 1 - k;
+            for (int t = 0; t < 3; t++) W[k * 3 + t] += kap * I[o][t];
+          } else {
+            const int o1 = (k == 0) ? 1 : 0, o2 = (k == 2) ? 1 : 2;
+            for (int t2 = 0; t2 < 3; t2++)
+              for (int t1 = 0; t1 < 3; t1++) W[k * 9 + t1 + 3 * t2] += kap * I[o1][t1] * I[o2][t2];
+          }
+        }
+        for (int a = 0; a < (1 << D); a++) {
+          double v = 1.0;
+          for (int i = 0; i < D; i++) v *= Lc[i][(a >> i) & 1];
+          Mc[id * (1 << D) + a] += v;
+        }
+      }
+  double* wo = const_cast<double*>(A.W) + gc * DimC<D>::NW;
+  for (int i = 0; i < DimC<D>::NW; i++) wo[i] = W[i] * wscale;
+  double* mo = const_cast<double*>(A.Mc) + gc * (A.N << D);
+  for (int i = 0; i < (A.N << D); i++) mo[i] = Mc[i] * hd;
+}
+
+// ---------------------------------------------------------------------------------------
+// targets: one CTA per macropoint
+template <int D>
+__global__ void k_targets(LevelArgs A) {
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  __shared__ double scratch[32 * 16];
+  __shared__ double tot[16];
+  __shared__ double cm[3][4];
+  const int N = A.N;
+  const double hd = (D == 2) ? A.h * A.h : A.h * A.h * A.h;
+  // process K_p first (subcell index of slot l in every dim), then all subcells
+  int qc = 0;
+  for (int i = D - 1; i >= 0; i--) qc = qc * A.w + A.l;
+  for (int pass = 0; pass <= A.nsub; pass++) {
+    const int q = (pass == 0) ? qc : pass - 1;
+    // fine-cell box of subcell q
+    int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
+    bool present = true;
+    int rem = q;
+    for (int i = 0; i < D; i++) {
+      const int slot = rem % A.w;
+      rem /= A.w;
+      const int v = P.k[i] - A.l + slot;
+      int flo = v * A.c - A.c / 2, fhi = v * A.c + A.c / 2;
+      flo = flo < 0 ? 0 : flo;
+      fhi = fhi > A.n ? A.n : fhi;
+      if (v < 0 || v > A.n / A.c || fhi <= flo) present = false;
+      lo[i] = flo;
+      ext[i] = fhi - flo;
+    }
+    double v[16];
+    for (int i = 0; i < 16; i++) v[i] = 0.0;
+    if (present) {
+      const int64_t cnt = (int64_t)ext[0] * ext[1] * ext[2];
+      for (int64_t idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+        const int f[3] = {lo[0] + (int)(idx % ext[0]), lo[1] + (int)((idx / ext[0]) % ext[1]),
+                          lo[2] + (int)(idx / ((int64_t)ext[0] * ext[1]))};
+        int64_t fi = 0;
+        for (int i = D - 1; i >= 0; i--) fi = fi * A.n + f[i];
+        const int id = A.ids[fi];
+        // v[j*(1+D)] = count, v[j*(1+D)+1+m] = sum (f_m + 1/2)
+        for (int j = 0; j < 4; j++) {
+          if (j == id) {
+            v[j * 4] += 1.0;
+            for (int m = 0; m < D; m++) v[j * 4 + 1 + m] += f[m] + 0.5;
+          }
+        }
+      }
+    }
+    block_sum<16>(v, scratch, tot);
+    if (pass == 0) {
+      if (threadIdx.x == 0) {
+        for (int j = 0; j < N; j++) {
+          const double cnt = tot[j * 4];
+          if (cnt == 0.0) atomicOr(&A.flags[mp], 1);
+          for (int m = 0; m < D; m++) cm[m][j] = (cnt > 0) ? (tot[j * 4 + 1 + m] * A.h) / cnt : 0.0;
+        }
+        for (int m = 0; m < D; m++)
+          for (int j = 0; j < N; j++) A.cm[(mp * 3 + m) * 4 + j] = cm[m][j];
+      }
+      __syncthreads();
+    } else {
+      if (threadIdx.x == 0) {
+        for (int j = 0; j < N; j++) {
+          const int row = q * N + j;
+          const double cnt = present ? tot[j * 4] : 0.0;
+          A.meas[(int64_t)mp * A.ncon + row] = cnt * hd;
+          double* gr = A.g0 + ((int64_t)mp * A.ncon + row) * A.n_rhs;
+          for (int a = 0; a < A.n_rhs; a++) gr[a] = 0.0;
+          gr[j] = cnt * hd;
+          for (int m = 0; m < D; m++)
+            gr[N + j * D + m] = (cnt > 0) ? hd * (tot[j * 4 + 1 + m] * A.h - cm[m][j] * cnt) : 0.0;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// transport (levels >= 2): one CTA per problem (macropoint, rhs)
+template <int D>
+__global__ void k_transport(LevelArgs A) {
+  const int prob = blockIdx.x;
+  const int mp = prob / A.n_rhs, r = prob % A.n_rhs;
+  const ProbDesc& P = A.probs[mp];
+  extern __shared__ double smem[];
+  const Geo<D> gf = fine_geo<D>(P);
+  const Geo<D> gl = level_geo<D>(A, P);
+  double* I = A.FI + P.fine_off + (int64_t)r * gf.nnodes;
+  double* Y = A.FY + P.fine_off + (int64_t)r * gf.nnodes;
+  // phase 1: I_p at fine nodes (local-coordinate transport, reading R9)
+  for (int k = threadIdx.x; k < gf.nnodes; k += blockDim.x) {
+    int x[3];
+    node_xyz<D>(gf, k, x);
+    double s = 0.0;
+    for (int t = 0; t < P.npar; t++) {
+      int64_t idx = 0;
+      for (int i = D - 1; i >= 0; i--) {
+        const int xt = P.lo[i] + x[i] + (P.par_k[t][i] - P.k[i]) * A.c - P.par_lo[t][i];
+        idx = idx * (P.par_ncf[t][i] + 1) + xt;
+      }
+      int64_t pn = 1;
+      for (int i = 0; i < D; i++) pn *= (P.par_ncf[t][i] + 1);
+      s += P.par_w[t] * A.pool[P.par_pool[t] + (int64_t)r * pn + idx];
+    }
+    I[k] = s;
+  }
+  __syncthreads();
+  // phase 2: Y = A_1 I (fine operator on the window, natural BC)
+  for (int k = threadIdx.x; k < gf.nnodes; k += blockDim.x) Y[k] = apply_node<D>(A, P, gf, I, k);
+  // C_1 I -> g = g0 - C_1 I
+  int* eb = reinterpret_cast<int*>(smem);
+  double* bins = smem + 512;  // after int area (1024 ints)
+  double* cI = bins + 32 * A.ncon;
+  __shared__ int ntask;
+  subcell_boxes<D>(A, P, gf, eb, &ntask);
+  constraint_apply<D>(A, P, gf, eb, ntask, [&](int k) { return I[k]; }, bins, cI);
+  for (int i = threadIdx.x; i < A.ncon; i += blockDim.x) {
+    const int64_t gi = ((int64_t)mp * A.ncon + i) * A.n_rhs + r;
+    A.g[gi] = A.g0[gi] - cI[i];
+  }
+  __syncthreads();
+  // phase 3: b = -P_n^T Y at level-n nodes
+  const int s = A.s;
+  double* bvec = A.B + P.vec_off + (int64_t)r * gl.nnodes;
+  for (int K = threadIdx.x; K < gl.nnodes; K += blockDim.x) {
+    int X[3];
+    node_xyz<D>(gl, K, X);
+    int flo[3], fhi[3];
+    for (int i = 0; i < 3; i++) {
+      if (i < D) {
+        flo[i] = X[i] * s - (s - 1);
+        fhi[i] = X[i] * s + (s - 1);
+        if (flo[i] < 0) flo[i] = 0;
+        if (fhi[i] > gf.nn[i] - 1) fhi[i] = gf.nn[i] - 1;
+      } else {
+        flo[i] = fhi[i] = 0;
+      }
+    }
+    double acc = 0.0;
+    for (int z = flo[2]; z <= fhi[2]; z++)
+      for (int y = flo[1]; y <= fhi[1]; y++) {
+        const double wy = 1.0 - fabs((double)(y - X[1] * s)) / s;
+        const double wz = (D == 3) ? 1.0 - fabs((double)(z - X[2] * s)) / s : 1.0;
+        for (int xx = flo[0]; xx <= fhi[0]; xx++) {
+          const double wx = 1.0 - fabs((double)(xx - X[0] * s)) / s;
+          const int xf[3] = {xx, y, z};
+          acc += wx * wy * wz * Y[node_id<D>(gf, xf)];
+        }
+      }
+    bvec[K] = -acc;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// projector setup: one CTA per macropoint
+template <int D>
+__global__ void k_proj_setup(LevelArgs A) {
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<D> g = level_geo<D>(A, P);
+  extern __shared__ double smem[];
+  const int nc = A.ncon;
+  double* S = smem;                 // nc*nc
+  double* scratch = S + nc * nc;    // 32*16
+  double* tot = scratch + 32 * 16;  // 16
+  int* eb = reinterpret_cast<int*>(tot + 16);
+  double* dinv = A.dinv + P.node_off;
+  for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) dinv[k] = 1.0 / diag_node<D>(A, P, g, k);
+  for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) S[i] = 0.0;
+  __shared__ int ntask;
+  subcell_boxes<D>(A, P, g, eb, &ntask);  // also syncs (dinv visible to block)
+  const int N = A.N;
+  // S = C D^-1 C^T over pairs of subcells that share nodes
+  for (int q1 = 0; q1 < A.nsub; q1++) {
+    for (int q2 = q1; q2 < A.nsub; q2++) {
+      const int* b1 = eb + q1 * 6;
+      const int* b2 = eb + q2 * 6;
+      int lo[3], hi[3];
+      bool empty = false;
+      for (int i = 0; i < 3; i++) {
+        if (i >= D) { lo[i] = 0; hi[i] = 0; continue; }
+        if (b1[3 + i] == 0 || b2[3 + i] == 0) { empty = true; break; }
+        lo[i] = max(b1[i], b2[i]);
+        hi[i] = min(b1[i] + b1[3 + i], b2[i] + b2[3 + i]);  // node ranges are [lo, lo+ext] inclusive
+        if (hi[i] < lo[i]) { empty = true; break; }
+      }
+      if (empty) continue;  // uniform across the block
+      const int ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
+      const int cnt = ex * ey * ez;
+      double v[16];
+      for (int i = 0; i < 16; i++) v[i] = 0.0;
+      for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+        const int x[3] = {lo[0] + idx % ex, lo[1] + (idx / ex) % ey, lo[2] + idx / (ex * ey)};
+        const int k = node_id<D>(g, x);
+        double w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0};
+        for (int ep = 0; ep < (1 << D); ep++) {
+          int e[3] = {0, 0, 0};
+          bool ok = true;
+          for (int i = 0; i < D; i++) {
+            e[i] = x[i] - 1 + ((ep >> i) & 1);
+            ok = ok && e[i] >= 0 && e[i] < g.nc[i];
+          }
+          if (!ok) continue;
+          const int q = elem_subcell<D>(A, P, g, e);
+          if (q != q1 && q != q2) continue;
+          const int a = (~ep) & ((1 << D) - 1);
+          for (int j = 0; j < N; j++) {
+            const double m = elem_m<D>(A, P, g, e, j, a);
+            if (q == q1) w1[j] += m;
+            if (q == q2) w2[j] += m;
+          }
+        }
+        const double di = dinv[k];
+        for (int j1 = 0; j1 < N; j1++)
+          for (int j2 = 0; j2 < N; j2++) v[j1 * 4 + j2] += w1[j1] * w2[j2] * di;
+      }
+      block_sum<16>(v, scratch, tot);
+      if (threadIdx.x == 0) {
+        for (int j1 = 0; j1 < N; j1++)
+          for (int j2 = 0; j2 < N; j2++) {
+            const int r1 = q1 * N + j1, r2 = q2 * N + j2;
+            S[r1 * nc + r2] = tot[j1 * 4 + j2];
+            S[r2 * nc + r1] = tot[j1 * 4 + j2];
+          }
+      }
+      __syncthreads();
+    }
+  }
+  // equilibrate, mark inactive rows, Gauss-Jordan inverse (SPD, no pivoting)
+  __shared__ double ds[128];
+  const double* meas = A.meas + (int64_t)mp * nc;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    const bool act = meas[i] > 0.0 && S[i * nc + i] > 0.0;
+    ds[i] = act ? 1.0 / sqrt(S[i * nc + i]) : 0.0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+    const int i = idx / nc, j = idx % nc;
+    if (ds[i] == 0.0 || ds[j] == 0.0)
+      S[idx] = (i == j) ? 1.0 : 0.0;
+    else
+      S[idx] = S[idx] * ds[i] * ds[j];
+  }
+  __syncthreads();
+  // in-place Gauss-Jordan: S <- S^-1
+  for (int p = 0; p < nc; p++) {
+    const double piv = S[p * nc + p];
+    __syncthreads();
+    // update all entries not in pivot row/col
+    for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+      const int i = idx / nc, j = idx % nc;
+      if (i != p && j != p) S[idx] -= S[i * nc + p] * S[p * nc + j] / piv;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      if (i != p) {
+        S[i * nc + p] = -S[i * nc + p] / piv;
+        S[p * nc + i] = S[p * nc + i] / piv;  // symmetric: row p
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) S[p * nc + p] = 1.0 / piv;
+    __syncthreads();
+  }
+  double* out = A.Sinv + (int64_t)mp * nc * nc;
+  for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+    const int i = idx / nc, j = idx % nc;
+    out[idx] = S[idx] * ds[i] * ds[j];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// projected PCG: one CTA per problem (macropoint, rhs)
+template <int D>
+__global__ void __launch_bounds__(512) k_pcg(LevelArgs A) {
+  const int prob = blockIdx.x;
+  const int mp = prob / A.n_rhs, r = prob % A.n_rhs;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<D> g = level_geo<D>(A, P);
+  const int nc = A.ncon;
+  extern __shared__ double smem[];
+  double* Si = smem;                  // nc*nc
+  double* yhat = Si + nc * nc;        // nc
+  double* cvec = yhat + nc;           // nc
+  double* tg = cvec + nc;             // nc
+  double* bins = tg + nc;             // 32*nc
+  double* scratch = bins + 32 * nc;   // 32*4
+  double* tot = scratch + 32 * 4;     // 4
+  int* eb = reinterpret_cast<int*>(tot + 4);
+  __shared__ int ntask;
+
+  const int nn = g.nnodes;
+  double* x = A.X + P.vec_off + (int64_t)r * nn;
+  double* rv = A.R + P.vec_off + (int64_t)r * nn;
+  double* p = A.P + P.vec_off + (int64_t)r * nn;
+  double* q = A.Q + P.vec_off + (int64_t)r * nn;
+  const double* b = (A.level >= 2) ? A.B + P.vec_off + (int64_t)r * nn : nullptr;
+  const double* dinv = A.dinv + P.node_off;
+  for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Si[i] = A.Sinv[(int64_t)mp * nc * nc + i];
+  subcell_boxes<D>(A, P, g, eb, &ntask);
+
+  auto sinv_apply = [&](const double* in, double* out) {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      double s = 0.0;
+      for (int j = 0; j < nc; j++) s += Si[i * nc + j] * in[j];
+      out[i] = s;
+    }
+    __syncthreads();
+  };
+  // init: x = D^-1 C^T S^-1 t, r = A x - b (unprojected), c = C D^-1 r, yhat = S^-1 c.
+  // returns rr - c.yhat (= projected r^T D^-1 r)
+  auto init = [&](const double* targets, const double* bb) -> double {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) tg[i] = targets[i];
+    __syncthreads();
+    sinv_apply(tg, yhat);
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) x[k] = dinv[k] * ct_node<D>(A, P, g, yhat, k);
+    __syncthreads();
+    double v[1] = {0.0};
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      const double rk = apply_node<D>(A, P, g, x, k) - (bb ? bb[k] : 0.0);
+      rv[k] = rk;
+      v[0] += dinv[k] * rk * rk;
+    }
+    block_sum<1>(v, scratch, tot);
+    const double rr = tot[0];
+    constraint_apply<D>(A, P, g, eb, ntask, [&](int k) { return dinv[k] * rv[k]; }, bins, cvec);
+    sinv_apply(cvec, yhat);
+    double cy = 0.0;
+    for (int j = 0; j < nc; j++) cy += cvec[j] * yhat[j];
+    return rr - cy;
+  };
+
+  // targets of this rhs: column r of g (or g0 at level 1)
+  const double* gsrc = (A.level >= 2) ? A.g : A.g0;
+  __shared__ double gcol[128], g0col[128];
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    gcol[i] = gsrc[((int64_t)mp * nc + i) * A.n_rhs + r];
+    g0col[i] = A.g0[((int64_t)mp * nc + i) * A.n_rhs + r];
+  }
+  __syncthreads();
+  double rz_ref = 0.0;
+  if (A.level >= 2) {
+    // reference scale: initial projected residual of the full (non-hierarchical) problem
+    rz_ref = init(g0col, nullptr);
+  }
+  init(gcol, b);
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) p[k] = 0.0;
+  __syncthreads();
+
+  const double tol2 = A.rtol * A.rtol;
+  double beta = 0.0, rz = 0.0, ref = 0.0;
+  int it = 0;
+  for (;; it++) {
+    // pass 1: r <- r - C^T yhat (re-projection), z = D^-1 r, p <- -z + beta p, rz = r.z
+    double v[1] = {0.0};
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      const double rk = rv[k] - ct_node<D>(A, P, g, yhat, k);
+      const double zk = dinv[k] * rk;
+      rv[k] = rk;
+      p[k] = -zk + beta * p[k];
+      v[0] += rk * zk;
+    }
+    block_sum<1>(v, scratch, tot);
+    rz = tot[0];
+    if (it == 0) ref = fmax(rz, rz_ref);
+    if (!(rz > tol2 * ref) || it >= A.max_iter) break;
+    // pass 1b: q = A p, pq
+    double w[1] = {0.0};
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      const double qk = apply_node<D>(A, P, g, p, k);
+      q[k] = qk;
+      w[0] += p[k] * qk;
+    }
+    block_sum<1>(w, scratch, tot);
+    const double alpha = rz / tot[0];
+    // pass 2: x += alpha p, r += alpha q, rr = r^T D^-1 r
+    double u[1] = {0.0};
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      x[k] += alpha * p[k];
+      const double rk = rv[k] + alpha * q[k];
+      rv[k] = rk;
+      u[0] += dinv[k] * rk * rk;
+    }
+    block_sum<1>(u, scratch, tot);
+    const double rr = tot[0];
+    constraint_apply<D>(A, P, g, eb, ntask, [&](int k) { return dinv[k] * rv[k]; }, bins, cvec);
+    sinv_apply(cvec, yhat);
+    double cy = 0.0;
+    for (int j = 0; j < nc; j++) cy += cvec[j] * yhat[j];
+    beta = (rr - cy) / rz;
+  }
+  // feasibility restoration: x += D^-1 C^T S^-1 (g - C x)
+  constraint_apply<D>(A, P, g, eb, ntask, [&](int k) { return x[k]; }, bins, cvec);
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) tg[i] = gcol[i] - cvec[i];
+  __syncthreads();
+  sinv_apply(tg, yhat);
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) x[k] += dinv[k] * ct_node<D>(A, P, g, yhat, k);
+  __syncthreads();
+  if (A.level == 1 && P.pool_off >= 0) {
+    double* dst = A.pool + P.pool_off + (int64_t)r * nn;
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) dst[k] = x[k];
+  }
+  if (threadIdx.x == 0) {
+    A.iters[prob] = it;
+    A.relres[prob] = (ref > 0.0) ? sqrt(fmax(rz, 0.0) / ref) : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// combine (levels >= 2): phi = P_n xi + I_p, one CTA per problem
+template <int D>
+__global__ void k_combine(LevelArgs A) {
+  const int prob = blockIdx.x;
+  const int mp = prob / A.n_rhs, r = prob % A.n_rhs;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<D> gf = fine_geo<D>(P);
+  const Geo<D> gl = level_geo<D>(A, P);
+  double* I = A.FI + P.fine_off + (int64_t)r * gf.nnodes;
+  const double* xi = A.X + P.vec_off + (int64_t)r * gl.nnodes;
+  double* dst = (P.pool_off >= 0) ? A.pool + P.pool_off + (int64_t)r * gf.nnodes : nullptr;
+  const int s = A.s;
+  for (int k = threadIdx.x; k < gf.nnodes; k += blockDim.x) {
+    int x[3];
+    node_xyz<D>(gf, k, x);
+    int c0[3];
+    double t[3];
+    for (int i = 0; i < 3; i++) {
+      if (i < D) {
+        c0[i] = x[i] / s;
+        t[i] = (double)(x[i] - c0[i] * s) / s;
+        if (c0[i] == gl.nc[i]) { c0[i] -= 1; t[i] = 1.0; }
+      } else {
+        c0[i] = 0;
+        t[i] = 0.0;
+      }
+    }
+    double v = 0.0;
+    for (int a = 0; a < (1 << D); a++) {
+      double wgt = 1.0;
+      int xc[3] = {0, 0, 0};
+      for (int i = 0; i < D; i++) {
+        const int ai = (a >> i) & 1;
+        wgt *= ai ? t[i] : 1.0 - t[i];
+        xc[i] = c0[i] + ai;
+      }
+      if (wgt != 0.0) v += wgt * xi[node_id<D>(gl, xc)];
+    }
+    const double phi = I[k] + v;
+    I[k] = phi;
+    if (dst) dst[k] = phi;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Gram / Eq. (7): one CTA per macropoint
+template <int D>
+__global__ void k_gram(LevelArgs A) {
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<D> gf = fine_geo<D>(P);
+  __shared__ double scratch[32 * 16];
+  __shared__ double tot[16];
+  const int nr = A.n_rhs;
+  int ext[3] = {1, 1, 1}, lo[3] = {0, 0, 0};
+  for (int i = 0; i < D; i++) {
+    lo[i] = P.kp_lo[i] - P.lo[i];
+    ext[i] = P.kp_hi[i] - P.kp_lo[i];
+  }
+  const int cnt = ext[0] * ext[1] * ext[2];
+  auto field = [&](int rr) -> const double* {
+    if (A.level == 1) return A.X + P.vec_off + (int64_t)rr * gf.nnodes;
+    return A.FI + P.fine_off + (int64_t)rr * gf.nnodes;
+  };
+  double* Gout = A.G + P.lin * nr * nr;
+  for (int a = 0; a < nr; a++) {
+    double v[16];
+    for (int i = 0; i < 16; i++) v[i] = 0.0;
+    const double* fa = field(a);
+    for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+      int e[3] = {lo[0] + idx % ext[0], lo[1] + (idx / ext[0]) % ext[1], lo[2] + idx / (ext[0] * ext[1])};
+      double W[DimC<D>::NW];
+      elem_W<D>(A, P, gf, e, W);
+      int nid[1 << D];
+      double ca[1 << D];
+      for (int bb = 0; bb < (1 << D); bb++) {
+        int xb[3] = {e[0] + (bb & 1), e[1] + ((bb >> 1) & 1), (D == 3) ? e[2] + ((bb >> 2) & 1) : 0};
+        nid[bb] = node_id<D>(gf, xb);
+        ca[bb] = fa[nid[bb]];
+      }
+      // K_E phi_a (all corners), then dot with phi_b
+      double ka[1 << D];
+      for (int c = 0; c < (1 << D); c++) ka[c] = elem_row<D>(W, ca, c);
+      for (int b = a; b < nr; b++) {
+        const double* fb = field(b);
+        double s = 0.0;
+        for (int c = 0; c < (1 << D); c++) s += ka[c] * fb[nid[c]];
+        v[b - a] += s;
+      }
+    }
+    block_sum<16>(v, scratch, tot);
+    if (threadIdx.x == 0) {
+      for (int b = a; b < nr; b++) {
+        Gout[a * nr + b] = tot[b - a];
+        Gout[b * nr + a] = tot[b - a];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// input validation: kappa > 0 finite, ids < N
+__global__ void k_validate(const double* kappa, const uint8_t* ids, int64_t cnt, int N, int* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+    const double k = kappa[i];
+    if (!(k > 0.0) || !isfinite(k) || ids[i] >= N) atomicOr(bad, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// host launchers
+static size_t pcg_smem(const LevelArgs& A) {
+  const int nc = A.ncon;
+  return sizeof(double) * ((size_t)nc * nc + 3 * nc + 32 * nc + 32 * 4 + 4) + sizeof(int) * (A.nsub * 7 + 2);
+}
+
+cudaError_t launch_level_ops(const LevelArgs& A, cudaStream_t st) {
+  const int64_t ncell = (A.D == 2) ? (int64_t)A.gn * A.gn : (int64_t)A.gn * A.gn * A.gn;
+  const int bs = 128;
+  const unsigned grid = (unsigned)((ncell + bs - 1) / bs);
+  if (A.D == 2) k_level_ops<2><<<grid, bs, 0, st>>>(A);
+  else k_level_ops<3><<<grid, bs, 0, st>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_targets(const LevelArgs& A, cudaStream_t st) {
+  if (A.D == 2) k_targets<2><<<A.nprob_mp, 256, 0, st>>>(A);
+  else k_targets<3><<<A.nprob_mp, 256, 0, st>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
+  const size_t sm = sizeof(double) * (512 + 32 * A.ncon + A.ncon);
+  const unsigned grid = (unsigned)A.nprob_mp * A.n_rhs;
+  if (A.D == 2) k_transport<2><<<grid, threads, sm, st>>>(A);
+  else k_transport<3><<<grid, threads, sm, st>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_proj_setup(const LevelArgs& A, int threads, cudaStream_t st) {
+  const size_t sm = sizeof(double) * ((size_t)A.ncon * A.ncon + 32 * 16 + 16) + sizeof(int) * (A.nsub * 7 + 2);
+  cudaError_t e;
+  if (A.D == 2) {
+    e = cudaFuncSetAttribute(k_proj_setup<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_proj_setup<2><<<A.nprob_mp, threads, sm, st>>>(A);
+  } else {
+    e = cudaFuncSetAttribute(k_proj_setup<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_proj_setup<3><<<A.nprob_mp, threads, sm, st>>>(A);
+  }
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pcg(const LevelArgs& A, int threads, cudaStream_t st) {
+  const size_t sm = pcg_smem(A);
+  const unsigned grid = (unsigned)A.nprob_mp * A.n_rhs;
+  cudaError_t e;
+  if (A.D == 2) {
+    e = cudaFuncSetAttribute(k_pcg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_pcg<2><<<grid, threads, sm, st>>>(A);
+  } else {
+    e = cudaFuncSetAttribute(k_pcg<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_pcg<3><<<grid, threads, sm, st>>>(A);
+  }
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const LevelArgs& A, int threads, cudaStream_t st) {
+  const unsigned grid = (unsigned)A.nprob_mp * A.n_rhs;
+  if (A.D == 2) k_combine<2><<<grid, threads, 0, st>>>(A);
+  else k_combine<3><<<grid, threads, 0, st>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram(const LevelArgs& A, int threads, cudaStream_t st) {
+  if (A.D == 2) k_gram<2><<<A.nprob_mp, threads, 0, st>>>(A);
+  else k_gram<3><<<A.nprob_mp, threads, 0, st>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const double* kappa, const uint8_t* ids, int64_t cnt, int N, int* bad, cudaStream_t st) {
+  k_validate<<<592, 256, 0, st>>>(kappa, ids, cnt, N, bad);
+  return cudaGetLastError();
+}

@@ -1,0 +1,479 @@
+// C ABI (include/mch.h) and per-level orchestration of Algorithm 1.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mch.h"
+#include "kernels.h"
+#include "mch_internal.h"
+#include "plan.h"
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= bytes && ptr) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    size_t alloc = std::max<size_t>(want, 256);
+    cudaError_t e = cudaMalloc(&ptr, alloc);
+    if (e == cudaSuccess) bytes = alloc;
+    return e;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(ptr); }
+};
+
+int64_t ipow64(int64_t b, int e) {
+  int64_t r = 1;
+  while (e-- > 0) r *= b;
+  return r;
+}
+
+}  // namespace
+
+struct mch_ctx {
+  mch_params p{};
+  int D = 2, N = 1, n_rhs = 3, l = 1, w = 3, nsub = 9, ncon = 9;
+  cudaStream_t st = nullptr;
+  HostPlan plan;
+  double* kappa = nullptr;
+  uint8_t* ids = nullptr;
+  double* pool = nullptr;
+  int64_t pool_len = 0;
+  std::vector<int64_t> pool_off;  // per lexicographic index
+  double* G = nullptr;
+  int solved = 0;
+  std::vector<mch_level_stats> stats;
+  std::string err;
+  // grow-only scratch
+  DevBuf descs, W, Mc, g0, g, meas, cm, flags, dinv, Sinv, X, R, P, Q, B, FI, FY, iters, relres;
+  cudaEvent_t ev[8];
+  bool events = false;
+};
+
+static int fail(mch_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  else g_create_error = msg;
+  return code;
+}
+
+#define CKC(ctx, call)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? MCH_ENOMEM : MCH_ECUDA,              \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+
+extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint8_t* ids, int on_dev,
+                          mch_ctx** out) {
+  if (!out) return fail(nullptr, MCH_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!prm || !kappa || !ids) return fail(nullptr, MCH_EINVAL, "NULL argument");
+  mch_params p = *prm;
+  if (p.d != 2 && p.d != 3) return fail(nullptr, MCH_EINVAL, "d must be 2 or 3");
+  if (p.n <= 0 || p.M <= 0 || p.levels < 1 || p.eta < 2 || p.num_continua < 1 || p.num_continua > 4)
+    return fail(nullptr, MCH_EINVAL, "bad n / M / levels / eta / num_continua");
+  if (p.oversample < 1) p.oversample = 1;
+  if (p.rtol <= 0) p.rtol = 1e-12;
+  if (p.max_iter <= 0) p.max_iter = 20000;
+  if (p.world < 1) { p.world = 1; p.rank = 0; }
+  if (p.rank < 0 || p.rank >= p.world) return fail(nullptr, MCH_EINVAL, "bad rank/world");
+  const int w = 2 * p.oversample + 1;
+  const int nsub = (p.d == 2) ? w * w : w * w * w;
+  if (nsub * p.num_continua > 128) return fail(nullptr, MCH_EINVAL, "too many constraint rows (>128)");
+  if (p.n > (1 << 20)) return fail(nullptr, MCH_EINVAL, "n too large");
+
+  mch_ctx* c = new mch_ctx();
+  c->p = p;
+  c->D = p.d;
+  c->N = p.num_continua;
+  c->n_rhs = p.num_continua * (1 + p.d);
+  c->l = p.oversample;
+  c->w = w;
+  c->nsub = nsub;
+  c->ncon = nsub * p.num_continua;
+  c->st = reinterpret_cast<cudaStream_t>(p.stream);
+  c->plan.D = p.d;
+  c->plan.n = p.n;
+  c->plan.M = p.M;
+  c->plan.L = p.levels;
+  c->plan.eta = p.eta;
+  c->plan.l = p.oversample;
+  std::string perr;
+  int rc = c->plan.build(perr);
+  if (rc != 0) {
+    delete c;
+    return fail(nullptr, rc == -8 ? MCH_EPLAN : MCH_EDIVISIBILITY, perr);
+  }
+  const int64_t cells = (p.d == 2) ? p.n * p.n : p.n * p.n * p.n;
+  // host-side validation when inputs are on the host
+  if (!on_dev) {
+    for (int64_t i = 0; i < cells; i++) {
+      if (!(kappa[i] > 0.0) || !std::isfinite(kappa[i])) {
+        delete c;
+        return fail(nullptr, MCH_EINVAL, "kappa must be positive and finite");
+      }
+      if (ids[i] >= p.num_continua) {
+        delete c;
+        return fail(nullptr, MCH_EINVAL, "continuum id >= num_continua");
+      }
+    }
+  }
+  auto cleanup = [&](int code, const std::string& m) {
+    mch_destroy(c);
+    return fail(nullptr, code, m);
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->kappa, cells * sizeof(double))) != cudaSuccess) return cleanup(MCH_ENOMEM, "kappa alloc");
+  if ((e = cudaMalloc(&c->ids, cells)) != cudaSuccess) return cleanup(MCH_ENOMEM, "ids alloc");
+  const cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  if ((e = cudaMemcpyAsync(c->kappa, kappa, cells * sizeof(double), kind, c->st)) != cudaSuccess)
+    return cleanup(MCH_ECUDA, std::string("kappa copy: ") + cudaGetErrorString(e));
+  if ((e = cudaMemcpyAsync(c->ids, ids, cells, kind, c->st)) != cudaSuccess)
+    return cleanup(MCH_ECUDA, std::string("ids copy: ") + cudaGetErrorString(e));
+  if (on_dev) {
+    int* bad = nullptr;
+    if (cudaMalloc(&bad, sizeof(int)) != cudaSuccess) return cleanup(MCH_ENOMEM, "alloc");
+    cudaMemsetAsync(bad, 0, sizeof(int), c->st);
+    launch_validate(c->kappa, c->ids, cells, p.num_continua, bad, c->st);
+    int hb = 0;
+    cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st);
+    e = cudaStreamSynchronize(c->st);
+    cudaFree(bad);
+    if (e != cudaSuccess) return cleanup(MCH_ECUDA, cudaGetErrorString(e));
+    if (hb) return cleanup(MCH_EINVAL, "kappa must be positive and finite; ids < num_continua");
+  }
+  // parent pool: T_{L-1} (or everything with keep_all)
+  const int64_t nmac = (int64_t)c->plan.all.size();
+  c->pool_off.assign(nmac, -1);
+  int64_t off = 0;
+  for (int64_t i = 0; i < nmac; i++) {
+    const MacroHost& m = c->plan.all[i];
+    if (m.level < p.levels || p.keep_all) {
+      int64_t fn = 1;
+      for (int d = 0; d < p.d; d++) fn *= (m.hi[d] - m.lo[d] + 1);
+      c->pool_off[i] = off;
+      off += fn * c->n_rhs;
+    }
+  }
+  c->pool_len = off;
+  if (off > 0 && cudaMalloc(&c->pool, off * sizeof(double)) != cudaSuccess) return cleanup(MCH_ENOMEM, "pool alloc");
+  const size_t gbytes = (size_t)nmac * c->n_rhs * c->n_rhs * sizeof(double);
+  if (cudaMalloc(&c->G, gbytes) != cudaSuccess) return cleanup(MCH_ENOMEM, "G alloc");
+  cudaMemsetAsync(c->G, 0, gbytes, c->st);
+  c->stats.assign(p.levels + 1, mch_level_stats{});
+  for (int i = 0; i < 8; i++) cudaEventCreate(&c->ev[i]);
+  c->events = true;
+  if ((e = cudaStreamSynchronize(c->st)) != cudaSuccess) return cleanup(MCH_ECUDA, cudaGetErrorString(e));
+  *out = c;
+  return MCH_OK;
+}
+
+extern "C" int mch_solve_level(mch_ctx* c, int level) {
+  if (!c) return MCH_EINVAL;
+  if (level != c->solved + 1 || level > c->p.levels)
+    return fail(c, MCH_EORDER, "levels must be solved 1..L in order");
+  const int D = c->D, N = c->N, nr = c->n_rhs, nc = c->ncon;
+  const HostPlan& pl = c->plan;
+  const int s = (int)ipow64(c->p.eta, level - 1);
+  const int gn = (int)(pl.n / s);
+  cudaStream_t st = c->st;
+  mch_level_stats& S = c->stats[level];
+  S = mch_level_stats{};
+  cudaEventRecord(c->ev[0], st);
+
+  LevelArgs A{};
+  A.D = D; A.N = N; A.n_rhs = nr; A.l = c->l; A.w = c->w; A.nsub = c->nsub; A.ncon = nc;
+  A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.gn = gn; A.h = 1.0 / (double)pl.n;
+  A.kappa = c->kappa; A.ids = c->ids; A.pool = c->pool; A.G = c->G;
+  A.rtol = c->p.rtol; A.max_iter = c->p.max_iter;
+  float ms_setup = 0, ms_pcg = 0, ms_gram = 0;
+  if (level >= 2) {
+    const int64_t gcells = (D == 2) ? (int64_t)gn * gn : (int64_t)gn * gn * gn;
+    const int NW = (D == 2) ? 6 : 27;
+    CKC(c, c->W.ensure(gcells * NW * sizeof(double)));
+    CKC(c, c->Mc.ensure(gcells * (N << D) * sizeof(double)));
+    A.W = c->W.as<double>();
+    A.Mc = c->Mc.as<double>();
+    CKC(c, launch_level_ops(A, st));
+  }
+  // this rank's macropoints of S_level
+  const std::vector<int64_t>& Sl = pl.S[level];
+  std::vector<int64_t> mine;
+  for (size_t i = 0; i < Sl.size(); i++)
+    if ((int)(i % c->p.world) == c->p.rank) mine.push_back(Sl[i]);
+  // per-macropoint sizes and batching by memory
+  auto sizes = [&](const MacroHost& m, int64_t& ln, int64_t& fnn, int64_t& lcells) {
+    ln = 1; fnn = 1; lcells = 1;
+    for (int d = 0; d < D; d++) {
+      const int ncf = m.hi[d] - m.lo[d];
+      ln *= (ncf / s + 1);
+      fnn *= (ncf + 1);
+      lcells *= ncf / s;
+    }
+  };
+  size_t freeb = 0, totb = 0;
+  cudaMemGetInfo(&freeb, &totb);
+  const double budget = std::min<double>(48e9, 0.5 * (double)freeb);
+  size_t bstart = 0;
+  std::vector<int> h_iters;
+  std::vector<double> h_relres;
+  while (bstart < mine.size()) {
+    // choose batch
+    size_t bend = bstart;
+    double bytes = 0;
+    while (bend < mine.size()) {
+      int64_t ln, fnn, lc;
+      sizes(pl.all[mine[bend]], ln, fnn, lc);
+      double b = 8.0 * (5.0 * nr * ln + ln + (double)nc * nc + 3.0 * nc * nr + nc + 12) +
+                 (level >= 2 ? 16.0 * nr * fnn : 0.0);
+      if (bend > bstart && bytes + b > budget) break;
+      bytes += b;
+      bend++;
+    }
+    const int nmp = (int)(bend - bstart);
+    std::vector<ProbDesc> descs(nmp);
+    int64_t node_off = 0, vec_off = 0, fine_off = 0;
+    int max_ln = 0, max_fn = 0;
+    for (int i = 0; i < nmp; i++) {
+      const MacroHost& m = pl.all[mine[bstart + i]];
+      ProbDesc& P = descs[i];
+      memset(&P, 0, sizeof(P));
+      int64_t ln, fnn, lc;
+      sizes(m, ln, fnn, lc);
+      for (int d = 0; d < 3; d++) {
+        P.k[d] = m.k[d];
+        P.lo[d] = (d < D) ? m.lo[d] : 0;
+        P.ncf[d] = (d < D) ? m.hi[d] - m.lo[d] : 0;
+        P.nc[d] = (d < D) ? P.ncf[d] / s : 0;
+        const int64_t a = (int64_t)m.k[d] * pl.c - pl.c / 2, b = (int64_t)m.k[d] * pl.c + pl.c / 2;
+        P.kp_lo[d] = (d < D) ? (int)std::max<int64_t>(0, a) : 0;
+        P.kp_hi[d] = (d < D) ? (int)std::min<int64_t>(pl.n, b) : 1;
+      }
+      P.lin = m.lin;
+      P.node_off = node_off;
+      P.vec_off = vec_off;
+      P.fine_off = fine_off;
+      P.pool_off = c->pool_off[m.lin];
+      node_off += ln;
+      vec_off += ln * nr;
+      if (level >= 2) fine_off += fnn * nr;
+      max_ln = std::max<int>(max_ln, (int)ln);
+      max_fn = std::max<int>(max_fn, (int)fnn);
+      P.npar = m.npar;
+      for (int t = 0; t < m.npar; t++) {
+        const MacroHost& pm = pl.all[m.par_lin[t]];
+        for (int d = 0; d < 3; d++) {
+          P.par_k[t][d] = pm.k[d];
+          P.par_lo[t][d] = (d < D) ? pm.lo[d] : 0;
+          P.par_ncf[t][d] = (d < D) ? pm.hi[d] - pm.lo[d] : 0;
+        }
+        P.par_pool[t] = c->pool_off[pm.lin];
+        P.par_w[t] = m.par_w[t];
+        if (P.par_pool[t] < 0) return fail(c, MCH_EPLAN, "parent not in pool");
+      }
+      S.unknowns_level += ln;
+      S.cells_level += lc;
+    }
+    CKC(c, c->descs.ensure(sizeof(ProbDesc) * nmp));
+    CKC(c, cudaMemcpyAsync(c->descs.ptr, descs.data(), sizeof(ProbDesc) * nmp, cudaMemcpyHostToDevice, st));
+    CKC(c, c->g0.ensure(sizeof(double) * nmp * nc * nr));
+    CKC(c, c->g.ensure(sizeof(double) * nmp * nc * nr));
+    CKC(c, c->meas.ensure(sizeof(double) * nmp * nc));
+    CKC(c, c->cm.ensure(sizeof(double) * nmp * 12));
+    CKC(c, c->flags.ensure(sizeof(int) * nmp));
+    CKC(c, c->dinv.ensure(sizeof(double) * node_off));
+    CKC(c, c->Sinv.ensure(sizeof(double) * nmp * nc * nc));
+    CKC(c, c->X.ensure(sizeof(double) * vec_off));
+    CKC(c, c->R.ensure(sizeof(double) * vec_off));
+    CKC(c, c->P.ensure(sizeof(double) * vec_off));
+    CKC(c, c->Q.ensure(sizeof(double) * vec_off));
+    CKC(c, c->B.ensure(sizeof(double) * vec_off));
+    CKC(c, c->iters.ensure(sizeof(int) * nmp * nr));
+    CKC(c, c->relres.ensure(sizeof(double) * nmp * nr));
+    if (level >= 2) {
+      CKC(c, c->FI.ensure(sizeof(double) * fine_off));
+      CKC(c, c->FY.ensure(sizeof(double) * fine_off));
+    }
+    CKC(c, cudaMemsetAsync(c->flags.ptr, 0, sizeof(int) * nmp, st));
+    A.probs = c->descs.as<ProbDesc>();
+    A.nprob_mp = nmp;
+    A.g0 = c->g0.as<double>(); A.g = c->g.as<double>(); A.meas = c->meas.as<double>();
+    A.cm = c->cm.as<double>(); A.flags = c->flags.as<int>();
+    A.dinv = c->dinv.as<double>(); A.Sinv = c->Sinv.as<double>();
+    A.X = c->X.as<double>(); A.R = c->R.as<double>(); A.P = c->P.as<double>(); A.Q = c->Q.as<double>();
+    A.B = c->B.as<double>();
+    A.FI = c->FI.as<double>(); A.FY = c->FY.as<double>();
+    A.iters = c->iters.as<int>(); A.relres = c->relres.as<double>();
+
+    auto pick = [](int nodes) {
+      int t = ((nodes / 4 + 31) / 32) * 32;
+      return std::max(64, std::min(512, t));
+    };
+    const int th_l = pick(max_ln), th_f = pick(max_fn);
+    cudaEventRecord(c->ev[1], st);
+    CKC(c, launch_targets(A, st));
+    if (level >= 2) CKC(c, launch_transport(A, th_f, st));
+    CKC(c, launch_proj_setup(A, th_l, st));
+    cudaEventRecord(c->ev[2], st);
+    CKC(c, launch_pcg(A, th_l, st));
+    cudaEventRecord(c->ev[3], st);
+    if (level >= 2) CKC(c, launch_combine(A, th_f, st));
+    CKC(c, launch_gram(A, 256, st));
+    cudaEventRecord(c->ev[4], st);
+    // results of this batch
+    std::vector<int> hf(nmp), hit(nmp * nr);
+    std::vector<double> hrr(nmp * nr);
+    CKC(c, cudaMemcpyAsync(hf.data(), c->flags.ptr, sizeof(int) * nmp, cudaMemcpyDeviceToHost, st));
+    CKC(c, cudaMemcpyAsync(hit.data(), c->iters.ptr, sizeof(int) * nmp * nr, cudaMemcpyDeviceToHost, st));
+    CKC(c, cudaMemcpyAsync(hrr.data(), c->relres.ptr, sizeof(double) * nmp * nr, cudaMemcpyDeviceToHost, st));
+    CKC(c, cudaStreamSynchronize(st));
+    float t1 = 0, t2 = 0, t3 = 0;
+    cudaEventElapsedTime(&t1, c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&t2, c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&t3, c->ev[3], c->ev[4]);
+    ms_setup += t1; ms_pcg += t2; ms_gram += t3;
+    for (int i = 0; i < nmp; i++) {
+      if (hf[i] & 1) {
+        const MacroHost& m = pl.all[mine[bstart + i]];
+        char buf[200];
+        snprintf(buf, sizeof buf, "continuum absent from K_p of macropoint (%d,%d,%d)", m.k[0], m.k[1], m.k[2]);
+        return fail(c, MCH_ERANK, buf);
+      }
+      int64_t ln, fnn, lc;
+      sizes(pl.all[mine[bstart + i]], ln, fnn, lc);
+      int mx = 0;
+      for (int r = 0; r < nr; r++) {
+        const int it = hit[i * nr + r];
+        S.iters_total += it;
+        mx = std::max(mx, it);
+        S.relres_max = std::max(S.relres_max, hrr[i * nr + r]);
+        S.pcg_bytes += 8.0 * 6.0 * (double)ln * it;
+      }
+      S.iters_max = std::max<int64_t>(S.iters_max, mx);
+      const double Dn = (level == 1) ? 1.0 : ((D == 2) ? 5.0 : 19.0);
+      S.pcg_bytes += 8.0 * Dn * (double)lc * mx;
+      if (mx >= c->p.max_iter) {
+        const MacroHost& m = pl.all[mine[bstart + i]];
+        char buf[200];
+        snprintf(buf, sizeof buf, "PCG did not converge at macropoint (%d,%d,%d): relres %.3e", m.k[0], m.k[1],
+                 m.k[2], hrr[i * nr]);
+        return fail(c, MCH_ENOCONV, buf);
+      }
+    }
+    S.macropoints += nmp;
+    S.problems += (int64_t)nmp * nr;
+    bstart = bend;
+  }
+  cudaEventRecord(c->ev[5], st);
+  CKC(c, cudaEventSynchronize(c->ev[5]));
+  float tt = 0;
+  cudaEventElapsedTime(&tt, c->ev[0], c->ev[5]);
+  S.ms_total = tt;
+  S.ms_setup = ms_setup;
+  S.ms_pcg = ms_pcg;
+  S.ms_gram = ms_gram;
+  c->solved = level;
+  return MCH_OK;
+}
+
+extern "C" int mch_effective_coeffs(mch_ctx* c, double* out, size_t out_len, int out_on_device) {
+  if (!c || !out) return MCH_EINVAL;
+  if (c->solved != c->p.levels) return fail(c, MCH_EORDER, "coefficients need all levels solved");
+  const size_t need = c->plan.all.size() * (size_t)c->n_rhs * c->n_rhs;
+  if (out_len < need) return fail(c, MCH_EINVAL, "out_len too small");
+  CKC(c, cudaMemcpyAsync(out, c->G, need * sizeof(double),
+                         out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
+  CKC(c, cudaStreamSynchronize(c->st));
+  return MCH_OK;
+}
+
+extern "C" int mch_num_macropoints(const mch_ctx* c, int level, int64_t* count) {
+  if (!c || !count || level < 1 || level > c->p.levels) return MCH_EINVAL;
+  *count = (int64_t)c->plan.S[level].size();
+  return MCH_OK;
+}
+
+extern "C" int mch_local_solution(mch_ctx* c, int64_t mp, int rhs, double* out, size_t out_len, int64_t ext[3]) {
+  if (!c || !out || mp < 0 || mp >= (int64_t)c->plan.all.size() || rhs < 0 || rhs >= c->n_rhs)
+    return c ? fail(c, MCH_EINVAL, "bad macropoint/rhs") : MCH_EINVAL;
+  const MacroHost& m = c->plan.all[mp];
+  if (c->pool_off[mp] < 0) return fail(c, MCH_EINVAL, "local solution not kept (use keep_all)");
+  if (m.level > c->solved) return fail(c, MCH_EORDER, "level not solved yet");
+  int64_t fn = 1;
+  for (int d = 0; d < 3; d++) {
+    const int64_t e = (d < c->D) ? (m.hi[d] - m.lo[d] + 1) : 1;
+    if (ext) ext[d] = e;
+    fn *= e;
+  }
+  if (out_len < (size_t)fn) return fail(c, MCH_EINVAL, "out_len too small");
+  CKC(c, cudaMemcpyAsync(out, c->pool + c->pool_off[mp] + (int64_t)rhs * fn, fn * sizeof(double),
+                         cudaMemcpyDefault, c->st));
+  CKC(c, cudaStreamSynchronize(c->st));
+  return MCH_OK;
+}
+
+extern "C" int mch_get_level_stats(const mch_ctx* c, int level, mch_level_stats* out) {
+  if (!c || !out || level < 1 || level > c->p.levels) return MCH_EINVAL;
+  *out = c->stats[level];
+  return MCH_OK;
+}
+
+extern "C" int mch_pool_info(const mch_ctx* c, double** pool, int64_t* len) {
+  if (!c) return MCH_EINVAL;
+  if (pool) *pool = c->pool;
+  if (len) *len = c->pool_len;
+  return MCH_OK;
+}
+
+extern "C" int mch_pool_slot(const mch_ctx* c, int64_t mp, int64_t* offset, int64_t* length) {
+  if (!c || mp < 0 || mp >= (int64_t)c->plan.all.size()) return MCH_EINVAL;
+  const MacroHost& m = c->plan.all[mp];
+  int64_t fn = 1;
+  for (int d = 0; d < c->D; d++) fn *= (m.hi[d] - m.lo[d] + 1);
+  if (offset) *offset = c->pool_off[mp];
+  if (length) *length = (c->pool_off[mp] >= 0) ? fn * c->n_rhs : 0;
+  return MCH_OK;
+}
+
+extern "C" int mch_coeffs_device(const mch_ctx* c, double** G) {
+  if (!c || !G) return MCH_EINVAL;
+  *G = c->G;
+  return MCH_OK;
+}
+
+extern "C" const char* mch_last_error(const mch_ctx* c) {
+  return c ? c->err.c_str() : g_create_error.c_str();
+}
+
+extern "C" void mch_destroy(mch_ctx* c) {
+  if (!c) return;
+  if (c->st) cudaStreamSynchronize(c->st);
+  else cudaDeviceSynchronize();
+  cudaFree(c->kappa);
+  cudaFree(c->ids);
+  cudaFree(c->pool);
+  cudaFree(c->G);
+  DevBuf* bufs[] = {&c->descs, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->Sinv,
+                    &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres};
+  for (DevBuf* b : bufs) b->release();
+  if (c->events)
+    for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);
+  delete c;
+}

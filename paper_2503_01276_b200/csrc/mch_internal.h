@@ -1,0 +1,57 @@
+// Internal structures shared by the host planner, the C ABI and the kernels.
+#pragma once
+#include <cstdint>
+
+#define MCH_MAXPAR 8  // 2^d parents at most (d-linear interpolation, Eq. 11)
+
+// One macropoint solved at its level (device-visible POD).
+struct ProbDesc {
+  int k[3];          // macro vertex multi-index (x_p = H k)
+  int lo[3];         // window R_p^+ lower fine-cell index (global)
+  int ncf[3];        // window fine cells per dimension
+  int nc[3];         // window level-n cells per dimension (ncf / s)
+  int kp_lo[3];      // K_p fine-cell range [kp_lo, kp_hi) (global)
+  int kp_hi[3];
+  int64_t lin;       // lexicographic macropoint index
+  int64_t node_off;  // offset of this macropoint's level-n node block (dinv)
+  int64_t vec_off;   // offset of rhs 0 of the level-n vectors; rhs r at vec_off + r*nodes
+  int64_t fine_off;  // offset of rhs 0 in the fine workspace (levels >= 2)
+  int64_t pool_off;  // offset of rhs 0 in the parent pool, -1 if not stored
+  int npar;
+  int par_k[MCH_MAXPAR][3];
+  int par_lo[MCH_MAXPAR][3];
+  int par_ncf[MCH_MAXPAR][3];
+  int64_t par_pool[MCH_MAXPAR];
+  double par_w[MCH_MAXPAR];
+};
+
+// Per-level constants passed by value to every kernel.
+struct LevelArgs {
+  int D, N, n_rhs, l, w;   // w = 2l+1 subcells per dimension
+  int nsub, ncon;          // w^D subcells, ncon = nsub*N constraint rows
+  int level, s;            // s = eta^(level-1)
+  int n, c;                // fine cells per dim, fine cells per H
+  int gn;                  // global level-n cells per dim (n/s)
+  double h;
+  const double* kappa;     // fine, n^D, x fastest
+  const uint8_t* ids;
+  const double* W;         // level >= 2: per global level-n cell, D*3^(D-1) operator weights
+  const double* Mc;        // level >= 2: per global level-n cell, N*2^D constraint weights
+  const ProbDesc* probs;
+  int nprob_mp;            // macropoints in this batch
+  // per-macropoint arrays (indexed by batch-local macropoint index)
+  double* g0;              // [mp][ncon][n_rhs] original targets (Eqs. 3/4)
+  double* g;               // [mp][ncon][n_rhs] targets of the solved problem (Eq. 12/13)
+  double* meas;            // [mp][ncon] int_{R_q} psi_j
+  double* cm;              // [mp][D][N] centring constants c_mj
+  int* flags;              // [mp] bit0: continuum absent from K_p
+  double* dinv;            // level-n node blocks
+  double* Sinv;            // [mp][ncon][ncon]
+  // per-problem vectors (problem = mp*n_rhs + r)
+  double* X; double* R; double* P; double* Q; double* B;
+  double* FI; double* FY;  // fine workspace (levels >= 2): I_p / phi and A1 I_p
+  double* pool;            // parent pool
+  double* G;               // [(M+1)^D][n_rhs][n_rhs]
+  int* iters; double* relres;  // [problem]
+  double rtol; int max_iter;
+};

@@ -1,0 +1,115 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE north_star): every effective-coefficient entry
+|ΔG_ab| ≤ 1e-8·max(|G_ab|, sqrt(G_aa G_bb)); every local solution ‖Δφ‖₂/‖φ‖₂ ≤ 1e-7 per
+macropoint and right-hand side (fine combined field on R_p^+).
+"""
+import numpy as np
+import pytest
+
+from mch_inputs import CONFIGS, make_medium, random_medium
+from oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+
+G_TOL = 1e-8
+PHI_TOL = 1e-7
+
+
+def _gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_01276_b200 import Homogenizer
+    return Homogenizer
+
+
+def g_err(Gg, Go):
+    scale = np.sqrt(np.abs(np.outer(np.diag(Go), np.diag(Go))))
+    return float(np.max(np.abs(Gg - Go) / np.maximum(np.maximum(np.abs(Go), scale), 1e-300)))
+
+
+def phi_err(pg, po):
+    return float(np.linalg.norm(pg - po) / max(np.linalg.norm(po), 1e-300))
+
+
+def _admissible(d, n, M, N, seed0):
+    for seed in range(seed0, seed0 + 50):
+        kap, ids = random_medium(d, n, N, seed=seed)
+        try:
+            o = Oracle(d, n, M, 1, 2, N, kap, ids)
+            for k in o.plan.all_vertices():
+                o.local_system(k)
+            return kap, ids
+        except RuntimeError:
+            continue
+    raise AssertionError
+
+
+@pytest.mark.parametrize("d,n,M,L,N", [(2, 16, 4, 1, 2), (2, 16, 4, 2, 2), (2, 32, 4, 2, 3),
+                                       (2, 64, 8, 3, 2), (3, 16, 4, 2, 2), (3, 16, 2, 1, 2)])
+def test_tiny_all_points(d, n, M, L, N):
+    """every macropoint of tiny random media: G and φ vs oracle (several tiles, clipped windows)"""
+    H = _gpu()
+    kap, ids = _admissible(d, n, M, N, 10 * d + N)
+    o = Oracle(d, n, M, L, 2, N, kap, ids)
+    Go = o.effective_coeffs()
+    with H(d, n, N, M, L, 2, kap, ids, keep_all=True) as h:
+        h.solve_all()
+        Gg = h.effective_coeffs()
+        for k in o.plan.all_vertices():
+            i = o.plan.linear_index(k)
+            assert g_err(Gg[i], Go[i]) < G_TOL, (k, g_err(Gg[i], Go[i]))
+            po = o.solve(k)["phi"]
+            for r in range(o.n_rhs):
+                pg = h.local_solution(k, r)
+                assert pg.shape == po[r].shape
+                assert phi_err(pg, po[r]) < PHI_TOL, (k, r, phi_err(pg, po[r]))
+
+
+def test_config1_full():
+    """BASELINE config 1 (2D 256², 81 macropoints, L = 1): every G entry, φ at sampled points"""
+    H = _gpu()
+    cfg = CONFIGS[1]
+    kap, ids = make_medium(cfg)
+    o = Oracle.from_config(cfg, kap, ids)
+    from oracle.hmh import run_parallel
+    run_parallel(o, [o.plan.S(1)])
+    Go = o.effective_coeffs()
+    with H.from_config(cfg, kap, ids, keep_all=True) as h:
+        h.solve_all()
+        Gg = h.effective_coeffs()
+        errs = [g_err(Gg[i], Go[i]) for i in range(len(Go))]
+        assert max(errs) < G_TOL, max(errs)
+        for k in [(0, 0), (4, 4), (8, 3), (1, 7)]:
+            po = o.solve(k)["phi"]
+            for r in range(cfg.n_rhs):
+                assert phi_err(h.local_solution(k, r), po[r]) < PHI_TOL
+
+
+@pytest.mark.parametrize("cid,points", [
+    (2, [(5, 5), (1, 0), (31, 32), (6, 4), (2, 3), (16, 17)]),
+    (3, [(5, 5), (63, 1), (0, 1), (34, 36), (64, 64)]),
+])
+def test_config_sampled(cid, points):
+    """BASELINE configs 2/3 at full size in the bench's launch configuration: the GPU solves every
+    macropoint; the oracle solves the sampled points (plus the ancestors they need)."""
+    H = _gpu()
+    cfg = CONFIGS[cid]
+    kap, ids = make_medium(cfg)
+    o = Oracle.from_config(cfg, kap, ids)
+    with H.from_config(cfg, kap, ids, keep_all=True) as h:
+        h.solve_all()
+        Gg = h.effective_coeffs()
+        for k in points:
+            r = o.solve(k)
+            i = o.plan.linear_index(k)
+            assert g_err(Gg[i], r["G"]) < G_TOL, (k, g_err(Gg[i], r["G"]))
+            for a in range(cfg.n_rhs):
+                e = phi_err(h.local_solution(k, a), r["phi"][a])
+                assert e < PHI_TOL, (k, a, e)
+        # properties at every macropoint: symmetry and partition of unity (Σ_i B_ji = 0)
+        N = cfg.N
+        sc = np.abs(Gg).max(axis=(1, 2))[:, None, None]
+        assert np.max(np.abs(Gg - Gg.transpose(0, 2, 1)) / sc) < 1e-12
+        assert np.max(np.abs(Gg[:, :, :N].sum(axis=2)) / sc[:, :, 0]) < 1e-10
