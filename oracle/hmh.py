@@ -37,6 +37,32 @@ class OracleError(RuntimeError):
     pass
 
 
+RANK_TOL = 1e-11
+
+
+def constraint_rows(An, Cn, g):
+    """Reading R20: if the level-n constraint rows are linearly dependent
+    (the level mesh cannot separate the continua inside a subcell, i.e. PAPER.md:374's
+    assumption that ηᴸ⁻¹h resolves the heterogeneity fails), the constraints are imposed in
+    the least-squares sense for rows normalised in the D⁻¹ norm, D = diag(A_n):
+    with S̃ = Λ C D⁻¹ Cᵀ Λ, Λ = diag(C D⁻¹ Cᵀ)^(-1/2), S̃ = V diag(λ) Vᵀ, keep the
+    eigenvectors with λ > RANK_TOL·λ_max and replace (C, g) by (V_kᵀ Λ C, V_kᵀ Λ g).
+    Full-rank systems are returned unchanged.  Returns (C, g, rank_deficient)."""
+    import scipy.sparse as sp
+    dinv = 1.0 / An.diagonal()
+    S = (Cn @ sp.diags(dinv) @ Cn.T).toarray()
+    lam = 1.0 / np.sqrt(np.diag(S))
+    St = S * lam[:, None] * lam[None, :]
+    ev, V = np.linalg.eigh(St)
+    keep = ev > RANK_TOL * ev.max()
+    if keep.all():
+        return Cn, g, False
+    Vk = V[:, keep]
+    Cr = sp.csr_matrix(Vk.T @ (lam[:, None] * Cn.toarray()))
+    gr = Vk.T @ (lam[:, None] * g)
+    return Cr, gr, True
+
+
 class Oracle:
     def __init__(self, d, n, M, L, eta, N, kappa, ids, l=1, keep_all_phi=False):
         self.plan = Plan(d, n, M, L, eta, l)
@@ -143,8 +169,12 @@ class Oracle:
             I = None
             b = np.zeros((An.shape[0], self.n_rhs))
             g = S["g0"]
-        scale = float(np.mean(An.diagonal())) / S["V"][active]
-        xi, lam, berr = solve_kkt(An, Cn[active], b, g[active], row_scale=scale)
+        Ca, ga, rank_def = constraint_rows(An, Cn[active], g[active])
+        if rank_def:
+            scale = np.full(Ca.shape[0], float(np.mean(An.diagonal())) / np.abs(Ca).sum(axis=1).max())
+        else:
+            scale = float(np.mean(An.diagonal())) / S["V"][active]
+        xi, lam, berr = solve_kkt(An, Ca, b, ga, row_scale=scale)
         phi = (P @ xi).T
         if I is not None:
             phi = phi + I

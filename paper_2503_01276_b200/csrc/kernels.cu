@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(512) k_pcg(LevelArgs A) {
     __syncthreads();
   };
   // init: x = D^-1 C^T S^-1 t, r = A x - b (unprojected), c = C D^-1 r, yhat = S^-1 c.
-  // returns rr - c.yhat (= projected r^T D^-1 r)
+  // returns r^T D^-1 r of the unprojected residual
   auto init = [&](const double* targets, const double* bb) -> double {
     for (int i = threadIdx.x; i < nc; i += blockDim.x) tg[i] = targets[i];
     __syncthreads();
@@ -406,9 +406,7 @@ __global__ void __launch_bounds__(512) k_pcg(LevelArgs A) {
     const double rr = tot[0];
     constraint_apply<D>(A, P, g, eb, ntask, [&](int k) { return dinv[k] * rv[k]; }, bins, cvec);
     sinv_apply(cvec, yhat);
-    double cy = 0.0;
-    for (int j = 0; j < nc; j++) cy += cvec[j] * yhat[j];
-    return rr - cy;
+    return rr;
   };
 
   // targets of this rhs: column r of g (or g0 at level 1)
@@ -419,18 +417,28 @@ __global__ void __launch_bounds__(512) k_pcg(LevelArgs A) {
     g0col[i] = A.g0[((int64_t)mp * nc + i) * A.n_rhs + r];
   }
   __syncthreads();
-  double rz_ref = 0.0;
+  double rz_ref = 0.0, rr_ref = 0.0;
   if (A.level >= 2) {
-    // reference scale: initial projected residual of the full (non-hierarchical) problem
-    rz_ref = init(g0col, nullptr);
+    // reference scale: initial projected residual of the full (non-hierarchical) problem,
+    // projected explicitly (no cancellation formula)
+    rr_ref = init(g0col, nullptr);
+    double v[1] = {0.0};
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      const double rk = rv[k] - ct_node<D>(A, P, g, yhat, k);
+      v[0] += dinv[k] * rk * rk;
+    }
+    block_sum<1>(v, scratch, tot);
+    rz_ref = tot[0];
   }
-  init(gcol, b);
+  const double rr0 = init(gcol, b);
   for (int k = threadIdx.x; k < nn; k += blockDim.x) p[k] = 0.0;
   __syncthreads();
 
   const double tol2 = A.rtol * A.rtol;
+  // attainable-accuracy floor: the first projection leaves roundoff of ~eps*|r_unprojected|
+  const double floor2 = 1e-30 * fmax(rr0, rr_ref);
   double beta = 0.0, rz = 0.0, ref = 0.0;
-  int it = 0;
+  int it = 0, breakdown = 0;
   for (;; it++) {
     // pass 1: r <- r - C^T yhat (re-projection), z = D^-1 r, p <- -z + beta p, rz = r.z
     double v[1] = {0.0};
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(512) k_pcg(LevelArgs A) {
     block_sum<1>(v, scratch, tot);
     rz = tot[0];
     if (it == 0) ref = fmax(rz, rz_ref);
-    if (!(rz > tol2 * ref) || it >= A.max_iter) break;
+    if (!(rz > fmax(tol2 * ref, floor2)) || it >= A.max_iter) break;
     // pass 1b: q = A p, pq
     double w[1] = {0.0};
     for (int k = threadIdx.x; k < nn; k += blockDim.x) {
@@ -453,6 +461,10 @@ __global__ void __launch_bounds__(512) k_pcg(LevelArgs A) {
       w[0] += p[k] * qk;
     }
     block_sum<1>(w, scratch, tot);
+    if (!(tot[0] > 0.0) || !isfinite(tot[0])) {  // loss of definiteness: report, do not loop
+      breakdown = 1;
+      break;
+    }
     const double alpha = rz / tot[0];
     // pass 2: x += alpha p, r += alpha q, rr = r^T D^-1 r
     double u[1] = {0.0};
@@ -484,6 +496,11 @@ __global__ void __launch_bounds__(512) k_pcg(LevelArgs A) {
   if (threadIdx.x == 0) {
     A.iters[prob] = it;
     A.relres[prob] = (ref > 0.0) ? sqrt(fmax(rz, 0.0) / ref) : 0.0;
+    double* dg = A.diag + (int64_t)prob * 4;
+    dg[0] = rz;
+    dg[1] = ref;
+    dg[2] = floor2;
+    dg[3] = breakdown;
   }
 }
 

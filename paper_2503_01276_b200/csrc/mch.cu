@@ -61,7 +61,7 @@ struct mch_ctx {
   std::vector<mch_level_stats> stats;
   std::string err;
   // grow-only scratch
-  DevBuf descs, W, Mc, g0, g, meas, cm, flags, dinv, Sinv, X, R, P, Q, B, FI, FY, iters, relres;
+  DevBuf descs, W, Mc, g0, g, meas, cm, flags, dinv, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
   cudaEvent_t ev[8];
   bool events = false;
 };
@@ -307,6 +307,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     CKC(c, c->B.ensure(sizeof(double) * vec_off));
     CKC(c, c->iters.ensure(sizeof(int) * nmp * nr));
     CKC(c, c->relres.ensure(sizeof(double) * nmp * nr));
+    CKC(c, c->diag.ensure(sizeof(double) * nmp * nr * 4));
     if (level >= 2) {
       CKC(c, c->FI.ensure(sizeof(double) * fine_off));
       CKC(c, c->FY.ensure(sizeof(double) * fine_off));
@@ -320,7 +321,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     A.X = c->X.as<double>(); A.R = c->R.as<double>(); A.P = c->P.as<double>(); A.Q = c->Q.as<double>();
     A.B = c->B.as<double>();
     A.FI = c->FI.as<double>(); A.FY = c->FY.as<double>();
-    A.iters = c->iters.as<int>(); A.relres = c->relres.as<double>();
+    A.iters = c->iters.as<int>(); A.relres = c->relres.as<double>(); A.diag = c->diag.as<double>();
 
     auto pick = [](int nodes) {
       int t = ((nodes / 4 + 31) / 32) * 32;
@@ -339,10 +340,11 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     cudaEventRecord(c->ev[4], st);
     // results of this batch
     std::vector<int> hf(nmp), hit(nmp * nr);
-    std::vector<double> hrr(nmp * nr);
+    std::vector<double> hrr(nmp * nr), hdg(nmp * nr * 4);
     CKC(c, cudaMemcpyAsync(hf.data(), c->flags.ptr, sizeof(int) * nmp, cudaMemcpyDeviceToHost, st));
     CKC(c, cudaMemcpyAsync(hit.data(), c->iters.ptr, sizeof(int) * nmp * nr, cudaMemcpyDeviceToHost, st));
     CKC(c, cudaMemcpyAsync(hrr.data(), c->relres.ptr, sizeof(double) * nmp * nr, cudaMemcpyDeviceToHost, st));
+    CKC(c, cudaMemcpyAsync(hdg.data(), c->diag.ptr, sizeof(double) * nmp * nr * 4, cudaMemcpyDeviceToHost, st));
     CKC(c, cudaStreamSynchronize(st));
     float t1 = 0, t2 = 0, t3 = 0;
     cudaEventElapsedTime(&t1, c->ev[1], c->ev[2]);
@@ -359,8 +361,11 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       int64_t ln, fnn, lc;
       sizes(pl.all[mine[bstart + i]], ln, fnn, lc);
       int mx = 0;
+      bool bad = false;
+      int badr = 0;
       for (int r = 0; r < nr; r++) {
         const int it = hit[i * nr + r];
+        if (hdg[(i * nr + r) * 4 + 3] != 0.0 || it >= c->p.max_iter) { bad = true; badr = r; }
         S.iters_total += it;
         mx = std::max(mx, it);
         S.relres_max = std::max(S.relres_max, hrr[i * nr + r]);
@@ -369,11 +374,15 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       S.iters_max = std::max<int64_t>(S.iters_max, mx);
       const double Dn = (level == 1) ? 1.0 : ((D == 2) ? 5.0 : 19.0);
       S.pcg_bytes += 8.0 * Dn * (double)lc * mx;
-      if (mx >= c->p.max_iter) {
+      if (bad) {
         const MacroHost& m = pl.all[mine[bstart + i]];
-        char buf[200];
-        snprintf(buf, sizeof buf, "PCG did not converge at macropoint (%d,%d,%d): relres %.3e", m.k[0], m.k[1],
-                 m.k[2], hrr[i * nr]);
+        const double* dg = &hdg[(i * nr + badr) * 4];
+        char buf[320];
+        snprintf(buf, sizeof buf,
+                 "PCG did not converge at level %d macropoint (%d,%d,%d) rhs %d: %s after %d iterations, "
+                 "relres %.3e (rz %.3e, ref %.3e, floor %.3e)",
+                 level, m.k[0], m.k[1], m.k[2], badr, dg[3] != 0.0 ? "breakdown" : "iteration cap",
+                 hit[i * nr + badr], hrr[i * nr + badr], dg[0], dg[1], dg[2]);
         return fail(c, MCH_ENOCONV, buf);
       }
     }
@@ -471,7 +480,7 @@ extern "C" void mch_destroy(mch_ctx* c) {
   cudaFree(c->pool);
   cudaFree(c->G);
   DevBuf* bufs[] = {&c->descs, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->Sinv,
-                    &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres};
+                    &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres, &c->diag};
   for (DevBuf* b : bufs) b->release();
   if (c->events)
     for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);

@@ -53,5 +53,6 @@ struct LevelArgs {
   double* pool;            // parent pool
   double* G;               // [(M+1)^D][n_rhs][n_rhs]
   int* iters; double* relres;  // [problem]
+  double* diag;            // [problem][4]: final rz, reference rz, floor, breakdown flag
   double rtol; int max_iter;
 };

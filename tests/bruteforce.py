@@ -156,8 +156,14 @@ class BruteForce:
         Cn = (C1 @ P)[active]
         b = -P.T @ (A1 @ I)
         g = (g0 - C1 @ I)[active]
-        xp = np.linalg.lstsq(Cn, g, rcond=None)[0]
-        Z = sla.null_space(Cn)
+        # rows normalised in the D⁻¹ norm (D = diag A_n); constraints imposed in the
+        # least-squares sense when the level-n rows are dependent (reading R20)
+        dn = np.diag(An)
+        ds = 1.0 / np.sqrt(np.einsum("ij,j,ij->i", Cn, 1.0 / dn, Cn))
+        Cn = ds[:, None] * Cn
+        g = ds[:, None] * g
+        xp = np.linalg.lstsq(Cn, g, rcond=1e-9)[0]
+        Z = sla.null_space(Cn, rcond=1e-9)
         y = np.linalg.solve(Z.T @ An @ Z, Z.T @ (b - An @ xp))
         xi = xp + Z @ y
         phi = P @ xi + I

@@ -4,7 +4,7 @@ grids, levels 1 and 2 (BASELINE north_star "dense brute-for
 import numpy as np
 import pytest
 
-from mch_inputs import random_medium
+from mch_inputs import periodic_medium, random_medium
 from oracle import Oracle
 from tests.bruteforce import BruteForce
 
@@ -40,3 +40,20 @@ def test_oracle_equals_dense_bruteforce(d, n, M, L, N):
         assert np.max(np.abs(Go - Gb) / np.maximum(np.abs(Gb), scale)) < 1e-10, k
         po = ro["phi"].reshape(o.n_rhs, -1).T
         assert np.abs(po - rb["phi"]).max() / np.abs(rb["phi"]).max() < 1e-10, k
+
+
+def test_rank_deficient_level_constraints():
+    """Reading R20: a level mesh equal to the period of a centred inclusion (level 3, mesh 4h,
+    period 4h) makes the two continuum rows of a subcell proportional in V_3; oracle (eigen
+    truncation + KKT) equals the brute force (least squares + null space)."""
+    kap, ids = periodic_medium(2, 64, 4, 0.3, 1.0, 30.0)
+    o = Oracle(2, 64, 8, 3, 2, 2, kap, ids)
+    bf = BruteForce(2, 64, 8, 3, 2, 2, kap, ids)
+    for k in [(1, 0), (1, 1), (3, 2), (0, 1), (2, 1), (7, 8), (5, 3)]:
+        ro, rb = o.solve(k), bf.solve(k)
+        assert ro["level"] == 3
+        Go, Gb = ro["G"], rb["G"]
+        scale = np.sqrt(np.outer(np.diag(Gb), np.diag(Gb))) + 1e-300
+        assert np.max(np.abs(Go - Gb) / np.maximum(np.abs(Gb), scale)) < 1e-9, k
+        po = ro["phi"].reshape(o.n_rhs, -1).T
+        assert np.abs(po - rb["phi"]).max() / np.abs(rb["phi"]).max() < 1e-9, k
