@@ -78,6 +78,8 @@ typedef struct {
   double   ms_setup;       /* device time of targets, operators, transport and projector setup */
   double   ms_gram;        /* device time of combine + Eq. (7) reductions */
   double   pcg_bytes;      /* algorithmic bytes moved by the PCG: see DESIGN.md §6 */
+  int64_t  rank_deficient; /* windows whose level-n constraint rows were dependent (reading R20:
+                              constraints imposed in the least-squares sense) */
 } mch_level_stats;
 
 /* Validate params and inputs, copy kappa (float64, n^d, x fastest) and

@@ -208,17 +208,22 @@ class Oracle:
 _POOL_ORACLE = None
 
 
+_POOL_KEEP = False
+
+
 def _pool_solve(k):
     r = _POOL_ORACLE.solve(k)
-    return k, r["G"], (r["phi"] if r["level"] < _POOL_ORACLE.L else None), _POOL_ORACLE.timings[k]
+    keep = _POOL_KEEP or r["level"] < _POOL_ORACLE.L
+    return k, r["G"], (r["phi"] if keep else None), _POOL_ORACLE.timings[k]
 
 
-def run_parallel(oracle: Oracle, points_by_level, workers=None):
+def run_parallel(oracle: Oracle, points_by_level, workers=None, keep_phi=False):
     """Solve macropoints level by level with a fork-based process pool (one macropoint
     per task); parents must be in earlier levels of ``points_by_level``.  Returns
     (per-level wall seconds, workers used)."""
     import multiprocessing as mp
-    global _POOL_ORACLE
+    global _POOL_ORACLE, _POOL_KEEP
+    _POOL_KEEP = keep_phi
     workers = workers or len(os.sched_getaffinity(0))
     ctx = mp.get_context("fork")
     walls = []

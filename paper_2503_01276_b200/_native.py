@@ -35,7 +35,8 @@ class MchLevelStats(ctypes.Structure):
                 ("unknowns_level", ctypes.c_int64), ("cells_level", ctypes.c_int64),
                 ("relres_max", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("ms_pcg", ctypes.c_double), ("ms_setup", ctypes.c_double),
-                ("ms_gram", ctypes.c_double), ("pcg_bytes", ctypes.c_double)]
+                ("ms_gram", ctypes.c_double), ("pcg_bytes", ctypes.c_double),
+                ("rank_deficient", ctypes.c_int64)]
 
 
 class MchError(RuntimeError):

@@ -245,6 +245,7 @@ __global__ void k_proj_setup(LevelArgs A) {
   double* scratch = S + nc * nc;    // 32*16
   double* tot = scratch + 32 * 16;  // 16
   int* eb = reinterpret_cast<int*>(tot + 16);
+  double* eb_end = tot + 16 + (A.nsub * 7 + 2 + 1) / 2 + 1;  // V (nc*nc) after the int area
   double* dinv = A.dinv + P.node_off;
   for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) dinv[k] = 1.0 / diag_node<D>(A, P, g, k);
   for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) S[i] = 0.0;
@@ -323,11 +324,16 @@ __global__ void k_proj_setup(LevelArgs A) {
       S[idx] = S[idx] * ds[i] * ds[j];
   }
   __syncthreads();
-  // in-place Gauss-Jordan: S <- S^-1
+  // backup S~ in V, then in-place Gauss-Jordan: S <- S~^-1, tracking the smallest pivot
+  double* V = eb_end;
+  for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) V[idx] = S[idx];
+  __shared__ double minpiv;
+  if (threadIdx.x == 0) minpiv = 1e300;
+  __syncthreads();
   for (int p = 0; p < nc; p++) {
     const double piv = S[p * nc + p];
     __syncthreads();
-    // update all entries not in pivot row/col
+    if (threadIdx.x == 0) minpiv = fmin(minpiv, piv);
     for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
       const int i = idx / nc, j = idx % nc;
       if (i != p && j != p) S[idx] -= S[i * nc + p] * S[p * nc + j] / piv;
@@ -336,7 +342,7 @@ __global__ void k_proj_setup(LevelArgs A) {
     for (int i = threadIdx.x; i < nc; i += blockDim.x) {
       if (i != p) {
         S[i * nc + p] = -S[i * nc + p] / piv;
-        S[p * nc + i] = S[p * nc + i] / piv;  // symmetric: row p
+        S[p * nc + i] = S[p * nc + i] / piv;
       }
     }
     __syncthreads();
@@ -344,9 +350,93 @@ __global__ void k_proj_setup(LevelArgs A) {
     __syncthreads();
   }
   double* out = A.Sinv + (int64_t)mp * nc * nc;
+  if (minpiv > 1e-10) {
+    for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+      const int i = idx / nc, j = idx % nc;
+      out[idx] = S[idx] * ds[i] * ds[j];
+    }
+    return;
+  }
+  // Reading R20: dependent level-n constraint rows.  Pseudo-inverse of S~ by cyclic Jacobi
+  // eigen-decomposition, eigenvalues below 1e-11 lambda_max dropped.
+  if (threadIdx.x == 0) atomicOr(&A.flags[mp], 2);
+  for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+    S[idx] = V[idx];
+    V[idx] = (idx / nc == idx % nc) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  __shared__ double rot[3];
+  __shared__ int skip;
+  for (int sweep = 0; sweep < 40; sweep++) {
+    double v[2] = {0.0, 0.0};
+    for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+      const int i = idx / nc, j = idx % nc;
+      const double a = S[idx];
+      if (i < j) v[0] += a * a;
+      else if (i == j) v[1] += a * a;
+    }
+    block_sum<2>(v, scratch, tot);
+    if (tot[0] <= 1e-34 * tot[1]) break;
+    for (int p = 0; p < nc - 1; p++) {
+      for (int q = p + 1; q < nc; q++) {
+        if (threadIdx.x == 0) {
+          const double apq = S[p * nc + q];
+          if (fabs(apq) < 1e-300) {
+            skip = 1;
+          } else {
+            skip = 0;
+            const double th = (S[q * nc + q] - S[p * nc + p]) / (2.0 * apq);
+            const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+            const double cc = 1.0 / sqrt(t * t + 1.0);
+            rot[0] = cc;
+            rot[1] = t * cc;
+            rot[2] = t;
+          }
+        }
+        __syncthreads();
+        if (!skip) {
+          const double cc = rot[0], ss = rot[1], t = rot[2];
+          const double apq = S[p * nc + q];
+          for (int k = threadIdx.x; k < nc; k += blockDim.x) {
+            if (k != p && k != q) {
+              const double skp = S[k * nc + p], skq = S[k * nc + q];
+              const double nkp = cc * skp - ss * skq, nkq = ss * skp + cc * skq;
+              S[k * nc + p] = nkp;
+              S[p * nc + k] = nkp;
+              S[k * nc + q] = nkq;
+              S[q * nc + k] = nkq;
+            }
+            const double vkp = V[k * nc + p], vkq = V[k * nc + q];
+            V[k * nc + p] = cc * vkp - ss * vkq;
+            V[k * nc + q] = ss * vkp + cc * vkq;
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            S[p * nc + p] -= t * apq;
+            S[q * nc + q] += t * apq;
+            S[p * nc + q] = 0.0;
+            S[q * nc + p] = 0.0;
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  __shared__ double lmax;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < nc; i++) m = fmax(m, S[i * nc + i]);
+    lmax = m;
+  }
+  __syncthreads();
   for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
     const int i = idx / nc, j = idx % nc;
-    out[idx] = S[idx] * ds[i] * ds[j];
+    double acc = 0.0;
+    for (int k = 0; k < nc; k++) {
+      const double lk = S[k * nc + k];
+      if (lk > 1e-11 * lmax) acc += V[i * nc + k] * V[j * nc + k] / lk;
+    }
+    out[idx] = acc * ds[i] * ds[j];
   }
 }
 
@@ -646,7 +736,7 @@ cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
 }
 
 cudaError_t launch_proj_setup(const LevelArgs& A, int threads, cudaStream_t st) {
-  const size_t sm = sizeof(double) * ((size_t)A.ncon * A.ncon + 32 * 16 + 16) + sizeof(int) * (A.nsub * 7 + 2);
+  const size_t sm = sizeof(double) * (2 * (size_t)A.ncon * A.ncon + 32 * 16 + 16 + (A.nsub * 7 + 2 + 1) / 2 + 2);
   cudaError_t e;
   if (A.D == 2) {
     e = cudaFuncSetAttribute(k_proj_setup<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

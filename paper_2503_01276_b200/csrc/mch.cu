@@ -96,7 +96,7 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   if (p.rank < 0 || p.rank >= p.world) return fail(nullptr, MCH_EINVAL, "bad rank/world");
   const int w = 2 * p.oversample + 1;
   const int nsub = (p.d == 2) ? w * w : w * w * w;
-  if (nsub * p.num_continua > 128) return fail(nullptr, MCH_EINVAL, "too many constraint rows (>128)");
+  if (nsub * p.num_continua > 108) return fail(nullptr, MCH_EINVAL, "too many constraint rows (>108)");
   if (p.n > (1 << 20)) return fail(nullptr, MCH_EINVAL, "n too large");
 
   mch_ctx* c = new mch_ctx();
@@ -352,6 +352,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     cudaEventElapsedTime(&t3, c->ev[3], c->ev[4]);
     ms_setup += t1; ms_pcg += t2; ms_gram += t3;
     for (int i = 0; i < nmp; i++) {
+      if (hf[i] & 2) S.rank_deficient++;
       if (hf[i] & 1) {
         const MacroHost& m = pl.all[mine[bstart + i]];
         char buf[200];

@@ -7,7 +7,7 @@ macropoint and right-hand side (fine combined field on R_p^+).
 import numpy as np
 import pytest
 
-from mch_inputs import CONFIGS, make_medium, random_medium
+from mch_inputs import CONFIGS, make_medium, periodic_medium, random_medium
 from oracle import Oracle
 
 pytestmark = pytest.mark.gpu
@@ -67,6 +67,24 @@ def test_tiny_all_points(d, n, M, L, N):
                 assert phi_err(pg, po[r]) < PHI_TOL, (k, r, phi_err(pg, po[r]))
 
 
+def test_rank_deficient_level():
+    """Reading R20 on the GPU: level-3 mesh equal to the inclusion period (dependent constraint
+    rows in V_3) — pseudo-inverse projector vs the oracle's eigen-truncated KKT."""
+    H = _gpu()
+    kap, ids = periodic_medium(2, 64, 4, 0.3, 1.0, 30.0)
+    o = Oracle(2, 64, 8, 3, 2, 2, kap, ids)
+    Go = o.effective_coeffs()
+    with H(2, 64, 2, 8, 3, 2, kap, ids, keep_all=True) as h:
+        h.solve_all()
+        assert h.level_stats(3)["rank_deficient"] > 0
+        Gg = h.effective_coeffs()
+        for k in o.plan.all_vertices():
+            i = o.plan.linear_index(k)
+            assert g_err(Gg[i], Go[i]) < G_TOL, (k, g_err(Gg[i], Go[i]))
+            for r in range(o.n_rhs):
+                assert phi_err(h.local_solution(k, r), o.solve(k)["phi"][r]) < PHI_TOL
+
+
 def test_config1_full():
     """BASELINE config 1 (2D 256², 81 macropoints, L = 1): every G entry, φ at sampled points"""
     H = _gpu()
@@ -74,7 +92,7 @@ def test_config1_full():
     kap, ids = make_medium(cfg)
     o = Oracle.from_config(cfg, kap, ids)
     from oracle.hmh import run_parallel
-    run_parallel(o, [o.plan.S(1)])
+    run_parallel(o, [o.plan.S(1)], keep_phi=True)
     Go = o.effective_coeffs()
     with H.from_config(cfg, kap, ids, keep_all=True) as h:
         h.solve_all()
