@@ -1,0 +1,286 @@
+"""Benchmark of the hot path (Algorithm 1 lines 3-7 for every level) on the
+BASELINE workload: configs[1] (config 2: 2D 1024², ε = 1/128, contrast 1e3, L = 3, η = 2,
+33×33 macropoints, 2 continua, 6 cell problems per macropoint).
+
+One "step" = mch_solve_level(1..L) + mch_effective_coeffs on the device-resident medium
+(every macropoint of every level, all N(1+d) cell problems, the Eq. (7) reductions).
+value = cell-problem solves / s (whole job, all ranks).  `e2e` repeats the step through the
+C ABI with HOST buffers: mch_create from pinned host κ/ψ (H2D inside), solve, coefficients
+copied back to pinned host memory, destroy.
+
+  python bench.py [--gpus N --steps K --warmup W --config C --impl {mch,reference}]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from mch_inputs import CONFIGS, make_medium  # noqa: E402
+
+METRIC = "cell-problem solves/sec per level (L, η, d); HBM GB/s vs B200 ~8 TB/s"
+UNIT = "cell-problem solves/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="mch", choices=["mch", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------------------
+def _oracle_sample(cfg, kap, ids, workers):
+    """Oracle (as it stands) on the vertex sub-box k ∈ [0, 2^(L-1)·2]^d of the workload, levels
+    in order with a process pool; returns (cpu-seconds per macropoint per level, sample text)."""
+    from oracle import Oracle
+    from oracle.hmh import run_parallel
+    o = Oracle.from_config(cfg, kap, ids)
+    span = 2 * cfg.eta ** (cfg.L - 1)
+    pts = [[k for k in o.plan.S(lev) if max(k) <= span] for lev in range(1, cfg.L + 1)]
+    walls, used = run_parallel(o, pts, workers=workers)
+    per = []
+    for lev, p in enumerate(pts, start=1):
+        per.append(sum(o.timings[tuple(k)] for k in p) / len(p))
+    sample = (f"oracle on vertex sub-box k∈[0,{span}]^{cfg.d} of {cfg.name} "
+              f"({'/'.join(str(len(p)) for p in pts)} macropoints at levels 1..{cfg.L}), "
+              f"per-level cpu-seconds/macropoint extrapolated to all {(cfg.M + 1) ** cfg.d}")
+    return per, sample, used, sum(walls)
+
+
+def _oracle_value(cfg, per, cores):
+    from oracle.planner import Plan
+    pl = Plan(cfg.d, cfg.n, cfg.M, cfg.L, cfg.eta, cfg.l)
+    counts = [len(pl.S(l)) for l in range(1, cfg.L + 1)]
+    t = sum(c * p for c, p in zip(counts, per)) / cores
+    return sum(counts) * cfg.n_rhs / t
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[a.config]
+    kap, ids = make_medium(cfg)
+    cores = len(os.sched_getaffinity(0))
+    vals = []
+    sample = ""
+    for step in range(a.warmup + a.steps):
+        per, sample, used, wall = _oracle_sample(cfg, kap, ids, cores)
+        if step >= a.warmup:
+            vals.append(_oracle_value(cfg, per, used))
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "d": cfg.d, "fine": f"{cfg.n}^{cfg.d}", "L": cfg.L,
+                       "eta": cfg.eta, "macropoints": (cfg.M + 1) ** cfg.d, "n_rhs": cfg.n_rhs},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def main():
+    a = _args()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2503_01276_b200.parallel import ShardedHomogenizer
+
+    cfg = CONFIGS[a.config]
+    kap, ids = make_medium(cfg)
+    kd = torch.from_numpy(kap).cuda()
+    idd = torch.from_numpy(ids).cuda()
+    sh = ShardedHomogenizer(cfg, kd, idd, rank, world)
+    n_cell = (cfg.M + 1) ** cfg.d * cfg.n_rhs
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+    st = torch.cuda.current_stream()
+
+    def step():
+        sh.reset()
+        sh.solve_all()
+        return sh.effective_coeffs()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ms, levels, launches = [], [], 0
+    for _ in range(a.steps):
+        flush.fill_(1.0)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        step()
+        e1.record(st)
+        torch.cuda.synchronize()
+        barrier()
+        ms.append(e0.elapsed_time(e1))
+        levels.append([sh.h.level_stats(l) for l in range(1, cfg.L + 1)])
+        launches += sum(s["launches"] for s in levels[-1])
+    clk = clocks.stop()
+    t = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    value = n_cell / (ms_step * 1e-3)
+
+    # dominant kernel (projected PCG): algorithmic bytes / device time, summed over levels
+    pk, pk_src = _peaks()
+    pcg_b = sum(s["pcg_bytes"] for st_ in levels for s in st_) / len(levels)
+    pcg_ms = sum(s["ms_pcg"] for st_ in levels for s in st_) / len(levels)
+    achieved = pcg_b / (pcg_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "pcg_dram_per_launch.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(cfg.name)
+        except Exception:
+            traffic = None
+    per_level = []
+    for l in range(cfg.L):
+        s = levels[-1][l]
+        per_level.append({"level": l + 1, "macropoints": s["macropoints"], "ms": round(s["ms_total"], 3),
+                          "cell_solves_per_s": round(s["problems"] / (s["ms_total"] * 1e-3), 1),
+                          "avg_iters": round(s["iters_total"] / max(1, s["problems"]), 1),
+                          "pcg_ms": round(s["ms_pcg"], 3),
+                          "pcg_GBps": round(s["pcg_bytes"] / max(s["ms_pcg"], 1e-9) / 1e6, 1),
+                          "rank_deficient": s["rank_deficient"]})
+
+    # e2e through the C ABI with host buffers (pinned), H2D/D2H inside the timed region
+    kh = torch.from_numpy(kap).pin_memory()
+    ih = torch.from_numpy(ids).pin_memory()
+    Gh = torch.zeros(((cfg.M + 1) ** cfg.d, cfg.n_rhs, cfg.n_rhs), dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for i in range(a.warmup + a.steps):
+        flush.fill_(1.0)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        h = ShardedHomogenizer(cfg, kh, ih, rank, world)
+        h.solve_all()
+        Gh.copy_(h.effective_coeffs(), non_blocking=True)
+        h.close()
+        e1.record(st)
+        torch.cuda.synchronize()
+        if i >= a.warmup:
+            e2e_ms.append(e0.elapsed_time(e1))
+    te = torch.tensor([sum(e2e_ms) / len(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = n_cell / (float(te.item()) * 1e-3)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "d": cfg.d, "fine": f"{cfg.n}^{cfg.d}", "H": f"1/{cfg.M}",
+                   "L": cfg.L, "eta": cfg.eta, "N": cfg.N, "macropoints": (cfg.M + 1) ** cfg.d,
+                   "n_rhs": cfg.n_rhs, "cell_problems_per_step": n_cell,
+                   "parallelism": f"macropoint-shard x{world}",
+                   "l2": "flushed between timed steps (512 MB write)",
+                   "macropoint_solves_per_s": (cfg.M + 1) ** cfg.d / (ms_step * 1e-3),
+                   "per_level": per_level},
+        "roofline": {"kernel": "k_pcg (projected block-PCG, all levels)", "bound": "hbm",
+                     "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "peak_source": pk_src,
+                     "algorithmic_bytes": "8*(6*nodes*iters per problem + D_n*cells*max_iters per macropoint), D_n = 1 (L1) / 5 (2D) / 19 (3D)"},
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": kap.nbytes + ids.nbytes,
+                "d2h_bytes_per_step": Gh.numel() * 8},
+        "gpu_launches": launches // a.steps,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        per, sample, used, wall = _oracle_sample(cfg, kap, ids, cores)
+        line["cpu_baseline"] = {"value": _oracle_value(cfg, per, used), "unit": UNIT, "cores": used,
+                                "kind": "oracle", "sample": sample, "wall_s": round(wall, 2)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    sh.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

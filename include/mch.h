@@ -78,6 +78,7 @@ typedef struct {
   double   ms_setup;       /* device time of targets, operators, transport and projector setup */
   double   ms_gram;        /* device time of combine + Eq. (7) reductions */
   double   pcg_bytes;      /* algorithmic bytes moved by the PCG: see DESIGN.md §6 */
+  int64_t  launches;       /* kernels launched by mch_solve_level(level) */
   int64_t  rank_deficient; /* windows whose level-n constraint rows were dependent (reading R20:
                               constraints imposed in the least-squares sense) */
 } mch_level_stats;
@@ -104,8 +105,15 @@ int mch_solve_level(mch_ctx* ctx, int level);
  * are left as 0 (the Python layer all-gathers them).  Requires all levels. */
 int mch_effective_coeffs(mch_ctx* ctx, double* out, size_t out_len, int out_on_device);
 
+/* Rewind the level counter so the same context (inputs, plan, pool, scratch) solves levels
+ * 1..L again — for repeated runs (benchmarks, serving) without re-creating the context. */
+int mch_reset(mch_ctx* ctx);
+
 /* |S_level| (all ranks). */
 int mch_num_macropoints(const mch_ctx* ctx, int level, int64_t* count);
+
+/* Lexicographic indices of S_level in solve order (position i is owned by rank i mod world). */
+int mch_level_macropoints(const mch_ctx* ctx, int level, int64_t* out, size_t cap);
 
 /* Fine-grid combined local solution phi_p (Eq. 11) of macropoint `macropoint`
  * (lexicographic vertex index) for right-hand side `rhs` on its clipped window,

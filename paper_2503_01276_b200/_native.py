@@ -16,7 +16,7 @@ ERRORS = {-1: "MCH_EINVAL", -2: "MCH_EDIVISIBILITY", -3: "MCH_ERANK", -4: "MCH_E
           -5: "MCH_EORDER", -6: "MCH_ECUDA", -7: "MCH_ENOMEM", -8: "MCH_EPLAN"}
 
 # every symbol include/mch.h declares
-SYMBOLS = ["mch_create", "mch_solve_level", "mch_effective_coeffs", "mch_num_macropoints",
+SYMBOLS = ["mch_create", "mch_reset", "mch_solve_level", "mch_effective_coeffs", "mch_num_macropoints", "mch_level_macropoints",
            "mch_local_solution", "mch_get_level_stats", "mch_pool_info", "mch_pool_slot",
            "mch_coeffs_device", "mch_last_error", "mch_destroy"]
 
@@ -36,7 +36,7 @@ class MchLevelStats(ctypes.Structure):
                 ("relres_max", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("ms_pcg", ctypes.c_double), ("ms_setup", ctypes.c_double),
                 ("ms_gram", ctypes.c_double), ("pcg_bytes", ctypes.c_double),
-                ("rank_deficient", ctypes.c_int64)]
+                ("launches", ctypes.c_int64), ("rank_deficient", ctypes.c_int64)]
 
 
 class MchError(RuntimeError):
@@ -54,8 +54,10 @@ def _load():
     vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     lib.mch_create.argtypes = [P(MchParams), vp, vp, i32, P(vp)]
     lib.mch_solve_level.argtypes = [vp, i32]
+    lib.mch_reset.argtypes = [vp]
     lib.mch_effective_coeffs.argtypes = [vp, vp, ctypes.c_size_t, i32]
     lib.mch_num_macropoints.argtypes = [vp, i32, P(i64)]
+    lib.mch_level_macropoints.argtypes = [vp, i32, P(i64), ctypes.c_size_t]
     lib.mch_local_solution.argtypes = [vp, i64, i32, vp, ctypes.c_size_t, P(i64)]
     lib.mch_get_level_stats.argtypes = [vp, i32, P(MchLevelStats)]
     lib.mch_pool_info.argtypes = [vp, P(vp), P(i64)]

@@ -92,6 +92,10 @@ class Homogenizer:
         mch_solve_level(self.ctx, level)
         self.solved = level
 
+    def reset(self):
+        check(lib.mch_reset(self.ctx), self.ctx)
+        self.solved = 0
+
     def solve_all(self):
         for lev in range(self.solved + 1, self.L + 1):
             self.solve_level(lev)
@@ -145,6 +149,12 @@ class Homogenizer:
         c = ctypes.c_int64()
         check(lib.mch_num_macropoints(self.ctx, level, ctypes.byref(c)), self.ctx)
         return c.value
+
+    def level_macropoints(self, level):
+        n = self.num_macropoints_level(level)
+        buf = (ctypes.c_int64 * max(n, 1))()
+        check(lib.mch_level_macropoints(self.ctx, level, buf, n), self.ctx)
+        return [buf[i] for i in range(n)]
 
     def close(self):
         if self.ctx is not None and self.ctx.value:

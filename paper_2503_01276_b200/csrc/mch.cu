@@ -58,6 +58,7 @@ struct mch_ctx {
   std::vector<int64_t> pool_off;  // per lexicographic index
   double* G = nullptr;
   int solved = 0;
+  int64_t launches = 0;
   std::vector<mch_level_stats> stats;
   std::string err;
   // grow-only scratch
@@ -162,14 +163,20 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   // parent pool: T_{L-1} (or everything with keep_all)
   const int64_t nmac = (int64_t)c->plan.all.size();
   c->pool_off.assign(nmac, -1);
+  // layout: by level, then owner rank (position in S_n mod world), then lexicographic, so the
+  // slots one rank produces at one level are contiguous (one broadcast per (level, owner)).
   int64_t off = 0;
-  for (int64_t i = 0; i < nmac; i++) {
-    const MacroHost& m = c->plan.all[i];
-    if (m.level < p.levels || p.keep_all) {
-      int64_t fn = 1;
-      for (int d = 0; d < p.d; d++) fn *= (m.hi[d] - m.lo[d] + 1);
-      c->pool_off[i] = off;
-      off += fn * c->n_rhs;
+  for (int lev = 1; lev <= p.levels; lev++) {
+    if (!(lev < p.levels || p.keep_all)) continue;
+    const std::vector<int64_t>& Sl = c->plan.S[lev];
+    for (int owner = 0; owner < p.world; owner++) {
+      for (size_t pos = owner; pos < Sl.size(); pos += p.world) {
+        const MacroHost& m = c->plan.all[Sl[pos]];
+        int64_t fn = 1;
+        for (int d = 0; d < p.d; d++) fn *= (m.hi[d] - m.lo[d] + 1);
+        c->pool_off[Sl[pos]] = off;
+        off += fn * c->n_rhs;
+      }
     }
   }
   c->pool_len = off;
@@ -212,6 +219,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     A.W = c->W.as<double>();
     A.Mc = c->Mc.as<double>();
     CKC(c, launch_level_ops(A, st));
+    S.launches += 1;
   }
   // this rank's macropoints of S_level
   const std::vector<int64_t>& Sl = pl.S[level];
@@ -329,6 +337,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     };
     const int th_l = pick(max_ln), th_f = pick(max_fn);
     cudaEventRecord(c->ev[1], st);
+    S.launches += (level >= 2) ? 6 : 4;
     CKC(c, launch_targets(A, st));
     if (level >= 2) CKC(c, launch_transport(A, th_f, st));
     CKC(c, launch_proj_setup(A, th_l, st));
@@ -403,6 +412,12 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   return MCH_OK;
 }
 
+extern "C" int mch_reset(mch_ctx* c) {
+  if (!c) return MCH_EINVAL;
+  c->solved = 0;
+  return MCH_OK;
+}
+
 extern "C" int mch_effective_coeffs(mch_ctx* c, double* out, size_t out_len, int out_on_device) {
   if (!c || !out) return MCH_EINVAL;
   if (c->solved != c->p.levels) return fail(c, MCH_EORDER, "coefficients need all levels solved");
@@ -417,6 +432,14 @@ extern "C" int mch_effective_coeffs(mch_ctx* c, double* out, size_t out_len, int
 extern "C" int mch_num_macropoints(const mch_ctx* c, int level, int64_t* count) {
   if (!c || !count || level < 1 || level > c->p.levels) return MCH_EINVAL;
   *count = (int64_t)c->plan.S[level].size();
+  return MCH_OK;
+}
+
+extern "C" int mch_level_macropoints(const mch_ctx* c, int level, int64_t* out, size_t cap) {
+  if (!c || !out || level < 1 || level > c->p.levels) return MCH_EINVAL;
+  const std::vector<int64_t>& Sl = c->plan.S[level];
+  if (cap < Sl.size()) return MCH_EINVAL;
+  for (size_t i = 0; i < Sl.size(); i++) out[i] = Sl[i];
   return MCH_OK;
 }
 
