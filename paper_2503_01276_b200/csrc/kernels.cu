@@ -443,7 +443,7 @@ __global__ void k_proj_setup(LevelArgs A) {
 // ---------------------------------------------------------------------------------------
 // projected PCG: one CTA per problem (macropoint, rhs)
 template <int D>
-__global__ void __launch_bounds__(512) k_pcg(LevelArgs A) {
+__global__ void __launch_bounds__(512, 2) k_pcg(LevelArgs A) {
   const int prob = blockIdx.x;
   const int mp = prob / A.n_rhs, r = prob % A.n_rhs;
   const ProbDesc& P = A.probs[mp];
