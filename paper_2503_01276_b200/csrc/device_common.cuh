@@ -30,7 +30,12 @@ template <int D> struct Geo {
   int nnodes;
   int s;          // fine cells per element edge
   bool fineop;    // element data from fine kappa/ids (level-1 form)
+  float inv0, inv01;  // 1/nn[0], 1/(nn[0] nn[1]) for division-free index decoding
 };
+
+// floor(a / b) for 0 <= a < 2^22, 1 <= b < 2^11, given inv = 1/b in float (exact: the +0.5 keeps
+// the product away from integers by more than the float rounding error)
+__device__ __forceinline__ int fdiv(int a, float inv) { return (int)(((float)a + 0.5f) * inv); }
 
 template <int D>
 __device__ __forceinline__ Geo<D> level_geo(const LevelArgs& A, const ProbDesc& P) {
@@ -43,6 +48,8 @@ __device__ __forceinline__ Geo<D> level_geo(const LevelArgs& A, const ProbDesc& 
   }
   g.s = A.s;
   g.fineop = (A.level == 1);
+  g.inv0 = 1.0f / (float)g.nn[0];
+  g.inv01 = 1.0f / (float)(g.nn[0] * g.nn[1]);
   return g;
 }
 
@@ -57,19 +64,22 @@ __device__ __forceinline__ Geo<D> fine_geo(const ProbDesc& P) {
   }
   g.s = 1;
   g.fineop = true;
+  g.inv0 = 1.0f / (float)g.nn[0];
+  g.inv01 = 1.0f / (float)(g.nn[0] * g.nn[1]);
   return g;
 }
 
 template <int D>
 __device__ __forceinline__ void node_xyz(const Geo<D>& g, int k, int* x) {
-  x[0] = k % g.nn[0];
-  int t = k / g.nn[0];
   if (D == 2) {
-    x[1] = t;
+    x[1] = fdiv(k, g.inv0);
+    x[0] = k - x[1] * g.nn[0];
     x[2] = 0;
   } else {
-    x[1] = t % g.nn[1];
-    x[2] = t / g.nn[1];
+    x[2] = fdiv(k, g.inv01);
+    const int t = k - x[2] * g.nn[0] * g.nn[1];
+    x[1] = fdiv(t, g.inv0);
+    x[0] = t - x[1] * g.nn[0];
   }
 }
 
@@ -92,7 +102,7 @@ template <int D>
 __device__ __forceinline__ int64_t level_cell_index(const LevelArgs& A, const ProbDesc& P, const int* e) {
   int64_t f = 0;
 #pragma unroll
-  for (int i = D - 1; i >= 0; i--) f = f * A.gn + (P.lo[i] / A.s + e[i]);
+  for (int i = D - 1; i >= 0; i--) f = f * A.gn + (P.glo[i] + e[i]);
   return f;
 }
 
@@ -103,7 +113,7 @@ __device__ __forceinline__ int elem_subcell(const LevelArgs& A, const ProbDesc& 
 #pragma unroll
   for (int i = D - 1; i >= 0; i--) {
     int f = P.lo[i] + e[i] * g.s;
-    int slot = (f + A.c / 2) / A.c - P.k[i] + A.l;
+    int slot = fdiv(f + A.c / 2, A.inv_c) - P.k[i] + A.l;
     q = q * A.w + slot;
   }
   return q;
@@ -187,35 +197,64 @@ __device__ __forceinline__ double elem_diag(const double* W, int a) {
   return y;
 }
 
-// (A v)_k by gathering the 2^D elements around node k (natural BC: elements outside skipped)
+// (A v)_k by gathering the 2^D elements around node k (natural BC: elements outside skipped),
+// from the node's 3^D neighbourhood.  Level 1 uses the Q1 element rows written out
+// (2D: kappa/6 (4 v_a - v_{a^1} - v_{a^2} - 2 v_{a^3}); 3D: kappa h/12 (4 v_a - the 4 corners
+// differing in >= 2 coordinates)); levels >= 2 the exact-Galerkin weights W.
+template <int D>
+__device__ __forceinline__ double apply_xyz(const LevelArgs& A, const ProbDesc& P, const Geo<D>& g,
+                                            const double* __restrict__ v, const int* xx, int k) {
+  constexpr int NB = DimC<D>::NB;
+  const int sy = g.nn[0], sz = g.nn[0] * g.nn[1];
+  double nb[NB];
+#pragma unroll
+  for (int c = 0; c < NB; c++) {
+    const int dx = c % 3 - 1, dy = (c / 3) % 3 - 1, dz = (D == 3) ? c / 9 - 1 : 0;
+    const bool ok = (xx[0] + dx >= 0) && (xx[0] + dx < g.nn[0]) && (xx[1] + dy >= 0) && (xx[1] + dy < g.nn[1]) &&
+                    (D == 2 || ((xx[2] + dz >= 0) && (xx[2] + dz < g.nn[2])));
+    nb[c] = ok ? v[k + dx + dy * sy + dz * sz] : 0.0;
+  }
+  double out = 0.0;
+#pragma unroll
+  for (int o = 0; o < (1 << D); o++) {
+    int e[3] = {0, 0, 0};
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < D; i++) {
+      e[i] = xx[i] - 1 + ((o >> i) & 1);
+      ok = ok && (e[i] >= 0) && (e[i] < g.nc[i]);
+    }
+    if (!ok) continue;
+    const int a = (~o) & ((1 << D) - 1);
+    auto nbv = [&](int b) {
+      const int dx = (b & 1) - (a & 1), dy = ((b >> 1) & 1) - ((a >> 1) & 1);
+      const int dz = (D == 3) ? ((b >> 2) & 1) - ((a >> 2) & 1) : 0;
+      return nb[(dx + 1) + 3 * (dy + 1) + (D == 3 ? 9 * (dz + 1) : 0)];
+    };
+    if (g.fineop) {
+      const double kap = A.kappa[fine_cell_index<D>(A, P, g, e, nullptr)];
+      if (D == 2)
+        out += kap * (1.0 / 6.0) * (4.0 * nbv(a) - nbv(a ^ 1) - nbv(a ^ 2) - 2.0 * nbv(a ^ 3));
+      else
+        out += kap * A.h * (1.0 / 12.0) * (4.0 * nbv(a) - nbv(a ^ 3) - nbv(a ^ 5) - nbv(a ^ 6) - nbv(a ^ 7));
+    } else {
+      double W[DimC<D>::NW];
+      elem_W<D>(A, P, g, e, W);
+      double c[1 << D];
+#pragma unroll
+      for (int b = 0; b < (1 << D); b++) c[b] = nbv(b);
+      out += elem_row<D>(W, c, a);
+    }
+  }
+  return out;
+}
+
 template <int D>
 __device__ __forceinline__ double apply_node(const LevelArgs& A, const ProbDesc& P, const Geo<D>& g,
                                              const double* v, int k) {
   int x[3];
   node_xyz<D>(g, k, x);
-  double y = 0.0;
-#pragma unroll
-  for (int ep = 0; ep < (1 << D); ep++) {
-    int e[3] = {0, 0, 0};
-    bool ok = true;
-#pragma unroll
-    for (int i = 0; i < D; i++) {
-      e[i] = x[i] - 1 + ((ep >> i) & 1);
-      ok = ok && (e[i] >= 0) && (e[i] < g.nc[i]);
-    }
-    if (!ok) continue;
-    double W[DimC<D>::NW];
-    elem_W<D>(A, P, g, e, W);
-    double c[1 << D];
-#pragma unroll
-    for (int b = 0; b < (1 << D); b++) {
-      int xb[3] = {e[0] + (b & 1), e[1] + ((b >> 1) & 1), (D == 3) ? e[2] + ((b >> 2) & 1) : 0};
-      c[b] = v[node_id<D>(g, xb)];
-    }
-    const int a = (~ep) & ((1 << D) - 1);
-    y += elem_row<D>(W, c, a);
-  }
-  return y;
+  return apply_xyz<D>(A, P, g, v, x, k);
 }
 
 template <int D>
@@ -267,6 +306,32 @@ __device__ __forceinline__ double ct_node(const LevelArgs& A, const ProbDesc& P,
     }
   }
   if (g.fineop) y *= (D == 2) ? 0.25 * A.h * A.h : 0.125 * A.h * A.h * A.h;
+  return y;
+}
+
+// (C^T yhat)_k with the subcell-interior fast path: if every element around node k lies in one
+// subcell q, (C^T yhat)_k = sum_j nw[j][k] yhat[q][j] (nw precomputed per window, shared by the
+// right-hand sides); interface nodes take the per-element path.
+template <int D>
+__device__ __forceinline__ double ct_fast(const LevelArgs& A, const ProbDesc& P, const Geo<D>& g,
+                                          const double* __restrict__ nw, const double* yhat, int k) {
+  int x[3];
+  node_xyz<D>(g, k, x);
+  bool interior = true;
+  int q = 0;
+#pragma unroll
+  for (int i = D - 1; i >= 0; i--) {
+    const int xi = x[i];
+    const int t = P.lo[i] + xi * g.s + A.c / 2;
+    const int v = fdiv(t, A.inv_c);
+    if (xi > 0 && xi < g.nn[i] - 1 && v * A.c == t) interior = false;  // on a dual-block face
+    const int e = (xi < g.nc[i]) ? xi : xi - 1;
+    const int slot = fdiv(P.lo[i] + e * g.s + A.c / 2, A.inv_c) - P.k[i] + A.l;
+    q = q * A.w + slot;
+  }
+  if (!interior) return ct_node<D>(A, P, g, yhat, k);
+  double y = 0.0;
+  for (int j = 0; j < A.N; j++) y += nw[(int64_t)j * g.nnodes + k] * yhat[q * A.N + j];
   return y;
 }
 
@@ -352,9 +417,12 @@ __device__ void constraint_apply(const LevelArgs& A, const ProbDesc& P, const Ge
     double part[4] = {0.0, 0.0, 0.0, 0.0};
     if (idx < cnt) {
       int e[3];
-      e[0] = bx[0] + idx % bx[3];
-      e[1] = bx[1] + (idx / bx[3]) % bx[4];
-      e[2] = (D == 3) ? bx[2] + idx / (bx[3] * bx[4]) : 0;
+      const int i2 = (D == 3) ? fdiv(idx, 1.0f / (float)(bx[3] * bx[4])) : 0;
+      const int r2 = idx - i2 * bx[3] * bx[4];
+      const int i1 = fdiv(r2, 1.0f / (float)bx[3]);
+      e[0] = bx[0] + r2 - i1 * bx[3];
+      e[1] = bx[1] + i1;
+      e[2] = bx[2] + i2;
       double u[1 << D];
 #pragma unroll
       for (int b = 0; b < (1 << D); b++) {

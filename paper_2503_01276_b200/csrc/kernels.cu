@@ -248,6 +248,25 @@ __global__ void k_proj_setup(LevelArgs A) {
   double* eb_end = tot + 16 + (A.nsub * 7 + 2 + 1) / 2 + 1;  // V (nc*nc) after the int area
   double* dinv = A.dinv + P.node_off;
   for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) dinv[k] = 1.0 / diag_node<D>(A, P, g, k);
+  // nw[j][k] = sum over the elements around node k of m_{E,j,a} (used for subcell-interior nodes)
+  double* nwt = A.NWt + P.node_off * A.N;
+  for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) {
+    int x[3];
+    node_xyz<D>(g, k, x);
+    double w[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int ep = 0; ep < (1 << D); ep++) {
+      int e[3] = {0, 0, 0};
+      bool ok = true;
+      for (int i = 0; i < D; i++) {
+        e[i] = x[i] - 1 + ((ep >> i) & 1);
+        ok = ok && e[i] >= 0 && e[i] < g.nc[i];
+      }
+      if (!ok) continue;
+      const int a = (~ep) & ((1 << D) - 1);
+      for (int j = 0; j < A.N; j++) w[j] += elem_m<D>(A, P, g, e, j, a);
+    }
+    for (int j = 0; j < A.N; j++) nwt[(int64_t)j * g.nnodes + k] = w[j];
+  }
   for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) S[i] = 0.0;
   __shared__ int ntask;
   subcell_boxes<D>(A, P, g, eb, &ntask);  // also syncs (dinv visible to block)
@@ -443,7 +462,7 @@ __global__ void k_proj_setup(LevelArgs A) {
 // ---------------------------------------------------------------------------------------
 // projected PCG: one CTA per problem (macropoint, rhs)
 template <int D>
-__global__ void __launch_bounds__(512, 2) k_pcg(LevelArgs A) {
+__global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
   const int prob = blockIdx.x;
   const int mp = prob / A.n_rhs, r = prob % A.n_rhs;
   const ProbDesc& P = A.probs[mp];
@@ -467,6 +486,7 @@ __global__ void __launch_bounds__(512, 2) k_pcg(LevelArgs A) {
   double* q = A.Q + P.vec_off + (int64_t)r * nn;
   const double* b = (A.level >= 2) ? A.B + P.vec_off + (int64_t)r * nn : nullptr;
   const double* dinv = A.dinv + P.node_off;
+  const double* nwt = A.NWt + P.node_off * A.N;
   for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Si[i] = A.Sinv[(int64_t)mp * nc * nc + i];
   subcell_boxes<D>(A, P, g, eb, &ntask);
 
@@ -533,7 +553,7 @@ __global__ void __launch_bounds__(512, 2) k_pcg(LevelArgs A) {
     // pass 1: r <- r - C^T yhat (re-projection), z = D^-1 r, p <- -z + beta p, rz = r.z
     double v[1] = {0.0};
     for (int k = threadIdx.x; k < nn; k += blockDim.x) {
-      const double rk = rv[k] - ct_node<D>(A, P, g, yhat, k);
+      const double rk = rv[k] - ct_fast<D>(A, P, g, nwt, yhat, k);
       const double zk = dinv[k] * rk;
       rv[k] = rk;
       p[k] = -zk + beta * p[k];

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -62,7 +63,7 @@ struct mch_ctx {
   std::vector<mch_level_stats> stats;
   std::string err;
   // grow-only scratch
-  DevBuf descs, W, Mc, g0, g, meas, cm, flags, dinv, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
+  DevBuf descs, W, Mc, g0, g, meas, cm, flags, dinv, nwt, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
   cudaEvent_t ev[8];
   bool events = false;
 };
@@ -207,7 +208,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
 
   LevelArgs A{};
   A.D = D; A.N = N; A.n_rhs = nr; A.l = c->l; A.w = c->w; A.nsub = c->nsub; A.ncon = nc;
-  A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.gn = gn; A.h = 1.0 / (double)pl.n;
+  A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.gn = gn; A.h = 1.0 / (double)pl.n; A.inv_c = 1.0f / (float)pl.c;
   A.kappa = c->kappa; A.ids = c->ids; A.pool = c->pool; A.G = c->G;
   A.rtol = c->p.rtol; A.max_iter = c->p.max_iter;
   float ms_setup = 0, ms_pcg = 0, ms_gram = 0;
@@ -270,6 +271,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
         P.lo[d] = (d < D) ? m.lo[d] : 0;
         P.ncf[d] = (d < D) ? m.hi[d] - m.lo[d] : 0;
         P.nc[d] = (d < D) ? P.ncf[d] / s : 0;
+        P.glo[d] = (d < D) ? P.lo[d] / s : 0;
         const int64_t a = (int64_t)m.k[d] * pl.c - pl.c / 2, b = (int64_t)m.k[d] * pl.c + pl.c / 2;
         P.kp_lo[d] = (d < D) ? (int)std::max<int64_t>(0, a) : 0;
         P.kp_hi[d] = (d < D) ? (int)std::min<int64_t>(pl.n, b) : 1;
@@ -307,6 +309,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     CKC(c, c->cm.ensure(sizeof(double) * nmp * 12));
     CKC(c, c->flags.ensure(sizeof(int) * nmp));
     CKC(c, c->dinv.ensure(sizeof(double) * node_off));
+    CKC(c, c->nwt.ensure(sizeof(double) * node_off * N));
     CKC(c, c->Sinv.ensure(sizeof(double) * nmp * nc * nc));
     CKC(c, c->X.ensure(sizeof(double) * vec_off));
     CKC(c, c->R.ensure(sizeof(double) * vec_off));
@@ -325,7 +328,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     A.nprob_mp = nmp;
     A.g0 = c->g0.as<double>(); A.g = c->g.as<double>(); A.meas = c->meas.as<double>();
     A.cm = c->cm.as<double>(); A.flags = c->flags.as<int>();
-    A.dinv = c->dinv.as<double>(); A.Sinv = c->Sinv.as<double>();
+    A.dinv = c->dinv.as<double>(); A.NWt = c->nwt.as<double>(); A.Sinv = c->Sinv.as<double>();
     A.X = c->X.as<double>(); A.R = c->R.as<double>(); A.P = c->P.as<double>(); A.Q = c->Q.as<double>();
     A.B = c->B.as<double>();
     A.FI = c->FI.as<double>(); A.FY = c->FY.as<double>();
@@ -503,7 +506,7 @@ extern "C" void mch_destroy(mch_ctx* c) {
   cudaFree(c->ids);
   cudaFree(c->pool);
   cudaFree(c->G);
-  DevBuf* bufs[] = {&c->descs, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->Sinv,
+  DevBuf* bufs[] = {&c->descs, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
                     &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres, &c->diag};
   for (DevBuf* b : bufs) b->release();
   if (c->events)

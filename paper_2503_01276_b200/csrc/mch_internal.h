@@ -10,6 +10,7 @@ struct ProbDesc {
   int lo[3];         // window R_p^+ lower fine-cell index (global)
   int ncf[3];        // window fine cells per dimension
   int nc[3];         // window level-n cells per dimension (ncf / s)
+  int glo[3];        // global level-n cell index of the window origin (lo / s)
   int kp_lo[3];      // K_p fine-cell range [kp_lo, kp_hi) (global)
   int kp_hi[3];
   int64_t lin;       // lexicographic macropoint index
@@ -33,6 +34,7 @@ struct LevelArgs {
   int n, c;                // fine cells per dim, fine cells per H
   int gn;                  // global level-n cells per dim (n/s)
   double h;
+  float inv_c;             // 1/c
   const double* kappa;     // fine, n^D, x fastest
   const uint8_t* ids;
   const double* W;         // level >= 2: per global level-n cell, D*3^(D-1) operator weights
@@ -46,6 +48,7 @@ struct LevelArgs {
   double* cm;              // [mp][D][N] centring constants c_mj
   int* flags;              // [mp] bit0: continuum absent from K_p
   double* dinv;            // level-n node blocks
+  double* NWt;             // [node blocks][N][nodes] interior-node constraint weights
   double* Sinv;            // [mp][ncon][ncon]
   // per-problem vectors (problem = mp*n_rhs + r)
   double* X; double* R; double* P; double* Q; double* B;
