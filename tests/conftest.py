@@ -11,3 +11,10 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 and the built CUDA library")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_library():
+    """Compile libmch.so (sm_100a, nvcc cross-compiles without a GPU) if it is missing or stale."""
+    from paper_2503_01276_b200.build import build
+    build()

@@ -1,0 +1,61 @@
+"""C-ABI checks that need no GPU: libmch.so loads, exports every function include/mch.h declares,
+and rejects invalid arguments before touching the device (error codes of mch.h)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "mch.h")
+
+
+def _declared():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mch_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2503_01276_b200 import _native
+    decl = _declared()
+    assert "mch_create" in decl and "mch_solve_level" in decl and "mch_effective_coeffs" in decl
+    nm = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\b(mch_[a-z_]+)\b", nm))
+    missing = [s for s in decl if s not in exported]
+    assert not missing, missing
+    assert sorted(_native.SYMBOLS) == decl
+
+
+def _create(**kw):
+    from paper_2503_01276_b200._native import MchParams, lib
+    d = kw.pop("d", 2)
+    n = kw.pop("n", 32)
+    kap = kw.pop("kappa", np.ones((n,) * d))
+    ids = kw.pop("ids", np.zeros((n,) * d, dtype=np.uint8))
+    p = MchParams(d=d, n=n, num_continua=kw.pop("N", 1), M=kw.pop("M", 4), levels=kw.pop("L", 1),
+                  eta=kw.pop("eta", 2), oversample=1, rtol=1e-12, max_iter=100, rank=0, world=1,
+                  keep_all=0, stream=None)
+    ctx = ctypes.c_void_p()
+    rc = lib.mch_create(ctypes.byref(p), kap.ctypes.data, ids.ctypes.data, 0, ctypes.byref(ctx))
+    return rc, lib.mch_last_error(None).decode()
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(d=4), -1),                                  # MCH_EINVAL: d
+    (dict(N=5), -1),                                  # MCH_EINVAL: N > 4
+    (dict(M=5), -2),                                  # MCH_EDIVISIBILITY: M does not divide n
+    (dict(n=24, M=8), -2),                            # H/(2h) not an integer (c = 3)
+    (dict(n=32, M=8, L=3), -2),                       # H/(2 h eta^(L-1)) not an integer
+    (dict(n=48, M=6, L=3), -2),                       # eta^(L-1) = 4 does not divide M
+    (dict(n=32, M=4, L=3), -8),                       # MCH_EPLAN: T_1 = {0, 4}, no covering parent
+    (dict(kappa=-np.ones((32, 32))), -1),             # kappa <= 0
+    (dict(kappa=np.full((32, 32), np.nan)), -1),      # kappa not finite
+    (dict(ids=np.full((32, 32), 3, dtype=np.uint8), N=2), -1),  # id >= N
+])
+def test_create_rejects_invalid_inputs(kw, code):
+    rc, msg = _create(**kw)
+    assert rc == code, (rc, msg)
+    assert msg
