@@ -16,5 +16,9 @@ def pytest_configure(config):
 @pytest.fixture(scope="session", autouse=True)
 def _built_library():
     """Compile libmch.so (sm_100a, nvcc cross-compiles without a GPU) if it is missing or stale."""
-    from paper_2503_01276_b200.build import build
-    build()
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "mch_build", os.path.join(ROOT, "paper_2503_01276_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)  # no package import: the package needs the built library
+    mod.build()
