@@ -209,16 +209,20 @@ def main():
     ms_step = float(t.item())
     value = n_cell / (ms_step * 1e-3)
 
-    # dominant kernel (projected PCG): algorithmic bytes / device time, summed over levels
+    # dominant kernel launch: the level-1 k_pcg launch (one launch per level and batch; level 1 is
+    # the largest share of the step, see profiles/r01_launches_c2.csv).  achieved = algorithmic
+    # bytes of that launch / its device time (CUDA events on the library stream, mean over steps).
     pk, pk_src = _peaks()
-    pcg_b = sum(s["pcg_bytes"] for st_ in levels for s in st_) / len(levels)
-    pcg_ms = sum(s["ms_pcg"] for st_ in levels for s in st_) / len(levels)
-    achieved = pcg_b / (pcg_ms * 1e-3) / 1e9
+    l1_b = sum(st_[0]["pcg_bytes"] for st_ in levels) / len(levels)
+    l1_ms = sum(st_[0]["ms_pcg"] for st_ in levels) / len(levels)
+    achieved = l1_b / (l1_ms * 1e-3) / 1e9
+    all_b = sum(s["pcg_bytes"] for st_ in levels for s in st_) / len(levels)
+    all_ms = sum(s["ms_pcg"] for st_ in levels for s in st_) / len(levels)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "pcg_dram_per_launch.json")
+    prof = os.path.join(ROOT, "profiles", "pcg_dram_per_launch_r01.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(cfg.name)
+            traffic = json.load(open(prof)).get(cfg.name, {}).get("dram_bytes_pcg_L1_launch")
         except Exception:
             traffic = None
     per_level = []
@@ -266,9 +270,11 @@ def main():
                    "l2": "flushed between timed steps (512 MB write)",
                    "macropoint_solves_per_s": (cfg.M + 1) ** cfg.d / (ms_step * 1e-3),
                    "per_level": per_level},
-        "roofline": {"kernel": "k_pcg (projected block-PCG, all levels)", "bound": "hbm",
+        "roofline": {"kernel": "k_pcg level-1 launch (projected PCG)", "bound": "hbm",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "algorithmic_bytes_per_launch": l1_b, "launch_ms": l1_ms,
+                     "all_levels_pcg_GBps": all_b / (all_ms * 1e-3) / 1e9,
                      "peak_source": pk_src,
                      "algorithmic_bytes": "8*(6*nodes*iters per problem + D_n*cells*max_iters per macropoint), D_n = 1 (L1) / 5 (2D) / 19 (3D)"},
         "e2e": {"value": e2e_value, "unit": UNIT,
