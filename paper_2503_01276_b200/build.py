@@ -8,11 +8,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libmch.so")
-SOURCES = ["mch.cu", "kernels.cu", "plan.cpp"]
+SOURCES = ["mch.cu", "kernels.cu", "pcg2d.cu", "plan.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-         "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
-         "-Xptxas", "-v"]
+FLAGS_C = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+           "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
 def needs_build() -> bool:
@@ -27,20 +26,38 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every source to an object in parallel, then link the shared library."""
     if not force and not needs_build():
         return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(os.path.dirname(LIB), "build.log")
+    libdir = os.path.dirname(LIB)
+    objdir = os.path.join(libdir, "obj")
+    os.makedirs(objdir, exist_ok=True)
+    procs, objs = [], []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src + ".o")
+        objs.append(obj)
+        cmd = [NVCC, *FLAGS_C, "-c", "-o", obj, os.path.join(CSRC, src)]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    log_parts, failed = [], False
+    for cmd, pr in procs:
+        out, err = pr.communicate()
+        log_parts.append(" ".join(cmd) + "\n" + out + err)
+        failed = failed or pr.returncode != 0
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+            "-o", LIB + ".tmp", *objs]
+    if not failed:
+        res = subprocess.run(link, capture_output=True, text=True)
+        log_parts.append(" ".join(link) + "\n" + res.stdout + res.stderr)
+        failed = res.returncode != 0
+    log = os.path.join(libdir, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stderr[-6000:])
+        f.write("\n".join(log_parts))
+    if failed:
+        sys.stderr.write("\n".join(log_parts)[-8000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     os.replace(LIB + ".tmp", LIB)
     if verbose:
-        print(res.stderr)
+        print("\n".join(log_parts))
     return LIB
 
 

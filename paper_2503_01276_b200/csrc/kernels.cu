@@ -247,7 +247,12 @@ __global__ void k_proj_setup(LevelArgs A) {
   int* eb = reinterpret_cast<int*>(tot + 16);
   double* eb_end = tot + 16 + (A.nsub * 7 + 2 + 1) / 2 + 1;  // V (nc*nc) after the int area
   double* dinv = A.dinv + P.node_off;
-  for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) dinv[k] = 1.0 / diag_node<D>(A, P, g, k);
+  // D^-1 rounded to fp32 in 2D: the on-chip PCG (pcg2d.cu) keeps it in fp32 shared memory, and S
+  // below must be formed with the identical values for the projection to be exact
+  for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) {
+    const double dv = 1.0 / diag_node<D>(A, P, g, k);
+    dinv[k] = (D == 2) ? (double)(float)dv : dv;
+  }
   // nw[j][k] = sum over the elements around node k of m_{E,j,a} (used for subcell-interior nodes)
   double* nwt = A.NWt + P.node_off * A.N;
   for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) {

@@ -63,9 +63,10 @@ struct mch_ctx {
   std::vector<mch_level_stats> stats;
   std::string err;
   // grow-only scratch
-  DevBuf descs, W, Mc, g0, g, meas, cm, flags, dinv, nwt, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
+  DevBuf descs, segs, nseg, STC, MLR, W, Mc, g0, g, meas, cm, flags, dinv, nwt, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
   cudaEvent_t ev[8];
   bool events = false;
+  int pcg_mode = 0;  // 0: on-chip 2D PCG where it applies; 1: generic k_pcg; 2: on-chip, precomputed operator at level 1
 };
 
 static int fail(mch_ctx* c, int code, const std::string& msg) {
@@ -81,6 +82,30 @@ static int fail(mch_ctx* c, int code, const std::string& msg) {
       return fail(ctx, e_ == cudaErrorMemoryAllocation ? MCH_ENOMEM : MCH_ECUDA,              \
                   std::string(#call) + ": " + cudaGetErrorString(e_));                        \
   } while (0)
+
+// Row chunks of a 2D window for the on-chip PCG (pcg2d.cu): node rows are grouped by the subcell
+// row of the elements above them, and each group is cut into near-equal chunks of <= rpt rows.
+// Chunk = (first node row, rows, subcell row, subcell row of the elements below the first row if
+// those belong to the previous subcell row, else -1).
+static void seg_plan_2d(const ProbDesc& P, int s, int c, int l, int rpt, std::vector<short4>& out) {
+  out.clear();
+  const int ncy = P.nc[1];
+  auto slot = [&](int ey) { return (P.lo[1] + ey * s + c / 2) / c - P.k[1] + l; };
+  int ea = 0;
+  while (ea < ncy) {
+    int eb = ea + 1;
+    while (eb < ncy && slot(eb) == slot(ea)) eb++;
+    const int G = eb - ea + (eb == ncy ? 1 : 0);
+    const int nch = (G + rpt - 1) / rpt, base = G / nch, rem = G % nch;
+    int y = ea;
+    for (int ch = 0; ch < nch; ch++) {
+      const int n = base + (ch < rem ? 1 : 0);
+      out.push_back(make_short4((short)y, (short)n, (short)slot(ea), (short)((ch == 0 && ea > 0) ? slot(ea - 1) : -1)));
+      y += n;
+    }
+    ea = eb;
+  }
+}
 
 extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint8_t* ids, int on_dev,
                           mch_ctx** out) {
@@ -111,6 +136,10 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   c->nsub = nsub;
   c->ncon = nsub * p.num_continua;
   c->st = reinterpret_cast<cudaStream_t>(p.stream);
+  if (const char* pm = getenv("MCH_PCG")) {
+    if (!strcmp(pm, "old")) c->pcg_mode = 1;
+    else if (!strcmp(pm, "gn")) c->pcg_mode = 2;
+  }
   c->plan.D = p.d;
   c->plan.n = p.n;
   c->plan.M = p.M;
@@ -250,7 +279,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     while (bend < mine.size()) {
       int64_t ln, fnn, lc;
       sizes(pl.all[mine[bend]], ln, fnn, lc);
-      double b = 8.0 * (5.0 * nr * ln + ln + (double)nc * nc + 3.0 * nc * nr + nc + 12) +
+      double b = 8.0 * (5.0 * nr * ln + ln * (10.0 + 4.0 * N) + (double)nc * nc + 3.0 * nc * nr + nc + 12) +
                  (level >= 2 ? 16.0 * nr * fnn : 0.0);
       if (bend > bstart && bytes + b > budget) break;
       bytes += b;
@@ -344,8 +373,67 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     CKC(c, launch_targets(A, st));
     if (level >= 2) CKC(c, launch_transport(A, th_f, st));
     CKC(c, launch_proj_setup(A, th_l, st));
+    // on-chip 2D PCG (pcg2d.cu) unless MCH_PCG=old; MCH_PCG=gn forces the precomputed-operator
+    // variant at level 1 as well (cross-check of the two operator paths)
+    bool on2d = (D == 2) && N <= 3 && nc <= 32 && c->pcg_mode != 1;
+    bool l1op = on2d && level == 1 && c->pcg_mode != 2;
+    int threads2 = 0;
+    size_t smem2 = 0;
+    if (on2d) {
+      for (int pass = 0; pass < 2 && on2d; pass++) {
+        const int rpt = l1op ? PCG2D_RPT_L1 : PCG2D_RPT_GN;
+        std::vector<int> nsegs(nmp);
+        std::vector<std::vector<short4>> per(nmp);
+        int maxseg = 0, maxw = 0;
+        for (int i = 0; i < nmp; i++) {
+          seg_plan_2d(descs[i], s, (int)pl.c, c->l, rpt, per[i]);
+          nsegs[i] = (int)per[i].size();
+          maxseg = std::max(maxseg, nsegs[i]);
+          const int nx = descs[i].nc[0] + 1;
+          maxw = std::max(maxw, ((nx + 31) / 32) * nsegs[i]);
+        }
+        threads2 = 32 * maxw;
+        smem2 = 0;
+        for (int i = 0; i < nmp; i++)
+          smem2 = std::max(smem2, pcg2d_smem(descs[i].nc[0] + 1, descs[i].nc[1] + 1, nc, maxw, l1op));
+        const int need = ((maxw + 3) / 4) * 4 * rpt;
+        int cols = 32;
+        while (cols < need) cols *= 2;
+        const bool fits = threads2 <= (l1op ? 768 : 384) && smem2 <= 232448 && cols <= 512;
+        if (!fits) {
+          if (l1op) {  // level 1 with the precomputed operator
+            l1op = false;
+            continue;
+          }
+          on2d = false;
+          break;
+        }
+        std::vector<short4> all_segs((size_t)nmp * maxseg, make_short4(0, 0, 0, -1));
+        for (int i = 0; i < nmp; i++)
+          for (int k = 0; k < nsegs[i]; k++) all_segs[(size_t)i * maxseg + k] = per[i][k];
+        CKC(c, c->segs.ensure(sizeof(short4) * all_segs.size()));
+        CKC(c, c->nseg.ensure(sizeof(int) * nmp));
+        CKC(c, cudaMemcpyAsync(c->segs.ptr, all_segs.data(), sizeof(short4) * all_segs.size(),
+                               cudaMemcpyHostToDevice, st));
+        CKC(c, cudaMemcpyAsync(c->nseg.ptr, nsegs.data(), sizeof(int) * nmp, cudaMemcpyHostToDevice, st));
+        A.segs = c->segs.as<short4>();
+        A.nseg = c->nseg.as<int>();
+        A.maxseg = maxseg;
+        A.tm_cols = cols;
+        if (!l1op) {
+          CKC(c, c->STC.ensure(sizeof(double) * 9 * node_off));
+          CKC(c, c->MLR.ensure(sizeof(double) * 4 * N * node_off));
+          A.STC = c->STC.as<double>();
+          A.MLR = c->MLR.as<double>();
+          CKC(c, launch_node_ops2d(A, max_ln, st));
+          S.launches += 1;
+        }
+        break;
+      }
+    }
     cudaEventRecord(c->ev[2], st);
-    CKC(c, launch_pcg(A, th_l, st));
+    if (on2d) CKC(c, launch_pcg2d(A, l1op, threads2, smem2, st));
+    else CKC(c, launch_pcg(A, th_l, st));
     cudaEventRecord(c->ev[3], st);
     if (level >= 2) CKC(c, launch_combine(A, th_f, st));
     CKC(c, launch_gram(A, 256, st));
@@ -506,7 +594,7 @@ extern "C" void mch_destroy(mch_ctx* c) {
   cudaFree(c->ids);
   cudaFree(c->pool);
   cudaFree(c->G);
-  DevBuf* bufs[] = {&c->descs, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
+  DevBuf* bufs[] = {&c->descs, &c->segs, &c->nseg, &c->STC, &c->MLR, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
                     &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres, &c->diag};
   for (DevBuf* b : bufs) b->release();
   if (c->events)

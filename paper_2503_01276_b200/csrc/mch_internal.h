@@ -1,6 +1,7 @@
 // Internal structures shared by the host planner, the C ABI and the kernels.
 #pragma once
 #include <cstdint>
+#include <vector_types.h>
 
 #define MCH_MAXPAR 8  // 2^d parents at most (d-linear interpolation, Eq. 11)
 
@@ -58,4 +59,13 @@ struct LevelArgs {
   int* iters; double* relres;  // [problem]
   double* diag;            // [problem][4]: final rz, reference rz, floor, breakdown flag
   double rtol; int max_iter;
+  // on-chip 2D PCG (pcg2d.cu)
+  const short4* segs;      // [mp][maxseg] row chunks: (first node row, rows, subcell row, subcell row
+                           //  of the lower elements of the first row if it is an interface row, else -1)
+  const int* nseg;         // [mp]
+  int maxseg;
+  int tm_cols;             // TMEM columns allocated per CTA
+  double* STC;             // levels >= 2: per window node 9 stencil coefficients, SoA [9][nodes]
+  double* MLR;             // levels >= 2: per node constraint side sums, SoA [4N][nodes]:
+                           //  [L|R][j] over lower+upper elements, then [L|R][j] lower elements only
 };

@@ -131,3 +131,22 @@ def test_config_sampled(cid, points):
         sc = np.abs(Gg).max(axis=(1, 2))[:, None, None]
         assert np.max(np.abs(Gg - Gg.transpose(0, 2, 1)) / sc) < 1e-12
         assert np.max(np.abs(Gg[:, :, :N].sum(axis=2)) / sc[:, :, 0]) < 1e-10
+
+
+@pytest.mark.parametrize("mode", ["gn", "old"])
+def test_pcg_variants_agree(mode, monkeypatch):
+    """the on-chip 2D PCG (level-1 smem operator, precomputed operator) and the generic k_pcg
+    solve the same problems: all three agree with the oracle and with each other"""
+    H = _gpu()
+    d, n, M, L, N = 2, 64, 8, 3, 2
+    kap, ids = _admissible(d, n, M, N, 7)
+    Go = Oracle(d, n, M, L, 2, N, kap, ids).effective_coeffs()
+    with H(d, n, N, M, L, 2, kap, ids) as h:
+        h.solve_all()
+        G0 = h.effective_coeffs()
+    monkeypatch.setenv("MCH_PCG", mode)
+    with H(d, n, N, M, L, 2, kap, ids) as h:
+        h.solve_all()
+        G1 = h.effective_coeffs()
+    for Gp, Gq in ((G0, Go), (G1, Go), (G0, G1)):
+        assert max(g_err(Gp[i], Gq[i]) for i in range(len(Go))) < G_TOL
