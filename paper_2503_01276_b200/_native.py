@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libmch.so")
+LIB_PATH = os.environ.get("MCH_LIB") or os.path.join(_HERE, "lib", "libmch.so")
 
 MCH_OK = 0
 ERRORS = {-1: "MCH_EINVAL", -2: "MCH_EDIVISIBILITY", -3: "MCH_ERANK", -4: "MCH_ENOCONV",

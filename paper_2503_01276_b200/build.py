@@ -10,6 +10,9 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libmch.so")
 SOURCES = ["mch.cu", "kernels.cu", "pcg2d.cu", "plan.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# MCH_BUILD_TIMING=1 builds lib/libmch_timing.so with per-phase PCG cycle counters (dev tool)
+if os.environ.get("MCH_BUILD_TIMING"):
+    LIB = os.path.join(HERE, "lib", "libmch_timing.so")
 FLAGS_C = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
@@ -34,9 +37,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     procs, objs = [], []
     for src in SOURCES:
-        obj = os.path.join(objdir, src + ".o")
+        timing = bool(os.environ.get("MCH_BUILD_TIMING"))
+        obj = os.path.join(objdir, src + (".timing.o" if timing else ".o"))
         objs.append(obj)
-        cmd = [NVCC, *FLAGS_C, "-c", "-o", obj, os.path.join(CSRC, src)]
+        cmd = [NVCC, *FLAGS_C, *(["-DPCG2D_TIMING"] if timing else []), "-c", "-o", obj,
+               os.path.join(CSRC, src)]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     log_parts, failed = [], False
     for cmd, pr in procs:

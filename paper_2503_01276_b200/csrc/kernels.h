@@ -12,11 +12,14 @@ cudaError_t launch_gram(const LevelArgs& A, int threads, cudaStream_t st);
 cudaError_t launch_validate(const double* kappa, const uint8_t* ids, int64_t cnt, int N, int* bad,
                             cudaStream_t st);
 
-// on-chip 2D projected PCG (pcg2d.cu)
-#define PCG2D_RPT_L1 17  // rows per thread, level 1 (kappa/ids in shared memory)
-#define PCG2D_RPT_GN 9   // rows per thread, levels >= 2 (precomputed per-node operator)
-#define PCG2D_NXMAX_L1 97  // widest window (nodes) of the level-1 variant: 3H at 32 cells per H
-#define PCG2D_NXMAX_GN 97  // and of the precomputed-operator variant
-size_t pcg2d_smem(int nx, int ny, int nc, int nwarps, bool l1op);
+// on-chip 2D projected PCG (pcg2d.cu).  Variants: level 1 with kappa/ids in shared memory, and
+// the precomputed per-node operator for windows of <= 49 / 25 / 97 nodes per side.
+#define PCG2D_V_L1 0
+#define PCG2D_V_GN49 1
+#define PCG2D_V_GN25 2
+#define PCG2D_V_GN97 3
+void pcg2d_variant(int variant, int* rpt, int* nxm, int* maxw, int* l1op);
+size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw);
 cudaError_t launch_node_ops2d(const LevelArgs& A, int max_nodes, cudaStream_t st);
-cudaError_t launch_pcg2d(const LevelArgs& A, bool l1op, int threads, size_t smem, cudaStream_t st);
+cudaError_t launch_pcg2d(const LevelArgs& A, int variant, int threads, cudaStream_t st);
+void pcg2d_phase_dump(const char* tag);  // PCG2D_TIMING builds: per-phase cycle counters

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -267,6 +268,10 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     }
   };
   size_t freeb = 0, totb = 0;
+  const bool htime = getenv("MCH_HOST_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto th0 = now();
+  double h_plan = 0, h_launch = 0, h_sync = 0, h_post = 0;
   cudaMemGetInfo(&freeb, &totb);
   const double budget = std::min<double>(48e9, 0.5 * (double)freeb);
   size_t bstart = 0;
@@ -330,6 +335,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       S.unknowns_level += ln;
       S.cells_level += lc;
     }
+    auto tb0 = now();
     CKC(c, c->descs.ensure(sizeof(ProbDesc) * nmp));
     CKC(c, cudaMemcpyAsync(c->descs.ptr, descs.data(), sizeof(ProbDesc) * nmp, cudaMemcpyHostToDevice, st));
     CKC(c, c->g0.ensure(sizeof(double) * nmp * nc * nr));
@@ -368,6 +374,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       return std::max(64, std::min(512, t));
     };
     const int th_l = pick(max_ln), th_f = pick(max_fn);
+    auto tb1 = now();
     cudaEventRecord(c->ev[1], st);
     S.launches += (level >= 2) ? 6 : 4;
     CKC(c, launch_targets(A, st));
@@ -375,39 +382,33 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     CKC(c, launch_proj_setup(A, th_l, st));
     // on-chip 2D PCG (pcg2d.cu) unless MCH_PCG=old; MCH_PCG=gn forces the precomputed-operator
     // variant at level 1 as well (cross-check of the two operator paths)
-    bool on2d = (D == 2) && N <= 3 && nc <= 32 && c->pcg_mode != 1;
-    bool l1op = on2d && level == 1 && c->pcg_mode != 2;
-    int threads2 = 0;
-    size_t smem2 = 0;
+    bool on2d = (D == 2) && N <= 3 && nc == 9 * N && c->pcg_mode != 1;  // 3x3 subcells (l = 1)
+    int variant = -1, threads2 = 0;
     if (on2d) {
-      for (int pass = 0; pass < 2 && on2d; pass++) {
-        const int rpt = l1op ? PCG2D_RPT_L1 : PCG2D_RPT_GN;
+      int maxn = 0;
+      for (int i = 0; i < nmp; i++) maxn = std::max(maxn, std::max(descs[i].nc[0], descs[i].nc[1]) + 1);
+      std::vector<int> cands;
+      if (level == 1 && c->pcg_mode != 2) cands.push_back(PCG2D_V_L1);
+      cands.push_back(PCG2D_V_GN25);
+      cands.push_back(PCG2D_V_GN49);
+      cands.push_back(PCG2D_V_GN97);
+      for (int v : cands) {
+        int rpt, nxm, maxw, l1op;
+        pcg2d_variant(v, &rpt, &nxm, &maxw, &l1op);
+        if (maxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw) > 232448) continue;
         std::vector<int> nsegs(nmp);
         std::vector<std::vector<short4>> per(nmp);
-        int maxseg = 0, maxw = 0;
+        int maxseg = 0, maxwp = 0;
         for (int i = 0; i < nmp; i++) {
           seg_plan_2d(descs[i], s, (int)pl.c, c->l, rpt, per[i]);
           nsegs[i] = (int)per[i].size();
           maxseg = std::max(maxseg, nsegs[i]);
-          const int nx = descs[i].nc[0] + 1;
-          maxw = std::max(maxw, ((nx + 31) / 32) * nsegs[i]);
+          maxwp = std::max(maxwp, ((descs[i].nc[0] + 1 + 31) / 32) * nsegs[i]);
         }
-        threads2 = 32 * maxw;
-        smem2 = 0;
-        for (int i = 0; i < nmp; i++)
-          smem2 = std::max(smem2, pcg2d_smem(descs[i].nc[0] + 1, descs[i].nc[1] + 1, nc, maxw, l1op));
-        const int need = ((maxw + 3) / 4) * 4 * rpt;
+        const int need = ((maxwp + 3) / 4) * 4 * ((rpt + 3) & ~3);  // TMEM: warps per lane quarter x (q, x)
         int cols = 32;
         while (cols < need) cols *= 2;
-        const bool fits = threads2 <= (l1op ? 768 : 384) && smem2 <= 232448 && cols <= 512;
-        if (!fits) {
-          if (l1op) {  // level 1 with the precomputed operator
-            l1op = false;
-            continue;
-          }
-          on2d = false;
-          break;
-        }
+        if (maxwp > maxw || cols > 512) continue;
         std::vector<short4> all_segs((size_t)nmp * maxseg, make_short4(0, 0, 0, -1));
         for (int i = 0; i < nmp; i++)
           for (int k = 0; k < nsegs[i]; k++) all_segs[(size_t)i * maxseg + k] = per[i][k];
@@ -420,6 +421,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
         A.nseg = c->nseg.as<int>();
         A.maxseg = maxseg;
         A.tm_cols = cols;
+        threads2 = 32 * maxwp;
+        variant = v;
         if (!l1op) {
           CKC(c, c->STC.ensure(sizeof(double) * 9 * node_off));
           CKC(c, c->MLR.ensure(sizeof(double) * 4 * N * node_off));
@@ -430,11 +433,17 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
         }
         break;
       }
+      on2d = variant >= 0;
     }
     cudaEventRecord(c->ev[2], st);
-    if (on2d) CKC(c, launch_pcg2d(A, l1op, threads2, smem2, st));
+    if (on2d) CKC(c, launch_pcg2d(A, variant, threads2, st));
     else CKC(c, launch_pcg(A, th_l, st));
     cudaEventRecord(c->ev[3], st);
+    if (getenv("MCH_PCG_TIMING") && on2d) {
+      char tag[64];
+      snprintf(tag, sizeof tag, "level %d variant %d", level, variant);
+      pcg2d_phase_dump(tag);
+    }
     if (level >= 2) CKC(c, launch_combine(A, th_f, st));
     CKC(c, launch_gram(A, 256, st));
     cudaEventRecord(c->ev[4], st);
@@ -445,7 +454,12 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     CKC(c, cudaMemcpyAsync(hit.data(), c->iters.ptr, sizeof(int) * nmp * nr, cudaMemcpyDeviceToHost, st));
     CKC(c, cudaMemcpyAsync(hrr.data(), c->relres.ptr, sizeof(double) * nmp * nr, cudaMemcpyDeviceToHost, st));
     CKC(c, cudaMemcpyAsync(hdg.data(), c->diag.ptr, sizeof(double) * nmp * nr * 4, cudaMemcpyDeviceToHost, st));
+    auto tb2 = now();
     CKC(c, cudaStreamSynchronize(st));
+    auto tb3 = now();
+    h_plan += std::chrono::duration<double, std::milli>(tb1 - tb0).count();
+    h_launch += std::chrono::duration<double, std::milli>(tb2 - tb1).count();
+    h_sync += std::chrono::duration<double, std::milli>(tb3 - tb2).count();
     float t1 = 0, t2 = 0, t3 = 0;
     cudaEventElapsedTime(&t1, c->ev[1], c->ev[2]);
     cudaEventElapsedTime(&t2, c->ev[2], c->ev[3]);
@@ -491,6 +505,10 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     S.problems += (int64_t)nmp * nr;
     bstart = bend;
   }
+  if (htime)
+    fprintf(stderr, "[mch host] level %d: total %.3f ms, desc/upload %.3f, launches %.3f, sync %.3f\n", level,
+            std::chrono::duration<double, std::milli>(now() - th0).count(), h_plan, h_launch, h_sync);
+  (void)h_post;
   cudaEventRecord(c->ev[5], st);
   CKC(c, cudaEventSynchronize(c->ev[5]));
   float tt = 0;

@@ -26,30 +26,32 @@
 // chunk of a subcell row touches elements of the previous subcell row ("interface row").
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "device_common.cuh"
 #include "kernels.h"
 
 namespace {
 
 // ------------------------------------------------------------------------------------------
-// TMEM helpers (32x32b shape: lane i of the warp <-> TMEM lane 32*(warp%4) + i)
-__device__ __forceinline__ void tm_st2(uint32_t ta, double v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(ta),
-               "r"(__double2loint(v)), "r"(__double2hiint(v)));
+// TMEM helpers (32x32b shape: lane i of the warp <-> TMEM lane 32*(warp%4) + i).  No "memory"
+// clobbers: they would pin every address-taken local in local memory; volatile asm statements
+// keep their relative order.
+__device__ __forceinline__ void tm_st8(uint32_t ta, const double (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(ta),
+               "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])),
+               "r"(__double2hiint(v[1])), "r"(__double2loint(v[2])), "r"(__double2hiint(v[2])),
+               "r"(__double2loint(v[3])), "r"(__double2hiint(v[3])));
 }
-__device__ __forceinline__ void tm_ld4(uint32_t ta, uint32_t (&v)[4]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+__device__ __forceinline__ void tm_ld8(uint32_t ta, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                 "=r"(v[7])
                : "r"(ta));
 }
-// (no "memory" clobbers on the per-row TMEM asm: they would pin every address-taken local in
-// local memory; volatile asm statements keep their relative order)
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n"); }
 __device__ __forceinline__ double dbl(uint32_t lo, uint32_t hi) { return __hiloint2double((int)hi, (int)lo); }
-// compiler-only fence between unrolled rows: keeps ptxas from hoisting every row's loads to the
-// top of the sweep (which needs ~250 registers); latency is hidden by the other warps instead
-__device__ __forceinline__ void row_fence() {}
 // An opaque copy of v: values derived from it cannot be hoisted out of the CG loop (otherwise
 // ptxas precomputes every row address of every sweep once and keeps them all live).
 __device__ __forceinline__ int opaque(int v) {
@@ -65,68 +67,100 @@ __device__ __forceinline__ double warp_sum0(double v) {
   return __shfl_sync(FULLMASK, v, 0);
 }
 
-// y_lane = sum_j Sinv[lane][j] c_j with c_j held by lane j (Sinv symmetric: read column-wise)
+// y_lane = sum_j Sinv[lane][j] c_j with c_j held by lane j (Sinv symmetric: read column-wise);
+// NC rows at compile time (unrolled, two partial sums), nc <= NC the rows in use
+template <int NC>
 __device__ __forceinline__ double warp_sinv(const double* Si, int nc, double cv) {
   const int lane = threadIdx.x & 31;
-  double y = 0.0;
-  for (int j = 0; j < nc; j++) {
+  const int l = (lane < nc) ? lane : 0;
+  double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < NC; j++) {
     const double cj = __shfl_sync(FULLMASK, cv, j);
-    if (lane < nc) y += Si[j * nc + lane] * cj;
+    if (j < nc) {
+      if (j & 1) y1 += Si[j * nc + l] * cj;
+      else y0 += Si[j * nc + l] * cj;
+    }
   }
-  return y;
+  return (lane < nc) ? y0 + y1 : 0.0;
 }
 
 __device__ __forceinline__ int sub_slot(const LevelArgs& A, const ProbDesc& P, int dim, int e) {
   return fdiv(P.lo[dim] + e * A.s + A.c / 2, A.inv_c) - P.k[dim] + A.l;
 }
 
-// Constraint weights of one node, by side (L: elements of column x-1, R: column x) summed over
-// the lower (row y-1) and upper (row y) elements, and the lower element alone (interface rows).
+// multiset state of two element ids a, b in {0..N-1, 0xFF = no element}: index of (min, max)
+// in the triangular enumeration of pairs over N+1 symbols (N continua + "none")
+template <int N>
+__device__ __forceinline__ int pair_state(int a, int b) {
+  a = (a == 0xFF) ? N : a;
+  b = (b == 0xFF) ? N : b;
+  const int lo = min(a, b), hi = max(a, b);
+  return lo * (N + 1) - (lo * (lo - 1)) / 2 + (hi - lo);
+}
+template <int N> struct PairStates { static constexpr int value = (N + 1) * (N + 2) / 2; };
+
 template <int N, bool L1OP, int KX>
 struct NodeW {
-  // level 1: continuum ids of the window cells (border 0xFF), pitch KX
-  const uint8_t* ids;
-  double hq, hq2;
-  uint8_t dL, dR;
+  static constexpr int LW = (N == 1) ? 1 : ((N + 1) & ~1);  // padded table row (16-byte loads)
+  // level 1: per-node side states (low nibble: left pair of elements, high: right pair) and
+  // the table lut[state][j] = h^2/4 * multiplicity of continuum j in the pair
+  const uint8_t* codes;
+  const double* lut;
+  const uint8_t* ids;  // cell ids (border 0xFF), only for interface rows
+  int hqhi, hqlo;      // bit pattern of hq = h^2/4
   // levels >= 2: precomputed SoA [4N][nn]
   const double* base;
   int nn, nx;
   int xc;
-  const uint8_t* ip;  // running row pointers
+  const uint8_t* cp;  // running row pointers
   const double* mp;
-  int hqhi, hqlo;     // bit pattern of hq = h^2/4 (level-1 weight of one element corner)
+  int y0;
 
-  // c * hq for c in {0, 1, 2}, branch-free on the bit pattern (hq is a normal double, so
-  // 2 hq is hq with the exponent incremented)
-  __device__ __forceinline__ double cnt_w(int c) const {
-    const int m = -(c != 0);
-    return __hiloint2double((hqhi + ((c - 1) << 20)) & m, hqlo & m);
+  // c * hq for c in {0, 1}, branch-free on the bit pattern
+  __device__ __forceinline__ double one_w(bool c) const {
+    const int m = -(int)c;
+    return __hiloint2double(hqhi & m, hqlo & m);
   }
-
-  __device__ __forceinline__ void start(int y0) {
-    if (L1OP) {
-      ip = ids + y0 * KX + xc;
-      dL = ip[0];
-      dR = ip[1];
-    } else {
-      mp = base + y0 * nx + xc;
-    }
+  __device__ __forceinline__ void start(int y) {
+    y0 = y;
+    if (L1OP) cp = codes + y * (KX - 1) + xc;
+    else mp = base + y * nx + xc;
   }
-  // node (x, y0 + i) for consecutive i
+  // node (x, y0 + i) for consecutive i; low: also the weights of the lower elements alone
   __device__ __forceinline__ void row(bool low, double (&mL)[N], double (&mR)[N], double (&lL)[N],
                                       double (&lR)[N]) {
     if (L1OP) {
-      ip += KX;
-      const uint8_t uL = ip[0], uR = ip[1];
+      const int code = *cp;
+      cp += KX - 1;
+      const double* tl = lut + (code & 15) * LW;
+      const double* tr = lut + (code >> 4) * LW;
+      if (N == 1) {
+        mL[0] = tl[0];
+        mR[0] = tr[0];
+      } else {
 #pragma unroll
-      for (int j = 0; j < N; j++) {
-        mL[j] = cnt_w((dL == j) + (uL == j));
-        mR[j] = cnt_w((dR == j) + (uR == j));
-        lL[j] = cnt_w(dL == j);
-        lR[j] = cnt_w(dR == j);
+        for (int j = 0; j < N; j += 2) {  // 16-byte loads of the (padded) table rows
+          const double2 vl = *reinterpret_cast<const double2*>(tl + j);
+          const double2 vr = *reinterpret_cast<const double2*>(tr + j);
+          mL[j] = vl.x;
+          mR[j] = vr.x;
+          if (j + 1 < N) {
+            mL[j + 1] = vl.y;
+            mR[j + 1] = vr.y;
+          }
+        }
       }
-      dL = uL;
-      dR = uR;
+#pragma unroll
+      for (int j = 0; j < N; j++) lL[j] = lR[j] = 0.0;
+      if (low) {  // interface row (first row of a chunk): elements of row y0 - 1
+        const int dL = ids[y0 * KX + xc], dR = ids[y0 * KX + xc + 1];
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          lL[j] = one_w(dL == j);
+          lR[j] = one_w(dR == j);
+        }
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < N; j++) {
@@ -195,11 +229,31 @@ __global__ void k_node_ops2d(LevelArgs A) {
 
 // ------------------------------------------------------------------------------------------
 // the solver: one CTA per problem (macropoint, rhs)
-template <int RPT, int N, bool L1OP>
-__global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelArgs A) {
-  constexpr int NBC = 4 * RPT;  // TMEM columns per thread: (q, x) per row
-  // compile-time pitches (host checks nx <= NXM): per-row addresses become immediate offsets
-  constexpr int NXM = L1OP ? PCG2D_NXMAX_L1 : PCG2D_NXMAX_GN;
+#ifdef PCG2D_TIMING
+__device__ unsigned long long g_pcg2d_phase[16];
+void pcg2d_phase_dump(const char* tag) {
+  unsigned long long h[16];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, g_pcg2d_phase, sizeof h);
+  const char* nm[7] = {"passA", "B1", "passB", "B2", "passC", "c_reduce", "B3+fin"};
+  double tot = 0;
+  for (int k = 0; k < 7; k++) tot += (double)h[k];
+  fprintf(stderr, "[pcg2d timing %s] active-warp cycles per warp-iteration:", tag);
+  for (int k = 0; k < 7; k++) fprintf(stderr, " %s=%.0f", nm[k], (double)h[k] / (double)h[7]);
+  fprintf(stderr, " total=%.0f\n", tot / (double)h[7]);
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_pcg2d_phase, z, sizeof z);
+}
+#else
+void pcg2d_phase_dump(const char*) {}
+#endif
+
+template <int RPT, int N, bool L1OP, int NXM, int MAXW>
+__global__ void __launch_bounds__(MAXW * 32, MAXW >= 24 ? 1 : (MAXW >= 12 ? 2 : 6)) k_pcg2d(LevelArgs A) {
+  constexpr int RP4 = (RPT + 3) & ~3;  // rows rounded to the 4-row TMEM groups
+  constexpr int NBC = 4 * RP4;         // TMEM columns per thread: q block, then x block
+  // compile-time pitches and shared-memory offsets (host checks nx, ny <= NXM and warps <= MAXW):
+  // every per-row address is an immediate offset from one per-thread base
   constexpr int PX = NXM + 2, KX = NXM + 1, DX = NXM;
   const int prob = blockIdx.x;
   const int mp = prob / A.n_rhs, rhs = prob - mp * A.n_rhs;
@@ -207,7 +261,7 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
   const int nx = P.nc[0] + 1, ny = P.nc[1] + 1, nn = nx * ny;
   const int ncx = nx - 1, ncy = ny - 1;
   const int nc = A.ncon, ws = A.w;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int WX = (nx + 31) >> 5;
   const int sgi = warp / WX, wx = warp - sgi * WX;
   const bool wact = sgi < A.nseg[mp];
@@ -219,14 +273,22 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
   const int y0 = sg.x, nrow = sg.y, sy = sg.z, syp = sg.w;
 
   extern __shared__ __align__(16) double smem[];
-  double* Si = smem;                      // nc*nc
-  double* Yw = Si + nc * nc;              // [nwarps][32] projector coefficients yhat, per warp
-  double* bins = Yw + nwarps * 32;        // [nwarps][32] constraint partial sums, per warp
-  double* slots = bins + nwarps * 32;     // [3][32] scalar partial sums (rz, pq, rr)
-  double* p_s = slots + 3 * 32;           // (nx+2)(ny+2)
-  double* kap_s = p_s + PX * (ny + 2);    // level 1: (nx+1)(ny+1)
-  float* dinv_s = reinterpret_cast<float*>(kap_s + (L1OP ? KX * (ny + 1) : 0));  // DX*ny
-  uint8_t* ids_s = reinterpret_cast<uint8_t*>(dinv_s + DX * ny);
+  constexpr int LW = NodeW<N, L1OP, KX>::LW;
+  constexpr int NCM = 9 * N;              // constraint rows of a 3x3-subcell window (host: nc <= NCM)
+  constexpr int O_Y = (NCM * NCM + 1) & ~1, O_SL = O_Y + 64, O_B = O_SL + 3 * 32;
+  constexpr int O_P = O_B + MAXW * 32;
+  constexpr int O_K = O_P + PX * (NXM + 2), O_LUT = (O_K + (L1OP ? KX * (NXM + 1) : 0) + 1) & ~1;
+  constexpr int O_D = O_LUT + (L1OP ? 16 * LW : 0);  // end of the double region
+  double* Si = smem;                      // [NCM*NCM] S^-1 (nc*nc used)
+  double* Ysh = smem + O_Y;               // [32] yhat, [32] beta (written by warp 0)
+  double* slots = smem + O_SL;            // [3][32] scalar partial sums (rz, pq, rr)
+  double* bins = smem + O_B;              // [MAXW][32] constraint partial sums, per warp
+  double* p_s = smem + O_P;               // PX*(NXM+2), zero halo
+  double* kap_s = smem + O_K;             // level 1: KX*(NXM+1), zero border
+  double* lut_s = smem + O_LUT;           // level 1: 16*LW
+  float* dinv_s = reinterpret_cast<float*>(smem + O_D);                   // DX*NXM
+  uint8_t* ids_s = reinterpret_cast<uint8_t*>(dinv_s + DX * NXM);         // KX*(NXM+1), border 0xFF
+  uint8_t* codes_s = ids_s + (L1OP ? KX * (NXM + 1) : 0);                 // DX*NXM
   __shared__ uint32_t tm_base_s;
 
   if (warp == 0) {
@@ -238,10 +300,8 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
   }
   for (int i = threadIdx.x; i < PX * (ny + 2); i += blockDim.x) p_s[i] = 0.0;
   for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Si[i] = A.Sinv[(int64_t)mp * nc * nc + i];
-  for (int i = threadIdx.x; i < nwarps * 32; i += blockDim.x) {
-    bins[i] = 0.0;
-    Yw[i] = 0.0;
-  }
+  for (int i = threadIdx.x; i < MAXW * 32; i += blockDim.x) bins[i] = 0.0;
+  if (threadIdx.x < 96) slots[threadIdx.x] = 0.0;
   {
     const double* dg = A.dinv + P.node_off;
     for (int k = threadIdx.x; k < nn; k += blockDim.x) dinv_s[(k / nx) * DX + k % nx] = (float)dg[k];
@@ -259,109 +319,149 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
       kap_s[i] = kv;
       ids_s[i] = id;
     }
+    for (int i = threadIdx.x; i < PairStates<N>::value * LW; i += blockDim.x) {
+      // lut[state][j]: decode the state back to its pair (a <= b) and count j
+      const int st = i / LW, j = i - st * LW;
+      int a = 0, rem = st;
+      while (rem >= N + 1 - a) {
+        rem -= N + 1 - a;
+        a++;
+      }
+      const int b = a + rem;
+      lut_s[i] = 0.25 * A.h * A.h * (double)((a == j) + (b == j));
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      const int y = k / nx, xx = k - y * nx;
+      const uint8_t* c0 = ids_s + y * KX + xx;  // element (xx-1, y-1)
+      const int sL = pair_state<N>(c0[0], c0[KX]), sR = pair_state<N>(c0[1], c0[KX + 1]);
+      codes_s[y * DX + xx] = (uint8_t)(sL | (sR << 4));
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tm = tm_base_s + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * NBC);
+  const uint32_t tmq = tm_base_s + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * NBC);
+  const uint32_t tmx = tmq + 2 * RP4;
 
   // per-thread subcell columns of the left / right elements
   const int sxL = (xc >= 1) ? sub_slot(A, P, 0, xc - 1) : 0;
   const int sxR = (xc < ncx) ? sub_slot(A, P, 0, xc) : 0;
   NodeW<N, L1OP, KX> cw;
   cw.ids = ids_s;
-  cw.hq = 0.25 * A.h * A.h;
-  cw.hq2 = 0.5 * A.h * A.h;
-  cw.hqhi = __double2hiint(cw.hq);
-  cw.hqlo = __double2loint(cw.hq);
+  cw.codes = codes_s;
+  cw.lut = lut_s;
+  cw.hqhi = __double2hiint(0.25 * A.h * A.h);
+  cw.hqlo = __double2loint(0.25 * A.h * A.h);
   cw.base = A.MLR + P.node_off * 4 * N;
   cw.nn = nn;
   cw.nx = nx;
   cw.xc = xc;
   const double* S9 = A.STC + P.node_off * 9;
 
-  auto Pref = [&](int yy, int xx) -> double& { return p_s[(yy + 1) * PX + (xx + 1)]; };
-  auto Kld = [&](int ey, int ex) { return kap_s[(ey + 1) * KX + (ex + 1)]; };
-  auto dinv = [&](int y) { return (double)dinv_s[y * DX + xc]; };
-
   double r[RPT];
 #pragma unroll
   for (int i = 0; i < RPT; i++) r[i] = 0.0;
+  double yh = 0.0;  // projector coefficients: lane t holds yhat_t (identical in every warp)
 
   // ---- C^T yhat per row: f(i, y, ct) -------------------------------------------------------
   auto sweep_ct = [&](auto&& f) {
-    const double* Y = Yw + warp * 32;
-    double YL[N], YR[N];
+    double YL[N], YR[N], YLp[N], YRp[N];
 #pragma unroll
     for (int j = 0; j < N; j++) {
-      YL[j] = Y[(sy * ws + sxL) * N + j];
-      YR[j] = Y[(sy * ws + sxR) * N + j];
+      YL[j] = __shfl_sync(FULLMASK, yh, (sy * ws + sxL) * N + j);
+      YR[j] = __shfl_sync(FULLMASK, yh, (sy * ws + sxR) * N + j);
+      YLp[j] = __shfl_sync(FULLMASK, yh, (max(syp, 0) * ws + sxL) * N + j);
+      YRp[j] = __shfl_sync(FULLMASK, yh, (max(syp, 0) * ws + sxR) * N + j);
     }
     const int yb = opaque(y0);
     cw.start(yb);
 #pragma unroll
     for (int i = 0; i < RPT; i++) {
-      if (i < nrow) {
-        const int y = yb + i;
-        const bool split = (i == 0) && (syp >= 0);
-        double mL[N], mR[N], lL[N], lR[N];
-        cw.row(split, mL, mR, lL, lR);
-        double ct = 0.0;
-        if (split) {
+      if (i >= nrow) break;
+      const bool split = (i == 0) && (syp >= 0);
+      double mL[N], mR[N], lL[N], lR[N];
+      cw.row(split, mL, mR, lL, lR);
+      double ct = 0.0;
+      if (split) {
 #pragma unroll
-          for (int j = 0; j < N; j++) {
-            const double YLp = Y[(syp * ws + sxL) * N + j], YRp = Y[(syp * ws + sxR) * N + j];
-            ct += lL[j] * YLp + (mL[j] - lL[j]) * YL[j] + lR[j] * YRp + (mR[j] - lR[j]) * YR[j];
-          }
-        } else {
+        for (int j = 0; j < N; j++)
+          ct += lL[j] * YLp[j] + (mL[j] - lL[j]) * YL[j] + lR[j] * YRp[j] + (mR[j] - lR[j]) * YR[j];
+      } else {
 #pragma unroll
-          for (int j = 0; j < N; j++) ct += mL[j] * YL[j] + mR[j] * YR[j];
-        }
-        f(i, y, ct);
+        for (int j = 0; j < N; j++) ct += mL[j] * YL[j] + mR[j] * YR[j];
       }
-      row_fence();
+      f(i, yb + i, ct);
     }
   };
 
   // ---- (A p)_k per row from the smem vector p_s: f(i, y, Ap, p_k) ----------------------------
   auto sweep_stencil = [&](auto&& f) {
     const int yb = opaque(y0);
-    double a0 = Pref(yb - 1, xc - 1), b0 = Pref(yb - 1, xc), c0 = Pref(yb - 1, xc + 1);
-    double a1 = Pref(yb, xc - 1), b1 = Pref(yb, xc), c1 = Pref(yb, xc + 1);
+    const double* pp = p_s + (yb + 1) * PX + (xc + 1);  // node (xc, yb)
+    double a0 = pp[-PX - 1], b0 = pp[-PX], c0 = pp[-PX + 1];
+    double a1 = pp[-1], b1 = pp[0], c1 = pp[1];
+    const double* kp = kap_s + yb * KX + xc;  // element (xc-1, yb-1)
     double kL0 = 0.0, kR0 = 0.0;
     if (L1OP) {
-      kL0 = Kld(yb - 1, xc - 1);
-      kR0 = Kld(yb - 1, xc);
+      kL0 = kp[0];
+      kR0 = kp[1];
     }
     const double* s9 = S9 + yb * nx + xc;
 #pragma unroll
     for (int i = 0; i < RPT; i++) {
-      if (i < nrow) {
-        const int y = yb + i;
-        const double a2 = Pref(y + 1, xc - 1), b2 = Pref(y + 1, xc), c2 = Pref(y + 1, xc + 1);
-        double Ap;
-        if (L1OP) {
-          // Q1 element rows kappa/6 (4 v_a - v_a^1 - v_a^2 - 2 v_a^3) summed over the 4 cells
-          const double kL1 = Kld(y, xc - 1), kR1 = Kld(y, xc);
-          const double sL = kL0 + kL1, sR = kR0 + kR1, sD = kL0 + kR0, sU = kL1 + kR1;
-          double acc = 4.0 * (sL + sR) * b1 - sR * c1 - sL * a1 - sU * b2 - sD * b0;
-          acc -= 2.0 * (kR1 * c2 + kL1 * a2 + kR0 * c0 + kL0 * a0);
-          Ap = acc * (1.0 / 6.0);
-          kL0 = kL1;
-          kR0 = kR1;
-        } else {
-          const double* s = s9;
-          s9 += nx;
-          Ap = __ldg(s) * a0 + __ldg(s + nn) * b0 + __ldg(s + 2 * nn) * c0 + __ldg(s + 3 * nn) * a1 +
-               __ldg(s + 4 * nn) * b1 + __ldg(s + 5 * nn) * c1 + __ldg(s + 6 * nn) * a2 +
-               __ldg(s + 7 * nn) * b2 + __ldg(s + 8 * nn) * c2;
-        }
-        f(i, y, Ap, b1);
-        a0 = a1; b0 = b1; c0 = c1;
-        a1 = a2; b1 = b2; c1 = c2;
+      if (i >= nrow) break;
+      const double a2 = pp[(i + 1) * PX - 1], b2 = pp[(i + 1) * PX], c2 = pp[(i + 1) * PX + 1];
+      double Ap;
+      if (L1OP) {
+        // Q1 element rows kappa/6 (4 v_a - v_a^1 - v_a^2 - 2 v_a^3) summed over the 4 cells
+        const double kL1 = kp[(i + 1) * KX], kR1 = kp[(i + 1) * KX + 1];
+        const double sL = kL0 + kL1, sR = kR0 + kR1, sD = kL0 + kR0, sU = kL1 + kR1;
+        double acc = 4.0 * (sL + sR) * b1 - sR * c1 - sL * a1 - sU * b2 - sD * b0;
+        acc -= 2.0 * (kR1 * c2 + kL1 * a2 + kR0 * c0 + kL0 * a0);
+        Ap = acc * (1.0 / 6.0);
+        kL0 = kL1;
+        kR0 = kR1;
+      } else {
+        const double* s = s9 + i * nx;
+        Ap = __ldg(s) * a0 + __ldg(s + nn) * b0 + __ldg(s + 2 * nn) * c0 + __ldg(s + 3 * nn) * a1 +
+             __ldg(s + 4 * nn) * b1 + __ldg(s + 5 * nn) * c1 + __ldg(s + 6 * nn) * a2 +
+             __ldg(s + 7 * nn) * b2 + __ldg(s + 8 * nn) * c2;
       }
-      row_fence();
+      f(i, yb + i, Ap, b1);
+      a0 = a1; b0 = b1; c0 = c1;
+      a1 = a2; b1 = b2; c1 = c2;
     }
+  };
+
+  // ---- TMEM row groups: a value per row is buffered and stored 4 rows at a time -------------
+  double gb[4] = {0.0, 0.0, 0.0, 0.0};
+  auto gput = [&](uint32_t base, int i, double v) {
+    gb[i & 3] = v;
+    if ((i & 3) == 3) tm_st8(base + 2 * (i - 3), gb);
+  };
+  auto gflush = [&](uint32_t base) {  // the partial last group
+    if (nrow & 3) tm_st8(base + 2 * (nrow & ~3), gb);
+    tm_wait_st();
+  };
+  // x from TMEM per row: f(i, y, x_k); x_k returned by f is stored back
+  auto sweep_x = [&](auto&& f) {
+    const int yb = opaque(y0);
+#pragma unroll
+    for (int g = 0; g < RPT; g += 4) {
+      if (g >= nrow) break;
+      uint32_t xa[8];
+      tm_ld8(tmx + 2 * g, xa);
+      tm_wait_ld();
+      double xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        xv[u] = dbl(xa[2 * u], xa[2 * u + 1]);
+        if (g + u < RPT && g + u < nrow) xv[u] = f(g + u, yb + g + u, xv[u]);
+      }
+      tm_st8(tmx + 2 * g, xv);
+    }
+    tm_wait_st();
   };
 
   // ---- constraint accumulation: aC (current subcell row), aP (previous, interface row) -------
@@ -370,8 +470,8 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
 #pragma unroll
     for (int j = 0; j < N; j++) aC[0][j] = aC[1][j] = aP[0][j] = aP[1][j] = 0.0;
   };
-  auto acc_row = [&](int i, int y, double u, const double (&mL)[N], const double (&mR)[N],
-                     const double (&lL)[N], const double (&lR)[N]) {
+  auto acc_row = [&](int i, double u, const double (&mL)[N], const double (&mR)[N], const double (&lL)[N],
+                     const double (&lR)[N]) {
     if (i == 0 && syp >= 0) {
 #pragma unroll
       for (int j = 0; j < N; j++) {
@@ -435,35 +535,33 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
       }
     }
   };
+  // after a barrier, every warp: c and yhat summed over warps in a fixed order (lane t: entry t)
   auto fin_c = [&]() -> double {
     double s = 0.0;
-    if (lane < nc)
-      for (int w2 = 0; w2 < nwarps; w2++) s += bins[w2 * 32 + lane];
+#pragma unroll
+    for (int w2 = 0; w2 < MAXW; w2++) s += bins[w2 * 32 + lane];
     return s;
   };
-  auto put_y = [&](double yv) {
-    Yw[warp * 32 + lane] = (lane < nc) ? yv : 0.0;
-    __syncwarp();
-  };
+
   auto slot_put = [&](int which, double v) {
     v = warp_sum0(v);
     if (lane == 0) slots[which * 32 + warp] = v;
   };
-  auto slot_fin = [&](int which) { return warp_sum0((lane < nwarps) ? slots[which * 32 + lane] : 0.0); };
+  auto slot_fin = [&](int which) { return warp_sum0((lane < MAXW) ? slots[which * 32 + lane] : 0.0); };
 
   // ---- init: x0 = D^-1 C^T S^-1 t (minimum-norm feasible point), r0 = A x0 - b,
   //      c = C D^-1 r0, yhat = S^-1 c; returns r0^T D^-1 r0 -----------------------------------
   const bool lev2 = !L1OP && A.level >= 2;  // the level-1 variant is only launched at level 1
   const double* bvec = lev2 ? A.B + P.vec_off + (int64_t)rhs * nn : nullptr;
   auto init = [&](double tval) -> double {
-    put_y(warp_sinv(Si, nc, tval));
+    yh = warp_sinv<NCM>(Si, nc, tval);
     if (wact) {
       sweep_ct([&](int i, int y, double ct) {
-        const double x0 = dinv(y) * ct;
-        if (lact) Pref(y, x) = x0;
-        tm_st2(tm + 4 * i + 2, x0);
+        const double x0 = (double)dinv_s[y * DX + xc] * ct;
+        if (lact) p_s[(y + 1) * PX + x + 1] = x0;
+        gput(tmx, i, x0);
       });
-      tm_wait_st();
+      gflush(tmx);
     }
     __syncthreads();
     double rr = 0.0;
@@ -476,22 +574,19 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
       cw.start(yb);
 #pragma unroll
       for (int i = 0; i < RPT; i++) {
-        if (i < nrow) {
-          const int y = yb + i;
-          double mL[N], mR[N], lL[N], lR[N];
-          cw.row(i == 0 && syp >= 0, mL, mR, lL, lR);
-          const double u = dinv(y) * r[i];
-          rr += r[i] * u;
-          acc_row(i, y, u, mL, mR, lL, lR);
-        }
-        row_fence();
+        if (i >= nrow) break;
+        double mL[N], mR[N], lL[N], lR[N];
+        cw.row(i == 0 && syp >= 0, mL, mR, lL, lR);
+        const double u = (double)dinv_s[(yb + i) * DX + xc] * r[i];
+        rr += r[i] * u;
+        acc_row(i, u, mL, mR, lL, lR);
       }
       c_reduce();
     }
     slot_put(2, rr);
     __syncthreads();
     rr = slot_fin(2);
-    put_y(warp_sinv(Si, nc, fin_c()));
+    yh = warp_sinv<NCM>(Si, nc, fin_c());
     return rr;
   };
 
@@ -509,7 +604,7 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
     if (wact) {
       sweep_ct([&](int i, int y, double ct) {
         const double w = r[i] - ct;
-        v += lact ? dinv(y) * w * w : 0.0;
+        v += lact ? (double)dinv_s[y * DX + xc] * w * w : 0.0;
       });
     }
     slot_put(0, v);
@@ -522,134 +617,178 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
   const double floor2 = 1e-30 * fmax(rr0, rr_ref);
   double beta = 0.0, rz = 0.0, ref = 0.0;
   int it = 0, breakdown = 0;
+#ifdef PCG2D_TIMING
+  unsigned long long tacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long tprev = clock64();
+#define TMARK(k)                              \
+  {                                           \
+    const unsigned long long t_ = clock64();  \
+    tacc[k] += t_ - tprev;                    \
+    tprev = t_;                               \
+  }
+#else
+#define TMARK(k)
+#endif
+  double alpha = 0.0;
   for (;; it++) {
-    // pass A: r <- r - C^T yhat (re-projection), z = D^-1 r, p <- -z + beta p, rz = r.z
+    // pass A: x += alpha_prev p_prev (deferred update), r <- r - C^T yhat (re-projection),
+    // z = D^-1 r, p <- -z + beta p, rz = r.z
     double v = 0.0;
     if (wact) {
       const bool first = (it == 0);
-      sweep_ct([&](int i, int y, double ct) {
-        const double rk = lact ? r[i] - ct : 0.0;
-        r[i] = rk;
-        const double z = dinv(y) * rk;
-        if (lact) {
-          double& pk = Pref(y, x);
-          pk = first ? -z : -z + beta * pk;
+      double YL[N], YR[N], YLp[N], YRp[N];
+#pragma unroll
+      for (int j = 0; j < N; j++) {
+        YL[j] = __shfl_sync(FULLMASK, yh, (sy * ws + sxL) * N + j);
+        YR[j] = __shfl_sync(FULLMASK, yh, (sy * ws + sxR) * N + j);
+        YLp[j] = __shfl_sync(FULLMASK, yh, (max(syp, 0) * ws + sxL) * N + j);
+        YRp[j] = __shfl_sync(FULLMASK, yh, (max(syp, 0) * ws + sxR) * N + j);
+      }
+      const int yb = opaque(y0);
+      cw.start(yb);
+#pragma unroll
+      for (int g = 0; g < RPT; g += 4) {
+        if (g >= nrow) break;
+        uint32_t xa[8];
+        tm_ld8(tmx + 2 * g, xa);
+        tm_wait_ld();
+        double xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int i = g + u;
+          xv[u] = dbl(xa[2 * u], xa[2 * u + 1]);
+          if (i < RPT && i < nrow) {
+            const int y = yb + i;
+            double mL[N], mR[N], lL[N], lR[N];
+            const bool split = (i == 0) && (syp >= 0);
+            cw.row(split, mL, mR, lL, lR);
+            double ct = 0.0;
+            if (split) {
+#pragma unroll
+              for (int j = 0; j < N; j++)
+                ct += lL[j] * YLp[j] + (mL[j] - lL[j]) * YL[j] + lR[j] * YRp[j] + (mR[j] - lR[j]) * YR[j];
+            } else {
+#pragma unroll
+              for (int j = 0; j < N; j++) ct += mL[j] * YL[j] + mR[j] * YR[j];
+            }
+            const double rk = lact ? r[i] - ct : 0.0;
+            r[i] = rk;
+            const double z = (double)dinv_s[y * DX + xc] * rk;
+            double& pk = p_s[(y + 1) * PX + xc + 1];
+            const double pold = pk;
+            xv[u] += alpha * pold;
+            if (lact) pk = first ? -z : -z + beta * pold;
+            v += rk * z;
+          }
         }
-        v += rk * z;
-      });
+        tm_st8(tmx + 2 * g, xv);
+      }
+      tm_wait_st();
     }
+    TMARK(0);
     slot_put(0, v);
     __syncthreads();  // B1: p complete
-    rz = slot_fin(0);
-    if (it == 0) ref = fmax(rz, rz_ref);
-    if (!(rz > fmax(tol2 * ref, floor2)) || it >= A.max_iter) break;
-    // pass B: q = A p, pq
+    TMARK(1);
+    // pass B: q = A p (to TMEM), pq
     double w = 0.0;
     if (wact) {
       sweep_stencil([&](int i, int y, double Ap, double pk) {
         w += lact ? pk * Ap : 0.0;
-        tm_st2(tm + 4 * i, Ap);
+        gput(tmq, i, Ap);
       });
-      tm_wait_st();
+      gflush(tmq);
     }
+    TMARK(2);
     slot_put(1, w);
     __syncthreads();  // B2
+    rz = slot_fin(0);
     const double pq = slot_fin(1);
+    TMARK(3);
+    if (it == 0) ref = fmax(rz, rz_ref);
+    if (!(rz > fmax(tol2 * ref, floor2)) || it >= A.max_iter) break;
     if (!(pq > 0.0) || !isfinite(pq)) {  // loss of definiteness: report, do not loop
       breakdown = 1;
       break;
     }
-    const double alpha = rz / pq;
-    // pass C: x += alpha p, r += alpha q, rr = r^T D^-1 r, c = C D^-1 r (warp part)
+    alpha = rz / pq;
+    // pass C: r += alpha q, rr = r^T D^-1 r, c = C D^-1 r (warp part)
     double rr = 0.0;
     if (wact) {
       acc_zero();
       const int yb = opaque(y0);
       cw.start(yb);
 #pragma unroll
-      for (int i0 = 0; i0 < RPT; i0 += 4) {
-        if (i0 < nrow) {
-          uint32_t tv[4][4];
-#pragma unroll
-          for (int u = 0; u < 4; u++)
-            if (i0 + u < RPT) tm_ld4(tm + 4 * (i0 + u), tv[u]);
-          tm_wait_ld();
-#pragma unroll
-          for (int u = 0; u < 4; u++) {
-            const int i = i0 + u;
-            if (i < RPT && i < nrow) {
-              const int y = yb + i;
-              const double q = dbl(tv[u][0], tv[u][1]);
-              const double xv = dbl(tv[u][2], tv[u][3]) + alpha * Pref(y, xc);
-              const double rk = lact ? r[i] + alpha * q : 0.0;
-              r[i] = rk;
-              const double uu = dinv(y) * rk;
-              rr += rk * uu;
-              double mL[N], mR[N], lL[N], lR[N];
-              cw.row(i == 0 && syp >= 0, mL, mR, lL, lR);
-              acc_row(i, y, uu, mL, mR, lL, lR);
-              tm_st2(tm + 4 * i + 2, xv);
-            }
-            row_fence();
-          }
-        }
-      }
-      tm_wait_st();
-      c_reduce();
-    }
-    slot_put(2, rr);
-    __syncthreads();  // B3
-    rr = slot_fin(2);
-    const double cv = fin_c();
-    const double yv = warp_sinv(Si, nc, cv);
-    const double cy = warp_sum0((lane < nc) ? cv * yv : 0.0);
-    put_y(yv);
-    beta = (rr - cy) / rz;
-  }
-
-  // feasibility restoration: x += D^-1 C^T S^-1 (g - C x)
-  auto sweep_x = [&](auto&& f) {  // f(i, y, x_k) with x from TMEM
-    const int yb = opaque(y0);
-#pragma unroll
-    for (int i0 = 0; i0 < RPT; i0 += 4) {
-      if (i0 < nrow) {
-        uint32_t tv[4][4];
-#pragma unroll
-        for (int u = 0; u < 4; u++)
-          if (i0 + u < RPT) tm_ld4(tm + 4 * (i0 + u), tv[u]);
+      for (int g = 0; g < RPT; g += 4) {
+        if (g >= nrow) break;
+        uint32_t qa[8];
+        tm_ld8(tmq + 2 * g, qa);
         tm_wait_ld();
 #pragma unroll
         for (int u = 0; u < 4; u++) {
-          const int i = i0 + u;
-          if (i < RPT && i < nrow) f(i, yb + i, dbl(tv[u][2], tv[u][3]));
-          row_fence();
+          const int i = g + u;
+          if (i < RPT && i < nrow) {
+            const int y = yb + i;
+            const double rk = lact ? r[i] + alpha * dbl(qa[2 * u], qa[2 * u + 1]) : 0.0;
+            r[i] = rk;
+            const double uu = (double)dinv_s[y * DX + xc] * rk;
+            rr += rk * uu;
+            double mL[N], mR[N], lL[N], lR[N];
+            cw.row(i == 0 && syp >= 0, mL, mR, lL, lR);
+            acc_row(i, uu, mL, mR, lL, lR);
+          }
         }
       }
+      TMARK(4);
+      c_reduce();
     }
-  };
+    TMARK(5);
+    slot_put(2, rr);
+    __syncthreads();  // B3
+    if (warp == 0) {  // yhat = S^-1 c, beta = (r^T D^-1 r - c.yhat) / rz
+      const double cv = fin_c();
+      const double yv = warp_sinv<NCM>(Si, nc, cv);
+      const double cy = warp_sum0(cv * yv);
+      const double rrs = slot_fin(2);
+      Ysh[lane] = yv;
+      if (lane == 0) Ysh[32] = (rrs - cy) / rz;
+    }
+    __syncthreads();  // B4
+    yh = Ysh[lane];
+    beta = Ysh[32];
+    TMARK(6);
+  }
+#ifdef PCG2D_TIMING
+  if (lane == 0)
+    for (int k = 0; k < 7; k++) atomicAdd(&g_pcg2d_phase[(wact ? 0 : 8) + k], tacc[k]);
+  if (lane == 0 && wact) atomicAdd(&g_pcg2d_phase[7], (unsigned long long)it);
+#endif
+
+  // feasibility restoration: x += D^-1 C^T S^-1 (g - C x)
   if (wact) {
     acc_zero();
     cw.start(opaque(y0));
-    sweep_x([&](int i, int y, double xv) {
+    sweep_x([&](int i, int, double xv) {
       double mL[N], mR[N], lL[N], lR[N];
       cw.row(i == 0 && syp >= 0, mL, mR, lL, lR);
-      acc_row(i, y, lact ? xv : 0.0, mL, mR, lL, lR);
+      acc_row(i, lact ? xv : 0.0, mL, mR, lL, lR);
+      return xv;
     });
     c_reduce();
   }
   __syncthreads();
-  put_y(warp_sinv(Si, nc, gcol - fin_c()));
+  yh = warp_sinv<NCM>(Si, nc, gcol - fin_c());
   if (wact) {
     double ctv[RPT];
-    sweep_ct([&](int i, int y, double ct) { ctv[i] = ct; });
+    sweep_ct([&](int i, int, double ct) { ctv[i] = ct; });
     double* xo = A.X + P.vec_off + (int64_t)rhs * nn;
     double* po = (A.level == 1 && P.pool_off >= 0) ? A.pool + P.pool_off + (int64_t)rhs * nn : nullptr;
     sweep_x([&](int i, int y, double xv) {
-      const double xf = xv + dinv(y) * ctv[i];
+      const double xf = xv + (double)dinv_s[y * DX + xc] * ctv[i];
       if (lact) {
         xo[y * nx + x] = xf;
         if (po) po[y * nx + x] = xf;
       }
+      return xf;
     });
   }
   if (threadIdx.x == 0) {
@@ -671,13 +810,13 @@ __global__ void __launch_bounds__(L1OP ? 768 : 384, L1OP ? 1 : 2) k_pcg2d(LevelA
 }
 
 // ------------------------------------------------------------------------------------------
-size_t pcg2d_smem(int nx, int ny, int nc, int nwarps, bool l1op) {
-  const int nxm = l1op ? PCG2D_NXMAX_L1 : PCG2D_NXMAX_GN;
-  (void)nx;
-  size_t d = (size_t)nc * nc + 2 * (size_t)nwarps * 32 + 3 * 32 + (size_t)(nxm + 2) * (ny + 2);
-  if (l1op) d += (size_t)(nxm + 1) * (ny + 1);
-  size_t b = d * sizeof(double) + (size_t)nxm * ny * sizeof(float);
-  if (l1op) b += (size_t)(nxm + 1) * (ny + 1);
+size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw) {
+  const int PX = nxm + 2, KX = nxm + 1, DX = nxm, LW = (N == 1) ? 1 : ((N + 1) & ~1);
+  size_t d = ((81 * N * N + 1) & ~1) + 64 + 3 * 32 + (size_t)maxw * 32 + (size_t)PX * (nxm + 2);
+  d += 1;  // O_LUT rounded up to 16 bytes
+  if (l1op) d += (size_t)KX * (nxm + 1) + 16 * LW;
+  size_t b = d * sizeof(double) + (size_t)DX * nxm * sizeof(float);
+  if (l1op) b += (size_t)KX * (nxm + 1) + (size_t)DX * nxm;
   return (b + 15) & ~(size_t)15;
 }
 
@@ -692,28 +831,41 @@ cudaError_t launch_node_ops2d(const LevelArgs& A, int max_nodes, cudaStream_t st
   return cudaGetLastError();
 }
 
-template <int RPT, int N, bool L1OP>
-static cudaError_t launch_one(const LevelArgs& A, int threads, size_t smem, cudaStream_t st) {
-  auto k = k_pcg2d<RPT, N, L1OP>;
+template <int RPT, int N, bool L1OP, int NXM, int MAXW>
+static cudaError_t launch_one(const LevelArgs& A, int threads, cudaStream_t st) {
+  auto k = k_pcg2d<RPT, N, L1OP, NXM, MAXW>;
+  const size_t smem = pcg2d_smem_t(N, L1OP, NXM, MAXW);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<(unsigned)A.nprob_mp * A.n_rhs, threads, smem, st>>>(A);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pcg2d(const LevelArgs& A, bool l1op, int threads, size_t smem, cudaStream_t st) {
-  if (l1op) {
-    switch (A.N) {
-      case 1: return launch_one<PCG2D_RPT_L1, 1, true>(A, threads, smem, st);
-      case 2: return launch_one<PCG2D_RPT_L1, 2, true>(A, threads, smem, st);
-      case 3: return launch_one<PCG2D_RPT_L1, 3, true>(A, threads, smem, st);
-    }
-  } else {
-    switch (A.N) {
-      case 1: return launch_one<PCG2D_RPT_GN, 1, false>(A, threads, smem, st);
-      case 2: return launch_one<PCG2D_RPT_GN, 2, false>(A, threads, smem, st);
-      case 3: return launch_one<PCG2D_RPT_GN, 3, false>(A, threads, smem, st);
-    }
+template <int N>
+static cudaError_t launch_n(const LevelArgs& A, int variant, int threads, cudaStream_t st) {
+  switch (variant) {
+    case PCG2D_V_L1: return launch_one<17, N, true, 97, 24>(A, threads, st);
+    case PCG2D_V_GN49: return launch_one<9, N, false, 49, 12>(A, threads, st);
+    case PCG2D_V_GN25: return launch_one<9, N, false, 25, 4>(A, threads, st);
+    case PCG2D_V_GN97: return launch_one<17, N, false, 97, 24>(A, threads, st);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_pcg2d(const LevelArgs& A, int variant, int threads, cudaStream_t st) {
+  switch (A.N) {
+    case 1: return launch_n<1>(A, variant, threads, st);
+    case 2: return launch_n<2>(A, variant, threads, st);
+    case 3: return launch_n<3>(A, variant, threads, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// variant limits: rows per thread, widest window (nodes), warps per CTA
+void pcg2d_variant(int variant, int* rpt, int* nxm, int* maxw, int* l1op) {
+  static const int T[4][4] = {{17, 97, 24, 1}, {9, 49, 12, 0}, {9, 25, 4, 0}, {17, 97, 24, 0}};
+  *rpt = T[variant][0];
+  *nxm = T[variant][1];
+  *maxw = T[variant][2];
+  *l1op = T[variant][3];
 }
