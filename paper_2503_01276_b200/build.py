@@ -10,9 +10,12 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libmch.so")
 SOURCES = ["mch.cu", "kernels.cu", "pcg2d.cu", "plan.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-# MCH_BUILD_TIMING=1 builds lib/libmch_timing.so with per-phase PCG cycle counters (dev tool)
+# dev variants: MCH_BUILD_TIMING=1 builds lib/libmch_timing.so with per-phase PCG cycle counters;
+# MCH_BUILD_TAG=t MCH_BUILD_DEFS="-DX=1 ..." builds lib/libmch_t.so with extra defines
 if os.environ.get("MCH_BUILD_TIMING"):
     LIB = os.path.join(HERE, "lib", "libmch_timing.so")
+if os.environ.get("MCH_BUILD_TAG"):
+    LIB = os.path.join(HERE, "lib", "libmch_" + os.environ["MCH_BUILD_TAG"] + ".so")
 FLAGS_C = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
@@ -38,10 +41,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs, objs = [], []
     for src in SOURCES:
         timing = bool(os.environ.get("MCH_BUILD_TIMING"))
-        obj = os.path.join(objdir, src + (".timing.o" if timing else ".o"))
+        tag = os.environ.get("MCH_BUILD_TAG", "") + (".timing" if timing else "")
+        obj = os.path.join(objdir, src + (f".{tag}.o" if tag else ".o"))
         objs.append(obj)
-        cmd = [NVCC, *FLAGS_C, *(["-DPCG2D_TIMING"] if timing else []), "-c", "-o", obj,
-               os.path.join(CSRC, src)]
+        defs = (["-DPCG2D_TIMING"] if timing else []) + os.environ.get("MCH_BUILD_DEFS", "").split()
+        cmd = [NVCC, *FLAGS_C, *defs, "-c", "-o", obj, os.path.join(CSRC, src)]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     log_parts, failed = [], False
     for cmd, pr in procs:

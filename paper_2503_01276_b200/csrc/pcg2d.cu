@@ -248,8 +248,8 @@ void pcg2d_phase_dump(const char* tag) {
 void pcg2d_phase_dump(const char*) {}
 #endif
 
-template <int RPT, int N, bool L1OP, int NXM, int MAXW>
-__global__ void __launch_bounds__(MAXW * 32, MAXW >= 24 ? 1 : (MAXW >= 12 ? 2 : 6)) k_pcg2d(LevelArgs A) {
+template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB>
+__global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   constexpr int RP4 = (RPT + 3) & ~3;  // rows rounded to the 4-row TMEM groups
   constexpr int NBC = 4 * RP4;         // TMEM columns per thread: q block, then x block
   // compile-time pitches and shared-memory offsets (host checks nx, ny <= NXM and warps <= MAXW):
@@ -831,9 +831,9 @@ cudaError_t launch_node_ops2d(const LevelArgs& A, int max_nodes, cudaStream_t st
   return cudaGetLastError();
 }
 
-template <int RPT, int N, bool L1OP, int NXM, int MAXW>
+template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB>
 static cudaError_t launch_one(const LevelArgs& A, int threads, cudaStream_t st) {
-  auto k = k_pcg2d<RPT, N, L1OP, NXM, MAXW>;
+  auto k = k_pcg2d<RPT, N, L1OP, NXM, MAXW, MINB>;
   const size_t smem = pcg2d_smem_t(N, L1OP, NXM, MAXW);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -841,13 +841,32 @@ static cudaError_t launch_one(const LevelArgs& A, int threads, cudaStream_t st) 
   return cudaGetLastError();
 }
 
+#ifndef L1_RPT
+#define L1_RPT 33
+#endif
+#ifndef L1_MAXW
+#define L1_MAXW 12
+#endif
+#ifndef GN49_RPT
+#define GN49_RPT 9
+#endif
+#ifndef GN49_MAXW
+#define GN49_MAXW 12
+#endif
+#ifndef GN49_MINB
+#define GN49_MINB 1
+#endif
+#ifndef GN25_MINB
+#define GN25_MINB 6
+#endif
+
 template <int N>
 static cudaError_t launch_n(const LevelArgs& A, int variant, int threads, cudaStream_t st) {
   switch (variant) {
-    case PCG2D_V_L1: return launch_one<17, N, true, 97, 24>(A, threads, st);
-    case PCG2D_V_GN49: return launch_one<9, N, false, 49, 12>(A, threads, st);
-    case PCG2D_V_GN25: return launch_one<9, N, false, 25, 4>(A, threads, st);
-    case PCG2D_V_GN97: return launch_one<17, N, false, 97, 24>(A, threads, st);
+    case PCG2D_V_L1: return launch_one<L1_RPT, N, true, 97, L1_MAXW, 1>(A, threads, st);
+    case PCG2D_V_GN49: return launch_one<GN49_RPT, N, false, 49, GN49_MAXW, GN49_MINB>(A, threads, st);
+    case PCG2D_V_GN25: return launch_one<9, N, false, 25, 4, GN25_MINB>(A, threads, st);
+    case PCG2D_V_GN97: return launch_one<17, N, false, 97, 24, 1>(A, threads, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -863,7 +882,7 @@ cudaError_t launch_pcg2d(const LevelArgs& A, int variant, int threads, cudaStrea
 
 // variant limits: rows per thread, widest window (nodes), warps per CTA
 void pcg2d_variant(int variant, int* rpt, int* nxm, int* maxw, int* l1op) {
-  static const int T[4][4] = {{17, 97, 24, 1}, {9, 49, 12, 0}, {9, 25, 4, 0}, {17, 97, 24, 0}};
+  static const int T[4][4] = {{L1_RPT, 97, L1_MAXW, 1}, {GN49_RPT, 49, GN49_MAXW, 0}, {9, 25, 4, 0}, {17, 97, 24, 0}};
   *rpt = T[variant][0];
   *nxm = T[variant][1];
   *maxw = T[variant][2];
