@@ -105,6 +105,15 @@ int mch_solve_level(mch_ctx* ctx, int level);
  * are left as 0 (the Python layer all-gathers them).  Requires all levels. */
 int mch_effective_coeffs(mch_ctx* ctx, double* out, size_t out_len, int out_on_device);
 
+/* Replace the medium of an existing context: validate and copy kappa (float64, n^d) and
+ * continuum ids (uint8, n^d) exactly as mch_create does, keeping the hierarchy, the per-level
+ * plans and all device buffers, and rewind the level counter (as mch_reset).  The coefficients
+ * of the previous medium are discarded.  PAPER.md:124-125 (kappa, psi_j define the problem;
+ * the macropoint hierarchy of Algorithm 1, depends only on the grid).  The
+ * copy is ordered on params.stream; the call returns after the inputs were validated.  Errors:
+ * MCH_EINVAL (NULL pointers, kappa <= 0 / non-finite, id >= N), MCH_ECUDA. */
+int mch_set_medium(mch_ctx* ctx, const double* kappa, const uint8_t* continuum_id, int inputs_on_device);
+
 /* Rewind the level counter so the same context (inputs, plan, pool, scratch) solves levels
  * 1..L again — for repeated runs (benchmarks, serving) without re-creating the context. */
 int mch_reset(mch_ctx* ctx);

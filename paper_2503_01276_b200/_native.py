@@ -16,7 +16,7 @@ ERRORS = {-1: "MCH_EINVAL", -2: "MCH_EDIVISIBILITY", -3: "MCH_ERANK", -4: "MCH_E
           -5: "MCH_EORDER", -6: "MCH_ECUDA", -7: "MCH_ENOMEM", -8: "MCH_EPLAN"}
 
 # every symbol include/mch.h declares
-SYMBOLS = ["mch_create", "mch_reset", "mch_solve_level", "mch_effective_coeffs", "mch_num_macropoints", "mch_level_macropoints",
+SYMBOLS = ["mch_create", "mch_set_medium", "mch_reset", "mch_solve_level", "mch_effective_coeffs", "mch_num_macropoints", "mch_level_macropoints",
            "mch_local_solution", "mch_get_level_stats", "mch_pool_info", "mch_pool_slot",
            "mch_coeffs_device", "mch_last_error", "mch_destroy"]
 
@@ -53,6 +53,7 @@ def _load():
     P = ctypes.POINTER
     vp, i64, i32, dbl = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     lib.mch_create.argtypes = [P(MchParams), vp, vp, i32, P(vp)]
+    lib.mch_set_medium.argtypes = [vp, vp, vp, i32]
     lib.mch_solve_level.argtypes = [vp, i32]
     lib.mch_reset.argtypes = [vp]
     lib.mch_effective_coeffs.argtypes = [vp, vp, ctypes.c_size_t, i32]

@@ -56,6 +56,18 @@ def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversamp
     return ctx
 
 
+def mch_set_medium(ctx, kappa, continuum_id):
+    """New medium into an existing context (plan and buffers reused); host or device inputs."""
+    if isinstance(kappa, np.ndarray):
+        kappa = np.ascontiguousarray(kappa, dtype=np.float64)
+        continuum_id = np.ascontiguousarray(continuum_id, dtype=np.uint8)
+    kp, kdev = _ptr(kappa)
+    ip, idev = _ptr(continuum_id)
+    if kdev != idev:
+        raise ValueError("kappa and continuum_id must both be host or both be device buffers")
+    check(lib.mch_set_medium(ctx, kp, ip, kdev), ctx)
+
+
 def mch_solve_level(ctx, level):
     check(lib.mch_solve_level(ctx, level), ctx)
 
@@ -94,6 +106,10 @@ class Homogenizer:
 
     def reset(self):
         check(lib.mch_reset(self.ctx), self.ctx)
+        self.solved = 0
+
+    def set_medium(self, kappa, ids):
+        mch_set_medium(self.ctx, kappa, ids)
         self.solved = 0
 
     def solve_all(self):
@@ -174,5 +190,5 @@ class Homogenizer:
         self.close()
 
 
-__all__ = ["Homogenizer", "mch_create", "mch_solve_level", "mch_effective_coeffs", "mch_destroy",
+__all__ = ["Homogenizer", "mch_create", "mch_set_medium", "mch_solve_level", "mch_effective_coeffs", "mch_destroy",
            "_native"]

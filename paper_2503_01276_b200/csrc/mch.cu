@@ -2,7 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <chrono>
+#include <memory>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -48,6 +48,36 @@ int64_t ipow64(int64_t b, int e) {
 
 }  // namespace
 
+// Host plan of one level, built on its first solve and reused by every later solve (mch_reset):
+// macropoint batches, their device descriptors and row-chunk tables, the chosen PCG variant,
+// pinned result buffers and timing events, so a solve issues only kernel launches, async copies
+// into pinned memory and one stream synchronisation.
+struct LevelBatch {
+  int nmp = 0;
+  int64_t node_off = 0, vec_off = 0, fine_off = 0;
+  int max_ln = 0, max_fn = 0, th_l = 64, th_f = 64;
+  std::vector<int64_t> mps, ln, lc;
+  DevBuf descs, segs, nseg;
+  bool on2d = false, l1op = false;
+  int variant = -1, threads2 = 0, maxseg = 0, tm_cols = 32;
+  int* h_flags = nullptr;  // pinned results
+  int* h_iters = nullptr;
+  double* h_relres = nullptr;
+  double* h_diag = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  ~LevelBatch() {
+    descs.release();
+    segs.release();
+    nseg.release();
+    if (h_flags) cudaFreeHost(h_flags);
+    if (h_iters) cudaFreeHost(h_iters);
+    if (h_relres) cudaFreeHost(h_relres);
+    if (h_diag) cudaFreeHost(h_diag);
+    for (cudaEvent_t& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
 struct mch_ctx {
   mch_params p{};
   int D = 2, N = 1, n_rhs = 3, l = 1, w = 3, nsub = 9, ncon = 9;
@@ -64,9 +94,12 @@ struct mch_ctx {
   std::vector<mch_level_stats> stats;
   std::string err;
   // grow-only scratch
-  DevBuf descs, segs, nseg, STC, MLR, W, Mc, g0, g, meas, cm, flags, dinv, nwt, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
+  DevBuf STC, MLR, W, Mc, g0, g, meas, cm, flags, dinv, nwt, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
   cudaEvent_t ev[8];
   bool events = false;
+  std::vector<std::vector<std::unique_ptr<LevelBatch>>> lplans;  // per level, built on first solve
+  int* h_bad = nullptr;  // mch_set_medium validation flag (pinned / device)
+  int* d_bad = nullptr;
   int pcg_mode = 0;  // 0: on-chip 2D PCG where it applies; 1: generic k_pcg; 2: on-chip, precomputed operator at level 1
 };
 
@@ -223,41 +256,14 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   return MCH_OK;
 }
 
-extern "C" int mch_solve_level(mch_ctx* c, int level) {
-  if (!c) return MCH_EINVAL;
-  if (level != c->solved + 1 || level > c->p.levels)
-    return fail(c, MCH_EORDER, "levels must be solved 1..L in order");
+static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelBatch>>& out) {
   const int D = c->D, N = c->N, nr = c->n_rhs, nc = c->ncon;
   const HostPlan& pl = c->plan;
   const int s = (int)ipow64(c->p.eta, level - 1);
-  const int gn = (int)(pl.n / s);
-  cudaStream_t st = c->st;
-  mch_level_stats& S = c->stats[level];
-  S = mch_level_stats{};
-  cudaEventRecord(c->ev[0], st);
-
-  LevelArgs A{};
-  A.D = D; A.N = N; A.n_rhs = nr; A.l = c->l; A.w = c->w; A.nsub = c->nsub; A.ncon = nc;
-  A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.gn = gn; A.h = 1.0 / (double)pl.n; A.inv_c = 1.0f / (float)pl.c;
-  A.kappa = c->kappa; A.ids = c->ids; A.pool = c->pool; A.G = c->G;
-  A.rtol = c->p.rtol; A.max_iter = c->p.max_iter;
-  float ms_setup = 0, ms_pcg = 0, ms_gram = 0;
-  if (level >= 2) {
-    const int64_t gcells = (D == 2) ? (int64_t)gn * gn : (int64_t)gn * gn * gn;
-    const int NW = (D == 2) ? 6 : 27;
-    CKC(c, c->W.ensure(gcells * NW * sizeof(double)));
-    CKC(c, c->Mc.ensure(gcells * (N << D) * sizeof(double)));
-    A.W = c->W.as<double>();
-    A.Mc = c->Mc.as<double>();
-    CKC(c, launch_level_ops(A, st));
-    S.launches += 1;
-  }
-  // this rank's macropoints of S_level
   const std::vector<int64_t>& Sl = pl.S[level];
   std::vector<int64_t> mine;
   for (size_t i = 0; i < Sl.size(); i++)
     if ((int)(i % c->p.world) == c->p.rank) mine.push_back(Sl[i]);
-  // per-macropoint sizes and batching by memory
   auto sizes = [&](const MacroHost& m, int64_t& ln, int64_t& fnn, int64_t& lcells) {
     ln = 1; fnn = 1; lcells = 1;
     for (int d = 0; d < D; d++) {
@@ -268,17 +274,10 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     }
   };
   size_t freeb = 0, totb = 0;
-  const bool htime = getenv("MCH_HOST_TIMING") != nullptr;
-  auto now = [] { return std::chrono::steady_clock::now(); };
-  auto th0 = now();
-  double h_plan = 0, h_launch = 0, h_sync = 0, h_post = 0;
   cudaMemGetInfo(&freeb, &totb);
   const double budget = std::min<double>(48e9, 0.5 * (double)freeb);
   size_t bstart = 0;
-  std::vector<int> h_iters;
-  std::vector<double> h_relres;
   while (bstart < mine.size()) {
-    // choose batch
     size_t bend = bstart;
     double bytes = 0;
     while (bend < mine.size()) {
@@ -290,16 +289,19 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       bytes += b;
       bend++;
     }
+    std::unique_ptr<LevelBatch> B(new LevelBatch());
     const int nmp = (int)(bend - bstart);
+    B->nmp = nmp;
     std::vector<ProbDesc> descs(nmp);
-    int64_t node_off = 0, vec_off = 0, fine_off = 0;
-    int max_ln = 0, max_fn = 0;
     for (int i = 0; i < nmp; i++) {
       const MacroHost& m = pl.all[mine[bstart + i]];
       ProbDesc& P = descs[i];
       memset(&P, 0, sizeof(P));
       int64_t ln, fnn, lc;
       sizes(m, ln, fnn, lc);
+      B->mps.push_back(mine[bstart + i]);
+      B->ln.push_back(ln);
+      B->lc.push_back(lc);
       for (int d = 0; d < 3; d++) {
         P.k[d] = m.k[d];
         P.lo[d] = (d < D) ? m.lo[d] : 0;
@@ -311,15 +313,15 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
         P.kp_hi[d] = (d < D) ? (int)std::min<int64_t>(pl.n, b) : 1;
       }
       P.lin = m.lin;
-      P.node_off = node_off;
-      P.vec_off = vec_off;
-      P.fine_off = fine_off;
+      P.node_off = B->node_off;
+      P.vec_off = B->vec_off;
+      P.fine_off = B->fine_off;
       P.pool_off = c->pool_off[m.lin];
-      node_off += ln;
-      vec_off += ln * nr;
-      if (level >= 2) fine_off += fnn * nr;
-      max_ln = std::max<int>(max_ln, (int)ln);
-      max_fn = std::max<int>(max_fn, (int)fnn);
+      B->node_off += ln;
+      B->vec_off += ln * nr;
+      if (level >= 2) B->fine_off += fnn * nr;
+      B->max_ln = std::max<int>(B->max_ln, (int)ln);
+      B->max_fn = std::max<int>(B->max_fn, (int)fnn);
       P.npar = m.npar;
       for (int t = 0; t < m.npar; t++) {
         const MacroHost& pm = pl.all[m.par_lin[t]];
@@ -332,59 +334,18 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
         P.par_w[t] = m.par_w[t];
         if (P.par_pool[t] < 0) return fail(c, MCH_EPLAN, "parent not in pool");
       }
-      S.unknowns_level += ln;
-      S.cells_level += lc;
     }
-    auto tb0 = now();
-    CKC(c, c->descs.ensure(sizeof(ProbDesc) * nmp));
-    CKC(c, cudaMemcpyAsync(c->descs.ptr, descs.data(), sizeof(ProbDesc) * nmp, cudaMemcpyHostToDevice, st));
-    CKC(c, c->g0.ensure(sizeof(double) * nmp * nc * nr));
-    CKC(c, c->g.ensure(sizeof(double) * nmp * nc * nr));
-    CKC(c, c->meas.ensure(sizeof(double) * nmp * nc));
-    CKC(c, c->cm.ensure(sizeof(double) * nmp * 12));
-    CKC(c, c->flags.ensure(sizeof(int) * nmp));
-    CKC(c, c->dinv.ensure(sizeof(double) * node_off));
-    CKC(c, c->nwt.ensure(sizeof(double) * node_off * N));
-    CKC(c, c->Sinv.ensure(sizeof(double) * nmp * nc * nc));
-    CKC(c, c->X.ensure(sizeof(double) * vec_off));
-    CKC(c, c->R.ensure(sizeof(double) * vec_off));
-    CKC(c, c->P.ensure(sizeof(double) * vec_off));
-    CKC(c, c->Q.ensure(sizeof(double) * vec_off));
-    CKC(c, c->B.ensure(sizeof(double) * vec_off));
-    CKC(c, c->iters.ensure(sizeof(int) * nmp * nr));
-    CKC(c, c->relres.ensure(sizeof(double) * nmp * nr));
-    CKC(c, c->diag.ensure(sizeof(double) * nmp * nr * 4));
-    if (level >= 2) {
-      CKC(c, c->FI.ensure(sizeof(double) * fine_off));
-      CKC(c, c->FY.ensure(sizeof(double) * fine_off));
-    }
-    CKC(c, cudaMemsetAsync(c->flags.ptr, 0, sizeof(int) * nmp, st));
-    A.probs = c->descs.as<ProbDesc>();
-    A.nprob_mp = nmp;
-    A.g0 = c->g0.as<double>(); A.g = c->g.as<double>(); A.meas = c->meas.as<double>();
-    A.cm = c->cm.as<double>(); A.flags = c->flags.as<int>();
-    A.dinv = c->dinv.as<double>(); A.NWt = c->nwt.as<double>(); A.Sinv = c->Sinv.as<double>();
-    A.X = c->X.as<double>(); A.R = c->R.as<double>(); A.P = c->P.as<double>(); A.Q = c->Q.as<double>();
-    A.B = c->B.as<double>();
-    A.FI = c->FI.as<double>(); A.FY = c->FY.as<double>();
-    A.iters = c->iters.as<int>(); A.relres = c->relres.as<double>(); A.diag = c->diag.as<double>();
-
     auto pick = [](int nodes) {
       int t = ((nodes / 4 + 31) / 32) * 32;
       return std::max(64, std::min(512, t));
     };
-    const int th_l = pick(max_ln), th_f = pick(max_fn);
-    auto tb1 = now();
-    cudaEventRecord(c->ev[1], st);
-    S.launches += (level >= 2) ? 6 : 4;
-    CKC(c, launch_targets(A, st));
-    if (level >= 2) CKC(c, launch_transport(A, th_f, st));
-    CKC(c, launch_proj_setup(A, th_l, st));
+    B->th_l = pick(B->max_ln);
+    B->th_f = pick(B->max_fn);
+    CKC(c, B->descs.ensure(sizeof(ProbDesc) * nmp));
+    CKC(c, cudaMemcpy(B->descs.ptr, descs.data(), sizeof(ProbDesc) * nmp, cudaMemcpyHostToDevice));
     // on-chip 2D PCG (pcg2d.cu) unless MCH_PCG=old; MCH_PCG=gn forces the precomputed-operator
     // variant at level 1 as well (cross-check of the two operator paths)
-    bool on2d = (D == 2) && N <= 3 && nc == 9 * N && c->pcg_mode != 1;  // 3x3 subcells (l = 1)
-    int variant = -1, threads2 = 0;
-    if (on2d) {
+    if ((D == 2) && N <= 3 && nc == 9 * N && c->pcg_mode != 1) {  // 3x3 subcells (l = 1)
       int maxn = 0;
       for (int i = 0; i < nmp; i++) maxn = std::max(maxn, std::max(descs[i].nc[0], descs[i].nc[1]) + 1);
       std::vector<int> cands;
@@ -412,105 +373,190 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
         std::vector<short4> all_segs((size_t)nmp * maxseg, make_short4(0, 0, 0, -1));
         for (int i = 0; i < nmp; i++)
           for (int k = 0; k < nsegs[i]; k++) all_segs[(size_t)i * maxseg + k] = per[i][k];
-        CKC(c, c->segs.ensure(sizeof(short4) * all_segs.size()));
-        CKC(c, c->nseg.ensure(sizeof(int) * nmp));
-        CKC(c, cudaMemcpyAsync(c->segs.ptr, all_segs.data(), sizeof(short4) * all_segs.size(),
-                               cudaMemcpyHostToDevice, st));
-        CKC(c, cudaMemcpyAsync(c->nseg.ptr, nsegs.data(), sizeof(int) * nmp, cudaMemcpyHostToDevice, st));
-        A.segs = c->segs.as<short4>();
-        A.nseg = c->nseg.as<int>();
-        A.maxseg = maxseg;
-        A.tm_cols = cols;
-        threads2 = 32 * maxwp;
-        variant = v;
-        if (!l1op) {
-          CKC(c, c->STC.ensure(sizeof(double) * 9 * node_off));
-          CKC(c, c->MLR.ensure(sizeof(double) * 4 * N * node_off));
-          A.STC = c->STC.as<double>();
-          A.MLR = c->MLR.as<double>();
-          CKC(c, launch_node_ops2d(A, max_ln, st));
-          S.launches += 1;
-        }
+        CKC(c, B->segs.ensure(sizeof(short4) * all_segs.size()));
+        CKC(c, B->nseg.ensure(sizeof(int) * nmp));
+        CKC(c, cudaMemcpy(B->segs.ptr, all_segs.data(), sizeof(short4) * all_segs.size(), cudaMemcpyHostToDevice));
+        CKC(c, cudaMemcpy(B->nseg.ptr, nsegs.data(), sizeof(int) * nmp, cudaMemcpyHostToDevice));
+        B->maxseg = maxseg;
+        B->tm_cols = cols;
+        B->threads2 = 32 * maxwp;
+        B->variant = v;
+        B->l1op = l1op != 0;
+        B->on2d = true;
         break;
       }
-      on2d = variant >= 0;
     }
-    cudaEventRecord(c->ev[2], st);
-    if (on2d) CKC(c, launch_pcg2d(A, variant, threads2, st));
-    else CKC(c, launch_pcg(A, th_l, st));
-    cudaEventRecord(c->ev[3], st);
-    if (getenv("MCH_PCG_TIMING") && on2d) {
+    // scratch shared by all levels and batches (grow-only, allocated here, never in a solve)
+    CKC(c, c->g0.ensure(sizeof(double) * nmp * nc * nr));
+    CKC(c, c->g.ensure(sizeof(double) * nmp * nc * nr));
+    CKC(c, c->meas.ensure(sizeof(double) * nmp * nc));
+    CKC(c, c->cm.ensure(sizeof(double) * nmp * 12));
+    CKC(c, c->flags.ensure(sizeof(int) * nmp));
+    CKC(c, c->dinv.ensure(sizeof(double) * B->node_off));
+    CKC(c, c->nwt.ensure(sizeof(double) * B->node_off * N));
+    CKC(c, c->Sinv.ensure(sizeof(double) * nmp * nc * nc));
+    CKC(c, c->X.ensure(sizeof(double) * B->vec_off));
+    CKC(c, c->iters.ensure(sizeof(int) * nmp * nr));
+    CKC(c, c->relres.ensure(sizeof(double) * nmp * nr));
+    CKC(c, c->diag.ensure(sizeof(double) * nmp * nr * 4));
+    if (!B->on2d) {  // the generic k_pcg keeps r, p, q in global memory
+      CKC(c, c->R.ensure(sizeof(double) * B->vec_off));
+      CKC(c, c->P.ensure(sizeof(double) * B->vec_off));
+      CKC(c, c->Q.ensure(sizeof(double) * B->vec_off));
+    }
+    if (level >= 2) {
+      CKC(c, c->B.ensure(sizeof(double) * B->vec_off));
+      CKC(c, c->FI.ensure(sizeof(double) * B->fine_off));
+      CKC(c, c->FY.ensure(sizeof(double) * B->fine_off));
+    }
+    if (B->on2d && !B->l1op) {
+      CKC(c, c->STC.ensure(sizeof(double) * 9 * B->node_off));
+      CKC(c, c->MLR.ensure(sizeof(double) * 4 * N * B->node_off));
+    }
+    CKC(c, cudaMallocHost(&B->h_flags, sizeof(int) * nmp));
+    CKC(c, cudaMallocHost(&B->h_iters, sizeof(int) * nmp * nr));
+    CKC(c, cudaMallocHost(&B->h_relres, sizeof(double) * nmp * nr));
+    CKC(c, cudaMallocHost(&B->h_diag, sizeof(double) * nmp * nr * 4));
+    for (cudaEvent_t& e : B->ev) CKC(c, cudaEventCreate(&e));
+    out.push_back(std::move(B));
+    bstart = bend;
+  }
+  return MCH_OK;
+}
+
+extern "C" int mch_solve_level(mch_ctx* c, int level) {
+  if (!c) return MCH_EINVAL;
+  if (level != c->solved + 1 || level > c->p.levels)
+    return fail(c, MCH_EORDER, "levels must be solved 1..L in order");
+  const int D = c->D, N = c->N, nr = c->n_rhs, nc = c->ncon;
+  const HostPlan& pl = c->plan;
+  const int s = (int)ipow64(c->p.eta, level - 1);
+  const int gn = (int)(pl.n / s);
+  cudaStream_t st = c->st;
+  if ((int)c->lplans.size() <= level) c->lplans.resize(level + 1);
+  std::vector<std::unique_ptr<LevelBatch>>& batches = c->lplans[level];
+  if (batches.empty()) {
+    const int rc = build_level(c, level, batches);
+    if (rc != MCH_OK) {
+      batches.clear();
+      return rc;
+    }
+  }
+  mch_level_stats& S = c->stats[level];
+  S = mch_level_stats{};
+  cudaEventRecord(c->ev[0], st);
+
+  LevelArgs A{};
+  A.D = D; A.N = N; A.n_rhs = nr; A.l = c->l; A.w = c->w; A.nsub = c->nsub; A.ncon = nc;
+  A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.gn = gn; A.h = 1.0 / (double)pl.n; A.inv_c = 1.0f / (float)pl.c;
+  A.kappa = c->kappa; A.ids = c->ids; A.pool = c->pool; A.G = c->G;
+  A.rtol = c->p.rtol; A.max_iter = c->p.max_iter;
+  if (level >= 2) {
+    const int64_t gcells = (D == 2) ? (int64_t)gn * gn : (int64_t)gn * gn * gn;
+    const int NW = (D == 2) ? 6 : 27;
+    CKC(c, c->W.ensure(gcells * NW * sizeof(double)));
+    CKC(c, c->Mc.ensure(gcells * (N << D) * sizeof(double)));
+    A.W = c->W.as<double>();
+    A.Mc = c->Mc.as<double>();
+    CKC(c, launch_level_ops(A, st));
+    S.launches += 1;
+  }
+  A.g0 = c->g0.as<double>(); A.g = c->g.as<double>(); A.meas = c->meas.as<double>();
+  A.cm = c->cm.as<double>(); A.flags = c->flags.as<int>();
+  A.dinv = c->dinv.as<double>(); A.NWt = c->nwt.as<double>(); A.Sinv = c->Sinv.as<double>();
+  A.X = c->X.as<double>(); A.R = c->R.as<double>(); A.P = c->P.as<double>(); A.Q = c->Q.as<double>();
+  A.B = c->B.as<double>();
+  A.FI = c->FI.as<double>(); A.FY = c->FY.as<double>();
+  A.iters = c->iters.as<int>(); A.relres = c->relres.as<double>(); A.diag = c->diag.as<double>();
+  A.STC = c->STC.as<double>(); A.MLR = c->MLR.as<double>();
+  const bool multi = batches.size() > 1;
+  for (size_t bi = 0; bi < batches.size(); bi++) {
+    LevelBatch& B = *batches[bi];
+    const int nmp = B.nmp;
+    A.probs = B.descs.as<ProbDesc>();
+    A.nprob_mp = nmp;
+    A.segs = B.segs.as<short4>();
+    A.nseg = B.nseg.as<int>();
+    A.maxseg = B.maxseg;
+    A.tm_cols = B.tm_cols;
+    CKC(c, cudaMemsetAsync(c->flags.ptr, 0, sizeof(int) * nmp, st));
+    cudaEventRecord(B.ev[0], st);
+    S.launches += (level >= 2) ? 6 : 4;
+    CKC(c, launch_targets(A, st));
+    if (level >= 2) CKC(c, launch_transport(A, B.th_f, st));
+    CKC(c, launch_proj_setup(A, B.th_l, st));
+    if (B.on2d && !B.l1op) {
+      CKC(c, launch_node_ops2d(A, B.max_ln, st));
+      S.launches += 1;
+    }
+    cudaEventRecord(B.ev[1], st);
+    if (B.on2d) CKC(c, launch_pcg2d(A, B.variant, B.threads2, st));
+    else CKC(c, launch_pcg(A, B.th_l, st));
+    cudaEventRecord(B.ev[2], st);
+    if (getenv("MCH_PCG_TIMING") && B.on2d) {
       char tag[64];
-      snprintf(tag, sizeof tag, "level %d variant %d", level, variant);
+      snprintf(tag, sizeof tag, "level %d variant %d", level, B.variant);
       pcg2d_phase_dump(tag);
     }
-    if (level >= 2) CKC(c, launch_combine(A, th_f, st));
+    if (level >= 2) CKC(c, launch_combine(A, B.th_f, st));
     CKC(c, launch_gram(A, 256, st));
-    cudaEventRecord(c->ev[4], st);
-    // results of this batch
-    std::vector<int> hf(nmp), hit(nmp * nr);
-    std::vector<double> hrr(nmp * nr), hdg(nmp * nr * 4);
-    CKC(c, cudaMemcpyAsync(hf.data(), c->flags.ptr, sizeof(int) * nmp, cudaMemcpyDeviceToHost, st));
-    CKC(c, cudaMemcpyAsync(hit.data(), c->iters.ptr, sizeof(int) * nmp * nr, cudaMemcpyDeviceToHost, st));
-    CKC(c, cudaMemcpyAsync(hrr.data(), c->relres.ptr, sizeof(double) * nmp * nr, cudaMemcpyDeviceToHost, st));
-    CKC(c, cudaMemcpyAsync(hdg.data(), c->diag.ptr, sizeof(double) * nmp * nr * 4, cudaMemcpyDeviceToHost, st));
-    auto tb2 = now();
-    CKC(c, cudaStreamSynchronize(st));
-    auto tb3 = now();
-    h_plan += std::chrono::duration<double, std::milli>(tb1 - tb0).count();
-    h_launch += std::chrono::duration<double, std::milli>(tb2 - tb1).count();
-    h_sync += std::chrono::duration<double, std::milli>(tb3 - tb2).count();
+    cudaEventRecord(B.ev[3], st);
+    CKC(c, cudaMemcpyAsync(B.h_flags, c->flags.ptr, sizeof(int) * nmp, cudaMemcpyDeviceToHost, st));
+    CKC(c, cudaMemcpyAsync(B.h_iters, c->iters.ptr, sizeof(int) * nmp * nr, cudaMemcpyDeviceToHost, st));
+    CKC(c, cudaMemcpyAsync(B.h_relres, c->relres.ptr, sizeof(double) * nmp * nr, cudaMemcpyDeviceToHost, st));
+    CKC(c, cudaMemcpyAsync(B.h_diag, c->diag.ptr, sizeof(double) * nmp * nr * 4, cudaMemcpyDeviceToHost, st));
+    // batches share the scratch: a later batch may only start after this one's results are read
+    if (multi) CKC(c, cudaStreamSynchronize(st));
+  }
+  cudaEventRecord(c->ev[5], st);
+  CKC(c, cudaEventSynchronize(c->ev[5]));
+  float ms_setup = 0, ms_pcg = 0, ms_gram = 0;
+  for (size_t bi = 0; bi < batches.size(); bi++) {
+    LevelBatch& B = *batches[bi];
     float t1 = 0, t2 = 0, t3 = 0;
-    cudaEventElapsedTime(&t1, c->ev[1], c->ev[2]);
-    cudaEventElapsedTime(&t2, c->ev[2], c->ev[3]);
-    cudaEventElapsedTime(&t3, c->ev[3], c->ev[4]);
+    cudaEventElapsedTime(&t1, B.ev[0], B.ev[1]);
+    cudaEventElapsedTime(&t2, B.ev[1], B.ev[2]);
+    cudaEventElapsedTime(&t3, B.ev[2], B.ev[3]);
     ms_setup += t1; ms_pcg += t2; ms_gram += t3;
-    for (int i = 0; i < nmp; i++) {
-      if (hf[i] & 2) S.rank_deficient++;
-      if (hf[i] & 1) {
-        const MacroHost& m = pl.all[mine[bstart + i]];
+    for (int i = 0; i < B.nmp; i++) {
+      const MacroHost& m = pl.all[B.mps[i]];
+      if (B.h_flags[i] & 2) S.rank_deficient++;
+      if (B.h_flags[i] & 1) {
         char buf[200];
         snprintf(buf, sizeof buf, "continuum absent from K_p of macropoint (%d,%d,%d)", m.k[0], m.k[1], m.k[2]);
         return fail(c, MCH_ERANK, buf);
       }
-      int64_t ln, fnn, lc;
-      sizes(pl.all[mine[bstart + i]], ln, fnn, lc);
+      const int64_t ln = B.ln[i], lc = B.lc[i];
       int mx = 0;
       bool bad = false;
       int badr = 0;
       for (int r = 0; r < nr; r++) {
-        const int it = hit[i * nr + r];
-        if (hdg[(i * nr + r) * 4 + 3] != 0.0 || it >= c->p.max_iter) { bad = true; badr = r; }
+        const int it = B.h_iters[i * nr + r];
+        if (B.h_diag[(i * nr + r) * 4 + 3] != 0.0 || it >= c->p.max_iter) { bad = true; badr = r; }
         S.iters_total += it;
         mx = std::max(mx, it);
-        S.relres_max = std::max(S.relres_max, hrr[i * nr + r]);
+        S.relres_max = std::max(S.relres_max, B.h_relres[i * nr + r]);
         S.pcg_bytes += 8.0 * 6.0 * (double)ln * it;
       }
       S.iters_max = std::max<int64_t>(S.iters_max, mx);
+      S.unknowns_level += ln;
+      S.cells_level += lc;
       const double Dn = (level == 1) ? 1.0 : ((D == 2) ? 5.0 : 19.0);
       S.pcg_bytes += 8.0 * Dn * (double)lc * mx;
       if (bad) {
-        const MacroHost& m = pl.all[mine[bstart + i]];
-        const double* dg = &hdg[(i * nr + badr) * 4];
+        const double* dg = &B.h_diag[(i * nr + badr) * 4];
         char buf[320];
         snprintf(buf, sizeof buf,
                  "PCG did not converge at level %d macropoint (%d,%d,%d) rhs %d: %s after %d iterations, "
                  "relres %.3e (rz %.3e, ref %.3e, floor %.3e)",
                  level, m.k[0], m.k[1], m.k[2], badr, dg[3] != 0.0 ? "breakdown" : "iteration cap",
-                 hit[i * nr + badr], hrr[i * nr + badr], dg[0], dg[1], dg[2]);
+                 B.h_iters[i * nr + badr], B.h_relres[i * nr + badr], dg[0], dg[1], dg[2]);
         return fail(c, MCH_ENOCONV, buf);
       }
     }
-    S.macropoints += nmp;
-    S.problems += (int64_t)nmp * nr;
-    bstart = bend;
+    S.macropoints += B.nmp;
+    S.problems += (int64_t)B.nmp * nr;
   }
-  if (htime)
-    fprintf(stderr, "[mch host] level %d: total %.3f ms, desc/upload %.3f, launches %.3f, sync %.3f\n", level,
-            std::chrono::duration<double, std::milli>(now() - th0).count(), h_plan, h_launch, h_sync);
-  (void)h_post;
-  cudaEventRecord(c->ev[5], st);
-  CKC(c, cudaEventSynchronize(c->ev[5]));
   float tt = 0;
   cudaEventElapsedTime(&tt, c->ev[0], c->ev[5]);
   S.ms_total = tt;
@@ -518,6 +564,26 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   S.ms_pcg = ms_pcg;
   S.ms_gram = ms_gram;
   c->solved = level;
+  return MCH_OK;
+}
+
+extern "C" int mch_set_medium(mch_ctx* c, const double* kappa, const uint8_t* ids, int on_dev) {
+  if (!c) return MCH_EINVAL;
+  if (!kappa || !ids) return fail(c, MCH_EINVAL, "NULL argument");
+  const int64_t n = c->p.n;
+  const int64_t cells = (c->D == 2) ? n * n : n * n * n;
+  const cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CKC(c, cudaMemcpyAsync(c->kappa, kappa, cells * sizeof(double), kind, c->st));
+  CKC(c, cudaMemcpyAsync(c->ids, ids, cells, kind, c->st));
+  // validation on the device (no host pass over the inputs), one pinned flag read back
+  if (!c->h_bad) CKC(c, cudaMallocHost(&c->h_bad, sizeof(int)));
+  if (!c->d_bad) CKC(c, cudaMalloc(&c->d_bad, sizeof(int)));
+  CKC(c, cudaMemsetAsync(c->d_bad, 0, sizeof(int), c->st));
+  CKC(c, launch_validate(c->kappa, c->ids, cells, c->N, c->d_bad, c->st));
+  CKC(c, cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CKC(c, cudaStreamSynchronize(c->st));
+  c->solved = 0;
+  if (*c->h_bad) return fail(c, MCH_EINVAL, "kappa must be positive and finite; ids < num_continua");
   return MCH_OK;
 }
 
@@ -612,7 +678,10 @@ extern "C" void mch_destroy(mch_ctx* c) {
   cudaFree(c->ids);
   cudaFree(c->pool);
   cudaFree(c->G);
-  DevBuf* bufs[] = {&c->descs, &c->segs, &c->nseg, &c->STC, &c->MLR, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
+  c->lplans.clear();
+  if (c->h_bad) cudaFreeHost(c->h_bad);
+  if (c->d_bad) cudaFree(c->d_bad);
+  DevBuf* bufs[] = {&c->STC, &c->MLR, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
                     &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres, &c->diag};
   for (DevBuf* b : bufs) b->release();
   if (c->events)

@@ -83,6 +83,9 @@ class ShardedHomogenizer:
     def reset(self):
         self.h.reset()
 
+    def set_medium(self, kappa, ids):
+        self.h.set_medium(kappa, ids)
+
     def solve_all(self):
         for lev in range(1, self.h.L + 1):
             self.h.solve_level(lev)

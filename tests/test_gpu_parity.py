@@ -150,3 +150,23 @@ def test_pcg_variants_agree(mode, monkeypatch):
         G1 = h.effective_coeffs()
     for Gp, Gq in ((G0, Go), (G1, Go), (G0, G1)):
         assert max(g_err(Gp[i], Gq[i]) for i in range(len(Go))) < G_TOL
+
+
+def test_set_medium_reuses_context():
+    """mch_set_medium: a context re-used for a second medium gives the same coefficients as a
+    fresh context on that medium (bitwise: same kernels, same plan), and matches the oracle"""
+    H = _gpu()
+    d, n, M, L, N = 2, 64, 8, 3, 2
+    ka, ia = _admissible(d, n, M, N, 21)
+    kb, ib = _admissible(d, n, M, N, 40)
+    with H(d, n, N, M, L, 2, kb, ib) as h:
+        h.solve_all()
+        Gfresh = h.effective_coeffs()
+    with H(d, n, N, M, L, 2, ka, ia) as h:
+        h.solve_all()
+        h.set_medium(kb, ib)
+        h.solve_all()
+        Greuse = h.effective_coeffs()
+    assert np.array_equal(Gfresh, Greuse)
+    Go = Oracle(d, n, M, L, 2, N, kb, ib).effective_coeffs()
+    assert max(g_err(Greuse[i], Go[i]) for i in range(len(Go))) < G_TOL
