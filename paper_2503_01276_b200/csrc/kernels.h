@@ -18,8 +18,8 @@ cudaError_t launch_validate(const double* kappa, const uint8_t* ids, int64_t cnt
 #define PCG2D_V_GN49 1
 #define PCG2D_V_GN25 2
 #define PCG2D_V_GN97 3
-void pcg2d_variant(int variant, int* rpt, int* nxm, int* maxw, int* l1op);
-size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw);
+void pcg2d_variant(int variant, int* rpt, int* nxm, int* maxw, int* l1op, int* sstc, int* smlr);
+size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw, bool sstc, bool smlr);
 cudaError_t launch_node_ops2d(const LevelArgs& A, int max_nodes, cudaStream_t st);
 cudaError_t launch_pcg2d(const LevelArgs& A, int variant, int threads, cudaStream_t st);
 void pcg2d_phase_dump(const char* tag);  // PCG2D_TIMING builds: per-phase cycle counters

@@ -354,9 +354,9 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       cands.push_back(PCG2D_V_GN49);
       cands.push_back(PCG2D_V_GN97);
       for (int v : cands) {
-        int rpt, nxm, maxw, l1op;
-        pcg2d_variant(v, &rpt, &nxm, &maxw, &l1op);
-        if (maxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw) > 232448) continue;
+        int rpt, nxm, maxw, l1op, sstc, smlr;
+        pcg2d_variant(v, &rpt, &nxm, &maxw, &l1op, &sstc, &smlr);
+        if (maxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0) > 232448) continue;
         std::vector<int> nsegs(nmp);
         std::vector<std::vector<short4>> per(nmp);
         int maxseg = 0, maxwp = 0;

@@ -100,7 +100,7 @@ __device__ __forceinline__ int pair_state(int a, int b) {
 }
 template <int N> struct PairStates { static constexpr int value = (N + 1) * (N + 2) / 2; };
 
-template <int N, bool L1OP, int KX>
+template <int N, bool L1OP, int KX, bool SMLR = false, int PLANE = 0>
 struct NodeW {
   static constexpr int LW = (N == 1) ? 1 : ((N + 1) & ~1);  // padded table row (16-byte loads)
   // level 1: per-node side states (low nibble: left pair of elements, high: right pair) and
@@ -115,6 +115,8 @@ struct NodeW {
   int xc;
   const uint8_t* cp;  // running row pointers
   const double* mp;
+  const double* ms;   // SMLR: side sums staged in shared memory, [2N][PLANE] with pitch KX-1
+  const double* msp;
   int y0;
 
   // c * hq for c in {0, 1}, branch-free on the bit pattern
@@ -126,6 +128,7 @@ struct NodeW {
     y0 = y;
     if (L1OP) cp = codes + y * (KX - 1) + xc;
     else mp = base + y * nx + xc;
+    if (SMLR) msp = ms + y * (KX - 1) + xc;
   }
   // node (x, y0 + i) for consecutive i; low: also the weights of the lower elements alone
   __device__ __forceinline__ void row(bool low, double (&mL)[N], double (&mR)[N], double (&lL)[N],
@@ -164,12 +167,18 @@ struct NodeW {
     } else {
 #pragma unroll
       for (int j = 0; j < N; j++) {
-        mL[j] = __ldg(mp + (int64_t)j * nn);
-        mR[j] = __ldg(mp + (int64_t)(N + j) * nn);
+        if (SMLR) {
+          mL[j] = msp[j * PLANE];
+          mR[j] = msp[(N + j) * PLANE];
+        } else {
+          mL[j] = __ldg(mp + (int64_t)j * nn);
+          mR[j] = __ldg(mp + (int64_t)(N + j) * nn);
+        }
         lL[j] = low ? __ldg(mp + (int64_t)(2 * N + j) * nn) : 0.0;
         lR[j] = low ? __ldg(mp + (int64_t)(3 * N + j) * nn) : 0.0;
       }
       mp += nx;
+      if (SMLR) msp += KX - 1;
     }
   }
 };
@@ -248,7 +257,7 @@ void pcg2d_phase_dump(const char* tag) {
 void pcg2d_phase_dump(const char*) {}
 #endif
 
-template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB>
+template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB, bool SSTC, bool SMLR>
 __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   constexpr int RP4 = (RPT + 3) & ~3;  // rows rounded to the 4-row TMEM groups
   constexpr int NBC = 4 * RP4;         // TMEM columns per thread: q block, then x block
@@ -274,11 +283,14 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
 
   extern __shared__ __align__(16) double smem[];
   constexpr int LW = NodeW<N, L1OP, KX>::LW;
+  constexpr int PLANE = DX * NXM;
   constexpr int NCM = 9 * N;              // constraint rows of a 3x3-subcell window (host: nc <= NCM)
   constexpr int O_Y = (NCM * NCM + 1) & ~1, O_SL = O_Y + 64, O_B = O_SL + 3 * 32;
   constexpr int O_P = O_B + MAXW * 32;
   constexpr int O_K = O_P + PX * (NXM + 2), O_LUT = (O_K + (L1OP ? KX * (NXM + 1) : 0) + 1) & ~1;
-  constexpr int O_D = O_LUT + (L1OP ? 16 * LW : 0);  // end of the double region
+  constexpr int O_S9 = O_LUT + (L1OP ? 16 * LW : 0);  // levels >= 2, SSTC: 9 x DX*NXM stencil
+  constexpr int O_ML = O_S9 + (SSTC ? 9 * PLANE : 0);    // levels >= 2, SMLR: 2N x DX*NXM side sums
+  constexpr int O_D = O_ML + (SMLR ? 2 * N * PLANE : 0);  // end of the double region
   double* Si = smem;                      // [NCM*NCM] S^-1 (nc*nc used)
   double* Ysh = smem + O_Y;               // [32] yhat, [32] beta (written by warp 0)
   double* slots = smem + O_SL;            // [3][32] scalar partial sums (rz, pq, rr)
@@ -347,7 +359,17 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   // per-thread subcell columns of the left / right elements
   const int sxL = (xc >= 1) ? sub_slot(A, P, 0, xc - 1) : 0;
   const int sxR = (xc < ncx) ? sub_slot(A, P, 0, xc) : 0;
-  NodeW<N, L1OP, KX> cw;
+  NodeW<N, L1OP, KX, SMLR, PLANE> cw;
+  double* ml_s = smem + O_ML;
+  if (SMLR) {  // stage the side sums [L|R][j] of the window (pitch DX), once per problem
+    const double* src = A.MLR + P.node_off * 4 * N;
+    for (int i = threadIdx.x; i < 2 * N * nn; i += blockDim.x) {
+      const int tt = i / nn, k = i - tt * nn, y = k / nx;
+      ml_s[tt * PLANE + y * DX + (k - y * nx)] = src[i];
+    }
+    __syncthreads();
+  }
+  cw.ms = ml_s;
   cw.ids = ids_s;
   cw.codes = codes_s;
   cw.lut = lut_s;
@@ -358,6 +380,14 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   cw.nx = nx;
   cw.xc = xc;
   const double* S9 = A.STC + P.node_off * 9;
+  double* s9_s = smem + O_S9;
+  if (SSTC) {  // stage the window's stencil rows in shared memory (pitch DX), once per problem
+    for (int i = threadIdx.x; i < 9 * nn; i += blockDim.x) {
+      const int cc = i / nn, k = i - cc * nn, y = k / nx;
+      s9_s[cc * DX * NXM + y * DX + (k - y * nx)] = S9[i];
+    }
+    __syncthreads();
+  }
 
   double r[RPT];
 #pragma unroll
@@ -408,6 +438,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
       kR0 = kp[1];
     }
     const double* s9 = S9 + yb * nx + xc;
+    const double* s9s = s9_s + yb * DX + xc;
 #pragma unroll
     for (int i = 0; i < RPT; i++) {
       if (i >= nrow) break;
@@ -422,6 +453,11 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
         Ap = acc * (1.0 / 6.0);
         kL0 = kL1;
         kR0 = kR1;
+      } else if (SSTC) {
+        constexpr int CS = DX * NXM;
+        const double* s = s9s + i * DX;
+        Ap = s[0] * a0 + s[CS] * b0 + s[2 * CS] * c0 + s[3 * CS] * a1 + s[4 * CS] * b1 + s[5 * CS] * c1 +
+             s[6 * CS] * a2 + s[7 * CS] * b2 + s[8 * CS] * c2;
       } else {
         const double* s = s9 + i * nx;
         Ap = __ldg(s) * a0 + __ldg(s + nn) * b0 + __ldg(s + 2 * nn) * c0 + __ldg(s + 3 * nn) * a1 +
@@ -810,10 +846,12 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
-size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw) {
+size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw, bool sstc, bool smlr) {
   const int PX = nxm + 2, KX = nxm + 1, DX = nxm, LW = (N == 1) ? 1 : ((N + 1) & ~1);
   size_t d = ((81 * N * N + 1) & ~1) + 64 + 3 * 32 + (size_t)maxw * 32 + (size_t)PX * (nxm + 2);
   d += 1;  // O_LUT rounded up to 16 bytes
+  if (sstc) d += 9 * (size_t)DX * nxm;
+  if (smlr) d += 2 * (size_t)N * DX * nxm;
   if (l1op) d += (size_t)KX * (nxm + 1) + 16 * LW;
   size_t b = d * sizeof(double) + (size_t)DX * nxm * sizeof(float);
   if (l1op) b += (size_t)KX * (nxm + 1) + (size_t)DX * nxm;
@@ -831,10 +869,10 @@ cudaError_t launch_node_ops2d(const LevelArgs& A, int max_nodes, cudaStream_t st
   return cudaGetLastError();
 }
 
-template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB>
+template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB, bool SSTC, bool SMLR>
 static cudaError_t launch_one(const LevelArgs& A, int threads, cudaStream_t st) {
-  auto k = k_pcg2d<RPT, N, L1OP, NXM, MAXW, MINB>;
-  const size_t smem = pcg2d_smem_t(N, L1OP, NXM, MAXW);
+  auto k = k_pcg2d<RPT, N, L1OP, NXM, MAXW, MINB, SSTC, SMLR>;
+  const size_t smem = pcg2d_smem_t(N, L1OP, NXM, MAXW, SSTC, SMLR);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<(unsigned)A.nprob_mp * A.n_rhs, threads, smem, st>>>(A);
@@ -856,6 +894,18 @@ static cudaError_t launch_one(const LevelArgs& A, int threads, cudaStream_t st) 
 #ifndef GN49_MINB
 #define GN49_MINB 1
 #endif
+#ifndef GN49_SSTC
+#define GN49_SSTC false
+#endif
+#ifndef GN49_SMLR
+#define GN49_SMLR true
+#endif
+#ifndef GN25_SMLR
+#define GN25_SMLR true
+#endif
+#ifndef GN25_SSTC
+#define GN25_SSTC false
+#endif
 #ifndef GN25_MINB
 #define GN25_MINB 6
 #endif
@@ -863,10 +913,11 @@ static cudaError_t launch_one(const LevelArgs& A, int threads, cudaStream_t st) 
 template <int N>
 static cudaError_t launch_n(const LevelArgs& A, int variant, int threads, cudaStream_t st) {
   switch (variant) {
-    case PCG2D_V_L1: return launch_one<L1_RPT, N, true, 97, L1_MAXW, 1>(A, threads, st);
-    case PCG2D_V_GN49: return launch_one<GN49_RPT, N, false, 49, GN49_MAXW, GN49_MINB>(A, threads, st);
-    case PCG2D_V_GN25: return launch_one<9, N, false, 25, 4, GN25_MINB>(A, threads, st);
-    case PCG2D_V_GN97: return launch_one<17, N, false, 97, 24, 1>(A, threads, st);
+    case PCG2D_V_L1: return launch_one<L1_RPT, N, true, 97, L1_MAXW, 1, false, false>(A, threads, st);
+    case PCG2D_V_GN49:
+      return launch_one<GN49_RPT, N, false, 49, GN49_MAXW, GN49_MINB, GN49_SSTC, GN49_SMLR>(A, threads, st);
+    case PCG2D_V_GN25: return launch_one<9, N, false, 25, 4, GN25_MINB, GN25_SSTC, GN25_SMLR>(A, threads, st);
+    case PCG2D_V_GN97: return launch_one<17, N, false, 97, 24, 1, false, false>(A, threads, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -881,7 +932,9 @@ cudaError_t launch_pcg2d(const LevelArgs& A, int variant, int threads, cudaStrea
 }
 
 // variant limits: rows per thread, widest window (nodes), warps per CTA
-void pcg2d_variant(int variant, int* rpt, int* nxm, int* maxw, int* l1op) {
+void pcg2d_variant(int variant, int* rpt, int* nxm, int* maxw, int* l1op, int* sstc, int* smlr) {
+  *sstc = (variant == PCG2D_V_GN49) ? (int)GN49_SSTC : ((variant == PCG2D_V_GN25) ? (int)GN25_SSTC : 0);
+  *smlr = (variant == PCG2D_V_GN49) ? (int)GN49_SMLR : ((variant == PCG2D_V_GN25) ? (int)GN25_SMLR : 0);
   static const int T[4][4] = {{L1_RPT, 97, L1_MAXW, 1}, {GN49_RPT, 49, GN49_MAXW, 0}, {9, 25, 4, 0}, {17, 97, 24, 0}};
   *rpt = T[variant][0];
   *nxm = T[variant][1];
