@@ -133,6 +133,12 @@ int mch_local_solution(mch_ctx* ctx, int64_t macropoint, int rhs, double* out, s
 
 int mch_get_level_stats(const mch_ctx* ctx, int level, mch_level_stats* out);
 
+/* PCG iteration count of every problem of the last solve of `level` on this context: out[i*n_rhs + r]
+ * for the i-th macropoint this context solved (the order of mch_level_macropoints restricted to
+ * this rank) and right-hand side r.  cap: capacity of out in elements.  Diagnostics (load
+ * balance, preconditioner studies).  Errors: MCH_EINVAL, MCH_EORDER (level not solved). */
+int mch_level_iterations(const mch_ctx* ctx, int level, int32_t* out, size_t cap);
+
 /* Parent-pool layout for the multi-GPU exchange (one process per GPU): device
  * pointer of the pool of fine parent solutions, and for macropoint index m its
  * element offset and length (-1, 0 if not stored). */

@@ -17,7 +17,7 @@ ERRORS = {-1: "MCH_EINVAL", -2: "MCH_EDIVISIBILITY", -3: "MCH_ERANK", -4: "MCH_E
 
 # every symbol include/mch.h declares
 SYMBOLS = ["mch_create", "mch_set_medium", "mch_reset", "mch_solve_level", "mch_effective_coeffs", "mch_num_macropoints", "mch_level_macropoints",
-           "mch_local_solution", "mch_get_level_stats", "mch_pool_info", "mch_pool_slot",
+           "mch_local_solution", "mch_get_level_stats", "mch_level_iterations", "mch_pool_info", "mch_pool_slot",
            "mch_coeffs_device", "mch_last_error", "mch_destroy"]
 
 
@@ -61,6 +61,7 @@ def _load():
     lib.mch_level_macropoints.argtypes = [vp, i32, P(i64), ctypes.c_size_t]
     lib.mch_local_solution.argtypes = [vp, i64, i32, vp, ctypes.c_size_t, P(i64)]
     lib.mch_get_level_stats.argtypes = [vp, i32, P(MchLevelStats)]
+    lib.mch_level_iterations.argtypes = [vp, i32, P(ctypes.c_int32), ctypes.c_size_t]
     lib.mch_pool_info.argtypes = [vp, P(vp), P(i64)]
     lib.mch_pool_slot.argtypes = [vp, i64, P(i64), P(i64)]
     lib.mch_coeffs_device.argtypes = [vp, P(vp)]

@@ -161,6 +161,13 @@ class Homogenizer:
         check(lib.mch_get_level_stats(self.ctx, level, ctypes.byref(s)), self.ctx)
         return {f: getattr(s, f) for f, _ in MchLevelStats._fields_}
 
+    def level_iterations(self, level):
+        """[macropoints solved here, n_rhs] PCG iteration counts of the last solve of `level`"""
+        n = self.level_stats(level)["problems"]
+        buf = (ctypes.c_int32 * max(n, 1))()
+        check(lib.mch_level_iterations(self.ctx, level, buf, n), self.ctx)
+        return np.frombuffer(buf, dtype=np.int32, count=n).reshape(-1, self.n_rhs).copy()
+
     def num_macropoints_level(self, level):
         c = ctypes.c_int64()
         check(lib.mch_num_macropoints(self.ctx, level, ctypes.byref(c)), self.ctx)

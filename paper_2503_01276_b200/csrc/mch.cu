@@ -57,6 +57,7 @@ struct LevelBatch {
   int64_t node_off = 0, vec_off = 0, fine_off = 0;
   int max_ln = 0, max_fn = 0, th_l = 64, th_f = 64;
   std::vector<int64_t> mps, ln, lc;
+  std::vector<int> lexpos;  // position of each batch macropoint in the lexicographic list of this rank
   DevBuf descs, segs, nseg;
   bool on2d = false, l1op = false;
   int variant = -1, threads2 = 0, maxseg = 0, tm_cols = 32;
@@ -273,6 +274,20 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       lcells *= ncf / s;
     }
   };
+  // solve order: largest (unclipped) windows first.  Their problems are the longest (more work per
+  // iteration and more iterations), so starting them first shortens the tail of the launch
+  // (longest-processing-time-first list scheduling over the SMs).  Stable: lexicographic within
+  // a window size.  mch_level_iterations reports in the lexicographic order.
+  std::vector<int64_t> lexi = mine;
+  {
+    std::vector<int64_t> key(pl.all.size(), 0);
+    for (int64_t m : mine) {
+      int64_t ln, fnn, lc;
+      sizes(pl.all[m], ln, fnn, lc);
+      key[m] = ln;
+    }
+    std::stable_sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) { return key[a] > key[b]; });
+  }
   size_t freeb = 0, totb = 0;
   cudaMemGetInfo(&freeb, &totb);
   const double budget = std::min<double>(48e9, 0.5 * (double)freeb);
@@ -300,6 +315,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       int64_t ln, fnn, lc;
       sizes(m, ln, fnn, lc);
       B->mps.push_back(mine[bstart + i]);
+      B->lexpos.push_back((int)(std::lower_bound(lexi.begin(), lexi.end(), mine[bstart + i]) - lexi.begin()));
       B->ln.push_back(ln);
       B->lc.push_back(lc);
       for (int d = 0; d < 3; d++) {
@@ -640,6 +656,18 @@ extern "C" int mch_local_solution(mch_ctx* c, int64_t mp, int rhs, double* out, 
 extern "C" int mch_get_level_stats(const mch_ctx* c, int level, mch_level_stats* out) {
   if (!c || !out || level < 1 || level > c->p.levels) return MCH_EINVAL;
   *out = c->stats[level];
+  return MCH_OK;
+}
+
+extern "C" int mch_level_iterations(const mch_ctx* c, int level, int32_t* out, size_t cap) {
+  if (!c || !out || level < 1 || level > c->p.levels) return MCH_EINVAL;
+  if (level > c->solved || (int)c->lplans.size() <= level) return MCH_EORDER;
+  size_t total = 0;
+  for (const auto& B : c->lplans[level]) total += (size_t)B->nmp * c->n_rhs;
+  if (total > cap) return MCH_EINVAL;
+  for (const auto& B : c->lplans[level])
+    for (int i = 0; i < B->nmp; i++)
+      memcpy(out + (size_t)B->lexpos[i] * c->n_rhs, B->h_iters + (size_t)i * c->n_rhs, c->n_rhs * sizeof(int32_t));
   return MCH_OK;
 }
 

@@ -907,7 +907,7 @@ static cudaError_t launch_one(const LevelArgs& A, int threads, cudaStream_t st) 
 #define GN25_SSTC false
 #endif
 #ifndef GN25_MINB
-#define GN25_MINB 6
+#define GN25_MINB 4
 #endif
 
 template <int N>
