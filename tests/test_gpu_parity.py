@@ -108,9 +108,14 @@ def test_config1_full():
 @pytest.mark.parametrize("cid,points", [
     (2, [(5, 5), (1, 0), (31, 32), (6, 4), (2, 3), (16, 17)]),
     (3, [(5, 5), (63, 1), (0, 1), (34, 36), (64, 64)]),
+    # 3D configs: points along the x-axis edge, whose (clipped) windows and ancestors keep the
+    # oracle's sparse LU small; (1,0,0) of config 5 is a level-4 child of the chain
+    # (0,0,0)/(8,0,0) [L1] -> (4,0,0) [L2] -> (2,0,0) [L3]
+    (4, [(0, 0, 0), (1, 0, 0)]),
+    (5, [(1, 0, 0), (4, 0, 0)]),
 ])
 def test_config_sampled(cid, points):
-    """BASELINE configs 2/3 at full size in the bench's launch configuration: the GPU solves every
+    """BASELINE configs 2-5 at full size in the bench's launch configuration: the GPU solves every
     macropoint; the oracle solves the sampled points (plus the ancestors they need)."""
     H = _gpu()
     cfg = CONFIGS[cid]
