@@ -219,7 +219,7 @@ def main():
     all_b = sum(s["pcg_bytes"] for st_ in levels for s in st_) / len(levels)
     all_ms = sum(s["ms_pcg"] for st_ in levels for s in st_) / len(levels)
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "pcg_dram_per_launch_r01.json")
+    prof = os.path.join(ROOT, "profiles", "pcg_dram_per_launch_r01.json")  # ncu, same launch
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof)).get(cfg.name, {}).get("dram_bytes_pcg_L1_launch")
@@ -271,13 +271,14 @@ def main():
                    "l2": "flushed between timed steps (512 MB write)",
                    "macropoint_solves_per_s": (cfg.M + 1) ** cfg.d / (ms_step * 1e-3),
                    "per_level": per_level},
-        "roofline": {"kernel": "k_pcg level-1 launch (projected PCG)", "bound": "hbm",
+        "roofline": {"kernel": "k_pcg2d level-1 launch (on-chip projected PCG)", "bound": "hbm",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "algorithmic_bytes_per_launch": l1_b, "launch_ms": l1_ms,
                      "all_levels_pcg_GBps": all_b / (all_ms * 1e-3) / 1e9,
                      "peak_source": pk_src,
-                     "algorithmic_bytes": "8*(6*nodes*iters per problem + D_n*cells*max_iters per macropoint), D_n = 1 (L1) / 5 (2D) / 19 (3D)"},
+                     "algorithmic_bytes": "8*(6*nodes*iters per problem + D_n*cells*max_iters per macropoint), D_n = 1 (L1) / 5 (2D) / 19 (3D)",
+                     "note": "SURVEY 8(d) streaming bytes; the kernel keeps its state on chip (DRAM traffic = 'traffic'), it is issue/latency bound - DESIGN.md 6"},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": kap.nbytes + ids.nbytes,
                 "d2h_bytes_per_step": Gh.numel() * 8},
