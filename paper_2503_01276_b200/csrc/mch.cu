@@ -506,8 +506,25 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       S.launches += 1;
     }
     cudaEventRecord(B.ev[1], st);
+    double* dbgp = nullptr;
+    if (getenv("MCH_PCG_DEBUG") && B.on2d) {  // dev: per-iteration scalars of one problem to stderr
+      A.dbg_prob = atoi(getenv("MCH_PCG_DEBUG"));
+      A.dbg_cap = 400;
+      cudaMalloc(&dbgp, 8 * sizeof(double) * A.dbg_cap);
+      cudaMemset(dbgp, 0, 8 * sizeof(double) * A.dbg_cap);
+      A.dbg = dbgp;
+    }
     if (B.on2d) CKC(c, launch_pcg2d(A, B.variant, B.threads2, st));
     else CKC(c, launch_pcg(A, B.th_l, st));
+    if (dbgp) {
+      std::vector<double> h(8 * A.dbg_cap);
+      cudaMemcpy(h.data(), dbgp, h.size() * sizeof(double), cudaMemcpyDeviceToHost);
+      for (int i = 0; i < A.dbg_cap && h[8 * i] != 0.0; i++)
+        fprintf(stderr, "[dbg L%d prob %d] it %d rz %.17e pq %.17e alpha %.17e beta %.17e\n", level, A.dbg_prob, i,
+                h[8 * i], h[8 * i + 1], h[8 * i + 2], h[8 * i + 3]);
+      cudaFree(dbgp);
+      A.dbg = nullptr;
+    }
     cudaEventRecord(B.ev[2], st);
     if (getenv("MCH_PCG_TIMING") && B.on2d) {
       char tag[64];

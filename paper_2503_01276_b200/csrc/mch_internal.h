@@ -66,6 +66,8 @@ struct LevelArgs {
   int maxseg;
   int tm_cols;             // TMEM columns allocated per CTA
   double* STC;             // levels >= 2: per window node 9 stencil coefficients, SoA [9][nodes]
+  double* dbg;             // debug: per-iteration scalars of problem dbg_prob (NULL: off)
+  int dbg_prob, dbg_cap;
   double* MLR;             // levels >= 2: per node constraint side sums, SoA [4N][nodes]:
                            //  [L|R][j] over lower+upper elements, then [L|R][j] lower elements only
 };

@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   for (int i = threadIdx.x; i < PX * (ny + 2); i += blockDim.x) p_s[i] = 0.0;
   for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Si[i] = A.Sinv[(int64_t)mp * nc * nc + i];
   for (int i = threadIdx.x; i < MAXW * 32; i += blockDim.x) bins[i] = 0.0;
-  if (threadIdx.x < 96) slots[threadIdx.x] = 0.0;
+  for (int i = threadIdx.x; i < 3 * 32; i += blockDim.x) slots[i] = 0.0;  // incl. slots of absent warps
   {
     const double* dg = A.dinv + P.node_off;
     for (int k = threadIdx.x; k < nn; k += blockDim.x) dinv_s[(k / nx) * DX + k % nx] = (float)dg[k];
@@ -791,6 +791,10 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
     __syncthreads();  // B4
     yh = Ysh[lane];
     beta = Ysh[32];
+    if (A.dbg && prob == A.dbg_prob && threadIdx.x == 0 && it < A.dbg_cap) {  // dev: MCH_PCG_DEBUG
+      double* o = A.dbg + 8 * it;
+      o[0] = rz; o[1] = pq; o[2] = alpha; o[3] = beta;
+    }
     TMARK(6);
   }
 #ifdef PCG2D_TIMING
