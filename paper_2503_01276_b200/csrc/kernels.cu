@@ -381,86 +381,110 @@ __global__ void k_proj_setup(LevelArgs A) {
     }
     return;
   }
-  // Reading R20: dependent level-n constraint rows.  Pseudo-inverse of S~ by cyclic Jacobi
-  // eigen-decomposition, eigenvalues below 1e-11 lambda_max dropped.
+  // Reading R20: dependent level-n constraint rows.  The pseudo-inverse of S~ is formed by
+  // k_pinv (parallel Jacobi, one warp per window): hand over S~ and the row scales.
   if (threadIdx.x == 0) atomicOr(&A.flags[mp], 2);
-  for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
-    S[idx] = V[idx];
-    V[idx] = (idx / nc == idx % nc) ? 1.0 : 0.0;
+  double* so = A.Sinv + (int64_t)mp * nc * nc;  // S~ in place of S^-1 until k_pinv replaces it
+  for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) so[idx] = V[idx];
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) A.pinv_ds[(int64_t)mp * nc + i] = ds[i];
+}
+
+// ---------------------------------------------------------------------------------------
+// Reading R20: S^+ = Lambda S~^+ Lambda with S~ = V diag(lambda) V^T, eigenvalues
+// below 1e-11 lambda_max dropped.  One warp per flagged window: parallel cyclic Jacobi with the
+// round-robin ordering (each round rotates nc/2 disjoint pairs at once: lane k owns pair k),
+// sweeps until the off-diagonal mass is below 1e-34 of the diagonal's (at most 40 sweeps).
+__global__ void k_pinv(LevelArgs A) {
+  const int mp = blockIdx.x;
+  if (!(A.flags[mp] & 2)) return;
+  const int nc = A.ncon, lane = threadIdx.x;
+  extern __shared__ double sm[];
+  double* S = sm;            // nc*nc (padded to even m)
+  const int m = (nc + 1) & ~1;
+  double* V = S + m * m;     // m*m
+  int* pos = reinterpret_cast<int*>(V + m * m);  // m
+  double* Sg = A.Sinv + (int64_t)mp * nc * nc;
+  for (int idx = lane; idx < m * m; idx += 32) {
+    const int i = idx / m, j = idx % m;
+    S[idx] = (i < nc && j < nc) ? Sg[i * nc + j] : 0.0;  // padded row/column: decoupled zero
+    V[idx] = (i == j) ? 1.0 : 0.0;
   }
-  __syncthreads();
-  __shared__ double rot[3];
-  __shared__ int skip;
+  for (int i = lane; i < m; i += 32) pos[i] = i;
+  __syncwarp();
   for (int sweep = 0; sweep < 40; sweep++) {
-    double v[2] = {0.0, 0.0};
-    for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
-      const int i = idx / nc, j = idx % nc;
+    double off = 0.0, dia = 0.0;
+    for (int idx = lane; idx < m * m; idx += 32) {
+      const int i = idx / m, j = idx % m;
       const double a = S[idx];
-      if (i < j) v[0] += a * a;
-      else if (i == j) v[1] += a * a;
+      if (i < j) off += a * a;
+      else if (i == j) dia += a * a;
     }
-    block_sum<2>(v, scratch, tot);
-    if (tot[0] <= 1e-34 * tot[1]) break;
-    for (int p = 0; p < nc - 1; p++) {
-      for (int q = p + 1; q < nc; q++) {
-        if (threadIdx.x == 0) {
-          const double apq = S[p * nc + q];
-          if (fabs(apq) < 1e-300) {
-            skip = 1;
-          } else {
-            skip = 0;
-            const double th = (S[q * nc + q] - S[p * nc + p]) / (2.0 * apq);
-            const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
-            const double cc = 1.0 / sqrt(t * t + 1.0);
-            rot[0] = cc;
-            rot[1] = t * cc;
-            rot[2] = t;
-          }
+    for (int o = 16; o > 0; o >>= 1) {
+      off += __shfl_xor_sync(FULLMASK, off, o);
+      dia += __shfl_xor_sync(FULLMASK, dia, o);
+    }
+    if (off <= 1e-34 * dia) break;
+    for (int round = 0; round < m - 1; round++) {
+      // pairs of this round: (pos[k], pos[m-1-k]), k < m/2
+      int p = 0, q = 0;
+      double c = 1.0, sn = 0.0, t = 0.0, apq = 0.0;
+      bool rot = false;
+      if (lane < m / 2) {
+        p = pos[lane];
+        q = pos[m - 1 - lane];
+        if (p > q) { const int tt = p; p = q; q = tt; }
+        apq = S[p * m + q];
+        if (fabs(apq) >= 1e-300) {
+          const double th = (S[q * m + q] - S[p * m + p]) / (2.0 * apq);
+          t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+          c = 1.0 / sqrt(t * t + 1.0);
+          sn = t * c;
+          rot = true;
         }
-        __syncthreads();
-        if (!skip) {
-          const double cc = rot[0], ss = rot[1], t = rot[2];
-          const double apq = S[p * nc + q];
-          for (int k = threadIdx.x; k < nc; k += blockDim.x) {
-            if (k != p && k != q) {
-              const double skp = S[k * nc + p], skq = S[k * nc + q];
-              const double nkp = cc * skp - ss * skq, nkq = ss * skp + cc * skq;
-              S[k * nc + p] = nkp;
-              S[p * nc + k] = nkp;
-              S[k * nc + q] = nkq;
-              S[q * nc + k] = nkq;
-            }
-            const double vkp = V[k * nc + p], vkq = V[k * nc + q];
-            V[k * nc + p] = cc * vkp - ss * vkq;
-            V[k * nc + q] = ss * vkp + cc * vkq;
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            S[p * nc + p] -= t * apq;
-            S[q * nc + q] += t * apq;
-            S[p * nc + q] = 0.0;
-            S[q * nc + p] = 0.0;
-          }
-        }
-        __syncthreads();
       }
+      __syncwarp();
+      // rows p, q (all columns), then columns p, q (all rows): S <- J^T S J, V <- V J
+      if (rot)
+        for (int k = 0; k < m; k++) {
+          const double skp = S[p * m + k], skq = S[q * m + k];
+          S[p * m + k] = c * skp - sn * skq;
+          S[q * m + k] = sn * skp + c * skq;
+        }
+      __syncwarp();
+      if (rot)
+        for (int k = 0; k < m; k++) {
+          const double skp = S[k * m + p], skq = S[k * m + q];
+          S[k * m + p] = c * skp - sn * skq;
+          S[k * m + q] = sn * skp + c * skq;
+          const double vkp = V[k * m + p], vkq = V[k * m + q];
+          V[k * m + p] = c * vkp - sn * vkq;
+          V[k * m + q] = sn * vkp + c * vkq;
+        }
+      __syncwarp();
+      if (rot) {
+        S[p * m + q] = 0.0;
+        S[q * m + p] = 0.0;
+      }
+      // rotate positions 1..m-1 (circle method)
+      int nxt[2] = {0, 0};  // m <= 64
+      for (int i = lane, r = 0; i < m; i += 32, r++) nxt[r] = (i == 0) ? pos[0] : pos[(i == 1) ? m - 1 : i - 1];
+      __syncwarp();
+      for (int i = lane, r = 0; i < m; i += 32, r++) pos[i] = nxt[r];
+      __syncwarp();
     }
   }
-  __shared__ double lmax;
-  if (threadIdx.x == 0) {
-    double m = 0.0;
-    for (int i = 0; i < nc; i++) m = fmax(m, S[i * nc + i]);
-    lmax = m;
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+  double lmax = 0.0;
+  for (int i = lane; i < nc; i += 32) lmax = fmax(lmax, S[i * m + i]);
+  for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(FULLMASK, lmax, o));
+  const double* ds = A.pinv_ds + (int64_t)mp * nc;
+  for (int idx = lane; idx < nc * nc; idx += 32) {
     const int i = idx / nc, j = idx % nc;
     double acc = 0.0;
     for (int k = 0; k < nc; k++) {
-      const double lk = S[k * nc + k];
-      if (lk > 1e-11 * lmax) acc += V[i * nc + k] * V[j * nc + k] / lk;
+      const double lk = S[k * m + k];
+      if (lk > 1e-11 * lmax) acc += V[i * m + k] * V[j * m + k] / lk;
     }
-    out[idx] = acc * ds[i] * ds[j];
+    Sg[idx] = acc * ds[i] * ds[j];
   }
 }
 
@@ -771,6 +795,15 @@ cudaError_t launch_proj_setup(const LevelArgs& A, int threads, cudaStream_t st) 
     k_proj_setup<3><<<A.nprob_mp, threads, sm, st>>>(A);
   }
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pinv(const LevelArgs& A, cudaStream_t st) {
+  const int m = (A.ncon + 1) & ~1;
+  const size_t sm = sizeof(double) * 2 * (size_t)m * m + sizeof(int) * m;
+  cudaError_t e = cudaFuncSetAttribute(k_pinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  k_pinv<<<A.nprob_mp, 32, sm, st>>>(A);
   return cudaGetLastError();
 }
 

@@ -6,6 +6,7 @@ cudaError_t launch_level_ops(const LevelArgs& A, cudaStream_t st);
 cudaError_t launch_targets(const LevelArgs& A, cudaStream_t st);
 cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st);
 cudaError_t launch_proj_setup(const LevelArgs& A, int threads, cudaStream_t st);
+cudaError_t launch_pinv(const LevelArgs& A, cudaStream_t st);  // R20 windows flagged by proj_setup
 cudaError_t launch_pcg(const LevelArgs& A, int threads, cudaStream_t st);
 cudaError_t launch_combine(const LevelArgs& A, int threads, cudaStream_t st);
 cudaError_t launch_gram(const LevelArgs& A, int threads, cudaStream_t st);

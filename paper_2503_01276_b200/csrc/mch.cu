@@ -95,7 +95,7 @@ struct mch_ctx {
   std::vector<mch_level_stats> stats;
   std::string err;
   // grow-only scratch
-  DevBuf STC, MLR, W, Mc, g0, g, meas, cm, flags, dinv, nwt, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
+  DevBuf STC, MLR, pinv_ds, W, Mc, g0, g, meas, cm, flags, dinv, nwt, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
   cudaEvent_t ev[8];
   bool events = false;
   std::vector<std::vector<std::unique_ptr<LevelBatch>>> lplans;  // per level, built on first solve
@@ -411,6 +411,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     CKC(c, c->dinv.ensure(sizeof(double) * B->node_off));
     CKC(c, c->nwt.ensure(sizeof(double) * B->node_off * N));
     CKC(c, c->Sinv.ensure(sizeof(double) * nmp * nc * nc));
+    CKC(c, c->pinv_ds.ensure(sizeof(double) * nmp * nc));
     CKC(c, c->X.ensure(sizeof(double) * B->vec_off));
     CKC(c, c->iters.ensure(sizeof(int) * nmp * nr));
     CKC(c, c->relres.ensure(sizeof(double) * nmp * nr));
@@ -480,6 +481,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   A.g0 = c->g0.as<double>(); A.g = c->g.as<double>(); A.meas = c->meas.as<double>();
   A.cm = c->cm.as<double>(); A.flags = c->flags.as<int>();
   A.dinv = c->dinv.as<double>(); A.NWt = c->nwt.as<double>(); A.Sinv = c->Sinv.as<double>();
+  A.pinv_ds = c->pinv_ds.as<double>();
   A.X = c->X.as<double>(); A.R = c->R.as<double>(); A.P = c->P.as<double>(); A.Q = c->Q.as<double>();
   A.B = c->B.as<double>();
   A.FI = c->FI.as<double>(); A.FY = c->FY.as<double>();
@@ -501,6 +503,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     CKC(c, launch_targets(A, st));
     if (level >= 2) CKC(c, launch_transport(A, B.th_f, st));
     CKC(c, launch_proj_setup(A, B.th_l, st));
+    CKC(c, launch_pinv(A, st));
+    S.launches += 1;
     if (B.on2d && !B.l1op) {
       CKC(c, launch_node_ops2d(A, B.max_ln, st));
       S.launches += 1;
@@ -726,7 +730,7 @@ extern "C" void mch_destroy(mch_ctx* c) {
   c->lplans.clear();
   if (c->h_bad) cudaFreeHost(c->h_bad);
   if (c->d_bad) cudaFree(c->d_bad);
-  DevBuf* bufs[] = {&c->STC, &c->MLR, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
+  DevBuf* bufs[] = {&c->STC, &c->MLR, &c->pinv_ds, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
                     &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres, &c->diag};
   for (DevBuf* b : bufs) b->release();
   if (c->events)

@@ -51,6 +51,7 @@ struct LevelArgs {
   double* dinv;            // level-n node blocks
   double* NWt;             // [node blocks][N][nodes] interior-node constraint weights
   double* Sinv;            // [mp][ncon][ncon]
+  double* pinv_ds;         // [mp][ncon] row scales of S~ (reading R20 windows)
   // per-problem vectors (problem = mp*n_rhs + r)
   double* X; double* R; double* P; double* Q; double* B;
   double* FI; double* FY;  // fine workspace (levels >= 2): I_p / phi and A1 I_p
