@@ -63,7 +63,14 @@ typedef struct {
   int      keep_all;       /* 1: keep every macropoint's fine local solution (for
                               mch_local_solution); 0: keep only parents (T_{L-1}) */
   void*    stream;         /* cudaStream_t */
+  int      interp;         /* interpolation of preceding levels (Eq. 11): MCH_INTERP_DLINEAR (0,
+                              default) = d-linear on the corners of the T_{n-1} cell (reading
+                              R10); MCH_INTERP_NEAREST_S1 (1) = the single nearest S_1 point,
+                              weight 1, as in the paper's experiments */
 } mch_params;
+
+#define MCH_INTERP_DLINEAR    0
+#define MCH_INTERP_NEAREST_S1 1
 
 typedef struct {
   int64_t  macropoints;    /* macropoints of this level solved by this context */

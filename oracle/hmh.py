@@ -64,8 +64,8 @@ def constraint_rows(An, Cn, g):
 
 
 class Oracle:
-    def __init__(self, d, n, M, L, eta, N, kappa, ids, l=1, keep_all_phi=False):
-        self.plan = Plan(d, n, M, L, eta, l)
+    def __init__(self, d, n, M, L, eta, N, kappa, ids, l=1, keep_all_phi=False, interp="dlinear"):
+        self.plan = Plan(d, n, M, L, eta, l, interp=interp)
         self.d, self.n, self.M, self.L, self.eta, self.N, self.l = d, n, M, L, eta, N, l
         self.h = 1.0 / n
         self.kappa = np.asarray(kappa, dtype=np.float64).reshape((n,) * d)

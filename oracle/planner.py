@@ -29,10 +29,13 @@ def oversampling_layers_paper(H: float) -> int:
 
 
 class Plan:
-    def __init__(self, d: int, n: int, M: int, L: int, eta: int, l: int = 1):
+    def __init__(self, d: int, n: int, M: int, L: int, eta: int, l: int = 1, interp: str = "dlinear"):
         if n % M:
             raise ValueError("M must divide n (H/h integer)")
         self.d, self.n, self.M, self.L, self.eta, self.l = d, n, M, L, eta, l
+        if interp not in ("dlinear", "nearest_s1"):
+            raise ValueError("interp must be 'dlinear' or 'nearest_s1'")
+        self.interp = interp
         self.c = n // M  # fine cells per H
         if self.c % 2:
             raise ValueError("H/(2h) must be an integer")
@@ -106,10 +109,26 @@ class Plan:
         return lo_t <= lo_p and hi_t >= hi_p
 
     def parents(self, k):
-        """[(t, c_t)] for k ∈ S_n, n ≥ 2 (Eq. 11, reading R10 + R9 boundary rule)."""
+        """[(t, c_t)] for k ∈ S_n, n ≥ 2 (Eq. 11, reading R10 + R9 boundary rule).
+
+        interp = "nearest_s1" (NEXT-1; "we only consider the first level for the
+        interpolation operator, i.e. I_p = Φ_t with x_t ∈ S_1"): the single S_1 point nearest to
+        x_p (Euclidean) among those whose window covers the child's (reading R9), weight 1; ties
+        go to the smaller coordinate in each dimension."""
         lev = self.level_of(k)
         if lev == 1:
             return []
+        if self.interp == "nearest_s1":
+            s1 = self.eta ** (self.L - 1)  # spacing of T_1 = S_1 in macro units
+            t = []
+            for ki in k:
+                a = (ki // s1) * s1
+                cands = [a] if ki == a else [a, a + s1]
+                cands = [ti for ti in cands if self.covers(ti, ki)]
+                if not cands:
+                    raise ValueError(f"no covering parent for macropoint {k}")
+                t.append(min(cands, key=lambda ti: (abs(ti - ki), ti)))
+            return [(tuple(t), 1.0)]
         s = self.eta ** (self.L - lev + 1)  # spacing of T_{n-1} in macro units
         per_dim = []
         for ki in k:

@@ -38,8 +38,11 @@ def _current_stream():
     return None
 
 
+INTERP = {"dlinear": 0, "nearest_s1": 1}
+
+
 def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversample=1, rtol=1e-12,
-               max_iter=20000, rank=0, world=1, keep_all=False, stream=None):
+               max_iter=20000, rank=0, world=1, keep_all=False, stream=None, interp="dlinear"):
     """Returns an opaque context handle (ctypes.c_void_p)."""
     if isinstance(kappa, np.ndarray):
         kappa = np.ascontiguousarray(kappa, dtype=np.float64)
@@ -50,7 +53,8 @@ def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversamp
         raise ValueError("kappa and continuum_id must both be host or both be device buffers")
     p = MchParams(d=d, n=n, num_continua=num_continua, M=M, levels=levels, eta=eta,
                   oversample=oversample, rtol=rtol, max_iter=max_iter, rank=rank, world=world,
-                  keep_all=int(keep_all), stream=stream if stream is not None else _current_stream())
+                  keep_all=int(keep_all), stream=stream if stream is not None else _current_stream(),
+                  interp=INTERP[interp])
     ctx = ctypes.c_void_p()
     check(lib.mch_create(ctypes.byref(p), kp, ip, kdev, ctypes.byref(ctx)), None)
     return ctx
@@ -87,13 +91,13 @@ class Homogenizer:
     """Hierarchical multicontinuum homogenization hot path on one GPU (or one rank's shard)."""
 
     def __init__(self, d, n, N, M, L, eta, kappa, ids, l=1, rtol=1e-12, max_iter=20000, rank=0,
-                 world=1, keep_all=False, stream=None):
+                 world=1, keep_all=False, stream=None, interp="dlinear"):
         self.d, self.n, self.N, self.M, self.L, self.eta, self.l = d, n, N, M, L, eta, l
         self.n_rhs = N * (1 + d)
         self.num_macropoints = (M + 1) ** d
         self.ctx = mch_create(d, n, N, M, L, eta, kappa, ids, oversample=l, rtol=rtol,
                               max_iter=max_iter, rank=rank, world=world, keep_all=keep_all,
-                              stream=stream)
+                              stream=stream, interp=interp)
         self.solved = 0
 
     @classmethod

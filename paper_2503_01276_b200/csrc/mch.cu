@@ -181,6 +181,11 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   c->plan.L = p.levels;
   c->plan.eta = p.eta;
   c->plan.l = p.oversample;
+  if (p.interp != 0 && p.interp != 1) {
+    delete c;
+    return fail(nullptr, MCH_EINVAL, "interp must be MCH_INTERP_DLINEAR or MCH_INTERP_NEAREST_S1");
+  }
+  c->plan.interp = p.interp;
   std::string perr;
   int rc = c->plan.build(perr);
   if (rc != 0) {

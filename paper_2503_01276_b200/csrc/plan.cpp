@@ -7,6 +7,8 @@
 //  sum c_t = 1 (Eq. 11; reading R10); a parent whose window does not
 //  cover the child's window after the local shift is dropped per coordinate and its
 //  weight moved to the opposite parent (reading R9).
+//  interp = 1 (NEXT-1): the single nearest S_1 point whose window covers the
+//  child's, weight 1 (ties: the smaller coordinate).
 #include "plan.h"
 
 #include <cstdio>
@@ -81,6 +83,28 @@ int HostPlan::build(std::string& err) {
     MacroHost& m = all[lin];
     m.npar = 0;
     if (m.level == 1) continue;
+    if (interp == 1) {  // nearest covering S_1 point per dimension (Euclidean distance is separable)
+      const int64_t s1 = ipow(eta, L - 1);
+      int t[3] = {0, 0, 0};
+      for (int i = 0; i < D; i++) {
+        const int ki = m.k[i];
+        const int a = (int)((ki / s1) * s1), b = (int)(a + s1);
+        const bool ca = covers(a, ki), cb = (ki != a) && covers(b, ki);
+        if (!ca && !cb) {
+          char buf[160];
+          snprintf(buf, sizeof buf, "no covering parent for macropoint (%d,%d,%d)", m.k[0], m.k[1], m.k[2]);
+          err = buf;
+          return -8;
+        }
+        t[i] = (ca && (!cb || ki - a <= b - ki)) ? a : b;  // tie: the smaller coordinate
+      }
+      int64_t tl = 0;
+      for (int i = D - 1; i >= 0; i--) tl = tl * V + t[i];
+      m.par_lin[0] = tl;
+      m.par_w[0] = 1.0;
+      m.npar = 1;
+      continue;
+    }
     const int64_t s = ipow(eta, L - m.level + 1);
     int cand[3][2], ncand[3];
     double wc[3][2];

@@ -15,6 +15,7 @@ struct MacroHost {
 
 struct HostPlan {
   int D = 2, L = 1, eta = 2, l = 1;
+  int interp = 0;  // 0: d-linear on T_{n-1} (R10); 1: nearest covering S_1 point, weight 1
   int64_t n = 0, M = 0, c = 0;
   std::vector<MacroHost> all;             // by lexicographic index
   std::vector<std::vector<int64_t>> S;    // S[level] = indices, lexicographic

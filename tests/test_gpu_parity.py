@@ -206,3 +206,22 @@ def test_oversampling_l2(d, n, M, L, N):
             po = o.solve(k)["phi"]
             for r in range(o.n_rhs):
                 assert phi_err(h.local_solution(k, r), po[r]) < PHI_TOL
+
+
+@pytest.mark.parametrize("d,n,M,L,N", [(2, 64, 8, 3, 2), (2, 32, 4, 2, 3), (3, 16, 4, 2, 2)])
+def test_nearest_s1_all_points(d, n, M, L, N):
+    """NEXT-1: nearest-S_1 single-parent interpolation, every macropoint vs the
+    oracle with the same reading"""
+    H = _gpu()
+    kap, ids = _admissible(d, n, M, N, 30 + d + N)
+    o = Oracle(d, n, M, L, 2, N, kap, ids, interp="nearest_s1")
+    Go = o.effective_coeffs()
+    with H(d, n, N, M, L, 2, kap, ids, keep_all=True, interp="nearest_s1") as h:
+        h.solve_all()
+        Gg = h.effective_coeffs()
+        for k in o.plan.all_vertices():
+            i = o.plan.linear_index(k)
+            assert g_err(Gg[i], Go[i]) < G_TOL, (k, g_err(Gg[i], Go[i]))
+            po = o.solve(k)["phi"]
+            for r in range(o.n_rhs):
+                assert phi_err(h.local_solution(k, r), po[r]) < PHI_TOL

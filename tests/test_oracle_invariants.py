@@ -240,3 +240,26 @@ def test_P9_level1_points_equal_plain_method():
     o2 = Oracle(2, 32, 4, 2, 2, 2, kap, ids)
     for k in o2.plan.S(1):
         assert np.array_equal(o2.solve(k)["G"], o1.solve(k)["G"])
+
+
+def test_P3_P5_nearest_s1_interpolation():
+    """Nearest-S_1 interpolation (NEXT-1): the partition of unity survives
+    (Σ_t c_t = 1 with a single parent), and on a periodic aligned medium the hierarchy is exact
+    (ξ ≡ 0, G^hier = G^{L=1}) for children whose S_1 parent is interior."""
+    kap, ids = random_medium(2, 64, 2, seed=12)
+    o = Oracle(2, 64, 8, 3, 2, 2, kap, ids, interp="nearest_s1")
+    for k in [(1, 1), (2, 3), (6, 5), (3, 0), (8, 7)]:
+        r = o.solve(k)
+        assert np.abs(r["phi"][0] + r["phi"][1] - 1.0).max() < 1e-12
+        sc = np.abs(r["G"]).max()
+        assert np.abs(r["G"][:, :2].sum(axis=1)).max() < 1e-11 * sc
+    n, M = 128, 8
+    kp, ip = periodic_medium(2, n, 8, 0.3, 1.0, 20.0)
+    o1 = Oracle(2, n, M, 1, 2, 2, kp, ip)
+    o3 = Oracle(2, n, M, 3, 2, 2, kp, ip, interp="nearest_s1")
+    sc = np.abs(o1.solve((4, 4))["G"]).max()
+    for k in [(3, 3), (5, 4), (4, 3)]:
+        r = o3.solve(k)
+        assert r["level"] >= 2
+        assert np.abs(r["xi"]).max() < 1e-10
+        assert np.abs(r["G"] - o1.solve(k)["G"]).max() < 1e-11 * sc

@@ -104,3 +104,26 @@ def test_subcell_partition():
             q = p.subcell_of_cell(k, cell)
             v = tuple(k[i] + (q // 3 ** i) % 3 - 1 for i in range(2))
             assert all(abs(cell[i] + 0.5 - v[i] * p.c) <= p.c / 2 for i in range(2))
+
+
+@pytest.mark.parametrize("d,n,M,L,eta", [(2, 64, 8, 3, 2), (2, 72, 12, 2, 3), (3, 64, 8, 3, 2)])
+def test_nearest_s1_parents_brute_force(d, n, M, L, eta):
+    """NEXT-1, PAPER.md:425 (I_p = Φ_t, x_t ∈ S_1): brute force over every S_1 point — the chosen
+    parent is in S_1, its window covers the child's in local coordinates (reading R9), it is the
+    nearest such point (Euclidean), ties resolved to the smallest coordinates; weight 1."""
+    p = Plan(d, n, M, L, eta, interp="nearest_s1")
+    s1 = set(p.S(1))
+    for k in p.all_vertices():
+        par = p.parents(k)
+        if p.level_of(k) == 1:
+            assert par == []
+            continue
+        assert len(par) == 1 and par[0][1] == 1.0
+        t = par[0][0]
+        assert t in s1
+        ok = [u for u in s1 if all(p.covers(u[i], k[i]) for i in range(d))]
+        dist = lambda u: sum((u[i] - k[i]) ** 2 for i in range(d))
+        best = min(dist(u) for u in ok)
+        assert dist(t) == best
+        ties = [u for u in ok if dist(u) == best]
+        assert all(t[i] == min(u[i] for u in ties) for i in range(d)), (k, t, ties)
