@@ -67,10 +67,16 @@ typedef struct {
                               default) = d-linear on the corners of the T_{n-1} cell (reading
                               R10); MCH_INTERP_NEAREST_S1 (1) = the single nearest S_1 point,
                               weight 1, as in the paper's experiments */
+  int      layout;         /* macropoint layout: MCH_LAYOUT_VERTEX (0, default) = x_p = H k,
+                              k in {0..M}^d (reading R1); MCH_LAYOUT_BLOCK (1) = block centres
+                              x_p = (k + 1/2) H, k in {0..M-1}^d, K_p the block, T_n as in the
+                              paper's Figures 2-3 */
 } mch_params;
 
 #define MCH_INTERP_DLINEAR    0
 #define MCH_INTERP_NEAREST_S1 1
+#define MCH_LAYOUT_VERTEX     0
+#define MCH_LAYOUT_BLOCK      1
 
 typedef struct {
   int64_t  macropoints;    /* macropoints of this level solved by this context */
@@ -103,8 +109,9 @@ int mch_create(const mch_params* params, const double* kappa, const uint8_t* con
  * after the level's device work is complete. */
 int mch_solve_level(mch_ctx* ctx, int level);
 
-/* Copy the Eq. (7) coefficients of all (M+1)^d macropoints into out,
- * layout [(M+1)^d][n_rhs][n_rhs] with n_rhs = N(1+d), macropoints in
+/* Copy the Eq. (7) coefficients of all macropoints into out,
+ * layout [P][n_rhs][n_rhs] with P = (M+1)^d (vertex layout) or M^d (block layout),
+ * n_rhs = N(1+d), macropoints in
  * lexicographic vertex order (x fastest); G[a][b] = int_{K_p} kappa grad(Phi_a).grad(Phi_b)
  * with Phi = (phi_0..phi_{N-1}, phi_0^0..phi_0^{d-1}, .., phi_{N-1}^{d-1}), i.e.
  * B_ji = G[j][i], B^m_ji = G[j][N+i*d+m], Bbar^n_ji = G[N+j*d+n][i],

@@ -64,8 +64,9 @@ def constraint_rows(An, Cn, g):
 
 
 class Oracle:
-    def __init__(self, d, n, M, L, eta, N, kappa, ids, l=1, keep_all_phi=False, interp="dlinear"):
-        self.plan = Plan(d, n, M, L, eta, l, interp=interp)
+    def __init__(self, d, n, M, L, eta, N, kappa, ids, l=1, keep_all_phi=False, interp="dlinear",
+                 layout="vertex"):
+        self.plan = Plan(d, n, M, L, eta, l, interp=interp, layout=layout)
         self.d, self.n, self.M, self.L, self.eta, self.N, self.l = d, n, M, L, eta, N, l
         self.h = 1.0 / n
         self.kappa = np.asarray(kappa, dtype=np.float64).reshape((n,) * d)
@@ -103,7 +104,7 @@ class Oracle:
         sub = np.zeros(kap.shape, dtype=np.int64)
         for i in range(d):
             gi = np.arange(lo[i], hi[i])
-            slot = (gi + c // 2) // c - k[i] + l
+            slot = self.plan.subcell_coord(gi) - k[i] + l
             sub = sub + (slot * w ** i).reshape(self._axis_shape(i, len(gi)))
         n_sub = w ** d
         A1 = assemble_stiffness(kap, h)
@@ -197,7 +198,7 @@ class Oracle:
 
     def effective_coeffs(self):
         """G for all (M+1)^d macropoints in lexicographic order, shape [P, n_rhs, n_rhs]."""
-        out = np.zeros(((self.M + 1) ** self.d, self.n_rhs, self.n_rhs))
+        out = np.zeros((self.plan.num_macropoints(), self.n_rhs, self.n_rhs))
         for lev in range(1, self.L + 1):
             for k in self.plan.S(lev):
                 out[self.plan.linear_index(k)] = self.solve(k)["G"]

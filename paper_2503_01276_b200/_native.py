@@ -26,7 +26,7 @@ class MchParams(ctypes.Structure):
                 ("M", ctypes.c_int64), ("levels", ctypes.c_int), ("eta", ctypes.c_int),
                 ("oversample", ctypes.c_int), ("rtol", ctypes.c_double), ("max_iter", ctypes.c_int),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("keep_all", ctypes.c_int),
-                ("stream", ctypes.c_void_p), ("interp", ctypes.c_int)]
+                ("stream", ctypes.c_void_p), ("interp", ctypes.c_int), ("layout", ctypes.c_int)]
 
 
 class MchLevelStats(ctypes.Structure):

@@ -39,10 +39,12 @@ def _current_stream():
 
 
 INTERP = {"dlinear": 0, "nearest_s1": 1}
+LAYOUT = {"vertex": 0, "block": 1}
 
 
 def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversample=1, rtol=1e-12,
-               max_iter=20000, rank=0, world=1, keep_all=False, stream=None, interp="dlinear"):
+               max_iter=20000, rank=0, world=1, keep_all=False, stream=None, interp="dlinear",
+               layout="vertex"):
     """Returns an opaque context handle (ctypes.c_void_p)."""
     if isinstance(kappa, np.ndarray):
         kappa = np.ascontiguousarray(kappa, dtype=np.float64)
@@ -54,7 +56,7 @@ def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversamp
     p = MchParams(d=d, n=n, num_continua=num_continua, M=M, levels=levels, eta=eta,
                   oversample=oversample, rtol=rtol, max_iter=max_iter, rank=rank, world=world,
                   keep_all=int(keep_all), stream=stream if stream is not None else _current_stream(),
-                  interp=INTERP[interp])
+                  interp=INTERP[interp], layout=LAYOUT[layout])
     ctx = ctypes.c_void_p()
     check(lib.mch_create(ctypes.byref(p), kp, ip, kdev, ctypes.byref(ctx)), None)
     return ctx
@@ -91,13 +93,14 @@ class Homogenizer:
     """Hierarchical multicontinuum homogenization hot path on one GPU (or one rank's shard)."""
 
     def __init__(self, d, n, N, M, L, eta, kappa, ids, l=1, rtol=1e-12, max_iter=20000, rank=0,
-                 world=1, keep_all=False, stream=None, interp="dlinear"):
+                 world=1, keep_all=False, stream=None, interp="dlinear", layout="vertex"):
         self.d, self.n, self.N, self.M, self.L, self.eta, self.l = d, n, N, M, L, eta, l
         self.n_rhs = N * (1 + d)
-        self.num_macropoints = (M + 1) ** d
+        self.mv = M + 1 if layout == "vertex" else M  # macropoints per dimension
+        self.num_macropoints = self.mv ** d
         self.ctx = mch_create(d, n, N, M, L, eta, kappa, ids, oversample=l, rtol=rtol,
                               max_iter=max_iter, rank=rank, world=world, keep_all=keep_all,
-                              stream=stream, interp=interp)
+                              stream=stream, interp=interp, layout=layout)
         self.solved = 0
 
     @classmethod
@@ -145,7 +148,7 @@ class Homogenizer:
     def linear_index(self, k):
         idx = 0
         for i in reversed(range(self.d)):
-            idx = idx * (self.M + 1) + int(k[i])
+            idx = idx * self.mv + int(k[i])
         return idx
 
     def local_solution(self, k, rhs):

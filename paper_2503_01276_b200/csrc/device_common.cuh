@@ -113,7 +113,7 @@ __device__ __forceinline__ int elem_subcell(const LevelArgs& A, const ProbDesc& 
 #pragma unroll
   for (int i = D - 1; i >= 0; i--) {
     int f = P.lo[i] + e[i] * g.s;
-    int slot = fdiv(f + A.c / 2, A.inv_c) - P.k[i] + A.l;
+    int slot = fdiv(f + A.coff, A.inv_c) - P.k[i] + A.l;
     q = q * A.w + slot;
   }
   return q;
@@ -322,11 +322,11 @@ __device__ __forceinline__ double ct_fast(const LevelArgs& A, const ProbDesc& P,
 #pragma unroll
   for (int i = D - 1; i >= 0; i--) {
     const int xi = x[i];
-    const int t = P.lo[i] + xi * g.s + A.c / 2;
+    const int t = P.lo[i] + xi * g.s + A.coff;
     const int v = fdiv(t, A.inv_c);
     if (xi > 0 && xi < g.nn[i] - 1 && v * A.c == t) interior = false;  // on a dual-block face
     const int e = (xi < g.nc[i]) ? xi : xi - 1;
-    const int slot = fdiv(P.lo[i] + e * g.s + A.c / 2, A.inv_c) - P.k[i] + A.l;
+    const int slot = fdiv(P.lo[i] + e * g.s + A.coff, A.inv_c) - P.k[i] + A.l;
     q = q * A.w + slot;
   }
   if (!interior) return ct_node<D>(A, P, g, yhat, k);
@@ -376,10 +376,10 @@ __device__ void subcell_boxes(const LevelArgs& A, const ProbDesc& P, const Geo<D
           const int slot = rem % A.w;
           rem /= A.w;
           const int v = P.k[i] - A.l + slot;
-          int flo = v * A.c - A.c / 2, fhi = v * A.c + A.c / 2;
+          int flo = v * A.c - A.coff, fhi = flo + A.c;
           if (flo < 0) flo = 0;
           if (fhi > A.n) fhi = A.n;
-          if (v < 0 || v > A.n / A.c || fhi <= flo) {
+          if (fhi <= flo) {
             ext = 0;
           } else {
             lo = (flo - P.lo[i]) / g.s;

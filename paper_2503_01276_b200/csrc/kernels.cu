@@ -100,10 +100,10 @@ __global__ void k_targets(LevelArgs A) {
       const int slot = rem % A.w;
       rem /= A.w;
       const int v = P.k[i] - A.l + slot;
-      int flo = v * A.c - A.c / 2, fhi = v * A.c + A.c / 2;
+      int flo = v * A.c - A.coff, fhi = flo + A.c;
       flo = flo < 0 ? 0 : flo;
       fhi = fhi > A.n ? A.n : fhi;
-      if (v < 0 || v > A.n / A.c || fhi <= flo) present = false;
+      if (fhi <= flo) present = false;
       lo[i] = flo;
       ext[i] = fhi - flo;
     }
@@ -374,7 +374,9 @@ __global__ void k_proj_setup(LevelArgs A) {
     __syncthreads();
   }
   double* out = A.Sinv + (int64_t)mp * nc * nc;
-  if (minpiv > 1e-10) {
+  // a small pivot only flags possible dependence: k_pinv then decides by the eigenvalues with
+  // exactly the oracle's criterion (lambda < 1e-11 lambda_max dropped, reading R20)
+  if (minpiv > 1e-6) {
     for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
       const int i = idx / nc, j = idx % nc;
       out[idx] = S[idx] * ds[i] * ds[j];
@@ -477,6 +479,9 @@ __global__ void k_pinv(LevelArgs A) {
   for (int i = lane; i < nc; i += 32) lmax = fmax(lmax, S[i * m + i]);
   for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(FULLMASK, lmax, o));
   const double* ds = A.pinv_ds + (int64_t)mp * nc;
+  bool trunc = false;
+  for (int k = lane; k < nc; k += 32) trunc = trunc || !(S[k * m + k] > 1e-11 * lmax);
+  if (__any_sync(FULLMASK, trunc) && lane == 0) atomicOr(&A.flags[mp], 4);  // rows were dependent
   for (int idx = lane; idx < nc * nc; idx += 32) {
     const int i = idx / nc, j = idx % nc;
     double acc = 0.0;

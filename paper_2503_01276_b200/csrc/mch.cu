@@ -122,10 +122,10 @@ static int fail(mch_ctx* c, int code, const std::string& msg) {
 // row of the elements above them, and each group is cut into near-equal chunks of <= rpt rows.
 // Chunk = (first node row, rows, subcell row, subcell row of the elements below the first row if
 // those belong to the previous subcell row, else -1).
-static void seg_plan_2d(const ProbDesc& P, int s, int c, int l, int rpt, std::vector<short4>& out) {
+static void seg_plan_2d(const ProbDesc& P, int s, int c, int coff, int l, int rpt, std::vector<short4>& out) {
   out.clear();
   const int ncy = P.nc[1];
-  auto slot = [&](int ey) { return (P.lo[1] + ey * s + c / 2) / c - P.k[1] + l; };
+  auto slot = [&](int ey) { return (P.lo[1] + ey * s + coff) / c - P.k[1] + l; };
   int ea = 0;
   while (ea < ncy) {
     int eb = ea + 1;
@@ -186,6 +186,11 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
     return fail(nullptr, MCH_EINVAL, "interp must be MCH_INTERP_DLINEAR or MCH_INTERP_NEAREST_S1");
   }
   c->plan.interp = p.interp;
+  if (p.layout != 0 && p.layout != 1) {
+    delete c;
+    return fail(nullptr, MCH_EINVAL, "layout must be MCH_LAYOUT_VERTEX or MCH_LAYOUT_BLOCK");
+  }
+  c->plan.layout = p.layout;
   std::string perr;
   int rc = c->plan.build(perr);
   if (rc != 0) {
@@ -329,7 +334,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
         P.ncf[d] = (d < D) ? m.hi[d] - m.lo[d] : 0;
         P.nc[d] = (d < D) ? P.ncf[d] / s : 0;
         P.glo[d] = (d < D) ? P.lo[d] / s : 0;
-        const int64_t a = (int64_t)m.k[d] * pl.c - pl.c / 2, b = (int64_t)m.k[d] * pl.c + pl.c / 2;
+        const int64_t a = (int64_t)m.k[d] * pl.c - pl.coff(), b = a + pl.c;  // K_p
         P.kp_lo[d] = (d < D) ? (int)std::max<int64_t>(0, a) : 0;
         P.kp_hi[d] = (d < D) ? (int)std::min<int64_t>(pl.n, b) : 1;
       }
@@ -382,7 +387,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
         std::vector<std::vector<short4>> per(nmp);
         int maxseg = 0, maxwp = 0;
         for (int i = 0; i < nmp; i++) {
-          seg_plan_2d(descs[i], s, (int)pl.c, c->l, rpt, per[i]);
+          seg_plan_2d(descs[i], s, (int)pl.c, (int)pl.coff(), c->l, rpt, per[i]);
           nsegs[i] = (int)per[i].size();
           maxseg = std::max(maxseg, nsegs[i]);
           maxwp = std::max(maxwp, ((descs[i].nc[0] + 1 + 31) / 32) * nsegs[i]);
@@ -470,7 +475,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
 
   LevelArgs A{};
   A.D = D; A.N = N; A.n_rhs = nr; A.l = c->l; A.w = c->w; A.nsub = c->nsub; A.ncon = nc;
-  A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.gn = gn; A.h = 1.0 / (double)pl.n; A.inv_c = 1.0f / (float)pl.c;
+  A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.coff = (int)pl.coff(); A.gn = gn; A.h = 1.0 / (double)pl.n; A.inv_c = 1.0f / (float)pl.c;
   A.kappa = c->kappa; A.ids = c->ids; A.pool = c->pool; A.G = c->G;
   A.rtol = c->p.rtol; A.max_iter = c->p.max_iter;
   if (level >= 2) {
@@ -562,7 +567,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     ms_setup += t1; ms_pcg += t2; ms_gram += t3;
     for (int i = 0; i < B.nmp; i++) {
       const MacroHost& m = pl.all[B.mps[i]];
-      if (B.h_flags[i] & 2) S.rank_deficient++;
+      if (B.h_flags[i] & 4) S.rank_deficient++;  // k_pinv truncated eigenvalues (reading R20)
       if (B.h_flags[i] & 1) {
         char buf[200];
         snprintf(buf, sizeof buf, "continuum absent from K_p of macropoint (%d,%d,%d)", m.k[0], m.k[1], m.k[2]);

@@ -33,6 +33,7 @@ struct LevelArgs {
   int nsub, ncon;          // w^D subcells, ncon = nsub*N constraint rows
   int level, s;            // s = eta^(level-1)
   int n, c;                // fine cells per dim, fine cells per H
+  int coff;                // subcell of fine cell f: (f + coff) / c - k + l (c/2 vertex layout, 0 block)
   int gn;                  // global level-n cells per dim (n/s)
   double h;
   float inv_c;             // 1/c

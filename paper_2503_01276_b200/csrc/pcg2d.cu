@@ -86,7 +86,7 @@ __device__ __forceinline__ double warp_sinv(const double* Si, int nc, double cv)
 }
 
 __device__ __forceinline__ int sub_slot(const LevelArgs& A, const ProbDesc& P, int dim, int e) {
-  return fdiv(P.lo[dim] + e * A.s + A.c / 2, A.inv_c) - P.k[dim] + A.l;
+  return fdiv(P.lo[dim] + e * A.s + A.coff, A.inv_c) - P.k[dim] + A.l;
 }
 
 // multiset state of two element ids a, b in {0..N-1, 0xFF = no element}: index of (min, max)

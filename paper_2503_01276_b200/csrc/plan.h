@@ -16,11 +16,17 @@ struct MacroHost {
 struct HostPlan {
   int D = 2, L = 1, eta = 2, l = 1;
   int interp = 0;  // 0: d-linear on T_{n-1} (R10); 1: nearest covering S_1 point, weight 1
+  int layout = 0;  // 0: vertex-centred (R1); 1: block-centred (paper Figs. 2-3)
   int64_t n = 0, M = 0, c = 0;
+  int64_t mv = 0;          // macropoints per dimension: M+1 (vertex) or M (block)
+  std::vector<int64_t> r;  // r[lev]: T_lev = {k : k_i = r[lev] mod eta^(L-lev)}
   std::vector<MacroHost> all;             // by lexicographic index
   std::vector<std::vector<int64_t>> S;    // S[level] = indices, lexicographic
   int build(std::string& err);
   int level_of(const int* k) const;
   void window(const int* k, int* lo, int* hi) const;
   bool covers(int t, int k) const;
+  int64_t origin2(int k) const;
+  int bracket(int k, int lev, int* t, double* w) const;
+  int64_t coff() const { return layout == 0 ? c / 2 : 0; }  // subcell of fine cell f: (f + coff) / c
 };

@@ -21,29 +21,64 @@ def _vertices(d, M):
 
 
 class BruteForce:
-    def __init__(self, d, n, M, L, eta, N, kappa, ids, l=1):
+    def __init__(self, d, n, M, L, eta, N, kappa, ids, l=1, layout="vertex"):
         self.d, self.n, self.M, self.L, self.eta, self.N, self.l = d, n, M, L, eta, N, l
+        self.layout = layout
         self.h = 1.0 / n
         self.H = 1.0 / M
         self.kappa = kappa.reshape((n,) * d)
         self.ids = ids.reshape((n,) * d)
         self.n_rhs = N * (1 + d)
         self.res = {}
+        if layout == "block":
+            self._block_levels()
+
+    def points(self):
+        m = self.M + 1 if self.layout == "vertex" else self.M
+        return [tuple(reversed(r)) for r in itertools.product(range(m), repeat=self.d)]
+
+    def xp(self, k):
+        off = 0.5 if self.layout == "block" else 0.0
+        return [(ki + off) * self.H for ki in k]
+
+    def _block_levels(self):
+        """T_n of the block layout by enumerating coarse blocks in physical space: T_L = every
+        block; each coarse block of size η^{L-n}H keeps the T_{n+1} point inside it whose centre is
+        closest to the block's centre (ties: the smaller coordinates)."""
+        self.Tsets = {self.L: set(self.points())}
+        for lev in range(self.L - 1, 0, -1):
+            S = self.eta ** (self.L - lev) * self.H
+            nb = int(round(1.0 / S))
+            keep = set()
+            for cb in itertools.product(range(nb), repeat=self.d):
+                inside = [t for t in self.Tsets[lev + 1]
+                          if all(cb[i] * S - 1e-12 <= self.xp(t)[i] < (cb[i] + 1) * S - 1e-12 for i in range(self.d))]
+                centre = [(cb[i] + 0.5) * S for i in range(self.d)]
+                best = min(inside, key=lambda t: (round(max(abs(self.xp(t)[i] - centre[i])
+                                                            for i in range(self.d)) / self.H, 9),
+                                                  tuple(reversed(t))))
+                keep.add(best)
+            self.Tsets[lev] = keep
+
+    def in_T(self, k, lev):
+        if self.layout == "block":
+            return k in self.Tsets[lev]
+        return all(ki % self.eta ** (self.L - lev) == 0 for ki in k)
 
     def level(self, k):
         for lev in range(1, self.L + 1):
-            if all(ki % self.eta ** (self.L - lev) == 0 for ki in k):
+            if self.in_T(k, lev):
                 return lev
 
     def window(self, k):
         """physical box [a_i, b_i] of R_p^+ = x_p ± (l+1/2)H clipped to [0,1]"""
         r = (self.l + 0.5) * self.H
-        return [(max(0.0, ki * self.H - r), min(1.0, ki * self.H + r)) for ki in k]
+        return [(max(0.0, x - r), min(1.0, x + r)) for x in self.xp(k)]
 
     def parents(self, k):
         lev = self.level(k)
         s = self.eta ** (self.L - lev + 1)
-        Tprev = [t for t in _vertices(self.d, self.M) if all(ti % s == 0 for ti in t)]
+        Tprev = [t for t in self.points() if self.in_T(t, lev - 1)]
         # per coordinate: candidate lattice values within distance < s, linear weights
         per = []
         wk = self.window(k)
@@ -59,7 +94,8 @@ class BruteForce:
                     ok.append(ti)
             if len(ok) < len(cands):
                 ws = {ok[0]: 1.0}
-            per.append([(ti, ws[ti]) for ti in ok])
+            tot = sum(ws[ti] for ti in ok)  # Σ c_t = 1 with one-sided neighbours
+            per.append([(ti, ws[ti] / tot) for ti in ok])
         out = []
         for combo in itertools.product(*per):
             out.append((tuple(c[0] for c in combo), float(np.prod([c[1] for c in combo]))))
@@ -118,7 +154,8 @@ class BruteForce:
             kap = self.kappa[tuple(reversed(gcell))]
             j = int(self.ids[tuple(reversed(gcell))])
             centre = [x0[i] + (e[i] + 0.5) * h for i in range(d)]
-            vq = [int(np.floor(centre[i] / self.H + 0.5)) for i in range(d)]
+            vq = [int(np.floor(centre[i] / self.H + (0.5 if self.layout == "vertex" else 0.0)))
+                  for i in range(d)]
             q = 0
             for i in reversed(range(d)):
                 q = q * (2 * self.l + 1) + (vq[i] - k[i] + self.l)

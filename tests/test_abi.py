@@ -37,7 +37,7 @@ def _create(**kw):
     ids = kw.pop("ids", np.zeros((n,) * d, dtype=np.uint8))
     p = MchParams(d=d, n=n, num_continua=kw.pop("N", 1), M=kw.pop("M", 4), levels=kw.pop("L", 1),
                   eta=kw.pop("eta", 2), oversample=kw.pop("l", 1), rtol=1e-12, max_iter=100, rank=0, world=1,
-                  keep_all=0, stream=None, interp=kw.pop("interp", 0))
+                  keep_all=0, stream=None, interp=kw.pop("interp", 0), layout=kw.pop("layout", 0))
     ctx = ctypes.c_void_p()
     rc = lib.mch_create(ctypes.byref(p), kap.ctypes.data, ids.ctypes.data, 0, ctypes.byref(ctx))
     return rc, lib.mch_last_error(None).decode()
@@ -56,6 +56,8 @@ def _create(**kw):
     (dict(ids=np.full((32, 32), 3, dtype=np.uint8), N=2), -1),  # id >= N
     (dict(d=3, n=16, M=2, N=2, l=2), -1),             # 5^3 subcells x 2 continua > 108 constraint rows
     (dict(interp=2), -1),                             # unknown interpolation mode
+    (dict(layout=2), -1),                             # unknown macropoint layout
+    (dict(n=36, M=6, L=3, layout=1), -2),             # block layout: H/(2 h eta^(L-1)) = 3/4 not integer
 ])
 def test_create_rejects_invalid_inputs(kw, code):
     rc, msg = _create(**kw)

@@ -225,3 +225,31 @@ def test_nearest_s1_all_points(d, n, M, L, N):
             po = o.solve(k)["phi"]
             for r in range(o.n_rhs):
                 assert phi_err(h.local_solution(k, r), po[r]) < PHI_TOL
+
+
+@pytest.mark.parametrize("d,n,M,L,N", [(2, 32, 8, 1, 2), (2, 64, 8, 3, 2), (2, 48, 12, 2, 3), (3, 12, 3, 1, 2),
+                                       (3, 16, 4, 2, 2)])
+def test_block_layout_all_points(d, n, M, L, N):
+    """NEXT-1: block-centred macropoints (x_p at block centres, K_p the block, T_n of the paper's
+    Figure 2), every macropoint vs the oracle with the same layout"""
+    H = _gpu()
+    for seed in range(40 + d + N, 90 + d + N):
+        kap, ids = random_medium(d, n, N, seed=seed)
+        try:
+            o = Oracle(d, n, M, L, 2, N, kap, ids, layout="block")
+            for k in o.plan.all_vertices():
+                o.local_system(k)
+            break
+        except RuntimeError:
+            continue
+    Go = o.effective_coeffs()
+    with H(d, n, N, M, L, 2, kap, ids, keep_all=True, layout="block") as h:
+        assert h.num_macropoints == M ** d
+        h.solve_all()
+        Gg = h.effective_coeffs()
+        for k in o.plan.all_vertices():
+            i = o.plan.linear_index(k)
+            assert g_err(Gg[i], Go[i]) < G_TOL, (k, g_err(Gg[i], Go[i]))
+            po = o.solve(k)["phi"]
+            for r in range(o.n_rhs):
+                assert phi_err(h.local_solution(k, r), po[r]) < PHI_TOL

@@ -57,3 +57,31 @@ def test_rank_deficient_level_constraints():
         assert np.max(np.abs(Go - Gb) / np.maximum(np.abs(Gb), scale)) < 1e-9, k
         po = ro["phi"].reshape(o.n_rhs, -1).T
         assert np.abs(po - rb["phi"]).max() / np.abs(rb["phi"]).max() < 1e-9, k
+
+
+@pytest.mark.parametrize("d,n,M,L,N", [(2, 16, 4, 1, 2), (2, 24, 6, 2, 2), (2, 64, 8, 3, 2),
+                                       (3, 12, 3, 1, 2)])
+def test_block_layout_oracle_equals_dense_bruteforce(d, n, M, L, N):
+    """P1 for the block-centred layout (NEXT-1): x_p at block centres, K_p the
+    block, subcells the blocks of R_p^+, T_n of Figure 2 — oracle vs the independent dense solver,
+    every macropoint (3D: a sample)."""
+    for seed in range(40 + d + N, 90 + d + N):
+        kap, ids = random_medium(d, n, N, seed=seed)
+        try:
+            o = Oracle(d, n, M, L, 2, N, kap, ids, layout="block")
+            for k in o.plan.all_vertices():
+                o.local_system(k)
+            break
+        except RuntimeError:
+            continue
+    bf = BruteForce(d, n, M, L, 2, N, kap, ids, layout="block")
+    pts = list(o.plan.all_vertices())
+    if d == 3:
+        pts = [(0, 0, 0), (1, 0, 0), (1, 1, 1), (2, 1, 0)]
+    for k in pts:
+        ro, rb = o.solve(k), bf.solve(k)
+        Go, Gb = ro["G"], rb["G"]
+        scale = np.sqrt(np.outer(np.diag(Gb), np.diag(Gb))) + 1e-300
+        assert np.max(np.abs(Go - Gb) / np.maximum(np.abs(Gb), scale)) < 1e-10, k
+        po = ro["phi"].reshape(o.n_rhs, -1).T
+        assert np.abs(po - rb["phi"]).max() / np.abs(rb["phi"]).max() < 1e-10, k

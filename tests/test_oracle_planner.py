@@ -127,3 +127,35 @@ def test_nearest_s1_parents_brute_force(d, n, M, L, eta):
         assert dist(t) == best
         ties = [u for u in ok if dist(u) == best]
         assert all(t[i] == min(u[i] for u in ties) for i in range(d)), (k, t, ties)
+
+
+def test_paper_fig2_block_centred_positions():
+    """Block-centred layout (NEXT-1): T_n reproduces the star positions of the paper's Figure 2
+    (golden fixture with the tikz coordinates) and the S_n counts 4/12/48 of Figure 3."""
+    g = json.load(open(os.path.join(GOLDEN, "paper_fig2_block_T_positions.json")))
+    p = Plan(2, 8 * g["M"], g["M"], g["L"], g["eta"], layout="block")
+    for lev in range(1, g["L"] + 1):
+        idx = g["T_block_indices_per_dim"][str(lev)]
+        assert sorted(p.T(lev)) == sorted(itertools.product(idx, repeat=2))
+    c = json.load(open(os.path.join(GOLDEN, "paper_fig2_3_level_counts.json")))
+    assert [len(p.S(lev)) for lev in range(1, 4)] == c["S_counts"]
+
+
+@pytest.mark.parametrize("d,M,L,eta", [(2, 8, 3, 2), (2, 9, 3, 3), (2, 16, 4, 2), (3, 8, 3, 2)])
+def test_block_levels_and_parents_brute_force(d, M, L, eta):
+    """block layout: T_n from the oracle's modular rule equals the brute-force enumeration of coarse
+    blocks (tests/bruteforce.py), and the oracle's parents equal the brute force's."""
+    from tests.bruteforce import BruteForce
+    import numpy as np
+    n = M * eta ** (L - 1) * 2
+    p = Plan(d, n, M, L, eta, layout="block")
+    bf = BruteForce(d, n, M, L, eta, 1, np.ones((n,) * d), np.zeros((n,) * d, dtype=np.uint8),
+                    layout="block")
+    for lev in range(1, L + 1):
+        assert set(p.T(lev)) == bf.Tsets[lev]
+    for k in p.all_vertices():
+        if p.level_of(k) == 1:
+            continue
+        a = sorted((t, round(w, 12)) for t, w in p.parents(k))
+        b = sorted((t, round(w, 12)) for t, w in bf.parents(k))
+        assert a == b, (k, a, b)
