@@ -192,3 +192,17 @@ def periodic_medium(d: int, n: int, period: int, radius: float, k_matrix: float,
     ids = incl.astype(np.uint8)
     kappa = np.where(incl, k_incl, k_matrix).astype(np.float64)
     return np.ascontiguousarray(kappa), np.ascontiguousarray(ids)
+
+
+def paper_source(d: int, n: int, ids, eps: float, low=(0,)):
+    """Source of the paper's experiments at fine-cell centres:
+    f = e^{-40((x_1-1/2)^2 + (x_2-1/2)^2)}, scaled by ε/10 in the low-conductivity region Ω_1
+    (cells whose continuum id is in ``low``; continuum 0, the matrix, in the BASELINE media).
+    The paper's f depends on x_1, x_2 only; in 3D the same formula is used (reading R24)."""
+    xs = _grid(d, n)
+    shape = (n,) * d
+    g = np.broadcast_to(np.exp(-40.0 * ((xs[0] - 0.5) ** 2 + (xs[1] - 0.5) ** 2)), shape).copy()
+    ids = np.asarray(ids).reshape(shape)
+    in_low = np.isin(ids, np.asarray(low, dtype=ids.dtype))
+    g[in_low] *= eps / 10.0
+    return np.ascontiguousarray(g)
