@@ -128,6 +128,34 @@ int mch_effective_coeffs(mch_ctx* ctx, double* out, size_t out_len, int out_on_d
  * MCH_EINVAL (NULL pointers, kappa <= 0 / non-finite, id >= N), MCH_ECUDA. */
 int mch_set_medium(mch_ctx* ctx, const double* kappa, const uint8_t* continuum_id, int inputs_on_device);
 
+/* NEXT-2 (upscaled system).  Source term f for the load vectors of Eq. (7) (PAPER.md:221,
+ * b_j = |K_p|/|R_p| int_{R_p} f phi_j with R_p = K_p): float64, n^d, x fastest,
+ * constant per fine cell (the paper's f, sampled at cell centres by the caller).
+ * The loads are then computed alongside the Gram matrices of every level solved afterwards,
+ * b_j(p) = sum_{cells e of K_p} f_e (h^d/2^d) sum_{corners a of e} phi_j(a) (exact for Q1 phi_j).
+ * f = NULL removes the source.  Must be called before level 1 (or after mch_reset /
+ * mch_set_medium): MCH_EORDER otherwise.  Errors: MCH_EINVAL (non-finite host f), MCH_ECUDA. */
+int mch_set_source(mch_ctx* ctx, const double* f, int input_on_device);
+
+/* Copy the load vectors b[P][N] (macropoints in lexicographic order, P as for the coefficients;
+ * entries of macropoints owned by other ranks are 0).  Errors: MCH_EINVAL (no source, out_len <
+ * P*N), MCH_EORDER (levels missing). */
+int mch_load_vectors(mch_ctx* ctx, double* out, size_t out_len, int out_on_device);
+
+/* Solve the upscaled system, Eq. (6), through its bilinear form with U_i,
+ * V_j and their gradients taken at the block midpoints, on the block-centred layout only
+ * (MCH_EINVAL otherwise): U_i continuous Q1 on the coarse vertex grid {0..M}^d, U_i = 0 on the
+ * boundary (Eq. 1), a(U,V) = sum_p t_p(V)^T G_p t_p(U) with t_p = (U_0..U_{N-1}, grad U_0, ..,
+ * grad U_{N-1}) at x_p, l(V) = sum_p sum_j V_j(x_p) b_j(p) (reading R23).  G
+ * [P][n_rhs][n_rhs] and b [P][N] as returned by mch_effective_coeffs / mch_load_vectors; pass
+ * both NULL to use this context's own (world == 1, all levels solved, source set).
+ * inputs_on_device applies to G and b.  U receives [N][(M+1)^d] nodal values (x fastest).
+ * Deterministic one-CTA Jacobi-PCG to ||r|| <= rtol ||F|| (rtol <= 0: 1e-12; max_iter <= 0:
+ * 100000); *iters (may be NULL) receives the iteration count.  Errors: MCH_EINVAL, MCH_EORDER,
+ * MCH_ENOCONV (tolerance not reached), MCH_ECUDA. */
+int mch_macro_solve(mch_ctx* ctx, const double* G, const double* b, int inputs_on_device, double* U,
+                    size_t U_len, int out_on_device, double rtol, int max_iter, int* iters);
+
 /* Rewind the level counter so the same context (inputs, plan, pool, scratch) solves levels
  * 1..L again — for repeated runs (benchmarks, serving) without re-creating the context. */
 int mch_reset(mch_ctx* ctx);

@@ -85,6 +85,44 @@ def mch_effective_coeffs(ctx, out):
     return out
 
 
+def mch_set_source(ctx, f):
+    """Source f (cellwise, n^d) for the Eq. (7) load vectors; None removes it."""
+    if f is None:
+        check(lib.mch_set_source(ctx, None, 0), ctx)
+        return
+    if isinstance(f, np.ndarray):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+    fp, fdev = _ptr(f)
+    check(lib.mch_set_source(ctx, fp, fdev), ctx)
+
+
+def mch_load_vectors(ctx, out):
+    op, odev = _ptr(out)
+    n = out.numel() if hasattr(out, "numel") else out.size
+    check(lib.mch_load_vectors(ctx, op, n, odev), ctx)
+    return out
+
+
+def mch_macro_solve(ctx, out, G=None, b=None, rtol=1e-12, max_iter=0):
+    """Upscaled system (Eq. 6) into out [N][(M+1)^d]; G, b default to the context's own.
+    Returns the PCG iteration count."""
+    gp = bp = None
+    gdev = 0
+    if G is not None:
+        if isinstance(G, np.ndarray):
+            G = np.ascontiguousarray(G, dtype=np.float64)
+            b = np.ascontiguousarray(b, dtype=np.float64)
+        gp, gdev = _ptr(G)
+        bp, bdev = _ptr(b)
+        if gdev != bdev:
+            raise ValueError("G and b must both be host or both be device buffers")
+    op, odev = _ptr(out)
+    n = out.numel() if hasattr(out, "numel") else out.size
+    it = ctypes.c_int(0)
+    check(lib.mch_macro_solve(ctx, gp, bp, gdev, op, n, odev, rtol, max_iter, ctypes.byref(it)), ctx)
+    return it.value
+
+
 def mch_destroy(ctx):
     lib.mch_destroy(ctx)
 
@@ -127,6 +165,22 @@ class Homogenizer:
         if out is None:
             out = np.zeros((self.num_macropoints, self.n_rhs, self.n_rhs))
         return mch_effective_coeffs(self.ctx, out)
+
+    def set_source(self, f):
+        """NEXT-2: source term for the load vectors (before solve_all)."""
+        mch_set_source(self.ctx, f)
+
+    def load_vectors(self, out=None):
+        if out is None:
+            out = np.zeros((self.num_macropoints, self.N))
+        return mch_load_vectors(self.ctx, out)
+
+    def macro_solve(self, G=None, b=None, out=None, rtol=1e-12, max_iter=0):
+        """U [N][(M+1)^d] of the upscaled system (block layout).  Returns (U, iterations)."""
+        if out is None:
+            out = np.zeros((self.N, (self.M + 1) ** self.d))
+        it = mch_macro_solve(self.ctx, out, G, b, rtol=rtol, max_iter=max_iter)
+        return out, it
 
     def coeffs_device_ptr(self):
         p = ctypes.c_void_p()
@@ -204,5 +258,5 @@ class Homogenizer:
         self.close()
 
 
-__all__ = ["Homogenizer", "mch_create", "mch_set_medium", "mch_solve_level", "mch_effective_coeffs", "mch_destroy",
-           "_native"]
+__all__ = ["Homogenizer", "mch_create", "mch_set_medium", "mch_solve_level", "mch_effective_coeffs",
+           "mch_set_source", "mch_load_vectors", "mch_macro_solve", "mch_destroy", "_native"]

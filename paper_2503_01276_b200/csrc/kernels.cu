@@ -748,6 +748,32 @@ __global__ void k_gram(LevelArgs A) {
     }
     __syncthreads();
   }
+  // load vectors (NEXT-2, Eq. 7 with R_p = K_p): f cellwise constant and
+  // phi_j Q1 on the fine grid, so int_e f phi_j = f_e (h^D / 2^D) sum_{corners} phi_j, exactly
+  if (A.f == nullptr) return;
+  double v[16];
+  for (int i = 0; i < 16; i++) v[i] = 0.0;
+  const int N = A.N;
+  for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+    int e[3] = {lo[0] + idx % ext[0], lo[1] + (idx / ext[0]) % ext[1], lo[2] + idx / (ext[0] * ext[1])};
+    int64_t gl = 0;
+    for (int i = D - 1; i >= 0; i--) gl = gl * A.n + (P.lo[i] + e[i]);
+    const double fe = A.f[gl];
+    for (int j = 0; j < N; j++) {
+      const double* fj = field(j);
+      double s = 0.0;
+      for (int bb = 0; bb < (1 << D); bb++) {
+        int xb[3] = {e[0] + (bb & 1), e[1] + ((bb >> 1) & 1), (D == 3) ? e[2] + ((bb >> 2) & 1) : 0};
+        s += fj[node_id<D>(gf, xb)];
+      }
+      v[j] += fe * s;
+    }
+  }
+  block_sum<16>(v, scratch, tot);
+  if (threadIdx.x == 0) {
+    const double wq = (D == 2) ? A.h * A.h * 0.25 : A.h * A.h * A.h * 0.125;
+    for (int j = 0; j < N; j++) A.bload[P.lin * N + j] = tot[j] * wq;
+  }
 }
 
 // ---------------------------------------------------------------------------------------

@@ -24,3 +24,8 @@ size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw, bool sstc, bool smlr);
 cudaError_t launch_node_ops2d(const LevelArgs& A, int max_nodes, cudaStream_t st);
 cudaError_t launch_pcg2d(const LevelArgs& A, int variant, int threads, cudaStream_t st);
 void pcg2d_phase_dump(const char* tag);  // PCG2D_TIMING builds: per-phase cycle counters
+
+// upscaled system (macro.cu, NEXT-2): one-CTA matrix-free Jacobi-PCG on the coarse vertex grid
+size_t macro_workspace_doubles(int D, int N, int64_t M);
+cudaError_t launch_macro_pcg(int D, int N, int64_t M, const double* G, const double* b, double* U, double* ws,
+                             double rtol, int max_iter, int* iters, double* relres, cudaStream_t st);

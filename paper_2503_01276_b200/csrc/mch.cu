@@ -101,6 +101,11 @@ struct mch_ctx {
   std::vector<std::vector<std::unique_ptr<LevelBatch>>> lplans;  // per level, built on first solve
   int* h_bad = nullptr;  // mch_set_medium validation flag (pinned / device)
   int* d_bad = nullptr;
+  // NEXT-2: source f (cellwise, n^D), load vectors [P][N], macro-solve workspace and results
+  DevBuf fsrc, bload, mws, mG, mb, mU, mres;
+  bool has_source = false;
+  int* h_mit = nullptr;
+  double* h_mrel = nullptr;
   int pcg_mode = 0;  // 0: on-chip 2D PCG where it applies; 1: generic k_pcg; 2: on-chip, precomputed operator at level 1
 };
 
@@ -477,6 +482,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   A.D = D; A.N = N; A.n_rhs = nr; A.l = c->l; A.w = c->w; A.nsub = c->nsub; A.ncon = nc;
   A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.coff = (int)pl.coff(); A.gn = gn; A.h = 1.0 / (double)pl.n; A.inv_c = 1.0f / (float)pl.c;
   A.kappa = c->kappa; A.ids = c->ids; A.pool = c->pool; A.G = c->G;
+  A.f = c->has_source ? c->fsrc.as<double>() : nullptr;
+  A.bload = c->bload.as<double>();
   A.rtol = c->p.rtol; A.max_iter = c->p.max_iter;
   if (level >= 2) {
     const int64_t gcells = (D == 2) ? (int64_t)gn * gn : (int64_t)gn * gn * gn;
@@ -651,6 +658,96 @@ extern "C" int mch_effective_coeffs(mch_ctx* c, double* out, size_t out_len, int
   return MCH_OK;
 }
 
+extern "C" int mch_set_source(mch_ctx* c, const double* f, int on_dev) {
+  if (!c) return MCH_EINVAL;
+  if (c->solved != 0) return fail(c, MCH_EORDER, "set the source before solving level 1 (or after mch_reset)");
+  if (!f) {
+    c->has_source = false;
+    return MCH_OK;
+  }
+  const int64_t n = c->p.n;
+  const int64_t cells = (c->D == 2) ? n * n : n * n * n;
+  if (!on_dev)
+    for (int64_t i = 0; i < cells; i++)
+      if (!std::isfinite(f[i])) return fail(c, MCH_EINVAL, "source must be finite");
+  const size_t nb = c->plan.all.size() * (size_t)c->N;
+  CKC(c, c->fsrc.ensure(cells * sizeof(double)));
+  CKC(c, c->bload.ensure(nb * sizeof(double)));
+  CKC(c, cudaMemcpyAsync(c->fsrc.ptr, f, cells * sizeof(double), on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->st));
+  CKC(c, cudaMemsetAsync(c->bload.ptr, 0, nb * sizeof(double), c->st));
+  CKC(c, cudaStreamSynchronize(c->st));
+  c->has_source = true;
+  return MCH_OK;
+}
+
+extern "C" int mch_load_vectors(mch_ctx* c, double* out, size_t out_len, int out_on_device) {
+  if (!c || !out) return MCH_EINVAL;
+  if (!c->has_source) return fail(c, MCH_EINVAL, "no source set (mch_set_source)");
+  if (c->solved != c->p.levels) return fail(c, MCH_EORDER, "load vectors need all levels solved");
+  const size_t need = c->plan.all.size() * (size_t)c->N;
+  if (out_len < need) return fail(c, MCH_EINVAL, "out_len too small");
+  CKC(c, cudaMemcpyAsync(out, c->bload.ptr, need * sizeof(double),
+                         out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
+  CKC(c, cudaStreamSynchronize(c->st));
+  return MCH_OK;
+}
+
+extern "C" int mch_macro_solve(mch_ctx* c, const double* G, const double* b, int inputs_on_device, double* U,
+                               size_t U_len, int out_on_device, double rtol, int max_iter, int* iters) {
+  if (!c || !U) return MCH_EINVAL;
+  if (c->p.layout != MCH_LAYOUT_BLOCK)
+    return fail(c, MCH_EINVAL, "the macro solve needs the block-centred layout (PAPER.md:199: block midpoints)");
+  const int D = c->D, N = c->N, nr = c->n_rhs;
+  const int64_t M = c->p.M;
+  int64_t nodes = 1;
+  for (int i = 0; i < D; i++) nodes *= M + 1;
+  const size_t P = c->plan.all.size();
+  if (U_len < (size_t)(nodes * N)) return fail(c, MCH_EINVAL, "U_len too small");
+  if ((G == nullptr) != (b == nullptr)) return fail(c, MCH_EINVAL, "pass both G and b, or neither");
+  if (rtol <= 0.0) rtol = 1e-12;
+  if (max_iter <= 0) max_iter = 100000;
+  const double* dG = G;
+  const double* db = b;
+  if (!G) {
+    if (c->p.world > 1) return fail(c, MCH_EINVAL, "world > 1: pass the all-reduced coefficients and loads");
+    if (!c->has_source) return fail(c, MCH_EINVAL, "no source set (mch_set_source)");
+    if (c->solved != c->p.levels) return fail(c, MCH_EORDER, "the macro solve needs all levels solved");
+    dG = c->G;
+    db = c->bload.as<double>();
+  } else if (!inputs_on_device) {
+    CKC(c, c->mG.ensure(P * nr * nr * sizeof(double)));
+    CKC(c, c->mb.ensure(P * N * sizeof(double)));
+    CKC(c, cudaMemcpyAsync(c->mG.ptr, G, P * nr * nr * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CKC(c, cudaMemcpyAsync(c->mb.ptr, b, P * N * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    dG = c->mG.as<double>();
+    db = c->mb.as<double>();
+  }
+  double* dU = U;
+  if (!out_on_device) {
+    CKC(c, c->mU.ensure(nodes * N * sizeof(double)));
+    dU = c->mU.as<double>();
+  }
+  CKC(c, c->mws.ensure(macro_workspace_doubles(D, N, M) * sizeof(double)));
+  CKC(c, c->mres.ensure(2 * sizeof(double)));
+  if (!c->h_mit) CKC(c, cudaMallocHost(&c->h_mit, sizeof(int)));
+  if (!c->h_mrel) CKC(c, cudaMallocHost(&c->h_mrel, sizeof(double)));
+  int* d_it = reinterpret_cast<int*>(c->mres.as<double>() + 1);
+  CKC(c, launch_macro_pcg(D, N, M, dG, db, dU, c->mws.as<double>(), rtol, max_iter, d_it, c->mres.as<double>(), c->st));
+  c->launches += 1;
+  if (!out_on_device)
+    CKC(c, cudaMemcpyAsync(U, dU, nodes * N * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CKC(c, cudaMemcpyAsync(c->h_mit, d_it, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CKC(c, cudaMemcpyAsync(c->h_mrel, c->mres.ptr, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CKC(c, cudaStreamSynchronize(c->st));
+  if (iters) *iters = *c->h_mit;
+  if (!(*c->h_mrel <= rtol)) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "macro PCG: relative residual %.3e after %d iterations", *c->h_mrel, *c->h_mit);
+    return fail(c, MCH_ENOCONV, buf);
+  }
+  return MCH_OK;
+}
+
 extern "C" int mch_num_macropoints(const mch_ctx* c, int level, int64_t* count) {
   if (!c || !count || level < 1 || level > c->p.levels) return MCH_EINVAL;
   *count = (int64_t)c->plan.S[level].size();
@@ -739,9 +836,12 @@ extern "C" void mch_destroy(mch_ctx* c) {
   cudaFree(c->G);
   c->lplans.clear();
   if (c->h_bad) cudaFreeHost(c->h_bad);
+  if (c->h_mit) cudaFreeHost(c->h_mit);
+  if (c->h_mrel) cudaFreeHost(c->h_mrel);
   if (c->d_bad) cudaFree(c->d_bad);
   DevBuf* bufs[] = {&c->STC, &c->MLR, &c->pinv_ds, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
-                    &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres, &c->diag};
+                    &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres, &c->diag,
+                    &c->fsrc, &c->bload, &c->mws, &c->mG, &c->mb, &c->mU, &c->mres};
   for (DevBuf* b : bufs) b->release();
   if (c->events)
     for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);

@@ -58,6 +58,8 @@ struct LevelArgs {
   double* FI; double* FY;  // fine workspace (levels >= 2): I_p / phi and A1 I_p
   double* pool;            // parent pool
   double* G;               // [(M+1)^D][n_rhs][n_rhs]
+  const double* f;         // NEXT-2: cellwise source, n^D, x fastest (NULL: no load vectors)
+  double* bload;           // NEXT-2: [P][N] load vectors b_j = int_{K_p} f phi_j (Eq. 7)
   int* iters; double* relres;  // [problem]
   double* diag;            // [problem][4]: final rz, reference rz, floor, breakdown flag
   double rtol; int max_iter;

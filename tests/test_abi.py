@@ -63,3 +63,16 @@ def test_create_rejects_invalid_inputs(kw, code):
     rc, msg = _create(**kw)
     assert rc == code, (rc, msg)
     assert msg
+
+
+def test_null_context_is_rejected():
+    """Every context call returns MCH_EINVAL for a NULL context without touching the device."""
+    from paper_2503_01276_b200._native import lib
+    buf = np.zeros(16)
+    it = ctypes.c_int(0)
+    assert lib.mch_set_source(None, buf.ctypes.data, 0) == -1
+    assert lib.mch_load_vectors(None, buf.ctypes.data, 16, 0) == -1
+    assert lib.mch_macro_solve(None, None, None, 0, buf.ctypes.data, 16, 0, 1e-12, 0, ctypes.byref(it)) == -1
+    assert lib.mch_solve_level(None, 1) == -1
+    assert lib.mch_effective_coeffs(None, buf.ctypes.data, 16, 0) == -1
+    assert lib.mch_set_medium(None, buf.ctypes.data, buf.ctypes.data, 0) == -1

@@ -253,3 +253,79 @@ def test_block_layout_all_points(d, n, M, L, N):
             po = o.solve(k)["phi"]
             for r in range(o.n_rhs):
                 assert phi_err(h.local_solution(k, r), po[r]) < PHI_TOL
+
+
+def _block_oracle(d, n, M, L, N, seed0):
+    for seed in range(seed0, seed0 + 50):
+        kap, ids = random_medium(d, n, N, seed=seed)
+        try:
+            o = Oracle(d, n, M, L, 2, N, kap, ids, layout="block")
+            for k in o.plan.all_vertices():
+                o.local_system(k)
+            return o, kap, ids
+        except RuntimeError:
+            continue
+    raise AssertionError
+
+
+def _int_abs_f(o, f):
+    """∫_{K_p}|f| per macropoint (the scale of the load-vector bar)"""
+    d, n, c = o.d, o.n, o.plan.c
+    out = np.zeros(o.plan.num_macropoints())
+    fa = np.abs(f)
+    for k in o.plan.all_vertices():
+        sl = tuple(slice(k[i] * c, (k[i] + 1) * c) for i in reversed(range(d)))
+        out[o.plan.linear_index(k)] = fa[sl].sum() / n ** d
+    return out
+
+
+@pytest.mark.parametrize("d,n,M,L,N", [(2, 64, 8, 3, 2), (3, 16, 4, 2, 2)])
+def test_load_vectors_and_macro_solve(d, n, M, L, N):
+    """NEXT-2: b_j = ∫_{K_p} f φ_j (Eq. 7) for the paper's source f vs the oracle,
+    |Δb_j| ≤ 1e-8 ∫_{K_p}|f| (φ_j is bounded by O(1), R15's φ bar is 1e-7 relative); the upscaled
+    system (Eq. 6) solved on the GPU from the oracle's G, b vs the oracle's direct sparse solve,
+    ‖ΔU‖∞ ≤ 1e-8 ‖U‖∞, and end to end from the GPU's own G, b within 1e-6 (the macro system's
+    condition number times the 1e-8 coefficient bar); two solves bitwise equal."""
+    from mch_inputs import paper_source
+    from oracle.macro import load_vectors, macro_solve
+    H = _gpu()
+    o, kap, ids = _block_oracle(d, n, M, L, N, 300 + 10 * d)
+    f = paper_source(d, n, ids, eps=0.05)
+    bo = load_vectors(o, f)
+    Go = o.effective_coeffs()
+    Uo = macro_solve(d, N, M, Go, bo)
+    with H(d, n, N, M, L, 2, kap, ids, layout="block") as h:
+        h.set_source(f)
+        h.solve_all()
+        bg = h.load_vectors()
+        scale = _int_abs_f(o, f)
+        assert np.all(np.abs(bg - bo) <= 1e-8 * scale[:, None]), np.max(np.abs(bg - bo) / scale[:, None])
+        U1, it1 = h.macro_solve(Go.copy(), bo.copy(), rtol=1e-13)
+        assert it1 > 0
+        assert np.abs(U1 - Uo).max() <= 1e-8 * np.abs(Uo).max(), np.abs(U1 - Uo).max() / np.abs(Uo).max()
+        U2, it2 = h.macro_solve(Go.copy(), bo.copy(), rtol=1e-13)
+        assert it2 == it1 and np.array_equal(U1, U2)
+        Ue, _ = h.macro_solve(rtol=1e-13)
+        assert np.abs(Ue - Uo).max() <= 1e-6 * np.abs(Uo).max(), np.abs(Ue - Uo).max() / np.abs(Uo).max()
+
+
+@pytest.mark.parametrize("d,n,M,N", [(2, 128, 64, 2), (3, 32, 16, 2)])
+def test_macro_solve_large_synthetic(d, n, M, N):
+    """NEXT-2 at many blocks per thread: random SPD G_p (N continua coupled) on M^d blocks, GPU PCG
+    vs the oracle's direct sparse solve, ‖ΔU‖∞ ≤ 1e-8 ‖U‖∞ (nodes > threads of the one CTA)."""
+    from oracle.macro import macro_solve
+    H = _gpu()
+    rng = np.random.default_rng(5)
+    nr = N * (1 + d)
+    P = M ** d
+    Hs = 1.0 / M
+    A = rng.normal(size=(P, nr, nr)) * 0.3
+    G = np.einsum("pij,pkj->pik", A, A)
+    G[:, N:, N:] += np.eye(nr - N) * Hs ** d * 2.0
+    b = rng.uniform(0.5, 1.5, size=(P, N)) * Hs ** d
+    Uo = macro_solve(d, N, M, G, b)
+    kap = np.ones((n,) * d)
+    ids = (np.arange(n ** d).reshape((n,) * d) % N).astype(np.uint8)
+    with H(d, n, N, M, 1, 2, kap, ids, layout="block") as h:
+        Ug, it = h.macro_solve(G, b, rtol=1e-13)
+        assert np.abs(Ug - Uo).max() <= 1e-8 * np.abs(Uo).max(), (it, np.abs(Ug - Uo).max() / np.abs(Uo).max())
