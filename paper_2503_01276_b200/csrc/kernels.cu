@@ -200,35 +200,43 @@ __global__ void k_transport(LevelArgs A) {
     A.g[gi] = A.g0[gi] - cI[i];
   }
   __syncthreads();
-  // phase 3: b = -P_n^T Y at level-n nodes
+  // phase 3: b = -P_n^T Y at level-n nodes.  P_n^T is the tensor product of the 1D restrictions
+  // (weights 1 - |d|/s, |d| < s), applied dimension by dimension in place in Y: one thread per
+  // fine row writes its restricted values over the row's head in increasing order (output X only
+  // reads positions >= (X-1)s+1 >= X, so nothing is overwritten before it is read).
   const int s = A.s;
-  double* bvec = A.B + P.vec_off + (int64_t)r * gl.nnodes;
-  for (int K = threadIdx.x; K < gl.nnodes; K += blockDim.x) {
-    int X[3];
-    node_xyz<D>(gl, K, X);
-    int flo[3], fhi[3];
-    for (int i = 0; i < 3; i++) {
-      if (i < D) {
-        flo[i] = X[i] * s - (s - 1);
-        fhi[i] = X[i] * s + (s - 1);
-        if (flo[i] < 0) flo[i] = 0;
-        if (fhi[i] > gf.nn[i] - 1) fhi[i] = gf.nn[i] - 1;
-      } else {
-        flo[i] = fhi[i] = 0;
+  const double inv_s = 1.0 / (double)s;
+  const int nfx = gf.nn[0], nfy = gf.nn[1], nfz = gf.nn[2];
+  const int nlx = gl.nn[0], nly = gl.nn[1], nlz = gl.nn[2];
+  auto restrict1 = [&](double* v, int64_t stride, int nf, int nl, auto&& put) {
+    for (int X = 0; X < nl; X++) {
+      const int c0 = X * s;
+      double acc = v[(int64_t)c0 * stride];
+      for (int d = 1; d < s; d++) {
+        const double w = 1.0 - d * inv_s;
+        if (c0 - d >= 0) acc += w * v[(int64_t)(c0 - d) * stride];
+        if (c0 + d < nf) acc += w * v[(int64_t)(c0 + d) * stride];
       }
+      put(X, acc);
     }
-    double acc = 0.0;
-    for (int z = flo[2]; z <= fhi[2]; z++)
-      for (int y = flo[1]; y <= fhi[1]; y++) {
-        const double wy = 1.0 - fabs((double)(y - X[1] * s)) / s;
-        const double wz = (D == 3) ? 1.0 - fabs((double)(z - X[2] * s)) / s : 1.0;
-        for (int xx = flo[0]; xx <= fhi[0]; xx++) {
-          const double wx = 1.0 - fabs((double)(xx - X[0] * s)) / s;
-          const int xf[3] = {xx, y, z};
-          acc += wx * wy * wz * Y[node_id<D>(gf, xf)];
-        }
-      }
-    bvec[K] = -acc;
+  };
+  __syncthreads();
+  for (int row = threadIdx.x; row < nfy * nfz; row += blockDim.x) {
+    double* v = Y + (int64_t)row * nfx;
+    restrict1(v, 1, nfx, nlx, [&](int X, double a) { v[X] = a; });
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < nfz * nlx; col += blockDim.x) {
+    const int fz = col / nlx, X = col - fz * nlx;
+    double* v = Y + (int64_t)fz * nfy * nfx + X;
+    restrict1(v, nfx, nfy, nly, [&](int Yc, double a) { v[(int64_t)Yc * nfx] = a; });
+  }
+  __syncthreads();
+  double* bvec = A.B + P.vec_off + (int64_t)r * gl.nnodes;
+  for (int col = threadIdx.x; col < nly * nlx; col += blockDim.x) {
+    const int Yc = col / nlx, X = col - Yc * nlx;
+    double* v = Y + (int64_t)Yc * nfx + X;
+    restrict1(v, (int64_t)nfy * nfx, nfz, nlz, [&](int Z, double a) { bvec[((int64_t)Z * nly + Yc) * nlx + X] = -a; });
   }
 }
 
