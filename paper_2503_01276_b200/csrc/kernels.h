@@ -29,3 +29,9 @@ void pcg2d_phase_dump(const char* tag);  // PCG2D_TIMING builds: per-phase cycle
 size_t macro_workspace_doubles(int D, int N, int64_t M);
 cudaError_t launch_macro_pcg(int D, int N, int64_t M, const double* G, const double* b, double* U, double* ws,
                              double rtol, int max_iter, int* iters, double* relres, cudaStream_t st);
+
+// on-chip 3D PCG at levels >= 2 (pcg3d.cu): windows of <= 7 / 13 / 25 level nodes per side
+int pcg3d_nxm(int max_nodes_per_side);
+size_t pcg3d_smem(int N, int nxm);
+cudaError_t launch_node_ops3d(const LevelArgs& A, int max_nodes, cudaStream_t st);
+cudaError_t launch_pcg3d(const LevelArgs& A, int nxm, cudaStream_t st);

@@ -60,6 +60,8 @@ struct LevelBatch {
   std::vector<int> lexpos;  // position of each batch macropoint in the lexicographic list of this rank
   DevBuf descs, segs, nseg;
   bool on2d = false, l1op = false;
+  bool on3d = false;  // on-chip 3D PCG (pcg3d.cu), levels >= 2
+  int nxm3 = 0;
   int variant = -1, threads2 = 0, maxseg = 0, tm_cols = 32;
   int* h_flags = nullptr;  // pinned results
   int* h_iters = nullptr;
@@ -417,6 +419,17 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
         break;
       }
     }
+    // on-chip 3D PCG at levels >= 2 (pcg3d.cu) for windows of <= 25 level nodes per side
+    if (D == 3 && level >= 2 && nc == 27 * N && N <= 4 && c->pcg_mode != 1) {
+      int maxn = 0;
+      for (int i = 0; i < nmp; i++)
+        for (int d = 0; d < 3; d++) maxn = std::max(maxn, descs[i].nc[d] + 1);
+      const int nxm = pcg3d_nxm(maxn);
+      if (nxm > 0 && pcg3d_smem(N, nxm) <= 232448) {
+        B->on3d = true;
+        B->nxm3 = nxm;
+      }
+    }
     // scratch shared by all levels and batches (grow-only, allocated here, never in a solve)
     CKC(c, c->g0.ensure(sizeof(double) * nmp * nc * nr));
     CKC(c, c->g.ensure(sizeof(double) * nmp * nc * nr));
@@ -444,6 +457,10 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     if (B->on2d && !B->l1op) {
       CKC(c, c->STC.ensure(sizeof(double) * 9 * B->node_off));
       CKC(c, c->MLR.ensure(sizeof(double) * 4 * N * B->node_off));
+    }
+    if (B->on3d) {
+      CKC(c, c->STC.ensure(sizeof(double) * 27 * B->node_off));
+      CKC(c, c->MLR.ensure(sizeof(double) * 8 * N * B->node_off));
     }
     CKC(c, cudaMallocHost(&B->h_flags, sizeof(int) * nmp));
     CKC(c, cudaMallocHost(&B->h_iters, sizeof(int) * nmp * nr));
@@ -526,6 +543,10 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       CKC(c, launch_node_ops2d(A, B.max_ln, st));
       S.launches += 1;
     }
+    if (B.on3d) {
+      CKC(c, launch_node_ops3d(A, B.max_ln, st));
+      S.launches += 1;
+    }
     cudaEventRecord(B.ev[1], st);
     double* dbgp = nullptr;
     if (getenv("MCH_PCG_DEBUG") && B.on2d) {  // dev: per-iteration scalars of one problem to stderr
@@ -536,6 +557,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       A.dbg = dbgp;
     }
     if (B.on2d) CKC(c, launch_pcg2d(A, B.variant, B.threads2, st));
+    else if (B.on3d) CKC(c, launch_pcg3d(A, B.nxm3, st));
     else CKC(c, launch_pcg(A, B.th_l, st));
     if (dbgp) {
       std::vector<double> h(8 * A.dbg_cap);

@@ -1,0 +1,531 @@
+// On-chip projected PCG for 3D windows at levels >= 2 (sm_100a) and its per-node setup.
+//
+// Same method as k_pcg (kernels.cu) and k_pcg2d (pcg2d.cu): for each problem (macropoint p,
+// right-hand side r) the correction problem of Eqs. (12)/(13) on the level-n
+// grid, min 1/2 x^T A x - b^T x s.t. C x = g, by projected Jacobi-PCG with the residual
+// re-projected every iteration (readings R16, R19).
+//
+//   p          shared memory, zero halo planes in y and z; x-neighbours by warp shuffles
+//   r, q, x    global memory (L2-resident: <= 125 KB each per problem)
+//   A_n        per-node 27-point stencil rows of A_n = P_n^T A_1 P_n (reading R11), precomputed
+//              per window by k_node_ops3d (streamed from L2, shared by the right-hand sides)
+//   C_n        per-node constraint weights m_{E,j,a} = int_E psi_j N_a merged over the elements
+//              around the node that lie in one subcell, per octant (k_node_ops3d)
+//
+// Thread layout: warp y owns node row y of every plane, lane x its node x (windows of at most
+// NXM <= 25 nodes per side, so a row fits a warp); every thread walks its column in z.  The
+// constraint vector c = C D^-1 r is accumulated per thread for the current subcell layer in z,
+// merged across x by one shuffle, reduced per warp with a segmented scan keyed by the subcell
+// column and written to per-row bins; the bins are summed over rows in a fixed order, so every
+// run gives bitwise identical results.  Five block barriers per iteration.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace {
+
+__device__ __forceinline__ double wsum0(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULLMASK, v, o);
+  return __shfl_sync(FULLMASK, v, 0);
+}
+
+__device__ __forceinline__ int slot3(const LevelArgs& A, const ProbDesc& P, int dim, int e) {
+  return fdiv(P.lo[dim] + e * A.s + A.coff, A.inv_c) - P.k[dim] + A.l;
+}
+
+// The elements on the two sides of a node along one dimension (side 0: cell X-1, side 1: cell X)
+// are grouped by subcell: pm = 3 if both exist in different subcells (keys k0, k1); pm = 1 if
+// they share a subcell or only the lower one exists (all weight stored on side 0, key k0);
+// pm = 2 if only the upper one exists (side 1, key k1).
+struct Sides {
+  int pm, k0, k1;
+};
+__device__ __forceinline__ Sides sides_of(const LevelArgs& A, const ProbDesc& P, int dim, int X, int ncd) {
+  Sides s;
+  const bool lo = X >= 1, up = X < ncd;
+  const int sl = lo ? slot3(A, P, dim, X - 1) : -1, su = up ? slot3(A, P, dim, X) : -1;
+  if (lo && up && sl != su) {
+    s.pm = 3; s.k0 = sl; s.k1 = su;
+  } else if (lo) {
+    s.pm = 1; s.k0 = sl; s.k1 = sl;
+  } else {
+    s.pm = 2; s.k0 = su; s.k1 = su;
+  }
+  return s;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// per-node stencil rows STC[27][nodes] (offset (dx+1) + 3(dy+1) + 9(dz+1)) and octant-merged
+// constraint weights MW[8][N][nodes] (octant o = xs + 2 ys + 4 zs, sides as in Sides) of every
+// window of the batch.  grid (ceil(max nodes / 128), macropoints)
+template <int N>
+__global__ void k_node_ops3d(LevelArgs A) {
+  const int mp = blockIdx.y;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<3> g = level_geo<3>(A, P);
+  const int nn = g.nnodes;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nn) return;
+  int X[3];
+  node_xyz<3>(g, k, X);
+  double st[27];
+  double mw[8][N];
+  for (int i = 0; i < 27; i++) st[i] = 0.0;
+  for (int o = 0; o < 8; o++)
+    for (int j = 0; j < N; j++) mw[o][j] = 0.0;
+  Sides sd[3];
+  for (int i = 0; i < 3; i++) sd[i] = sides_of(A, P, i, X[i], g.nc[i]);
+  for (int o = 0; o < 8; o++) {
+    int e[3];
+    bool ok = true;
+    int t = 0;
+    for (int i = 0; i < 3; i++) {
+      const int ob = (o >> i) & 1;
+      e[i] = X[i] - 1 + ob;
+      ok = ok && e[i] >= 0 && e[i] < g.nc[i];
+      const int tb = (sd[i].pm == 3) ? ob : ((sd[i].pm == 2) ? 1 : 0);
+      t |= tb << i;
+    }
+    if (!ok) continue;
+    double W[DimC<3>::NW];
+    elem_W<3>(A, P, g, e, W);
+    const int a = (~o) & 7;  // corner of the node in element e
+    for (int b = 0; b < 8; b++) {
+      double c[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      c[b] = 1.0;
+      const int dx = e[0] + (b & 1) - X[0], dy = e[1] + ((b >> 1) & 1) - X[1], dz = e[2] + ((b >> 2) & 1) - X[2];
+      st[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)] += elem_row<3>(W, c, a);
+    }
+    for (int j = 0; j < N; j++) mw[t][j] += elem_m<3>(A, P, g, e, j, a);
+  }
+  double* so = A.STC + P.node_off * 27;
+  for (int c = 0; c < 27; c++) so[(int64_t)c * nn + k] = st[c];
+  double* mo = A.MLR + P.node_off * 8 * N;
+  for (int o = 0; o < 8; o++)
+    for (int j = 0; j < N; j++) mo[(int64_t)(o * N + j) * nn + k] = mw[o][j];
+}
+
+// ------------------------------------------------------------------------------------------
+// the solver: one CTA per problem (macropoint, rhs), 32*NXM threads
+template <int N, int NXM, int MINB>
+__global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
+  constexpr int PY = NXM + 2;   // p_s rows per plane (zero halo rows y = -1, ny)
+  constexpr int PZ = PY * NXM;  // p_s plane (x pitch NXM, no x halo: x-neighbours by shuffle)
+  constexpr int NQ = 27 * N;    // constraint rows of a 3x3x3-subcell window
+  const int prob = blockIdx.x;
+  const int mp = prob / A.n_rhs, rhs = prob - mp * A.n_rhs;
+  const ProbDesc& P = A.probs[mp];
+  const int nx = P.nc[0] + 1, ny = P.nc[1] + 1, nz = P.nc[2] + 1, nn = nx * ny * nz;
+  const int ncx = nx - 1;
+  const int nc = A.ncon;  // == NQ (host check)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x = lane, y = warp;
+  const bool wact = y < ny;              // warp-uniform
+  const bool lact = wact && x < nx;
+  const bool xin = x < NXM;
+
+  extern __shared__ __align__(16) double smem[];
+  double* p_s = smem;                  // [NXM+2][PY][NXM], zero halo planes / rows
+  double* bins = p_s + (NXM + 2) * PZ;  // [NXM rows][NQ]
+  double* Ysh = bins + NXM * NQ;        // [NQ] yhat
+  double* csh = Ysh + NQ;               // [NQ] c
+  double* slots = csh + NQ;             // [4][32] scalar partial sums
+  int* zsm = reinterpret_cast<int*>(slots + 4 * 32);  // [NXM][3] z sides (pm, k0, k1)
+
+  for (int i = threadIdx.x; i < (NXM + 2) * PZ; i += blockDim.x) p_s[i] = 0.0;
+  for (int i = threadIdx.x; i < NXM * NQ + 2 * NQ + 4 * 32; i += blockDim.x) bins[i] = 0.0;
+  for (int z = threadIdx.x; z < nz; z += blockDim.x) {
+    const Sides s = sides_of(A, P, 2, z, nz - 1);
+    zsm[z * 3] = s.pm;
+    zsm[z * 3 + 1] = s.k0;
+    zsm[z * 3 + 2] = s.k1;
+  }
+  Sides sx{0, 0, 0}, sy{0, 0, 0};
+  if (lact) sx = sides_of(A, P, 0, x, ncx);
+  if (wact) sy = sides_of(A, P, 1, y, ny - 1);
+  const int kxe = (lact && x < ncx) ? slot3(A, P, 0, x) : 1000;  // subcell column of element x
+  __syncthreads();
+
+  const double* S27 = A.STC + P.node_off * 27;
+  const double* MW = A.MLR + P.node_off * 8 * N;
+  const double* dg = A.dinv + P.node_off;
+  double* Xv = A.X + P.vec_off + (int64_t)rhs * nn;
+  double* Rv = A.R + P.vec_off + (int64_t)rhs * nn;
+  double* Qv = A.Q + P.vec_off + (int64_t)rhs * nn;
+  const double* Si = A.Sinv + (int64_t)mp * nc * nc;
+  const double* gsrc = A.g;  // levels >= 2 only
+  const double* bvec = A.B + P.vec_off + (int64_t)rhs * nn;
+
+  auto nidx = [&](int z) { return (z * ny + y) * nx + x; };
+  auto pidx = [&](int z) { return (z + 1) * PZ + (y + 1) * NXM + x; };
+
+  // (C^T yhat)_k over the present octants
+  auto ct_at = [&](int z, int k) -> double {
+    const int pmz = zsm[z * 3];
+    double ct = 0.0;
+#pragma unroll
+    for (int zs = 0; zs < 2; zs++) {
+      if (!((pmz >> zs) & 1)) continue;
+      const int kz = zsm[z * 3 + 1 + zs];
+#pragma unroll
+      for (int ys = 0; ys < 2; ys++) {
+        if (!((sy.pm >> ys) & 1)) continue;
+        const int ky = ys ? sy.k1 : sy.k0;
+#pragma unroll
+        for (int xs = 0; xs < 2; xs++) {
+          if (!((sx.pm >> xs) & 1)) continue;
+          const int kx = xs ? sx.k1 : sx.k0;
+          const int o = xs + 2 * ys + 4 * zs;
+          const double* yq = Ysh + ((kz * 3 + ky) * 3 + kx) * N;
+#pragma unroll
+          for (int j = 0; j < N; j++) ct += __ldg(MW + (int64_t)(o * N + j) * nn + k) * yq[j];
+        }
+      }
+    }
+    return ct;
+  };
+
+  // constraint accumulation: acc[ys][xs][j] for the current subcell layer in z
+  double acc[2][2][N];
+  auto acc_zero = [&]() {
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int b = 0; b < 2; b++)
+#pragma unroll
+        for (int j = 0; j < N; j++) acc[a][b][j] = 0.0;
+  };
+  auto acc_add = [&](int zs, int k, double u) {
+#pragma unroll
+    for (int ys = 0; ys < 2; ys++) {
+      if (!((sy.pm >> ys) & 1)) continue;
+#pragma unroll
+      for (int xs = 0; xs < 2; xs++) {
+        if (!((sx.pm >> xs) & 1)) continue;
+        const int o = xs + 2 * ys + 4 * zs;
+#pragma unroll
+        for (int j = 0; j < N; j++) acc[ys][xs][j] += __ldg(MW + (int64_t)(o * N + j) * nn + k) * u;
+      }
+    }
+  };
+  // warp-collective (wact warps): layer kz of this row -> bins[y]
+  auto flush = [&](int kz) {
+#pragma unroll
+    for (int ys = 0; ys < 2; ys++) {
+      if (!((sy.pm >> ys) & 1)) continue;  // warp-uniform
+      const int ky = ys ? sy.k1 : sy.k0;
+      double v[N];
+#pragma unroll
+      for (int j = 0; j < N; j++) {
+        const double t = __shfl_down_sync(FULLMASK, acc[ys][0][j], 1);  // element x of lane x+1
+        v[j] = acc[ys][1][j] + ((lane < 31) ? t : 0.0);
+      }
+      const int kup = __shfl_up_sync(FULLMASK, kxe, 1);
+      const unsigned hm = __ballot_sync(FULLMASK, lane == 0 || kxe != kup);
+      const int head = 31 - __clz(hm & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          const double t = __shfl_up_sync(FULLMASK, v[j], d);
+          if (lane - d >= head) v[j] += t;
+        }
+      }
+      const bool tail = (lane == 31) || ((hm >> (lane + 1)) & 1u);
+      if (tail && kxe < 1000) {
+        double* B = bins + y * NQ + ((kz * 3 + ky) * 3 + kxe) * N;
+#pragma unroll
+        for (int j = 0; j < N; j++) B[j] = v[j];
+      }
+    }
+    acc_zero();
+  };
+  // walk the column accumulating u(z, k) into the constraint bins (wact warps)
+  auto sweep_c = [&](auto&& ufun) {
+    acc_zero();
+    int layer = 0;
+    for (int z = 0; z < nz; z++) {
+      const int k = nidx(z);
+      const double u = ufun(z, k);
+      const int pmz = zsm[z * 3];
+      if (pmz == 3) {
+        if (lact) acc_add(0, k, u);
+        flush(zsm[z * 3 + 1]);
+        if (lact) acc_add(1, k, u);
+        layer = zsm[z * 3 + 2];
+      } else {
+        if (lact) acc_add((pmz == 2) ? 1 : 0, k, u);
+        layer = (pmz == 2) ? zsm[z * 3 + 2] : zsm[z * 3 + 1];
+      }
+    }
+    flush(layer);
+  };
+  // (A p)_k from p_s: f(z, k, Ap, p_k)  (wact warps; lanes >= nx carry zeros)
+  auto sweep_stencil = [&](auto&& f) {
+    const double* pb = p_s + (y + 1) * NXM + x;
+    double v[3][3];  // [dy][dz]
+#pragma unroll
+    for (int dy = 0; dy < 3; dy++) {
+      v[dy][0] = xin ? pb[(dy - 1) * NXM] : 0.0;
+      v[dy][1] = xin ? pb[PZ + (dy - 1) * NXM] : 0.0;
+    }
+    for (int z = 0; z < nz; z++) {
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++) v[dy][2] = xin ? pb[(z + 2) * PZ + (dy - 1) * NXM] : 0.0;
+      const int k = nidx(z);
+      double Ap = 0.0;
+#pragma unroll
+      for (int dz = 0; dz < 3; dz++)
+#pragma unroll
+        for (int dy = 0; dy < 3; dy++) {
+          const double c0 = v[dy][dz];
+          double l = __shfl_up_sync(FULLMASK, c0, 1);
+          double r = __shfl_down_sync(FULLMASK, c0, 1);
+          if (lane == 0) l = 0.0;
+          if (lane == 31) r = 0.0;
+          if (lact) {
+            const double* s = S27 + (int64_t)(9 * dz + 3 * dy) * nn + k;
+            Ap += __ldg(s) * l + __ldg(s + nn) * c0 + __ldg(s + 2 * nn) * r;
+          }
+        }
+      f(z, k, Ap, v[1][1]);
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++) {
+        v[dy][0] = v[dy][1];
+        v[dy][1] = v[dy][2];
+      }
+    }
+  };
+
+  auto slot_put = [&](int which, double v) {
+    v = wsum0(v);
+    if (lane == 0) slots[which * 32 + warp] = v;
+  };
+  auto slot_fin = [&](int which) { return wsum0((lane < NXM) ? slots[which * 32 + lane] : 0.0); };
+  // c = sum over rows of the bins (fixed order) into csh; call between barriers
+  auto reduce_c = [&]() {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      double s = 0.0;
+      for (int yy = 0; yy < ny; yy++) s += bins[yy * NQ + i];
+      csh[i] = s;
+    }
+  };
+  // Ysh = S^-1 csh (rows over warps), slots[3] = per-warp partial c.yhat; call between barriers
+  auto solve_y = [&]() {
+    double cyw = 0.0;
+    for (int i = warp; i < nc; i += NXM) {
+      double s = 0.0;
+      for (int j = lane; j < nc; j += 32) s += __ldg(Si + (int64_t)i * nc + j) * csh[j];
+      s = wsum0(s);
+      if (lane == 0) Ysh[i] = s;
+      cyw += s * csh[i];
+    }
+    if (lane == 0) slots[3 * 32 + warp] = cyw;
+  };
+
+  // ---- init: x0 = D^-1 C^T S^-1 t, r0 = A x0 - b, c = C D^-1 r0, yhat = S^-1 c; returns r0^T D^-1 r0
+  auto init = [&](const double* tcol, const double* bb) -> double {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) csh[i] = tcol[((int64_t)mp * nc + i) * A.n_rhs + rhs];
+    __syncthreads();
+    solve_y();
+    __syncthreads();
+    if (lact)
+      for (int z = 0; z < nz; z++) {
+        const int k = nidx(z);
+        const double x0 = dg[k] * ct_at(z, k);
+        p_s[pidx(z)] = x0;
+        Xv[k] = x0;
+      }
+    __syncthreads();
+    if (wact)
+      sweep_stencil([&](int, int k, double Ap, double) {
+        if (lact) Rv[k] = Ap - (bb ? bb[k] : 0.0);
+      });
+    double rr = 0.0;
+    if (wact)
+      sweep_c([&](int, int k) -> double {
+        if (!lact) return 0.0;
+        const double rk = Rv[k];
+        const double u = dg[k] * rk;
+        rr += rk * u;
+        return u;
+      });
+    slot_put(2, rr);
+    __syncthreads();
+    reduce_c();
+    __syncthreads();
+    solve_y();
+    __syncthreads();
+    return slot_fin(2);
+  };
+
+  // reference scale: initial projected residual of the full (non-hierarchical) problem
+  const double rr_ref = init(A.g0, nullptr);
+  double rz_ref;
+  {
+    double v = 0.0;
+    if (lact)
+      for (int z = 0; z < nz; z++) {
+        const int k = nidx(z);
+        const double w = Rv[k] - ct_at(z, k);
+        v += dg[k] * w * w;
+      }
+    slot_put(0, v);
+    __syncthreads();
+    rz_ref = slot_fin(0);
+    __syncthreads();
+  }
+  const double rr0 = init(gsrc, bvec);
+
+  const double tol2 = A.rtol * A.rtol;
+  const double floor2 = 1e-30 * fmax(rr0, rr_ref);
+  double beta = 0.0, rz = 0.0, ref = 0.0, alpha = 0.0;
+  int it = 0, breakdown = 0;
+  for (;; it++) {
+    // pass A: x += alpha_prev p_prev (deferred), r <- r - C^T yhat, z = D^-1 r, p <- -z + beta p
+    double v = 0.0;
+    if (lact) {
+      const bool first = (it == 0);
+      for (int z = 0; z < nz; z++) {
+        const int k = nidx(z);
+        const double rk = Rv[k] - ct_at(z, k);
+        const double zz = dg[k] * rk;
+        double& pk = p_s[pidx(z)];
+        const double pold = pk;
+        if (!first) Xv[k] += alpha * pold;
+        pk = first ? -zz : -zz + beta * pold;
+        Rv[k] = rk;
+        v += rk * zz;
+      }
+    }
+    slot_put(0, v);
+    __syncthreads();  // B1: p complete
+    // pass B: q = A p, pq
+    double w = 0.0;
+    if (wact)
+      sweep_stencil([&](int, int k, double Ap, double pk) {
+        if (lact) {
+          Qv[k] = Ap;
+          w += pk * Ap;
+        }
+      });
+    slot_put(1, w);
+    __syncthreads();  // B2
+    rz = slot_fin(0);
+    const double pq = slot_fin(1);
+    if (it == 0) ref = fmax(rz, rz_ref);
+    if (!(rz > fmax(tol2 * ref, floor2)) || it >= A.max_iter) break;
+    if (!(pq > 0.0) || !isfinite(pq)) {
+      breakdown = 1;
+      break;
+    }
+    alpha = rz / pq;
+    // pass C: r += alpha q, rr = r^T D^-1 r, c = C D^-1 r (per row)
+    double rr = 0.0;
+    if (wact)
+      sweep_c([&](int, int k) -> double {
+        if (!lact) return 0.0;
+        const double rk = Rv[k] + alpha * Qv[k];
+        Rv[k] = rk;
+        const double u = dg[k] * rk;
+        rr += rk * u;
+        return u;
+      });
+    slot_put(2, rr);
+    __syncthreads();  // B3
+    reduce_c();
+    __syncthreads();  // B3b
+    solve_y();
+    __syncthreads();  // B4
+    const double cy = slot_fin(3);
+    beta = (slot_fin(2) - cy) / rz;
+  }
+
+  // feasibility restoration: x += D^-1 C^T S^-1 (g - C x)
+  if (wact) sweep_c([&](int, int k) -> double { return lact ? Xv[k] : 0.0; });
+  __syncthreads();
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    double s = 0.0;
+    for (int yy = 0; yy < ny; yy++) s += bins[yy * NQ + i];
+    csh[i] = gsrc[((int64_t)mp * nc + i) * A.n_rhs + rhs] - s;
+  }
+  __syncthreads();
+  solve_y();
+  __syncthreads();
+  if (lact)
+    for (int z = 0; z < nz; z++) {
+      const int k = nidx(z);
+      Xv[k] += dg[k] * ct_at(z, k);
+    }
+  if (threadIdx.x == 0) {
+    A.iters[prob] = it;
+    A.relres[prob] = (ref > 0.0) ? sqrt(fmax(rz, 0.0) / ref) : 0.0;
+    double* dgo = A.diag + (int64_t)prob * 4;
+    dgo[0] = rz;
+    dgo[1] = ref;
+    dgo[2] = floor2;
+    dgo[3] = breakdown;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+size_t pcg3d_smem(int N, int nxm) {
+  const size_t d = (size_t)(nxm + 2) * (nxm + 2) * nxm + (size_t)nxm * 27 * N + 2 * 27 * N + 4 * 32;
+  return d * sizeof(double) + (size_t)nxm * 3 * sizeof(int);
+}
+
+cudaError_t launch_node_ops3d(const LevelArgs& A, int max_nodes, cudaStream_t st) {
+  dim3 grid((unsigned)((max_nodes + 127) / 128), (unsigned)A.nprob_mp);
+  switch (A.N) {
+    case 1: k_node_ops3d<1><<<grid, 128, 0, st>>>(A); break;
+    case 2: k_node_ops3d<2><<<grid, 128, 0, st>>>(A); break;
+    case 3: k_node_ops3d<3><<<grid, 128, 0, st>>>(A); break;
+    case 4: k_node_ops3d<4><<<grid, 128, 0, st>>>(A); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <int N, int NXM, int MINB>
+static cudaError_t launch3(const LevelArgs& A, cudaStream_t st) {
+  auto k = k_pcg3d<N, NXM, MINB>;
+  const size_t smem = pcg3d_smem(N, NXM);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)A.nprob_mp * A.n_rhs, 32 * NXM, smem, st>>>(A);
+  return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch3n(const LevelArgs& A, int nxm, cudaStream_t st) {
+  switch (nxm) {
+    case 7: return launch3<N, 7, 4>(A, st);
+    case 13: return launch3<N, 13, 2>(A, st);
+    case 25: return launch3<N, 25, 1>(A, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// smallest compiled window width >= nodes per side (0: none)
+int pcg3d_nxm(int max_nodes_per_side) {
+  if (max_nodes_per_side <= 7) return 7;
+  if (max_nodes_per_side <= 13) return 13;
+  if (max_nodes_per_side <= 25) return 25;
+  return 0;
+}
+
+cudaError_t launch_pcg3d(const LevelArgs& A, int nxm, cudaStream_t st) {
+  switch (A.N) {
+    case 1: return launch3n<1>(A, nxm, st);
+    case 2: return launch3n<2>(A, nxm, st);
+    case 3: return launch3n<3>(A, nxm, st);
+    case 4: return launch3n<4>(A, nxm, st);
+  }
+  return cudaErrorInvalidValue;
+}
