@@ -112,9 +112,10 @@ __global__ void k_node_ops3d(LevelArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
-// the solver: one CTA per problem (macropoint, rhs), 32*NXM threads
-template <int N, int NXM, int MINB>
-__global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
+// the solver: one CTA per problem (macropoint, rhs), NW = ceil(NXM / RW) warps of RW rows each
+template <int N, int NXM, int RW, int MINB>
+__global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(LevelArgs A) {
+  constexpr int NW = (NXM + RW - 1) / RW;
   constexpr int PY = NXM + 2;   // p_s rows per plane (zero halo rows y = -1, ny)
   constexpr int PZ = PY * NXM;  // p_s plane (x pitch NXM, no x halo: x-neighbours by shuffle)
   constexpr int NQ = 27 * N;    // constraint rows of a 3x3x3-subcell window
@@ -125,10 +126,11 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
   const int ncx = nx - 1;
   const int nc = A.ncon;  // == NQ (host check)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x = lane, y = warp;
-  const bool wact = y < ny;              // warp-uniform
-  const bool lact = wact && x < nx;
+  const int x = lane;
   const bool xin = x < NXM;
+  // current row of this warp (rows warp, warp + NW, ..): set by set_row
+  int y = warp;
+  bool wact = false, lact = false;  // wact warp-uniform
 
   extern __shared__ __align__(16) double smem[];
   double* p_s = smem;                  // [NXM+2][PY][NXM], zero halo planes / rows
@@ -146,10 +148,20 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
     zsm[z * 3 + 1] = s.k0;
     zsm[z * 3 + 2] = s.k1;
   }
-  Sides sx{0, 0, 0}, sy{0, 0, 0};
-  if (lact) sx = sides_of(A, P, 0, x, ncx);
-  if (wact) sy = sides_of(A, P, 1, y, ny - 1);
-  const int kxe = (lact && x < ncx) ? slot3(A, P, 0, x) : 1000;  // subcell column of element x
+  Sides sx{0, 0, 0}, sy{0, 0, 0}, syr[RW];
+  if (x < nx) sx = sides_of(A, P, 0, x, ncx);
+#pragma unroll
+  for (int ri = 0; ri < RW; ri++) {
+    const int yy = warp + ri * NW;
+    syr[ri] = (yy < ny) ? sides_of(A, P, 1, yy, ny - 1) : Sides{0, 0, 0};
+  }
+  const int kxe = (x < ncx) ? slot3(A, P, 0, x) : 1000;  // subcell column of element x
+  auto set_row = [&](int ri) {
+    y = warp + ri * NW;
+    wact = y < ny;
+    lact = wact && x < nx;
+    sy = syr[ri];
+  };
   __syncthreads();
 
   const double* S27 = A.STC + P.node_off * 27;
@@ -162,6 +174,13 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
   const double* gsrc = A.g;  // levels >= 2 only
   const double* bvec = A.B + P.vec_off + (int64_t)rhs * nn;
 
+  auto rows = [&](auto&& f) {
+#pragma unroll
+    for (int ri = 0; ri < RW; ri++) {
+      set_row(ri);
+      f();
+    }
+  };
   auto nidx = [&](int z) { return (z * ny + y) * nx + x; };
   auto pidx = [&](int z) { return (z + 1) * PZ + (y + 1) * NXM + x; };
 
@@ -279,6 +298,9 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
 #pragma unroll
       for (int dy = 0; dy < 3; dy++) v[dy][2] = xin ? pb[(z + 2) * PZ + (dy - 1) * NXM] : 0.0;
       const int k = nidx(z);
+      double cf[27];  // all 27 coefficient loads in flight before the first use
+#pragma unroll
+      for (int c = 0; c < 27; c++) cf[c] = lact ? __ldg(S27 + (int64_t)c * nn + k) : 0.0;
       double Ap = 0.0;
 #pragma unroll
       for (int dz = 0; dz < 3; dz++)
@@ -289,10 +311,8 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
           double r = __shfl_down_sync(FULLMASK, c0, 1);
           if (lane == 0) l = 0.0;
           if (lane == 31) r = 0.0;
-          if (lact) {
-            const double* s = S27 + (int64_t)(9 * dz + 3 * dy) * nn + k;
-            Ap += __ldg(s) * l + __ldg(s + nn) * c0 + __ldg(s + 2 * nn) * r;
-          }
+          const int cb = 9 * dz + 3 * dy;
+          Ap += cf[cb] * l + cf[cb + 1] * c0 + cf[cb + 2] * r;
         }
       f(z, k, Ap, v[1][1]);
 #pragma unroll
@@ -307,7 +327,7 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
     v = wsum0(v);
     if (lane == 0) slots[which * 32 + warp] = v;
   };
-  auto slot_fin = [&](int which) { return wsum0((lane < NXM) ? slots[which * 32 + lane] : 0.0); };
+  auto slot_fin = [&](int which) { return wsum0((lane < NW) ? slots[which * 32 + lane] : 0.0); };
   // c = sum over rows of the bins (fixed order) into csh; call between barriers
   auto reduce_c = [&]() {
     for (int i = threadIdx.x; i < nc; i += blockDim.x) {
@@ -319,7 +339,7 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
   // Ysh = S^-1 csh (rows over warps), slots[3] = per-warp partial c.yhat; call between barriers
   auto solve_y = [&]() {
     double cyw = 0.0;
-    for (int i = warp; i < nc; i += NXM) {
+    for (int i = warp; i < nc; i += NW) {
       double s = 0.0;
       for (int j = lane; j < nc; j += 32) s += __ldg(Si + (int64_t)i * nc + j) * csh[j];
       s = wsum0(s);
@@ -335,27 +355,33 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
     __syncthreads();
     solve_y();
     __syncthreads();
-    if (lact)
-      for (int z = 0; z < nz; z++) {
-        const int k = nidx(z);
-        const double x0 = dg[k] * ct_at(z, k);
-        p_s[pidx(z)] = x0;
-        Xv[k] = x0;
-      }
+    rows([&] {
+      if (lact)
+        for (int z = 0; z < nz; z++) {
+          const int k = nidx(z);
+          const double x0 = dg[k] * ct_at(z, k);
+          p_s[pidx(z)] = x0;
+          Xv[k] = x0;
+        }
+    });
     __syncthreads();
-    if (wact)
-      sweep_stencil([&](int, int k, double Ap, double) {
-        if (lact) Rv[k] = Ap - (bb ? bb[k] : 0.0);
-      });
+    rows([&] {
+      if (wact)
+        sweep_stencil([&](int, int k, double Ap, double) {
+          if (lact) Rv[k] = Ap - (bb ? bb[k] : 0.0);
+        });
+    });
     double rr = 0.0;
-    if (wact)
-      sweep_c([&](int, int k) -> double {
-        if (!lact) return 0.0;
-        const double rk = Rv[k];
-        const double u = dg[k] * rk;
-        rr += rk * u;
-        return u;
-      });
+    rows([&] {
+      if (wact)
+        sweep_c([&](int, int k) -> double {
+          if (!lact) return 0.0;
+          const double rk = Rv[k];
+          const double u = dg[k] * rk;
+          rr += rk * u;
+          return u;
+        });
+    });
     slot_put(2, rr);
     __syncthreads();
     reduce_c();
@@ -370,12 +396,14 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
   double rz_ref;
   {
     double v = 0.0;
-    if (lact)
-      for (int z = 0; z < nz; z++) {
-        const int k = nidx(z);
-        const double w = Rv[k] - ct_at(z, k);
-        v += dg[k] * w * w;
-      }
+    rows([&] {
+      if (lact)
+        for (int z = 0; z < nz; z++) {
+          const int k = nidx(z);
+          const double w = Rv[k] - ct_at(z, k);
+          v += dg[k] * w * w;
+        }
+    });
     slot_put(0, v);
     __syncthreads();
     rz_ref = slot_fin(0);
@@ -390,7 +418,8 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
   for (;; it++) {
     // pass A: x += alpha_prev p_prev (deferred), r <- r - C^T yhat, z = D^-1 r, p <- -z + beta p
     double v = 0.0;
-    if (lact) {
+    rows([&] {
+      if (!lact) return;
       const bool first = (it == 0);
       for (int z = 0; z < nz; z++) {
         const int k = nidx(z);
@@ -403,18 +432,20 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
         Rv[k] = rk;
         v += rk * zz;
       }
-    }
+    });
     slot_put(0, v);
     __syncthreads();  // B1: p complete
     // pass B: q = A p, pq
     double w = 0.0;
-    if (wact)
-      sweep_stencil([&](int, int k, double Ap, double pk) {
-        if (lact) {
-          Qv[k] = Ap;
-          w += pk * Ap;
-        }
-      });
+    rows([&] {
+      if (wact)
+        sweep_stencil([&](int, int k, double Ap, double pk) {
+          if (lact) {
+            Qv[k] = Ap;
+            w += pk * Ap;
+          }
+        });
+    });
     slot_put(1, w);
     __syncthreads();  // B2
     rz = slot_fin(0);
@@ -428,15 +459,17 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
     alpha = rz / pq;
     // pass C: r += alpha q, rr = r^T D^-1 r, c = C D^-1 r (per row)
     double rr = 0.0;
-    if (wact)
-      sweep_c([&](int, int k) -> double {
-        if (!lact) return 0.0;
-        const double rk = Rv[k] + alpha * Qv[k];
-        Rv[k] = rk;
-        const double u = dg[k] * rk;
-        rr += rk * u;
-        return u;
-      });
+    rows([&] {
+      if (wact)
+        sweep_c([&](int, int k) -> double {
+          if (!lact) return 0.0;
+          const double rk = Rv[k] + alpha * Qv[k];
+          Rv[k] = rk;
+          const double u = dg[k] * rk;
+          rr += rk * u;
+          return u;
+        });
+    });
     slot_put(2, rr);
     __syncthreads();  // B3
     reduce_c();
@@ -448,7 +481,9 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
   }
 
   // feasibility restoration: x += D^-1 C^T S^-1 (g - C x)
-  if (wact) sweep_c([&](int, int k) -> double { return lact ? Xv[k] : 0.0; });
+  rows([&] {
+    if (wact) sweep_c([&](int, int k) -> double { return lact ? Xv[k] : 0.0; });
+  });
   __syncthreads();
   for (int i = threadIdx.x; i < nc; i += blockDim.x) {
     double s = 0.0;
@@ -458,11 +493,13 @@ __global__ void __launch_bounds__(32 * NXM, MINB) k_pcg3d(LevelArgs A) {
   __syncthreads();
   solve_y();
   __syncthreads();
-  if (lact)
-    for (int z = 0; z < nz; z++) {
-      const int k = nidx(z);
-      Xv[k] += dg[k] * ct_at(z, k);
-    }
+  rows([&] {
+    if (lact)
+      for (int z = 0; z < nz; z++) {
+        const int k = nidx(z);
+        Xv[k] += dg[k] * ct_at(z, k);
+      }
+  });
   if (threadIdx.x == 0) {
     A.iters[prob] = it;
     A.relres[prob] = (ref > 0.0) ? sqrt(fmax(rz, 0.0) / ref) : 0.0;
@@ -492,22 +529,22 @@ cudaError_t launch_node_ops3d(const LevelArgs& A, int max_nodes, cudaStream_t st
   return cudaGetLastError();
 }
 
-template <int N, int NXM, int MINB>
+template <int N, int NXM, int RW, int MINB>
 static cudaError_t launch3(const LevelArgs& A, cudaStream_t st) {
-  auto k = k_pcg3d<N, NXM, MINB>;
+  auto k = k_pcg3d<N, NXM, RW, MINB>;
   const size_t smem = pcg3d_smem(N, NXM);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)A.nprob_mp * A.n_rhs, 32 * NXM, smem, st>>>(A);
+  k<<<(unsigned)A.nprob_mp * A.n_rhs, 32 * ((NXM + RW - 1) / RW), smem, st>>>(A);
   return cudaGetLastError();
 }
 
 template <int N>
 static cudaError_t launch3n(const LevelArgs& A, int nxm, cudaStream_t st) {
   switch (nxm) {
-    case 7: return launch3<N, 7, 4>(A, st);
-    case 13: return launch3<N, 13, 2>(A, st);
-    case 25: return launch3<N, 25, 1>(A, st);
+    case 7: return launch3<N, 7, 1, 2>(A, st);
+    case 13: return launch3<N, 13, 2, 2>(A, st);
+    case 25: return launch3<N, 25, 2, 1>(A, st);
   }
   return cudaErrorInvalidValue;
 }

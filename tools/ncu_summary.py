@@ -1,31 +1,31 @@
-"""Summarise an ncu report: key raw metrics per launch and top source lines by stall samples."""
-import collections, csv, io, subprocess, sys
+"""Print the key metrics and stall reasons of the first kernel in an ncu report (dev tool)."""
+import csv
+import subprocess
+import sys
 
 rep = sys.argv[1]
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(raw)))
-h, units = rows[0], rows[1]
-keys = ["Kernel Name", "gpu__time_duration.sum", "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
-        "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
-        "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "smsp__pcsamp_warps_issue_stalled_barrier",
-        "smsp__pcsamp_warps_issue_stalled_wait", "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
-        "smsp__pcsamp_warps_issue_stalled_selected", "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle"]
-idx = {k: h.index(k) for k in keys if k in h}
-for r in rows[2:]:
-    print(" | ".join(f"{k.split('.')[0].replace('smsp__pcsamp_warps_issue_stalled_','stall_')}={r[i]}{units[i] if units[i] not in ('','inst') else ''}" for k, i in idx.items()))
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
-per = collections.Counter(); text = {}; cur = None; last = None
-for r in csv.reader(io.StringIO(src)):
-    if not r: continue
-    if r[0] == "File Path": cur = r[1].split("/")[-1]; continue
-    if r[0] in ("Function Name", "Line No"): continue
-    try: ln = int(r[0]) if r[0] else None
-    except ValueError: ln = None
-    if ln is not None: last = (cur, ln); text[last] = r[1].strip()[:100]
-    try: per[last] += int(r[4])
-    except (ValueError, IndexError): pass
-tot = sum(per.values()) or 1
-print("stall samples", tot)
-for k, v in per.most_common(top): print(f"{100*v/tot:5.1f}% {k[0]}:{k[1]}  {text.get(k,'')}")
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(out.splitlines()))
+h, u, v = rows[0], rows[1], rows[2]
+want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "lts__t_bytes.sum", "l1tex__t_bytes.sum", "launch__registers_per_thread", "launch__grid_size",
+        "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
+        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+        "l1tex__t_sector_hit_rate.pct", "lts__t_sectors_srcunit_tex_op_read.sum"]
+for w in want:
+    if w in h:
+        i = h.index(w)
+        print(f"{w:70s} {v[i]:>20s} {u[i]}")
+st = []
+for i, x in enumerate(h):
+    if x.startswith("smsp__average_warps_issue_stalled_") and x.endswith("_per_issue_active.ratio"):
+        try:
+            st.append((float(v[i]), x.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", "")))
+        except ValueError:
+            pass
+for val, name in sorted(st, reverse=True)[:10]:
+    print(f"  stall {name:30s} {val:.3f}")
