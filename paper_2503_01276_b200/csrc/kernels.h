@@ -35,3 +35,6 @@ int pcg3d_nxm(int max_nodes_per_side);
 size_t pcg3d_smem(int N, int nxm);
 cudaError_t launch_node_ops3d(const LevelArgs& A, int max_nodes, cudaStream_t st);
 cudaError_t launch_pcg3d(const LevelArgs& A, int nxm, cudaStream_t st);
+// level 1 (windows of <= 49 fine nodes per side)
+size_t pcg3d_l1_smem(int N);
+cudaError_t launch_pcg3d_l1(const LevelArgs& A, cudaStream_t st);

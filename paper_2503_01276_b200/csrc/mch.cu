@@ -420,14 +420,20 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       }
     }
     // on-chip 3D PCG at levels >= 2 (pcg3d.cu) for windows of <= 25 level nodes per side
-    if (D == 3 && level >= 2 && nc == 27 * N && N <= 4 && c->pcg_mode != 1) {
+    // and at level 1 (k_pcg3d_l1) for windows of <= 49 fine nodes per side
+    if (D == 3 && nc == 27 * N && N <= 4 && c->pcg_mode != 1) {
       int maxn = 0;
       for (int i = 0; i < nmp; i++)
         for (int d = 0; d < 3; d++) maxn = std::max(maxn, descs[i].nc[d] + 1);
-      const int nxm = pcg3d_nxm(maxn);
-      if (nxm > 0 && pcg3d_smem(N, nxm) <= 232448) {
+      if (level >= 2) {
+        const int nxm = pcg3d_nxm(maxn);
+        if (nxm > 0 && pcg3d_smem(N, nxm) <= 232448) {
+          B->on3d = true;
+          B->nxm3 = nxm;
+        }
+      } else if (maxn <= 49 && pcg3d_l1_smem(N) <= 232448) {
         B->on3d = true;
-        B->nxm3 = nxm;
+        B->nxm3 = 49;
       }
     }
     // scratch shared by all levels and batches (grow-only, allocated here, never in a solve)
@@ -458,7 +464,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       CKC(c, c->STC.ensure(sizeof(double) * 9 * B->node_off));
       CKC(c, c->MLR.ensure(sizeof(double) * 4 * N * B->node_off));
     }
-    if (B->on3d) {
+    if (B->on3d && level >= 2) {
       CKC(c, c->STC.ensure(sizeof(double) * 27 * B->node_off));
       CKC(c, c->MLR.ensure(sizeof(double) * 8 * N * B->node_off));
     }
@@ -543,7 +549,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       CKC(c, launch_node_ops2d(A, B.max_ln, st));
       S.launches += 1;
     }
-    if (B.on3d) {
+    if (B.on3d && level >= 2) {
       CKC(c, launch_node_ops3d(A, B.max_ln, st));
       S.launches += 1;
     }
@@ -557,6 +563,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       A.dbg = dbgp;
     }
     if (B.on2d) CKC(c, launch_pcg2d(A, B.variant, B.threads2, st));
+    else if (B.on3d && level == 1) CKC(c, launch_pcg3d_l1(A, st));
     else if (B.on3d) CKC(c, launch_pcg3d(A, B.nxm3, st));
     else CKC(c, launch_pcg(A, B.th_l, st));
     if (dbgp) {

@@ -512,6 +512,466 @@ __global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(Leve
 }
 
 // ------------------------------------------------------------------------------------------
+// Level 1 (fine grid, windows of <= 49 nodes per side), same method and barriers as k_pcg3d.
+// One CTA of 14 warps per problem; task t = (node row y = t / 2, segment t % 2 of 32 nodes in x),
+// 7 tasks per warp.  p lives in global memory (its three active planes stay in L1); every thread
+// walks its column in z with a sliding 3x3x3 window of p (9 loads per node) and a sliding 2x2x2
+// window of the cells' kappa and ids (4 loads per node).  Operator: the Q1 element rows
+// kappa h/12 (4 p_a - p_{a^3} - p_{a^5} - p_{a^6} - p_{a^7}) summed over the 8 cells;
+// constraint weights m_{E,j,a} = [id_E = j] h^3/8.
+template <int N>
+__global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
+  constexpr int NW = 14, RW = 7, NT = NW * RW;  // 98 row segments = 49 rows x 2
+  constexpr int NQ = 27 * N;
+  const int prob = blockIdx.x;
+  const int mp = prob / A.n_rhs, rhs = prob - mp * A.n_rhs;
+  const ProbDesc& P = A.probs[mp];
+  const int nx = P.nc[0] + 1, ny = P.nc[1] + 1, nz = P.nc[2] + 1, nn = nx * ny * nz;
+  const int ncx = nx - 1, ncy = ny - 1, ncz = nz - 1;
+  const int nc = A.ncon;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = A.n;
+
+  extern __shared__ __align__(16) double smem[];
+  double* bins = smem;          // [NT task rows][NQ]
+  double* Ysh = bins + NT * NQ;  // [NQ]
+  double* csh = Ysh + NQ;        // [NQ]
+  double* slots = csh + NQ;      // [4][32]
+  int* zsm = reinterpret_cast<int*>(slots + 4 * 32);  // [49][3]
+  for (int i = threadIdx.x; i < NT * NQ + 2 * NQ + 4 * 32; i += blockDim.x) bins[i] = 0.0;
+  for (int z = threadIdx.x; z < nz; z += blockDim.x) {
+    const Sides sd = sides_of(A, P, 2, z, ncz);
+    zsm[z * 3] = sd.pm;
+    zsm[z * 3 + 1] = sd.k0;
+    zsm[z * 3 + 2] = sd.k1;
+  }
+  __syncthreads();
+
+  int t = 0, y = 0, seg = 0, x = 0, kxe = 1000;
+  bool wact = false, lact = false;
+  Sides sx{0, 0, 0}, sy{0, 0, 0};
+  const int nxy = nx * ny;
+  const int64_t n2 = (int64_t)A.n * A.n;
+  unsigned pvm = 0;      // bit dy*3+dx: p neighbour (x+dx-1, y+dy-1) inside the window
+  unsigned cvm = 0;      // bit oy*2+ox: cell (x-1+ox, y-1+oy) inside the window
+  int64_t cbase = 0;     // global index of cell (x-1, y-1, -1) of the window
+  auto set_task = [&](int ri) {
+    t = warp + ri * NW;
+    y = t >> 1;
+    seg = t & 1;
+    x = seg * 32 + lane;
+    wact = (y < ny) && (seg * 32 < nx);
+    lact = wact && x < nx;
+    sx = lact ? sides_of(A, P, 0, x, ncx) : Sides{0, 0, 0};
+    sy = wact ? sides_of(A, P, 1, y, ncy) : Sides{0, 0, 0};
+    kxe = (lact && x < ncx) ? slot3(A, P, 0, x) : 1000;
+    pvm = 0;
+    cvm = 0;
+    if (lact) {
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+        for (int dx = 0; dx < 3; dx++) {
+          const int xx = x + dx - 1, yy = y + dy - 1;
+          if (xx >= 0 && xx < nx && yy >= 0 && yy < ny) pvm |= 1u << (dy * 3 + dx);
+        }
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        const int ex = x - 1 + (o & 1), ey = y - 1 + (o >> 1);
+        if (ex >= 0 && ex < ncx && ey >= 0 && ey < ncy) cvm |= 1u << o;
+      }
+    }
+    cbase = ((int64_t)(P.lo[2] - 1) * A.n + (P.lo[1] + y - 1)) * A.n + (P.lo[0] + x - 1);
+  };
+  auto tasks = [&](auto&& f) {
+    for (int ri = 0; ri < RW; ri++) {
+      set_task(ri);
+      f();
+    }
+  };
+
+  const double* dg = A.dinv + P.node_off;
+  double* pv = A.P + P.vec_off + (int64_t)rhs * nn;
+  double* Xv = A.X + P.vec_off + (int64_t)rhs * nn;
+  double* Rv = A.R + P.vec_off + (int64_t)rhs * nn;
+  double* Qv = A.Q + P.vec_off + (int64_t)rhs * nn;
+  const double* Si = A.Sinv + (int64_t)mp * nc * nc;
+  const double hq = 0.125 * A.h * A.h * A.h, kh = A.h * (1.0 / 12.0);
+  auto nidx = [&](int z) { return (z * ny + y) * nx + x; };
+  // fine cell (x-1+ox, y-1+oy, ez) of the window: kappa (0 outside) and id (0xFF outside)
+  auto cell = [&](int ox, int oy, int ez, double& kv, int& id) {
+    kv = 0.0;
+    id = 0xFF;
+    if (((cvm >> (oy * 2 + ox)) & 1u) && ez >= 0 && ez < ncz) {
+      const int64_t f = cbase + (int64_t)(ez + 1) * n2 + oy * n + ox;
+      kv = __ldg(A.kappa + f);
+      id = __ldg(A.ids + f);
+    }
+  };
+  auto cell_id = [&](int ox, int oy, int ez) -> int {
+    if (((cvm >> (oy * 2 + ox)) & 1u) && ez >= 0 && ez < ncz)
+      return __ldg(A.ids + cbase + (int64_t)(ez + 1) * n2 + oy * n + ox);
+    return 0xFF;
+  };
+  auto cell_k = [&](int ox, int oy, int ez) -> double {
+    if (((cvm >> (oy * 2 + ox)) & 1u) && ez >= 0 && ez < ncz)
+      return __ldg(A.kappa + cbase + (int64_t)(ez + 1) * n2 + oy * n + ox);
+    return 0.0;
+  };
+  // subcell key of cell octant o and its target side (group) per dimension
+  auto okey = [&](int o, int z) {
+    const int pmz = zsm[z * 3];
+    const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+    const int kx = ox ? ((sx.pm == 1) ? sx.k0 : sx.k1) : sx.k0;
+    const int ky = oy ? ((sy.pm == 1) ? sy.k0 : sy.k1) : sy.k0;
+    const int kz = oz ? ((pmz == 1) ? zsm[z * 3 + 1] : zsm[z * 3 + 2]) : zsm[z * 3 + 1];
+    return (kz * 3 + ky) * 3 + kx;
+  };
+  auto tside = [](int pm, int ob) { return (pm == 3) ? ob : ((pm == 2) ? 1 : 0); };
+
+  // column walkers over the cell ids: f(z, k, id[8]) with id[o] of cell octant o
+  auto walk_ids = [&](auto&& f) {
+    int idc[8];
+#pragma unroll
+    for (int o = 0; o < 4; o++) idc[o] = 0xFF;
+#pragma unroll
+    for (int o = 0; o < 4; o++) idc[4 + o] = cell_id(o & 1, o >> 1, 0);
+    for (int z = 0; z < nz; z++) {
+      int nxt[4];
+#pragma unroll
+      for (int o = 0; o < 4; o++) nxt[o] = cell_id(o & 1, o >> 1, z + 1);  // prefetch the next plane
+      f(z, nidx(z), idc);
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        idc[o] = idc[4 + o];
+        idc[4 + o] = nxt[o];
+      }
+    }
+  };
+  auto ct_of = [&](int z, const int (&idc)[8]) -> double {
+    double ct = 0.0;
+#pragma unroll
+    for (int o = 0; o < 8; o++)
+      if (idc[o] != 0xFF) ct += Ysh[okey(o, z) * N + idc[o]];
+    return ct * hq;
+  };
+
+  double acc[2][2][N];
+  auto acc_zero = [&]() {
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int b = 0; b < 2; b++)
+#pragma unroll
+        for (int j = 0; j < N; j++) acc[a][b][j] = 0.0;
+  };
+  // add u h^3/8 for the cells whose z side is zsel
+  auto acc_add = [&](int zsel, int z, const int (&idc)[8], double u) {
+    const int pmz = zsm[z * 3];
+    const double w = u * hq;
+#pragma unroll
+    for (int o = 0; o < 8; o++) {
+      if (idc[o] == 0xFF || tside(pmz, o >> 2) != zsel) continue;
+      const int txs = tside(sx.pm, o & 1), tys = tside(sy.pm, (o >> 1) & 1);
+#pragma unroll
+      for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 2; b++)
+#pragma unroll
+          for (int j = 0; j < N; j++)
+            if (a == tys && b == txs && j == idc[o]) acc[a][b][j] += w;
+    }
+  };
+  auto flush = [&](int kz) {
+    double* B = bins + t * NQ;
+#pragma unroll
+    for (int ys = 0; ys < 2; ys++) {
+      if (!((sy.pm >> ys) & 1)) continue;  // warp-uniform
+      const int ky = ys ? sy.k1 : sy.k0;
+      double v[N];
+#pragma unroll
+      for (int j = 0; j < N; j++) {
+        const double tt = __shfl_down_sync(FULLMASK, acc[ys][0][j], 1);
+        v[j] = acc[ys][1][j] + ((lane < 31) ? tt : 0.0);
+      }
+      const int kup = __shfl_up_sync(FULLMASK, kxe, 1);
+      const unsigned hm = __ballot_sync(FULLMASK, lane == 0 || kxe != kup);
+      const int head = 31 - __clz(hm & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          const double tt = __shfl_up_sync(FULLMASK, v[j], d);
+          if (lane - d >= head) v[j] += tt;
+        }
+      }
+      const bool tail = (lane == 31) || ((hm >> (lane + 1)) & 1u);
+      if (tail && kxe < 1000) {
+#pragma unroll
+        for (int j = 0; j < N; j++) B[((kz * 3 + ky) * 3 + kxe) * N + j] += v[j];
+      }
+      __syncwarp();
+      if (lane == 0 && lact && x >= 1) {  // element x-1 belongs to the previous segment's lane 31
+#pragma unroll
+        for (int j = 0; j < N; j++) B[((kz * 3 + ky) * 3 + sx.k0) * N + j] += acc[ys][0][j];
+      }
+      __syncwarp();
+    }
+    acc_zero();
+  };
+  auto sweep_c = [&](auto&& ufun) {
+    for (int i = lane; i < NQ; i += 32) bins[t * NQ + i] = 0.0;
+    __syncwarp();
+    acc_zero();
+    int layer = 0;
+    walk_ids([&](int z, int k, const int (&idc)[8]) {
+      const double u = ufun(z, k);
+      const int pmz = zsm[z * 3];
+      if (pmz == 3) {
+        acc_add(0, z, idc, u);
+        flush(zsm[z * 3 + 1]);
+        acc_add(1, z, idc, u);
+        layer = zsm[z * 3 + 2];
+      } else {
+        acc_add((pmz == 2) ? 1 : 0, z, idc, u);
+        layer = (pmz == 2) ? zsm[z * 3 + 2] : zsm[z * 3 + 1];
+      }
+    });
+    flush(layer);
+  };
+  // (A p)_k: f(z, k, Ap, p_k)
+  auto sweep_stencil = [&](auto&& f) {
+    const double* pc = pv + y * nx + x;
+    auto pl = [&](int dx, int dy, int zz) -> double {  // dx, dy in {-1, 0, 1}
+      return (((pvm >> ((dy + 1) * 3 + dx + 1)) & 1u) && zz >= 0 && zz < nz) ? pc[zz * nxy + dy * nx + dx] : 0.0;
+    };
+    double v[3][3][3];  // [dz][dy][dx]
+    double kc[2][2][2];  // [oz][oy][ox]
+    int idd;
+#pragma unroll
+    for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+      for (int dx = 0; dx < 3; dx++) {
+        v[0][dy][dx] = 0.0;
+        v[1][dy][dx] = pl(dx - 1, dy - 1, 0);
+      }
+#pragma unroll
+    for (int o = 0; o < 4; o++) {
+      kc[0][o >> 1][o & 1] = 0.0;
+      kc[1][o >> 1][o & 1] = cell_k(o & 1, o >> 1, 0);
+    }
+    (void)idd;
+    for (int z = 0; z < nz; z++) {
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+        for (int dx = 0; dx < 3; dx++) v[2][dy][dx] = pl(dx - 1, dy - 1, z + 1);
+      double kn[4];
+#pragma unroll
+      for (int o = 0; o < 4; o++) kn[o] = cell_k(o & 1, o >> 1, z + 1);  // next plane's cells
+      double Ap = 0.0;
+#pragma unroll
+      for (int o = 0; o < 8; o++) {
+        const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+        const int a = (~o) & 7;
+        auto pv_b = [&](int b) {  // p at corner b of cell octant o
+          return v[oz + ((b >> 2) & 1)][oy + ((b >> 1) & 1)][ox + (b & 1)];
+        };
+        Ap += kc[oz][oy][ox] * (4.0 * pv_b(a) - pv_b(a ^ 3) - pv_b(a ^ 5) - pv_b(a ^ 6) - pv_b(a ^ 7));
+      }
+      f(z, nidx(z), Ap * kh, v[1][1][1]);
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+        for (int dx = 0; dx < 3; dx++) {
+          v[0][dy][dx] = v[1][dy][dx];
+          v[1][dy][dx] = v[2][dy][dx];
+        }
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        kc[0][o >> 1][o & 1] = kc[1][o >> 1][o & 1];
+        kc[1][o >> 1][o & 1] = kn[o];
+      }
+    }
+  };
+
+  auto slot_put = [&](int which, double v) {
+    v = wsum0(v);
+    if (lane == 0) slots[which * 32 + warp] = v;
+  };
+  auto slot_fin = [&](int which) { return wsum0((lane < NW) ? slots[which * 32 + lane] : 0.0); };
+  auto reduce_c = [&](const double* sub) {  // csh = (sub ? sub - : ) sum of the task rows
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      double s = 0.0;
+      for (int tt = 0; tt < NT; tt++) s += bins[tt * NQ + i];
+      csh[i] = sub ? sub[((int64_t)mp * nc + i) * A.n_rhs + rhs] - s : s;
+    }
+  };
+  auto solve_y = [&]() {
+    double cyw = 0.0;
+    for (int i = warp; i < nc; i += NW) {
+      double s = 0.0;
+      for (int j = lane; j < nc; j += 32) s += __ldg(Si + (int64_t)i * nc + j) * csh[j];
+      s = wsum0(s);
+      if (lane == 0) Ysh[i] = s;
+      cyw += s * csh[i];
+    }
+    if (lane == 0) slots[3 * 32 + warp] = cyw;
+  };
+
+  // init: x0 = D^-1 C^T S^-1 g0, r0 = A x0, c = C D^-1 r0, yhat = S^-1 c
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) csh[i] = A.g0[((int64_t)mp * nc + i) * A.n_rhs + rhs];
+  __syncthreads();
+  solve_y();
+  __syncthreads();
+  tasks([&] {
+    if (!wact) return;
+    walk_ids([&](int z, int k, const int (&idc)[8]) {
+      if (!lact) return;
+      const double x0 = dg[k] * ct_of(z, idc);
+      pv[k] = x0;
+      Xv[k] = x0;
+    });
+  });
+  __syncthreads();
+  tasks([&] {
+    if (wact) sweep_stencil([&](int, int k, double Ap, double) { if (lact) Rv[k] = Ap; });
+  });
+  double rr0 = 0.0;
+  tasks([&] {
+    if (wact)
+      sweep_c([&](int, int k) -> double {
+        if (!lact) return 0.0;
+        const double rk = Rv[k];
+        const double u = dg[k] * rk;
+        rr0 += rk * u;
+        return u;
+      });
+  });
+  slot_put(2, rr0);
+  __syncthreads();
+  reduce_c(nullptr);
+  __syncthreads();
+  solve_y();
+  __syncthreads();
+  rr0 = slot_fin(2);
+
+  const double tol2 = A.rtol * A.rtol;
+  const double floor2 = 1e-30 * rr0;
+  double beta = 0.0, rz = 0.0, ref = 0.0, alpha = 0.0;
+  int it = 0, breakdown = 0;
+  for (;; it++) {
+    double v = 0.0;
+    const bool first = (it == 0);
+    tasks([&] {
+      if (!wact) return;
+      walk_ids([&](int z, int k, const int (&idc)[8]) {
+        if (!lact) return;
+        const double rk = Rv[k] - ct_of(z, idc);
+        const double zz = dg[k] * rk;
+        const double pold = pv[k];
+        if (!first) Xv[k] += alpha * pold;
+        pv[k] = first ? -zz : -zz + beta * pold;
+        Rv[k] = rk;
+        v += rk * zz;
+      });
+    });
+    slot_put(0, v);
+    __syncthreads();  // B1
+    double w = 0.0;
+    tasks([&] {
+      if (wact)
+        sweep_stencil([&](int, int k, double Ap, double pk) {
+          if (lact) {
+            Qv[k] = Ap;
+            w += pk * Ap;
+          }
+        });
+    });
+    slot_put(1, w);
+    __syncthreads();  // B2
+    rz = slot_fin(0);
+    const double pq = slot_fin(1);
+    if (it == 0) ref = rz;
+    if (!(rz > fmax(tol2 * ref, floor2)) || it >= A.max_iter) break;
+    if (!(pq > 0.0) || !isfinite(pq)) {
+      breakdown = 1;
+      break;
+    }
+    alpha = rz / pq;
+    double rr = 0.0;
+    tasks([&] {
+      if (wact)
+        sweep_c([&](int, int k) -> double {
+          if (!lact) return 0.0;
+          const double rk = Rv[k] + alpha * Qv[k];
+          Rv[k] = rk;
+          const double u = dg[k] * rk;
+          rr += rk * u;
+          return u;
+        });
+    });
+    slot_put(2, rr);
+    __syncthreads();  // B3
+    reduce_c(nullptr);
+    __syncthreads();
+    solve_y();
+    __syncthreads();  // B4
+    beta = (slot_fin(2) - slot_fin(3)) / rz;
+  }
+
+  // feasibility restoration: x += D^-1 C^T S^-1 (g - C x); parents also into the pool
+  tasks([&] {
+    if (wact) sweep_c([&](int, int k) -> double { return lact ? Xv[k] : 0.0; });
+  });
+  __syncthreads();
+  reduce_c(A.g0);
+  __syncthreads();
+  solve_y();
+  __syncthreads();
+  double* po = (P.pool_off >= 0) ? A.pool + P.pool_off + (int64_t)rhs * nn : nullptr;
+  tasks([&] {
+    if (!wact) return;
+    walk_ids([&](int z, int k, const int (&idc)[8]) {
+      if (!lact) return;
+      const double xf = Xv[k] + dg[k] * ct_of(z, idc);
+      Xv[k] = xf;
+      if (po) po[k] = xf;
+    });
+  });
+  if (threadIdx.x == 0) {
+    A.iters[prob] = it;
+    A.relres[prob] = (ref > 0.0) ? sqrt(fmax(rz, 0.0) / ref) : 0.0;
+    double* dgo = A.diag + (int64_t)prob * 4;
+    dgo[0] = rz;
+    dgo[1] = ref;
+    dgo[2] = floor2;
+    dgo[3] = breakdown;
+  }
+}
+
+size_t pcg3d_l1_smem(int N) {
+  return (size_t)(98 * 27 * N + 2 * 27 * N + 4 * 32) * sizeof(double) + 49 * 3 * sizeof(int);
+}
+
+cudaError_t launch_pcg3d_l1(const LevelArgs& A, cudaStream_t st) {
+  const size_t smem = pcg3d_l1_smem(A.N);
+  auto go = [&](auto k) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)A.nprob_mp * A.n_rhs, 448, smem, st>>>(A);
+    return cudaGetLastError();
+  };
+  switch (A.N) {
+    case 1: return go(k_pcg3d_l1<1>);
+    case 2: return go(k_pcg3d_l1<2>);
+    case 3: return go(k_pcg3d_l1<3>);
+    case 4: return go(k_pcg3d_l1<4>);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------------------------------
 size_t pcg3d_smem(int N, int nxm) {
   const size_t d = (size_t)(nxm + 2) * (nxm + 2) * nxm + (size_t)nxm * 27 * N + 2 * 27 * N + 4 * 32;
   return d * sizeof(double) + (size_t)nxm * 3 * sizeof(int);
