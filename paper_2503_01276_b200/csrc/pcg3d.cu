@@ -329,11 +329,12 @@ __global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(Leve
   };
   auto slot_fin = [&](int which) { return wsum0((lane < NW) ? slots[which * 32 + lane] : 0.0); };
   // c = sum over rows of the bins (fixed order) into csh; call between barriers
-  auto reduce_c = [&]() {
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+  auto reduce_c = [&]() {  // one warp per constraint row, fixed tree over the row bins
+    for (int i = warp; i < nc; i += NW) {
       double s = 0.0;
-      for (int yy = 0; yy < ny; yy++) s += bins[yy * NQ + i];
-      csh[i] = s;
+      for (int yy = lane; yy < ny; yy += 32) s += bins[yy * NQ + i];
+      s = wsum0(s);
+      if (lane == 0) csh[i] = s;
     }
   };
   // Ysh = S^-1 csh (rows over warps), slots[3] = per-warp partial c.yhat; call between barriers
@@ -555,6 +556,19 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
   unsigned pvm = 0;      // bit dy*3+dx: p neighbour (x+dx-1, y+dy-1) inside the window
   unsigned cvm = 0;      // bit oy*2+ox: cell (x-1+ox, y-1+oy) inside the window
   int64_t cbase = 0;     // global index of cell (x-1, y-1, -1) of the window
+  auto tside = [](int pm, int ob) { return (pm == 3) ? ob : ((pm == 2) ? 1 : 0); };
+  // subcell of the cell in xy-octant oxy = ox + 2 oy: ky * 3 + kx (per task)
+  auto kxy = [&](int oxy) {
+    const int ox = oxy & 1, oy = oxy >> 1;
+    const int kx = ox ? ((sx.pm == 1) ? sx.k0 : sx.k1) : sx.k0;
+    const int ky = oy ? ((sy.pm == 1) ? sy.k0 : sy.k1) : sy.k0;
+    return ky * 3 + kx;
+  };
+  int kq[4];  // kxy per xy-octant of the current task (set by prep_keys)
+  auto prep_keys = [&]() {
+#pragma unroll
+    for (int o = 0; o < 4; o++) kq[o] = kxy(o);
+  };
   auto set_task = [&](int ri) {
     t = warp + ri * NW;
     y = t >> 1;
@@ -582,6 +596,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
       }
     }
     cbase = ((int64_t)(P.lo[2] - 1) * A.n + (P.lo[1] + y - 1)) * A.n + (P.lo[0] + x - 1);
+    prep_keys();
   };
   auto tasks = [&](auto&& f) {
     for (int ri = 0; ri < RW; ri++) {
@@ -618,16 +633,6 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
       return __ldg(A.kappa + cbase + (int64_t)(ez + 1) * n2 + oy * n + ox);
     return 0.0;
   };
-  // subcell key of cell octant o and its target side (group) per dimension
-  auto okey = [&](int o, int z) {
-    const int pmz = zsm[z * 3];
-    const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-    const int kx = ox ? ((sx.pm == 1) ? sx.k0 : sx.k1) : sx.k0;
-    const int ky = oy ? ((sy.pm == 1) ? sy.k0 : sy.k1) : sy.k0;
-    const int kz = oz ? ((pmz == 1) ? zsm[z * 3 + 1] : zsm[z * 3 + 2]) : zsm[z * 3 + 1];
-    return (kz * 3 + ky) * 3 + kx;
-  };
-  auto tside = [](int pm, int ob) { return (pm == 3) ? ob : ((pm == 2) ? 1 : 0); };
 
   // column walkers over the cell ids: f(z, k, id[8]) with id[o] of cell octant o
   auto walk_ids = [&](auto&& f) {
@@ -649,37 +654,36 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
     }
   };
   auto ct_of = [&](int z, const int (&idc)[8]) -> double {
+    const int pmz = zsm[z * 3];
+    const int kz0 = zsm[z * 3 + 1] * 9, kz1 = ((pmz == 1) ? zsm[z * 3 + 1] : zsm[z * 3 + 2]) * 9;
     double ct = 0.0;
 #pragma unroll
     for (int o = 0; o < 8; o++)
-      if (idc[o] != 0xFF) ct += Ysh[okey(o, z) * N + idc[o]];
+      if (idc[o] != 0xFF) ct += Ysh[(((o >> 2) ? kz1 : kz0) + kq[o & 3]) * N + idc[o]];
     return ct * hq;
   };
 
-  double acc[2][2][N];
+  // constraint accumulation for the current subcell layer in z, per xy-octant of the cells
+  double acc[4][N];
   auto acc_zero = [&]() {
 #pragma unroll
-    for (int a = 0; a < 2; a++)
+    for (int a = 0; a < 4; a++)
 #pragma unroll
-      for (int b = 0; b < 2; b++)
-#pragma unroll
-        for (int j = 0; j < N; j++) acc[a][b][j] = 0.0;
+      for (int j = 0; j < N; j++) acc[a][j] = 0.0;
   };
   // add u h^3/8 for the cells whose z side is zsel
   auto acc_add = [&](int zsel, int z, const int (&idc)[8], double u) {
     const int pmz = zsm[z * 3];
     const double w = u * hq;
 #pragma unroll
-    for (int o = 0; o < 8; o++) {
-      if (idc[o] == 0xFF || tside(pmz, o >> 2) != zsel) continue;
-      const int txs = tside(sx.pm, o & 1), tys = tside(sy.pm, (o >> 1) & 1);
+    for (int oz = 0; oz < 2; oz++) {
+      if (tside(pmz, oz) != zsel) continue;  // uniform per plane
 #pragma unroll
-      for (int a = 0; a < 2; a++)
+      for (int oxy = 0; oxy < 4; oxy++) {
+        const int id = idc[oz * 4 + oxy];
 #pragma unroll
-        for (int b = 0; b < 2; b++)
-#pragma unroll
-          for (int j = 0; j < N; j++)
-            if (a == tys && b == txs && j == idc[o]) acc[a][b][j] += w;
+        for (int j = 0; j < N; j++) acc[oxy][j] += (id == j) ? w : 0.0;
+      }
     }
   };
   auto flush = [&](int kz) {
@@ -688,11 +692,22 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
     for (int ys = 0; ys < 2; ys++) {
       if (!((sy.pm >> ys) & 1)) continue;  // warp-uniform
       const int ky = ys ? sy.k1 : sy.k0;
+      double g[2][N];  // side groups xs of this ys
+#pragma unroll
+      for (int xs = 0; xs < 2; xs++)
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          double a = 0.0;
+#pragma unroll
+          for (int oxy = 0; oxy < 4; oxy++)
+            if (tside(sy.pm, oxy >> 1) == ys && tside(sx.pm, oxy & 1) == xs) a += acc[oxy][j];
+          g[xs][j] = a;
+        }
       double v[N];
 #pragma unroll
       for (int j = 0; j < N; j++) {
-        const double tt = __shfl_down_sync(FULLMASK, acc[ys][0][j], 1);
-        v[j] = acc[ys][1][j] + ((lane < 31) ? tt : 0.0);
+        const double tt = __shfl_down_sync(FULLMASK, g[0][j], 1);
+        v[j] = g[1][j] + ((lane < 31) ? tt : 0.0);
       }
       const int kup = __shfl_up_sync(FULLMASK, kxe, 1);
       const unsigned hm = __ballot_sync(FULLMASK, lane == 0 || kxe != kup);
@@ -713,7 +728,7 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
       __syncwarp();
       if (lane == 0 && lact && x >= 1) {  // element x-1 belongs to the previous segment's lane 31
 #pragma unroll
-        for (int j = 0; j < N; j++) B[((kz * 3 + ky) * 3 + sx.k0) * N + j] += acc[ys][0][j];
+        for (int j = 0; j < N; j++) B[((kz * 3 + ky) * 3 + sx.k0) * N + j] += g[0][j];
       }
       __syncwarp();
     }
@@ -800,11 +815,12 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
     if (lane == 0) slots[which * 32 + warp] = v;
   };
   auto slot_fin = [&](int which) { return wsum0((lane < NW) ? slots[which * 32 + lane] : 0.0); };
-  auto reduce_c = [&](const double* sub) {  // csh = (sub ? sub - : ) sum of the task rows
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+  auto reduce_c = [&](const double* sub) {  // csh = [sub -] sum of the task rows (one warp per row)
+    for (int i = warp; i < nc; i += NW) {
       double s = 0.0;
-      for (int tt = 0; tt < NT; tt++) s += bins[tt * NQ + i];
-      csh[i] = sub ? sub[((int64_t)mp * nc + i) * A.n_rhs + rhs] - s : s;
+      for (int tt = lane; tt < NT; tt += 32) s += bins[tt * NQ + i];
+      s = wsum0(s);
+      if (lane == 0) csh[i] = sub ? sub[((int64_t)mp * nc + i) * A.n_rhs + rhs] - s : s;
     }
   };
   auto solve_y = [&]() {
