@@ -514,15 +514,15 @@ __global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(Leve
 
 // ------------------------------------------------------------------------------------------
 // Level 1 (fine grid, windows of <= 49 nodes per side), same method and barriers as k_pcg3d.
-// One CTA of 14 warps per problem; task t = (node row y = t / 2, segment t % 2 of 32 nodes in x),
-// 7 tasks per warp.  p lives in global memory (its three active planes stay in L1); every thread
+// One CTA of NW = 14 or 7 warps per problem; task t = (node row y = t / 2, segment t % 2 of 32 nodes
+// in x), 98 / NW tasks per warp.  p lives in global memory (its three active planes stay in L1); every thread
 // walks its column in z with a sliding 3x3x3 window of p (9 loads per node) and a sliding 2x2x2
 // window of the cells' kappa and ids (4 loads per node).  Operator: the Q1 element rows
 // kappa h/12 (4 p_a - p_{a^3} - p_{a^5} - p_{a^6} - p_{a^7}) summed over the 8 cells;
 // constraint weights m_{E,j,a} = [id_E = j] h^3/8.
-template <int N>
-__global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
-  constexpr int NW = 14, RW = 7, NT = NW * RW;  // 98 row segments = 49 rows x 2
+template <int N, int NW>
+__global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs A) {
+  constexpr int NT = 98, RW = NT / NW;  // 98 row segments = 49 rows x 2
   constexpr int NQ = 27 * N;
   const int prob = blockIdx.x;
   const int mp = prob / A.n_rhs, rhs = prob - mp * A.n_rhs;
@@ -614,38 +614,26 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
   const double hq = 0.125 * A.h * A.h * A.h, kh = A.h * (1.0 / 12.0);
   auto nidx = [&](int z) { return (z * ny + y) * nx + x; };
   // fine cell (x-1+ox, y-1+oy, ez) of the window: kappa (0 outside) and id (0xFF outside)
-  auto cell = [&](int ox, int oy, int ez, double& kv, int& id) {
-    kv = 0.0;
-    id = 0xFF;
-    if (((cvm >> (oy * 2 + ox)) & 1u) && ez >= 0 && ez < ncz) {
-      const int64_t f = cbase + (int64_t)(ez + 1) * n2 + oy * n + ox;
-      kv = __ldg(A.kappa + f);
-      id = __ldg(A.ids + f);
-    }
-  };
-  auto cell_id = [&](int ox, int oy, int ez) -> int {
-    if (((cvm >> (oy * 2 + ox)) & 1u) && ez >= 0 && ez < ncz)
-      return __ldg(A.ids + cbase + (int64_t)(ez + 1) * n2 + oy * n + ox);
-    return 0xFF;
-  };
-  auto cell_k = [&](int ox, int oy, int ez) -> double {
-    if (((cvm >> (oy * 2 + ox)) & 1u) && ez >= 0 && ez < ncz)
-      return __ldg(A.kappa + cbase + (int64_t)(ez + 1) * n2 + oy * n + ox);
-    return 0.0;
-  };
 
   // column walkers over the cell ids: f(z, k, id[8]) with id[o] of cell octant o
   auto walk_ids = [&](auto&& f) {
     int idc[8];
+    const uint8_t* ip = A.ids + cbase + n2;  // cell (x-1, y-1) of cell plane 0
+    const int oxy[4] = {0, 1, (int)A.n, (int)A.n + 1};
 #pragma unroll
-    for (int o = 0; o < 4; o++) idc[o] = 0xFF;
-#pragma unroll
-    for (int o = 0; o < 4; o++) idc[4 + o] = cell_id(o & 1, o >> 1, 0);
+    for (int o = 0; o < 4; o++) {
+      idc[o] = 0xFF;
+      idc[4 + o] = (((cvm >> o) & 1u) && ncz > 0) ? __ldg(ip + oxy[o]) : 0xFF;
+    }
+    int k = y * nx + x;
     for (int z = 0; z < nz; z++) {
+      ip += n2;
+      const bool nv = z + 1 < ncz;
       int nxt[4];
 #pragma unroll
-      for (int o = 0; o < 4; o++) nxt[o] = cell_id(o & 1, o >> 1, z + 1);  // prefetch the next plane
-      f(z, nidx(z), idc);
+      for (int o = 0; o < 4; o++) nxt[o] = (((cvm >> o) & 1u) && nv) ? __ldg(ip + oxy[o]) : 0xFF;  // next plane
+      f(z, k, idc);
+      k += nxy;
 #pragma unroll
       for (int o = 0; o < 4; o++) {
         idc[o] = idc[4 + o];
@@ -756,34 +744,41 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
   };
   // (A p)_k: f(z, k, Ap, p_k)
   auto sweep_stencil = [&](auto&& f) {
-    const double* pc = pv + y * nx + x;
-    auto pl = [&](int dx, int dy, int zz) -> double {  // dx, dy in {-1, 0, 1}
-      return (((pvm >> ((dy + 1) * 3 + dx + 1)) & 1u) && zz >= 0 && zz < nz) ? pc[zz * nxy + dy * nx + dx] : 0.0;
-    };
-    double v[3][3][3];  // [dz][dy][dx]
+    const double* pz = pv + y * nx + x;               // node (x, y) of plane z
+    const double* kp = A.kappa + cbase + n2;          // cell (x-1, y-1) of cell plane z
+    const int oxy[4] = {0, 1, (int)A.n, (int)A.n + 1};
+    int poff[9];
+#pragma unroll
+    for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+      for (int dx = 0; dx < 3; dx++) poff[dy * 3 + dx] = (dy - 1) * nx + (dx - 1);
+    double v[3][3][3];   // [dz][dy][dx]
     double kc[2][2][2];  // [oz][oy][ox]
-    int idd;
 #pragma unroll
     for (int dy = 0; dy < 3; dy++)
 #pragma unroll
       for (int dx = 0; dx < 3; dx++) {
         v[0][dy][dx] = 0.0;
-        v[1][dy][dx] = pl(dx - 1, dy - 1, 0);
+        v[1][dy][dx] = ((pvm >> (dy * 3 + dx)) & 1u) ? pz[poff[dy * 3 + dx]] : 0.0;
       }
 #pragma unroll
     for (int o = 0; o < 4; o++) {
       kc[0][o >> 1][o & 1] = 0.0;
-      kc[1][o >> 1][o & 1] = cell_k(o & 1, o >> 1, 0);
+      kc[1][o >> 1][o & 1] = (((cvm >> o) & 1u) && ncz > 0) ? __ldg(kp + oxy[o]) : 0.0;
     }
-    (void)idd;
+    int k = y * nx + x;
     for (int z = 0; z < nz; z++) {
+      pz += nxy;
+      kp += n2;
+      const bool pn = z + 1 < nz, cn = z + 1 < ncz;
 #pragma unroll
       for (int dy = 0; dy < 3; dy++)
 #pragma unroll
-        for (int dx = 0; dx < 3; dx++) v[2][dy][dx] = pl(dx - 1, dy - 1, z + 1);
+        for (int dx = 0; dx < 3; dx++)
+          v[2][dy][dx] = (((pvm >> (dy * 3 + dx)) & 1u) && pn) ? pz[poff[dy * 3 + dx]] : 0.0;
       double kn[4];
 #pragma unroll
-      for (int o = 0; o < 4; o++) kn[o] = cell_k(o & 1, o >> 1, z + 1);  // next plane's cells
+      for (int o = 0; o < 4; o++) kn[o] = (((cvm >> o) & 1u) && cn) ? __ldg(kp + oxy[o]) : 0.0;  // next cells
       double Ap = 0.0;
 #pragma unroll
       for (int o = 0; o < 8; o++) {
@@ -794,7 +789,8 @@ __global__ void __launch_bounds__(448, 1) k_pcg3d_l1(LevelArgs A) {
         };
         Ap += kc[oz][oy][ox] * (4.0 * pv_b(a) - pv_b(a ^ 3) - pv_b(a ^ 5) - pv_b(a ^ 6) - pv_b(a ^ 7));
       }
-      f(z, nidx(z), Ap * kh, v[1][1][1]);
+      f(z, k, Ap * kh, v[1][1][1]);
+      k += nxy;
 #pragma unroll
       for (int dy = 0; dy < 3; dy++)
 #pragma unroll
@@ -970,19 +966,30 @@ size_t pcg3d_l1_smem(int N) {
   return (size_t)(98 * 27 * N + 2 * 27 * N + 4 * 32) * sizeof(double) + 49 * 3 * sizeof(int);
 }
 
+// 14 warps (one CTA per SM) when the launch is at most a few waves, else 7 warps (two CTAs per SM:
+// measured 12% faster on the 1000 problems of config 4, but 1.8x slower on the 216 of config 5)
 cudaError_t launch_pcg3d_l1(const LevelArgs& A, cudaStream_t st) {
   const size_t smem = pcg3d_l1_smem(A.N);
-  auto go = [&](auto k) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int probs = A.nprob_mp * A.n_rhs;
+  const bool wide = probs >= 4 * sms;
+  auto go = [&](auto k, int nw) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k<<<(unsigned)A.nprob_mp * A.n_rhs, 448, smem, st>>>(A);
+    k<<<(unsigned)probs, nw * 32, smem, st>>>(A);
     return cudaGetLastError();
   };
   switch (A.N) {
-    case 1: return go(k_pcg3d_l1<1>);
-    case 2: return go(k_pcg3d_l1<2>);
-    case 3: return go(k_pcg3d_l1<3>);
-    case 4: return go(k_pcg3d_l1<4>);
+    case 1: return wide ? go(k_pcg3d_l1<1, 7>, 7) : go(k_pcg3d_l1<1, 14>, 14);
+    case 2: return wide ? go(k_pcg3d_l1<2, 7>, 7) : go(k_pcg3d_l1<2, 14>, 14);
+    case 3: return wide ? go(k_pcg3d_l1<3, 7>, 7) : go(k_pcg3d_l1<3, 14>, 14);
+    case 4: return wide ? go(k_pcg3d_l1<4, 7>, 7) : go(k_pcg3d_l1<4, 14>, 14);
   }
   return cudaErrorInvalidValue;
 }
