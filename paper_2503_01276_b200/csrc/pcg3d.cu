@@ -112,10 +112,16 @@ __global__ void k_node_ops3d(LevelArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
-// the solver: one CTA per problem (macropoint, rhs), NW = ceil(NXM / RW) warps of RW rows each
+// the solver: one CTA per problem (macropoint, rhs).  A row of the window occupies LPR lanes
+// (32, 16 or 8: the smallest that holds NXM nodes), so a warp carries RPW = 32 / LPR rows at a
+// time; NW warps, RW rounds of rows each.
 template <int N, int NXM, int RW, int MINB>
-__global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(LevelArgs A) {
-  constexpr int NW = (NXM + RW - 1) / RW;
+__global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 8) ? 16 : 8))) * RW - 1) /
+                                        ((32 / ((NXM > 16) ? 32 : ((NXM > 8) ? 16 : 8))) * RW)),
+                                  MINB) k_pcg3d(LevelArgs A) {
+  constexpr int LPR = (NXM > 16) ? 32 : ((NXM > 8) ? 16 : 8);  // lanes per row
+  constexpr int RPW = 32 / LPR;                                 // rows per warp and round
+  constexpr int NW = (NXM + RPW * RW - 1) / (RPW * RW);
   constexpr int PY = NXM + 2;   // p_s rows per plane (zero halo rows y = -1, ny)
   constexpr int PZ = PY * NXM;  // p_s plane (x pitch NXM, no x halo: x-neighbours by shuffle)
   constexpr int NQ = 27 * N;    // constraint rows of a 3x3x3-subcell window
@@ -126,11 +132,11 @@ __global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(Leve
   const int ncx = nx - 1;
   const int nc = A.ncon;  // == NQ (host check)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int x = lane;
+  const int x = lane & (LPR - 1), ry = lane / LPR;
   const bool xin = x < NXM;
-  // current row of this warp (rows warp, warp + NW, ..): set by set_row
+  // current row of this lane group: set by set_row
   int y = warp;
-  bool wact = false, lact = false;  // wact warp-uniform
+  bool wact = false, lact = false;  // wact warp-uniform (some row of the warp is in the window)
 
   extern __shared__ __align__(16) double smem[];
   double* p_s = smem;                  // [NXM+2][PY][NXM], zero halo planes / rows
@@ -152,14 +158,16 @@ __global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(Leve
   if (x < nx) sx = sides_of(A, P, 0, x, ncx);
 #pragma unroll
   for (int ri = 0; ri < RW; ri++) {
-    const int yy = warp + ri * NW;
+    const int yy = (warp + ri * NW) * RPW + ry;
     syr[ri] = (yy < ny) ? sides_of(A, P, 1, yy, ny - 1) : Sides{0, 0, 0};
   }
   const int kxe = (x < ncx) ? slot3(A, P, 0, x) : 1000;  // subcell column of element x
+  const int kseg = ry * 1024 + kxe;                      // scan key: never equal across rows
   auto set_row = [&](int ri) {
-    y = warp + ri * NW;
-    wact = y < ny;
-    lact = wact && x < nx;
+    const int yb = (warp + ri * NW) * RPW;
+    y = yb + ry;
+    wact = yb < ny;
+    lact = (y < ny) && x < nx;
     sy = syr[ri];
   };
   __syncthreads();
@@ -233,20 +241,20 @@ __global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(Leve
       }
     }
   };
-  // warp-collective (wact warps): layer kz of this row -> bins[y]
+  // warp-collective (wact warps): layer kz of each row -> bins[y]
   auto flush = [&](int kz) {
 #pragma unroll
     for (int ys = 0; ys < 2; ys++) {
-      if (!((sy.pm >> ys) & 1)) continue;  // warp-uniform
+      const bool has = (sy.pm >> ys) & 1;  // per row (acc is zero where the side is absent)
       const int ky = ys ? sy.k1 : sy.k0;
       double v[N];
 #pragma unroll
       for (int j = 0; j < N; j++) {
         const double t = __shfl_down_sync(FULLMASK, acc[ys][0][j], 1);  // element x of lane x+1
-        v[j] = acc[ys][1][j] + ((lane < 31) ? t : 0.0);
+        v[j] = acc[ys][1][j] + ((x < LPR - 1) ? t : 0.0);
       }
-      const int kup = __shfl_up_sync(FULLMASK, kxe, 1);
-      const unsigned hm = __ballot_sync(FULLMASK, lane == 0 || kxe != kup);
+      const int kup = __shfl_up_sync(FULLMASK, kseg, 1);
+      const unsigned hm = __ballot_sync(FULLMASK, lane == 0 || kseg != kup);
       const int head = 31 - __clz(hm & (0xffffffffu >> (31 - lane)));
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -257,7 +265,7 @@ __global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(Leve
         }
       }
       const bool tail = (lane == 31) || ((hm >> (lane + 1)) & 1u);
-      if (tail && kxe < 1000) {
+      if (tail && kxe < 1000 && has && y < ny) {
         double* B = bins + y * NQ + ((kz * 3 + ky) * 3 + kxe) * N;
 #pragma unroll
         for (int j = 0; j < N; j++) B[j] = v[j];
@@ -309,8 +317,8 @@ __global__ void __launch_bounds__(32 * ((NXM + RW - 1) / RW), MINB) k_pcg3d(Leve
           const double c0 = v[dy][dz];
           double l = __shfl_up_sync(FULLMASK, c0, 1);
           double r = __shfl_down_sync(FULLMASK, c0, 1);
-          if (lane == 0) l = 0.0;
-          if (lane == 31) r = 0.0;
+          if (x == 0) l = 0.0;
+          if (x == LPR - 1) r = 0.0;
           const int cb = 9 * dz + 3 * dy;
           Ap += cf[cb] * l + cf[cb + 1] * c0 + cf[cb + 2] * r;
         }
@@ -1018,15 +1026,17 @@ static cudaError_t launch3(const LevelArgs& A, cudaStream_t st) {
   const size_t smem = pcg3d_smem(N, NXM);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)A.nprob_mp * A.n_rhs, 32 * ((NXM + RW - 1) / RW), smem, st>>>(A);
+  constexpr int LPR = (NXM > 16) ? 32 : ((NXM > 8) ? 16 : 8), RPW = 32 / LPR;
+  constexpr int NW = (NXM + RPW * RW - 1) / (RPW * RW);
+  k<<<(unsigned)A.nprob_mp * A.n_rhs, 32 * NW, smem, st>>>(A);
   return cudaGetLastError();
 }
 
 template <int N>
 static cudaError_t launch3n(const LevelArgs& A, int nxm, cudaStream_t st) {
   switch (nxm) {
-    case 7: return launch3<N, 7, 1, 2>(A, st);
-    case 13: return launch3<N, 13, 2, 2>(A, st);
+    case 7: return launch3<N, 7, 1, 8>(A, st);
+    case 13: return launch3<N, 13, 1, 2>(A, st);
     case 25: return launch3<N, 25, 2, 1>(A, st);
   }
   return cudaErrorInvalidValue;
