@@ -156,6 +156,24 @@ int mch_load_vectors(mch_ctx* ctx, double* out, size_t out_len, int out_on_devic
 int mch_macro_solve(mch_ctx* ctx, const double* G, const double* b, int inputs_on_device, double* U,
                     size_t U_len, int out_on_device, double rtol, int max_iter, int* iters);
 
+/* NEXT-3 (validation workload).  Global fine-grid reference solution of Eq. (2):
+ * u in Q1 on the n^d fine cells of Omega = [0,1]^d, u = 0 on the boundary (Eq. 1), with this
+ * context's kappa and the cellwise source f (float64, n^d, x fastest; f_on_device as for kappa).
+ * u receives the (n+1)^d nodal values (x fastest).  Matrix-free Jacobi-PCG in fp64, one
+ * persistent cooperative kernel, to ||r|| <= rtol ||F|| (rtol <= 0: 1e-10; max_iter <= 0: 10^6);
+ * *iters (may be NULL) receives the iteration count.  Deterministic for a given GPU model (the
+ * grid is sized from the SM count).  Errors: MCH_EINVAL, MCH_ENOCONV, MCH_ECUDA. */
+int mch_fine_solve(mch_ctx* ctx, const double* f, int f_on_device, double* u, size_t u_len, int u_on_device,
+                   double rtol, int max_iter, int* iters);
+
+/* Fine block averages of the error metric e_2: out[p][i] =
+ * (1/|K_p cap Omega_i|) int_{K_p cap Omega_i} u for the (n+1)^d nodal Q1 field u (e.g. from
+ * mch_fine_solve), Omega_i = the cells of continuum i, K_p as for the coefficients (block or
+ * clipped dual block); NaN where K_p holds no cell of continuum i.  out [P][N].  Errors:
+ * MCH_EINVAL, MCH_ECUDA. */
+int mch_fine_block_averages(mch_ctx* ctx, const double* u, int u_on_device, double* out, size_t out_len,
+                            int out_on_device);
+
 /* Rewind the level counter so the same context (inputs, plan, pool, scratch) solves levels
  * 1..L again — for repeated runs (benchmarks, serving) without re-creating the context. */
 int mch_reset(mch_ctx* ctx);

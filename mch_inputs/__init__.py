@@ -5,7 +5,7 @@ and the BASELINE configuration table, the source f of the paper's experiments). 
 arithmetic (no stiffness, constraints, solves or reductions), so both sides of
 every parity test may import it without sharing method code.
 """
-from .media import (CONFIGS, Config, make_medium, paper_source, random_medium, layered_medium,
+from .media import (CONFIGS, Config, make_medium, paper_medium, paper_source, random_medium, layered_medium,
                     periodic_medium)
 
-__all__ = ["CONFIGS", "Config", "make_medium", "paper_source", "random_medium", "layered_medium", "periodic_medium"]
+__all__ = ["CONFIGS", "Config", "make_medium", "paper_medium", "paper_source", "random_medium", "layered_medium", "periodic_medium"]

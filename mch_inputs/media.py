@@ -206,3 +206,19 @@ def paper_source(d: int, n: int, ids, eps: float, low=(0,)):
     in_low = np.isin(ids, np.asarray(low, dtype=ids.dtype))
     g[in_low] *= eps / 10.0
     return np.ascontiguousarray(g)
+
+
+def paper_medium(d: int, n: int, eps: float, geometry: str = "layered"):
+    """The paper's permeability κ = g1·g2 at fine-cell centres:
+    g1 = 2 + sin(πx_1) sin(πx_2); g2 = ε/10⁴ in the low-conductivity region Ω_1 (continuum 0),
+    1/(100ε) in Ω_2 (continuum 1).  The geometries are figures in the paper (reading R25):
+    "layered" = layers normal to x_2 of period ε, Ω_2 the upper half of each period;
+    "crossed" = Ω_2 the union of the x_2-layers and the same layers normal to x_1."""
+    xs = _grid(d, n)
+    shape = (n,) * d
+    g1 = np.broadcast_to(2.0 + np.sin(np.pi * xs[0]) * np.sin(np.pi * xs[1]), shape)
+    ph = [np.broadcast_to((xs[i] / eps) % 1.0 >= 0.5, shape) for i in range(2)]
+    hi = ph[1] if geometry == "layered" else (ph[0] | ph[1])
+    ids = hi.astype(np.uint8)
+    kappa = g1 * np.where(hi, 1.0 / (100.0 * eps), eps / 1e4)
+    return np.ascontiguousarray(kappa), np.ascontiguousarray(ids)

@@ -18,7 +18,8 @@ ERRORS = {-1: "MCH_EINVAL", -2: "MCH_EDIVISIBILITY", -3: "MCH_ERANK", -4: "MCH_E
 # every symbol include/mch.h declares
 SYMBOLS = ["mch_create", "mch_set_medium", "mch_reset", "mch_solve_level", "mch_effective_coeffs", "mch_num_macropoints", "mch_level_macropoints",
            "mch_local_solution", "mch_get_level_stats", "mch_level_iterations", "mch_pool_info", "mch_pool_slot",
-           "mch_coeffs_device", "mch_set_source", "mch_load_vectors", "mch_macro_solve", "mch_last_error",
+           "mch_coeffs_device", "mch_set_source", "mch_load_vectors", "mch_macro_solve", "mch_fine_solve",
+           "mch_fine_block_averages", "mch_last_error",
            "mch_destroy"]
 
 
@@ -69,6 +70,8 @@ def _load():
     lib.mch_set_source.argtypes = [vp, vp, i32]
     lib.mch_load_vectors.argtypes = [vp, vp, ctypes.c_size_t, i32]
     lib.mch_macro_solve.argtypes = [vp, vp, vp, i32, vp, ctypes.c_size_t, i32, dbl, i32, P(i32)]
+    lib.mch_fine_solve.argtypes = [vp, vp, i32, vp, ctypes.c_size_t, i32, dbl, i32, P(i32)]
+    lib.mch_fine_block_averages.argtypes = [vp, vp, i32, vp, ctypes.c_size_t, i32]
     lib.mch_last_error.argtypes = [vp]
     lib.mch_last_error.restype = ctypes.c_char_p
     lib.mch_destroy.argtypes = [vp]

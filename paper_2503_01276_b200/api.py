@@ -182,6 +182,32 @@ class Homogenizer:
         it = mch_macro_solve(self.ctx, out, G, b, rtol=rtol, max_iter=max_iter)
         return out, it
 
+    def fine_solve(self, f, rtol=1e-10, max_iter=0, out=None):
+        """NEXT-3: global fine reference solution of Eq. (2) with this context's kappa and the
+        cellwise source f.  Returns (u nodal [(n+1)^d], iterations)."""
+        if isinstance(f, np.ndarray):
+            f = np.ascontiguousarray(f, dtype=np.float64)
+        fp, fdev = _ptr(f)
+        if out is None:
+            out = np.zeros(((self.n + 1),) * self.d)
+        op, odev = _ptr(out)
+        n = out.numel() if hasattr(out, "numel") else out.size
+        it = ctypes.c_int(0)
+        check(lib.mch_fine_solve(self.ctx, fp, fdev, op, n, odev, rtol, max_iter, ctypes.byref(it)), self.ctx)
+        return out, it.value
+
+    def fine_block_averages(self, u, out=None):
+        """[P][N]: (1/|K_p cap Omega_i|) int_{K_p cap Omega_i} u."""
+        if isinstance(u, np.ndarray):
+            u = np.ascontiguousarray(u, dtype=np.float64)
+        up, udev = _ptr(u)
+        if out is None:
+            out = np.zeros((self.num_macropoints, self.N))
+        op, odev = _ptr(out)
+        n = out.numel() if hasattr(out, "numel") else out.size
+        check(lib.mch_fine_block_averages(self.ctx, up, udev, op, n, odev), self.ctx)
+        return out
+
     def coeffs_device_ptr(self):
         p = ctypes.c_void_p()
         check(lib.mch_coeffs_device(self.ctx, ctypes.byref(p)), self.ctx)

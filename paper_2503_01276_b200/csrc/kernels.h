@@ -38,3 +38,11 @@ cudaError_t launch_pcg3d(const LevelArgs& A, int nxm, cudaStream_t st);
 // level 1 (windows of <= 49 fine nodes per side)
 size_t pcg3d_l1_smem(int N);
 cudaError_t launch_pcg3d_l1(const LevelArgs& A, cudaStream_t st);
+
+// validation workload (fine.cu, NEXT-3): global fine reference solve of Eq. (2), block averages
+size_t fine_workspace_doubles(int D, int64_t n, int grid);
+int fine_grid_size(int D);
+cudaError_t launch_fine_pcg(int D, int64_t n, const double* kappa, const double* f, double* ws, unsigned* bar,
+                            int grid, double rtol, int max_iter, int* iters, double* relres, cudaStream_t st);
+cudaError_t launch_fine_block_avg(int D, const double* u, const uint8_t* ids, const int* kbox, int64_t P, int64_t n,
+                                  int N, double* out, cudaStream_t st);

@@ -105,6 +105,7 @@ struct mch_ctx {
   int* d_bad = nullptr;
   // NEXT-2: source f (cellwise, n^D), load vectors [P][N], macro-solve workspace and results
   DevBuf fsrc, bload, mws, mG, mb, mU, mres;
+  DevBuf fws, fbar, ff, fu, fkbox, fout;  // NEXT-3 fine solve / block averages
   bool has_source = false;
   int* h_mit = nullptr;
   double* h_mrel = nullptr;
@@ -777,6 +778,90 @@ extern "C" int mch_macro_solve(mch_ctx* c, const double* G, const double* b, int
   return MCH_OK;
 }
 
+extern "C" int mch_fine_solve(mch_ctx* c, const double* f, int f_on_device, double* u, size_t u_len, int u_on_device,
+                              double rtol, int max_iter, int* iters) {
+  if (!c || !f || !u) return c ? fail(c, MCH_EINVAL, "NULL argument") : MCH_EINVAL;
+  const int D = c->D;
+  const int64_t n = c->p.n;
+  int64_t cells = 1, nn = 1;
+  for (int i = 0; i < D; i++) {
+    cells *= n;
+    nn *= n + 1;
+  }
+  if (u_len < (size_t)nn) return fail(c, MCH_EINVAL, "u_len too small");
+  if (rtol <= 0.0) rtol = 1e-10;
+  if (max_iter <= 0) max_iter = 1000000;
+  if (!f_on_device)
+    for (int64_t i = 0; i < cells; i++)
+      if (!std::isfinite(f[i])) return fail(c, MCH_EINVAL, "source must be finite");
+  const double* df = f;
+  if (!f_on_device) {
+    CKC(c, c->ff.ensure(cells * sizeof(double)));
+    CKC(c, cudaMemcpyAsync(c->ff.ptr, f, cells * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    df = c->ff.as<double>();
+  }
+  const int grid = fine_grid_size(D);
+  CKC(c, c->fws.ensure(fine_workspace_doubles(D, n, grid) * sizeof(double)));
+  CKC(c, c->fbar.ensure(4 * sizeof(unsigned) + 2 * sizeof(double)));
+  if (!c->h_mit) CKC(c, cudaMallocHost(&c->h_mit, sizeof(int)));
+  if (!c->h_mrel) CKC(c, cudaMallocHost(&c->h_mrel, sizeof(double)));
+  unsigned* bar = reinterpret_cast<unsigned*>(c->fbar.ptr);
+  int* d_it = reinterpret_cast<int*>(bar + 2);
+  double* d_rel = reinterpret_cast<double*>(bar + 4);
+  CKC(c, launch_fine_pcg(D, n, c->kappa, df, c->fws.as<double>(), bar, grid, rtol, max_iter, d_it, d_rel, c->st));
+  c->launches += 1;
+  CKC(c, cudaMemcpyAsync(u, c->fws.ptr, nn * sizeof(double), u_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                         c->st));
+  CKC(c, cudaMemcpyAsync(c->h_mit, d_it, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CKC(c, cudaMemcpyAsync(c->h_mrel, d_rel, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CKC(c, cudaStreamSynchronize(c->st));
+  if (iters) *iters = *c->h_mit;
+  if (!(*c->h_mrel <= rtol)) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "fine PCG: relative residual %.3e after %d iterations", *c->h_mrel, *c->h_mit);
+    return fail(c, MCH_ENOCONV, buf);
+  }
+  return MCH_OK;
+}
+
+extern "C" int mch_fine_block_averages(mch_ctx* c, const double* u, int u_on_device, double* out, size_t out_len,
+                                       int out_on_device) {
+  if (!c || !u || !out) return c ? fail(c, MCH_EINVAL, "NULL argument") : MCH_EINVAL;
+  const int D = c->D, N = c->N;
+  const int64_t n = c->p.n;
+  int64_t nn = 1;
+  for (int i = 0; i < D; i++) nn *= n + 1;
+  const HostPlan& pl = c->plan;
+  const int64_t P = (int64_t)pl.all.size();
+  if (out_len < (size_t)(P * N)) return fail(c, MCH_EINVAL, "out_len too small");
+  std::vector<int> kb(6 * P, 0);
+  for (int64_t m = 0; m < P; m++)
+    for (int d = 0; d < 3; d++) {
+      const int64_t a = (int64_t)pl.all[m].k[d] * pl.c - pl.coff(), b = a + pl.c;  // K_p
+      kb[6 * m + d] = (d < D) ? (int)std::max<int64_t>(0, a) : 0;
+      kb[6 * m + 3 + d] = (d < D) ? (int)std::min<int64_t>(n, b) : 1;
+    }
+  CKC(c, c->fkbox.ensure(kb.size() * sizeof(int)));
+  CKC(c, cudaMemcpyAsync(c->fkbox.ptr, kb.data(), kb.size() * sizeof(int), cudaMemcpyHostToDevice, c->st));
+  const double* du = u;
+  if (!u_on_device) {
+    CKC(c, c->fu.ensure(nn * sizeof(double)));
+    CKC(c, cudaMemcpyAsync(c->fu.ptr, u, nn * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    du = c->fu.as<double>();
+  }
+  double* dout = out;
+  if (!out_on_device) {
+    CKC(c, c->fout.ensure(P * N * sizeof(double)));
+    dout = c->fout.as<double>();
+  }
+  CKC(c, launch_fine_block_avg(D, du, c->ids, c->fkbox.as<int>(), P, n, N, dout, c->st));
+  c->launches += 1;
+  if (!out_on_device)
+    CKC(c, cudaMemcpyAsync(out, dout, P * N * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CKC(c, cudaStreamSynchronize(c->st));
+  return MCH_OK;
+}
+
 extern "C" int mch_num_macropoints(const mch_ctx* c, int level, int64_t* count) {
   if (!c || !count || level < 1 || level > c->p.levels) return MCH_EINVAL;
   *count = (int64_t)c->plan.S[level].size();
@@ -870,7 +955,8 @@ extern "C" void mch_destroy(mch_ctx* c) {
   if (c->d_bad) cudaFree(c->d_bad);
   DevBuf* bufs[] = {&c->STC, &c->MLR, &c->pinv_ds, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
                     &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres, &c->diag,
-                    &c->fsrc, &c->bload, &c->mws, &c->mG, &c->mb, &c->mU, &c->mres};
+                    &c->fsrc, &c->bload, &c->mws, &c->mG, &c->mb, &c->mU, &c->mres,
+                    &c->fws, &c->fbar, &c->ff, &c->fu, &c->fkbox, &c->fout};
   for (DevBuf* b : bufs) b->release();
   if (c->events)
     for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);

@@ -329,3 +329,66 @@ def test_macro_solve_large_synthetic(d, n, M, N):
     with H(d, n, N, M, 1, 2, kap, ids, layout="block") as h:
         Ug, it = h.macro_solve(G, b, rtol=1e-13)
         assert np.abs(Ug - Uo).max() <= 1e-8 * np.abs(Uo).max(), (it, np.abs(Ug - Uo).max() / np.abs(Uo).max())
+
+
+@pytest.mark.parametrize("d,n,N", [(2, 64, 2), (2, 96, 3), (3, 16, 2)])
+def test_fine_solve_and_block_averages(d, n, N):
+    """NEXT-3: the global fine reference solve (Eq. 2) on the GPU vs the oracle's direct sparse
+    solve, ‖Δu‖∞ ≤ 1e-8 ‖u‖∞ (PCG to 1e-13 on a system of condition ≲ 1e7); fine block averages
+     of the same field vs the oracle's, ≤ 1e-13 relative; two solves bitwise equal."""
+    from mch_inputs import paper_source
+    from oracle.fine import fine_block_averages, fine_solve
+    H = _gpu()
+    kap, ids = random_medium(d, n, N, seed=70 + d + N)
+    f = paper_source(d, n, ids, eps=0.1)
+    uo = fine_solve(kap, f)
+    M = n // 8
+    with H(d, n, N, M, 1, 2, kap, ids, layout="block") as h:
+        ug, it = h.fine_solve(f, rtol=1e-13)
+        assert it > 0
+        assert np.abs(ug - uo).max() <= 1e-8 * np.abs(uo).max(), np.abs(ug - uo).max() / np.abs(uo).max()
+        ug2, it2 = h.fine_solve(f, rtol=1e-13)
+        assert it2 == it and np.array_equal(ug, ug2)
+        bg = h.fine_block_averages(uo)
+        bo = fine_block_averages(uo, ids, N, M)
+        ok = np.isfinite(bo)
+        assert np.array_equal(ok, np.isfinite(bg))
+        assert np.abs(bg[ok] - bo[ok]).max() <= 1e-13 * np.abs(bo[ok]).max()
+
+
+def test_type_errors_end_to_end():
+    """NEXT-3: the paper's Type 1/2/3 errors on a small block-layout case,
+    on the paper's layered medium κ = g1·g2 (reading R25) with ε = H, every GPU
+    stage (coefficients and loads at L = 1 and L = 2, macro solves, fine solve, fine block
+    averages) vs the oracle pipeline: each e₂ within 1e-6 relative of the oracle's; and the
+    paper's claim for Example 1: Type 3 (hierarchical vs plain) two orders
+    below Types 1/2 (oracle here: 9e-4 vs 0.12-0.22)."""
+    from mch_inputs import paper_medium, paper_source
+    from oracle.fine import e2, fine_block_averages, fine_solve, macro_block_averages
+    from oracle.macro import load_vectors, macro_solve
+    from paper_2503_01276_b200.validate import macro_block_averages as mba, relative_l2_error
+    H = _gpu()
+    d, n, M, N = 2, 64, 8, 2
+    kap, ids = paper_medium(d, n, 1.0 / 8)
+    o1 = Oracle(d, n, M, 1, 2, N, kap, ids, layout="block")
+    o2 = Oracle(d, n, M, 2, 2, N, kap, ids, layout="block")
+    f = paper_source(d, n, ids, eps=1.0 / 8)
+    ref = fine_block_averages(fine_solve(kap, f), ids, N, M)
+    Uo = {}
+    for L, o in ((1, o1), (2, o2)):
+        Uo[L] = macro_block_averages(macro_solve(d, N, M, o.effective_coeffs(), load_vectors(o, f)), d, M)
+    eo = [e2(Uo[1], ref), e2(Uo[2], ref), e2(Uo[2], Uo[1])]
+    Ug = {}
+    for L in (1, 2):
+        with H(d, n, N, M, L, 2, kap, ids, layout="block") as h:
+            h.set_source(f)
+            h.solve_all()
+            U, _ = h.macro_solve(rtol=1e-13)
+            Ug[L] = mba(U, d, M)
+            if L == 1:
+                ug, _ = h.fine_solve(f, rtol=1e-13)
+                refg = h.fine_block_averages(ug)
+    eg = [relative_l2_error(Ug[1], refg), relative_l2_error(Ug[2], refg), relative_l2_error(Ug[2], Ug[1])]
+    for a, b in zip(eg, eo):
+        assert np.all(np.abs(a - b) <= 1e-6 * np.maximum(b, 1e-12)), (eg, eo)
+    assert np.all(eo[2] < 0.05 * np.minimum(eo[0], eo[1])), eo

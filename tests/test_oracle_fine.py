@@ -72,3 +72,16 @@ def test_macro_block_average_and_e2():
         assert abs(Ub[p, 0] - (cx + 2 * cy)) < 1e-14 and abs(Ub[p, 1] - cx * cy) < 1e-14
     ub = np.random.default_rng(1).uniform(1, 2, size=(16, 2))
     assert np.allclose(e2(ub * 1.03, ub), 0.03, rtol=1e-12)
+
+
+def test_host_validate_matches_oracle():
+    """the product's host post-processing (validate.py) against the oracle's formulas"""
+    from paper_2503_01276_b200.validate import macro_block_averages as mba, relative_l2_error
+    rng = np.random.default_rng(0)
+    for d, M, N in ((2, 8, 3), (3, 4, 2)):
+        U = rng.normal(size=(N, (M + 1) ** d))
+        assert np.abs(mba(U, d, M) - macro_block_averages(U, d, M)).max() < 1e-15
+    ub = rng.uniform(1, 2, size=(20, 2))
+    ub[3, 1] = np.nan
+    Ub = ub + rng.normal(size=ub.shape) * 0.01
+    assert np.allclose(relative_l2_error(Ub, ub), e2(Ub, ub), rtol=1e-14)
