@@ -168,6 +168,7 @@ __global__ void k_transport(LevelArgs A) {
   const Geo<D> gl = level_geo<D>(A, P);
   double* I = A.FI + P.fine_off + (int64_t)r * gf.nnodes;
   double* Y = A.FY + P.fine_off + (int64_t)r * gf.nnodes;
+  if (A.tphase != 2) {
   // phase 1: I_p at fine nodes (local-coordinate transport, reading R9)
   for (int k = threadIdx.x; k < gf.nnodes; k += blockDim.x) {
     int x[3];
@@ -185,6 +186,7 @@ __global__ void k_transport(LevelArgs A) {
     }
     I[k] = s;
   }
+  if (A.tphase == 1) return;
   __syncthreads();
   // phase 2: Y = A_1 I (fine operator on the window, natural BC)
   for (int k = threadIdx.x; k < gf.nnodes; k += blockDim.x) Y[k] = apply_node<D>(A, P, gf, I, k);
@@ -199,6 +201,7 @@ __global__ void k_transport(LevelArgs A) {
     const int64_t gi = ((int64_t)mp * A.ncon + i) * A.n_rhs + r;
     A.g[gi] = A.g0[gi] - cI[i];
   }
+  }  // tphase != 2
   __syncthreads();
   // phase 3: b = -P_n^T Y at level-n nodes.  P_n^T is the tensor product of the 1D restrictions
   // (weights 1 - |d|/s, |d| < s), applied dimension by dimension in place in Y: one thread per

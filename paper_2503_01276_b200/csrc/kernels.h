@@ -46,3 +46,5 @@ cudaError_t launch_fine_pcg(int D, int64_t n, const double* kappa, const double*
                             int grid, double rtol, int max_iter, int* iters, double* relres, cudaStream_t st);
 cudaError_t launch_fine_block_avg(int D, const double* u, const uint8_t* ids, const int* kbox, int64_t P, int64_t n,
                                   int N, double* out, cudaStream_t st);
+// 3D transport split (levels >= 2): Y = A_1 I_p and g = g0 - C_1 I_p on the fine window
+cudaError_t launch_tapply3d(const LevelArgs& A, cudaStream_t st);

@@ -61,6 +61,7 @@ struct LevelBatch {
   DevBuf descs, segs, nseg;
   bool on2d = false, l1op = false;
   bool on3d = false;  // on-chip 3D PCG (pcg3d.cu), levels >= 2
+  bool tsplit = false;  // 3D transport through k_pcg3d_l1<MODE 1> (fine windows <= 49 nodes per side)
   int nxm3 = 0;
   int variant = -1, threads2 = 0, maxseg = 0, tm_cols = 32;
   int* h_flags = nullptr;  // pinned results
@@ -426,6 +427,10 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       int maxn = 0;
       for (int i = 0; i < nmp; i++)
         for (int d = 0; d < 3; d++) maxn = std::max(maxn, descs[i].nc[d] + 1);
+      int maxf = 0;
+      for (int i = 0; i < nmp; i++)
+        for (int d = 0; d < 3; d++) maxf = std::max(maxf, descs[i].ncf[d] + 1);
+      B->tsplit = level >= 2 && maxf <= 49 && pcg3d_l1_smem(N) <= 232448 && getenv("MCH_TRANSPORT_GENERIC") == nullptr;
       if (level >= 2) {
         const int nxm = pcg3d_nxm(maxn);
         if (nxm > 0 && pcg3d_smem(N, nxm) <= 232448) {
@@ -542,7 +547,17 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     cudaEventRecord(B.ev[0], st);
     S.launches += (level >= 2) ? 6 : 4;
     CKC(c, launch_targets(A, st));
-    if (level >= 2) CKC(c, launch_transport(A, B.th_f, st));
+    if (level >= 2 && B.tsplit) {  // 3D: I_p, then the column-walking apply, then P_n^T
+      A.tphase = 1;
+      CKC(c, launch_transport(A, B.th_f, st));
+      CKC(c, launch_tapply3d(A, st));
+      A.tphase = 2;
+      CKC(c, launch_transport(A, B.th_f, st));
+      A.tphase = 0;
+      S.launches += 2;
+    } else if (level >= 2) {
+      CKC(c, launch_transport(A, B.th_f, st));
+    }
     CKC(c, launch_proj_setup(A, B.th_l, st));
     CKC(c, launch_pinv(A, st));
     S.launches += 1;

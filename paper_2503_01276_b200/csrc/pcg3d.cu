@@ -33,8 +33,12 @@ __device__ __forceinline__ double wsum0(double v) {
   return __shfl_sync(FULLMASK, v, 0);
 }
 
+// subcell slot of the cell e of a grid of cell size s (in fine cells) along one dimension
+__device__ __forceinline__ int slot3(const LevelArgs& A, const ProbDesc& P, int dim, int e, int s) {
+  return fdiv(P.lo[dim] + e * s + A.coff, A.inv_c) - P.k[dim] + A.l;
+}
 __device__ __forceinline__ int slot3(const LevelArgs& A, const ProbDesc& P, int dim, int e) {
-  return fdiv(P.lo[dim] + e * A.s + A.coff, A.inv_c) - P.k[dim] + A.l;
+  return slot3(A, P, dim, e, A.s);
 }
 
 // The elements on the two sides of a node along one dimension (side 0: cell X-1, side 1: cell X)
@@ -44,10 +48,11 @@ __device__ __forceinline__ int slot3(const LevelArgs& A, const ProbDesc& P, int 
 struct Sides {
   int pm, k0, k1;
 };
-__device__ __forceinline__ Sides sides_of(const LevelArgs& A, const ProbDesc& P, int dim, int X, int ncd) {
+__device__ __forceinline__ Sides sides_of(const LevelArgs& A, const ProbDesc& P, int dim, int X, int ncd,
+                                          int cs) {
   Sides s;
   const bool lo = X >= 1, up = X < ncd;
-  const int sl = lo ? slot3(A, P, dim, X - 1) : -1, su = up ? slot3(A, P, dim, X) : -1;
+  const int sl = lo ? slot3(A, P, dim, X - 1, cs) : -1, su = up ? slot3(A, P, dim, X, cs) : -1;
   if (lo && up && sl != su) {
     s.pm = 3; s.k0 = sl; s.k1 = su;
   } else if (lo) {
@@ -56,6 +61,9 @@ __device__ __forceinline__ Sides sides_of(const LevelArgs& A, const ProbDesc& P,
     s.pm = 2; s.k0 = su; s.k1 = su;
   }
   return s;
+}
+__device__ __forceinline__ Sides sides_of(const LevelArgs& A, const ProbDesc& P, int dim, int X, int ncd) {
+  return sides_of(A, P, dim, X, ncd, A.s);
 }
 
 }  // namespace
@@ -528,14 +536,19 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
 // window of the cells' kappa and ids (4 loads per node).  Operator: the Q1 element rows
 // kappa h/12 (4 p_a - p_{a^3} - p_{a^5} - p_{a^6} - p_{a^7}) summed over the 8 cells;
 // constraint weights m_{E,j,a} = [id_E = j] h^3/8.
-template <int N, int NW>
+//
+// MODE 1 (transport, levels >= 2): the same walkers on the fine window of the problem compute
+// Y = A_1 I_p (into FY) and g = g^0 - C_1 I_p from the transported field I_p (FI), replacing the
+// generic per-node gather of k_transport (Eqs. 12-13; reading R9).
+template <int N, int NW, int MODE = 0>
 __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs A) {
   constexpr int NT = 98, RW = NT / NW;  // 98 row segments = 49 rows x 2
   constexpr int NQ = 27 * N;
   const int prob = blockIdx.x;
   const int mp = prob / A.n_rhs, rhs = prob - mp * A.n_rhs;
   const ProbDesc& P = A.probs[mp];
-  const int nx = P.nc[0] + 1, ny = P.nc[1] + 1, nz = P.nc[2] + 1, nn = nx * ny * nz;
+  const int* ncv = (MODE == 0) ? P.nc : P.ncf;  // fine cells of the window in both modes
+  const int nx = ncv[0] + 1, ny = ncv[1] + 1, nz = ncv[2] + 1, nn = nx * ny * nz;
   const int ncx = nx - 1, ncy = ny - 1, ncz = nz - 1;
   const int nc = A.ncon;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -549,7 +562,7 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
   int* zsm = reinterpret_cast<int*>(slots + 4 * 32);  // [49][3]
   for (int i = threadIdx.x; i < NT * NQ + 2 * NQ + 4 * 32; i += blockDim.x) bins[i] = 0.0;
   for (int z = threadIdx.x; z < nz; z += blockDim.x) {
-    const Sides sd = sides_of(A, P, 2, z, ncz);
+    const Sides sd = sides_of(A, P, 2, z, ncz, 1);
     zsm[z * 3] = sd.pm;
     zsm[z * 3 + 1] = sd.k0;
     zsm[z * 3 + 2] = sd.k1;
@@ -584,9 +597,9 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
     x = seg * 32 + lane;
     wact = (y < ny) && (seg * 32 < nx);
     lact = wact && x < nx;
-    sx = lact ? sides_of(A, P, 0, x, ncx) : Sides{0, 0, 0};
-    sy = wact ? sides_of(A, P, 1, y, ncy) : Sides{0, 0, 0};
-    kxe = (lact && x < ncx) ? slot3(A, P, 0, x) : 1000;
+    sx = lact ? sides_of(A, P, 0, x, ncx, 1) : Sides{0, 0, 0};
+    sy = wact ? sides_of(A, P, 1, y, ncy, 1) : Sides{0, 0, 0};
+    kxe = (lact && x < ncx) ? slot3(A, P, 0, x, 1) : 1000;
     pvm = 0;
     cvm = 0;
     if (lact) {
@@ -614,7 +627,7 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
   };
 
   const double* dg = A.dinv + P.node_off;
-  double* pv = A.P + P.vec_off + (int64_t)rhs * nn;
+  double* pv = (MODE == 0) ? A.P + P.vec_off + (int64_t)rhs * nn : A.FI + P.fine_off + (int64_t)rhs * nn;
   double* Xv = A.X + P.vec_off + (int64_t)rhs * nn;
   double* Rv = A.R + P.vec_off + (int64_t)rhs * nn;
   double* Qv = A.Q + P.vec_off + (int64_t)rhs * nn;
@@ -839,6 +852,23 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
     if (lane == 0) slots[3 * 32 + warp] = cyw;
   };
 
+  if (MODE == 1) {
+    double* Yv = A.FY + P.fine_off + (int64_t)rhs * nn;
+    tasks([&] {
+      if (wact) sweep_stencil([&](int, int k, double Ap, double) { if (lact) Yv[k] = Ap; });
+    });
+    tasks([&] {
+      if (wact) sweep_c([&](int, int k) -> double { return lact ? pv[k] : 0.0; });
+    });
+    __syncthreads();
+    reduce_c(nullptr);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      const int64_t gi = ((int64_t)mp * nc + i) * A.n_rhs + rhs;
+      A.g[gi] = A.g0[gi] - csh[i];
+    }
+    return;
+  }
   // init: x0 = D^-1 C^T S^-1 g0, r0 = A x0, c = C D^-1 r0, yhat = S^-1 c
   for (int i = threadIdx.x; i < nc; i += blockDim.x) csh[i] = A.g0[((int64_t)mp * nc + i) * A.n_rhs + rhs];
   __syncthreads();
@@ -998,6 +1028,24 @@ cudaError_t launch_pcg3d_l1(const LevelArgs& A, cudaStream_t st) {
     case 2: return wide ? go(k_pcg3d_l1<2, 7>, 7) : go(k_pcg3d_l1<2, 14>, 14);
     case 3: return wide ? go(k_pcg3d_l1<3, 7>, 7) : go(k_pcg3d_l1<3, 14>, 14);
     case 4: return wide ? go(k_pcg3d_l1<4, 7>, 7) : go(k_pcg3d_l1<4, 14>, 14);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_tapply3d(const LevelArgs& A, cudaStream_t st) {
+  const size_t smem = pcg3d_l1_smem(A.N);
+  const int probs = A.nprob_mp * A.n_rhs;
+  auto go = [&](auto k) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)probs, 7 * 32, smem, st>>>(A);
+    return cudaGetLastError();
+  };
+  switch (A.N) {
+    case 1: return go(k_pcg3d_l1<1, 7, 1>);
+    case 2: return go(k_pcg3d_l1<2, 7, 1>);
+    case 3: return go(k_pcg3d_l1<3, 7, 1>);
+    case 4: return go(k_pcg3d_l1<4, 7, 1>);
   }
   return cudaErrorInvalidValue;
 }
