@@ -399,6 +399,67 @@ __device__ void subcell_boxes(const LevelArgs& A, const ProbDesc& P, const Geo<D
   __syncthreads();
 }
 
+// Contribution of element idx (< cnt) of subcell box bx to the N constraint rows of its subcell.
+template <int D, typename UF>
+__device__ __forceinline__ void cell_constraint_part(const LevelArgs& A, const ProbDesc& P, const Geo<D>& g,
+                                                     const int* bx, int idx, UF uf, double (&part)[4]) {
+  int e[3];
+  const int i2 = (D == 3) ? fdiv(idx, 1.0f / (float)(bx[3] * bx[4])) : 0;
+  const int r2 = idx - i2 * bx[3] * bx[4];
+  const int i1 = fdiv(r2, 1.0f / (float)bx[3]);
+  e[0] = bx[0] + r2 - i1 * bx[3];
+  e[1] = bx[1] + i1;
+  e[2] = bx[2] + i2;
+  double u[1 << D];
+#pragma unroll
+  for (int b = 0; b < (1 << D); b++) {
+    int xb[3] = {e[0] + (b & 1), e[1] + ((b >> 1) & 1), (D == 3) ? e[2] + ((b >> 2) & 1) : 0};
+    u[b] = uf(node_id<D>(g, xb));
+  }
+  if (g.fineop) {
+    const int id = A.ids[fine_cell_index<D>(A, P, g, e, nullptr)];
+    double s = 0.0;
+#pragma unroll
+    for (int b = 0; b < (1 << D); b++) s += u[b];
+    s *= (D == 2) ? 0.25 * A.h * A.h : 0.125 * A.h * A.h * A.h;
+#pragma unroll
+    for (int j = 0; j < 4; j++) part[j] = (j == id) ? s : 0.0;
+  } else {
+    for (int j = 0; j < A.N; j++) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < (1 << D); b++) s += elem_m<D>(A, P, g, e, j, b) * u[b];
+      part[j] = s;
+    }
+  }
+}
+
+// Large constraint counts (banded projector, 2D l >= 4): warp w owns the subcells q = w mod
+// nwarps and sums each over its elements in a fixed order; out: ncon (no per-warp bins).
+template <int D, typename UF>
+__device__ void constraint_apply_owned(const LevelArgs& A, const ProbDesc& P, const Geo<D>& g, const int* eb, UF uf,
+                                       double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  for (int q = wid; q < A.nsub; q += nw) {
+    const int* bx = eb + q * 6;
+    const int cnt = bx[3] * bx[4] * bx[5];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int idx = lane; idx < cnt; idx += 32) {
+      double part[4] = {0.0, 0.0, 0.0, 0.0};
+      cell_constraint_part<D>(A, P, g, bx, idx, uf, part);
+#pragma unroll
+      for (int j = 0; j < 4; j++) acc[j] += part[j];
+    }
+    for (int j = 0; j < A.N; j++) {
+      double v = acc[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULLMASK, v, o);
+      if (lane == 0) out[q * A.N + j] = v;
+    }
+  }
+  __syncthreads();
+}
+
 // c[q*N+j] = sum_{E in R_q} sum_a m_{E,j,a} u(node(E,a)), u given by functor uf(node).
 // eb: subcell boxes (see subcell_boxes); bins: nwarps*ncon scratch; out: ncon.
 template <int D, typename UF>

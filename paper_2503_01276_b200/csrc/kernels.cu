@@ -193,10 +193,11 @@ __global__ void k_transport(LevelArgs A) {
   // C_1 I -> g = g0 - C_1 I
   int* eb = reinterpret_cast<int*>(smem);
   double* bins = smem + 512;  // after int area (1024 ints)
-  double* cI = bins + 32 * A.ncon;
+  double* cI = bins + (A.band > 0 ? 0 : 32 * A.ncon);
   __shared__ int ntask;
   subcell_boxes<D>(A, P, gf, eb, &ntask);
-  constraint_apply<D>(A, P, gf, eb, ntask, [&](int k) { return I[k]; }, bins, cI);
+  if (A.band > 0) constraint_apply_owned<D>(A, P, gf, eb, [&](int k) { return I[k]; }, cI);
+  else constraint_apply<D>(A, P, gf, eb, ntask, [&](int k) { return I[k]; }, bins, cI);
   for (int i = threadIdx.x; i < A.ncon; i += blockDim.x) {
     const int64_t gi = ((int64_t)mp * A.ncon + i) * A.n_rhs + r;
     A.g[gi] = A.g0[gi] - cI[i];
@@ -403,6 +404,154 @@ __global__ void k_proj_setup(LevelArgs A) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Large oversampling (2D windows with more constraint rows than the dense path holds, l >= 4):
+// S = C D^-1 C^T couples only subcells that share nodes, |q1 - q2| <= w + 1 in the lexicographic
+// subcell order, so with rows r = q N + j its half-bandwidth is (w + 2) N - 1.  The equilibrated
+// S~ = Lambda S Lambda (Lambda = diag(S)^-1/2, inactive rows -> identity, as in k_proj_setup) is
+// factored by banded Cholesky in shared memory (one warp, left-looking by columns); k_pcg applies
+// S^-1 = Lambda S~^-1 Lambda by two banded triangular solves.  A pivot below 1e-12 means
+// dependent rows (reading R20), which this path does not handle: flag 8, reported by the host.
+template <int D>
+__global__ void k_proj_setup_band(LevelArgs A) {
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<D> g = level_geo<D>(A, P);
+  extern __shared__ double smem[];
+  const int nc = A.ncon, bw = A.band, B1 = bw + 1;
+  double* Lb = smem;                // nc*B1: Lb[r*B1 + k] = S(r, r-k), then L(r, r-k)
+  double* ds = Lb + nc * B1;        // nc
+  double* scratch = ds + nc;        // 32*16
+  double* tot = scratch + 32 * 16;  // 16
+  int* eb = reinterpret_cast<int*>(tot + 16);
+  double* dinv = A.dinv + P.node_off;
+  for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) {
+    const double dv = 1.0 / diag_node<D>(A, P, g, k);
+    dinv[k] = (D == 2) ? (double)(float)dv : dv;
+  }
+  double* nwt = A.NWt + P.node_off * A.N;
+  for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) {
+    int x[3];
+    node_xyz<D>(g, k, x);
+    double w[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int ep = 0; ep < (1 << D); ep++) {
+      int e[3] = {0, 0, 0};
+      bool ok = true;
+      for (int i = 0; i < D; i++) {
+        e[i] = x[i] - 1 + ((ep >> i) & 1);
+        ok = ok && e[i] >= 0 && e[i] < g.nc[i];
+      }
+      if (!ok) continue;
+      const int a = (~ep) & ((1 << D) - 1);
+      for (int j = 0; j < A.N; j++) w[j] += elem_m<D>(A, P, g, e, j, a);
+    }
+    for (int j = 0; j < A.N; j++) nwt[(int64_t)j * g.nnodes + k] = w[j];
+  }
+  for (int i = threadIdx.x; i < nc * B1; i += blockDim.x) Lb[i] = 0.0;
+  __shared__ int ntask;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  subcell_boxes<D>(A, P, g, eb, &ntask);  // also syncs
+  const int N = A.N;
+  for (int q1 = 0; q1 < A.nsub; q1++) {
+    for (int q2 = q1; q2 < A.nsub; q2++) {
+      const int* b1 = eb + q1 * 6;
+      const int* b2 = eb + q2 * 6;
+      int lo[3], hi[3];
+      bool empty = false;
+      for (int i = 0; i < 3; i++) {
+        if (i >= D) { lo[i] = 0; hi[i] = 0; continue; }
+        if (b1[3 + i] == 0 || b2[3 + i] == 0) { empty = true; break; }
+        lo[i] = max(b1[i], b2[i]);
+        hi[i] = min(b1[i] + b1[3 + i], b2[i] + b2[3 + i]);
+        if (hi[i] < lo[i]) { empty = true; break; }
+      }
+      if (empty) continue;
+      const int ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
+      const int cnt = ex * ey * ez;
+      double v[16];
+      for (int i = 0; i < 16; i++) v[i] = 0.0;
+      for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+        const int x[3] = {lo[0] + idx % ex, lo[1] + (idx / ex) % ey, lo[2] + idx / (ex * ey)};
+        const int k = node_id<D>(g, x);
+        double w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0};
+        for (int ep = 0; ep < (1 << D); ep++) {
+          int e[3] = {0, 0, 0};
+          bool ok = true;
+          for (int i = 0; i < D; i++) {
+            e[i] = x[i] - 1 + ((ep >> i) & 1);
+            ok = ok && e[i] >= 0 && e[i] < g.nc[i];
+          }
+          if (!ok) continue;
+          const int q = elem_subcell<D>(A, P, g, e);
+          if (q != q1 && q != q2) continue;
+          const int a = (~ep) & ((1 << D) - 1);
+          for (int j = 0; j < N; j++) {
+            const double m = elem_m<D>(A, P, g, e, j, a);
+            if (q == q1) w1[j] += m;
+            if (q == q2) w2[j] += m;
+          }
+        }
+        const double di = dinv[k];
+        for (int j1 = 0; j1 < N; j1++)
+          for (int j2 = 0; j2 < N; j2++) v[j1 * 4 + j2] += w1[j1] * w2[j2] * di;
+      }
+      block_sum<16>(v, scratch, tot);
+      if (threadIdx.x == 0) {
+        for (int j1 = 0; j1 < N; j1++)
+          for (int j2 = 0; j2 < N; j2++) {
+            const int r1 = q1 * N + j1, r2 = q2 * N + j2;
+            const int r = max(r1, r2), c = min(r1, r2);
+            if (r - c > bw) {
+              if (tot[j1 * 4 + j2] != 0.0) bad = 1;
+            } else {
+              Lb[r * B1 + (r - c)] = tot[j1 * 4 + j2];
+            }
+          }
+      }
+      __syncthreads();
+    }
+  }
+  const double* meas = A.meas + (int64_t)mp * nc;
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+    const bool act = meas[i] > 0.0 && Lb[i * B1] > 0.0;
+    ds[i] = act ? 1.0 / sqrt(Lb[i * B1]) : 0.0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nc * B1; idx += blockDim.x) {
+    const int r = idx / B1, k = idx - r * B1, c = r - k;
+    if (c < 0) Lb[idx] = 0.0;
+    else if (ds[r] == 0.0 || ds[c] == 0.0) Lb[idx] = (k == 0) ? 1.0 : 0.0;
+    else Lb[idx] *= ds[r] * ds[c];
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // banded Cholesky, left-looking by columns
+    const int lane = threadIdx.x;
+    for (int j = 0; j < nc; j++) {
+      double sq = 0.0;
+      for (int k = 1 + lane; k <= min(bw, j); k += 32) sq += Lb[j * B1 + k] * Lb[j * B1 + k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(FULLMASK, sq, o);
+      const double d = Lb[j * B1] - sq;
+      if (!(d > 1e-12) && lane == 0) bad = 2;
+      const double ljj = sqrt(fmax(d, 1e-300));
+      __syncwarp();
+      if (lane == 0) Lb[j * B1] = ljj;
+      for (int i = j + 1 + lane; i <= min(j + bw, nc - 1); i += 32) {
+        double sv = Lb[i * B1 + (i - j)];
+        for (int m = max(i - bw, 0); m < j; m++) sv -= Lb[i * B1 + (i - m)] * Lb[j * B1 + (j - m)];
+        Lb[i * B1 + (i - j)] = sv / ljj;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (bad && threadIdx.x == 0) atomicOr(&A.flags[mp], 8);
+  double* out = A.Sinv + (int64_t)mp * nc * B1;
+  for (int idx = threadIdx.x; idx < nc * B1; idx += blockDim.x) out[idx] = Lb[idx];
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) A.pinv_ds[(int64_t)mp * nc + i] = ds[i];
+}
+
+// ---------------------------------------------------------------------------------------
 // Reading R20: S^+ = Lambda S~^+ Lambda with S~ = V diag(lambda) V^T, eigenvalues
 // below 1e-11 lambda_max dropped.  One warp per flagged window: parallel cyclic Jacobi with the
 // round-robin ordering (each round rotates nc/2 disjoint pairs at once: lane k owns pair k),
@@ -513,14 +662,21 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
   const ProbDesc& P = A.probs[mp];
   const Geo<D> g = level_geo<D>(A, P);
   const int nc = A.ncon;
+  const bool band = A.band > 0;
+  const int B1 = A.band + 1;
   extern __shared__ double smem[];
-  double* Si = smem;                  // nc*nc
-  double* yhat = Si + nc * nc;        // nc
-  double* cvec = yhat + nc;           // nc
-  double* tg = cvec + nc;             // nc
-  double* bins = tg + nc;             // 32*nc
-  double* scratch = bins + 32 * nc;   // 32*4
-  double* tot = scratch + 32 * 4;     // 4
+  // dense: S^-1 (nc*nc) and per-warp constraint bins (32*nc); band: the banded Cholesky factor
+  // (nc*B1) and its row scales, constraint sums owned per subcell (no bins)
+  double* Si = smem;
+  double* ds = Si + (band ? nc * B1 : nc * nc);  // band only: nc
+  double* yhat = ds + (band ? nc : 0);           // nc
+  double* cvec = yhat + nc;                       // nc
+  double* tg = cvec + nc;                         // nc
+  double* gcol = tg + nc;                         // nc
+  double* g0col = gcol + nc;                      // nc
+  double* bins = g0col + nc;                      // dense: 32*nc
+  double* scratch = bins + (band ? 0 : 32 * nc);  // 32*4
+  double* tot = scratch + 32 * 4;                 // 4
   int* eb = reinterpret_cast<int*>(tot + 4);
   __shared__ int ntask;
 
@@ -532,17 +688,52 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
   const double* b = (A.level >= 2) ? A.B + P.vec_off + (int64_t)r * nn : nullptr;
   const double* dinv = A.dinv + P.node_off;
   const double* nwt = A.NWt + P.node_off * A.N;
-  for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Si[i] = A.Sinv[(int64_t)mp * nc * nc + i];
+  if (band) {
+    for (int i = threadIdx.x; i < nc * B1; i += blockDim.x) Si[i] = A.Sinv[(int64_t)mp * nc * B1 + i];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) ds[i] = A.pinv_ds[(int64_t)mp * nc + i];
+  } else {
+    for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Si[i] = A.Sinv[(int64_t)mp * nc * nc + i];
+  }
   subcell_boxes<D>(A, P, g, eb, &ntask);
 
   auto sinv_apply = [&](const double* in, double* out) {
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-      double s = 0.0;
-      for (int j = 0; j < nc; j++) s += Si[i * nc + j] * in[j];
-      out[i] = s;
+    if (band) {  // out = Lambda L^-T L^-1 Lambda in (warp 0; in != out)
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x, bw = A.band;
+        for (int i = lane; i < nc; i += 32) out[i] = ds[i] * in[i];
+        __syncwarp();
+        for (int r = 0; r < nc; r++) {
+          double sv = 0.0;
+          for (int k = 1 + lane; k <= min(bw, r); k += 32) sv += Si[r * B1 + k] * out[r - k];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(FULLMASK, sv, o);
+          if (lane == 0) out[r] = (out[r] - sv) / Si[r * B1];
+          __syncwarp();
+        }
+        for (int r = nc - 1; r >= 0; r--) {
+          double sv = 0.0;
+          for (int k = 1 + lane; k <= bw && r + k < nc; k += 32) sv += Si[(r + k) * B1 + k] * out[r + k];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(FULLMASK, sv, o);
+          if (lane == 0) out[r] = (out[r] - sv) / Si[r * B1];
+          __syncwarp();
+        }
+        for (int i = lane; i < nc; i += 32) out[i] *= ds[i];
+      }
+    } else {
+      for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < nc; j++) s += Si[i * nc + j] * in[j];
+        out[i] = s;
+      }
     }
     __syncthreads();
   };
+  auto capply = [&](auto&& uf, double* out) {
+    if (band) constraint_apply_owned<D>(A, P, g, eb, uf, out);
+    else constraint_apply<D>(A, P, g, eb, ntask, uf, bins, out);
+  };
+
   // init: x = D^-1 C^T S^-1 t, r = A x - b (unprojected), c = C D^-1 r, yhat = S^-1 c.
   // returns r^T D^-1 r of the unprojected residual
   auto init = [&](const double* targets, const double* bb) -> double {
@@ -559,14 +750,13 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
     }
     block_sum<1>(v, scratch, tot);
     const double rr = tot[0];
-    constraint_apply<D>(A, P, g, eb, ntask, [&](int k) { return dinv[k] * rv[k]; }, bins, cvec);
+    capply([&](int k) { return dinv[k] * rv[k]; }, cvec);
     sinv_apply(cvec, yhat);
     return rr;
   };
 
   // targets of this rhs: column r of g (or g0 at level 1)
   const double* gsrc = (A.level >= 2) ? A.g : A.g0;
-  __shared__ double gcol[128], g0col[128];
   for (int i = threadIdx.x; i < nc; i += blockDim.x) {
     gcol[i] = gsrc[((int64_t)mp * nc + i) * A.n_rhs + r];
     g0col[i] = A.g0[((int64_t)mp * nc + i) * A.n_rhs + r];
@@ -631,14 +821,14 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
     }
     block_sum<1>(u, scratch, tot);
     const double rr = tot[0];
-    constraint_apply<D>(A, P, g, eb, ntask, [&](int k) { return dinv[k] * rv[k]; }, bins, cvec);
+    capply([&](int k) { return dinv[k] * rv[k]; }, cvec);
     sinv_apply(cvec, yhat);
     double cy = 0.0;
     for (int j = 0; j < nc; j++) cy += cvec[j] * yhat[j];
     beta = (rr - cy) / rz;
   }
   // feasibility restoration: x += D^-1 C^T S^-1 (g - C x)
-  constraint_apply<D>(A, P, g, eb, ntask, [&](int k) { return x[k]; }, bins, cvec);
+  capply([&](int k) { return x[k]; }, cvec);
   for (int i = threadIdx.x; i < nc; i += blockDim.x) tg[i] = gcol[i] - cvec[i];
   __syncthreads();
   sinv_apply(tg, yhat);
@@ -798,9 +988,15 @@ __global__ void k_validate(const double* kappa, const uint8_t* ids, int64_t cnt,
 
 // ---------------------------------------------------------------------------------------
 // host launchers
-static size_t pcg_smem(const LevelArgs& A) {
-  const int nc = A.ncon;
-  return sizeof(double) * ((size_t)nc * nc + 3 * nc + 32 * nc + 32 * 4 + 4) + sizeof(int) * (A.nsub * 7 + 2);
+size_t pcg_smem(const LevelArgs& A) {
+  const size_t nc = A.ncon;
+  const size_t mat = (A.band > 0) ? nc * (A.band + 1) + nc : nc * nc + 32 * nc;
+  return sizeof(double) * (mat + 5 * nc + 32 * 4 + 4) + sizeof(int) * (A.nsub * 7 + 2);
+}
+
+size_t proj_setup_band_smem(const LevelArgs& A) {
+  const size_t nc = A.ncon;
+  return sizeof(double) * (nc * (A.band + 1) + nc + 32 * 16 + 16) + sizeof(int) * (A.nsub * 7 + 2);
 }
 
 cudaError_t launch_level_ops(const LevelArgs& A, cudaStream_t st) {
@@ -819,7 +1015,7 @@ cudaError_t launch_targets(const LevelArgs& A, cudaStream_t st) {
 }
 
 cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
-  const size_t sm = sizeof(double) * (512 + 32 * A.ncon + A.ncon);
+  const size_t sm = sizeof(double) * (512 + (A.band > 0 ? 0 : 32 * A.ncon) + A.ncon);
   const unsigned grid = (unsigned)A.nprob_mp * A.n_rhs;
   if (A.D == 2) k_transport<2><<<grid, threads, sm, st>>>(A);
   else k_transport<3><<<grid, threads, sm, st>>>(A);
@@ -827,6 +1023,14 @@ cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
 }
 
 cudaError_t launch_proj_setup(const LevelArgs& A, int threads, cudaStream_t st) {
+  if (A.band > 0) {
+    if (A.D != 2) return cudaErrorInvalidValue;
+    const size_t sm = proj_setup_band_smem(A);
+    cudaError_t e = cudaFuncSetAttribute(k_proj_setup_band<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    k_proj_setup_band<2><<<A.nprob_mp, threads, sm, st>>>(A);
+    return cudaGetLastError();
+  }
   const size_t sm = sizeof(double) * (2 * (size_t)A.ncon * A.ncon + 32 * 16 + 16 + (A.nsub * 7 + 2 + 1) / 2 + 2);
   cudaError_t e;
   if (A.D == 2) {
@@ -841,6 +1045,7 @@ cudaError_t launch_proj_setup(const LevelArgs& A, int threads, cudaStream_t st) 
 }
 
 cudaError_t launch_pinv(const LevelArgs& A, cudaStream_t st) {
+  if (A.band > 0) return cudaSuccess;  // the banded projector reports dependent rows instead (flag 8)
   const int m = (A.ncon + 1) & ~1;
   const size_t sm = sizeof(double) * 2 * (size_t)m * m + sizeof(int) * m;
   cudaError_t e = cudaFuncSetAttribute(k_pinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

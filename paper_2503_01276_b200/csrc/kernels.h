@@ -48,3 +48,9 @@ cudaError_t launch_fine_block_avg(int D, const double* u, const uint8_t* ids, co
                                   int N, double* out, cudaStream_t st);
 // 3D transport split (levels >= 2): Y = A_1 I_p and g = g0 - C_1 I_p on the fine window
 cudaError_t launch_tapply3d(const LevelArgs& A, cudaStream_t st);
+// dynamic shared memory of k_pcg / k_proj_setup_band at these arguments
+size_t pcg_smem(const LevelArgs& A);
+size_t proj_setup_band_smem(const LevelArgs& A);
+// dynamic shared memory of k_pcg / k_proj_setup_band at these arguments
+size_t pcg_smem(const LevelArgs& A);
+size_t proj_setup_band_smem(const LevelArgs& A);

@@ -110,6 +110,7 @@ struct mch_ctx {
   bool has_source = false;
   int* h_mit = nullptr;
   double* h_mrel = nullptr;
+  int band = 0;      // > 0: banded projector (large oversampling, 2D), half-bandwidth
   int pcg_mode = 0;  // 0: on-chip 2D PCG where it applies; 1: generic k_pcg; 2: on-chip, precomputed operator at level 1
 };
 
@@ -167,11 +168,22 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   if (p.rank < 0 || p.rank >= p.world) return fail(nullptr, MCH_EINVAL, "bad rank/world");
   const int w = 2 * p.oversample + 1;
   const int nsub = (p.d == 2) ? w * w : w * w * w;
-  if (nsub * p.num_continua > 108) return fail(nullptr, MCH_EINVAL, "too many constraint rows (>108)");
+  // more than 108 constraint rows (or MCH_FORCE_BAND): 2D only, banded projector (k_proj_setup_band)
+  const int nrows = nsub * p.num_continua;
+  const bool want_band = nrows > 108 || (p.d == 2 && getenv("MCH_FORCE_BAND") != nullptr);
+  int band = 0;
+  if (want_band) {
+    if (p.d != 2) return fail(nullptr, MCH_EINVAL, "too many constraint rows (>108) for a 3D window");
+    band = (w + 2) * p.num_continua - 1;
+    const size_t need = sizeof(double) * ((size_t)nrows * (band + 1) + 6 * (size_t)nrows + 32 * 16 + 16) +
+                        sizeof(int) * (nsub * 7 + 2);
+    if (need > 232448) return fail(nullptr, MCH_EINVAL, "too many constraint rows for the banded projector");
+  }
   if (p.n > (1 << 20)) return fail(nullptr, MCH_EINVAL, "n too large");
 
   mch_ctx* c = new mch_ctx();
   c->p = p;
+  c->band = band;
   c->D = p.d;
   c->N = p.num_continua;
   c->n_rhs = p.num_continua * (1 + p.d);
@@ -380,7 +392,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     CKC(c, cudaMemcpy(B->descs.ptr, descs.data(), sizeof(ProbDesc) * nmp, cudaMemcpyHostToDevice));
     // on-chip 2D PCG (pcg2d.cu) unless MCH_PCG=old; MCH_PCG=gn forces the precomputed-operator
     // variant at level 1 as well (cross-check of the two operator paths)
-    if ((D == 2) && N <= 3 && nc == 9 * N && c->pcg_mode != 1) {  // 3x3 subcells (l = 1)
+    if ((D == 2) && N <= 3 && nc == 9 * N && c->pcg_mode != 1 && c->band == 0) {  // 3x3 subcells (l = 1)
       int maxn = 0;
       for (int i = 0; i < nmp; i++) maxn = std::max(maxn, std::max(descs[i].nc[0], descs[i].nc[1]) + 1);
       std::vector<int> cands;
@@ -512,6 +524,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.coff = (int)pl.coff(); A.gn = gn; A.h = 1.0 / (double)pl.n; A.inv_c = 1.0f / (float)pl.c;
   A.kappa = c->kappa; A.ids = c->ids; A.pool = c->pool; A.G = c->G;
   A.f = c->has_source ? c->fsrc.as<double>() : nullptr;
+  A.band = c->band;
   A.bload = c->bload.as<double>();
   A.rtol = c->p.rtol; A.max_iter = c->p.max_iter;
   if (level >= 2) {
@@ -620,6 +633,12 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     for (int i = 0; i < B.nmp; i++) {
       const MacroHost& m = pl.all[B.mps[i]];
       if (B.h_flags[i] & 4) S.rank_deficient++;  // k_pinv truncated eigenvalues (reading R20)
+      if (B.h_flags[i] & 8) {
+        char buf[200];
+        snprintf(buf, sizeof buf, "dependent constraint rows at macropoint (%d,%d,%d): the banded projector of "
+                 "large oversampling does not handle reading R20", m.k[0], m.k[1], m.k[2]);
+        return fail(c, MCH_ERANK, buf);
+      }
       if (B.h_flags[i] & 1) {
         char buf[200];
         snprintf(buf, sizeof buf, "continuum absent from K_p of macropoint (%d,%d,%d)", m.k[0], m.k[1], m.k[2]);

@@ -58,6 +58,8 @@ struct LevelArgs {
   double* FI; double* FY;  // fine workspace (levels >= 2): I_p / phi and A1 I_p
   double* pool;            // parent pool
   double* G;               // [(M+1)^D][n_rhs][n_rhs]
+  int band;                // 0: dense S^-1 per macropoint; > 0: banded Cholesky factor of the
+                           //  equilibrated S (half-bandwidth band, 2D large l), Sinv[mp][nc][band+1]
   int tphase;              // k_transport: 0 all phases; 1 only I_p; 2 only the restriction (3D split path)
   const double* f;         // NEXT-2: cellwise source, n^D, x fastest (NULL: no load vectors)
   double* bload;           // NEXT-2: [P][N] load vectors b_j = int_{K_p} f phi_j (Eq. 7)

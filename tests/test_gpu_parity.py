@@ -392,3 +392,48 @@ def test_type_errors_end_to_end():
     for a, b in zip(eg, eo):
         assert np.all(np.abs(a - b) <= 1e-6 * np.maximum(b, 1e-12)), (eg, eo)
     assert np.all(eo[2] < 0.05 * np.minimum(eo[0], eo[1])), eo
+
+
+@pytest.mark.parametrize("layout,n,M,L", [("vertex", 64, 8, 1), ("vertex", 96, 12, 2), ("block", 80, 10, 1)])
+def test_large_oversampling_banded_projector(layout, n, M, L):
+    """NEXT-1 general l (PAPER.md:533 uses l = ceil(-2 ln H) = 5-8): l = 4 gives 9x9 subcells and
+    162 constraint rows (N = 2), beyond the dense projector; the banded Cholesky path
+    (k_proj_setup_band + banded solves in k_pcg) vs the oracle at every macropoint."""
+    H = _gpu()
+    d, N, l = 2, 2, 4
+    for seed in range(900, 940):
+        kap, ids = random_medium(d, n, N, seed=seed, block=2)
+        try:
+            o = Oracle(d, n, M, L, 2, N, kap, ids, l=l, layout=layout)
+            for k in o.plan.all_vertices():
+                o.local_system(k)
+            break
+        except RuntimeError:
+            continue
+    Go = o.effective_coeffs()
+    with H(d, n, N, M, L, 2, kap, ids, l=l, keep_all=True, layout=layout) as h:
+        h.solve_all()
+        Gg = h.effective_coeffs()
+        for k in o.plan.all_vertices():
+            i = o.plan.linear_index(k)
+            assert g_err(Gg[i], Go[i]) < G_TOL, (k, g_err(Gg[i], Go[i]))
+            po = o.solve(k)["phi"]
+            for r in range(o.n_rhs):
+                assert phi_err(h.local_solution(k, r), po[r]) < PHI_TOL
+
+
+def test_banded_projector_matches_dense(monkeypatch):
+    """MCH_FORCE_BAND: the banded projector on a 2D l = 2 problem (50 rows, normally dense) gives
+    the dense path's coefficients to 1e-10 (same constrained problems, different factorisation)."""
+    H = _gpu()
+    d, n, M, L, N = 2, 64, 8, 2, 2
+    kap, ids = _admissible(d, n, M, N, 950)
+    with H(d, n, N, M, L, 2, kap, ids, l=2) as h:
+        h.solve_all()
+        Gd = h.effective_coeffs()
+    monkeypatch.setenv("MCH_FORCE_BAND", "1")
+    with H(d, n, N, M, L, 2, kap, ids, l=2) as h:
+        h.solve_all()
+        Gb = h.effective_coeffs()
+    for i in range(Gd.shape[0]):
+        assert g_err(Gb[i], Gd[i]) < 1e-10, (i, g_err(Gb[i], Gd[i]))
