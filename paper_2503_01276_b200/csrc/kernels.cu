@@ -192,7 +192,7 @@ __global__ void k_transport(LevelArgs A) {
   for (int k = threadIdx.x; k < gf.nnodes; k += blockDim.x) Y[k] = apply_node<D>(A, P, gf, I, k);
   // C_1 I -> g = g0 - C_1 I
   int* eb = reinterpret_cast<int*>(smem);
-  double* bins = smem + 512;  // after int area (1024 ints)
+  double* bins = smem + (A.nsub * 7 + 2 + 1) / 2;  // after the subcell-box int area (nsub*7+2 ints)
   double* cI = bins + (A.band > 0 ? 0 : 32 * A.ncon);
   __shared__ int ntask;
   subcell_boxes<D>(A, P, gf, eb, &ntask);
@@ -1015,7 +1015,7 @@ cudaError_t launch_targets(const LevelArgs& A, cudaStream_t st) {
 }
 
 cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
-  const size_t sm = sizeof(double) * (512 + (A.band > 0 ? 0 : 32 * A.ncon) + A.ncon);
+  const size_t sm = sizeof(double) * ((A.nsub * 7 + 2 + 1) / 2 + (A.band > 0 ? 0 : 32 * A.ncon) + A.ncon);
   const unsigned grid = (unsigned)A.nprob_mp * A.n_rhs;
   if (A.D == 2) k_transport<2><<<grid, threads, sm, st>>>(A);
   else k_transport<3><<<grid, threads, sm, st>>>(A);
