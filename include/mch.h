@@ -71,6 +71,13 @@ typedef struct {
                               k in {0..M}^d (reading R1); MCH_LAYOUT_BLOCK (1) = block centres
                               x_p = (k + 1/2) H, k in {0..M-1}^d, K_p the block, T_n as in the
                               paper's Figures 2-3 */
+  /* optional device allocator for every buffer the context owns (e.g. PyTorch's caching
+     allocator, so the framework's pool holds the memory); both NULL: cudaMalloc / cudaFree.
+     alloc(bytes, stream, alloc_user) returns a device pointer or NULL (-> MCH_ENOMEM);
+     free(ptr, stream, alloc_user).  stream is params.stream. */
+  void*  (*alloc)(size_t bytes, void* stream, void* user);
+  void   (*free)(void* ptr, void* stream, void* user);
+  void*    alloc_user;
 } mch_params;
 
 #define MCH_INTERP_DLINEAR    0

@@ -28,7 +28,29 @@ class MchParams(ctypes.Structure):
                 ("M", ctypes.c_int64), ("levels", ctypes.c_int), ("eta", ctypes.c_int),
                 ("oversample", ctypes.c_int), ("rtol", ctypes.c_double), ("max_iter", ctypes.c_int),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("keep_all", ctypes.c_int),
-                ("stream", ctypes.c_void_p), ("interp", ctypes.c_int), ("layout", ctypes.c_int)]
+                ("stream", ctypes.c_void_p), ("interp", ctypes.c_int), ("layout", ctypes.c_int),
+                ("alloc", ctypes.c_void_p), ("free", ctypes.c_void_p), ("alloc_user", ctypes.c_void_p)]
+
+
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+def torch_allocator():
+    """(alloc, free) C callbacks routing the library's device buffers through PyTorch's caching
+    allocator.  Keep the returned objects alive as long as any context created with them."""
+    import torch
+
+    def _alloc(nbytes, stream, user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), stream=int(stream or 0))
+        except Exception:  # out of memory -> NULL -> MCH_ENOMEM
+            return None
+
+    def _free(ptr, stream, user):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    return ALLOC_FN(_alloc), FREE_FN(_free)
 
 
 class MchLevelStats(ctypes.Structure):

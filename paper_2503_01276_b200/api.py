@@ -44,8 +44,9 @@ LAYOUT = {"vertex": 0, "block": 1}
 
 def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversample=1, rtol=1e-12,
                max_iter=20000, rank=0, world=1, keep_all=False, stream=None, interp="dlinear",
-               layout="vertex"):
-    """Returns an opaque context handle (ctypes.c_void_p)."""
+               layout="vertex", allocator=None):
+    """Returns an opaque context handle (ctypes.c_void_p).  allocator: None (cudaMalloc) or an
+    (alloc, free) pair of _native.ALLOC_FN / FREE_FN callbacks, e.g. _native.torch_allocator()."""
     if isinstance(kappa, np.ndarray):
         kappa = np.ascontiguousarray(kappa, dtype=np.float64)
         continuum_id = np.ascontiguousarray(continuum_id, dtype=np.uint8)
@@ -57,6 +58,9 @@ def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversamp
                   oversample=oversample, rtol=rtol, max_iter=max_iter, rank=rank, world=world,
                   keep_all=int(keep_all), stream=stream if stream is not None else _current_stream(),
                   interp=INTERP[interp], layout=LAYOUT[layout])
+    if allocator is not None:
+        p.alloc = ctypes.cast(allocator[0], ctypes.c_void_p)
+        p.free = ctypes.cast(allocator[1], ctypes.c_void_p)
     ctx = ctypes.c_void_p()
     check(lib.mch_create(ctypes.byref(p), kp, ip, kdev, ctypes.byref(ctx)), None)
     return ctx
@@ -131,14 +135,17 @@ class Homogenizer:
     """Hierarchical multicontinuum homogenization hot path on one GPU (or one rank's shard)."""
 
     def __init__(self, d, n, N, M, L, eta, kappa, ids, l=1, rtol=1e-12, max_iter=20000, rank=0,
-                 world=1, keep_all=False, stream=None, interp="dlinear", layout="vertex"):
+                 world=1, keep_all=False, stream=None, interp="dlinear", layout="vertex",
+                 torch_memory=False):
         self.d, self.n, self.N, self.M, self.L, self.eta, self.l = d, n, N, M, L, eta, l
         self.n_rhs = N * (1 + d)
         self.mv = M + 1 if layout == "vertex" else M  # macropoints per dimension
         self.num_macropoints = self.mv ** d
+        # torch_memory: every device buffer of the context comes from PyTorch's caching allocator
+        self._allocator = _native.torch_allocator() if torch_memory else None
         self.ctx = mch_create(d, n, N, M, L, eta, kappa, ids, oversample=l, rtol=rtol,
                               max_iter=max_iter, rank=rank, world=world, keep_all=keep_all,
-                              stream=stream, interp=interp, layout=layout)
+                              stream=stream, interp=interp, layout=layout, allocator=self._allocator)
         self.solved = 0
 
     @classmethod

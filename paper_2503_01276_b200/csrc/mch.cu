@@ -19,21 +19,46 @@ namespace {
 
 thread_local std::string g_create_error;
 
+// Device allocations go through the caller's allocator when mch_params supplies one (e.g.
+// PyTorch's caching allocator), else cudaMalloc / cudaFree.
+struct DevAlloc {
+  void* (*alloc)(size_t, void*, void*) = nullptr;
+  void (*free)(void*, void*, void*) = nullptr;
+  void* user = nullptr;
+  void* stream = nullptr;
+};
+
+cudaError_t dev_alloc(const DevAlloc* a, void** p, size_t bytes) {
+  if (a && a->alloc) {
+    *p = a->alloc(bytes, a->stream, a->user);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  return cudaMalloc(p, bytes);
+}
+
+void dev_free(const DevAlloc* a, void* p) {
+  if (!p) return;
+  if (a && a->free) a->free(p, a->stream, a->user);
+  else cudaFree(p);
+}
+
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
+  const DevAlloc* al = nullptr;
   cudaError_t ensure(size_t want) {
     if (want <= bytes && ptr) return cudaSuccess;
-    if (ptr) cudaFree(ptr);
+    dev_free(al, ptr);
     ptr = nullptr;
     bytes = 0;
     size_t alloc = std::max<size_t>(want, 256);
-    cudaError_t e = cudaMalloc(&ptr, alloc);
+    cudaError_t e = dev_alloc(al, &ptr, alloc);
     if (e == cudaSuccess) bytes = alloc;
+    else ptr = nullptr;
     return e;
   }
   void release() {
-    if (ptr) cudaFree(ptr);
+    dev_free(al, ptr);
     ptr = nullptr;
     bytes = 0;
   }
@@ -107,6 +132,12 @@ struct mch_ctx {
   // NEXT-2: source f (cellwise, n^D), load vectors [P][N], macro-solve workspace and results
   DevBuf fsrc, bload, mws, mG, mb, mU, mres;
   DevBuf fws, fbar, ff, fu, fkbox, fout;  // NEXT-3 fine solve / block averages
+  DevAlloc al;
+  std::vector<DevBuf*> bufs() {
+    return {&STC, &MLR, &pinv_ds, &W, &Mc, &g0, &g, &meas, &cm, &flags, &dinv, &nwt, &Sinv, &X, &R, &P, &Q, &B,
+            &FI, &FY, &iters, &relres, &diag, &fsrc, &bload, &mws, &mG, &mb, &mU, &mres, &fws, &fbar, &ff, &fu,
+            &fkbox, &fout};
+  }
   bool has_source = false;
   int* h_mit = nullptr;
   double* h_mrel = nullptr;
@@ -184,6 +215,15 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   mch_ctx* c = new mch_ctx();
   c->p = p;
   c->band = band;
+  if ((p.alloc == nullptr) != (p.free == nullptr)) {
+    delete c;
+    return fail(nullptr, MCH_EINVAL, "alloc and free must both be given or both be NULL");
+  }
+  c->al.alloc = p.alloc;
+  c->al.free = p.free;
+  c->al.user = p.alloc_user;
+  c->al.stream = p.stream;
+  for (DevBuf* b : c->bufs()) b->al = &c->al;
   c->D = p.d;
   c->N = p.num_continua;
   c->n_rhs = p.num_continua * (1 + p.d);
@@ -237,8 +277,8 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
     return fail(nullptr, code, m);
   };
   cudaError_t e;
-  if ((e = cudaMalloc(&c->kappa, cells * sizeof(double))) != cudaSuccess) return cleanup(MCH_ENOMEM, "kappa alloc");
-  if ((e = cudaMalloc(&c->ids, cells)) != cudaSuccess) return cleanup(MCH_ENOMEM, "ids alloc");
+  if ((e = dev_alloc(&c->al, (void**)&c->kappa, cells * sizeof(double))) != cudaSuccess) return cleanup(MCH_ENOMEM, "kappa alloc");
+  if ((e = dev_alloc(&c->al, (void**)&c->ids, cells)) != cudaSuccess) return cleanup(MCH_ENOMEM, "ids alloc");
   const cudaMemcpyKind kind = on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   if ((e = cudaMemcpyAsync(c->kappa, kappa, cells * sizeof(double), kind, c->st)) != cudaSuccess)
     return cleanup(MCH_ECUDA, std::string("kappa copy: ") + cudaGetErrorString(e));
@@ -246,13 +286,13 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
     return cleanup(MCH_ECUDA, std::string("ids copy: ") + cudaGetErrorString(e));
   if (on_dev) {
     int* bad = nullptr;
-    if (cudaMalloc(&bad, sizeof(int)) != cudaSuccess) return cleanup(MCH_ENOMEM, "alloc");
+    if (dev_alloc(&c->al, (void**)&bad, sizeof(int)) != cudaSuccess) return cleanup(MCH_ENOMEM, "alloc");
     cudaMemsetAsync(bad, 0, sizeof(int), c->st);
     launch_validate(c->kappa, c->ids, cells, p.num_continua, bad, c->st);
     int hb = 0;
     cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->st);
     e = cudaStreamSynchronize(c->st);
-    cudaFree(bad);
+    dev_free(&c->al, bad);
     if (e != cudaSuccess) return cleanup(MCH_ECUDA, cudaGetErrorString(e));
     if (hb) return cleanup(MCH_EINVAL, "kappa must be positive and finite; ids < num_continua");
   }
@@ -276,9 +316,9 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
     }
   }
   c->pool_len = off;
-  if (off > 0 && cudaMalloc(&c->pool, off * sizeof(double)) != cudaSuccess) return cleanup(MCH_ENOMEM, "pool alloc");
+  if (off > 0 && dev_alloc(&c->al, (void**)&c->pool, off * sizeof(double)) != cudaSuccess) return cleanup(MCH_ENOMEM, "pool alloc");
   const size_t gbytes = (size_t)nmac * c->n_rhs * c->n_rhs * sizeof(double);
-  if (cudaMalloc(&c->G, gbytes) != cudaSuccess) return cleanup(MCH_ENOMEM, "G alloc");
+  if (dev_alloc(&c->al, (void**)&c->G, gbytes) != cudaSuccess) return cleanup(MCH_ENOMEM, "G alloc");
   cudaMemsetAsync(c->G, 0, gbytes, c->st);
   c->stats.assign(p.levels + 1, mch_level_stats{});
   for (int i = 0; i < 8; i++) cudaEventCreate(&c->ev[i]);
@@ -336,6 +376,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       bend++;
     }
     std::unique_ptr<LevelBatch> B(new LevelBatch());
+    B->descs.al = B->segs.al = B->nseg.al = &c->al;
     const int nmp = (int)(bend - bstart);
     B->nmp = nmp;
     std::vector<ProbDesc> descs(nmp);
@@ -695,7 +736,7 @@ extern "C" int mch_set_medium(mch_ctx* c, const double* kappa, const uint8_t* id
   CKC(c, cudaMemcpyAsync(c->ids, ids, cells, kind, c->st));
   // validation on the device (no host pass over the inputs), one pinned flag read back
   if (!c->h_bad) CKC(c, cudaMallocHost(&c->h_bad, sizeof(int)));
-  if (!c->d_bad) CKC(c, cudaMalloc(&c->d_bad, sizeof(int)));
+  if (!c->d_bad) CKC(c, dev_alloc(&c->al, (void**)&c->d_bad, sizeof(int)));
   CKC(c, cudaMemsetAsync(c->d_bad, 0, sizeof(int), c->st));
   CKC(c, launch_validate(c->kappa, c->ids, cells, c->N, c->d_bad, c->st));
   CKC(c, cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
@@ -978,20 +1019,17 @@ extern "C" void mch_destroy(mch_ctx* c) {
   if (!c) return;
   if (c->st) cudaStreamSynchronize(c->st);
   else cudaDeviceSynchronize();
-  cudaFree(c->kappa);
-  cudaFree(c->ids);
-  cudaFree(c->pool);
-  cudaFree(c->G);
+  dev_free(&c->al, c->kappa);
+  dev_free(&c->al, c->ids);
+  dev_free(&c->al, c->pool);
+  dev_free(&c->al, c->G);
   c->lplans.clear();
   if (c->h_bad) cudaFreeHost(c->h_bad);
   if (c->h_mit) cudaFreeHost(c->h_mit);
   if (c->h_mrel) cudaFreeHost(c->h_mrel);
-  if (c->d_bad) cudaFree(c->d_bad);
-  DevBuf* bufs[] = {&c->STC, &c->MLR, &c->pinv_ds, &c->W, &c->Mc, &c->g0, &c->g, &c->meas, &c->cm, &c->flags, &c->dinv, &c->nwt, &c->Sinv,
-                    &c->X, &c->R, &c->P, &c->Q, &c->B, &c->FI, &c->FY, &c->iters, &c->relres, &c->diag,
-                    &c->fsrc, &c->bload, &c->mws, &c->mG, &c->mb, &c->mU, &c->mres,
-                    &c->fws, &c->fbar, &c->ff, &c->fu, &c->fkbox, &c->fout};
-  for (DevBuf* b : bufs) b->release();
+  if (c->d_bad) dev_free(&c->al, c->d_bad);
+  for (DevBuf* b : c->bufs()) b->release();
+  // (LevelBatch buffers are released by lplans.clear() above)
   if (c->events)
     for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);
   delete c;

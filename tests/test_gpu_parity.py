@@ -437,3 +437,27 @@ def test_banded_projector_matches_dense(monkeypatch):
         Gb = h.effective_coeffs()
     for i in range(Gd.shape[0]):
         assert g_err(Gb[i], Gd[i]) < 1e-10, (i, g_err(Gb[i], Gd[i]))
+
+
+def test_torch_caching_allocator_hooks():
+    """mch_params.alloc/free (SURVEY §8(b) ownership): with PyTorch's caching allocator every
+    library buffer is accounted by torch (memory_allocated grows while the context lives and
+    returns after close) and the coefficients are bitwise those of the cudaMalloc path."""
+    import torch
+    H = _gpu()
+    d, n, M, L, N = 2, 64, 8, 2, 2
+    kap, ids = _admissible(d, n, M, N, 960)
+    with H(d, n, N, M, L, 2, kap, ids) as h:
+        h.solve_all()
+        G0 = h.effective_coeffs()
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    h = H(d, n, N, M, L, 2, kap, ids, torch_memory=True)
+    h.solve_all()
+    G1 = h.effective_coeffs()
+    during = torch.cuda.memory_allocated()
+    h.close()
+    torch.cuda.synchronize()
+    after = torch.cuda.memory_allocated()
+    assert during > before and after == before, (before, during, after)
+    assert np.array_equal(G0, G1)
