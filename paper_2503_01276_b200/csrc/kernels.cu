@@ -344,6 +344,19 @@ __global__ void k_proj_setup(LevelArgs A) {
       __syncthreads();
     }
   }
+  // two-level preconditioner: S_M = C M^-1 C^T = C D^-1 C^T + (CZ) E^-1 (CZ)^T
+  if (A.coarse && A.level == 1) {
+    const int nca = A.ncomp[mp];
+    const double* CZ = A.CZ + (int64_t)mp * nc * A.ncmax;
+    const double* Ei = A.Einv + (int64_t)mp * A.ncmax;
+    for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+      const int i = idx / nc, j = idx % nc;
+      double acc = 0.0;
+      for (int a = 0; a < nca; a++) acc += CZ[(int64_t)i * A.ncmax + a] * Ei[a] * CZ[(int64_t)j * A.ncmax + a];
+      S[idx] += acc;
+    }
+    __syncthreads();
+  }
   // equilibrate, mark inactive rows, Gauss-Jordan inverse (SPD, no pivoting)
   __shared__ double ds[128];
   const double* meas = A.meas + (int64_t)mp * nc;
@@ -401,6 +414,266 @@ __global__ void k_proj_setup(LevelArgs A) {
   double* so = A.Sinv + (int64_t)mp * nc * nc;  // S~ in place of S^-1 until k_pinv replaces it
   for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) so[idx] = V[idx];
   for (int i = threadIdx.x; i < nc; i += blockDim.x) A.pinv_ds[(int64_t)mp * nc + i] = ds[i];
+}
+
+// ---------------------------------------------------------------------------------------
+// Two-level preconditioner setup (level 1, generic k_pcg): one CTA per macropoint.
+// High-contrast inclusions make the near-constant value of each inclusion the slowest mode of
+// Jacobi-PCG.  If the window's contrast kappa_max / kappa_min >= 100, every node touching a cell
+// with kappa > sqrt(kappa_min kappa_max) is "high"; the 3^D-connected components of high nodes
+// are the coarse basis Z (indicators).  Two nodes of different components never share a cell,
+// so E = Z^T A Z is diagonal.  Components are labelled by minimum-label propagation with
+// pointer jumping (the result is the smallest node index of each component, independent of
+// the order of updates) and numbered in node order.  Per component: bounding box, E_aa = z_a^T
+// A z_a, and C z_a (constraint rows of the indicator).  Everything summed in a fixed order.
+template <int D>
+__global__ void k_coarse_setup(LevelArgs A) {
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<D> g = level_geo<D>(A, P);
+  int* cm = A.cmap + P.node_off;
+  const int nn = g.nnodes, nc = A.ncon;
+  __shared__ double red[64];
+  __shared__ int flag, total;
+  extern __shared__ double smem[];
+  double* cvals = smem;                               // ncon
+  int* cnt = reinterpret_cast<int*>(cvals + nc);       // blockDim.x
+  // 1. contrast of the window
+  double kmin = 1e300, kmax = 0.0;
+  const int ncell = g.nc[0] * g.nc[1] * (D == 3 ? g.nc[2] : 1);
+  for (int idx = threadIdx.x; idx < ncell; idx += blockDim.x) {
+    int e[3] = {idx % g.nc[0], (idx / g.nc[0]) % g.nc[1], (D == 3) ? idx / (g.nc[0] * g.nc[1]) : 0};
+    const double kv = A.kappa[fine_cell_index<D>(A, P, g, e, nullptr)];
+    kmin = fmin(kmin, kv);
+    kmax = fmax(kmax, kv);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = fmin(kmin, __shfl_xor_sync(FULLMASK, kmin, o));
+    kmax = fmax(kmax, __shfl_xor_sync(FULLMASK, kmax, o));
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) { red[wid] = kmin; red[32 + wid] = kmax; }
+  __syncthreads();
+  kmin = 1e300; kmax = 0.0;
+  for (int w = 0; w < nw; w++) { kmin = fmin(kmin, red[w]); kmax = fmax(kmax, red[32 + w]); }
+  const bool use = kmax >= 100.0 * kmin;
+  const double thr = sqrt(kmin * kmax);
+  // 2. high nodes: label = own index
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+    int lab = -1;
+    if (use) {
+      int x[3];
+      node_xyz<D>(g, k, x);
+      for (int o = 0; o < (1 << D); o++) {
+        int e[3] = {0, 0, 0};
+        bool ok = true;
+        for (int i = 0; i < D; i++) {
+          e[i] = x[i] - 1 + ((o >> i) & 1);
+          ok = ok && e[i] >= 0 && e[i] < g.nc[i];
+        }
+        if (ok && A.kappa[fine_cell_index<D>(A, P, g, e, nullptr)] > thr) lab = k;
+      }
+    }
+    cm[k] = lab;
+  }
+  __syncthreads();
+  // 3. minimum-label propagation over the 3^D neighbourhood, with pointer jumping
+  if (use) {
+    for (;;) {
+      if (threadIdx.x == 0) flag = 0;
+      __syncthreads();
+      for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+        const int lk = cm[k];
+        if (lk < 0) continue;
+        int x[3];
+        node_xyz<D>(g, k, x);
+        int m = lk;
+        for (int c = 0; c < DimC<D>::NB; c++) {
+          const int dx = c % 3 - 1, dy = (c / 3) % 3 - 1, dz = (D == 3) ? c / 9 - 1 : 0;
+          const int xx[3] = {x[0] + dx, x[1] + dy, x[2] + dz};
+          bool ok = xx[0] >= 0 && xx[0] < g.nn[0] && xx[1] >= 0 && xx[1] < g.nn[1];
+          if (D == 3) ok = ok && xx[2] >= 0 && xx[2] < g.nn[2];
+          if (!ok) continue;
+          const int ln = cm[node_id<D>(g, xx)];
+          if (ln >= 0 && ln < m) m = ln;
+        }
+        if (m < lk) {
+          atomicMin(&cm[k], m);
+          flag = 1;
+        }
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+        int lk = cm[k];
+        if (lk < 0) continue;
+        int r = cm[lk];
+        while (r >= 0 && r < lk) { lk = r; r = cm[lk]; }
+        atomicMin(&cm[k], lk);
+      }
+      __syncthreads();
+      if (!flag) break;
+      __syncthreads();
+    }
+  }
+  // 4. number the roots (cm[k] == k) in node order: per-thread contiguous chunks + scan
+  const int chunk = (nn + blockDim.x - 1) / blockDim.x;
+  const int k0 = threadIdx.x * chunk, k1 = min(nn, k0 + chunk);
+  int mine = 0;
+  for (int k = k0; k < k1; k++) mine += (cm[k] == k);
+  cnt[threadIdx.x] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int t = 0; t < (int)blockDim.x; t++) {
+      const int c = cnt[t];
+      cnt[t] = s;
+      s += c;
+    }
+    total = s;
+  }
+  __syncthreads();
+  const int ncomp = (total <= A.ncmax) ? total : 0;
+  {
+    int id = cnt[threadIdx.x];
+    for (int k = k0; k < k1; k++)
+      if (cm[k] == k) cm[k] = -(id++) - 2;  // roots: encoded id
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+    const int lk = cm[k];
+    if (lk >= 0) cm[k] = -cm[lk] - 2;  // member: the root's id
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+    const int lk = cm[k];
+    if (lk <= -2) cm[k] = -lk - 2;  // root: decode
+    if (ncomp == 0) cm[k] = -1;
+  }
+  if (threadIdx.x == 0) A.ncomp[mp] = ncomp;
+  int* box = A.cbox + (int64_t)mp * A.ncmax * 6;
+  for (int a = threadIdx.x; a < ncomp; a += blockDim.x) {
+    box[a * 6 + 0] = box[a * 6 + 1] = box[a * 6 + 2] = 1 << 30;
+    box[a * 6 + 3] = box[a * 6 + 4] = box[a * 6 + 5] = -1;
+  }
+  __syncthreads();
+  if (ncomp == 0) return;
+  // 5. bounding boxes
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+    const int a = cm[k];
+    if (a < 0) continue;
+    int x[3];
+    node_xyz<D>(g, k, x);
+    for (int i = 0; i < 3; i++) {
+      atomicMin(&box[a * 6 + i], x[i]);
+      atomicMax(&box[a * 6 + 3 + i], x[i]);
+    }
+  }
+  __syncthreads();
+  // 5b. node lists per component (CSR, node order): counts, prefix, fill (thread per component)
+  int* cp = A.cptr + (int64_t)mp * (A.ncmax + 1);
+  int* cl = A.clist + P.node_off;
+  for (int a = threadIdx.x; a < ncomp; a += blockDim.x) {
+    const int* bx = box + a * 6;
+    int c = 0;
+    for (int z = bx[2]; z <= bx[5]; z++)
+      for (int y = bx[1]; y <= bx[4]; y++)
+        for (int x = bx[0]; x <= bx[3]; x++) {
+          const int xx[3] = {x, y, z};
+          c += (cm[node_id<D>(g, xx)] == a);
+        }
+    cp[a + 1] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    cp[0] = 0;
+    for (int a = 0; a < ncomp; a++) cp[a + 1] += cp[a];
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < ncomp; a += blockDim.x) {
+    const int* bx = box + a * 6;
+    int o = cp[a];
+    for (int z = bx[2]; z <= bx[5]; z++)
+      for (int y = bx[1]; y <= bx[4]; y++)
+        for (int x = bx[0]; x <= bx[3]; x++) {
+          const int xx[3] = {x, y, z};
+          const int k = node_id<D>(g, xx);
+          if (cm[k] == a) cl[o++] = k;
+        }
+  }
+  __syncthreads();
+  // 6. per component: E_aa = z_a^T A z_a (fine Q1 element rows) and C z_a
+  double* Ei = A.Einv + (int64_t)mp * A.ncmax;
+  double* CZ = A.CZ + (int64_t)mp * nc * A.ncmax;
+  __shared__ int ebs[125 * 7 + 2];
+  __shared__ int ntask;
+  subcell_boxes<D>(A, P, g, ebs, &ntask);
+  for (int a = 0; a < ncomp; a++) {
+    const int* bx = box + a * 6;
+    const int ex = bx[3] - bx[0] + 1, ey = bx[4] - bx[1] + 1, ez = (D == 3) ? bx[5] - bx[2] + 1 : 1;
+    double v[1] = {0.0};
+    for (int idx = threadIdx.x; idx < ex * ey * ez; idx += blockDim.x) {
+      const int x[3] = {bx[0] + idx % ex, bx[1] + (idx / ex) % ey, (D == 3) ? bx[2] + idx / (ex * ey) : 0};
+      const int k = node_id<D>(g, x);
+      if (cm[k] != a) continue;
+      double az = 0.0;  // (A z_a)_k
+      for (int o = 0; o < (1 << D); o++) {
+        int e[3] = {0, 0, 0};
+        bool ok = true;
+        for (int i = 0; i < D; i++) {
+          e[i] = x[i] - 1 + ((o >> i) & 1);
+          ok = ok && e[i] >= 0 && e[i] < g.nc[i];
+        }
+        if (!ok) continue;
+        const double kap = A.kappa[fine_cell_index<D>(A, P, g, e, nullptr)];
+        const int ac = (~o) & ((1 << D) - 1);  // corner of node k in cell e
+        auto zb = [&](int b) {
+          int xb[3] = {e[0] + (b & 1), e[1] + ((b >> 1) & 1), (D == 3) ? e[2] + ((b >> 2) & 1) : 0};
+          return (cm[node_id<D>(g, xb)] == a) ? 1.0 : 0.0;
+        };
+        if (D == 2) az += kap * (1.0 / 6.0) * (4.0 * zb(ac) - zb(ac ^ 1) - zb(ac ^ 2) - 2.0 * zb(ac ^ 3));
+        else az += kap * A.h * (1.0 / 12.0) * (4.0 * zb(ac) - zb(ac ^ 3) - zb(ac ^ 5) - zb(ac ^ 6) - zb(ac ^ 7));
+      }
+      v[0] += az;
+    }
+    block_sum<1>(v, red, red + 48);
+    if (threadIdx.x == 0) Ei[a] = (red[48] > 0.0) ? 1.0 / red[48] : 0.0;
+    __syncthreads();
+  }
+  // C z_a: thread per component over the cells touching it (its bounding box grown by one cell
+  // on the lower sides), contributions m_{E,j,a} = [id_E = j] h^D / 2^D per corner in the
+  // component, accumulated per constraint row in cell order (fixed order)
+  (void)ebs;
+  for (int a = threadIdx.x; a < ncomp; a += blockDim.x) {
+    for (int r = 0; r < nc; r++) CZ[(int64_t)r * A.ncmax + a] = 0.0;
+    const int* bx = box + a * 6;
+    int lo[3], hi[3];
+    for (int i = 0; i < 3; i++) {
+      lo[i] = (i < D) ? max(bx[i] - 1, 0) : 0;
+      hi[i] = (i < D) ? min(bx[3 + i], g.nc[i] - 1) : 0;
+    }
+    const double hq = (D == 2) ? 0.25 * A.h * A.h : 0.125 * A.h * A.h * A.h;
+    for (int ez = lo[2]; ez <= hi[2]; ez++)
+      for (int ey = lo[1]; ey <= hi[1]; ey++)
+        for (int ex = lo[0]; ex <= hi[0]; ex++) {
+          const int e[3] = {ex, ey, ez};
+          int cntc = 0;
+          for (int b = 0; b < (1 << D); b++) {
+            const int xb[3] = {ex + (b & 1), ey + ((b >> 1) & 1), (D == 3) ? ez + ((b >> 2) & 1) : 0};
+            cntc += (cm[node_id<D>(g, xb)] == a);
+          }
+          if (cntc == 0) continue;
+          const int q = elem_subcell<D>(A, P, g, e);
+          const int id = A.ids[fine_cell_index<D>(A, P, g, e, nullptr)];
+          CZ[(int64_t)(q * A.N + id) * A.ncmax + a] += hq * cntc;
+        }
+  }
+}
+
+cudaError_t launch_coarse_setup(const LevelArgs& A, cudaStream_t st) {
+  const size_t sm = sizeof(double) * A.ncon + sizeof(int) * 512;
+  if (A.D == 2) k_coarse_setup<2><<<A.nprob_mp, 512, sm, st>>>(A);
+  else k_coarse_setup<3><<<A.nprob_mp, 512, sm, st>>>(A);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -674,7 +947,10 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
   double* tg = cvec + nc;                         // nc
   double* gcol = tg + nc;                         // nc
   double* g0col = gcol + nc;                      // nc
-  double* bins = g0col + nc;                      // dense: 32*nc
+  const bool crs = A.coarse && A.level == 1 && !band && A.ncomp[mp] > 0;  // two-level preconditioner
+  double* zr = g0col + nc;                        // coarse: ncmax (E^-1 Z^T r)
+  double* vv = zr + (A.coarse ? A.ncmax : 0);     // coarse: ncmax (coarse part of z)
+  double* bins = vv + (A.coarse ? A.ncmax : 0);   // dense: 32*nc
   double* scratch = bins + (band ? 0 : 32 * nc);  // 32*4
   double* tot = scratch + 32 * 4;                 // 4
   int* eb = reinterpret_cast<int*>(tot + 4);
@@ -733,6 +1009,55 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
     if (band) constraint_apply_owned<D>(A, P, g, eb, uf, out);
     else constraint_apply<D>(A, P, g, eb, ntask, uf, bins, out);
   };
+  const int nca = crs ? A.ncomp[mp] : 0;
+  const int* cmp = A.cmap + P.node_off;
+  const int* cbx = A.cbox + (int64_t)mp * A.ncmax * 6;
+  const double* Ei = A.Einv + (int64_t)mp * A.ncmax;
+  const double* CZm = A.CZ + (int64_t)mp * nc * A.ncmax;
+  // zr = E^-1 Z^T rvec (one warp per component over its bounding box, fixed order), c += (CZ) zr;
+  // returns (Z^T r)^T E^-1 (Z^T r)
+  auto coarse_c = [&](const double* rvec, double* c) -> double {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    double part[1] = {0.0};
+    for (int a = wid; a < nca; a += nw) {
+      const int* bx = cbx + a * 6;
+      const int ex = bx[3] - bx[0] + 1, ey = bx[4] - bx[1] + 1, ez = (D == 3) ? bx[5] - bx[2] + 1 : 1;
+      double sv = 0.0;
+      for (int idx = lane; idx < ex * ey * ez; idx += 32) {
+        const int xx[3] = {bx[0] + idx % ex, bx[1] + (idx / ex) % ey, (D == 3) ? bx[2] + idx / (ex * ey) : 0};
+        const int k = node_id<D>(g, xx);
+        if (cmp[k] == a) sv += rvec[k];
+      }
+      for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(FULLMASK, sv, o);
+      if (lane == 0) {
+        zr[a] = sv * Ei[a];
+        part[0] += sv * sv * Ei[a];
+      }
+    }
+    block_sum<1>(part, scratch, tot);
+    const double zw = tot[0];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      double acc = 0.0;
+      for (int a = 0; a < nca; a++) acc += CZm[(int64_t)i * A.ncmax + a] * zr[a];
+      c[i] += acc;
+    }
+    __syncthreads();
+    return zw;
+  };
+  // vv = s0 * zr - E^-1 (CZ)^T yh   (s0 = 0: the coarse part of M^-1 C^T yh, negated)
+  auto coarse_v = [&](const double* yh, double s0) {
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) {
+      double acc = 0.0;
+      for (int i = 0; i < nc; i++) acc += CZm[(int64_t)i * A.ncmax + a] * yh[i];
+      vv[a] = (s0 != 0.0 ? s0 * zr[a] : 0.0) - Ei[a] * acc;  // zr is not yet set when s0 == 0
+    }
+    __syncthreads();
+  };
+  auto cz_at = [&](int k) -> double {  // coarse part of the preconditioned vector at node k
+    if (!crs) return 0.0;
+    const int a = cmp[k];
+    return (a >= 0) ? vv[a] : 0.0;
+  };
 
   // init: x = D^-1 C^T S^-1 t, r = A x - b (unprojected), c = C D^-1 r, yhat = S^-1 c.
   // returns r^T D^-1 r of the unprojected residual
@@ -740,7 +1065,8 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
     for (int i = threadIdx.x; i < nc; i += blockDim.x) tg[i] = targets[i];
     __syncthreads();
     sinv_apply(tg, yhat);
-    for (int k = threadIdx.x; k < nn; k += blockDim.x) x[k] = dinv[k] * ct_node<D>(A, P, g, yhat, k);
+    if (crs) coarse_v(yhat, 0.0);  // x0 = M^-1 C^T S^-1 t: coarse part = -vv
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) x[k] = dinv[k] * ct_node<D>(A, P, g, yhat, k) - cz_at(k);
     __syncthreads();
     double v[1] = {0.0};
     for (int k = threadIdx.x; k < nn; k += blockDim.x) {
@@ -749,9 +1075,11 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
       v[0] += dinv[k] * rk * rk;
     }
     block_sum<1>(v, scratch, tot);
-    const double rr = tot[0];
+    double rr = tot[0];
     capply([&](int k) { return dinv[k] * rv[k]; }, cvec);
+    if (crs) rr += coarse_c(rv, cvec);  // r^T M^-1 r and C M^-1 r
     sinv_apply(cvec, yhat);
+    if (crs) coarse_v(yhat, 1.0);  // z = M^-1 (r - C^T yhat): coarse part vv
     return rr;
   };
 
@@ -789,7 +1117,7 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
     double v[1] = {0.0};
     for (int k = threadIdx.x; k < nn; k += blockDim.x) {
       const double rk = rv[k] - ct_fast<D>(A, P, g, nwt, yhat, k);
-      const double zk = dinv[k] * rk;
+      const double zk = dinv[k] * rk + cz_at(k);
       rv[k] = rk;
       p[k] = -zk + beta * p[k];
       v[0] += rk * zk;
@@ -820,19 +1148,22 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
       u[0] += dinv[k] * rk * rk;
     }
     block_sum<1>(u, scratch, tot);
-    const double rr = tot[0];
+    double rr = tot[0];
     capply([&](int k) { return dinv[k] * rv[k]; }, cvec);
+    if (crs) rr += coarse_c(rv, cvec);
     sinv_apply(cvec, yhat);
     double cy = 0.0;
     for (int j = 0; j < nc; j++) cy += cvec[j] * yhat[j];
     beta = (rr - cy) / rz;
+    if (crs) coarse_v(yhat, 1.0);
   }
   // feasibility restoration: x += D^-1 C^T S^-1 (g - C x)
   capply([&](int k) { return x[k]; }, cvec);
   for (int i = threadIdx.x; i < nc; i += blockDim.x) tg[i] = gcol[i] - cvec[i];
   __syncthreads();
   sinv_apply(tg, yhat);
-  for (int k = threadIdx.x; k < nn; k += blockDim.x) x[k] += dinv[k] * ct_node<D>(A, P, g, yhat, k);
+  if (crs) coarse_v(yhat, 0.0);
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) x[k] += dinv[k] * ct_node<D>(A, P, g, yhat, k) - cz_at(k);
   __syncthreads();
   if (A.level == 1 && P.pool_off >= 0) {
     double* dst = A.pool + P.pool_off + (int64_t)r * nn;
@@ -991,7 +1322,8 @@ __global__ void k_validate(const double* kappa, const uint8_t* ids, int64_t cnt,
 size_t pcg_smem(const LevelArgs& A) {
   const size_t nc = A.ncon;
   const size_t mat = (A.band > 0) ? nc * (A.band + 1) + nc : nc * nc + 32 * nc;
-  return sizeof(double) * (mat + 5 * nc + 32 * 4 + 4) + sizeof(int) * (A.nsub * 7 + 2);
+  const size_t crs = A.coarse ? 2 * (size_t)A.ncmax : 0;
+  return sizeof(double) * (mat + 5 * nc + crs + 32 * 4 + 4) + sizeof(int) * (A.nsub * 7 + 2);
 }
 
 size_t proj_setup_band_smem(const LevelArgs& A) {

@@ -20,7 +20,7 @@ cudaError_t launch_validate(const double* kappa, const uint8_t* ids, int64_t cnt
 #define PCG2D_V_GN25 2
 #define PCG2D_V_GN97 3
 void pcg2d_variant(int variant, int* rpt, int* nxm, int* maxw, int* l1op, int* sstc, int* smlr);
-size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw, bool sstc, bool smlr);
+size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw, bool sstc, bool smlr, bool crs = false);
 cudaError_t launch_node_ops2d(const LevelArgs& A, int max_nodes, cudaStream_t st);
 cudaError_t launch_pcg2d(const LevelArgs& A, int variant, int threads, cudaStream_t st);
 void pcg2d_phase_dump(const char* tag);  // PCG2D_TIMING builds: per-phase cycle counters
@@ -54,3 +54,5 @@ size_t proj_setup_band_smem(const LevelArgs& A);
 // dynamic shared memory of k_pcg / k_proj_setup_band at these arguments
 size_t pcg_smem(const LevelArgs& A);
 size_t proj_setup_band_smem(const LevelArgs& A);
+// two-level preconditioner setup (generic k_pcg, level 1)
+cudaError_t launch_coarse_setup(const LevelArgs& A, cudaStream_t st);

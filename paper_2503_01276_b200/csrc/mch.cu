@@ -65,6 +65,8 @@ struct DevBuf {
   template <typename T> T* as() const { return reinterpret_cast<T*>(ptr); }
 };
 
+constexpr int kCoarseMax = 255;  // coarse components per window (two-level preconditioner; id 255 = none)
+
 int64_t ipow64(int64_t b, int e) {
   int64_t r = 1;
   while (e-- > 0) r *= b;
@@ -86,6 +88,7 @@ struct LevelBatch {
   DevBuf descs, segs, nseg;
   bool on2d = false, l1op = false;
   bool on3d = false;  // on-chip 3D PCG (pcg3d.cu), levels >= 2
+  bool coarse = false;  // two-level preconditioner at level 1 (generic k_pcg or k_pcg2d level-1 variant)
   bool tsplit = false;  // 3D transport through k_pcg3d_l1<MODE 1> (fine windows <= 49 nodes per side)
   int nxm3 = 0;
   int variant = -1, threads2 = 0, maxseg = 0, tm_cols = 32;
@@ -132,11 +135,13 @@ struct mch_ctx {
   // NEXT-2: source f (cellwise, n^D), load vectors [P][N], macro-solve workspace and results
   DevBuf fsrc, bload, mws, mG, mb, mU, mres;
   DevBuf fws, fbar, ff, fu, fkbox, fout;  // NEXT-3 fine solve / block averages
+  DevBuf cmap, ncomp, cbox, einv, cz, cptr, clist;  // two-level preconditioner (level 1)
+  bool coarse = false;
   DevAlloc al;
   std::vector<DevBuf*> bufs() {
     return {&STC, &MLR, &pinv_ds, &W, &Mc, &g0, &g, &meas, &cm, &flags, &dinv, &nwt, &Sinv, &X, &R, &P, &Q, &B,
             &FI, &FY, &iters, &relres, &diag, &fsrc, &bload, &mws, &mG, &mb, &mU, &mres, &fws, &fbar, &ff, &fu,
-            &fkbox, &fout};
+            &fkbox, &fout, &cmap, &ncomp, &cbox, &einv, &cz, &cptr, &clist};
   }
   bool has_source = false;
   int* h_mit = nullptr;
@@ -232,6 +237,8 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   c->nsub = nsub;
   c->ncon = nsub * p.num_continua;
   c->st = reinterpret_cast<cudaStream_t>(p.stream);
+  // two-level preconditioner at level 1: on unless MCH_COARSE=0
+  c->coarse = !(getenv("MCH_COARSE") != nullptr && atoi(getenv("MCH_COARSE")) == 0);
   if (const char* pm = getenv("MCH_PCG")) {
     if (!strcmp(pm, "old")) c->pcg_mode = 1;
     else if (!strcmp(pm, "gn")) c->pcg_mode = 2;
@@ -444,7 +451,8 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       for (int v : cands) {
         int rpt, nxm, maxw, l1op, sstc, smlr;
         pcg2d_variant(v, &rpt, &nxm, &maxw, &l1op, &sstc, &smlr);
-        if (maxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0) > 232448) continue;
+        const bool crs_v = c->coarse && level == 1 && v == PCG2D_V_L1;
+        if (maxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0, crs_v) > 232448) continue;
         std::vector<int> nsegs(nmp);
         std::vector<std::vector<short4>> per(nmp);
         int maxseg = 0, maxwp = 0;
@@ -454,7 +462,8 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
           maxseg = std::max(maxseg, nsegs[i]);
           maxwp = std::max(maxwp, ((descs[i].nc[0] + 1 + 31) / 32) * nsegs[i]);
         }
-        const int need = ((maxwp + 3) / 4) * 4 * ((rpt + 3) & ~3);  // TMEM: warps per lane quarter x (q, x)
+        const int rp4 = (rpt + 3) & ~3;  // TMEM: warps per lane quarter x (q, x [, component ids])
+        const int need = ((maxwp + 3) / 4) * (4 * rp4 + (crs_v ? rp4 / 4 : 0));
         int cols = 32;
         while (cols < need) cols *= 2;
         if (maxwp > maxw || cols > 512) continue;
@@ -522,6 +531,17 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     if (B->on2d && !B->l1op) {
       CKC(c, c->STC.ensure(sizeof(double) * 9 * B->node_off));
       CKC(c, c->MLR.ensure(sizeof(double) * 4 * N * B->node_off));
+    }
+    B->coarse = c->coarse && level == 1 && c->band == 0 && !B->on3d && (!B->on2d || B->variant == PCG2D_V_L1);
+    if (B->coarse) {
+      if (B->on2d) CKC(c, c->R.ensure(sizeof(double) * B->vec_off));  // r mirrored for the coarse sums
+      CKC(c, c->cmap.ensure(sizeof(int) * B->node_off));
+      CKC(c, c->ncomp.ensure(sizeof(int) * nmp));
+      CKC(c, c->cbox.ensure(sizeof(int) * 6 * kCoarseMax * (size_t)nmp));
+      CKC(c, c->einv.ensure(sizeof(double) * kCoarseMax * (size_t)nmp));
+      CKC(c, c->cz.ensure(sizeof(double) * kCoarseMax * (size_t)nmp * nc));
+      CKC(c, c->cptr.ensure(sizeof(int) * (kCoarseMax + 1) * (size_t)nmp));
+      CKC(c, c->clist.ensure(sizeof(int) * B->node_off));
     }
     if (B->on3d && level >= 2) {
       CKC(c, c->STC.ensure(sizeof(double) * 27 * B->node_off));
@@ -611,6 +631,15 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       S.launches += 2;
     } else if (level >= 2) {
       CKC(c, launch_transport(A, B.th_f, st));
+    }
+    A.coarse = B.coarse ? 1 : 0;
+    A.ncmax = kCoarseMax;
+    A.cmap = c->cmap.as<int>(); A.ncomp = c->ncomp.as<int>(); A.cbox = c->cbox.as<int>();
+    A.Einv = c->einv.as<double>(); A.CZ = c->cz.as<double>();
+    A.cptr = c->cptr.as<int>(); A.clist = c->clist.as<int>();
+    if (A.coarse) {
+      CKC(c, launch_coarse_setup(A, st));
+      S.launches += 1;
     }
     CKC(c, launch_proj_setup(A, B.th_l, st));
     CKC(c, launch_pinv(A, st));

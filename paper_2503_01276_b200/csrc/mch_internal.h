@@ -60,6 +60,17 @@ struct LevelArgs {
   double* G;               // [(M+1)^D][n_rhs][n_rhs]
   int band;                // 0: dense S^-1 per macropoint; > 0: banded Cholesky factor of the
                            //  equilibrated S (half-bandwidth band, 2D large l), Sinv[mp][nc][band+1]
+  // two-level preconditioner (generic k_pcg, level 1, dense projector): M^-1 = D^-1 + Z E^-1 Z^T with
+  // Z = indicators of the 8- (26-) connected components of nodes touching a high-kappa cell
+  int coarse;              // 1: build and use the coarse space
+  int ncmax;               // components per window capacity (more: the window runs without)
+  int* cmap;               // [nodes] component of each level-1 node, -1 none (node_off based)
+  int* ncomp;              // [mp]
+  int* cbox;               // [mp][ncmax][6] node bounding box per component (lo, hi inclusive)
+  double* Einv;            // [mp][ncmax] 1 / (z_a^T A z_a)
+  double* CZ;              // [mp][ncon][ncmax] C z_a
+  int* cptr;               // [mp][ncmax+1] start of each component's node list in clist
+  int* clist;              // [nodes] node indices of each component, in node order (node_off based)
   int tphase;              // k_transport: 0 all phases; 1 only I_p; 2 only the restriction (3D split path)
   const double* f;         // NEXT-2: cellwise source, n^D, x fastest (NULL: no load vectors)
   double* bload;           // NEXT-2: [P][N] load vectors b_j = int_{K_p} f phi_j (Eq. 7)

@@ -33,6 +33,8 @@
 
 namespace {
 
+constexpr int kCrsMax = 256;  // coarse components per window of the two-level preconditioner
+
 // ------------------------------------------------------------------------------------------
 // TMEM helpers (32x32b shape: lane i of the warp <-> TMEM lane 32*(warp%4) + i).  No "memory"
 // clobbers: they would pin every address-taken local in local memory; volatile asm statements
@@ -48,6 +50,14 @@ __device__ __forceinline__ void tm_ld8(uint32_t ta, uint32_t (&v)[8]) {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
                  "=r"(v[7])
                : "r"(ta));
+}
+__device__ __forceinline__ void tm_st1(uint32_t ta, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};\n" ::"r"(ta), "r"(v));
+}
+__device__ __forceinline__ uint32_t tm_ld1(uint32_t ta) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(v) : "r"(ta));
+  return v;
 }
 __device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n"); }
@@ -257,10 +267,11 @@ void pcg2d_phase_dump(const char* tag) {
 void pcg2d_phase_dump(const char*) {}
 #endif
 
-template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB, bool SSTC, bool SMLR>
+template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB, bool SSTC, bool SMLR, bool CRS = false>
 __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   constexpr int RP4 = (RPT + 3) & ~3;  // rows rounded to the 4-row TMEM groups
   constexpr int NBC = 4 * RP4;         // TMEM columns per thread: q block, then x block
+  constexpr int NBCW = NBC + (CRS ? RP4 / 4 : 0);  // CRS: + one column of 4 component bytes per 4 rows
   // compile-time pitches and shared-memory offsets (host checks nx, ny <= NXM and warps <= MAXW):
   // every per-row address is an immediate offset from one per-thread base
   constexpr int PX = NXM + 2, KX = NXM + 1, DX = NXM;
@@ -285,12 +296,16 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   constexpr int LW = NodeW<N, L1OP, KX>::LW;
   constexpr int PLANE = DX * NXM;
   constexpr int NCM = 9 * N;              // constraint rows of a 3x3-subcell window (host: nc <= NCM)
-  constexpr int O_Y = (NCM * NCM + 1) & ~1, O_SL = O_Y + 64, O_B = O_SL + 3 * 32;
+  constexpr int NCC = CRS ? kCrsMax : 0;  // two-level preconditioner: coarse components per window
+  constexpr int O_Y = (NCM * NCM + 1) & ~1, O_SL = O_Y + 64, O_B = O_SL + (CRS ? 4 : 3) * 32;
   constexpr int O_P = O_B + MAXW * 32;
   constexpr int O_K = O_P + PX * (NXM + 2), O_LUT = (O_K + (L1OP ? KX * (NXM + 1) : 0) + 1) & ~1;
   constexpr int O_S9 = O_LUT + (L1OP ? 16 * LW : 0);  // levels >= 2, SSTC: 9 x DX*NXM stencil
   constexpr int O_ML = O_S9 + (SSTC ? 9 * PLANE : 0);    // levels >= 2, SMLR: 2N x DX*NXM side sums
-  constexpr int O_D = O_ML + (SMLR ? 2 * N * PLANE : 0);  // end of the double region
+  constexpr int O_ZR = O_ML + (SMLR ? 2 * N * PLANE : 0);  // CRS: E^-1 Z^T r per component
+  constexpr int O_VV = O_ZR + NCC;                        // CRS: coarse part of z per component
+  constexpr int O_CS = O_VV + NCC;                        // CRS: (CZ) E^-1 Z^T r per constraint row
+  constexpr int O_D = O_CS + (CRS ? 32 : 0);              // end of the double region
   double* Si = smem;                      // [NCM*NCM] S^-1 (nc*nc used)
   double* Ysh = smem + O_Y;               // [32] yhat, [32] beta (written by warp 0)
   double* slots = smem + O_SL;            // [3][32] scalar partial sums (rz, pq, rr)
@@ -313,7 +328,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   for (int i = threadIdx.x; i < PX * (ny + 2); i += blockDim.x) p_s[i] = 0.0;
   for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) Si[i] = A.Sinv[(int64_t)mp * nc * nc + i];
   for (int i = threadIdx.x; i < MAXW * 32; i += blockDim.x) bins[i] = 0.0;
-  for (int i = threadIdx.x; i < 3 * 32; i += blockDim.x) slots[i] = 0.0;  // incl. slots of absent warps
+  for (int i = threadIdx.x; i < (CRS ? 4 : 3) * 32; i += blockDim.x) slots[i] = 0.0;  // incl. absent warps
   {
     const double* dg = A.dinv + P.node_off;
     for (int k = threadIdx.x; k < nn; k += blockDim.x) dinv_s[(k / nx) * DX + k % nx] = (float)dg[k];
@@ -353,8 +368,9 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmq = tm_base_s + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * NBC);
+  const uint32_t tmq = tm_base_s + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * NBCW);
   const uint32_t tmx = tmq + 2 * RP4;
+  const uint32_t tmc = tmq + NBC;  // CRS: component ids of this thread's rows, 4 per column
 
   // per-thread subcell columns of the left / right elements
   const int sxL = (xc >= 1) ? sub_slot(A, P, 0, xc - 1) : 0;
@@ -585,15 +601,92 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   };
   auto slot_fin = [&](int which) { return warp_sum0((lane < MAXW) ? slots[which * 32 + lane] : 0.0); };
 
+  // ---- two-level preconditioner M^-1 = D^-1 + Z E^-1 Z^T (level 1): r is mirrored
+  //      to global memory in pass C and summed per component there (one warp per component over
+  //      its bounding box, fixed order); the projection uses S_M = C M^-1 C^T (k_proj_setup) ----
+  const bool crs = CRS && A.level == 1 && A.ncomp[mp] > 0;
+  const int nca = crs ? A.ncomp[mp] : 0;
+  const int* cmp = A.cmap + P.node_off;
+  const int* cpt = A.cptr + (int64_t)mp * (A.ncmax + 1);
+  const int* cls = A.clist + P.node_off;
+  const double* Eiv = A.Einv + (int64_t)mp * A.ncmax;
+  const double* CZm = A.CZ + (int64_t)mp * nc * A.ncmax;
+  double* Rg = A.R + P.vec_off + (int64_t)rhs * nn;
+  double* zr = smem + O_ZR;
+  double* vv = smem + O_VV;
+  double* csum = smem + O_CS;
+  const int nwarps = blockDim.x >> 5;
+  // zr = E^-1 Z^T Rg, slot 3 = (Z^T r)^T E^-1 (Z^T r); then csum = (CZ) zr.  Two barriers.
+  auto coarse_c = [&]() {
+    double part = 0.0;
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) {  // one thread per component, fixed order
+      const int i0 = __ldg(cpt + a), i1 = __ldg(cpt + a + 1);
+      double sv = 0.0;
+#pragma unroll 16
+      for (int i = i0; i < i1; i++) sv += __ldcg(Rg + __ldg(cls + i));
+      const double ei = __ldg(Eiv + a);
+      zr[a] = sv * ei;
+      part += sv * sv * ei;
+    }
+    part = warp_sum0(part);
+    if (lane == 0) slots[3 * 32 + warp] = part;
+    __syncthreads();
+    for (int t = warp; t < nc; t += nwarps) {
+      double sv = 0.0;
+      for (int a = lane; a < nca; a += 32) sv += __ldg(CZm + (int64_t)t * A.ncmax + a) * zr[a];
+      sv = warp_sum0(sv);
+      if (lane == 0) csum[t] = sv;
+    }
+    __syncthreads();
+  };
+  // vv = s0 zr - E^-1 (CZ)^T Ysh (s0 = 0: minus the coarse part of M^-1 C^T yhat).  One barrier.
+  auto coarse_v = [&](double s0) {
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) {
+      double acc = 0.0;
+      for (int t = 0; t < nc; t++) acc += __ldg(CZm + (int64_t)t * A.ncmax + a) * Ysh[t];
+      vv[a] = (s0 != 0.0 ? s0 * zr[a] : 0.0) - __ldg(Eiv + a) * acc;
+    }
+    __syncthreads();
+  };
+  auto vv_at = [&](int y) -> double {
+    if (!crs) return 0.0;
+    const int a = __ldg(cmp + y * nx + xc);
+    return (a >= 0) ? vv[a] : 0.0;
+  };
+  auto vv_w = [&](uint32_t word, int u) -> double {  // component byte u of a TMEM word (255: none)
+    const uint32_t a = (word >> (8 * u)) & 255u;
+    return (a == 255u) ? 0.0 : vv[a];
+  };
+  if (CRS && crs && wact) {  // this thread's component ids into TMEM, 4 rows per column
+#pragma unroll
+    for (int gq = 0; gq < RP4 / 4; gq++) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int i = gq * 4 + u;
+        int a = -1;
+        if (lact && i < nrow) a = __ldg(cmp + (y0 + i) * nx + xc);
+        word |= (uint32_t)((a >= 0) ? a : 255) << (8 * u);
+      }
+      tm_st1(tmc + gq, word);
+    }
+    tm_wait_st();
+  }
+
   // ---- init: x0 = D^-1 C^T S^-1 t (minimum-norm feasible point), r0 = A x0 - b,
   //      c = C D^-1 r0, yhat = S^-1 c; returns r0^T D^-1 r0 -----------------------------------
   const bool lev2 = !L1OP && A.level >= 2;  // the level-1 variant is only launched at level 1
   const double* bvec = lev2 ? A.B + P.vec_off + (int64_t)rhs * nn : nullptr;
   auto init = [&](double tval) -> double {
     yh = warp_sinv<NCM>(Si, nc, tval);
+    if (crs) {  // x0 = M^-1 C^T S_M^-1 t: coarse part -vv with vv = -E^-1 (CZ)^T yhat
+      if (warp == 0) Ysh[lane] = yh;
+      __syncthreads();
+      coarse_v(0.0);
+    }
     if (wact) {
       sweep_ct([&](int i, int y, double ct) {
-        const double x0 = (double)dinv_s[y * DX + xc] * ct;
+        const double x0 = (double)dinv_s[y * DX + xc] * ct - vv_at(y);
         if (lact) p_s[(y + 1) * PX + x + 1] = x0;
         gput(tmx, i, x0);
       });
@@ -616,13 +709,20 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
         const double u = (double)dinv_s[(yb + i) * DX + xc] * r[i];
         rr += r[i] * u;
         acc_row(i, u, mL, mR, lL, lR);
+        if (crs && lact) Rg[(yb + i) * nx + x] = r[i];
       }
       c_reduce();
     }
     slot_put(2, rr);
     __syncthreads();
-    rr = slot_fin(2);
-    yh = warp_sinv<NCM>(Si, nc, fin_c());
+    if (crs) coarse_c();
+    rr = slot_fin(2) + (crs ? slot_fin(3) : 0.0);
+    yh = warp_sinv<NCM>(Si, nc, fin_c() + ((crs && lane < nc) ? csum[lane] : 0.0));
+    if (crs) {  // z of the first pass A: coarse part vv = zr - E^-1 (CZ)^T yhat
+      if (warp == 0) Ysh[lane] = yh;
+      __syncthreads();
+      coarse_v(1.0);
+    }
     return rr;
   };
 
@@ -687,6 +787,8 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
         if (g >= nrow) break;
         uint32_t xa[8];
         tm_ld8(tmx + 2 * g, xa);
+        uint32_t cword = 0;
+        if (CRS && crs) cword = tm_ld1(tmc + g / 4);
         tm_wait_ld();
         double xv[4];
 #pragma unroll
@@ -709,7 +811,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
             }
             const double rk = lact ? r[i] - ct : 0.0;
             r[i] = rk;
-            const double z = (double)dinv_s[y * DX + xc] * rk;
+            const double z = (double)dinv_s[y * DX + xc] * rk + ((CRS && crs && lact) ? vv_w(cword, u) : 0.0);
             double& pk = p_s[(y + 1) * PX + xc + 1];
             const double pold = pk;
             xv[u] += alpha * pold;
@@ -758,6 +860,8 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
         if (g >= nrow) break;
         uint32_t qa[8];
         tm_ld8(tmq + 2 * g, qa);
+        uint32_t cw4 = 0xFFFFFFFFu;
+        if (CRS && crs) cw4 = tm_ld1(tmc + g / 4);
         tm_wait_ld();
 #pragma unroll
         for (int u = 0; u < 4; u++) {
@@ -771,6 +875,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
             double mL[N], mR[N], lL[N], lR[N];
             cw.row(i == 0 && syp >= 0, mL, mR, lL, lR);
             acc_row(i, uu, mL, mR, lL, lR);
+            if (CRS && crs && lact && ((cw4 >> (8 * u)) & 255u) != 255u) Rg[y * nx + x] = rk;  // component nodes
           }
         }
       }
@@ -780,17 +885,19 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
     TMARK(5);
     slot_put(2, rr);
     __syncthreads();  // B3
-    if (warp == 0) {  // yhat = S^-1 c, beta = (r^T D^-1 r - c.yhat) / rz
-      const double cv = fin_c();
+    if (crs) coarse_c();
+    if (warp == 0) {  // yhat = S^-1 c, beta = (r^T D^-1 r - c.yhat) / rz  (M-metric with the coarse space)
+      const double cv = fin_c() + ((crs && lane < nc) ? csum[lane] : 0.0);
       const double yv = warp_sinv<NCM>(Si, nc, cv);
       const double cy = warp_sum0(cv * yv);
-      const double rrs = slot_fin(2);
+      const double rrs = slot_fin(2) + (crs ? slot_fin(3) : 0.0);
       Ysh[lane] = yv;
       if (lane == 0) Ysh[32] = (rrs - cy) / rz;
     }
     __syncthreads();  // B4
     yh = Ysh[lane];
     beta = Ysh[32];
+    if (crs) coarse_v(1.0);
     if (A.dbg && prob == A.dbg_prob && threadIdx.x == 0 && it < A.dbg_cap) {  // dev: MCH_PCG_DEBUG
       double* o = A.dbg + 8 * it;
       o[0] = rz; o[1] = pq; o[2] = alpha; o[3] = beta;
@@ -817,9 +924,14 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   }
   __syncthreads();
   yh = warp_sinv<NCM>(Si, nc, gcol - fin_c());
+  if (crs) {  // x += M^-1 C^T yhat: coarse part -vv with vv = -E^-1 (CZ)^T yhat
+    if (warp == 0) Ysh[lane] = yh;
+    __syncthreads();
+    coarse_v(0.0);
+  }
   if (wact) {
     double ctv[RPT];
-    sweep_ct([&](int i, int, double ct) { ctv[i] = ct; });
+    sweep_ct([&](int i, int y, double ct) { ctv[i] = ct - vv_at(y) / (double)dinv_s[y * DX + xc]; });
     double* xo = A.X + P.vec_off + (int64_t)rhs * nn;
     double* po = (A.level == 1 && P.pool_off >= 0) ? A.pool + P.pool_off + (int64_t)rhs * nn : nullptr;
     sweep_x([&](int i, int y, double xv) {
@@ -850,9 +962,10 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
-size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw, bool sstc, bool smlr) {
+size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw, bool sstc, bool smlr, bool crs) {
   const int PX = nxm + 2, KX = nxm + 1, DX = nxm, LW = (N == 1) ? 1 : ((N + 1) & ~1);
-  size_t d = ((81 * N * N + 1) & ~1) + 64 + 3 * 32 + (size_t)maxw * 32 + (size_t)PX * (nxm + 2);
+  size_t d = ((81 * N * N + 1) & ~1) + 64 + (crs ? 4 : 3) * 32 + (size_t)maxw * 32 + (size_t)PX * (nxm + 2);
+  if (crs) d += 2 * kCrsMax + 32;
   d += 1;  // O_LUT rounded up to 16 bytes
   if (sstc) d += 9 * (size_t)DX * nxm;
   if (smlr) d += 2 * (size_t)N * DX * nxm;
@@ -873,10 +986,10 @@ cudaError_t launch_node_ops2d(const LevelArgs& A, int max_nodes, cudaStream_t st
   return cudaGetLastError();
 }
 
-template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB, bool SSTC, bool SMLR>
+template <int RPT, int N, bool L1OP, int NXM, int MAXW, int MINB, bool SSTC, bool SMLR, bool CRS = false>
 static cudaError_t launch_one(const LevelArgs& A, int threads, cudaStream_t st) {
-  auto k = k_pcg2d<RPT, N, L1OP, NXM, MAXW, MINB, SSTC, SMLR>;
-  const size_t smem = pcg2d_smem_t(N, L1OP, NXM, MAXW, SSTC, SMLR);
+  auto k = k_pcg2d<RPT, N, L1OP, NXM, MAXW, MINB, SSTC, SMLR, CRS>;
+  const size_t smem = pcg2d_smem_t(N, L1OP, NXM, MAXW, SSTC, SMLR, CRS);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<(unsigned)A.nprob_mp * A.n_rhs, threads, smem, st>>>(A);
@@ -917,7 +1030,9 @@ static cudaError_t launch_one(const LevelArgs& A, int threads, cudaStream_t st) 
 template <int N>
 static cudaError_t launch_n(const LevelArgs& A, int variant, int threads, cudaStream_t st) {
   switch (variant) {
-    case PCG2D_V_L1: return launch_one<L1_RPT, N, true, 97, L1_MAXW, 1, false, false>(A, threads, st);
+    case PCG2D_V_L1:
+      if (A.coarse) return launch_one<L1_RPT, N, true, 97, L1_MAXW, 1, false, false, true>(A, threads, st);
+      return launch_one<L1_RPT, N, true, 97, L1_MAXW, 1, false, false>(A, threads, st);
     case PCG2D_V_GN49:
       return launch_one<GN49_RPT, N, false, 49, GN49_MAXW, GN49_MINB, GN49_SSTC, GN49_SMLR>(A, threads, st);
     case PCG2D_V_GN25: return launch_one<9, N, false, 25, 4, GN25_MINB, GN25_SSTC, GN25_SMLR>(A, threads, st);
