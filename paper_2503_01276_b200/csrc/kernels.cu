@@ -345,7 +345,7 @@ __global__ void k_proj_setup(LevelArgs A) {
     }
   }
   // two-level preconditioner: S_M = C M^-1 C^T = C D^-1 C^T + (CZ) E^-1 (CZ)^T
-  if (A.coarse && A.level == 1) {
+  if (A.coarse) {
     const int nca = A.ncomp[mp];
     const double* CZ = A.CZ + (int64_t)mp * nc * A.ncmax;
     const double* Ei = A.Einv + (int64_t)mp * A.ncmax;
@@ -426,6 +426,8 @@ __global__ void k_proj_setup(LevelArgs A) {
 // pointer jumping (the result is the smallest node index of each component, independent of
 // the order of updates) and numbered in node order.  Per component: bounding box, E_aa = z_a^T
 // A z_a, and C z_a (constraint rows of the indicator).  Everything summed in a fixed order.
+constexpr int kCompNodes = 96;  // largest component kept in the coarse space
+
 template <int D>
 __global__ void k_coarse_setup(LevelArgs A) {
   const int mp = blockIdx.x;
@@ -438,12 +440,25 @@ __global__ void k_coarse_setup(LevelArgs A) {
   extern __shared__ double smem[];
   double* cvals = smem;                               // ncon
   int* cnt = reinterpret_cast<int*>(cvals + nc);       // blockDim.x
+  // kappa of a level-n cell: the fine value (level 1) or the mean over its s^D fine cells
+  auto kcell = [&](const int* e) -> double {
+    if (g.fineop) return A.kappa[fine_cell_index<D>(A, P, g, e, nullptr)];
+    double sum = 0.0;
+    const int s = g.s;
+    for (int iz = 0; iz < (D == 3 ? s : 1); iz++)
+      for (int iy = 0; iy < s; iy++)
+        for (int ix = 0; ix < s; ix++) {
+          const int sub[3] = {ix, iy, iz};
+          sum += A.kappa[fine_cell_index<D>(A, P, g, e, sub)];
+        }
+    return sum / (double)((D == 3) ? s * s * s : s * s);
+  };
   // 1. contrast of the window
   double kmin = 1e300, kmax = 0.0;
   const int ncell = g.nc[0] * g.nc[1] * (D == 3 ? g.nc[2] : 1);
   for (int idx = threadIdx.x; idx < ncell; idx += blockDim.x) {
     int e[3] = {idx % g.nc[0], (idx / g.nc[0]) % g.nc[1], (D == 3) ? idx / (g.nc[0] * g.nc[1]) : 0};
-    const double kv = A.kappa[fine_cell_index<D>(A, P, g, e, nullptr)];
+    const double kv = kcell(e);
     kmin = fmin(kmin, kv);
     kmax = fmax(kmax, kv);
   }
@@ -471,7 +486,7 @@ __global__ void k_coarse_setup(LevelArgs A) {
           e[i] = x[i] - 1 + ((o >> i) & 1);
           ok = ok && e[i] >= 0 && e[i] < g.nc[i];
         }
-        if (ok && A.kappa[fine_cell_index<D>(A, P, g, e, nullptr)] > thr) lab = k;
+        if (ok && kcell(e) > thr) lab = k;
       }
     }
     cm[k] = lab;
@@ -532,7 +547,6 @@ __global__ void k_coarse_setup(LevelArgs A) {
     total = s;
   }
   __syncthreads();
-  const int ncomp = (total <= A.ncmax) ? total : 0;
   {
     int id = cnt[threadIdx.x];
     for (int k = k0; k < k1; k++)
@@ -547,7 +561,29 @@ __global__ void k_coarse_setup(LevelArgs A) {
   for (int k = threadIdx.x; k < nn; k += blockDim.x) {
     const int lk = cm[k];
     if (lk <= -2) cm[k] = -lk - 2;  // root: decode
-    if (ncomp == 0) cm[k] = -1;
+  }
+  __syncthreads();
+  // keep components of at most kCompNodes nodes (long ones, e.g. channels across the window,
+  // would make the per-component sums of every iteration a long serial chain), renumbered in
+  // order; at most ncmax of them
+  __shared__ int csize[1024];
+  __shared__ int cnew[1024];
+  const int nall = min(total, 1024);
+  for (int a = threadIdx.x; a < nall; a += blockDim.x) csize[a] = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < nn; k += blockDim.x)
+    if (cm[k] >= 0 && cm[k] < nall) atomicAdd(&csize[cm[k]], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int next = 0;
+    for (int a = 0; a < nall; a++) cnew[a] = (csize[a] <= kCompNodes && next < A.ncmax) ? next++ : -1;
+    total = (total > 1024) ? 0 : next;
+  }
+  __syncthreads();
+  const int ncomp = total;
+  for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+    const int lk = cm[k];
+    cm[k] = (lk >= 0 && lk < nall && ncomp > 0) ? cnew[lk] : -1;
   }
   if (threadIdx.x == 0) A.ncomp[mp] = ncomp;
   int* box = A.cbox + (int64_t)mp * A.ncmax * 6;
@@ -624,14 +660,15 @@ __global__ void k_coarse_setup(LevelArgs A) {
           ok = ok && e[i] >= 0 && e[i] < g.nc[i];
         }
         if (!ok) continue;
-        const double kap = A.kappa[fine_cell_index<D>(A, P, g, e, nullptr)];
         const int ac = (~o) & ((1 << D) - 1);  // corner of node k in cell e
-        auto zb = [&](int b) {
+        double zc[1 << D];
+        for (int b = 0; b < (1 << D); b++) {
           int xb[3] = {e[0] + (b & 1), e[1] + ((b >> 1) & 1), (D == 3) ? e[2] + ((b >> 2) & 1) : 0};
-          return (cm[node_id<D>(g, xb)] == a) ? 1.0 : 0.0;
-        };
-        if (D == 2) az += kap * (1.0 / 6.0) * (4.0 * zb(ac) - zb(ac ^ 1) - zb(ac ^ 2) - 2.0 * zb(ac ^ 3));
-        else az += kap * A.h * (1.0 / 12.0) * (4.0 * zb(ac) - zb(ac ^ 3) - zb(ac ^ 5) - zb(ac ^ 6) - zb(ac ^ 7));
+          zc[b] = (cm[node_id<D>(g, xb)] == a) ? 1.0 : 0.0;
+        }
+        double W[DimC<D>::NW];
+        elem_W<D>(A, P, g, e, W);  // level 1: kappa times the Q1 weights; n >= 2: exact Galerkin
+        az += elem_row<D>(W, zc, ac);
       }
       v[0] += az;
     }
@@ -651,20 +688,23 @@ __global__ void k_coarse_setup(LevelArgs A) {
       lo[i] = (i < D) ? max(bx[i] - 1, 0) : 0;
       hi[i] = (i < D) ? min(bx[3 + i], g.nc[i] - 1) : 0;
     }
-    const double hq = (D == 2) ? 0.25 * A.h * A.h : 0.125 * A.h * A.h * A.h;
     for (int ez = lo[2]; ez <= hi[2]; ez++)
       for (int ey = lo[1]; ey <= hi[1]; ey++)
         for (int ex = lo[0]; ex <= hi[0]; ex++) {
           const int e[3] = {ex, ey, ez};
-          int cntc = 0;
+          unsigned in = 0;
           for (int b = 0; b < (1 << D); b++) {
             const int xb[3] = {ex + (b & 1), ey + ((b >> 1) & 1), (D == 3) ? ez + ((b >> 2) & 1) : 0};
-            cntc += (cm[node_id<D>(g, xb)] == a);
+            if (cm[node_id<D>(g, xb)] == a) in |= 1u << b;
           }
-          if (cntc == 0) continue;
+          if (!in) continue;
           const int q = elem_subcell<D>(A, P, g, e);
-          const int id = A.ids[fine_cell_index<D>(A, P, g, e, nullptr)];
-          CZ[(int64_t)(q * A.N + id) * A.ncmax + a] += hq * cntc;
+          for (int j = 0; j < A.N; j++) {
+            double m = 0.0;
+            for (int b = 0; b < (1 << D); b++)
+              if ((in >> b) & 1u) m += elem_m<D>(A, P, g, e, j, b);
+            CZ[(int64_t)(q * A.N + j) * A.ncmax + a] += m;
+          }
         }
   }
 }
@@ -947,7 +987,7 @@ __global__ void __launch_bounds__(512, (D == 2) ? 2 : 1) k_pcg(LevelArgs A) {
   double* tg = cvec + nc;                         // nc
   double* gcol = tg + nc;                         // nc
   double* g0col = gcol + nc;                      // nc
-  const bool crs = A.coarse && A.level == 1 && !band && A.ncomp[mp] > 0;  // two-level preconditioner
+  const bool crs = A.coarse && !band && A.ncomp[mp] > 0;  // two-level preconditioner
   double* zr = g0col + nc;                        // coarse: ncmax (E^-1 Z^T r)
   double* vv = zr + (A.coarse ? A.ncmax : 0);     // coarse: ncmax (coarse part of z)
   double* bins = vv + (A.coarse ? A.ncmax : 0);   // dense: 32*nc

@@ -604,7 +604,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   // ---- two-level preconditioner M^-1 = D^-1 + Z E^-1 Z^T (level 1): r is mirrored
   //      to global memory in pass C and summed per component there (one warp per component over
   //      its bounding box, fixed order); the projection uses S_M = C M^-1 C^T (k_proj_setup) ----
-  const bool crs = CRS && A.level == 1 && A.ncomp[mp] > 0;
+  const bool crs = CRS && A.ncomp[mp] > 0;
   const int nca = crs ? A.ncomp[mp] : 0;
   const int* cmp = A.cmap + P.node_off;
   const int* cpt = A.cptr + (int64_t)mp * (A.ncmax + 1);
@@ -1034,6 +1034,8 @@ static cudaError_t launch_n(const LevelArgs& A, int variant, int threads, cudaSt
       if (A.coarse) return launch_one<L1_RPT, N, true, 97, L1_MAXW, 1, false, false, true>(A, threads, st);
       return launch_one<L1_RPT, N, true, 97, L1_MAXW, 1, false, false>(A, threads, st);
     case PCG2D_V_GN49:
+      if (A.coarse)
+        return launch_one<GN49_RPT, N, false, 49, GN49_MAXW, GN49_MINB, GN49_SSTC, GN49_SMLR, true>(A, threads, st);
       return launch_one<GN49_RPT, N, false, 49, GN49_MAXW, GN49_MINB, GN49_SSTC, GN49_SMLR>(A, threads, st);
     case PCG2D_V_GN25: return launch_one<9, N, false, 25, 4, GN25_MINB, GN25_SSTC, GN25_SMLR>(A, threads, st);
     case PCG2D_V_GN97: return launch_one<17, N, false, 97, 24, 1, false, false>(A, threads, st);
