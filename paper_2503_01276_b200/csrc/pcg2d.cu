@@ -250,6 +250,7 @@ __global__ void k_node_ops2d(LevelArgs A) {
 // the solver: one CTA per problem (macropoint, rhs)
 #ifdef PCG2D_TIMING
 __device__ unsigned long long g_pcg2d_phase[16];
+__device__ unsigned long long g_pcg2d_crs[8];
 void pcg2d_phase_dump(const char* tag) {
   unsigned long long h[16];
   cudaDeviceSynchronize();
@@ -260,6 +261,12 @@ void pcg2d_phase_dump(const char* tag) {
   fprintf(stderr, "[pcg2d timing %s] active-warp cycles per warp-iteration:", tag);
   for (int k = 0; k < 7; k++) fprintf(stderr, " %s=%.0f", nm[k], (double)h[k] / (double)h[7]);
   fprintf(stderr, " total=%.0f\n", tot / (double)h[7]);
+  unsigned long long cc[8];
+  cudaMemcpyFromSymbol(cc, g_pcg2d_crs, sizeof cc);
+  fprintf(stderr, "  coarse sub-phases per warp-iteration: zr=%.0f csum=%.0f warp0+B4=%.0f vv=%.0f\n",
+          (double)cc[0] / h[7], (double)cc[1] / h[7], (double)cc[2] / h[7], (double)cc[3] / h[7]);
+  unsigned long long zz[8] = {0};
+  cudaMemcpyToSymbol(g_pcg2d_crs, zz, sizeof zz);
   unsigned long long z[16] = {0};
   cudaMemcpyToSymbol(g_pcg2d_phase, z, sizeof z);
 }
@@ -619,14 +626,24 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   // zr = E^-1 Z^T Rg, slot 3 = (Z^T r)^T E^-1 (Z^T r); then csum = (CZ) zr.  Two barriers.
   auto coarse_c = [&]() {
     double part = 0.0;
-    for (int a = threadIdx.x; a < nca; a += blockDim.x) {  // one thread per component, fixed order
-      const int i0 = __ldg(cpt + a), i1 = __ldg(cpt + a + 1);
+    // groups of 4 lanes per component, each lane a strided quarter of its node list, combined by
+    // two xor shuffles (fixed order); rounds over the components are uniform per warp
+    const int sub = lane & 3, ngrp = blockDim.x >> 2;
+    for (int a0 = threadIdx.x >> 2; a0 - (int)(threadIdx.x >> 2) < nca; a0 += ngrp) {
+      const int a = a0;
       double sv = 0.0;
-#pragma unroll 16
-      for (int i = i0; i < i1; i++) sv += __ldcg(Rg + __ldg(cls + i));
-      const double ei = __ldg(Eiv + a);
-      zr[a] = sv * ei;
-      part += sv * sv * ei;
+      if (a < nca) {
+        const int i0 = __ldg(cpt + a), i1 = __ldg(cpt + a + 1);
+#pragma unroll 8
+        for (int i = i0 + sub; i < i1; i += 4) sv += __ldcg(Rg + __ldg(cls + i));
+      }
+      sv += __shfl_xor_sync(FULLMASK, sv, 1);
+      sv += __shfl_xor_sync(FULLMASK, sv, 2);
+      if (a < nca && sub == 0) {
+        const double ei = __ldg(Eiv + a);
+        zr[a] = sv * ei;
+        part += sv * sv * ei;
+      }
     }
     part = warp_sum0(part);
     if (lane == 0) slots[3 * 32 + warp] = part;
@@ -885,7 +902,13 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
     TMARK(5);
     slot_put(2, rr);
     __syncthreads();  // B3
+#ifdef PCG2D_TIMING
+    unsigned long long tc0 = clock64();
+#endif
     if (crs) coarse_c();
+#ifdef PCG2D_TIMING
+    unsigned long long tc1 = clock64();
+#endif
     if (warp == 0) {  // yhat = S^-1 c, beta = (r^T D^-1 r - c.yhat) / rz  (M-metric with the coarse space)
       const double cv = fin_c() + ((crs && lane < nc) ? csum[lane] : 0.0);
       const double yv = warp_sinv<NCM>(Si, nc, cv);
@@ -897,7 +920,18 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
     __syncthreads();  // B4
     yh = Ysh[lane];
     beta = Ysh[32];
+#ifdef PCG2D_TIMING
+    unsigned long long tc2 = clock64();
+#endif
     if (crs) coarse_v(1.0);
+#ifdef PCG2D_TIMING
+    unsigned long long tc3 = clock64();
+    if (lane == 0 && wact) {
+      atomicAdd(&g_pcg2d_crs[0], tc1 - tc0);
+      atomicAdd(&g_pcg2d_crs[2], tc2 - tc1);
+      atomicAdd(&g_pcg2d_crs[3], tc3 - tc2);
+    }
+#endif
     if (A.dbg && prob == A.dbg_prob && threadIdx.x == 0 && it < A.dbg_cap) {  // dev: MCH_PCG_DEBUG
       double* o = A.dbg + 8 * it;
       o[0] = rz; o[1] = pq; o[2] = alpha; o[3] = beta;
