@@ -278,7 +278,7 @@ def main():
                      "all_levels_pcg_GBps": all_b / (all_ms * 1e-3) / 1e9,
                      "peak_source": pk_src,
                      "algorithmic_bytes": "8*(6*nodes*iters per problem + D_n*cells*max_iters per macropoint), D_n = 1 (L1) / 5 (2D) / 19 (3D)",
-                     "note": "SURVEY 8(d) streaming bytes; the kernel keeps its state on chip (DRAM traffic = 'traffic'), it is issue/latency bound - DESIGN.md 6"},
+                     "note": "SURVEY 8(d) streaming bytes per PCG iteration; the kernel keeps its state on chip (DRAM traffic = 'traffic') and is issue/latency bound; the two-level preconditioner trades work per iteration for 3x fewer iterations, which lowers this per-iteration fraction while raising solves/s - DESIGN.md 6"},
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": kap.nbytes + ids.nbytes,
                 "d2h_bytes_per_step": Gh.numel() * 8},
