@@ -534,7 +534,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     }
     // level 1 only: at level 2 the fixed per-iteration cost of the coarse sums outweighs the saved
     // iterations (config 2: 245 -> 106 iterations but 15 -> 45 ms)
-    B->coarse = c->coarse && level == 1 && c->band == 0 && !B->on3d && (!B->on2d || B->variant == PCG2D_V_L1);
+    B->coarse = c->coarse && level == 1 && c->band == 0 && (!B->on2d || B->variant == PCG2D_V_L1);
     if (B->coarse) {
       if (B->on2d) CKC(c, c->R.ensure(sizeof(double) * B->vec_off));  // r mirrored for the coarse sums
       CKC(c, c->cmap.ensure(sizeof(int) * B->node_off));

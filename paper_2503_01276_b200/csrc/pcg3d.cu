@@ -558,9 +558,11 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
   double* bins = smem;          // [NT task rows][NQ]
   double* Ysh = bins + NT * NQ;  // [NQ]
   double* csh = Ysh + NQ;        // [NQ]
-  double* slots = csh + NQ;      // [4][32]
-  int* zsm = reinterpret_cast<int*>(slots + 4 * 32);  // [49][3]
-  for (int i = threadIdx.x; i < NT * NQ + 2 * NQ + 4 * 32; i += blockDim.x) bins[i] = 0.0;
+  double* slots = csh + NQ;      // [5][32]
+  double* zr = slots + 5 * 32;   // [256] coarse: E^-1 Z^T r
+  double* vv = zr + 256;         // [256] coarse: coarse part of z
+  int* zsm = reinterpret_cast<int*>(vv + 256);  // [49][3]
+  for (int i = threadIdx.x; i < NT * NQ + 2 * NQ + 5 * 32; i += blockDim.x) bins[i] = 0.0;
   for (int z = threadIdx.x; z < nz; z += blockDim.x) {
     const Sides sd = sides_of(A, P, 2, z, ncz, 1);
     zsm[z * 3] = sd.pm;
@@ -852,6 +854,60 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
     if (lane == 0) slots[3 * 32 + warp] = cyw;
   };
 
+  // two-level preconditioner (level 1): M^-1 = D^-1 + Z E^-1 Z^T, M-metric projection
+  const bool crs = (MODE == 0) && A.coarse && A.ncomp[mp] > 0;
+  const int nca = crs ? A.ncomp[mp] : 0;
+  const int* cmp = A.cmap + P.node_off;
+  const int* cpt = A.cptr + (int64_t)mp * (A.ncmax + 1);
+  const int* cls = A.clist + P.node_off;
+  const double* Eiv = A.Einv + (int64_t)mp * A.ncmax;
+  const double* CZm = A.CZ + (int64_t)mp * nc * A.ncmax;
+  // zr = E^-1 Z^T R (4-lane groups over each component's node list), slot 4 = (Z^T r)^T E^-1 Z^T r,
+  // then csh += (CZ) zr.  Two barriers.
+  auto coarse_c = [&]() {
+    double part = 0.0;
+    const int sub = lane & 3, ngrp = blockDim.x >> 2;
+    for (int a0 = threadIdx.x >> 2; a0 - (int)(threadIdx.x >> 2) < nca; a0 += ngrp) {
+      const int a = a0;
+      double sv = 0.0;
+      if (a < nca) {
+        const int i0 = __ldg(cpt + a), i1 = __ldg(cpt + a + 1);
+        for (int i = i0 + sub; i < i1; i += 4) sv += __ldcg(Rv + __ldg(cls + i));
+      }
+      sv += __shfl_xor_sync(FULLMASK, sv, 1);
+      sv += __shfl_xor_sync(FULLMASK, sv, 2);
+      if (a < nca && sub == 0) {
+        const double ei = __ldg(Eiv + a);
+        zr[a] = sv * ei;
+        part += sv * sv * ei;
+      }
+    }
+    part = wsum0(part);
+    if (lane == 0) slots[4 * 32 + warp] = part;
+    __syncthreads();
+    for (int t = warp; t < nc; t += NW) {
+      double sv = 0.0;
+      for (int a = lane; a < nca; a += 32) sv += __ldg(CZm + (int64_t)t * A.ncmax + a) * zr[a];
+      sv = wsum0(sv);
+      if (lane == 0) csh[t] += sv;
+    }
+    __syncthreads();
+  };
+  // vv = s0 zr - E^-1 (CZ)^T Ysh.  One barrier.
+  auto coarse_v = [&](double s0) {
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) {
+      double acc = 0.0;
+      for (int t = 0; t < nc; t++) acc += __ldg(CZm + (int64_t)t * A.ncmax + a) * Ysh[t];
+      vv[a] = (s0 != 0.0 ? s0 * zr[a] : 0.0) - __ldg(Eiv + a) * acc;
+    }
+    __syncthreads();
+  };
+  auto cz_at = [&](int k) -> double {
+    if (!crs) return 0.0;
+    const int a = __ldg(cmp + k);
+    return (a >= 0) ? vv[a] : 0.0;
+  };
+
   if (MODE == 1) {
     double* Yv = A.FY + P.fine_off + (int64_t)rhs * nn;
     tasks([&] {
@@ -874,11 +930,12 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
   __syncthreads();
   solve_y();
   __syncthreads();
+  if (crs) coarse_v(0.0);
   tasks([&] {
     if (!wact) return;
     walk_ids([&](int z, int k, const int (&idc)[8]) {
       if (!lact) return;
-      const double x0 = dg[k] * ct_of(z, idc);
+      const double x0 = dg[k] * ct_of(z, idc) - cz_at(k);
       pv[k] = x0;
       Xv[k] = x0;
     });
@@ -902,9 +959,11 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
   __syncthreads();
   reduce_c(nullptr);
   __syncthreads();
+  if (crs) coarse_c();
   solve_y();
   __syncthreads();
-  rr0 = slot_fin(2);
+  rr0 = slot_fin(2) + (crs ? slot_fin(4) : 0.0);
+  if (crs) coarse_v(1.0);
 
   const double tol2 = A.rtol * A.rtol;
   const double floor2 = 1e-30 * rr0;
@@ -918,7 +977,7 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
       walk_ids([&](int z, int k, const int (&idc)[8]) {
         if (!lact) return;
         const double rk = Rv[k] - ct_of(z, idc);
-        const double zz = dg[k] * rk;
+        const double zz = dg[k] * rk + cz_at(k);
         const double pold = pv[k];
         if (!first) Xv[k] += alpha * pold;
         pv[k] = first ? -zz : -zz + beta * pold;
@@ -965,9 +1024,11 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
     __syncthreads();  // B3
     reduce_c(nullptr);
     __syncthreads();
+    if (crs) coarse_c();
     solve_y();
     __syncthreads();  // B4
-    beta = (slot_fin(2) - slot_fin(3)) / rz;
+    beta = (slot_fin(2) + (crs ? slot_fin(4) : 0.0) - slot_fin(3)) / rz;
+    if (crs) coarse_v(1.0);
   }
 
   // feasibility restoration: x += D^-1 C^T S^-1 (g - C x); parents also into the pool
@@ -979,12 +1040,13 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
   __syncthreads();
   solve_y();
   __syncthreads();
+  if (crs) coarse_v(0.0);
   double* po = (P.pool_off >= 0) ? A.pool + P.pool_off + (int64_t)rhs * nn : nullptr;
   tasks([&] {
     if (!wact) return;
     walk_ids([&](int z, int k, const int (&idc)[8]) {
       if (!lact) return;
-      const double xf = Xv[k] + dg[k] * ct_of(z, idc);
+      const double xf = Xv[k] + dg[k] * ct_of(z, idc) - cz_at(k);
       Xv[k] = xf;
       if (po) po[k] = xf;
     });
@@ -1001,7 +1063,7 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1(LevelArgs
 }
 
 size_t pcg3d_l1_smem(int N) {
-  return (size_t)(98 * 27 * N + 2 * 27 * N + 4 * 32) * sizeof(double) + 49 * 3 * sizeof(int);
+  return (size_t)(98 * 27 * N + 2 * 27 * N + 5 * 32 + 512) * sizeof(double) + 49 * 3 * sizeof(int);
 }
 
 // 14 warps (one CTA per SM) when the launch is at most a few waves, else 7 warps (two CTAs per SM:
