@@ -484,3 +484,24 @@ def test_coarse_space_preconditioner(monkeypatch):
     G0, G1 = res["0"][1], res["1"][1]
     for i in range(G0.shape[0]):
         assert g_err(G1[i], G0[i]) < G_TOL, (i, g_err(G1[i], G0[i]))
+
+
+def test_transport_paths_agree(monkeypatch):
+    """3D levels >= 2: the split transport (I_p, column-walking A_1 I_p / C_1 I_p, separable
+    P_n^T) and the generic per-node k_transport (MCH_TRANSPORT_GENERIC) give the same
+    coefficients (R15 bar) and both match the oracle."""
+    H = _gpu()
+    d, n, M, L, N = 3, 16, 4, 2, 2
+    kap, ids = _admissible(d, n, M, N, 970)
+    o = Oracle(d, n, M, L, 2, N, kap, ids)
+    Go = o.effective_coeffs()
+    res = {}
+    for flag in (None, "1"):
+        if flag:
+            monkeypatch.setenv("MCH_TRANSPORT_GENERIC", flag)
+        with H(d, n, N, M, L, 2, kap, ids) as h:
+            h.solve_all()
+            res[flag] = h.effective_coeffs()
+    for i in range(Go.shape[0]):
+        assert g_err(res[None][i], Go[i]) < G_TOL and g_err(res["1"][i], Go[i]) < G_TOL
+        assert g_err(res[None][i], res["1"][i]) < 1e-10
