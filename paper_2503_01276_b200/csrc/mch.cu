@@ -451,7 +451,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       for (int v : cands) {
         int rpt, nxm, maxw, l1op, sstc, smlr;
         pcg2d_variant(v, &rpt, &nxm, &maxw, &l1op, &sstc, &smlr);
-        const bool crs_v = c->coarse && level == 1 && v == PCG2D_V_L1;
+        const bool crs_v = c->coarse && ((level == 1 && v == PCG2D_V_L1) || (level == 2 && v == PCG2D_V_GN49));
         if (maxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0, crs_v) > 232448) continue;
         std::vector<int> nsegs(nmp);
         std::vector<std::vector<short4>> per(nmp);
@@ -534,9 +534,12 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     }
     // level 1 only: at level 2 the fixed per-iteration cost of the coarse sums outweighs the saved
     // iterations (config 2: 245 -> 106 iterations but 15 -> 45 ms)
-    B->coarse = c->coarse && level == 1 && c->band == 0 && (!B->on2d || B->variant == PCG2D_V_L1);
+    // level 1 everywhere; level 2 on the 49-node on-chip variant, whose shared memory holds the
+    // coarse data (with it in L2 the fixed per-iteration cost outweighed the saved iterations)
+    B->coarse = c->coarse && c->band == 0 &&
+                ((level == 1 && (!B->on2d || B->variant == PCG2D_V_L1)) || (level == 2 && B->on2d && B->variant == PCG2D_V_GN49));
     if (B->coarse) {
-      if (B->on2d) CKC(c, c->R.ensure(sizeof(double) * B->vec_off));  // r mirrored for the coarse sums
+      if (B->on2d && B->variant == PCG2D_V_L1) CKC(c, c->R.ensure(sizeof(double) * B->vec_off));  // r mirror (L2)
       CKC(c, c->cmap.ensure(sizeof(int) * B->node_off));
       CKC(c, c->ncomp.ensure(sizeof(int) * nmp));
       CKC(c, c->cbox.ensure(sizeof(int) * 6 * kCoarseMax * (size_t)nmp));

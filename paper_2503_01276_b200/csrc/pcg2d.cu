@@ -312,7 +312,14 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   constexpr int O_ZR = O_ML + (SMLR ? 2 * N * PLANE : 0);  // CRS: E^-1 Z^T r per component
   constexpr int O_VV = O_ZR + NCC;                        // CRS: coarse part of z per component
   constexpr int O_CS = O_VV + NCC;                        // CRS: (CZ) E^-1 Z^T r per constraint row
-  constexpr int O_D = O_CS + (CRS ? 32 : 0);              // end of the double region
+  // CSM (coarse data resident in shared memory; the precomputed-operator variants have room):
+  // r mirror, CZ, E^-1 and the component node lists (ints)
+  constexpr bool CSM = CRS && !L1OP;
+  constexpr int O_RS = O_CS + (CRS ? 32 : 0);
+  constexpr int O_CZ = O_RS + (CSM ? PLANE : 0);
+  constexpr int O_EI = O_CZ + (CSM ? NCM * kCrsMax : 0);
+  constexpr int O_CL = O_EI + (CSM ? kCrsMax : 0);
+  constexpr int O_D = O_CL + (CSM ? (PLANE + kCrsMax + 2) / 2 : 0);  // end of the double region
   double* Si = smem;                      // [NCM*NCM] S^-1 (nc*nc used)
   double* Ysh = smem + O_Y;               // [32] yhat, [32] beta (written by warp 0)
   double* slots = smem + O_SL;            // [3][32] scalar partial sums (rz, pq, rr)
@@ -622,6 +629,22 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   double* zr = smem + O_ZR;
   double* vv = smem + O_VV;
   double* csum = smem + O_CS;
+  double* rsm = smem + O_RS;                                // CSM: r mirror [ny][nx]
+  double* czs = smem + O_CZ;                                // CSM: CZ [nc][kCrsMax]
+  double* eis = smem + O_EI;                                // CSM: E^-1
+  int* cls_s = reinterpret_cast<int*>(smem + O_CL);         // CSM: node lists
+  int* cpt_s = cls_s + PLANE;                               // CSM: list starts [nca+1]
+  if (CSM && crs) {
+    for (int i = threadIdx.x; i < nc * nca; i += blockDim.x) {
+      const int t = i / nca, a = i - t * nca;
+      czs[t * kCrsMax + a] = __ldg(CZm + (int64_t)t * A.ncmax + a);
+    }
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) eis[a] = __ldg(Eiv + a);
+    for (int a = threadIdx.x; a <= nca; a += blockDim.x) cpt_s[a] = __ldg(cpt + a);
+    const int nl = __ldg(cpt + nca);
+    for (int i = threadIdx.x; i < nl; i += blockDim.x) cls_s[i] = __ldg(cls + i);
+    __syncthreads();
+  }
   const int nwarps = blockDim.x >> 5;
   // zr = E^-1 Z^T Rg, slot 3 = (Z^T r)^T E^-1 (Z^T r); then csum = (CZ) zr.  Two barriers.
   auto coarse_c = [&]() {
@@ -633,14 +656,19 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
       const int a = a0;
       double sv = 0.0;
       if (a < nca) {
-        const int i0 = __ldg(cpt + a), i1 = __ldg(cpt + a + 1);
+        if (CSM) {
+          const int i0 = cpt_s[a], i1 = cpt_s[a + 1];
+          for (int i = i0 + sub; i < i1; i += 4) sv += rsm[cls_s[i]];
+        } else {
+          const int i0 = __ldg(cpt + a), i1 = __ldg(cpt + a + 1);
 #pragma unroll 8
-        for (int i = i0 + sub; i < i1; i += 4) sv += __ldcg(Rg + __ldg(cls + i));
+          for (int i = i0 + sub; i < i1; i += 4) sv += __ldcg(Rg + __ldg(cls + i));
+        }
       }
       sv += __shfl_xor_sync(FULLMASK, sv, 1);
       sv += __shfl_xor_sync(FULLMASK, sv, 2);
       if (a < nca && sub == 0) {
-        const double ei = __ldg(Eiv + a);
+        const double ei = CSM ? eis[a] : __ldg(Eiv + a);
         zr[a] = sv * ei;
         part += sv * sv * ei;
       }
@@ -650,7 +678,8 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
     __syncthreads();
     for (int t = warp; t < nc; t += nwarps) {
       double sv = 0.0;
-      for (int a = lane; a < nca; a += 32) sv += __ldg(CZm + (int64_t)t * A.ncmax + a) * zr[a];
+      for (int a = lane; a < nca; a += 32)
+        sv += (CSM ? czs[t * kCrsMax + a] : __ldg(CZm + (int64_t)t * A.ncmax + a)) * zr[a];
       sv = warp_sum0(sv);
       if (lane == 0) csum[t] = sv;
     }
@@ -660,8 +689,8 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   auto coarse_v = [&](double s0) {
     for (int a = threadIdx.x; a < nca; a += blockDim.x) {
       double acc = 0.0;
-      for (int t = 0; t < nc; t++) acc += __ldg(CZm + (int64_t)t * A.ncmax + a) * Ysh[t];
-      vv[a] = (s0 != 0.0 ? s0 * zr[a] : 0.0) - __ldg(Eiv + a) * acc;
+      for (int t = 0; t < nc; t++) acc += (CSM ? czs[t * kCrsMax + a] : __ldg(CZm + (int64_t)t * A.ncmax + a)) * Ysh[t];
+      vv[a] = (s0 != 0.0 ? s0 * zr[a] : 0.0) - (CSM ? eis[a] : __ldg(Eiv + a)) * acc;
     }
     __syncthreads();
   };
@@ -726,7 +755,10 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
         const double u = (double)dinv_s[(yb + i) * DX + xc] * r[i];
         rr += r[i] * u;
         acc_row(i, u, mL, mR, lL, lR);
-        if (crs && lact) Rg[(yb + i) * nx + x] = r[i];
+        if (crs && lact) {
+          if (CSM) rsm[(yb + i) * nx + x] = r[i];
+          else Rg[(yb + i) * nx + x] = r[i];
+        }
       }
       c_reduce();
     }
@@ -892,7 +924,10 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
             double mL[N], mR[N], lL[N], lR[N];
             cw.row(i == 0 && syp >= 0, mL, mR, lL, lR);
             acc_row(i, uu, mL, mR, lL, lR);
-            if (CRS && crs && lact && ((cw4 >> (8 * u)) & 255u) != 255u) Rg[y * nx + x] = rk;  // component nodes
+            if (CRS && crs && lact && ((cw4 >> (8 * u)) & 255u) != 255u) {  // component nodes
+              if (CSM) rsm[y * nx + x] = rk;
+              else Rg[y * nx + x] = rk;
+            }
           }
         }
       }
@@ -1000,6 +1035,7 @@ size_t pcg2d_smem_t(int N, bool l1op, int nxm, int maxw, bool sstc, bool smlr, b
   const int PX = nxm + 2, KX = nxm + 1, DX = nxm, LW = (N == 1) ? 1 : ((N + 1) & ~1);
   size_t d = ((81 * N * N + 1) & ~1) + 64 + (crs ? 4 : 3) * 32 + (size_t)maxw * 32 + (size_t)PX * (nxm + 2);
   if (crs) d += 2 * kCrsMax + 32;
+  if (crs && !l1op) d += (size_t)DX * nxm + 9 * N * kCrsMax + kCrsMax + ((size_t)DX * nxm + kCrsMax + 2) / 2;
   d += 1;  // O_LUT rounded up to 16 bytes
   if (sstc) d += 9 * (size_t)DX * nxm;
   if (smlr) d += 2 * (size_t)N * DX * nxm;
