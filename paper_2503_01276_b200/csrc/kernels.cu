@@ -426,7 +426,13 @@ __global__ void k_proj_setup(LevelArgs A) {
 // pointer jumping (the result is the smallest node index of each component, independent of
 // the order of updates) and numbered in node order.  Per component: bounding box, E_aa = z_a^T
 // A z_a, and C z_a (constraint rows of the indicator).  Everything summed in a fixed order.
-constexpr int kCompNodes = 96;  // largest component kept in the coarse space
+#ifndef MCH_COARSE_CONTRAST
+#define MCH_COARSE_CONTRAST 20.0  // window contrast kappa_max / kappa_min that turns the coarse space on
+#endif
+#ifndef MCH_COMP_NODES
+#define MCH_COMP_NODES 400
+#endif
+constexpr int kCompNodes = MCH_COMP_NODES;  // largest component kept in the coarse space
 
 template <int D>
 __global__ void k_coarse_setup(LevelArgs A) {
@@ -471,7 +477,7 @@ __global__ void k_coarse_setup(LevelArgs A) {
   __syncthreads();
   kmin = 1e300; kmax = 0.0;
   for (int w = 0; w < nw; w++) { kmin = fmin(kmin, red[w]); kmax = fmax(kmax, red[32 + w]); }
-  const bool use = kmax >= 100.0 * kmin;
+  const bool use = kmax >= MCH_COARSE_CONTRAST * kmin;
   const double thr = sqrt(kmin * kmax);
   // 2. high nodes: label = own index
   for (int k = threadIdx.x; k < nn; k += blockDim.x) {

@@ -89,6 +89,7 @@ struct LevelBatch {
   bool on2d = false, l1op = false;
   bool on3d = false;  // on-chip 3D PCG (pcg3d.cu), levels >= 2
   bool coarse = false;  // two-level preconditioner at level 1 (generic k_pcg or k_pcg2d level-1 variant)
+  bool crs2d = false;   // the on-chip 2D variant was planned with the coarse space (shared memory, TMEM)
   bool tsplit = false;  // 3D transport through k_pcg3d_l1<MODE 1> (fine windows <= 49 nodes per side)
   int nxm3 = 0;
   int variant = -1, threads2 = 0, maxseg = 0, tm_cols = 32;
@@ -451,7 +452,9 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       for (int v : cands) {
         int rpt, nxm, maxw, l1op, sstc, smlr;
         pcg2d_variant(v, &rpt, &nxm, &maxw, &l1op, &sstc, &smlr);
-        const bool crs_v = c->coarse && ((level == 1 && v == PCG2D_V_L1) || (level == 2 && v == PCG2D_V_GN49));
+        // the coarse-space variant where it is used and fits, else the same variant without it
+        bool crs_v = c->coarse && ((level == 1 && v == PCG2D_V_L1) || (level == 2 && v == PCG2D_V_GN49));
+        if (crs_v && pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0, true) > 232448) crs_v = false;
         if (maxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0, crs_v) > 232448) continue;
         std::vector<int> nsegs(nmp);
         std::vector<std::vector<short4>> per(nmp);
@@ -480,6 +483,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
         B->variant = v;
         B->l1op = l1op != 0;
         B->on2d = true;
+        B->crs2d = crs_v;
         break;
       }
     }
@@ -536,8 +540,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     // iterations (config 2: 245 -> 106 iterations but 15 -> 45 ms)
     // level 1 everywhere; level 2 on the 49-node on-chip variant, whose shared memory holds the
     // coarse data (with it in L2 the fixed per-iteration cost outweighed the saved iterations)
-    B->coarse = c->coarse && c->band == 0 &&
-                ((level == 1 && (!B->on2d || B->variant == PCG2D_V_L1)) || (level == 2 && B->on2d && B->variant == PCG2D_V_GN49));
+    B->coarse = c->coarse && c->band == 0 && (B->on2d ? B->crs2d : level == 1);
     if (B->coarse) {
       if (B->on2d && B->variant == PCG2D_V_L1) CKC(c, c->R.ensure(sizeof(double) * B->vec_off));  // r mirror (L2)
       CKC(c, c->cmap.ensure(sizeof(int) * B->node_off));
