@@ -540,7 +540,10 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     // iterations (config 2: 245 -> 106 iterations but 15 -> 45 ms)
     // level 1 everywhere; level 2 on the 49-node on-chip variant, whose shared memory holds the
     // coarse data (with it in L2 the fixed per-iteration cost outweighed the saved iterations)
-    B->coarse = c->coarse && c->band == 0 && (B->on2d ? B->crs2d : level == 1);
+    // 3D: level 1 and the 25-node level-2 windows (the 13- and 7-node windows of deeper levels
+    // showed no iteration change)
+    B->coarse = c->coarse && c->band == 0 &&
+                (B->on2d ? B->crs2d : (level == 1 || (B->on3d && B->nxm3 == 25)));
     if (B->coarse) {
       if (B->on2d && B->variant == PCG2D_V_L1) CKC(c, c->R.ensure(sizeof(double) * B->vec_off));  // r mirror (L2)
       CKC(c, c->cmap.ensure(sizeof(int) * B->node_off));

@@ -151,11 +151,13 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
   double* bins = p_s + (NXM + 2) * PZ;  // [NXM rows][NQ]
   double* Ysh = bins + NXM * NQ;        // [NQ] yhat
   double* csh = Ysh + NQ;               // [NQ] c
-  double* slots = csh + NQ;             // [4][32] scalar partial sums
-  int* zsm = reinterpret_cast<int*>(slots + 4 * 32);  // [NXM][3] z sides (pm, k0, k1)
+  double* slots = csh + NQ;             // [5][32] scalar partial sums
+  double* zr = slots + 5 * 32;          // [256] coarse: E^-1 Z^T r
+  double* vv = zr + 256;                // [256] coarse: coarse part of z
+  int* zsm = reinterpret_cast<int*>(vv + 256);  // [NXM][3] z sides (pm, k0, k1)
 
   for (int i = threadIdx.x; i < (NXM + 2) * PZ; i += blockDim.x) p_s[i] = 0.0;
-  for (int i = threadIdx.x; i < NXM * NQ + 2 * NQ + 4 * 32; i += blockDim.x) bins[i] = 0.0;
+  for (int i = threadIdx.x; i < NXM * NQ + 2 * NQ + 5 * 32; i += blockDim.x) bins[i] = 0.0;
   for (int z = threadIdx.x; z < nz; z += blockDim.x) {
     const Sides s = sides_of(A, P, 2, z, nz - 1);
     zsm[z * 3] = s.pm;
@@ -366,17 +368,69 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
     if (lane == 0) slots[3 * 32 + warp] = cyw;
   };
 
+  // two-level preconditioner, as in k_pcg3d_l1
+  const bool crs = A.coarse && A.ncomp[mp] > 0;
+  const int nca = crs ? A.ncomp[mp] : 0;
+  const int* cmp = A.cmap + P.node_off;
+  const int* cpt = A.cptr + (int64_t)mp * (A.ncmax + 1);
+  const int* cls = A.clist + P.node_off;
+  const double* Eiv = A.Einv + (int64_t)mp * A.ncmax;
+  const double* CZm = A.CZ + (int64_t)mp * nc * A.ncmax;
+  auto coarse_c = [&]() {  // zr, slot 4, csh += (CZ) zr; two barriers
+    double part = 0.0;
+    const int sub = lane & 3, ngrp = blockDim.x >> 2;
+    for (int a0 = threadIdx.x >> 2; a0 - (int)(threadIdx.x >> 2) < nca; a0 += ngrp) {
+      const int a = a0;
+      double sv = 0.0;
+      if (a < nca) {
+        const int i0 = __ldg(cpt + a), i1 = __ldg(cpt + a + 1);
+        for (int i = i0 + sub; i < i1; i += 4) sv += __ldcg(Rv + __ldg(cls + i));
+      }
+      sv += __shfl_xor_sync(FULLMASK, sv, 1);
+      sv += __shfl_xor_sync(FULLMASK, sv, 2);
+      if (a < nca && sub == 0) {
+        const double ei = __ldg(Eiv + a);
+        zr[a] = sv * ei;
+        part += sv * sv * ei;
+      }
+    }
+    part = wsum0(part);
+    if (lane == 0) slots[4 * 32 + warp] = part;
+    __syncthreads();
+    for (int t = warp; t < nc; t += NW) {
+      double sv = 0.0;
+      for (int a = lane; a < nca; a += 32) sv += __ldg(CZm + (int64_t)t * A.ncmax + a) * zr[a];
+      sv = wsum0(sv);
+      if (lane == 0) csh[t] += sv;
+    }
+    __syncthreads();
+  };
+  auto coarse_v = [&](double s0) {  // vv = s0 zr - E^-1 (CZ)^T Ysh; one barrier
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) {
+      double acc = 0.0;
+      for (int t = 0; t < nc; t++) acc += __ldg(CZm + (int64_t)t * A.ncmax + a) * Ysh[t];
+      vv[a] = (s0 != 0.0 ? s0 * zr[a] : 0.0) - __ldg(Eiv + a) * acc;
+    }
+    __syncthreads();
+  };
+  auto cz_at = [&](int k) -> double {
+    if (!crs) return 0.0;
+    const int a = __ldg(cmp + k);
+    return (a >= 0) ? vv[a] : 0.0;
+  };
+
   // ---- init: x0 = D^-1 C^T S^-1 t, r0 = A x0 - b, c = C D^-1 r0, yhat = S^-1 c; returns r0^T D^-1 r0
   auto init = [&](const double* tcol, const double* bb) -> double {
     for (int i = threadIdx.x; i < nc; i += blockDim.x) csh[i] = tcol[((int64_t)mp * nc + i) * A.n_rhs + rhs];
     __syncthreads();
     solve_y();
     __syncthreads();
+    if (crs) coarse_v(0.0);
     rows([&] {
       if (lact)
         for (int z = 0; z < nz; z++) {
           const int k = nidx(z);
-          const double x0 = dg[k] * ct_at(z, k);
+          const double x0 = dg[k] * ct_at(z, k) - cz_at(k);
           p_s[pidx(z)] = x0;
           Xv[k] = x0;
         }
@@ -403,9 +457,12 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
     __syncthreads();
     reduce_c();
     __syncthreads();
+    if (crs) coarse_c();
     solve_y();
     __syncthreads();
-    return slot_fin(2);
+    const double rrt = slot_fin(2) + (crs ? slot_fin(4) : 0.0);
+    if (crs) coarse_v(1.0);
+    return rrt;
   };
 
   // reference scale: initial projected residual of the full (non-hierarchical) problem
@@ -441,7 +498,7 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
       for (int z = 0; z < nz; z++) {
         const int k = nidx(z);
         const double rk = Rv[k] - ct_at(z, k);
-        const double zz = dg[k] * rk;
+        const double zz = dg[k] * rk + cz_at(k);
         double& pk = p_s[pidx(z)];
         const double pold = pk;
         if (!first) Xv[k] += alpha * pold;
@@ -491,10 +548,12 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
     __syncthreads();  // B3
     reduce_c();
     __syncthreads();  // B3b
+    if (crs) coarse_c();
     solve_y();
     __syncthreads();  // B4
     const double cy = slot_fin(3);
-    beta = (slot_fin(2) - cy) / rz;
+    beta = (slot_fin(2) + (crs ? slot_fin(4) : 0.0) - cy) / rz;
+    if (crs) coarse_v(1.0);
   }
 
   // feasibility restoration: x += D^-1 C^T S^-1 (g - C x)
@@ -510,11 +569,12 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
   __syncthreads();
   solve_y();
   __syncthreads();
+  if (crs) coarse_v(0.0);
   rows([&] {
     if (lact)
       for (int z = 0; z < nz; z++) {
         const int k = nidx(z);
-        Xv[k] += dg[k] * ct_at(z, k);
+        Xv[k] += dg[k] * ct_at(z, k) - cz_at(k);
       }
   });
   if (threadIdx.x == 0) {
@@ -1114,7 +1174,7 @@ cudaError_t launch_tapply3d(const LevelArgs& A, cudaStream_t st) {
 
 // ------------------------------------------------------------------------------------------
 size_t pcg3d_smem(int N, int nxm) {
-  const size_t d = (size_t)(nxm + 2) * (nxm + 2) * nxm + (size_t)nxm * 27 * N + 2 * 27 * N + 4 * 32;
+  const size_t d = (size_t)(nxm + 2) * (nxm + 2) * nxm + (size_t)nxm * 27 * N + 2 * 27 * N + 5 * 32 + 512;
   return d * sizeof(double) + (size_t)nxm * 3 * sizeof(int);
 }
 
