@@ -682,6 +682,76 @@ __global__ void k_coarse_setup(LevelArgs A) {
     if (threadIdx.x == 0) Ei[a] = (red[48] > 0.0) ? 1.0 / red[48] : 0.0;
     __syncthreads();
   }
+  // (A z_a) lists for the recurrence Z^T r_{k+1} = Z^T r~_k + alpha (A Z)^T p_k of the on-chip 2D
+  // kernels: thread per component over its bounding box grown by one node, nonzeros in node
+  // order; a window whose lists exceed kAzCap entries per node runs without the coarse space
+  if (A.azp != nullptr && D == 2) {
+    int* ap = A.azp + (int64_t)mp * (A.ncmax + 1);
+    int* ai = A.azi + (int64_t)kAzCap * P.node_off;
+    double* aw = A.azw + (int64_t)kAzCap * P.node_off;
+    auto azval = [&](int a, const int* x) -> double {  // (A z_a) at node x
+      double az = 0.0;
+      for (int o = 0; o < (1 << D); o++) {
+        int e[3] = {0, 0, 0};
+        bool ok = true;
+        for (int i = 0; i < D; i++) {
+          e[i] = x[i] - 1 + ((o >> i) & 1);
+          ok = ok && e[i] >= 0 && e[i] < g.nc[i];
+        }
+        if (!ok) continue;
+        const int ac = (~o) & ((1 << D) - 1);
+        double zc[1 << D];
+        bool any = false;
+        for (int b = 0; b < (1 << D); b++) {
+          int xb[3] = {e[0] + (b & 1), e[1] + ((b >> 1) & 1), 0};
+          zc[b] = (cm[node_id<D>(g, xb)] == a) ? 1.0 : 0.0;
+          any = any || zc[b] != 0.0;
+        }
+        if (!any) continue;
+        double W[DimC<D>::NW];
+        elem_W<D>(A, P, g, e, W);
+        az += elem_row<D>(W, zc, ac);
+      }
+      return az;
+    };
+    for (int a = threadIdx.x; a < ncomp; a += blockDim.x) {
+      const int* bx = box + a * 6;
+      int c = 0;
+      for (int y = max(bx[1] - 1, 0); y <= min(bx[4] + 1, g.nn[1] - 1); y++)
+        for (int x = max(bx[0] - 1, 0); x <= min(bx[3] + 1, g.nn[0] - 1); x++) {
+          const int xx[3] = {x, y, 0};
+          c += (azval(a, xx) != 0.0);
+        }
+      ap[a + 1] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ap[0] = 0;
+      for (int a = 0; a < ncomp; a++) ap[a + 1] += ap[a];
+      if (ap[ncomp] > kAzCap * nn) total = -1;  // overflow: no coarse space for this window
+    }
+    __syncthreads();
+    if (total < 0) {
+      for (int k = threadIdx.x; k < nn; k += blockDim.x) cm[k] = -1;
+      if (threadIdx.x == 0) A.ncomp[mp] = 0;
+      return;
+    }
+    for (int a = threadIdx.x; a < ncomp; a += blockDim.x) {
+      const int* bx = box + a * 6;
+      int o = ap[a];
+      for (int y = max(bx[1] - 1, 0); y <= min(bx[4] + 1, g.nn[1] - 1); y++)
+        for (int x = max(bx[0] - 1, 0); x <= min(bx[3] + 1, g.nn[0] - 1); x++) {
+          const int xx[3] = {x, y, 0};
+          const double w = azval(a, xx);
+          if (w != 0.0) {
+            ai[o] = x | (y << 16);
+            aw[o] = w;
+            o++;
+          }
+        }
+    }
+    __syncthreads();
+  }
   // C z_a: thread per component over the cells touching it (its bounding box grown by one cell
   // on the lower sides), contributions m_{E,j,a} = [id_E = j] h^D / 2^D per corner in the
   // component, accumulated per constraint row in cell order (fixed order)

@@ -137,12 +137,13 @@ struct mch_ctx {
   DevBuf fsrc, bload, mws, mG, mb, mU, mres;
   DevBuf fws, fbar, ff, fu, fkbox, fout;  // NEXT-3 fine solve / block averages
   DevBuf cmap, ncomp, cbox, einv, cz, cptr, clist;  // two-level preconditioner (level 1)
+  DevBuf azp, azi, azw;                               // (A z_a) lists of the 2D on-chip kernels
   bool coarse = false;
   DevAlloc al;
   std::vector<DevBuf*> bufs() {
     return {&STC, &MLR, &pinv_ds, &W, &Mc, &g0, &g, &meas, &cm, &flags, &dinv, &nwt, &Sinv, &X, &R, &P, &Q, &B,
             &FI, &FY, &iters, &relres, &diag, &fsrc, &bload, &mws, &mG, &mb, &mU, &mres, &fws, &fbar, &ff, &fu,
-            &fkbox, &fout, &cmap, &ncomp, &cbox, &einv, &cz, &cptr, &clist};
+            &fkbox, &fout, &cmap, &ncomp, &cbox, &einv, &cz, &cptr, &clist, &azp, &azi, &azw};
   }
   bool has_source = false;
   int* h_mit = nullptr;
@@ -553,6 +554,11 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       CKC(c, c->cz.ensure(sizeof(double) * kCoarseMax * (size_t)nmp * nc));
       CKC(c, c->cptr.ensure(sizeof(int) * (kCoarseMax + 1) * (size_t)nmp));
       CKC(c, c->clist.ensure(sizeof(int) * B->node_off));
+      if (B->on2d) {
+        CKC(c, c->azp.ensure(sizeof(int) * (kCoarseMax + 1) * (size_t)nmp));
+        CKC(c, c->azi.ensure(sizeof(int) * kAzCap * B->node_off));
+        CKC(c, c->azw.ensure(sizeof(double) * kAzCap * B->node_off));
+      }
     }
     if (B->on3d && level >= 2) {
       CKC(c, c->STC.ensure(sizeof(double) * 27 * B->node_off));
@@ -648,6 +654,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     A.cmap = c->cmap.as<int>(); A.ncomp = c->ncomp.as<int>(); A.cbox = c->cbox.as<int>();
     A.Einv = c->einv.as<double>(); A.CZ = c->cz.as<double>();
     A.cptr = c->cptr.as<int>(); A.clist = c->clist.as<int>();
+    A.azp = (B.coarse && B.on2d) ? c->azp.as<int>() : nullptr;
+    A.azi = c->azi.as<int>(); A.azw = c->azw.as<double>();
     if (A.coarse) {
       CKC(c, launch_coarse_setup(A, st));
       S.launches += 1;

@@ -4,6 +4,7 @@
 #include <vector_types.h>
 
 #define MCH_MAXPAR 8  // 2^d parents at most (d-linear interpolation, Eq. 11)
+constexpr int kAzCap = 4;  // (A z_a) list entries per window node (two-level preconditioner, 2D)
 
 // One macropoint solved at its level (device-visible POD).
 struct ProbDesc {
@@ -71,6 +72,9 @@ struct LevelArgs {
   double* CZ;              // [mp][ncon][ncmax] C z_a
   int* cptr;               // [mp][ncmax+1] start of each component's node list in clist
   int* clist;              // [nodes] node indices of each component, in node order (node_off based)
+  int* azp;                // [mp][ncmax+1] start of each component's (A z_a) list (2D on-chip kernels)
+  int* azi;                // [kAzCap * nodes] node of each entry, packed x | y << 16
+  double* azw;             // [kAzCap * nodes] (A z_a) at that node
   int tphase;              // k_transport: 0 all phases; 1 only I_p; 2 only the restriction (3D split path)
   const double* f;         // NEXT-2: cellwise source, n^D, x fastest (NULL: no load vectors)
   double* bload;           // NEXT-2: [P][N] load vectors b_j = int_{K_p} f phi_j (Eq. 7)

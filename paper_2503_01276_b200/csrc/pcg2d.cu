@@ -623,6 +623,9 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   const int* cmp = A.cmap + P.node_off;
   const int* cpt = A.cptr + (int64_t)mp * (A.ncmax + 1);
   const int* cls = A.clist + P.node_off;
+  const int* azp = A.azp + (int64_t)mp * (A.ncmax + 1);
+  const int* azi = A.azi + (int64_t)kAzCap * P.node_off;
+  const double* azw = A.azw + (int64_t)kAzCap * P.node_off;
   const double* Eiv = A.Einv + (int64_t)mp * A.ncmax;
   const double* CZm = A.CZ + (int64_t)mp * nc * A.ncmax;
   double* Rg = A.R + P.vec_off + (int64_t)rhs * nn;
@@ -646,14 +649,59 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
     __syncthreads();
   }
   const int nwarps = blockDim.x >> 5;
+  // csum = (CZ) E^-1 s (s = Z^T r in zr).  One barrier.
+  auto coarse_csum = [&]() {
+    for (int t = warp; t < nc; t += nwarps) {
+      double sv = 0.0;
+      for (int a = lane; a < nca; a += 32)
+        sv += (CSM ? czs[t * kCrsMax + a] : __ldg(CZm + (int64_t)t * A.ncmax + a)) *
+              (CSM ? eis[a] : __ldg(Eiv + a)) * zr[a];
+      sv = warp_sum0(sv);
+      if (lane == 0) csum[t] = sv;
+    }
+    __syncthreads();
+  };
+  // recurrence (after B3): s += alpha (A Z)^T p (the latter in vv, formed in pass B), slot 3 =
+  // s^T E^-1 s, then csum.  Two barriers.
+  auto coarse_rec = [&](double alpha_) {
+    double part = 0.0;
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) {
+      const double sv = zr[a] + alpha_ * vv[a];
+      zr[a] = sv;
+      part += sv * sv * (CSM ? eis[a] : __ldg(Eiv + a));
+    }
+    part = warp_sum0(part);
+    if (lane == 0) slots[3 * 32 + warp] = part;
+    __syncthreads();
+    coarse_csum();
+  };
+  // (A Z)^T p from p_s (after B1) into vv: 4-lane groups over each component's (A z_a) list
+  auto coarse_zq = [&]() {
+    const int sub = lane & 3, ngrp = blockDim.x >> 2;
+    for (int base = 0; base < nca; base += ngrp) {  // warp-uniform trip count
+      const int a = base + (threadIdx.x >> 2);
+      double sv = 0.0;
+      if (a < nca) {
+        const int i0 = __ldg(azp + a), i1 = __ldg(azp + a + 1);
+#pragma unroll 4
+        for (int i = i0 + sub; i < i1; i += 4) {
+          const int xy = __ldg(azi + i);
+          sv += __ldg(azw + i) * p_s[((xy >> 16) + 1) * PX + (xy & 0xFFFF) + 1];
+        }
+      }
+      sv += __shfl_xor_sync(FULLMASK, sv, 1);
+      sv += __shfl_xor_sync(FULLMASK, sv, 2);
+      if (a < nca && sub == 0) vv[a] = sv;
+    }
+  };
   // zr = E^-1 Z^T Rg, slot 3 = (Z^T r)^T E^-1 (Z^T r); then csum = (CZ) zr.  Two barriers.
   auto coarse_c = [&]() {
     double part = 0.0;
     // groups of 4 lanes per component, each lane a strided quarter of its node list, combined by
     // two xor shuffles (fixed order); rounds over the components are uniform per warp
     const int sub = lane & 3, ngrp = blockDim.x >> 2;
-    for (int a0 = threadIdx.x >> 2; a0 - (int)(threadIdx.x >> 2) < nca; a0 += ngrp) {
-      const int a = a0;
+    for (int base = 0; base < nca; base += ngrp) {  // warp-uniform trip count
+      const int a = base + (threadIdx.x >> 2);
       double sv = 0.0;
       if (a < nca) {
         if (CSM) {
@@ -669,28 +717,30 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
       sv += __shfl_xor_sync(FULLMASK, sv, 2);
       if (a < nca && sub == 0) {
         const double ei = CSM ? eis[a] : __ldg(Eiv + a);
-        zr[a] = sv * ei;
+        zr[a] = sv;  // s_a = (Z^T r)_a, carried by the recurrence from here on
         part += sv * sv * ei;
       }
     }
     part = warp_sum0(part);
     if (lane == 0) slots[3 * 32 + warp] = part;
     __syncthreads();
-    for (int t = warp; t < nc; t += nwarps) {
-      double sv = 0.0;
-      for (int a = lane; a < nca; a += 32)
-        sv += (CSM ? czs[t * kCrsMax + a] : __ldg(CZm + (int64_t)t * A.ncmax + a)) * zr[a];
-      sv = warp_sum0(sv);
-      if (lane == 0) csum[t] = sv;
-    }
-    __syncthreads();
+    coarse_csum();
   };
   // vv = s0 zr - E^-1 (CZ)^T Ysh (s0 = 0: minus the coarse part of M^-1 C^T yhat).  One barrier.
+  // s0 != 0: vv = E^-1 (s - (CZ)^T yhat) (coarse part of z = M^-1 r~) and s <- s - (CZ)^T yhat
+  // (= Z^T r~); s0 == 0: vv = -E^-1 (CZ)^T yhat (minus the coarse part of M^-1 C^T yhat), s kept
   auto coarse_v = [&](double s0) {
     for (int a = threadIdx.x; a < nca; a += blockDim.x) {
       double acc = 0.0;
       for (int t = 0; t < nc; t++) acc += (CSM ? czs[t * kCrsMax + a] : __ldg(CZm + (int64_t)t * A.ncmax + a)) * Ysh[t];
-      vv[a] = (s0 != 0.0 ? s0 * zr[a] : 0.0) - (CSM ? eis[a] : __ldg(Eiv + a)) * acc;
+      const double ei = CSM ? eis[a] : __ldg(Eiv + a);
+      if (s0 != 0.0) {
+        const double sr = zr[a] - acc;
+        vv[a] = ei * sr;
+        zr[a] = sr;
+      } else {
+        vv[a] = -ei * acc;
+      }
     }
     __syncthreads();
   };
@@ -885,6 +935,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
       });
       gflush(tmq);
     }
+    if (CRS && crs) coarse_zq();
     TMARK(2);
     slot_put(1, w);
     __syncthreads();  // B2
@@ -909,8 +960,6 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
         if (g >= nrow) break;
         uint32_t qa[8];
         tm_ld8(tmq + 2 * g, qa);
-        uint32_t cw4 = 0xFFFFFFFFu;
-        if (CRS && crs) cw4 = tm_ld1(tmc + g / 4);
         tm_wait_ld();
 #pragma unroll
         for (int u = 0; u < 4; u++) {
@@ -924,10 +973,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
             double mL[N], mR[N], lL[N], lR[N];
             cw.row(i == 0 && syp >= 0, mL, mR, lL, lR);
             acc_row(i, uu, mL, mR, lL, lR);
-            if (CRS && crs && lact && ((cw4 >> (8 * u)) & 255u) != 255u) {  // component nodes
-              if (CSM) rsm[y * nx + x] = rk;
-              else Rg[y * nx + x] = rk;
-            }
+
           }
         }
       }
@@ -940,7 +986,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
 #ifdef PCG2D_TIMING
     unsigned long long tc0 = clock64();
 #endif
-    if (crs) coarse_c();
+    if (crs) coarse_rec(alpha);
 #ifdef PCG2D_TIMING
     unsigned long long tc1 = clock64();
 #endif
