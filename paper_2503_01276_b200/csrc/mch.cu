@@ -554,7 +554,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       CKC(c, c->cz.ensure(sizeof(double) * kCoarseMax * (size_t)nmp * nc));
       CKC(c, c->cptr.ensure(sizeof(int) * (kCoarseMax + 1) * (size_t)nmp));
       CKC(c, c->clist.ensure(sizeof(int) * B->node_off));
-      if (B->on2d) {
+      if (B->on2d && B->variant == PCG2D_V_L1) {
         CKC(c, c->azp.ensure(sizeof(int) * (kCoarseMax + 1) * (size_t)nmp));
         CKC(c, c->azi.ensure(sizeof(int) * kAzCap * B->node_off));
         CKC(c, c->azw.ensure(sizeof(double) * kAzCap * B->node_off));
@@ -654,7 +654,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     A.cmap = c->cmap.as<int>(); A.ncomp = c->ncomp.as<int>(); A.cbox = c->cbox.as<int>();
     A.Einv = c->einv.as<double>(); A.CZ = c->cz.as<double>();
     A.cptr = c->cptr.as<int>(); A.clist = c->clist.as<int>();
-    A.azp = (B.coarse && B.on2d) ? c->azp.as<int>() : nullptr;
+    A.azp = (B.coarse && B.on2d && B.variant == PCG2D_V_L1) ? c->azp.as<int>() : nullptr;
     A.azi = c->azi.as<int>(); A.azw = c->azw.as<double>();
     if (A.coarse) {
       CKC(c, launch_coarse_setup(A, st));

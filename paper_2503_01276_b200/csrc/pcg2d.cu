@@ -315,6 +315,9 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   // CSM (coarse data resident in shared memory; the precomputed-operator variants have room):
   // r mirror, CZ, E^-1 and the component node lists (ints)
   constexpr bool CSM = CRS && !L1OP;
+  // level 1: Z^T r by the recurrence over (A z_a) lists; 49-node windows (r mirror in shared
+  // memory): direct component sums every iteration
+  constexpr bool REC = CRS && L1OP;
   constexpr int O_RS = O_CS + (CRS ? 32 : 0);
   constexpr int O_CZ = O_RS + (CSM ? PLANE : 0);
   constexpr int O_EI = O_CZ + (CSM ? NCM * kCrsMax : 0);
@@ -935,7 +938,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
       });
       gflush(tmq);
     }
-    if (CRS && crs) coarse_zq();
+    if (REC && crs) coarse_zq();
     TMARK(2);
     slot_put(1, w);
     __syncthreads();  // B2
@@ -960,6 +963,8 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
         if (g >= nrow) break;
         uint32_t qa[8];
         tm_ld8(tmq + 2 * g, qa);
+        uint32_t cw4 = 0xFFFFFFFFu;
+        if (CSM && crs) cw4 = tm_ld1(tmc + g / 4);
         tm_wait_ld();
 #pragma unroll
         for (int u = 0; u < 4; u++) {
@@ -973,7 +978,7 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
             double mL[N], mR[N], lL[N], lR[N];
             cw.row(i == 0 && syp >= 0, mL, mR, lL, lR);
             acc_row(i, uu, mL, mR, lL, lR);
-
+            if (CSM && crs && lact && ((cw4 >> (8 * u)) & 255u) != 255u) rsm[y * nx + x] = rk;
           }
         }
       }
@@ -986,7 +991,8 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
 #ifdef PCG2D_TIMING
     unsigned long long tc0 = clock64();
 #endif
-    if (crs) coarse_rec(alpha);
+    if (REC && crs) coarse_rec(alpha);
+    else if (crs) coarse_c();
 #ifdef PCG2D_TIMING
     unsigned long long tc1 = clock64();
 #endif
