@@ -209,12 +209,14 @@ def main():
     ms_step = float(t.item())
     value = n_cell / (ms_step * 1e-3)
 
-    # dominant kernel launch: the level-1 k_pcg launch (one launch per level and batch; level 1 is
-    # the largest share of the step, see profiles/r01_launches_c2.csv).  achieved = algorithmic
-    # bytes of that launch / its device time (CUDA events on the library stream, mean over steps).
+    # dominant kernel launch: the PCG launch of the level with the largest PCG device time (one
+    # launch per level and batch; config 2: level 2 since the level-1 Z^T r recurrence, see
+    # profiles/r01_launches_c2_final.csv).  achieved = algorithmic bytes of that launch / its device
+    # time (CUDA events on the library stream, mean over steps).
     pk, pk_src = _peaks()
-    l1_b = sum(st_[0]["pcg_bytes"] for st_ in levels) / len(levels)
-    l1_ms = sum(st_[0]["ms_pcg"] for st_ in levels) / len(levels)
+    lev = max(range(cfg.L), key=lambda l: sum(st_[l]["ms_pcg"] for st_ in levels))
+    l1_b = sum(st_[lev]["pcg_bytes"] for st_ in levels) / len(levels)
+    l1_ms = sum(st_[lev]["ms_pcg"] for st_ in levels) / len(levels)
     achieved = l1_b / (l1_ms * 1e-3) / 1e9
     all_b = sum(s["pcg_bytes"] for st_ in levels for s in st_) / len(levels)
     all_ms = sum(s["ms_pcg"] for st_ in levels for s in st_) / len(levels)
@@ -222,9 +224,11 @@ def main():
     prof = os.path.join(ROOT, "profiles", "pcg_dram_per_launch_r01.json")  # ncu, same launch
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(cfg.name, {}).get("dram_bytes_pcg_L1_launch")
+            traffic = json.load(open(prof)).get(cfg.name, {}).get(f"dram_bytes_pcg_L{lev + 1}_launch")
         except Exception:
             traffic = None
+    kname = ("k_pcg2d" if cfg.d == 2 else ("k_pcg3d_l1" if lev == 0 else "k_pcg3d")) + \
+        f" level-{lev + 1} launch (on-chip projected PCG)"
     per_level = []
     for l in range(cfg.L):
         s = levels[-1][l]
@@ -271,7 +275,7 @@ def main():
                    "l2": "flushed between timed steps (512 MB write)",
                    "macropoint_solves_per_s": (cfg.M + 1) ** cfg.d / (ms_step * 1e-3),
                    "per_level": per_level},
-        "roofline": {"kernel": "k_pcg2d level-1 launch (on-chip projected PCG)", "bound": "hbm",
+        "roofline": {"kernel": kname, "bound": "hbm",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "algorithmic_bytes_per_launch": l1_b, "launch_ms": l1_ms,

@@ -618,9 +618,10 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
   };
   auto slot_fin = [&](int which) { return warp_sum0((lane < MAXW) ? slots[which * 32 + lane] : 0.0); };
 
-  // ---- two-level preconditioner M^-1 = D^-1 + Z E^-1 Z^T (level 1): r is mirrored
-  //      to global memory in pass C and summed per component there (one warp per component over
-  //      its bounding box, fixed order); the projection uses S_M = C M^-1 C^T (k_proj_setup) ----
+  // ---- two-level preconditioner M^-1 = D^-1 + Z E^-1 Z^T: s = Z^T r summed per
+  //      component from a mirror of r (start; every iteration in the 49-node windows) or carried
+  //      by the recurrence over the (A z_a) lists (level 1); the projection uses S_M = C M^-1 C^T
+  //      (k_proj_setup) ----
   const bool crs = CRS && A.ncomp[mp] > 0;
   const int nca = crs ? A.ncomp[mp] : 0;
   const int* cmp = A.cmap + P.node_off;
