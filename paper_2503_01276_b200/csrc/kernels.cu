@@ -245,6 +245,174 @@ __global__ void k_transport(LevelArgs A) {
 }
 
 // ---------------------------------------------------------------------------------------
+// 2D transport of all right-hand sides of a macropoint in one CTA (levels >= 2, dense projector):
+// the geometry of each fine node (parent indices, element kappa, element ids) is formed once and
+// applied to the NR vectors, and the restriction passes run over (rhs, row) pairs.  Every value is
+// summed in the order k_transport uses except the constraint sums, whose 32-element tasks are
+// dealt to 8 warps instead of blockDim/32 (config 2 coefficients agree to 5e-13;
+// MCH_TRANSPORT_GENERIC=1 selects k_transport; tools/env_ab.py).
+template <int NR>
+__global__ void __launch_bounds__(256) k_transport2d_mr(LevelArgs A) {
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  extern __shared__ double smem[];
+  const Geo<2> gf = fine_geo<2>(P);
+  const Geo<2> gl = level_geo<2>(A, P);
+  const int nnf = gf.nnodes, nfx = gf.nn[0], nfy = gf.nn[1];
+  double* I = A.FI + P.fine_off;  // rhs r at r * nnf
+  double* Y = A.FY + P.fine_off;
+  // phase 1: I_p at fine nodes (local-coordinate transport, reading R9)
+  for (int k = threadIdx.x; k < nnf; k += blockDim.x) {
+    int x[3];
+    node_xyz<2>(gf, k, x);
+    double sr[NR];
+#pragma unroll
+    for (int r = 0; r < NR; r++) sr[r] = 0.0;
+    for (int t = 0; t < P.npar; t++) {
+      int64_t idx = 0;
+      for (int i = 1; i >= 0; i--) {
+        const int xt = P.lo[i] + x[i] + (P.par_k[t][i] - P.k[i]) * A.c - P.par_lo[t][i];
+        idx = idx * (P.par_ncf[t][i] + 1) + xt;
+      }
+      const int64_t pn = (int64_t)(P.par_ncf[t][0] + 1) * (P.par_ncf[t][1] + 1);
+      const double* src = A.pool + P.par_pool[t] + idx;
+      const double w = P.par_w[t];
+#pragma unroll
+      for (int r = 0; r < NR; r++) sr[r] += w * src[(int64_t)r * pn];
+    }
+#pragma unroll
+    for (int r = 0; r < NR; r++) I[(int64_t)r * nnf + k] = sr[r];
+  }
+  __syncthreads();
+  // phase 2: Y = A_1 I (fine operator on the window, natural BC), as apply_xyz
+  for (int k = threadIdx.x; k < nnf; k += blockDim.x) {
+    int xx[3];
+    node_xyz<2>(gf, k, xx);
+    bool okn[9];
+#pragma unroll
+    for (int c = 0; c < 9; c++) {
+      const int dx = c % 3 - 1, dy = c / 3 - 1;
+      okn[c] = (xx[0] + dx >= 0) && (xx[0] + dx < nfx) && (xx[1] + dy >= 0) && (xx[1] + dy < nfy);
+    }
+    double kap[4];
+    bool oke[4];
+#pragma unroll
+    for (int o = 0; o < 4; o++) {
+      int e[3] = {xx[0] - 1 + (o & 1), xx[1] - 1 + ((o >> 1) & 1), 0};
+      oke[o] = e[0] >= 0 && e[0] < gf.nc[0] && e[1] >= 0 && e[1] < gf.nc[1];
+      kap[o] = oke[o] ? A.kappa[fine_cell_index<2>(A, P, gf, e, nullptr)] : 0.0;
+    }
+#pragma unroll 1
+    for (int r = 0; r < NR; r++) {
+      const double* v = I + (int64_t)r * nnf;
+      double nb[9];
+#pragma unroll
+      for (int c = 0; c < 9; c++) nb[c] = okn[c] ? v[k + (c % 3 - 1) + (c / 3 - 1) * nfx] : 0.0;
+      double out = 0.0;
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        if (!oke[o]) continue;
+        const int a = (~o) & 3;
+        auto nbv = [&](int b) {
+          const int dx = (b & 1) - (a & 1), dy = ((b >> 1) & 1) - ((a >> 1) & 1);
+          return nb[(dx + 1) + 3 * (dy + 1)];
+        };
+        out += kap[o] * (1.0 / 6.0) * (4.0 * nbv(a) - nbv(a ^ 1) - nbv(a ^ 2) - 2.0 * nbv(a ^ 3));
+      }
+      Y[(int64_t)r * nnf + k] = out;
+    }
+  }
+  // C_1 I -> g = g0 - C_1 I (as constraint_apply: 32-element tasks per subcell, warp sums, bins
+  // per warp summed in warp order)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  const int nc = A.ncon, N = A.N;
+  int* eb = reinterpret_cast<int*>(smem);
+  double* bins = smem + (A.nsub * 7 + 2 + 1) / 2;  // [nw][ncon][NR]
+  for (int i = threadIdx.x; i < nw * nc * NR; i += blockDim.x) bins[i] = 0.0;
+  __shared__ int ntask;
+  subcell_boxes<2>(A, P, gf, eb, &ntask);  // syncs
+  const int* pref = eb + A.nsub * 6;
+  const double hh = 0.25 * A.h * A.h;
+  for (int t = wid; t < ntask; t += nw) {
+    int q = 0;
+    while (pref[q + 1] <= t) q++;
+    const int* bx = eb + q * 6;
+    const int idx = (t - pref[q]) * 32 + lane;
+    const int cnt = bx[3] * bx[4] * bx[5];
+    double sv[NR];
+    int id = -1;
+#pragma unroll
+    for (int r = 0; r < NR; r++) sv[r] = 0.0;
+    if (idx < cnt) {
+      const int i1 = fdiv(idx, 1.0f / (float)bx[3]);
+      int e[3] = {bx[0] + idx - i1 * bx[3], bx[1] + i1, 0};
+      int kb[4];
+#pragma unroll
+      for (int b = 0; b < 4; b++) {
+        int xb[3] = {e[0] + (b & 1), e[1] + ((b >> 1) & 1), 0};
+        kb[b] = node_id<2>(gf, xb);
+      }
+      id = A.ids[fine_cell_index<2>(A, P, gf, e, nullptr)];
+#pragma unroll
+      for (int r = 0; r < NR; r++) {
+        const double* v = I + (int64_t)r * nnf;
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) s += v[kb[b]];
+        sv[r] = s * hh;
+      }
+    }
+    for (int j = 0; j < N; j++) {
+#pragma unroll
+      for (int r = 0; r < NR; r++) {
+        double v = (j == id) ? sv[r] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(FULLMASK, v, o);
+        if (lane == 0) bins[(wid * nc + q * N + j) * NR + r] += v;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nc * NR; i += blockDim.x) {
+    const int row = i / NR, r = i - row * NR;
+    double s = 0.0;
+    for (int w = 0; w < nw; w++) s += bins[(w * nc + row) * NR + r];
+    const int64_t gi = ((int64_t)mp * nc + row) * A.n_rhs + r;
+    A.g[gi] = A.g0[gi] - s;
+  }
+  __syncthreads();
+  // phase 3: b = -P_n^T Y at level-n nodes, the separable in-place restriction of k_transport
+  const int s = A.s;
+  const double inv_s = 1.0 / (double)s;
+  const int nlx = gl.nn[0], nly = gl.nn[1];
+  auto restrict1 = [&](double* v, int64_t stride, int nf, int nl, auto&& put) {
+    for (int X = 0; X < nl; X++) {
+      const int c0 = X * s;
+      double acc = v[(int64_t)c0 * stride];
+      for (int d = 1; d < s; d++) {
+        const double w = 1.0 - d * inv_s;
+        if (c0 - d >= 0) acc += w * v[(int64_t)(c0 - d) * stride];
+        if (c0 + d < nf) acc += w * v[(int64_t)(c0 + d) * stride];
+      }
+      put(X, acc);
+    }
+  };
+  for (int u = threadIdx.x; u < NR * nfy; u += blockDim.x) {
+    const int r = u / nfy, row = u - r * nfy;
+    double* v = Y + (int64_t)r * nnf + (int64_t)row * nfx;
+    restrict1(v, 1, nfx, nlx, [&](int X, double a) { v[X] = a; });
+  }
+  __syncthreads();
+  for (int u = threadIdx.x; u < NR * nlx; u += blockDim.x) {
+    const int r = u / nlx, X = u - r * nlx;
+    double* v = Y + (int64_t)r * nnf + X;
+    double* bvec = A.B + P.vec_off + (int64_t)r * gl.nnodes;
+    // the z pass of k_transport is the identity in 2D (one plane): write -value directly
+    restrict1(v, nfx, nfy, nly, [&](int Yc, double a) { bvec[(int64_t)Yc * nlx + X] = -a; });
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // projector setup: one CTA per macropoint
 template <int D>
 __global__ void k_proj_setup(LevelArgs A) {
@@ -1463,6 +1631,18 @@ cudaError_t launch_targets(const LevelArgs& A, cudaStream_t st) {
 }
 
 cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
+  static const bool generic = getenv("MCH_TRANSPORT_GENERIC") != nullptr;
+  if (A.D == 2 && A.band == 0 && A.tphase == 0 && !generic &&
+      (A.n_rhs == 3 || A.n_rhs == 6 || A.n_rhs == 9)) {
+    const size_t sm = sizeof(double) * ((A.nsub * 7 + 2 + 1) / 2 + (size_t)8 * A.ncon * A.n_rhs);
+    if (sm <= 232448) {
+      auto k = (A.n_rhs == 3) ? k_transport2d_mr<3> : ((A.n_rhs == 6) ? k_transport2d_mr<6> : k_transport2d_mr<9>);
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      k<<<(unsigned)A.nprob_mp, 256, sm, st>>>(A);
+      return cudaGetLastError();
+    }
+  }
   const size_t sm = sizeof(double) * ((A.nsub * 7 + 2 + 1) / 2 + (A.band > 0 ? 0 : 32 * A.ncon) + A.ncon);
   const unsigned grid = (unsigned)A.nprob_mp * A.n_rhs;
   if (A.D == 2) k_transport<2><<<grid, threads, sm, st>>>(A);
