@@ -1631,7 +1631,7 @@ cudaError_t launch_targets(const LevelArgs& A, cudaStream_t st) {
 }
 
 cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
-  static const bool generic = getenv("MCH_TRANSPORT_GENERIC") != nullptr;
+  const bool generic = getenv("MCH_TRANSPORT_GENERIC") != nullptr;  // read per call (tests toggle it)
   if (A.D == 2 && A.band == 0 && A.tphase == 0 && !generic &&
       (A.n_rhs == 3 || A.n_rhs == 6 || A.n_rhs == 9)) {
     const size_t sm = sizeof(double) * ((A.nsub * 7 + 2 + 1) / 2 + (size_t)8 * A.ncon * A.n_rhs);

@@ -486,13 +486,15 @@ def test_coarse_space_preconditioner(monkeypatch):
         assert g_err(G1[i], G0[i]) < G_TOL, (i, g_err(G1[i], G0[i]))
 
 
-def test_transport_paths_agree(monkeypatch):
-    """3D levels >= 2: the split transport (I_p, column-walking A_1 I_p / C_1 I_p, separable
-    P_n^T) and the generic per-node k_transport (MCH_TRANSPORT_GENERIC) give the same
-    coefficients (R15 bar) and both match the oracle."""
+@pytest.mark.parametrize("d,n,M,L,N,seed", [(3, 16, 4, 2, 2, 970), (2, 64, 8, 3, 1, 41), (2, 64, 8, 3, 2, 7),
+                                             (2, 32, 4, 2, 3, 23)])
+def test_transport_paths_agree(d, n, M, L, N, seed, monkeypatch):
+    """Levels >= 2: the split transport of 3D (I_p, column-walking A_1 I_p / C_1 I_p, separable
+    P_n^T) and the multi-rhs transport of 2D (k_transport2d_mr, n_rhs = 3 / 6 / 9) give the same
+    coefficients as the generic per-(macropoint, rhs) k_transport (MCH_TRANSPORT_GENERIC), and
+    both match the oracle (R15 bar)."""
     H = _gpu()
-    d, n, M, L, N = 3, 16, 4, 2, 2
-    kap, ids = _admissible(d, n, M, N, 970)
+    kap, ids = _admissible(d, n, M, N, seed)
     o = Oracle(d, n, M, L, 2, N, kap, ids)
     Go = o.effective_coeffs()
     res = {}
