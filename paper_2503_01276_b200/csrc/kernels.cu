@@ -1632,7 +1632,13 @@ cudaError_t launch_targets(const LevelArgs& A, cudaStream_t st) {
 
 cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
   const bool generic = getenv("MCH_TRANSPORT_GENERIC") != nullptr;  // read per call (tests toggle it)
-  if (A.D == 2 && A.band == 0 && A.tphase == 0 && !generic &&
+  // the multi-rhs kernel has one CTA per macropoint: below two per SM the per-(macropoint, rhs)
+  // kernel fills the GPU better (config 2 level 2, 208 macropoints: 0.50 vs 0.41 ms)
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool force_mr = getenv("MCH_TRANSPORT_MR") != nullptr;  // tests: the multi-rhs kernel at any size
+  if (A.D == 2 && A.band == 0 && A.tphase == 0 && !generic && (force_mr || A.nprob_mp >= 2 * sms) &&
       (A.n_rhs == 3 || A.n_rhs == 6 || A.n_rhs == 9)) {
     const size_t sm = sizeof(double) * ((A.nsub * 7 + 2 + 1) / 2 + (size_t)8 * A.ncon * A.n_rhs);
     if (sm <= 232448) {
