@@ -1509,6 +1509,59 @@ __global__ void k_combine(LevelArgs A) {
   }
 }
 
+// all right-hand sides of a macropoint in one CTA: the interpolation weights and level-n node
+// ids of each fine node are formed once; per rhs the arithmetic is k_combine's (bitwise equal)
+template <int D>
+__global__ void __launch_bounds__(256) k_combine_mr(LevelArgs A) {
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<D> gf = fine_geo<D>(P);
+  const Geo<D> gl = level_geo<D>(A, P);
+  const int s = A.s, nr = A.n_rhs;
+  const int64_t nnf = gf.nnodes, nnl = gl.nnodes;
+  for (int k = threadIdx.x; k < gf.nnodes; k += blockDim.x) {
+    int x[3];
+    node_xyz<D>(gf, k, x);
+    int c0[3];
+    double t[3];
+    for (int i = 0; i < 3; i++) {
+      if (i < D) {
+        c0[i] = x[i] / s;
+        t[i] = (double)(x[i] - c0[i] * s) / s;
+        if (c0[i] == gl.nc[i]) { c0[i] -= 1; t[i] = 1.0; }
+      } else {
+        c0[i] = 0;
+        t[i] = 0.0;
+      }
+    }
+    double wgt[1 << D];
+    int nid[1 << D];
+#pragma unroll
+    for (int a = 0; a < (1 << D); a++) {
+      double w = 1.0;
+      int xc[3] = {0, 0, 0};
+      for (int i = 0; i < D; i++) {
+        const int ai = (a >> i) & 1;
+        w *= ai ? t[i] : 1.0 - t[i];
+        xc[i] = c0[i] + ai;
+      }
+      wgt[a] = w;
+      nid[a] = node_id<D>(gl, xc);
+    }
+    for (int r = 0; r < nr; r++) {
+      const double* xi = A.X + P.vec_off + (int64_t)r * nnl;
+      double v = 0.0;
+#pragma unroll
+      for (int a = 0; a < (1 << D); a++)
+        if (wgt[a] != 0.0) v += wgt[a] * xi[nid[a]];
+      double* I = A.FI + P.fine_off + (int64_t)r * nnf;
+      const double phi = I[k] + v;
+      I[k] = phi;
+      if (P.pool_off >= 0) A.pool[P.pool_off + (int64_t)r * nnf + k] = phi;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // Gram / Eq. (7): one CTA per macropoint
 template <int D>
@@ -1704,6 +1757,14 @@ cudaError_t launch_pcg(const LevelArgs& A, int threads, cudaStream_t st) {
 }
 
 cudaError_t launch_combine(const LevelArgs& A, int threads, cudaStream_t st) {
+  int dev = 0, sms = 148;  // one CTA per macropoint once there are two per SM (as the transport)
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (getenv("MCH_TRANSPORT_MR") != nullptr || (A.nprob_mp >= 2 * sms && getenv("MCH_TRANSPORT_GENERIC") == nullptr)) {
+    if (A.D == 2) k_combine_mr<2><<<(unsigned)A.nprob_mp, 256, 0, st>>>(A);
+    else k_combine_mr<3><<<(unsigned)A.nprob_mp, 256, 0, st>>>(A);
+    return cudaGetLastError();
+  }
   const unsigned grid = (unsigned)A.nprob_mp * A.n_rhs;
   if (A.D == 2) k_combine<2><<<grid, threads, 0, st>>>(A);
   else k_combine<3><<<grid, threads, 0, st>>>(A);
