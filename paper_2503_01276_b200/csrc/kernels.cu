@@ -412,6 +412,88 @@ __global__ void __launch_bounds__(256) k_transport2d_mr(LevelArgs A) {
   }
 }
 
+// 3D split transport, phases 1 (I_p) and 2 (b = -P_n^T Y) of k_transport for all right-hand
+// sides of a macropoint in one CTA (up to kMaxR): parent indices formed once per fine node, the
+// restriction passes over (rhs, line) pairs; per rhs the arithmetic is k_transport's.
+constexpr int kMaxR = 12;
+__global__ void __launch_bounds__(256) k_transport3d_mr(LevelArgs A) {
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<3> gf = fine_geo<3>(P);
+  const Geo<3> gl = level_geo<3>(A, P);
+  const int nr = A.n_rhs;
+  const int64_t nnf = gf.nnodes;
+  double* I = A.FI + P.fine_off;
+  double* Y = A.FY + P.fine_off;
+  if (A.tphase == 1) {
+    for (int k = threadIdx.x; k < gf.nnodes; k += blockDim.x) {
+      int x[3];
+      node_xyz<3>(gf, k, x);
+      double sr[kMaxR];
+#pragma unroll
+      for (int r = 0; r < kMaxR; r++) sr[r] = 0.0;
+      for (int t = 0; t < P.npar; t++) {
+        int64_t idx = 0;
+        for (int i = 2; i >= 0; i--) {
+          const int xt = P.lo[i] + x[i] + (P.par_k[t][i] - P.k[i]) * A.c - P.par_lo[t][i];
+          idx = idx * (P.par_ncf[t][i] + 1) + xt;
+        }
+        int64_t pn = 1;
+        for (int i = 0; i < 3; i++) pn *= (P.par_ncf[t][i] + 1);
+        const double* src = A.pool + P.par_pool[t] + idx;
+        const double w = P.par_w[t];
+#pragma unroll
+        for (int r = 0; r < kMaxR; r++)
+          if (r < nr) sr[r] += w * src[(int64_t)r * pn];
+      }
+#pragma unroll
+      for (int r = 0; r < kMaxR; r++)
+        if (r < nr) I[(int64_t)r * nnf + k] = sr[r];
+    }
+    return;
+  }
+  // phase 2: the separable in-place restriction of k_transport, per rhs
+  const int s = A.s;
+  const double inv_s = 1.0 / (double)s;
+  const int nfx = gf.nn[0], nfy = gf.nn[1], nfz = gf.nn[2];
+  const int nlx = gl.nn[0], nly = gl.nn[1], nlz = gl.nn[2];
+  auto restrict1 = [&](double* v, int64_t stride, int nf, int nl, auto&& put) {
+    for (int X = 0; X < nl; X++) {
+      const int c0 = X * s;
+      double acc = v[(int64_t)c0 * stride];
+      for (int d = 1; d < s; d++) {
+        const double w = 1.0 - d * inv_s;
+        if (c0 - d >= 0) acc += w * v[(int64_t)(c0 - d) * stride];
+        if (c0 + d < nf) acc += w * v[(int64_t)(c0 + d) * stride];
+      }
+      put(X, acc);
+    }
+  };
+  const int rows = nfy * nfz;
+  for (int u = threadIdx.x; u < nr * rows; u += blockDim.x) {
+    const int r = u / rows, row = u - r * rows;
+    double* v = Y + (int64_t)r * nnf + (int64_t)row * nfx;
+    restrict1(v, 1, nfx, nlx, [&](int X, double a) { v[X] = a; });
+  }
+  __syncthreads();
+  const int cols = nfz * nlx;
+  for (int u = threadIdx.x; u < nr * cols; u += blockDim.x) {
+    const int r = u / cols, col = u - r * cols;
+    const int fz = col / nlx, X = col - fz * nlx;
+    double* v = Y + (int64_t)r * nnf + (int64_t)fz * nfy * nfx + X;
+    restrict1(v, nfx, nfy, nly, [&](int Yc, double a) { v[(int64_t)Yc * nfx] = a; });
+  }
+  __syncthreads();
+  const int lines = nly * nlx;
+  for (int u = threadIdx.x; u < nr * lines; u += blockDim.x) {
+    const int r = u / lines, col = u - r * lines;
+    const int Yc = col / nlx, X = col - Yc * nlx;
+    double* v = Y + (int64_t)r * nnf + (int64_t)Yc * nfx + X;
+    double* bvec = A.B + P.vec_off + (int64_t)r * gl.nnodes;
+    restrict1(v, (int64_t)nfy * nfx, nfz, nlz, [&](int Z, double a) { bvec[((int64_t)Z * nly + Yc) * nlx + X] = -a; });
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // projector setup: one CTA per macropoint
 template <int D>
@@ -1691,6 +1773,12 @@ cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool force_mr = getenv("MCH_TRANSPORT_MR") != nullptr;  // tests: the multi-rhs kernel at any size
+  // 3D: its fine windows are 8x larger per macropoint; from eight macropoints per SM up (config 5
+  // level 4: 332 -> 306 ms; level 3, 604 macropoints: 66 -> 71 ms, kept per rhs)
+  if (A.D == 3 && A.tphase != 0 && A.n_rhs <= kMaxR && (force_mr || A.nprob_mp >= 8 * sms)) {
+    k_transport3d_mr<<<(unsigned)A.nprob_mp, 256, 0, st>>>(A);
+    return cudaGetLastError();
+  }
   if (A.D == 2 && A.band == 0 && A.tphase == 0 && !generic && (force_mr || A.nprob_mp >= 2 * sms) &&
       (A.n_rhs == 3 || A.n_rhs == 6 || A.n_rhs == 9)) {
     const size_t sm = sizeof(double) * ((A.nsub * 7 + 2 + 1) / 2 + (size_t)8 * A.ncon * A.n_rhs);

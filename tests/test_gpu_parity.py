@@ -489,10 +489,10 @@ def test_coarse_space_preconditioner(monkeypatch):
 @pytest.mark.parametrize("d,n,M,L,N,seed", [(3, 16, 4, 2, 2, 970), (2, 64, 8, 3, 1, 41), (2, 64, 8, 3, 2, 7),
                                              (2, 32, 4, 2, 3, 23)])
 def test_transport_paths_agree(d, n, M, L, N, seed, monkeypatch):
-    """Levels >= 2: the split transport of 3D (I_p, column-walking A_1 I_p / C_1 I_p, separable
-    P_n^T) and the multi-rhs transport of 2D (k_transport2d_mr, n_rhs = 3 / 6 / 9) give the same
-    coefficients as the generic per-(macropoint, rhs) k_transport (MCH_TRANSPORT_GENERIC), and
-    both match the oracle (R15 bar)."""
+    """Levels >= 2: the split transport of 3D (I_p and P_n^T for all rhs per CTA, column-walking
+    A_1 I_p / C_1 I_p) and the multi-rhs transport of 2D (k_transport2d_mr, n_rhs = 3 / 6 / 9),
+    both with the multi-rhs combine (MCH_TRANSPORT_MR), give the same coefficients as the generic
+    per-(macropoint, rhs) kernels (MCH_TRANSPORT_GENERIC), and both match the oracle (R15 bar)."""
     H = _gpu()
     kap, ids = _admissible(d, n, M, N, seed)
     o = Oracle(d, n, M, L, 2, N, kap, ids)
@@ -502,7 +502,7 @@ def test_transport_paths_agree(d, n, M, L, N, seed, monkeypatch):
         if flag:
             monkeypatch.delenv("MCH_TRANSPORT_MR", raising=False)
             monkeypatch.setenv("MCH_TRANSPORT_GENERIC", flag)
-        elif d == 2:  # small grids take the per-(macropoint, rhs) kernel by default: force the other
+        else:  # small grids take the per-(macropoint, rhs) kernels by default: force the others
             monkeypatch.setenv("MCH_TRANSPORT_MR", "1")
         with H(d, n, N, M, L, 2, kap, ids) as h:
             h.solve_all()
