@@ -1192,96 +1192,127 @@ __global__ void k_proj_setup_band(LevelArgs A) {
 
 // ---------------------------------------------------------------------------------------
 // Reading R20: S^+ = Lambda S~^+ Lambda with S~ = V diag(lambda) V^T, eigenvalues
-// below 1e-11 lambda_max dropped.  One warp per flagged window: parallel cyclic Jacobi with the
-// round-robin ordering (each round rotates nc/2 disjoint pairs at once: lane k owns pair k),
-// sweeps until the off-diagonal mass is below 1e-34 of the diagonal's (at most 40 sweeps).
-__global__ void k_pinv(LevelArgs A) {
+// below 1e-11 lambda_max dropped.  One CTA per flagged window: parallel cyclic Jacobi with the
+// round-robin ordering (each round rotates nc/2 disjoint pairs at once; the row and column updates
+// of all pairs are spread over the CTA), sweeps until the off-diagonal mass is below 1e-34 of the
+// diagonal's (at most 40 sweeps).
+__global__ void __launch_bounds__(256) k_pinv(LevelArgs A) {
   const int mp = blockIdx.x;
   if (!(A.flags[mp] & 2)) return;
-  const int nc = A.ncon, lane = threadIdx.x;
+  const int nc = A.ncon, tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
   extern __shared__ double sm[];
   double* S = sm;            // nc*nc (padded to even m)
   const int m = (nc + 1) & ~1;
   double* V = S + m * m;     // m*m
-  int* pos = reinterpret_cast<int*>(V + m * m);  // m
+  double* rc = V + m * m;    // [64] cos, [64] sin of this round's rotations (m <= 128)
+  double* rs = rc + 64;
+  int* pos = reinterpret_cast<int*>(rs + 64);  // m
+  int* rp = pos + m;         // [64] p, [64] q of this round's pairs (q = -1: no rotation)
+  int* rq = rp + 64;
+  __shared__ int done;
   double* Sg = A.Sinv + (int64_t)mp * nc * nc;
-  for (int idx = lane; idx < m * m; idx += 32) {
+  for (int idx = tid; idx < m * m; idx += nt) {
     const int i = idx / m, j = idx % m;
     S[idx] = (i < nc && j < nc) ? Sg[i * nc + j] : 0.0;  // padded row/column: decoupled zero
     V[idx] = (i == j) ? 1.0 : 0.0;
   }
-  for (int i = lane; i < m; i += 32) pos[i] = i;
-  __syncwarp();
+  for (int i = tid; i < m; i += nt) pos[i] = i;
+  __syncthreads();
+  const int np = m / 2;
   for (int sweep = 0; sweep < 40; sweep++) {
-    double off = 0.0, dia = 0.0;
-    for (int idx = lane; idx < m * m; idx += 32) {
-      const int i = idx / m, j = idx % m;
-      const double a = S[idx];
-      if (i < j) off += a * a;
-      else if (i == j) dia += a * a;
+    if (tid < 32) {  // convergence test by warp 0 (one fixed summation order)
+      double off = 0.0, dia = 0.0;
+      for (int idx = lane; idx < m * m; idx += 32) {
+        const int i = idx / m, j = idx % m;
+        const double a = S[idx];
+        if (i < j) off += a * a;
+        else if (i == j) dia += a * a;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        off += __shfl_xor_sync(FULLMASK, off, o);
+        dia += __shfl_xor_sync(FULLMASK, dia, o);
+      }
+      if (lane == 0) done = (off <= 1e-34 * dia);
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      off += __shfl_xor_sync(FULLMASK, off, o);
-      dia += __shfl_xor_sync(FULLMASK, dia, o);
-    }
-    if (off <= 1e-34 * dia) break;
+    __syncthreads();
+    if (done) break;
     for (int round = 0; round < m - 1; round++) {
       // pairs of this round: (pos[k], pos[m-1-k]), k < m/2
-      int p = 0, q = 0;
-      double c = 1.0, sn = 0.0, t = 0.0, apq = 0.0;
-      bool rot = false;
-      if (lane < m / 2) {
-        p = pos[lane];
-        q = pos[m - 1 - lane];
+      if (tid < np) {
+        int p = pos[tid], q = pos[m - 1 - tid];
         if (p > q) { const int tt = p; p = q; q = tt; }
-        apq = S[p * m + q];
+        const double apq = S[p * m + q];
+        double c = 1.0, sn = 0.0;
         if (fabs(apq) >= 1e-300) {
           const double th = (S[q * m + q] - S[p * m + p]) / (2.0 * apq);
-          t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+          const double t = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
           c = 1.0 / sqrt(t * t + 1.0);
           sn = t * c;
-          rot = true;
+        } else {
+          q = -1;  // no rotation
         }
+        rp[tid] = p;
+        rq[tid] = q;
+        rc[tid] = c;
+        rs[tid] = sn;
       }
-      __syncwarp();
-      // rows p, q (all columns), then columns p, q (all rows): S <- J^T S J, V <- V J
-      if (rot)
-        for (int k = 0; k < m; k++) {
-          const double skp = S[p * m + k], skq = S[q * m + k];
-          S[p * m + k] = c * skp - sn * skq;
-          S[q * m + k] = sn * skp + c * skq;
-        }
-      __syncwarp();
-      if (rot)
-        for (int k = 0; k < m; k++) {
-          const double skp = S[k * m + p], skq = S[k * m + q];
-          S[k * m + p] = c * skp - sn * skq;
-          S[k * m + q] = sn * skp + c * skq;
-          const double vkp = V[k * m + p], vkq = V[k * m + q];
-          V[k * m + p] = c * vkp - sn * vkq;
-          V[k * m + q] = sn * vkp + c * vkq;
-        }
-      __syncwarp();
-      if (rot) {
-        S[p * m + q] = 0.0;
-        S[q * m + p] = 0.0;
+      __syncthreads();
+      // rows p, q (all columns), then columns p, q (all rows): S <- J^T S J, V <- V J; the pairs
+      // are disjoint, so every element is updated once per phase (as the one-warp form)
+      for (int idx = tid; idx < np * m; idx += nt) {
+        const int k2 = idx / m, k = idx - k2 * m;
+        const int p = rp[k2], q = rq[k2];
+        if (q < 0) continue;
+        const double c = rc[k2], sn = rs[k2];
+        const double skp = S[p * m + k], skq = S[q * m + k];
+        S[p * m + k] = c * skp - sn * skq;
+        S[q * m + k] = sn * skp + c * skq;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < np * m; idx += nt) {
+        const int k2 = idx / m, k = idx - k2 * m;
+        const int p = rp[k2], q = rq[k2];
+        if (q < 0) continue;
+        const double c = rc[k2], sn = rs[k2];
+        const double skp = S[k * m + p], skq = S[k * m + q];
+        S[k * m + p] = c * skp - sn * skq;
+        S[k * m + q] = sn * skp + c * skq;
+        const double vkp = V[k * m + p], vkq = V[k * m + q];
+        V[k * m + p] = c * vkp - sn * vkq;
+        V[k * m + q] = sn * vkp + c * vkq;
+      }
+      __syncthreads();
+      if (tid < np && rq[tid] >= 0) {
+        S[rp[tid] * m + rq[tid]] = 0.0;
+        S[rq[tid] * m + rp[tid]] = 0.0;
       }
       // rotate positions 1..m-1 (circle method)
-      int nxt[2] = {0, 0};  // m <= 64
-      for (int i = lane, r = 0; i < m; i += 32, r++) nxt[r] = (i == 0) ? pos[0] : pos[(i == 1) ? m - 1 : i - 1];
-      __syncwarp();
-      for (int i = lane, r = 0; i < m; i += 32, r++) pos[i] = nxt[r];
-      __syncwarp();
+      int nxt = 0;
+      if (tid < m) nxt = (tid == 0) ? pos[0] : pos[(tid == 1) ? m - 1 : tid - 1];
+      __syncthreads();
+      if (tid < m) pos[tid] = nxt;
+      __syncthreads();
     }
   }
-  double lmax = 0.0;
-  for (int i = lane; i < nc; i += 32) lmax = fmax(lmax, S[i * m + i]);
-  for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(FULLMASK, lmax, o));
+  __shared__ double lmax_s;
+  __shared__ int trunc_s;
+  if (tid < 32) {
+    double lmax = 0.0;
+    for (int i = lane; i < nc; i += 32) lmax = fmax(lmax, S[i * m + i]);
+    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(FULLMASK, lmax, o));
+    bool trunc = false;
+    for (int k = lane; k < nc; k += 32) trunc = trunc || !(S[k * m + k] > 1e-11 * lmax);
+    const bool any = __any_sync(FULLMASK, trunc);
+    if (lane == 0) {
+      lmax_s = lmax;
+      trunc_s = any;
+      if (any) atomicOr(&A.flags[mp], 4);  // rows were dependent
+    }
+  }
+  __syncthreads();
+  const double lmax = lmax_s;
   const double* ds = A.pinv_ds + (int64_t)mp * nc;
-  bool trunc = false;
-  for (int k = lane; k < nc; k += 32) trunc = trunc || !(S[k * m + k] > 1e-11 * lmax);
-  if (__any_sync(FULLMASK, trunc) && lane == 0) atomicOr(&A.flags[mp], 4);  // rows were dependent
-  for (int idx = lane; idx < nc * nc; idx += 32) {
+  for (int idx = tid; idx < nc * nc; idx += nt) {
     const int i = idx / nc, j = idx % nc;
     double acc = 0.0;
     for (int k = 0; k < nc; k++) {
@@ -1822,10 +1853,11 @@ cudaError_t launch_proj_setup(const LevelArgs& A, int threads, cudaStream_t st) 
 cudaError_t launch_pinv(const LevelArgs& A, cudaStream_t st) {
   if (A.band > 0) return cudaSuccess;  // the banded projector reports dependent rows instead (flag 8)
   const int m = (A.ncon + 1) & ~1;
-  const size_t sm = sizeof(double) * 2 * (size_t)m * m + sizeof(int) * m;
+  if (m > 128) return cudaErrorInvalidValue;
+  const size_t sm = sizeof(double) * (2 * (size_t)m * m + 128) + sizeof(int) * ((size_t)m + 128);
   cudaError_t e = cudaFuncSetAttribute(k_pinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  k_pinv<<<A.nprob_mp, 32, sm, st>>>(A);
+  k_pinv<<<A.nprob_mp, 256, sm, st>>>(A);
   return cudaGetLastError();
 }
 
