@@ -599,10 +599,19 @@ __global__ void k_proj_setup(LevelArgs A) {
     const int nca = A.ncomp[mp];
     const double* CZ = A.CZ + (int64_t)mp * nc * A.ncmax;
     const double* Ei = A.Einv + (int64_t)mp * A.ncmax;
+    // staged in shared memory (after V's area) so the nc^2 dot products read no L2
+    double* czs = eb_end + nc * nc;  // [nc][nca]
+    double* eis = czs + nc * nca;    // [nca]
+    for (int idx = threadIdx.x; idx < nc * nca; idx += blockDim.x) {
+      const int i = idx / nca, a = idx - i * nca;
+      czs[idx] = CZ[(int64_t)i * A.ncmax + a];
+    }
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) eis[a] = Ei[a];
+    __syncthreads();
     for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
       const int i = idx / nc, j = idx % nc;
       double acc = 0.0;
-      for (int a = 0; a < nca; a++) acc += CZ[(int64_t)i * A.ncmax + a] * Ei[a] * CZ[(int64_t)j * A.ncmax + a];
+      for (int a = 0; a < nca; a++) acc += czs[i * nca + a] * eis[a] * czs[j * nca + a];
       S[idx] += acc;
     }
     __syncthreads();
@@ -899,11 +908,14 @@ __global__ void k_coarse_setup(LevelArgs A) {
   __shared__ int ebs[125 * 7 + 2];
   __shared__ int ntask;
   subcell_boxes<D>(A, P, g, ebs, &ntask);
-  for (int a = 0; a < ncomp; a++) {
+  // one warp per component (lanes over its bounding box, fixed-order warp sum): no block-wide
+  // reduction per component
+  const int lane_ = threadIdx.x & 31, nwarp_ = blockDim.x >> 5;
+  for (int a = threadIdx.x >> 5; a < ncomp; a += nwarp_) {
     const int* bx = box + a * 6;
     const int ex = bx[3] - bx[0] + 1, ey = bx[4] - bx[1] + 1, ez = (D == 3) ? bx[5] - bx[2] + 1 : 1;
     double v[1] = {0.0};
-    for (int idx = threadIdx.x; idx < ex * ey * ez; idx += blockDim.x) {
+    for (int idx = lane_; idx < ex * ey * ez; idx += 32) {
       const int x[3] = {bx[0] + idx % ex, bx[1] + (idx / ex) % ey, (D == 3) ? bx[2] + idx / (ex * ey) : 0};
       const int k = node_id<D>(g, x);
       if (cm[k] != a) continue;
@@ -928,10 +940,11 @@ __global__ void k_coarse_setup(LevelArgs A) {
       }
       v[0] += az;
     }
-    block_sum<1>(v, red, red + 48);
-    if (threadIdx.x == 0) Ei[a] = (red[48] > 0.0) ? 1.0 / red[48] : 0.0;
-    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[0] += __shfl_down_sync(FULLMASK, v[0], o);
+    if (lane_ == 0) Ei[a] = (v[0] > 0.0) ? 1.0 / v[0] : 0.0;
   }
+  __syncthreads();
   // (A z_a) lists for the recurrence Z^T r_{k+1} = Z^T r~_k + alpha (A Z)^T p_k of the on-chip 2D
   // kernels: thread per component over its bounding box grown by one node, nonzeros in node
   // order; a window whose lists exceed kAzCap entries per node runs without the coarse space
@@ -1837,7 +1850,8 @@ cudaError_t launch_proj_setup(const LevelArgs& A, int threads, cudaStream_t st) 
     k_proj_setup_band<2><<<A.nprob_mp, threads, sm, st>>>(A);
     return cudaGetLastError();
   }
-  const size_t sm = sizeof(double) * (2 * (size_t)A.ncon * A.ncon + 32 * 16 + 16 + (A.nsub * 7 + 2 + 1) / 2 + 2);
+  const size_t sm = sizeof(double) * (2 * (size_t)A.ncon * A.ncon + 32 * 16 + 16 + (A.nsub * 7 + 2 + 1) / 2 + 2 +
+                                       (A.coarse ? (size_t)(A.ncon + 1) * A.ncmax : 0));
   cudaError_t e;
   if (A.D == 2) {
     e = cudaFuncSetAttribute(k_proj_setup<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
