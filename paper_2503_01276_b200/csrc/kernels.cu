@@ -582,13 +582,21 @@ __global__ void k_proj_setup(LevelArgs A) {
         for (int j1 = 0; j1 < N; j1++)
           for (int j2 = 0; j2 < N; j2++) v[j1 * 4 + j2] += w1[j1] * w2[j2] * di;
       }
-      block_sum<16>(v, scratch, tot);
+      // reduce only the N x N entries in use (N <= 2: 4 of the 16; the shuffles dominated)
+      int ts = 4;
+      if (N <= 2) {
+        double v4[4] = {v[0], v[1], v[4], v[5]};
+        block_sum<4>(v4, scratch, tot);
+        ts = 2;
+      } else {
+        block_sum<16>(v, scratch, tot);
+      }
       if (threadIdx.x == 0) {
         for (int j1 = 0; j1 < N; j1++)
           for (int j2 = 0; j2 < N; j2++) {
             const int r1 = q1 * N + j1, r2 = q2 * N + j2;
-            S[r1 * nc + r2] = tot[j1 * 4 + j2];
-            S[r2 * nc + r1] = tot[j1 * 4 + j2];
+            S[r1 * nc + r2] = tot[j1 * ts + j2];
+            S[r2 * nc + r1] = tot[j1 * ts + j2];
           }
       }
       __syncthreads();
