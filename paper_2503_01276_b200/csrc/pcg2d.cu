@@ -616,7 +616,17 @@ __global__ void __launch_bounds__(MAXW * 32, MINB) k_pcg2d(LevelArgs A) {
     v = warp_sum0(v);
     if (lane == 0) slots[which * 32 + warp] = v;
   };
-  auto slot_fin = [&](int which) { return warp_sum0((lane < MAXW) ? slots[which * 32 + lane] : 0.0); };
+  // every lane sums the per-warp slots itself from broadcast reads: no shuffle chain after the
+  // barriers (two fixed-order chains)
+  auto slot_fin = [&](int which) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < MAXW; w2 += 2) {
+      s0 += slots[which * 32 + w2];
+      if (w2 + 1 < MAXW) s1 += slots[which * 32 + w2 + 1];
+    }
+    return s0 + s1;
+  };
 
   // ---- two-level preconditioner M^-1 = D^-1 + Z E^-1 Z^T: s = Z^T r summed per
   //      component from a mirror of r (start; every iteration in the 49-node windows) or carried
