@@ -509,6 +509,11 @@ __global__ void k_proj_setup(LevelArgs A) {
   int* eb = reinterpret_cast<int*>(tot + 16);
   double* eb_end = tot + 16 + (A.nsub * 7 + 2 + 1) / 2 + 1;  // V (nc*nc) after the int area
   double* dinv = A.dinv + P.node_off;
+  if (A.psplit == 2) {  // second half: S = C D^-1 C^T as the first half left it in Sinv
+    const double* si = A.Sinv + (int64_t)mp * nc * nc;
+    for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) S[i] = si[i];
+    __syncthreads();
+  } else {
   // D^-1 rounded to fp32 in 2D: the on-chip PCG (pcg2d.cu) keeps it in fp32 shared memory, and S
   // below must be formed with the identical values for the projection to be exact
   for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) {
@@ -602,6 +607,12 @@ __global__ void k_proj_setup(LevelArgs A) {
       __syncthreads();
     }
   }
+  if (A.psplit == 1) {  // first half (beside k_coarse_setup): hand S over in Sinv
+    double* so = A.Sinv + (int64_t)mp * nc * nc;
+    for (int i = threadIdx.x; i < nc * nc; i += blockDim.x) so[i] = S[i];
+    return;
+  }
+  }  // psplit != 2
   // two-level preconditioner: S_M = C M^-1 C^T = C D^-1 C^T + (CZ) E^-1 (CZ)^T
   if (A.coarse) {
     const int nca = A.ncomp[mp];

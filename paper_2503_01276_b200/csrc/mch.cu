@@ -115,6 +115,7 @@ struct mch_ctx {
   mch_params p{};
   int D = 2, N = 1, n_rhs = 3, l = 1, w = 3, nsub = 9, ncon = 9;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;  // side stream: the projector's C D^-1 C^T beside the coarse-space setup
   HostPlan plan;
   double* kappa = nullptr;
   uint8_t* ids = nullptr;
@@ -332,6 +333,8 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   c->stats.assign(p.levels + 1, mch_level_stats{});
   for (int i = 0; i < 8; i++) cudaEventCreate(&c->ev[i]);
   c->events = true;
+  if ((e = cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking)) != cudaSuccess)
+    return cleanup(MCH_ECUDA, cudaGetErrorString(e));
   if ((e = cudaStreamSynchronize(c->st)) != cudaSuccess) return cleanup(MCH_ECUDA, cudaGetErrorString(e));
   *out = c;
   return MCH_OK;
@@ -656,11 +659,26 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     A.cptr = c->cptr.as<int>(); A.clist = c->clist.as<int>();
     A.azp = (B.coarse && B.on2d && B.variant == PCG2D_V_L1) ? c->azp.as<int>() : nullptr;
     A.azi = c->azi.as<int>(); A.azw = c->azw.as<double>();
+    // with the coarse space, the projector's S = C D^-1 C^T (independent of it) is formed on the
+    // side stream beside k_coarse_setup (81 / 208 CTAs each at config 2), then completed with
+    // (CZ) E^-1 (CZ)^T and inverted
+    const bool psplit = A.coarse && c->band == 0 && c->st2 != nullptr;
+    if (psplit) {
+      CKC(c, cudaEventRecord(c->ev[6], st));
+      CKC(c, cudaStreamWaitEvent(c->st2, c->ev[6], 0));
+      A.psplit = 1;
+      CKC(c, launch_proj_setup(A, B.th_l, c->st2));
+      CKC(c, cudaEventRecord(c->ev[7], c->st2));
+      A.psplit = 2;
+      S.launches += 1;
+    }
     if (A.coarse) {
       CKC(c, launch_coarse_setup(A, st));
       S.launches += 1;
     }
+    if (psplit) CKC(c, cudaStreamWaitEvent(st, c->ev[7], 0));
     CKC(c, launch_proj_setup(A, B.th_l, st));
+    A.psplit = 0;
     CKC(c, launch_pinv(A, st));
     S.launches += 1;
     if (B.on2d && !B.l1op) {
@@ -1080,5 +1098,6 @@ extern "C" void mch_destroy(mch_ctx* c) {
   // (LevelBatch buffers are released by lplans.clear() above)
   if (c->events)
     for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);
+  if (c->st2) cudaStreamDestroy(c->st2);
   delete c;
 }

@@ -76,6 +76,7 @@ struct LevelArgs {
   int* azi;                // [kAzCap * nodes] node of each entry, packed x | y << 16
   double* azw;             // [kAzCap * nodes] (A z_a) at that node
   int tphase;              // k_transport: 0 all phases; 1 only I_p; 2 only the restriction (3D split path)
+  int psplit;              // k_proj_setup: 0 whole; 1 only S = C D^-1 C^T (into Sinv); 2 the rest from it
   const double* f;         // NEXT-2: cellwise source, n^D, x fastest (NULL: no load vectors)
   double* bload;           // NEXT-2: [P][N] load vectors b_j = int_{K_p} f phi_j (Eq. 7)
   int* iters; double* relres;  // [problem]
