@@ -704,6 +704,32 @@ __global__ void k_proj_setup(LevelArgs A) {
 // pointer jumping (the result is the smallest node index of each component, independent of
 // the order of updates) and numbered in node order.  Per component: bounding box, E_aa = z_a^T
 // A z_a, and C z_a (constraint rows of the indicator).  Everything summed in a fixed order.
+// exclusive prefix sum over the CTA of one int per thread (blockDim a multiple of 32): returns
+// this thread's prefix; *tot = the sum, valid after the call (two barriers inside)
+__device__ __forceinline__ int block_excl_scan(int v, int* wtot, int* tot) {
+  const int ln = threadIdx.x & 31, wd = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULLMASK, incl, o);
+    if (ln >= o) incl += t;
+  }
+  if (ln == 31) wtot[wd] = incl;
+  __syncthreads();
+  if (wd == 0) {
+    int w = (ln < nwp) ? wtot[ln] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(FULLMASK, w, o);
+      if (ln >= o) w += t;
+    }
+    if (ln < nwp) wtot[ln] = w;
+    if (ln == nwp - 1) *tot = w;
+  }
+  __syncthreads();
+  return incl - v + (wd > 0 ? wtot[wd - 1] : 0);
+}
+
 #ifndef MCH_COARSE_CONTRAST
 #define MCH_COARSE_CONTRAST 20.0  // window contrast kappa_max / kappa_min that turns the coarse space on
 #endif
@@ -819,17 +845,8 @@ __global__ void k_coarse_setup(LevelArgs A) {
   const int k0 = threadIdx.x * chunk, k1 = min(nn, k0 + chunk);
   int mine = 0;
   for (int k = k0; k < k1; k++) mine += (cm[k] == k);
-  cnt[threadIdx.x] = mine;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int s = 0;
-    for (int t = 0; t < (int)blockDim.x; t++) {
-      const int c = cnt[t];
-      cnt[t] = s;
-      s += c;
-    }
-    total = s;
-  }
+  __shared__ int wtot[32];
+  cnt[threadIdx.x] = block_excl_scan(mine, wtot, &total);
   __syncthreads();
   {
     int id = cnt[threadIdx.x];
@@ -996,24 +1013,23 @@ __global__ void k_coarse_setup(LevelArgs A) {
       }
       return az;
     };
-    for (int a = threadIdx.x; a < ncomp; a += blockDim.x) {
+    // thread a counts component a (ncomp <= ncmax < blockDim), then one block scan
+    int myc = 0;
+    if ((int)threadIdx.x < ncomp) {
+      const int a = threadIdx.x;
       const int* bx = box + a * 6;
-      int c = 0;
       for (int y = max(bx[1] - 1, 0); y <= min(bx[4] + 1, g.nn[1] - 1); y++)
         for (int x = max(bx[0] - 1, 0); x <= min(bx[3] + 1, g.nn[0] - 1); x++) {
           const int xx[3] = {x, y, 0};
-          c += (azval(a, xx) != 0.0);
+          myc += (azval(a, xx) != 0.0);
         }
-      ap[a + 1] = c;
     }
+    __shared__ int aztot;
+    const int aexcl = block_excl_scan(myc, wtot, &aztot);
+    if ((int)threadIdx.x < ncomp) ap[threadIdx.x] = aexcl;
+    if (threadIdx.x == 0) ap[ncomp] = aztot;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      ap[0] = 0;
-      for (int a = 0; a < ncomp; a++) ap[a + 1] += ap[a];
-      if (ap[ncomp] > kAzCap * nn) total = -1;  // overflow: no coarse space for this window
-    }
-    __syncthreads();
-    if (total < 0) {
+    if (aztot > kAzCap * nn) {  // overflow: no coarse space for this window
       for (int k = threadIdx.x; k < nn; k += blockDim.x) cm[k] = -1;
       if (threadIdx.x == 0) A.ncomp[mp] = 0;
       return;
