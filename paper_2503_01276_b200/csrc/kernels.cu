@@ -1013,17 +1013,34 @@ __global__ void k_coarse_setup(LevelArgs A) {
       }
       return az;
     };
-    // thread a counts component a (ncomp <= ncmax < blockDim), then one block scan
-    int myc = 0;
-    if ((int)threadIdx.x < ncomp) {
-      const int a = threadIdx.x;
+    // one warp per component over its grown bounding box in row-major chunks of 32 nodes
+    // (ballots keep the node order), counts then one block scan (ncomp <= ncmax < blockDim)
+    const int wl = threadIdx.x & 31, wn = blockDim.x >> 5;
+    auto gbox = [&](int a, int& x0, int& y0, int& ex, int& ey) {
       const int* bx = box + a * 6;
-      for (int y = max(bx[1] - 1, 0); y <= min(bx[4] + 1, g.nn[1] - 1); y++)
-        for (int x = max(bx[0] - 1, 0); x <= min(bx[3] + 1, g.nn[0] - 1); x++) {
-          const int xx[3] = {x, y, 0};
-          myc += (azval(a, xx) != 0.0);
+      x0 = max(bx[0] - 1, 0);
+      y0 = max(bx[1] - 1, 0);
+      ex = min(bx[3] + 1, g.nn[0] - 1) - x0 + 1;
+      ey = min(bx[4] + 1, g.nn[1] - 1) - y0 + 1;
+    };
+    __shared__ int azc[256];
+    for (int a = threadIdx.x >> 5; a < ncomp; a += wn) {
+      int x0, y0, ex, ey;
+      gbox(a, x0, y0, ex, ey);
+      int c = 0;
+      for (int base = 0; base < ex * ey; base += 32) {
+        const int idx = base + wl;
+        bool nz = false;
+        if (idx < ex * ey) {
+          const int xx[3] = {x0 + idx % ex, y0 + idx / ex, 0};
+          nz = azval(a, xx) != 0.0;
         }
+        c += __popc(__ballot_sync(FULLMASK, nz));
+      }
+      if (wl == 0) azc[a] = c;
     }
+    __syncthreads();
+    const int myc = ((int)threadIdx.x < ncomp) ? azc[threadIdx.x] : 0;
     __shared__ int aztot;
     const int aexcl = block_excl_scan(myc, wtot, &aztot);
     if ((int)threadIdx.x < ncomp) ap[threadIdx.x] = aexcl;
@@ -1034,19 +1051,28 @@ __global__ void k_coarse_setup(LevelArgs A) {
       if (threadIdx.x == 0) A.ncomp[mp] = 0;
       return;
     }
-    for (int a = threadIdx.x; a < ncomp; a += blockDim.x) {
-      const int* bx = box + a * 6;
+    for (int a = threadIdx.x >> 5; a < ncomp; a += wn) {
+      int x0, y0, ex, ey;
+      gbox(a, x0, y0, ex, ey);
       int o = ap[a];
-      for (int y = max(bx[1] - 1, 0); y <= min(bx[4] + 1, g.nn[1] - 1); y++)
-        for (int x = max(bx[0] - 1, 0); x <= min(bx[3] + 1, g.nn[0] - 1); x++) {
+      for (int base = 0; base < ex * ey; base += 32) {
+        const int idx = base + wl;
+        double w = 0.0;
+        int x = 0, y = 0;
+        if (idx < ex * ey) {
+          x = x0 + idx % ex;
+          y = y0 + idx / ex;
           const int xx[3] = {x, y, 0};
-          const double w = azval(a, xx);
-          if (w != 0.0) {
-            ai[o] = x | (y << 16);
-            aw[o] = w;
-            o++;
-          }
+          w = azval(a, xx);
         }
+        const unsigned m = __ballot_sync(FULLMASK, w != 0.0);
+        if (w != 0.0) {
+          const int at = o + __popc(m & ((1u << wl) - 1u));
+          ai[at] = x | (y << 16);
+          aw[at] = w;
+        }
+        o += __popc(m);
+      }
     }
     __syncthreads();
   }
