@@ -126,7 +126,14 @@ __global__ void k_targets(LevelArgs A) {
         }
       }
     }
-    block_sum<16>(v, scratch, tot);
+    if (N <= 2) {  // entries j*4 + (0..D) with j < N all lie in the first 8: reduce only those
+      double v8[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) v8[i] = v[i];
+      block_sum<8>(v8, scratch, tot);
+    } else {
+      block_sum<16>(v, scratch, tot);
+    }
     if (pass == 0) {
       if (threadIdx.x == 0) {
         for (int j = 0; j < N; j++) {
