@@ -1,0 +1,412 @@
+// Fused fine-window passes of the 3D correction problems (levels n >= 2, fine windows of at most
+// 49 nodes per side), SURVEY.md §8(a) rows a4 and a6:
+//
+//   k_fine3d_transport   I_p = sum_t c_t phi_t(x_t + .)           (Eq. 11, reading R9)
+//                        b   = -P_n^T A_1 I_p                       (Eqs. 12/13 first lines, R5)
+//                        g   = g^0 - C_1 I_p                        (Eqs. 12/13 second lines)
+//   k_fine3d_combine     phi_p = P_n xi + I_p on K_p (for Eq. 7) and, for parents, on R_p^+
+//
+// PAPER.md:382-419.  The transported field I_p and A_1 I_p never leave the chip: one CTA per
+// (child, rhs) walks the window plane by plane (z), forms I_p on plane z+1 from the parents' fine
+// fields (L2-resident, read once per node), keeps three I planes in shared memory, applies the
+// kappa-weighted Q1 element rows to the nodes of plane z (each thread owns a strip of 7 node rows
+// of one column and slides a 3x3x3 register window along it), accumulates the constraint sums
+// C_1 I_p per (subcell, continuum) from the cells' corner sums, and restricts A_1 I_p to the
+// level-n nodes with the separable 1D hat weights (x and y per plane, z into two running level
+// planes).  Every sum runs in a fixed order, so results are bitwise reproducible.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "device_common.cuh"
+#include "kernels.h"
+
+namespace {
+
+constexpr int kFX = 49;                       // max fine nodes per side
+constexpr int kFC = kFX - 1;                  // max fine cells per side
+constexpr int kStrip = 7;                     // node rows per thread
+constexpr int kFThreads = kFX * kStrip;       // 343 (49 columns x 7 strips)
+constexpr int kFBlock = 352;                  // 11 warps
+
+__device__ __forceinline__ int slot_f(const LevelArgs& A, const ProbDesc& P, int dim, int e) {
+  return fdiv(P.lo[dim] + e + A.coff, A.inv_c) - P.k[dim] + A.l;  // subcell slot of fine cell e
+}
+
+}  // namespace
+
+size_t fine3d_transport_smem(int N) {
+  // I ring 4 x 49^2, kappa ring 3 x 48^2, ids ring 3 x 48^2 (bytes), Y plane 49^2, Yx 49 x 25,
+  // level planes 2 x 25^2, constraint partials, constraint sums
+  const size_t d = 4 * kFX * kFX + 3 * kFC * kFC + kFX * kFX + kFX * 25 + 2 * 25 * 25 + (size_t)kFThreads * 3 * N + 27 * N;
+  return d * sizeof(double) + 3 * kFC * kFC;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
+  const int r = blockIdx.x / A.nprob_mp, mp = blockIdx.x - r * A.nprob_mp;  // rhs-major: siblings share parents in L2
+  const ProbDesc& P = A.probs[mp];
+  const int nx = P.ncf[0] + 1, ny = P.ncf[1] + 1, nz = P.ncf[2] + 1;
+  const int ncx = nx - 1, ncy = ny - 1, ncz = nz - 1;
+  const int s = A.s;
+  const int nlx = P.nc[0] + 1, nly = P.nc[1] + 1;
+  const int64_t n = A.n;
+  const int tid = threadIdx.x;
+  const int x = tid % kFX, strip = tid / kFX;
+  const int y0 = strip * kStrip;
+  const bool act = tid < kFThreads && x < nx && y0 < ny;
+
+  extern __shared__ __align__(16) double smem[];
+  double* Ir = smem;                    // [4][49*49] I_p planes (slot = plane & 3), pitch 49
+  double* Kr = Ir + 4 * kFX * kFX;      // [3][48*48] kappa of cell layers (slot = (layer + 3) % 3), 0 outside
+  double* Yp = Kr + 3 * kFC * kFC;      // [49*49] A_1 I_p on the current plane
+  double* Yx = Yp + kFX * kFX;          // [ny][nlx]
+  double* La = Yx + kFX * 25;           // [2][nly * nlx]
+  double* cb = La + 2 * 25 * 25;        // [kFThreads][3][N] constraint partials
+  double* cs = cb + kFThreads * 3 * N;  // [27][N] constraint sums
+  uint8_t* Dr = reinterpret_cast<uint8_t*>(cs + 27 * N);  // [3][48*48] ids of cell layers
+  for (int i = tid; i < 4 * kFX * kFX; i += blockDim.x) Ir[i] = 0.0;
+  for (int i = tid; i < 3 * kFC * kFC; i += blockDim.x) Kr[i] = 0.0;
+  for (int i = tid; i < 2 * 25 * 25; i += blockDim.x) La[i] = 0.0;
+  for (int i = tid; i < 27 * N; i += blockDim.x) cs[i] = 0.0;
+
+  // parents: per thread base of column (x, y0) at plane 0, and strides
+  const int npar = P.npar;
+  const double* pb[MCH_MAXPAR];
+  int psy[MCH_MAXPAR], psz[MCH_MAXPAR];
+  double pw[MCH_MAXPAR];
+#pragma unroll
+  for (int t = 0; t < MCH_MAXPAR; t++) {
+    pb[t] = A.pool;
+    psy[t] = psz[t] = 0;
+    pw[t] = 0.0;
+    if (t < npar) {
+      const int px = P.par_ncf[t][0] + 1, py = P.par_ncf[t][1] + 1, pz = P.par_ncf[t][2] + 1;
+      const int xt = P.lo[0] + x + (P.par_k[t][0] - P.k[0]) * A.c - P.par_lo[t][0];
+      const int yt = P.lo[1] + y0 + (P.par_k[t][1] - P.k[1]) * A.c - P.par_lo[t][1];
+      const int zt = P.lo[2] + (P.par_k[t][2] - P.k[2]) * A.c - P.par_lo[t][2];
+      psy[t] = px;
+      psz[t] = px * py;
+      pb[t] = A.pool + P.par_pool[t] + (int64_t)r * px * py * pz + ((int64_t)zt * py + yt) * px + xt;
+      pw[t] = P.par_w[t];
+    }
+  }
+  // global cell (x-1, y-1, z-1) of the window
+  const int64_t cbase = ((int64_t)(P.lo[2] - 1) * n + (P.lo[1] - 1)) * n + (P.lo[0] - 1);
+  // stage I_p on plane p (all parents' loads of the strip in flight together)
+  auto stage_I = [&](int p) {
+    if (!act || p >= nz) return;
+    double* dst = Ir + (p & 3) * kFX * kFX;
+    double v[kStrip];
+#pragma unroll
+    for (int i = 0; i < kStrip; i++) v[i] = 0.0;
+#pragma unroll
+    for (int t = 0; t < MCH_MAXPAR; t++) {
+      if (t >= npar) break;
+      const double* src = pb[t] + (int64_t)p * psz[t];
+#pragma unroll
+      for (int i = 0; i < kStrip; i++)
+        if (y0 + i < ny) v[i] += pw[t] * __ldg(src + (int64_t)i * psy[t]);
+    }
+#pragma unroll
+    for (int i = 0; i < kStrip; i++)
+      if (y0 + i < ny) dst[(y0 + i) * kFX + x] = v[i];
+  };
+  // stage kappa and ids of cell layer cz (0 / 0xFF outside the window)
+  auto stage_K = [&](int cz) {
+    if (!act || x >= ncx) return;
+    double* kd = Kr + ((cz + 3) % 3) * kFC * kFC;
+    uint8_t* dd = Dr + ((cz + 3) % 3) * kFC * kFC;
+    const bool zin = cz >= 0 && cz < ncz;
+    const int64_t g0 = cbase + ((int64_t)(cz + 1) * n + (y0 + 1)) * n + (x + 1);
+#pragma unroll
+    for (int i = 0; i < kStrip; i++) {
+      const int y = y0 + i;
+      if (y >= ncy) break;
+      const bool ok = zin;
+      kd[y * kFC + x] = ok ? __ldg(A.kappa + g0 + (int64_t)i * n) : 0.0;
+      dd[y * kFC + x] = ok ? __ldg(A.ids + g0 + (int64_t)i * n) : (uint8_t)0xFF;
+    }
+  };
+
+  // constraint partials: cell column x (subcell slot kx); the 7 rows of a strip lie in at most three
+  // subcell rows ky0 + a (host: at least 4 fine cells per H)
+  const int kx = (act && x < ncx) ? slot_f(A, P, 0, x) : -1;
+  const int ky0 = (act && y0 < ncy) ? slot_f(A, P, 1, y0) : -1;
+  int kya[kStrip];
+#pragma unroll
+  for (int i = 0; i < kStrip; i++) kya[i] = (act && y0 + i < ncy) ? slot_f(A, P, 1, y0 + i) - ky0 : -1;
+  double acc[3][N];
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+#pragma unroll
+    for (int j = 0; j < N; j++) acc[a][j] = 0.0;
+  auto flush = [&](int kz) {
+    double* mine = cb + tid * 3 * N;
+    if (tid < kFThreads) {
+#pragma unroll
+      for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          mine[a * N + j] = acc[a][j];
+          acc[a][j] = 0.0;
+        }
+    }
+    __syncthreads();
+    // target (qy, qx, j) of layer kz: one warp each, fixed order over the threads
+    const int lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    for (int tg = warp; tg < 9 * N; tg += nwarp) {
+      const int j = tg % N, q2 = tg / N, qy = q2 / 3, qx = q2 % 3;
+      double sum = 0.0;
+      for (int u = lane; u < kFThreads; u += 32) {
+        const int ux = u % kFX, ust = u / kFX, uy0 = ust * kStrip;
+        if (ux >= ncx || uy0 >= ncy || slot_f(A, P, 0, ux) != qx) continue;
+        const int a = qy - slot_f(A, P, 1, uy0);
+        if (a >= 0 && a < 3) sum += cb[(u * 3 + a) * N + j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULLMASK, sum, o);
+      if (lane == 0) cs[((kz * 3 + qy) * 3 + qx) * N + j] += sum;
+    }
+    __syncthreads();
+  };
+
+  __syncthreads();
+  stage_I(0);
+  stage_I(1);
+  stage_K(0);
+  __syncthreads();
+  const double kh = A.h * (1.0 / 12.0);
+  const double inv_s = 1.0 / (double)s;
+  double* bvec = A.B + P.vec_off + (int64_t)r * nlx * nly * (P.nc[2] + 1);
+  for (int z = 0; z < nz; z++) {
+    // stage plane z+2 and cell layer z+1 (slots not read in this iteration) while the stencil of
+    // plane z runs: no barrier between the two
+    stage_I(z + 2);
+    stage_K(z + 1);
+    if (act) {
+      const double* pl[3] = {Ir + ((z + 3) & 3) * kFX * kFX, Ir + (z & 3) * kFX * kFX, Ir + ((z + 1) & 3) * kFX * kFX};
+      const double* kl[2] = {Kr + ((z + 2) % 3) * kFC * kFC, Kr + (z % 3) * kFC * kFC};  // layers z-1, z
+      const uint8_t* dl = Dr + (z % 3) * kFC * kFC;
+      double v[3][3][3];   // [dz][dy][dx]
+      double kc[2][2][2];  // [oz][oy][ox]
+      auto ld_row = [&](int yy, int slot) {
+#pragma unroll
+        for (int dz = 0; dz < 3; dz++)
+#pragma unroll
+          for (int dx = 0; dx < 3; dx++) {
+            const int xx = x + dx - 1;
+            v[dz][slot][dx] = (yy >= 0 && yy < ny && xx >= 0 && xx < nx) ? pl[dz][yy * kFX + xx] : 0.0;
+          }
+      };
+      auto ld_kap = [&](int cy, int slot) {  // cells of row cy, columns x-1, x; layers z-1, z
+#pragma unroll
+        for (int oz = 0; oz < 2; oz++)
+#pragma unroll
+          for (int ox = 0; ox < 2; ox++) {
+            const int cx = x - 1 + ox;
+            kc[oz][slot][ox] = (cx >= 0 && cx < ncx && cy >= 0 && cy < ncy) ? kl[oz][cy * kFC + cx] : 0.0;
+          }
+      };
+      ld_row(y0 - 1, 0);
+      ld_row(y0, 1);
+      ld_kap(y0 - 1, 0);
+      const bool cl = kx >= 0 && z < ncz;  // this column has cells in layer z
+#pragma unroll
+      for (int i = 0; i < kStrip; i++) {
+        const int y = y0 + i;
+        if (y >= ny) break;
+        ld_row(y + 1, 2);
+        ld_kap(y, 1);
+        double Ap = 0.0;
+#pragma unroll
+        for (int o = 0; o < 8; o++) {
+          const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+          const int a = (~o) & 7;
+          auto vb = [&](int b) { return v[oz + ((b >> 2) & 1)][oy + ((b >> 1) & 1)][ox + (b & 1)]; };
+          Ap += kc[oz][oy][ox] * (4.0 * vb(a) - vb(a ^ 3) - vb(a ^ 5) - vb(a ^ 6) - vb(a ^ 7));
+        }
+        Yp[y * kFX + x] = Ap * kh;
+        // cell (x, y, z): corners on planes z, z+1, rows y, y+1, columns x, x+1
+        if (cl && y < ncy) {
+          const double sig = v[1][1][1] + v[1][1][2] + v[1][2][1] + v[1][2][2] + v[2][1][1] + v[2][1][2] +
+                             v[2][2][1] + v[2][2][2];
+          const int id = dl[y * kFC + x];
+          const int a = kya[i];
+#pragma unroll
+          for (int aa = 0; aa < 3; aa++)
+#pragma unroll
+            for (int j = 0; j < N; j++)
+              if (aa == a && id == j) acc[aa][j] += sig;
+        }
+#pragma unroll
+        for (int dz = 0; dz < 3; dz++)
+#pragma unroll
+          for (int dx = 0; dx < 3; dx++) {
+            v[dz][0][dx] = v[dz][1][dx];
+            v[dz][1][dx] = v[dz][2][dx];
+          }
+#pragma unroll
+        for (int oz = 0; oz < 2; oz++)
+#pragma unroll
+          for (int ox = 0; ox < 2; ox++) kc[oz][0][ox] = kc[oz][1][ox];
+      }
+    }
+    // constraint layer complete after cell layer z?
+    if (z < ncz) {
+      const int kz = slot_f(A, P, 2, z);
+      if (z + 1 == ncz || slot_f(A, P, 2, z + 1) != kz) flush(kz);
+    }
+    __syncthreads();  // Y plane complete; staged plane z+2 / layer z+1 visible from here on
+    // x restriction: Yx[y][X] = sum_d (1 - |d|/s) Y[y][X s + d]
+    for (int u = tid; u < ny * nlx; u += blockDim.x) {
+      const int y = u / nlx, X = u - y * nlx, c0 = X * s;
+      const double* row = Yp + y * kFX;
+      double a = row[c0];
+      for (int d = 1; d < s; d++) {
+        const double w = 1.0 - d * inv_s;
+        if (c0 - d >= 0) a += w * row[c0 - d];
+        if (c0 + d < nx) a += w * row[c0 + d];
+      }
+      Yx[y * nlx + X] = a;
+    }
+    __syncthreads();
+    // y restriction and z accumulation into the level planes; complete planes go to b
+    const int Z0 = z / s, rem = z - Z0 * s;
+    for (int u = tid; u < nly * nlx; u += blockDim.x) {
+      const int Yl = u / nlx, X = u - Yl * nlx, c0 = Yl * s;
+      double a = Yx[c0 * nlx + X];
+      for (int d = 1; d < s; d++) {
+        const double w = 1.0 - d * inv_s;
+        if (c0 - d >= 0) a += w * Yx[(c0 - d) * nlx + X];
+        if (c0 + d < ny) a += w * Yx[(c0 + d) * nlx + X];
+      }
+      double* L0 = La + (Z0 & 1) * nly * nlx;
+      L0[u] += (rem == 0) ? a : (1.0 - rem * inv_s) * a;
+      if (rem > 0) La[((Z0 + 1) & 1) * nly * nlx + u] += rem * inv_s * a;
+      if (rem == s - 1 || z == nz - 1) {
+        bvec[((int64_t)Z0 * nly + Yl) * nlx + X] = -L0[u];
+        L0[u] = 0.0;
+      }
+    }
+  }
+  __syncthreads();
+  const double hq = 0.125 * A.h * A.h * A.h;
+  for (int i = tid; i < 27 * N; i += blockDim.x) {
+    const int64_t gi = ((int64_t)mp * A.ncon + i) * A.n_rhs + r;
+    A.g[gi] = A.g0[gi] - cs[i] * hq;
+  }
+}
+
+cudaError_t launch_fine3d_transport(const LevelArgs& A, cudaStream_t st) {
+  if (A.ncon != 27 * A.N) return cudaErrorInvalidValue;
+  const size_t smem = fine3d_transport_smem(A.N);
+  auto go = [&](auto k) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)(A.nprob_mp * A.n_rhs), kFBlock, smem, st>>>(A);
+    return cudaGetLastError();
+  };
+  switch (A.N) {
+    case 1: return go(k_fine3d_transport<1>);
+    case 2: return go(k_fine3d_transport<2>);
+    case 3: return go(k_fine3d_transport<3>);
+    case 4: return go(k_fine3d_transport<4>);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------------------------------
+// phi_p = P_n xi + I_p (Eq. 11) for all right-hand sides of a macropoint: on the K_p node box
+// into FK (read by k_gram for Eq. 7), and on the whole window into the parent pool if p is
+// stored (parents of later levels, or keep_all).  I_p is formed again from the parents (the
+// transport kept it on chip); per value the arithmetic is k_combine's.
+__global__ void __launch_bounds__(256) k_fine3d_combine(LevelArgs A) {
+  const int mp = blockIdx.y;
+  const ProbDesc& P = A.probs[mp];
+  const Geo<3> gf = fine_geo<3>(P);
+  const Geo<3> gl = level_geo<3>(A, P);
+  const int s = A.s, nr = A.n_rhs;
+  const int64_t nnf = gf.nnodes, nnl = gl.nnodes;
+  int klo[3], kn[3];
+  for (int i = 0; i < 3; i++) {
+    klo[i] = P.kp_lo[i] - P.lo[i];
+    kn[i] = P.kp_hi[i] - P.kp_lo[i] + 1;
+  }
+  const int nkp = kn[0] * kn[1] * kn[2];
+  const bool full = P.pool_off >= 0;
+  const int cnt = full ? (int)nnf : nkp;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cnt) return;
+  int xf[3];
+  if (full) {
+    node_xyz<3>(gf, k, xf);
+  } else {
+    const int zz = k / (kn[0] * kn[1]), t = k - zz * kn[0] * kn[1], yy = t / kn[0];
+    xf[0] = klo[0] + t - yy * kn[0];
+    xf[1] = klo[1] + yy;
+    xf[2] = klo[2] + zz;
+  }
+  const int kf = node_id<3>(gf, xf);
+  // K_p box index (-1 outside)
+  int kk = -1;
+  {
+    const int a = xf[0] - klo[0], b = xf[1] - klo[1], c = xf[2] - klo[2];
+    if (a >= 0 && a < kn[0] && b >= 0 && b < kn[1] && c >= 0 && c < kn[2]) kk = (c * kn[1] + b) * kn[0] + a;
+  }
+  int c0[3];
+  double t[3];
+  for (int i = 0; i < 3; i++) {
+    c0[i] = xf[i] / s;
+    t[i] = (double)(xf[i] - c0[i] * s) / s;
+    if (c0[i] == gl.nc[i]) { c0[i] -= 1; t[i] = 1.0; }
+  }
+  double wgt[8];
+  int nid[8];
+#pragma unroll
+  for (int a = 0; a < 8; a++) {
+    double w = 1.0;
+    int xc[3];
+    for (int i = 0; i < 3; i++) {
+      const int ai = (a >> i) & 1;
+      w *= ai ? t[i] : 1.0 - t[i];
+      xc[i] = c0[i] + ai;
+    }
+    wgt[a] = w;
+    nid[a] = node_id<3>(gl, xc);
+  }
+  int64_t pidx[MCH_MAXPAR], pn[MCH_MAXPAR];
+#pragma unroll
+  for (int q = 0; q < MCH_MAXPAR; q++) {
+    pidx[q] = 0;
+    pn[q] = 0;
+    if (q >= P.npar) continue;
+    int64_t idx = 0;
+    for (int i = 2; i >= 0; i--) {
+      const int xt = P.lo[i] + xf[i] + (P.par_k[q][i] - P.k[i]) * A.c - P.par_lo[q][i];
+      idx = idx * (P.par_ncf[q][i] + 1) + xt;
+    }
+    pidx[q] = idx;
+    pn[q] = (int64_t)(P.par_ncf[q][0] + 1) * (P.par_ncf[q][1] + 1) * (P.par_ncf[q][2] + 1);
+  }
+  for (int r = 0; r < nr; r++) {
+    double I = 0.0;
+#pragma unroll
+    for (int q = 0; q < MCH_MAXPAR; q++)
+      if (q < P.npar) I += P.par_w[q] * __ldg(A.pool + P.par_pool[q] + (int64_t)r * pn[q] + pidx[q]);
+    const double* xi = A.X + P.vec_off + (int64_t)r * nnl;
+    double v = 0.0;
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+      if (wgt[a] != 0.0) v += wgt[a] * xi[nid[a]];
+    const double phi = I + v;
+    if (kk >= 0) A.FK[((int64_t)mp * nr + r) * A.nkp_max + kk] = phi;
+    if (full) A.pool[P.pool_off + (int64_t)r * nnf + kf] = phi;
+  }
+}
+
+cudaError_t launch_fine3d_combine(const LevelArgs& A, int max_fine_nodes, cudaStream_t st) {
+  dim3 grid((unsigned)((max_fine_nodes + 255) / 256), (unsigned)A.nprob_mp);
+  k_fine3d_combine<<<grid, 256, 0, st>>>(A);
+  return cudaGetLastError();
+}

@@ -1772,9 +1772,16 @@ __global__ void k_gram(LevelArgs A) {
     ext[i] = P.kp_hi[i] - P.kp_lo[i];
   }
   const int cnt = ext[0] * ext[1] * ext[2];
+  // fused 3D path (fine3d.cu): phi on the K_p node box in FK
+  const bool kpl = (D == 3) && A.level >= 2 && A.FK != nullptr;
+  const int kn0 = ext[0] + 1, kn1 = ext[1] + 1;
   auto field = [&](int rr) -> const double* {
     if (A.level == 1) return A.X + P.vec_off + (int64_t)rr * gf.nnodes;
+    if (kpl) return A.FK + ((int64_t)mp * nr + rr) * A.nkp_max;
     return A.FI + P.fine_off + (int64_t)rr * gf.nnodes;
+  };
+  auto nodeid = [&](const int* xb) {
+    return kpl ? ((xb[2] - lo[2]) * kn1 + (xb[1] - lo[1])) * kn0 + (xb[0] - lo[0]) : node_id<D>(gf, xb);
   };
   double* Gout = A.G + P.lin * nr * nr;
   for (int a = 0; a < nr; a++) {
@@ -1789,7 +1796,7 @@ __global__ void k_gram(LevelArgs A) {
       double ca[1 << D];
       for (int bb = 0; bb < (1 << D); bb++) {
         int xb[3] = {e[0] + (bb & 1), e[1] + ((bb >> 1) & 1), (D == 3) ? e[2] + ((bb >> 2) & 1) : 0};
-        nid[bb] = node_id<D>(gf, xb);
+        nid[bb] = nodeid(xb);
         ca[bb] = fa[nid[bb]];
       }
       // K_E phi_a (all corners), then dot with phi_b
@@ -1827,7 +1834,7 @@ __global__ void k_gram(LevelArgs A) {
       double s = 0.0;
       for (int bb = 0; bb < (1 << D); bb++) {
         int xb[3] = {e[0] + (bb & 1), e[1] + ((bb >> 1) & 1), (D == 3) ? e[2] + ((bb >> 2) & 1) : 0};
-        s += fj[node_id<D>(gf, xb)];
+        s += fj[nodeid(xb)];
       }
       v[j] += fe * s;
     }

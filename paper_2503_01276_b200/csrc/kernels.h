@@ -37,6 +37,9 @@ cudaError_t launch_node_ops3d(const LevelArgs& A, int max_nodes, cudaStream_t st
 cudaError_t launch_pcg3d(const LevelArgs& A, int nxm, cudaStream_t st);
 // level 1 (windows of <= 49 fine nodes per side)
 size_t pcg3d_l1_smem(int N);
+// windows of <= 7 level nodes per side, N <= 2: one CTA per macropoint, one warp per rhs
+size_t pcg3d_w7_smem(int N);
+cudaError_t launch_pcg3d_w7(const LevelArgs& A, cudaStream_t st);
 cudaError_t launch_pcg3d_l1(const LevelArgs& A, cudaStream_t st);
 
 // validation workload (fine.cu, NEXT-3): global fine reference solve of Eq. (2), block averages
@@ -56,3 +59,9 @@ size_t pcg_smem(const LevelArgs& A);
 size_t proj_setup_band_smem(const LevelArgs& A);
 // two-level preconditioner setup (generic k_pcg, level 1)
 cudaError_t launch_coarse_setup(const LevelArgs& A, cudaStream_t st);
+
+// fused 3D fine-window passes at levels >= 2 (fine3d.cu): transport + A_1 I_p + C_1 I_p +
+// restriction in one kernel; combine on K_p (and the whole window for stored parents)
+size_t fine3d_transport_smem(int N);
+cudaError_t launch_fine3d_transport(const LevelArgs& A, cudaStream_t st);
+cudaError_t launch_fine3d_combine(const LevelArgs& A, int max_fine_nodes, cudaStream_t st);

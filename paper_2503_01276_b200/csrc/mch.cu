@@ -90,6 +90,9 @@ struct LevelBatch {
   bool on3d = false;  // on-chip 3D PCG (pcg3d.cu), levels >= 2
   bool coarse = false;  // two-level preconditioner at level 1 (generic k_pcg or k_pcg2d level-1 variant)
   bool crs2d = false;   // the on-chip 2D variant was planned with the coarse space (shared memory, TMEM)
+  bool fused3 = false;  // 3D level >= 2: fused fine passes (fine3d.cu), no FI/FY workspace
+  int max_kp = 0;       // K_p node-box size (FK slot) of the fused path
+  bool w7 = false;      // 3D level >= 2, <= 7 level nodes per side: block PCG, one warp per rhs (k_pcg3d_w7)
   bool tsplit = false;  // 3D transport through k_pcg3d_l1<MODE 1> (fine windows <= 49 nodes per side)
   int nxm3 = 0;
   int variant = -1, threads2 = 0, maxseg = 0, tm_cols = 32;
@@ -128,7 +131,7 @@ struct mch_ctx {
   std::vector<mch_level_stats> stats;
   std::string err;
   // grow-only scratch
-  DevBuf STC, MLR, pinv_ds, W, Mc, g0, g, meas, cm, flags, dinv, nwt, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
+  DevBuf FK, STC, MLR, pinv_ds, W, Mc, g0, g, meas, cm, flags, dinv, nwt, Sinv, X, R, P, Q, B, FI, FY, iters, relres, diag;
   cudaEvent_t ev[8];
   bool events = false;
   std::vector<std::vector<std::unique_ptr<LevelBatch>>> lplans;  // per level, built on first solve
@@ -142,7 +145,7 @@ struct mch_ctx {
   bool coarse = false;
   DevAlloc al;
   std::vector<DevBuf*> bufs() {
-    return {&STC, &MLR, &pinv_ds, &W, &Mc, &g0, &g, &meas, &cm, &flags, &dinv, &nwt, &Sinv, &X, &R, &P, &Q, &B,
+    return {&FK, &STC, &MLR, &pinv_ds, &W, &Mc, &g0, &g, &meas, &cm, &flags, &dinv, &nwt, &Sinv, &X, &R, &P, &Q, &B,
             &FI, &FY, &iters, &relres, &diag, &fsrc, &bload, &mws, &mG, &mb, &mU, &mres, &fws, &fbar, &ff, &fu,
             &fkbox, &fout, &cmap, &ncomp, &cbox, &einv, &cz, &cptr, &clist, &azp, &azi, &azw};
   }
@@ -371,6 +374,13 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     }
     std::stable_sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) { return key[a] > key[b]; });
   }
+  // fused 3D fine passes (fine3d.cu) at levels >= 2: 3x3x3 subcells, windows of <= 49 fine nodes
+  // per side, >= 4 fine cells per H (a thread's 7-row strip spans <= 3 subcell rows)
+  const char* f3e = getenv("MCH_FINE3D");
+  const bool fused3_lvl = D == 3 && level >= 2 && nc == 27 * N && c->l == 1 && pl.c >= 4 && 3 * pl.c + 1 <= 49 &&
+                          fine3d_transport_smem(N) <= 232448 && !(f3e && atoi(f3e) == 0) &&
+                          getenv("MCH_TRANSPORT_GENERIC") == nullptr;
+  const double kpn = (double)(pl.c + 1) * (pl.c + 1) * (pl.c + 1);
   size_t freeb = 0, totb = 0;
   cudaMemGetInfo(&freeb, &totb);
   const double budget = std::min<double>(48e9, 0.5 * (double)freeb);
@@ -382,7 +392,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       int64_t ln, fnn, lc;
       sizes(pl.all[mine[bend]], ln, fnn, lc);
       double b = 8.0 * (5.0 * nr * ln + ln * (10.0 + 4.0 * N) + (double)nc * nc + 3.0 * nc * nr + nc + 12) +
-                 (level >= 2 ? 16.0 * nr * fnn : 0.0);
+                 (level >= 2 ? (fused3_lvl ? 8.0 * nr * kpn : 16.0 * nr * fnn) : 0.0);
       if (bend > bstart && bytes + b > budget) break;
       bytes += b;
       bend++;
@@ -501,12 +511,23 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       for (int i = 0; i < nmp; i++)
         for (int d = 0; d < 3; d++) maxf = std::max(maxf, descs[i].ncf[d] + 1);
       B->tsplit = level >= 2 && maxf <= 49 && pcg3d_l1_smem(N) <= 232448 && getenv("MCH_TRANSPORT_GENERIC") == nullptr;
+      B->fused3 = fused3_lvl && maxf <= 49;
+      if (B->fused3) {
+        for (int i = 0; i < nmp; i++) {
+          int kp = 1;
+          for (int d = 0; d < 3; d++) kp *= descs[i].kp_hi[d] - descs[i].kp_lo[d] + 1;
+          B->max_kp = std::max(B->max_kp, kp);
+        }
+      }
       if (level >= 2) {
         const int nxm = pcg3d_nxm(maxn);
         if (nxm > 0 && pcg3d_smem(N, nxm) <= 232448) {
           B->on3d = true;
           B->nxm3 = nxm;
         }
+        const char* w7e = getenv("MCH_PCG3D_W7");
+        B->w7 = B->on3d && nxm == 7 && N <= 2 && nr == 4 * N && pcg3d_w7_smem(N) <= 232448 &&
+                !(w7e && atoi(w7e) == 0);
       } else if (maxn <= 49 && pcg3d_l1_smem(N) <= 232448) {
         B->on3d = true;
         B->nxm3 = 49;
@@ -533,8 +554,12 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     }
     if (level >= 2) {
       CKC(c, c->B.ensure(sizeof(double) * B->vec_off));
-      CKC(c, c->FI.ensure(sizeof(double) * B->fine_off));
-      CKC(c, c->FY.ensure(sizeof(double) * B->fine_off));
+      if (B->fused3) {
+        CKC(c, c->FK.ensure(sizeof(double) * (size_t)nmp * nr * B->max_kp));
+      } else {
+        CKC(c, c->FI.ensure(sizeof(double) * B->fine_off));
+        CKC(c, c->FY.ensure(sizeof(double) * B->fine_off));
+      }
     }
     if (B->on2d && !B->l1op) {
       CKC(c, c->STC.ensure(sizeof(double) * 9 * B->node_off));
@@ -641,7 +666,11 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     cudaEventRecord(B.ev[0], st);
     S.launches += (level >= 2) ? 6 : 4;
     CKC(c, launch_targets(A, st));
-    if (level >= 2 && B.tsplit) {  // 3D: I_p, then the column-walking apply, then P_n^T
+    A.FK = B.fused3 ? c->FK.as<double>() : nullptr;
+    A.nkp_max = B.max_kp;
+    if (level >= 2 && B.fused3) {  // 3D: I_p, A_1 I_p, C_1 I_p and P_n^T in one pass (fine3d.cu)
+      CKC(c, launch_fine3d_transport(A, st));
+    } else if (level >= 2 && B.tsplit) {  // 3D: I_p, then the column-walking apply, then P_n^T
       A.tphase = 1;
       CKC(c, launch_transport(A, B.th_f, st));
       CKC(c, launch_tapply3d(A, st));
@@ -700,6 +729,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     }
     if (B.on2d) CKC(c, launch_pcg2d(A, B.variant, B.threads2, st));
     else if (B.on3d && level == 1) CKC(c, launch_pcg3d_l1(A, st));
+    else if (B.w7) CKC(c, launch_pcg3d_w7(A, st));
     else if (B.on3d) CKC(c, launch_pcg3d(A, B.nxm3, st));
     else CKC(c, launch_pcg(A, B.th_l, st));
     if (dbgp) {
@@ -717,7 +747,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       snprintf(tag, sizeof tag, "level %d variant %d", level, B.variant);
       pcg2d_phase_dump(tag);
     }
-    if (level >= 2) CKC(c, launch_combine(A, B.th_f, st));
+    if (level >= 2 && B.fused3) CKC(c, launch_fine3d_combine(A, B.max_fn, st));
+    else if (level >= 2) CKC(c, launch_combine(A, B.th_f, st));
     CKC(c, launch_gram(A, 256, st));
     cudaEventRecord(B.ev[3], st);
     CKC(c, cudaMemcpyAsync(B.h_flags, c->flags.ptr, sizeof(int) * nmp, cudaMemcpyDeviceToHost, st));

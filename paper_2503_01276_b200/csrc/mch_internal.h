@@ -57,6 +57,8 @@ struct LevelArgs {
   // per-problem vectors (problem = mp*n_rhs + r)
   double* X; double* R; double* P; double* Q; double* B;
   double* FI; double* FY;  // fine workspace (levels >= 2): I_p / phi and A1 I_p
+  double* FK;              // fused 3D path (fine3d.cu): phi_p on the K_p node box, [mp][n_rhs][nkp_max]
+  int nkp_max;             // K_p box nodes per (macropoint, rhs) slot of FK
   double* pool;            // parent pool
   double* G;               // [(M+1)^D][n_rhs][n_rhs]
   int band;                // 0: dense S^-1 per macropoint; > 0: banded Cholesky factor of the

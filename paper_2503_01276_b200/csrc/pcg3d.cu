@@ -1173,6 +1173,337 @@ cudaError_t launch_tapply3d(const LevelArgs& A, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Small 3D windows (<= 7 level nodes per side: config 5 level 4), block form of the same method:
+// one CTA per macropoint carries all n_rhs = 4N right-hand sides together, one warp per
+// right-hand side (north_star (c)).  The operator data the right-hand
+// sides share — the 27-point stencil rows of A_n, the octant-merged constraint weights, D^-1 and
+// the projector S^+ — are staged once in shared memory; each warp keeps its x, r, p, q in
+// registers (lane owns nodes lane + 32 i) and its p (zero halo) in shared memory.  Every sum
+// is a warp reduction in a fixed order and no block barrier is taken after the staging, so the
+// right-hand sides iterate independently (each to its own convergence) and the results are
+// bitwise reproducible.  Same iteration as k_pcg3d (init from the full problem's scale, pass A
+// with the re-projection, q = A p, r update, c = C D^-1 r, yhat = S^+ c, restoration).
+constexpr int kW7 = 7;                      // nodes per side
+constexpr int kW7P = kW7 + 2;               // padded p pitch
+constexpr int kW7NN = kW7 * kW7 * kW7;      // 343
+constexpr int kW7KPL = (kW7NN + 31) / 32;   // nodes per lane (11)
+
+template <int N>
+__global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
+  constexpr int NR = 4 * N;   // right-hand sides = warps
+  constexpr int NQ = 27 * N;  // constraint rows
+  constexpr int PP = kW7P * kW7P * kW7P;
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  const int nx = P.nc[0] + 1, ny = P.nc[1] + 1, nz = P.nc[2] + 1, nn = nx * ny * nz;
+  const int lane = threadIdx.x & 31, rhs = threadIdx.x >> 5;
+
+  extern __shared__ __align__(16) double smem[];
+  double* st_s = smem;                  // [27][nn] stencil rows
+  double* mw_s = st_s + 27 * kW7NN;     // [8N][nn] octant-merged constraint weights
+  double* dg_s = mw_s + 8 * N * kW7NN;  // [nn] D^-1
+  double* si_s = dg_s + kW7NN;          // [NQ][NQ] S^+ transposed: si_s[j*NQ + i] = S^+_ij
+  double* p_all = si_s + NQ * NQ;       // [NR][PP] p with zero halo (also D^-1 r / x for C u)
+  double* c_all = p_all + NR * PP;      // [NR][NQ]
+  double* y_all = c_all + NR * NQ;      // [NR][NQ]
+  int* sd_s = reinterpret_cast<int*>(y_all + NR * NQ);  // [3][7] sides packed pm | k0 << 4 | k1 << 8
+  int* rg_s = sd_s + 3 * kW7;                             // [3][3] node range of subcell coordinate: lo | hi << 8
+
+  {
+    const double* S27 = A.STC + P.node_off * 27;
+    for (int i = threadIdx.x; i < 27 * nn; i += blockDim.x) st_s[i] = __ldg(S27 + i);
+    const double* MW = A.MLR + P.node_off * 8 * N;
+    for (int i = threadIdx.x; i < 8 * N * nn; i += blockDim.x) mw_s[i] = __ldg(MW + i);
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) dg_s[i] = __ldg(A.dinv + P.node_off + i);
+    const double* Si = A.Sinv + (int64_t)mp * NQ * NQ;
+    for (int i = threadIdx.x; i < NQ * NQ; i += blockDim.x) {
+      const int r = i / NQ, c = i - r * NQ;
+      si_s[c * NQ + r] = __ldg(Si + i);
+    }
+    for (int i = threadIdx.x; i < NR * PP; i += blockDim.x) p_all[i] = 0.0;
+    if (threadIdx.x < 3 * kW7) {
+      const int d = threadIdx.x / kW7, X = threadIdx.x - d * kW7;
+      const int ncd = P.nc[d];
+      if (X <= ncd) {
+        const Sides s = sides_of(A, P, d, X, ncd);
+        sd_s[threadIdx.x] = s.pm | (s.k0 << 4) | (s.k1 << 8);
+      } else {
+        sd_s[threadIdx.x] = 0;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+      const int d = threadIdx.x / 3, q = threadIdx.x - d * 3;
+      int lo = 99, hi = -1;
+      for (int X = 0; X <= P.nc[d]; X++) {
+        const int v = sd_s[d * kW7 + X], pm = v & 15, k0 = (v >> 4) & 15, k1 = (v >> 8) & 15;
+        if (((pm & 1) && k0 == q) || ((pm & 2) && k1 == q)) {
+          lo = min(lo, X);
+          hi = max(hi, X);
+        }
+      }
+      rg_s[threadIdx.x] = (hi >= lo) ? (lo | (hi << 8)) : (1 | (0 << 8));  // empty: lo > hi
+    }
+    __syncthreads();
+  }
+  double* p_s = p_all + rhs * PP;
+  double* c_s = c_all + rhs * NQ;
+  double* y_s = y_all + rhs * NQ;
+
+  // owned nodes: k = lane + 32 i
+  int pix[kW7KPL];  // padded index of the node, -1 if absent
+  int nxy[kW7KPL];  // x | y << 4 | z << 8
+#pragma unroll
+  for (int i = 0; i < kW7KPL; i++) {
+    const int k = lane + 32 * i;
+    if (k < nn) {
+      const int z = k / (nx * ny), t = k - z * nx * ny, y = t / nx, x = t - y * nx;
+      pix[i] = ((z + 1) * kW7P + (y + 1)) * kW7P + (x + 1);
+      nxy[i] = x | (y << 4) | (z << 8);
+    } else {
+      pix[i] = -1;
+      nxy[i] = 0;
+    }
+  }
+  auto wsum = [](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    return v;
+  };
+  // (C^T yhat)_k over the present octants
+  auto ct_at = [&](int i) -> double {
+    const int k = lane + 32 * i;
+    const int v = nxy[i];
+    const int sx = sd_s[v & 15], sy = sd_s[kW7 + ((v >> 4) & 15)], sz = sd_s[2 * kW7 + (v >> 8)];
+    double ct = 0.0;
+#pragma unroll
+    for (int zs = 0; zs < 2; zs++) {
+      if (!((sz >> zs) & 1)) continue;
+      const int kz = (sz >> (4 + 4 * zs)) & 15;
+#pragma unroll
+      for (int ys = 0; ys < 2; ys++) {
+        if (!((sy >> ys) & 1)) continue;
+        const int ky = (sy >> (4 + 4 * ys)) & 15;
+#pragma unroll
+        for (int xs = 0; xs < 2; xs++) {
+          if (!((sx >> xs) & 1)) continue;
+          const int kx = (sx >> (4 + 4 * xs)) & 15;
+          const int o = xs + 2 * ys + 4 * zs;
+          const double* yq = y_s + ((kz * 3 + ky) * 3 + kx) * N;
+#pragma unroll
+          for (int j = 0; j < N; j++) ct += mw_s[(o * N + j) * nn + k] * yq[j];
+        }
+      }
+    }
+    return ct;
+  };
+  // c = C u with u in p_s (interior), rows over lanes; call after __syncwarp, ends with one
+  auto cmul = [&]() {
+    for (int row = lane; row < NQ; row += 32) {
+      const int q = row / N, j = row - q * N;
+      const int qz = q / 9, qy = (q / 3) % 3, qx = q % 3;
+      const int rx = rg_s[qx], ry = rg_s[3 + qy], rz = rg_s[6 + qz];
+      double s = 0.0;
+      for (int Z = rz & 255; Z <= (rz >> 8); Z++) {
+        const int vz = sd_s[2 * kW7 + Z];
+        const int bz = (((vz & 1) && ((vz >> 4) & 15) == qz) ? 0 : 1);
+        for (int Y = ry & 255; Y <= (ry >> 8); Y++) {
+          const int vy = sd_s[kW7 + Y];
+          const int by = (((vy & 1) && ((vy >> 4) & 15) == qy) ? 0 : 1);
+          for (int X = rx & 255; X <= (rx >> 8); X++) {
+            const int vx = sd_s[X];
+            const int bx = (((vx & 1) && ((vx >> 4) & 15) == qx) ? 0 : 1);
+            const int o = bx + 2 * by + 4 * bz;
+            const int k = (Z * ny + Y) * nx + X;
+            s += mw_s[(o * N + j) * nn + k] * p_s[((Z + 1) * kW7P + (Y + 1)) * kW7P + (X + 1)];
+          }
+        }
+      }
+      c_s[row] = s;
+    }
+    __syncwarp();
+  };
+  // y = S^+ c (rows over lanes); returns c . y (all lanes); ends with __syncwarp
+  auto smul = [&]() -> double {
+    double cy = 0.0;
+    for (int row = lane; row < NQ; row += 32) {
+      double s = 0.0;
+      for (int j = 0; j < NQ; j++) s += si_s[j * NQ + row] * c_s[j];
+      y_s[row] = s;
+      cy += s * c_s[row];
+    }
+    __syncwarp();
+    return wsum(cy);
+  };
+  // q = A p at the owned nodes (p from p_s)
+  auto apply = [&](int i) -> double {
+    const int k = lane + 32 * i;
+    const double* pb = p_s + pix[i];
+    double a = 0.0;
+#pragma unroll
+    for (int dz = -1; dz <= 1; dz++)
+#pragma unroll
+      for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+        for (int dx = -1; dx <= 1; dx++) {
+          const int c = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+          a += st_s[c * nn + k] * pb[(dz * kW7P + dy) * kW7P + dx];
+        }
+    return a;
+  };
+
+  double xr[kW7KPL], rr_[kW7KPL], pr[kW7KPL], qr[kW7KPL];
+#pragma unroll
+  for (int i = 0; i < kW7KPL; i++) xr[i] = rr_[i] = pr[i] = qr[i] = 0.0;
+  const double* bvec = A.B + P.vec_off + (int64_t)rhs * nn;
+  // init: x0 = D^-1 C^T S^+ t, r0 = A x0 - b, c = C D^-1 r0, yhat = S^+ c; returns r0^T D^-1 r0
+  auto init = [&](const double* tcol, const double* bb) -> double {
+    for (int i = lane; i < NQ; i += 32) c_s[i] = tcol[((int64_t)mp * NQ + i) * A.n_rhs + rhs];
+    __syncwarp();
+    smul();
+#pragma unroll
+    for (int i = 0; i < kW7KPL; i++)
+      if (pix[i] >= 0) {
+        const double x0 = dg_s[lane + 32 * i] * ct_at(i);
+        xr[i] = x0;
+        p_s[pix[i]] = x0;
+      }
+    __syncwarp();
+    double rr = 0.0;
+#pragma unroll
+    for (int i = 0; i < kW7KPL; i++)
+      if (pix[i] >= 0) rr_[i] = apply(i) - (bb ? bb[lane + 32 * i] : 0.0);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < kW7KPL; i++)
+      if (pix[i] >= 0) {
+        const double u = dg_s[lane + 32 * i] * rr_[i];
+        rr += rr_[i] * u;
+        p_s[pix[i]] = u;
+      }
+    __syncwarp();
+    cmul();
+    smul();
+    return wsum(rr);
+  };
+
+  const double rr_ref = init(A.g0, nullptr);
+  double rz_ref = 0.0;
+#pragma unroll
+  for (int i = 0; i < kW7KPL; i++)
+    if (pix[i] >= 0) {
+      const double w = rr_[i] - ct_at(i);
+      rz_ref += dg_s[lane + 32 * i] * w * w;
+    }
+  rz_ref = wsum(rz_ref);
+  const double rr0 = init(A.g, bvec);
+
+  const double tol2 = A.rtol * A.rtol;
+  const double floor2 = 1e-30 * fmax(rr0, rr_ref);
+  double beta = 0.0, rz = 0.0, ref = 0.0, alpha = 0.0;
+  int it = 0, breakdown = 0;
+  for (;; it++) {
+    // pass A: x += alpha_prev p_prev (deferred), r <- r - C^T yhat, z = D^-1 r, p <- -z + beta p
+    double v = 0.0;
+    const bool first = (it == 0);
+#pragma unroll
+    for (int i = 0; i < kW7KPL; i++)
+      if (pix[i] >= 0) {
+        const double rk = rr_[i] - ct_at(i);
+        const double zz = dg_s[lane + 32 * i] * rk;
+        const double pold = pr[i];
+        if (!first) xr[i] += alpha * pold;
+        const double pn = first ? -zz : -zz + beta * pold;
+        pr[i] = pn;
+        p_s[pix[i]] = pn;
+        rr_[i] = rk;
+        v += rk * zz;
+      }
+    __syncwarp();
+    // pass B: q = A p, pq
+    double w = 0.0;
+#pragma unroll
+    for (int i = 0; i < kW7KPL; i++)
+      if (pix[i] >= 0) {
+        qr[i] = apply(i);
+        w += pr[i] * qr[i];
+      }
+    rz = wsum(v);
+    const double pq = wsum(w);
+    if (it == 0) ref = fmax(rz, rz_ref);
+    if (!(rz > fmax(tol2 * ref, floor2)) || it >= A.max_iter) break;
+    if (!(pq > 0.0) || !isfinite(pq)) {
+      breakdown = 1;
+      break;
+    }
+    alpha = rz / pq;
+    // pass C: r += alpha q, rr = r^T D^-1 r, u = D^-1 r -> p_s (p itself stays in registers)
+    double rr = 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < kW7KPL; i++)
+      if (pix[i] >= 0) {
+        const double rk = rr_[i] + alpha * qr[i];
+        rr_[i] = rk;
+        const double u = dg_s[lane + 32 * i] * rk;
+        rr += rk * u;
+        p_s[pix[i]] = u;
+      }
+    __syncwarp();
+    cmul();
+    const double cy = smul();
+    beta = (wsum(rr) - cy) / rz;
+  }
+
+  // feasibility restoration: x += D^-1 C^T S^+ (g - C x)
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < kW7KPL; i++)
+    if (pix[i] >= 0) p_s[pix[i]] = xr[i];
+  __syncwarp();
+  cmul();
+  for (int i = lane; i < NQ; i += 32) c_s[i] = A.g[((int64_t)mp * NQ + i) * A.n_rhs + rhs] - c_s[i];
+  __syncwarp();
+  smul();
+  double* Xv = A.X + P.vec_off + (int64_t)rhs * nn;
+#pragma unroll
+  for (int i = 0; i < kW7KPL; i++)
+    if (pix[i] >= 0) Xv[lane + 32 * i] = xr[i] + dg_s[lane + 32 * i] * ct_at(i);
+  if (lane == 0) {
+    const int prob = mp * A.n_rhs + rhs;
+    A.iters[prob] = it;
+    A.relres[prob] = (ref > 0.0) ? sqrt(fmax(rz, 0.0) / ref) : 0.0;
+    double* dgo = A.diag + (int64_t)prob * 4;
+    dgo[0] = rz;
+    dgo[1] = ref;
+    dgo[2] = floor2;
+    dgo[3] = breakdown;
+  }
+}
+
+size_t pcg3d_w7_smem(int N) {
+  const size_t NQ = 27 * (size_t)N, NR = 4 * (size_t)N;
+  const size_t d = 27 * kW7NN + 8 * N * kW7NN + kW7NN + NQ * NQ + NR * kW7P * kW7P * kW7P + 2 * NR * NQ;
+  return d * sizeof(double) + (3 * kW7 + 9) * sizeof(int);
+}
+
+cudaError_t launch_pcg3d_w7(const LevelArgs& A, cudaStream_t st) {
+  const size_t smem = pcg3d_w7_smem(A.N);
+  auto go = [&](auto k, int N) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)A.nprob_mp, 128 * N, smem, st>>>(A);
+    return cudaGetLastError();
+  };
+  if (A.n_rhs != 4 * A.N) return cudaErrorInvalidValue;
+  switch (A.N) {
+    case 1: return go(k_pcg3d_w7<1>, 1);
+    case 2: return go(k_pcg3d_w7<2>, 2);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------------------------------
 size_t pcg3d_smem(int N, int nxm) {
   const size_t d = (size_t)(nxm + 2) * (nxm + 2) * nxm + (size_t)nxm * 27 * N + 2 * 27 * N + 5 * 32 + 512;
   return d * sizeof(double) + (size_t)nxm * 3 * sizeof(int);
