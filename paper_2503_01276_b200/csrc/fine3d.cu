@@ -25,6 +25,8 @@ namespace {
 
 constexpr int kFX = 49;                       // max fine nodes per side
 constexpr int kFC = kFX - 1;                  // max fine cells per side
+constexpr int kIP = kFX + 2;                  // padded I plane pitch (zero halo)
+constexpr int kKP = kFC + 2;                  // padded kappa layer pitch (zero halo)
 constexpr int kStrip = 7;                     // node rows per thread
 constexpr int kFThreads = kFX * kStrip;       // 343 (49 columns x 7 strips)
 constexpr int kFBlock = 352;                  // 11 warps
@@ -38,7 +40,7 @@ __device__ __forceinline__ int slot_f(const LevelArgs& A, const ProbDesc& P, int
 size_t fine3d_transport_smem(int N) {
   // I ring 4 x 49^2, kappa ring 3 x 48^2, ids ring 3 x 48^2 (bytes), Y plane 49^2, Yx 49 x 25,
   // level planes 2 x 25^2, constraint partials, constraint sums
-  const size_t d = 4 * kFX * kFX + 3 * kFC * kFC + kFX * kFX + kFX * 25 + 2 * 25 * 25 + (size_t)kFThreads * 3 * N + 27 * N;
+  const size_t d = 4 * kIP * kIP + 3 * kKP * kKP + kFX * kFX + kFX * 25 + 2 * 25 * 25 + (size_t)kFThreads * 3 * N + 27 * N;
   return d * sizeof(double) + 3 * kFC * kFC;
 }
 
@@ -57,16 +59,16 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
   const bool act = tid < kFThreads && x < nx && y0 < ny;
 
   extern __shared__ __align__(16) double smem[];
-  double* Ir = smem;                    // [4][49*49] I_p planes (slot = plane & 3), pitch 49
-  double* Kr = Ir + 4 * kFX * kFX;      // [3][48*48] kappa of cell layers (slot = (layer + 3) % 3), 0 outside
-  double* Yp = Kr + 3 * kFC * kFC;      // [49*49] A_1 I_p on the current plane
+  double* Ir = smem;                    // [4][51*51] I_p planes (slot = plane & 3), zero halo
+  double* Kr = Ir + 4 * kIP * kIP;      // [3][50*50] kappa of cell layers (slot = (layer + 3) % 3), 0 outside
+  double* Yp = Kr + 3 * kKP * kKP;      // [49*49] A_1 I_p on the current plane
   double* Yx = Yp + kFX * kFX;          // [ny][nlx]
   double* La = Yx + kFX * 25;           // [2][nly * nlx]
   double* cb = La + 2 * 25 * 25;        // [kFThreads][3][N] constraint partials
   double* cs = cb + kFThreads * 3 * N;  // [27][N] constraint sums
   uint8_t* Dr = reinterpret_cast<uint8_t*>(cs + 27 * N);  // [3][48*48] ids of cell layers
-  for (int i = tid; i < 4 * kFX * kFX; i += blockDim.x) Ir[i] = 0.0;
-  for (int i = tid; i < 3 * kFC * kFC; i += blockDim.x) Kr[i] = 0.0;
+  for (int i = tid; i < 4 * kIP * kIP; i += blockDim.x) Ir[i] = 0.0;
+  for (int i = tid; i < 3 * kKP * kKP; i += blockDim.x) Kr[i] = 0.0;
   for (int i = tid; i < 2 * 25 * 25; i += blockDim.x) La[i] = 0.0;
   for (int i = tid; i < 27 * N; i += blockDim.x) cs[i] = 0.0;
 
@@ -96,46 +98,69 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
   // stage I_p on plane p (all parents' loads of the strip in flight together)
   auto stage_I = [&](int p) {
     if (!act || p >= nz) return;
-    double* dst = Ir + (p & 3) * kFX * kFX;
+    double* dst = Ir + (p & 3) * kIP * kIP + (y0 + 1) * kIP + (x + 1);
     double v[kStrip];
 #pragma unroll
     for (int i = 0; i < kStrip; i++) v[i] = 0.0;
+    // parents in groups of four: every load of a group in flight before the first use
 #pragma unroll
-    for (int t = 0; t < MCH_MAXPAR; t++) {
-      if (t >= npar) break;
-      const double* src = pb[t] + (int64_t)p * psz[t];
+    for (int t0 = 0; t0 < MCH_MAXPAR; t0 += 4) {
+      if (t0 >= npar) break;
+      double raw[4][kStrip];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int t = t0 + u;
+        const double* src = pb[t] + (int64_t)p * psz[t];
+#pragma unroll
+        for (int i = 0; i < kStrip; i++) raw[u][i] = (t < npar && y0 + i < ny) ? __ldg(src + (int64_t)i * psy[t]) : 0.0;
+      }
 #pragma unroll
       for (int i = 0; i < kStrip; i++)
-        if (y0 + i < ny) v[i] += pw[t] * __ldg(src + (int64_t)i * psy[t]);
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+          if (t0 + u < npar) v[i] += pw[t0 + u] * raw[u][i];
     }
 #pragma unroll
     for (int i = 0; i < kStrip; i++)
-      if (y0 + i < ny) dst[(y0 + i) * kFX + x] = v[i];
+      if (y0 + i < ny) dst[i * kIP] = v[i];
   };
-  // stage kappa and ids of cell layer cz (0 / 0xFF outside the window)
-  auto stage_K = [&](int cz) {
-    if (!act || x >= ncx) return;
-    double* kd = Kr + ((cz + 3) % 3) * kFC * kFC;
-    uint8_t* dd = Dr + ((cz + 3) % 3) * kFC * kFC;
-    const bool zin = cz >= 0 && cz < ncz;
+  // kappa and ids of cell layer cz (0 / 0xFF outside the window): loads into registers first, the
+  // shared-memory stores after the stencil of the current plane (latency hidden behind it)
+  const bool kact = act && x < ncx;
+  double kreg[kStrip];
+  int dreg[kStrip];
+  auto load_K = [&](int cz) {
+    const bool zin = kact && cz >= 0 && cz < ncz;
     const int64_t g0 = cbase + ((int64_t)(cz + 1) * n + (y0 + 1)) * n + (x + 1);
 #pragma unroll
     for (int i = 0; i < kStrip; i++) {
-      const int y = y0 + i;
-      if (y >= ncy) break;
-      const bool ok = zin;
-      kd[y * kFC + x] = ok ? __ldg(A.kappa + g0 + (int64_t)i * n) : 0.0;
-      dd[y * kFC + x] = ok ? __ldg(A.ids + g0 + (int64_t)i * n) : (uint8_t)0xFF;
+      const bool ok = zin && y0 + i < ncy;
+      kreg[i] = ok ? __ldg(A.kappa + g0 + (int64_t)i * n) : 0.0;
+      dreg[i] = ok ? (int)__ldg(A.ids + g0 + (int64_t)i * n) : 0xFF;
     }
+  };
+  auto store_K = [&](int cz) {
+    if (!kact) return;
+    double* kd = Kr + ((cz + 3) % 3) * kKP * kKP + (y0 + 1) * kKP + (x + 1);
+    uint8_t* dd = Dr + ((cz + 3) % 3) * kFC * kFC + y0 * kFC + x;
+#pragma unroll
+    for (int i = 0; i < kStrip; i++)
+      if (y0 + i < ncy) {
+        kd[i * kKP] = kreg[i];
+        dd[i * kFC] = (uint8_t)dreg[i];
+      }
   };
 
   // constraint partials: cell column x (subcell slot kx); the 7 rows of a strip lie in at most three
-  // subcell rows ky0 + a (host: at least 4 fine cells per H)
+  // subcell rows ky0 + a (host: at least 4 fine cells per H); rows [0, i1) have a = 0, [i1, i2) a = 1
   const int kx = (act && x < ncx) ? slot_f(A, P, 0, x) : -1;
   const int ky0 = (act && y0 < ncy) ? slot_f(A, P, 1, y0) : -1;
-  int kya[kStrip];
-#pragma unroll
-  for (int i = 0; i < kStrip; i++) kya[i] = (act && y0 + i < ncy) ? slot_f(A, P, 1, y0 + i) - ky0 : -1;
+  int i1 = kStrip, i2 = kStrip;
+  for (int i = kStrip - 1; i >= 0; i--) {
+    const int a = (act && y0 + i < ncy) ? slot_f(A, P, 1, y0 + i) - ky0 : 9;
+    if (a >= 1) i1 = i;
+    if (a >= 2) i2 = i;
+  }
   double acc[3][N];
 #pragma unroll
   for (int a = 0; a < 3; a++)
@@ -174,7 +199,8 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
   __syncthreads();
   stage_I(0);
   stage_I(1);
-  stage_K(0);
+  load_K(0);
+  store_K(0);
   __syncthreads();
   const double kh = A.h * (1.0 / 12.0);
   const double inv_s = 1.0 / (double)s;
@@ -182,11 +208,11 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
   for (int z = 0; z < nz; z++) {
     // stage plane z+2 and cell layer z+1 (slots not read in this iteration) while the stencil of
     // plane z runs: no barrier between the two
+    load_K(z + 1);
     stage_I(z + 2);
-    stage_K(z + 1);
     if (act) {
-      const double* pl[3] = {Ir + ((z + 3) & 3) * kFX * kFX, Ir + (z & 3) * kFX * kFX, Ir + ((z + 1) & 3) * kFX * kFX};
-      const double* kl[2] = {Kr + ((z + 2) % 3) * kFC * kFC, Kr + (z % 3) * kFC * kFC};  // layers z-1, z
+      const double* pl[3] = {Ir + ((z + 3) & 3) * kIP * kIP, Ir + (z & 3) * kIP * kIP, Ir + ((z + 1) & 3) * kIP * kIP};
+      const double* kl[2] = {Kr + ((z + 2) % 3) * kKP * kKP, Kr + (z % 3) * kKP * kKP};  // layers z-1, z
       const uint8_t* dl = Dr + (z % 3) * kFC * kFC;
       double v[3][3][3];   // [dz][dy][dx]
       double kc[2][2][2];  // [oz][oy][ox]
@@ -195,8 +221,7 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
         for (int dz = 0; dz < 3; dz++)
 #pragma unroll
           for (int dx = 0; dx < 3; dx++) {
-            const int xx = x + dx - 1;
-            v[dz][slot][dx] = (yy >= 0 && yy < ny && xx >= 0 && xx < nx) ? pl[dz][yy * kFX + xx] : 0.0;
+            v[dz][slot][dx] = pl[dz][(yy + 1) * kIP + x + dx];  // zero halo / unwritten = outside
           }
       };
       auto ld_kap = [&](int cy, int slot) {  // cells of row cy, columns x-1, x; layers z-1, z
@@ -204,8 +229,7 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
         for (int oz = 0; oz < 2; oz++)
 #pragma unroll
           for (int ox = 0; ox < 2; ox++) {
-            const int cx = x - 1 + ox;
-            kc[oz][slot][ox] = (cx >= 0 && cx < ncx && cy >= 0 && cy < ncy) ? kl[oz][cy * kFC + cx] : 0.0;
+            kc[oz][slot][ox] = kl[oz][(cy + 1) * kKP + x + ox];  // zero halo / unwritten = outside
           }
       };
       ld_row(y0 - 1, 0);
@@ -232,12 +256,14 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
           const double sig = v[1][1][1] + v[1][1][2] + v[1][2][1] + v[1][2][2] + v[2][1][1] + v[2][1][2] +
                              v[2][2][1] + v[2][2][2];
           const int id = dl[y * kFC + x];
-          const int a = kya[i];
+          const int a = (i < i1) ? 0 : ((i < i2) ? 1 : 2);
 #pragma unroll
-          for (int aa = 0; aa < 3; aa++)
-#pragma unroll
-            for (int j = 0; j < N; j++)
-              if (aa == a && id == j) acc[aa][j] += sig;
+          for (int j = 0; j < N; j++) {
+            const double t = (id == j) ? sig : 0.0;
+            if (a == 0) acc[0][j] += t;
+            else if (a == 1) acc[1][j] += t;
+            else acc[2][j] += t;
+          }
         }
 #pragma unroll
         for (int dz = 0; dz < 3; dz++)
@@ -252,6 +278,7 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
           for (int ox = 0; ox < 2; ox++) kc[oz][0][ox] = kc[oz][1][ox];
       }
     }
+    store_K(z + 1);
     // constraint layer complete after cell layer z?
     if (z < ncz) {
       const int kz = slot_f(A, P, 2, z);
