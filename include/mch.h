@@ -44,6 +44,7 @@ extern "C" {
 #define MCH_ECUDA         -6  /* CUDA runtime failure */
 #define MCH_ENOMEM        -7  /* device allocation failed */
 #define MCH_EPLAN         -8  /* hierarchy cannot be built (no covering parent, reading R9) */
+#define MCH_ENCCL         -9  /* NCCL unavailable or a collective failed (world > 1) */
 
 typedef struct mch_ctx mch_ctx;
 
@@ -57,9 +58,11 @@ typedef struct {
   int      oversample;     /* l >= 1: R_p^+ = x_p +- (l+1/2)H (BASELINE: 1, i.e. a 3H window) */
   double   rtol;           /* projected-residual tolerance of the PCG (default 1e-12 if <= 0) */
   int      max_iter;       /* PCG iteration cap (default 20000 if <= 0) */
-  int      rank, world;    /* macropoint sharding across processes: this context solves the
-                              macropoints of each S_n whose position in S_n is congruent to
-                              rank mod world (world <= 1: all) */
+  int      rank, world;    /* macropoint sharding across processes (one per GPU; world <= 1: all
+                              macropoints here).  Each S_n (lexicographic order, i.e. slabs of the
+                              macrogrid) is cut into `world` contiguous runs of near-equal work
+                              (level-n window nodes); rank r solves run r (mch_shard_plan).
+                              PAPER.md:201 (macropoints independent), 256-261 (levels in order). */
   int      keep_all;       /* 1: keep every macropoint's fine local solution (for
                               mch_local_solution); 0: keep only parents (T_{L-1}) */
   void*    stream;         /* cudaStream_t */
@@ -78,6 +81,12 @@ typedef struct {
   void*  (*alloc)(size_t bytes, void* stream, void* user);
   void   (*free)(void* ptr, void* stream, void* user);
   void*    alloc_user;
+  /* ncclComm_t of the `world` ranks (from mch_comm_init, or the caller's own), or NULL.  With a
+     communicator and world > 1, mch_solve_level sends each level's parent solutions to the ranks
+     whose children need them and mch_effective_coeffs / mch_load_vectors all-reduce, so both are
+     collective and every rank returns the full results.  NULL with world > 1: no exchange (the
+     caller moves pool slots itself, see mch_shard_plan / mch_pool_slot; tests). */
+  void*    nccl_comm;
 } mch_params;
 
 #define MCH_INTERP_DLINEAR    0
@@ -101,19 +110,27 @@ typedef struct {
   int64_t  launches;       /* kernels launched by mch_solve_level(level) */
   int64_t  rank_deficient; /* windows whose level-n constraint rows were dependent (reading R20:
                               constraints imposed in the least-squares sense) */
+  double   ms_comm;        /* device time of the parent exchange after this level (world > 1) */
+  double   bytes_comm;     /* bytes this rank sent + received in that exchange */
 } mch_level_stats;
 
-/* Validate params and inputs, copy kappa (float64, n^d, x fastest) and
- * continuum ids (uint8, n^d, x fastest) into library-owned device memory, build
- * the hierarchy.  inputs_on_device: 1 if the pointers are device pointers.
- * The caller keeps ownership of its buffers.  *out is NULL on error. */
+/* Algorithm 1 REQUIRE (macropoint set T, coarsening factor eta, fine mesh h,
+ * levels L) with the medium kappa, psi_j.  Validate params and inputs, copy
+ * kappa (float64, n^d, x fastest) and continuum ids (uint8, n^d, x fastest; psi_j = [id == j])
+ * into library-owned device memory, build the hierarchy T_n / S_n (Eq. 10), the
+ * parents of every macropoint (Eq. 11) and the sharding plan.  inputs_on_device: 1 if the
+ * pointers are device pointers.  The caller keeps ownership of its buffers.  *out is NULL on error.
+ * Errors: MCH_EINVAL, MCH_EDIVISIBILITY, MCH_EPLAN, MCH_ENOMEM, MCH_ECUDA, MCH_ENCCL. */
 int mch_create(const mch_params* params, const double* kappa, const uint8_t* continuum_id,
                int inputs_on_device, mch_ctx** out);
 
 /* Algorithm 1 lines 4-7 for level `level` (1..L, strictly in order): solve the
  * N(1+d) constrained problems of every macropoint of S_level owned by this
  * context and compute their Eq. (7) Gram matrices.  Stream-ordered; returns
- * after the level's device work is complete. */
+ * after the level's device work is complete.  With params.nccl_comm and world > 1 it is
+ * collective: afterwards every parent of S_level that a child on another rank needs has been
+ * sent there (point-to-point NCCL, grouped).  Errors: MCH_EORDER, MCH_ERANK, MCH_ENOCONV
+ * (message names macropoint, rhs, residual), MCH_ECUDA, MCH_ENCCL. */
 int mch_solve_level(mch_ctx* ctx, int level);
 
 /* Copy the Eq. (7) coefficients of all macropoints into out,
@@ -122,8 +139,10 @@ int mch_solve_level(mch_ctx* ctx, int level);
  * lexicographic vertex order (x fastest); G[a][b] = int_{K_p} kappa grad(Phi_a).grad(Phi_b)
  * with Phi = (phi_0..phi_{N-1}, phi_0^0..phi_0^{d-1}, .., phi_{N-1}^{d-1}), i.e.
  * B_ji = G[j][i], B^m_ji = G[j][N+i*d+m], Bbar^n_ji = G[N+j*d+n][i],
- * B^{mn}_ji = G[N+j*d+n][N+i*d+m].  Entries of macropoints owned by other ranks
- * are left as 0 (the Python layer all-gathers them).  Requires all levels. */
+ * B^{mn}_ji = G[N+j*d+n][N+i*d+m].  Requires all levels (MCH_EORDER).  world > 1: with
+ * params.nccl_comm the call is collective (all-reduce of the owner-only tensors, exact because
+ * non-owned entries are 0) and returns every macropoint; without a communicator the entries of
+ * macropoints owned by other ranks are 0.  Synchronises params.stream. */
 int mch_effective_coeffs(mch_ctx* ctx, double* out, size_t out_len, int out_on_device);
 
 /* Replace the medium of an existing context: validate and copy kappa (float64, n^d) and
@@ -198,6 +217,9 @@ int mch_level_macropoints(const mch_ctx* ctx, int level, int64_t* out, size_t ca
 int mch_local_solution(mch_ctx* ctx, int64_t macropoint, int rhs, double* out, size_t out_len,
                        int64_t ext[3]);
 
+/* Per-level counters of the last solve of `level` on this context (SURVEY.md §8(d) metric:
+ * macropoint solves per level; PCG / fine-pass / exchange device times; iterations; the
+ * algorithmic PCG bytes of DESIGN.md §6).  Errors: MCH_EINVAL. */
 int mch_get_level_stats(const mch_ctx* ctx, int level, mch_level_stats* out);
 
 /* PCG iteration count of every problem of the last solve of `level` on this context: out[i*n_rhs + r]
@@ -213,6 +235,24 @@ int mch_pool_info(const mch_ctx* ctx, double** pool, int64_t* pool_len);
 int mch_pool_slot(const mch_ctx* ctx, int64_t macropoint, int64_t* offset, int64_t* length);
 /* device pointer of the [(M+1)^d][n_rhs][n_rhs] coefficient array */
 int mch_coeffs_device(const mch_ctx* ctx, double** G);
+
+/* ---- multi-GPU plumbing; NCCL is loaded at run time (libnccl.so.2) ----
+ * mch_comm_id: a new NCCL unique id (id_len >= 128 bytes) on one rank, to be broadcast to the
+ * others by the caller (e.g. torch.distributed).  mch_comm_init: ncclCommInitRank(world, id, rank)
+ * into *comm (collective over the ranks; call after cudaSetDevice).  mch_comm_destroy: release.
+ * Errors: MCH_EINVAL, MCH_ENCCL. */
+int mch_comm_id(void* id, size_t id_len);
+int mch_comm_init(void** comm, int world, int rank, const void* id, size_t id_len);
+int mch_comm_destroy(void* comm);
+
+/* Sharding plan of params (rank, world) at `level`, host only (no device work, no context):
+ * owned[0..*n_owned) = lexicographic indices of the macropoints of S_level this rank solves;
+ * xfers[3*i .. 3*i+2] = (macropoint, src rank, dst rank) of the parent solutions of S_level that
+ * move after level `level` (every rank lists all transfers; sorted by src, dst, macropoint).
+ * NULL buffers return only the counts.  Errors: MCH_EINVAL (also capacity too small),
+ * MCH_EDIVISIBILITY, MCH_EPLAN. */
+int mch_shard_plan(const mch_params* params, int level, int64_t* owned, size_t owned_cap, int64_t* n_owned,
+                   int64_t* xfers, size_t xfer_cap, int64_t* n_xfers);
 
 const char* mch_last_error(const mch_ctx* ctx);
 void mch_destroy(mch_ctx* ctx);

@@ -13,14 +13,14 @@ LIB_PATH = os.environ.get("MCH_LIB") or os.path.join(_HERE, "lib", "libmch.so")
 
 MCH_OK = 0
 ERRORS = {-1: "MCH_EINVAL", -2: "MCH_EDIVISIBILITY", -3: "MCH_ERANK", -4: "MCH_ENOCONV",
-          -5: "MCH_EORDER", -6: "MCH_ECUDA", -7: "MCH_ENOMEM", -8: "MCH_EPLAN"}
+          -5: "MCH_EORDER", -6: "MCH_ECUDA", -7: "MCH_ENOMEM", -8: "MCH_EPLAN", -9: "MCH_ENCCL"}
 
 # every symbol include/mch.h declares
 SYMBOLS = ["mch_create", "mch_set_medium", "mch_reset", "mch_solve_level", "mch_effective_coeffs", "mch_num_macropoints", "mch_level_macropoints",
            "mch_local_solution", "mch_get_level_stats", "mch_level_iterations", "mch_pool_info", "mch_pool_slot",
            "mch_coeffs_device", "mch_set_source", "mch_load_vectors", "mch_macro_solve", "mch_fine_solve",
-           "mch_fine_block_averages", "mch_last_error",
-           "mch_destroy"]
+           "mch_fine_block_averages", "mch_comm_id", "mch_comm_init", "mch_comm_destroy", "mch_shard_plan",
+           "mch_last_error", "mch_destroy"]
 
 
 class MchParams(ctypes.Structure):
@@ -29,7 +29,8 @@ class MchParams(ctypes.Structure):
                 ("oversample", ctypes.c_int), ("rtol", ctypes.c_double), ("max_iter", ctypes.c_int),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("keep_all", ctypes.c_int),
                 ("stream", ctypes.c_void_p), ("interp", ctypes.c_int), ("layout", ctypes.c_int),
-                ("alloc", ctypes.c_void_p), ("free", ctypes.c_void_p), ("alloc_user", ctypes.c_void_p)]
+                ("alloc", ctypes.c_void_p), ("free", ctypes.c_void_p), ("alloc_user", ctypes.c_void_p),
+                ("nccl_comm", ctypes.c_void_p)]
 
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -60,7 +61,8 @@ class MchLevelStats(ctypes.Structure):
                 ("relres_max", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("ms_pcg", ctypes.c_double), ("ms_setup", ctypes.c_double),
                 ("ms_gram", ctypes.c_double), ("pcg_bytes", ctypes.c_double),
-                ("launches", ctypes.c_int64), ("rank_deficient", ctypes.c_int64)]
+                ("launches", ctypes.c_int64), ("rank_deficient", ctypes.c_int64),
+                ("ms_comm", ctypes.c_double), ("bytes_comm", ctypes.c_double)]
 
 
 class MchError(RuntimeError):
@@ -94,6 +96,10 @@ def _load():
     lib.mch_macro_solve.argtypes = [vp, vp, vp, i32, vp, ctypes.c_size_t, i32, dbl, i32, P(i32)]
     lib.mch_fine_solve.argtypes = [vp, vp, i32, vp, ctypes.c_size_t, i32, dbl, i32, P(i32)]
     lib.mch_fine_block_averages.argtypes = [vp, vp, i32, vp, ctypes.c_size_t, i32]
+    lib.mch_comm_id.argtypes = [vp, ctypes.c_size_t]
+    lib.mch_comm_init.argtypes = [P(vp), i32, i32, vp, ctypes.c_size_t]
+    lib.mch_comm_destroy.argtypes = [vp]
+    lib.mch_shard_plan.argtypes = [P(MchParams), i32, P(i64), ctypes.c_size_t, P(i64), P(i64), ctypes.c_size_t, P(i64)]
     lib.mch_last_error.argtypes = [vp]
     lib.mch_last_error.restype = ctypes.c_char_p
     lib.mch_destroy.argtypes = [vp]

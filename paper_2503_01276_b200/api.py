@@ -44,7 +44,7 @@ LAYOUT = {"vertex": 0, "block": 1}
 
 def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversample=1, rtol=1e-12,
                max_iter=20000, rank=0, world=1, keep_all=False, stream=None, interp="dlinear",
-               layout="vertex", allocator=None):
+               layout="vertex", allocator=None, comm=None):
     """Returns an opaque context handle (ctypes.c_void_p).  allocator: None (cudaMalloc) or an
     (alloc, free) pair of _native.ALLOC_FN / FREE_FN callbacks, e.g. _native.torch_allocator()."""
     if isinstance(kappa, np.ndarray):
@@ -57,7 +57,7 @@ def mch_create(d, n, num_continua, M, levels, eta, kappa, continuum_id, oversamp
     p = MchParams(d=d, n=n, num_continua=num_continua, M=M, levels=levels, eta=eta,
                   oversample=oversample, rtol=rtol, max_iter=max_iter, rank=rank, world=world,
                   keep_all=int(keep_all), stream=stream if stream is not None else _current_stream(),
-                  interp=INTERP[interp], layout=LAYOUT[layout])
+                  interp=INTERP[interp], layout=LAYOUT[layout], nccl_comm=comm)
     if allocator is not None:
         p.alloc = ctypes.cast(allocator[0], ctypes.c_void_p)
         p.free = ctypes.cast(allocator[1], ctypes.c_void_p)
@@ -131,12 +131,47 @@ def mch_destroy(ctx):
     lib.mch_destroy(ctx)
 
 
+def mch_comm_id():
+    """A new NCCL unique id (128 bytes) — on one rank; broadcast it to the others."""
+    buf = ctypes.create_string_buffer(128)
+    check(lib.mch_comm_id(buf, 128), None)
+    return buf.raw
+
+
+def mch_comm_init(world, rank, uid):
+    """ncclComm_t of this rank (collective; call after torch.cuda.set_device)."""
+    comm = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    check(lib.mch_comm_init(ctypes.byref(comm), world, rank, buf, 128), None)
+    return comm.value
+
+
+def mch_comm_destroy(comm):
+    check(lib.mch_comm_destroy(comm), None)
+
+
+def mch_shard_plan(d, n, N, M, L, eta, rank, world, level, l=1, interp="dlinear", layout="vertex"):
+    """Host-only sharding plan (no GPU): (owned lexicographic indices of S_level on this rank,
+    transfers [k, 3] = (macropoint, src, dst) sent after level `level`)."""
+    p = MchParams(d=d, n=n, num_continua=N, M=M, levels=L, eta=eta, oversample=l, rtol=1e-12,
+                  max_iter=0, rank=rank, world=world, keep_all=0, stream=None,
+                  interp=INTERP[interp], layout=LAYOUT[layout])
+    no, nx = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(lib.mch_shard_plan(ctypes.byref(p), level, None, 0, ctypes.byref(no), None, 0, ctypes.byref(nx)), None)
+    owned = np.zeros(max(no.value, 1), dtype=np.int64)
+    xf = np.zeros((max(nx.value, 1), 3), dtype=np.int64)
+    check(lib.mch_shard_plan(ctypes.byref(p), level, owned.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                             owned.size, ctypes.byref(no), xf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                             xf.shape[0], ctypes.byref(nx)), None)
+    return owned[:no.value], xf[:nx.value]
+
+
 class Homogenizer:
     """Hierarchical multicontinuum homogenization hot path on one GPU (or one rank's shard)."""
 
     def __init__(self, d, n, N, M, L, eta, kappa, ids, l=1, rtol=1e-12, max_iter=20000, rank=0,
                  world=1, keep_all=False, stream=None, interp="dlinear", layout="vertex",
-                 torch_memory=False):
+                 torch_memory=False, comm=None):
         self.d, self.n, self.N, self.M, self.L, self.eta, self.l = d, n, N, M, L, eta, l
         self.n_rhs = N * (1 + d)
         self.mv = M + 1 if layout == "vertex" else M  # macropoints per dimension
@@ -145,7 +180,8 @@ class Homogenizer:
         self._allocator = _native.torch_allocator() if torch_memory else None
         self.ctx = mch_create(d, n, N, M, L, eta, kappa, ids, oversample=l, rtol=rtol,
                               max_iter=max_iter, rank=rank, world=world, keep_all=keep_all,
-                              stream=stream, interp=interp, layout=layout, allocator=self._allocator)
+                              stream=stream, interp=interp, layout=layout, allocator=self._allocator,
+                              comm=comm)
         self.solved = 0
 
     @classmethod

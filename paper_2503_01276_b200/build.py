@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libmch.so")
-SOURCES = ["mch.cu", "kernels.cu", "pcg2d.cu", "pcg3d.cu", "fine3d.cu", "macro.cu", "fine.cu", "plan.cpp"]
+SOURCES = ["mch.cu", "kernels.cu", "pcg2d.cu", "pcg3d.cu", "fine3d.cu", "macro.cu", "fine.cu", "plan.cpp", "shard.cpp", "comm.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # dev variants: MCH_BUILD_TIMING=1 builds lib/libmch_timing.so with per-phase PCG cycle counters;
 # MCH_BUILD_TAG=t MCH_BUILD_DEFS="-DX=1 ..." builds lib/libmch_t.so with extra defines
@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         out, err = pr.communicate()
         log_parts.append(" ".join(cmd) + "\n" + out + err)
         failed = failed or pr.returncode != 0
-    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-ldl",
             "-o", LIB + ".tmp", *objs]
     if not failed:
         res = subprocess.run(link, capture_output=True, text=True)

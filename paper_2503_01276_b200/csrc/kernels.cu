@@ -1894,11 +1894,11 @@ cudaError_t launch_transport(const LevelArgs& A, int threads, cudaStream_t st) {
   const bool force_mr = getenv("MCH_TRANSPORT_MR") != nullptr;  // tests: the multi-rhs kernel at any size
   // 3D: its fine windows are 8x larger per macropoint; from eight macropoints per SM up (config 5
   // level 4: 332 -> 306 ms; level 3, 604 macropoints: 66 -> 71 ms, kept per rhs)
-  if (A.D == 3 && A.tphase != 0 && A.n_rhs <= kMaxR && (force_mr || A.nprob_mp >= 8 * sms)) {
+  if (A.D == 3 && A.tphase != 0 && A.n_rhs <= kMaxR && (force_mr || A.nprob_level >= 8 * sms)) {
     k_transport3d_mr<<<(unsigned)A.nprob_mp, 256, 0, st>>>(A);
     return cudaGetLastError();
   }
-  if (A.D == 2 && A.band == 0 && A.tphase == 0 && !generic && (force_mr || A.nprob_mp >= 2 * sms) &&
+  if (A.D == 2 && A.band == 0 && A.tphase == 0 && !generic && (force_mr || A.nprob_level >= 2 * sms) &&
       (A.n_rhs == 3 || A.n_rhs == 6 || A.n_rhs == 9)) {
     const size_t sm = sizeof(double) * ((A.nsub * 7 + 2 + 1) / 2 + (size_t)8 * A.ncon * A.n_rhs);
     if (sm <= 232448) {
@@ -1969,7 +1969,7 @@ cudaError_t launch_combine(const LevelArgs& A, int threads, cudaStream_t st) {
   int dev = 0, sms = 148;  // one CTA per macropoint once there are two per SM (as the transport)
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (getenv("MCH_TRANSPORT_MR") != nullptr || (A.nprob_mp >= 2 * sms && getenv("MCH_TRANSPORT_GENERIC") == nullptr)) {
+  if (getenv("MCH_TRANSPORT_MR") != nullptr || (A.nprob_level >= 2 * sms && getenv("MCH_TRANSPORT_GENERIC") == nullptr)) {
     if (A.D == 2) k_combine_mr<2><<<(unsigned)A.nprob_mp, 256, 0, st>>>(A);
     else k_combine_mr<3><<<(unsigned)A.nprob_mp, 256, 0, st>>>(A);
     return cudaGetLastError();

@@ -14,6 +14,8 @@
 #include "kernels.h"
 #include "mch_internal.h"
 #include "plan.h"
+#include "shard.h"
+#include "comm.h"
 
 namespace {
 
@@ -120,6 +122,10 @@ struct mch_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;  // side stream: the projector's C D^-1 C^T beside the coarse-space setup
   HostPlan plan;
+  ShardPlan shard;          // ownership and parent transfers (world > 1)
+  ncclComm_t comm = nullptr;  // params.nccl_comm (not owned)
+  const NcclApi* nccl = nullptr;
+  DevBuf Gall, ball;        // all-reduced coefficients / loads (world > 1)
   double* kappa = nullptr;
   uint8_t* ids = nullptr;
   double* pool = nullptr;
@@ -235,6 +241,7 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   c->al.user = p.alloc_user;
   c->al.stream = p.stream;
   for (DevBuf* b : c->bufs()) b->al = &c->al;
+  c->Gall.al = c->ball.al = &c->al;
   c->D = p.d;
   c->N = p.num_continua;
   c->n_rhs = p.num_continua * (1 + p.d);
@@ -309,17 +316,26 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
     if (e != cudaSuccess) return cleanup(MCH_ECUDA, cudaGetErrorString(e));
     if (hb) return cleanup(MCH_EINVAL, "kappa must be positive and finite; ids < num_continua");
   }
+  // sharding: contiguous cost-balanced runs of each S_n per rank, parent transfers
+  shard_build(c->plan, p.world, c->shard);
+  if (p.world > 1 && p.nccl_comm) {
+    std::string nerr;
+    c->nccl = nccl_api(nerr);
+    if (!c->nccl) return cleanup(MCH_ENCCL, nerr);
+    c->comm = reinterpret_cast<ncclComm_t>(p.nccl_comm);
+  }
   // parent pool: T_{L-1} (or everything with keep_all)
   const int64_t nmac = (int64_t)c->plan.all.size();
   c->pool_off.assign(nmac, -1);
-  // layout: by level, then owner rank (position in S_n mod world), then lexicographic, so the
-  // slots one rank produces at one level are contiguous (one broadcast per (level, owner)).
+  // layout: by level, then owner rank, then lexicographic, so the slots one rank produces at one
+  // level are contiguous.  Every rank holds the whole pool layout.
   int64_t off = 0;
   for (int lev = 1; lev <= p.levels; lev++) {
     if (!(lev < p.levels || p.keep_all)) continue;
     const std::vector<int64_t>& Sl = c->plan.S[lev];
     for (int owner = 0; owner < p.world; owner++) {
-      for (size_t pos = owner; pos < Sl.size(); pos += p.world) {
+      for (size_t pos = 0; pos < Sl.size(); pos++) {
+        if (c->shard.owner[lev][pos] != owner) continue;
         const MacroHost& m = c->plan.all[Sl[pos]];
         int64_t fn = 1;
         for (int d = 0; d < p.d; d++) fn *= (m.hi[d] - m.lo[d] + 1);
@@ -330,6 +346,9 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   }
   c->pool_len = off;
   if (off > 0 && dev_alloc(&c->al, (void**)&c->pool, off * sizeof(double)) != cudaSuccess) return cleanup(MCH_ENOMEM, "pool alloc");
+  // world > 1: poison the pool (NaN) so a parent that should have been received but was not shows
+  // up as a non-finite coefficient instead of a silently wrong one
+  if (off > 0 && p.world > 1) cudaMemsetAsync(c->pool, 0xFF, off * sizeof(double), c->st);
   const size_t gbytes = (size_t)nmac * c->n_rhs * c->n_rhs * sizeof(double);
   if (dev_alloc(&c->al, (void**)&c->G, gbytes) != cudaSuccess) return cleanup(MCH_ENOMEM, "G alloc");
   cudaMemsetAsync(c->G, 0, gbytes, c->st);
@@ -343,6 +362,35 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   return MCH_OK;
 }
 
+// Geometry of one macropoint's problem at its level (offsets and parents are filled per batch).
+static void fill_geometry(const HostPlan& pl, int D, int s, const MacroHost& m, ProbDesc& P) {
+  memset(&P, 0, sizeof(P));
+  for (int d = 0; d < 3; d++) {
+    P.k[d] = m.k[d];
+    P.lo[d] = (d < D) ? m.lo[d] : 0;
+    P.ncf[d] = (d < D) ? m.hi[d] - m.lo[d] : 0;
+    P.nc[d] = (d < D) ? P.ncf[d] / s : 0;
+    P.glo[d] = (d < D) ? P.lo[d] / s : 0;
+    const int64_t a = (int64_t)m.k[d] * pl.c - pl.coff(), b = a + pl.c;  // K_p
+    P.kp_lo[d] = (d < D) ? (int)std::max<int64_t>(0, a) : 0;
+    P.kp_hi[d] = (d < D) ? (int)std::min<int64_t>(pl.n, b) : 1;
+  }
+  P.lin = m.lin;
+}
+
+// Kernel variants of one level, decided over ALL macropoints of S_level (every rank decides the
+// same), so a macropoint takes the same kernels and arithmetic whatever the sharding: results are
+// bitwise independent of world.
+struct LevelVariant {
+  bool on2d = false, l1op = false, crs2d = false;
+  int variant = -1, threads2 = 0, tm_cols = 32, rpt = 0;
+  bool on3d = false, w7 = false, tsplit = false, fused3 = false;
+  int nxm3 = 0;
+  int th_l = 64, th_f = 64;
+  int max_kp = 0;
+  bool coarse = false;
+};
+
 static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelBatch>>& out) {
   const int D = c->D, N = c->N, nr = c->n_rhs, nc = c->ncon;
   const HostPlan& pl = c->plan;
@@ -350,7 +398,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
   const std::vector<int64_t>& Sl = pl.S[level];
   std::vector<int64_t> mine;
   for (size_t i = 0; i < Sl.size(); i++)
-    if ((int)(i % c->p.world) == c->p.rank) mine.push_back(Sl[i]);
+    if (c->shard.owner[level][i] == c->p.rank) mine.push_back(Sl[i]);
   auto sizes = [&](const MacroHost& m, int64_t& ln, int64_t& fnn, int64_t& lcells) {
     ln = 1; fnn = 1; lcells = 1;
     for (int d = 0; d < D; d++) {
@@ -360,6 +408,98 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       lcells *= ncf / s;
     }
   };
+  // ---- level-global decisions
+  LevelVariant V;
+  std::vector<ProbDesc> gd(Sl.size());
+  int gmaxn = 0, gmaxf = 0;
+  int64_t gmax_ln = 0, gmax_fn = 0;
+  for (size_t i = 0; i < Sl.size(); i++) {
+    const MacroHost& m = pl.all[Sl[i]];
+    fill_geometry(pl, D, s, m, gd[i]);
+    int64_t ln, fnn, lc;
+    sizes(m, ln, fnn, lc);
+    gmax_ln = std::max(gmax_ln, ln);
+    gmax_fn = std::max(gmax_fn, fnn);
+    int kp = 1;
+    for (int d = 0; d < D; d++) {
+      gmaxn = std::max(gmaxn, gd[i].nc[d] + 1);
+      gmaxf = std::max(gmaxf, gd[i].ncf[d] + 1);
+      kp *= gd[i].kp_hi[d] - gd[i].kp_lo[d] + 1;
+    }
+    V.max_kp = std::max(V.max_kp, kp);
+  }
+  auto pick = [](int64_t nodes) {
+    int64_t t = ((nodes / 4 + 31) / 32) * 32;
+    return (int)std::max<int64_t>(64, std::min<int64_t>(512, t));
+  };
+  V.th_l = pick(gmax_ln);
+  V.th_f = pick(gmax_fn);
+  // on-chip 2D PCG (pcg2d.cu) unless MCH_PCG=old; MCH_PCG=gn forces the precomputed-operator
+  // variant at level 1 as well (cross-check of the two operator paths)
+  if ((D == 2) && N <= 3 && nc == 9 * N && c->pcg_mode != 1 && c->band == 0) {  // 3x3 subcells (l = 1)
+    std::vector<int> cands;
+    if (level == 1 && c->pcg_mode != 2) cands.push_back(PCG2D_V_L1);
+    cands.push_back(PCG2D_V_GN25);
+    cands.push_back(PCG2D_V_GN49);
+    cands.push_back(PCG2D_V_GN97);
+    std::vector<short4> tmp;
+    for (int v : cands) {
+      int rpt, nxm, maxw, l1op, sstc, smlr;
+      pcg2d_variant(v, &rpt, &nxm, &maxw, &l1op, &sstc, &smlr);
+      // the coarse-space variant where it is used and fits, else the same variant without it
+      bool crs_v = c->coarse && ((level == 1 && v == PCG2D_V_L1) || (level == 2 && v == PCG2D_V_GN49));
+      if (crs_v && pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0, true) > 232448) crs_v = false;
+      if (gmaxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0, crs_v) > 232448) continue;
+      int maxwp = 0;
+      for (size_t i = 0; i < gd.size(); i++) {
+        seg_plan_2d(gd[i], s, (int)pl.c, (int)pl.coff(), c->l, rpt, tmp);
+        maxwp = std::max(maxwp, ((gd[i].nc[0] + 1 + 31) / 32) * (int)tmp.size());
+      }
+      const int rp4 = (rpt + 3) & ~3;  // TMEM: warps per lane quarter x (q, x [, component ids])
+      const int need = ((maxwp + 3) / 4) * (4 * rp4 + (crs_v ? rp4 / 4 : 0));
+      int cols = 32;
+      while (cols < need) cols *= 2;
+      if (maxwp > maxw || cols > 512) continue;
+      V.tm_cols = cols;
+      V.threads2 = 32 * maxwp;
+      V.variant = v;
+      V.rpt = rpt;
+      V.l1op = l1op != 0;
+      V.on2d = true;
+      V.crs2d = crs_v;
+      break;
+    }
+  }
+  // 3D: on-chip PCG at levels >= 2 (pcg3d.cu) for windows of <= 25 level nodes per side, at level
+  // 1 (k_pcg3d_l1) for windows of <= 49 fine nodes per side; fused fine passes (fine3d.cu) at
+  // levels >= 2 for 3x3x3 subcells, windows of <= 49 fine nodes per side and >= 4 fine cells per H
+  // (a thread's 7-row strip spans <= 3 subcell rows)
+  if (D == 3 && nc == 27 * N && N <= 4 && c->pcg_mode != 1) {
+    const char* f3e = getenv("MCH_FINE3D");
+    const bool generic_t = getenv("MCH_TRANSPORT_GENERIC") != nullptr;
+    V.tsplit = level >= 2 && gmaxf <= 49 && pcg3d_l1_smem(N) <= 232448 && !generic_t;
+    V.fused3 = level >= 2 && c->l == 1 && pl.c >= 4 && gmaxf <= 49 && fine3d_transport_smem(N) <= 232448 &&
+               !(f3e && atoi(f3e) == 0) && !generic_t;
+    if (level >= 2) {
+      const int nxm = pcg3d_nxm(gmaxn);
+      if (nxm > 0 && pcg3d_smem(N, nxm) <= 232448) {
+        V.on3d = true;
+        V.nxm3 = nxm;
+      }
+      const char* w7e = getenv("MCH_PCG3D_W7");
+      V.w7 = V.on3d && nxm == 7 && N <= 2 && nr == 4 * N && pcg3d_w7_smem(N) <= 232448 && !(w7e && atoi(w7e) == 0);
+    } else if (gmaxn <= 49 && pcg3d_l1_smem(N) <= 232448) {
+      V.on3d = true;
+      V.nxm3 = 49;
+    }
+  }
+  // two-level preconditioner: level 1 everywhere; level 2 on the 49-node on-chip 2D variant,
+  // whose shared memory holds the coarse data; 3D level 1 and the 25-node level-2 windows (the 13-
+  // and 7-node windows of deeper levels showed no iteration change)
+  V.coarse = c->coarse && c->band == 0 && (V.on2d ? V.crs2d : (level == 1 || (V.on3d && V.nxm3 == 25)));
+  const double kpn = (double)V.max_kp;
+
+  // ---- this rank's macropoints, batched by memory
   // solve order: largest (unclipped) windows first.  Their problems are the longest (more work per
   // iteration and more iterations), so starting them first shortens the tail of the launch
   // (longest-processing-time-first list scheduling over the SMs).  Stable: lexicographic within
@@ -374,13 +514,6 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     }
     std::stable_sort(mine.begin(), mine.end(), [&](int64_t a, int64_t b) { return key[a] > key[b]; });
   }
-  // fused 3D fine passes (fine3d.cu) at levels >= 2: 3x3x3 subcells, windows of <= 49 fine nodes
-  // per side, >= 4 fine cells per H (a thread's 7-row strip spans <= 3 subcell rows)
-  const char* f3e = getenv("MCH_FINE3D");
-  const bool fused3_lvl = D == 3 && level >= 2 && nc == 27 * N && c->l == 1 && pl.c >= 4 && 3 * pl.c + 1 <= 49 &&
-                          fine3d_transport_smem(N) <= 232448 && !(f3e && atoi(f3e) == 0) &&
-                          getenv("MCH_TRANSPORT_GENERIC") == nullptr;
-  const double kpn = (double)(pl.c + 1) * (pl.c + 1) * (pl.c + 1);
   size_t freeb = 0, totb = 0;
   cudaMemGetInfo(&freeb, &totb);
   const double budget = std::min<double>(48e9, 0.5 * (double)freeb);
@@ -392,7 +525,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       int64_t ln, fnn, lc;
       sizes(pl.all[mine[bend]], ln, fnn, lc);
       double b = 8.0 * (5.0 * nr * ln + ln * (10.0 + 4.0 * N) + (double)nc * nc + 3.0 * nc * nr + nc + 12) +
-                 (level >= 2 ? (fused3_lvl ? 8.0 * nr * kpn : 16.0 * nr * fnn) : 0.0);
+                 (level >= 2 ? (V.fused3 ? 8.0 * nr * kpn : 16.0 * nr * fnn) : 0.0);
       if (bend > bstart && bytes + b > budget) break;
       bytes += b;
       bend++;
@@ -405,24 +538,13 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     for (int i = 0; i < nmp; i++) {
       const MacroHost& m = pl.all[mine[bstart + i]];
       ProbDesc& P = descs[i];
-      memset(&P, 0, sizeof(P));
+      fill_geometry(pl, D, s, m, P);
       int64_t ln, fnn, lc;
       sizes(m, ln, fnn, lc);
       B->mps.push_back(mine[bstart + i]);
       B->lexpos.push_back((int)(std::lower_bound(lexi.begin(), lexi.end(), mine[bstart + i]) - lexi.begin()));
       B->ln.push_back(ln);
       B->lc.push_back(lc);
-      for (int d = 0; d < 3; d++) {
-        P.k[d] = m.k[d];
-        P.lo[d] = (d < D) ? m.lo[d] : 0;
-        P.ncf[d] = (d < D) ? m.hi[d] - m.lo[d] : 0;
-        P.nc[d] = (d < D) ? P.ncf[d] / s : 0;
-        P.glo[d] = (d < D) ? P.lo[d] / s : 0;
-        const int64_t a = (int64_t)m.k[d] * pl.c - pl.coff(), b = a + pl.c;  // K_p
-        P.kp_lo[d] = (d < D) ? (int)std::max<int64_t>(0, a) : 0;
-        P.kp_hi[d] = (d < D) ? (int)std::min<int64_t>(pl.n, b) : 1;
-      }
-      P.lin = m.lin;
       P.node_off = B->node_off;
       P.vec_off = B->vec_off;
       P.fine_off = B->fine_off;
@@ -445,94 +567,41 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
         if (P.par_pool[t] < 0) return fail(c, MCH_EPLAN, "parent not in pool");
       }
     }
-    auto pick = [](int nodes) {
-      int t = ((nodes / 4 + 31) / 32) * 32;
-      return std::max(64, std::min(512, t));
-    };
-    B->th_l = pick(B->max_ln);
-    B->th_f = pick(B->max_fn);
+    B->th_l = V.th_l;
+    B->th_f = V.th_f;
     CKC(c, B->descs.ensure(sizeof(ProbDesc) * nmp));
     CKC(c, cudaMemcpy(B->descs.ptr, descs.data(), sizeof(ProbDesc) * nmp, cudaMemcpyHostToDevice));
-    // on-chip 2D PCG (pcg2d.cu) unless MCH_PCG=old; MCH_PCG=gn forces the precomputed-operator
-    // variant at level 1 as well (cross-check of the two operator paths)
-    if ((D == 2) && N <= 3 && nc == 9 * N && c->pcg_mode != 1 && c->band == 0) {  // 3x3 subcells (l = 1)
-      int maxn = 0;
-      for (int i = 0; i < nmp; i++) maxn = std::max(maxn, std::max(descs[i].nc[0], descs[i].nc[1]) + 1);
-      std::vector<int> cands;
-      if (level == 1 && c->pcg_mode != 2) cands.push_back(PCG2D_V_L1);
-      cands.push_back(PCG2D_V_GN25);
-      cands.push_back(PCG2D_V_GN49);
-      cands.push_back(PCG2D_V_GN97);
-      for (int v : cands) {
-        int rpt, nxm, maxw, l1op, sstc, smlr;
-        pcg2d_variant(v, &rpt, &nxm, &maxw, &l1op, &sstc, &smlr);
-        // the coarse-space variant where it is used and fits, else the same variant without it
-        bool crs_v = c->coarse && ((level == 1 && v == PCG2D_V_L1) || (level == 2 && v == PCG2D_V_GN49));
-        if (crs_v && pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0, true) > 232448) crs_v = false;
-        if (maxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0, crs_v) > 232448) continue;
-        std::vector<int> nsegs(nmp);
-        std::vector<std::vector<short4>> per(nmp);
-        int maxseg = 0, maxwp = 0;
-        for (int i = 0; i < nmp; i++) {
-          seg_plan_2d(descs[i], s, (int)pl.c, (int)pl.coff(), c->l, rpt, per[i]);
-          nsegs[i] = (int)per[i].size();
-          maxseg = std::max(maxseg, nsegs[i]);
-          maxwp = std::max(maxwp, ((descs[i].nc[0] + 1 + 31) / 32) * nsegs[i]);
-        }
-        const int rp4 = (rpt + 3) & ~3;  // TMEM: warps per lane quarter x (q, x [, component ids])
-        const int need = ((maxwp + 3) / 4) * (4 * rp4 + (crs_v ? rp4 / 4 : 0));
-        int cols = 32;
-        while (cols < need) cols *= 2;
-        if (maxwp > maxw || cols > 512) continue;
-        std::vector<short4> all_segs((size_t)nmp * maxseg, make_short4(0, 0, 0, -1));
-        for (int i = 0; i < nmp; i++)
-          for (int k = 0; k < nsegs[i]; k++) all_segs[(size_t)i * maxseg + k] = per[i][k];
-        CKC(c, B->segs.ensure(sizeof(short4) * all_segs.size()));
-        CKC(c, B->nseg.ensure(sizeof(int) * nmp));
-        CKC(c, cudaMemcpy(B->segs.ptr, all_segs.data(), sizeof(short4) * all_segs.size(), cudaMemcpyHostToDevice));
-        CKC(c, cudaMemcpy(B->nseg.ptr, nsegs.data(), sizeof(int) * nmp, cudaMemcpyHostToDevice));
-        B->maxseg = maxseg;
-        B->tm_cols = cols;
-        B->threads2 = 32 * maxwp;
-        B->variant = v;
-        B->l1op = l1op != 0;
-        B->on2d = true;
-        B->crs2d = crs_v;
-        break;
+    if (V.on2d) {
+      std::vector<int> nsegs(nmp);
+      std::vector<std::vector<short4>> per(nmp);
+      int maxseg = 0;
+      for (int i = 0; i < nmp; i++) {
+        seg_plan_2d(descs[i], s, (int)pl.c, (int)pl.coff(), c->l, V.rpt, per[i]);
+        nsegs[i] = (int)per[i].size();
+        maxseg = std::max(maxseg, nsegs[i]);
       }
-    }
-    // on-chip 3D PCG at levels >= 2 (pcg3d.cu) for windows of <= 25 level nodes per side
-    // and at level 1 (k_pcg3d_l1) for windows of <= 49 fine nodes per side
-    if (D == 3 && nc == 27 * N && N <= 4 && c->pcg_mode != 1) {
-      int maxn = 0;
+      std::vector<short4> all_segs((size_t)nmp * maxseg, make_short4(0, 0, 0, -1));
       for (int i = 0; i < nmp; i++)
-        for (int d = 0; d < 3; d++) maxn = std::max(maxn, descs[i].nc[d] + 1);
-      int maxf = 0;
-      for (int i = 0; i < nmp; i++)
-        for (int d = 0; d < 3; d++) maxf = std::max(maxf, descs[i].ncf[d] + 1);
-      B->tsplit = level >= 2 && maxf <= 49 && pcg3d_l1_smem(N) <= 232448 && getenv("MCH_TRANSPORT_GENERIC") == nullptr;
-      B->fused3 = fused3_lvl && maxf <= 49;
-      if (B->fused3) {
-        for (int i = 0; i < nmp; i++) {
-          int kp = 1;
-          for (int d = 0; d < 3; d++) kp *= descs[i].kp_hi[d] - descs[i].kp_lo[d] + 1;
-          B->max_kp = std::max(B->max_kp, kp);
-        }
-      }
-      if (level >= 2) {
-        const int nxm = pcg3d_nxm(maxn);
-        if (nxm > 0 && pcg3d_smem(N, nxm) <= 232448) {
-          B->on3d = true;
-          B->nxm3 = nxm;
-        }
-        const char* w7e = getenv("MCH_PCG3D_W7");
-        B->w7 = B->on3d && nxm == 7 && N <= 2 && nr == 4 * N && pcg3d_w7_smem(N) <= 232448 &&
-                !(w7e && atoi(w7e) == 0);
-      } else if (maxn <= 49 && pcg3d_l1_smem(N) <= 232448) {
-        B->on3d = true;
-        B->nxm3 = 49;
-      }
+        for (int k = 0; k < nsegs[i]; k++) all_segs[(size_t)i * maxseg + k] = per[i][k];
+      CKC(c, B->segs.ensure(sizeof(short4) * all_segs.size()));
+      CKC(c, B->nseg.ensure(sizeof(int) * nmp));
+      CKC(c, cudaMemcpy(B->segs.ptr, all_segs.data(), sizeof(short4) * all_segs.size(), cudaMemcpyHostToDevice));
+      CKC(c, cudaMemcpy(B->nseg.ptr, nsegs.data(), sizeof(int) * nmp, cudaMemcpyHostToDevice));
+      B->maxseg = maxseg;
+      B->tm_cols = V.tm_cols;
+      B->threads2 = V.threads2;
+      B->variant = V.variant;
+      B->l1op = V.l1op;
+      B->on2d = true;
+      B->crs2d = V.crs2d;
     }
+    B->on3d = V.on3d;
+    B->nxm3 = V.nxm3;
+    B->w7 = V.w7;
+    B->tsplit = V.tsplit;
+    B->fused3 = V.fused3;
+    B->max_kp = V.max_kp;
+    B->coarse = V.coarse;
     // scratch shared by all levels and batches (grow-only, allocated here, never in a solve)
     CKC(c, c->g0.ensure(sizeof(double) * nmp * nc * nr));
     CKC(c, c->g.ensure(sizeof(double) * nmp * nc * nr));
@@ -565,14 +634,6 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       CKC(c, c->STC.ensure(sizeof(double) * 9 * B->node_off));
       CKC(c, c->MLR.ensure(sizeof(double) * 4 * N * B->node_off));
     }
-    // level 1 only: at level 2 the fixed per-iteration cost of the coarse sums outweighs the saved
-    // iterations (config 2: 245 -> 106 iterations but 15 -> 45 ms)
-    // level 1 everywhere; level 2 on the 49-node on-chip variant, whose shared memory holds the
-    // coarse data (with it in L2 the fixed per-iteration cost outweighed the saved iterations)
-    // 3D: level 1 and the 25-node level-2 windows (the 13- and 7-node windows of deeper levels
-    // showed no iteration change)
-    B->coarse = c->coarse && c->band == 0 &&
-                (B->on2d ? B->crs2d : (level == 1 || (B->on3d && B->nxm3 == 25)));
     if (B->coarse) {
       if (B->on2d && B->variant == PCG2D_V_L1) CKC(c, c->R.ensure(sizeof(double) * B->vec_off));  // r mirror (L2)
       CKC(c, c->cmap.ensure(sizeof(int) * B->node_off));
@@ -633,6 +694,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   A.band = c->band;
   A.bload = c->bload.as<double>();
   A.rtol = c->p.rtol; A.max_iter = c->p.max_iter;
+  A.nprob_level = (int)pl.S[level].size();  // kernel heuristics use the level-global count (world-independent)
   if (level >= 2) {
     const int64_t gcells = (D == 2) ? (int64_t)gn * gn : (int64_t)gn * gn * gn;
     const int NW = (D == 2) ? 6 : 27;
@@ -758,8 +820,36 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     // batches share the scratch: a later batch may only start after this one's results are read
     if (multi) CKC(c, cudaStreamSynchronize(st));
   }
+  // exchange step (i): the parents of S_level go to the ranks whose children of
+  // later levels read them (Eq. 11), grouped point-to-point NCCL transfers of whole pool slots
+  cudaEventRecord(c->ev[4], st);
+  if (c->comm && level < c->p.levels && !c->shard.xfer[level].empty()) {
+    const NcclApi* nc_ = c->nccl;
+    ncclResult_t nr_ = nc_->GroupStart();
+    for (const auto& x : c->shard.xfer[level]) {
+      if (nr_ != ncclSuccess) break;
+      int64_t len = 0, offp = c->pool_off[x[0]];
+      {
+        const MacroHost& pm = pl.all[x[0]];
+        len = c->n_rhs;
+        for (int d = 0; d < D; d++) len *= (pm.hi[d] - pm.lo[d] + 1);
+      }
+      if (x[1] == c->p.rank) nr_ = nc_->Send(c->pool + offp, (size_t)len, ncclFloat64, (int)x[2], c->comm, st);
+      else if (x[2] == c->p.rank) nr_ = nc_->Recv(c->pool + offp, (size_t)len, ncclFloat64, (int)x[1], c->comm, st);
+      if (x[1] == c->p.rank || x[2] == c->p.rank) S.bytes_comm += 8.0 * (double)len;
+    }
+    const ncclResult_t ge = nc_->GroupEnd();
+    if (nr_ == ncclSuccess) nr_ = ge;
+    if (nr_ != ncclSuccess) return fail(c, MCH_ENCCL, std::string("parent exchange: ") + nc_->GetErrorString(nr_));
+    S.launches += 1;
+  }
   cudaEventRecord(c->ev[5], st);
   CKC(c, cudaEventSynchronize(c->ev[5]));
+  {
+    float tc = 0;
+    cudaEventElapsedTime(&tc, c->ev[4], c->ev[5]);
+    S.ms_comm = tc;
+  }
   float ms_setup = 0, ms_pcg = 0, ms_gram = 0;
   for (size_t bi = 0; bi < batches.size(); bi++) {
     LevelBatch& B = *batches[bi];
@@ -854,7 +944,14 @@ extern "C" int mch_effective_coeffs(mch_ctx* c, double* out, size_t out_len, int
   if (c->solved != c->p.levels) return fail(c, MCH_EORDER, "coefficients need all levels solved");
   const size_t need = c->plan.all.size() * (size_t)c->n_rhs * c->n_rhs;
   if (out_len < need) return fail(c, MCH_EINVAL, "out_len too small");
-  CKC(c, cudaMemcpyAsync(out, c->G, need * sizeof(double),
+  const double* src = c->G;
+  if (c->comm) {  // exchange step (ii): non-owned entries are exactly 0, so the sum is exact
+    CKC(c, c->Gall.ensure(need * sizeof(double)));
+    const ncclResult_t r = c->nccl->AllReduce(c->G, c->Gall.ptr, need, ncclFloat64, ncclSum, c->comm, c->st);
+    if (r != ncclSuccess) return fail(c, MCH_ENCCL, std::string("coefficient all-reduce: ") + c->nccl->GetErrorString(r));
+    src = c->Gall.as<double>();
+  }
+  CKC(c, cudaMemcpyAsync(out, src, need * sizeof(double),
                          out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
   CKC(c, cudaStreamSynchronize(c->st));
   return MCH_OK;
@@ -888,7 +985,14 @@ extern "C" int mch_load_vectors(mch_ctx* c, double* out, size_t out_len, int out
   if (c->solved != c->p.levels) return fail(c, MCH_EORDER, "load vectors need all levels solved");
   const size_t need = c->plan.all.size() * (size_t)c->N;
   if (out_len < need) return fail(c, MCH_EINVAL, "out_len too small");
-  CKC(c, cudaMemcpyAsync(out, c->bload.ptr, need * sizeof(double),
+  const void* bsrc = c->bload.ptr;
+  if (c->comm) {
+    CKC(c, c->ball.ensure(need * sizeof(double)));
+    const ncclResult_t r = c->nccl->AllReduce(c->bload.ptr, c->ball.ptr, need, ncclFloat64, ncclSum, c->comm, c->st);
+    if (r != ncclSuccess) return fail(c, MCH_ENCCL, std::string("load all-reduce: ") + c->nccl->GetErrorString(r));
+    bsrc = c->ball.ptr;
+  }
+  CKC(c, cudaMemcpyAsync(out, bsrc, need * sizeof(double),
                          out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->st));
   CKC(c, cudaStreamSynchronize(c->st));
   return MCH_OK;
@@ -1131,4 +1235,77 @@ extern "C" void mch_destroy(mch_ctx* c) {
     for (int i = 0; i < 8; i++) cudaEventDestroy(c->ev[i]);
   if (c->st2) cudaStreamDestroy(c->st2);
   delete c;
+}
+
+// ------------------------------------------------------------------------------------------
+// multi-GPU plumbing
+extern "C" int mch_comm_id(void* id, size_t id_len) {
+  if (!id || id_len < sizeof(ncclUniqueId)) return fail(nullptr, MCH_EINVAL, "id buffer too small (128 bytes)");
+  std::string err;
+  const NcclApi* api = nccl_api(err);
+  if (!api) return fail(nullptr, MCH_ENCCL, err);
+  ncclUniqueId u;
+  const ncclResult_t r = api->GetUniqueId(&u);
+  if (r != ncclSuccess) return fail(nullptr, MCH_ENCCL, api->GetErrorString(r));
+  memcpy(id, &u, sizeof(u));
+  return MCH_OK;
+}
+
+extern "C" int mch_comm_init(void** comm, int world, int rank, const void* id, size_t id_len) {
+  if (!comm || !id || id_len < sizeof(ncclUniqueId) || world < 1 || rank < 0 || rank >= world)
+    return fail(nullptr, MCH_EINVAL, "bad communicator arguments");
+  std::string err;
+  const NcclApi* api = nccl_api(err);
+  if (!api) return fail(nullptr, MCH_ENCCL, err);
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof(u));
+  ncclComm_t cm = nullptr;
+  const ncclResult_t r = api->CommInitRank(&cm, world, u, rank);
+  if (r != ncclSuccess) return fail(nullptr, MCH_ENCCL, api->GetErrorString(r));
+  *comm = cm;
+  return MCH_OK;
+}
+
+extern "C" int mch_comm_destroy(void* comm) {
+  if (!comm) return MCH_OK;
+  std::string err;
+  const NcclApi* api = nccl_api(err);
+  if (!api) return fail(nullptr, MCH_ENCCL, err);
+  const ncclResult_t r = api->CommDestroy(reinterpret_cast<ncclComm_t>(comm));
+  return r == ncclSuccess ? MCH_OK : fail(nullptr, MCH_ENCCL, api->GetErrorString(r));
+}
+
+extern "C" int mch_shard_plan(const mch_params* prm, int level, int64_t* owned, size_t owned_cap, int64_t* n_owned,
+                              int64_t* xfers, size_t xfer_cap, int64_t* n_xfers) {
+  if (!prm) return fail(nullptr, MCH_EINVAL, "NULL params");
+  mch_params p = *prm;
+  if (p.d != 2 && p.d != 3) return fail(nullptr, MCH_EINVAL, "d must be 2 or 3");
+  if (p.oversample < 1) p.oversample = 1;
+  if (p.world < 1) { p.world = 1; p.rank = 0; }
+  if (p.rank < 0 || p.rank >= p.world) return fail(nullptr, MCH_EINVAL, "bad rank/world");
+  if (level < 1 || level > p.levels) return fail(nullptr, MCH_EINVAL, "bad level");
+  HostPlan pl;
+  pl.D = p.d; pl.n = p.n; pl.M = p.M; pl.L = p.levels; pl.eta = p.eta; pl.l = p.oversample;
+  pl.interp = p.interp; pl.layout = p.layout;
+  std::string perr;
+  const int rc = pl.build(perr);
+  if (rc != 0) return fail(nullptr, rc == -8 ? MCH_EPLAN : MCH_EDIVISIBILITY, perr);
+  ShardPlan sp;
+  shard_build(pl, p.world, sp);
+  int64_t k = 0;
+  for (size_t i = 0; i < pl.S[level].size(); i++)
+    if (sp.owner[level][i] == p.rank) {
+      if (owned && (size_t)k < owned_cap) owned[k] = pl.S[level][i];
+      k++;
+    }
+  if (n_owned) *n_owned = k;
+  if (owned && (size_t)k > owned_cap) return fail(nullptr, MCH_EINVAL, "owned_cap too small");
+  const auto& xf = sp.xfer[level];
+  if (n_xfers) *n_xfers = (int64_t)xf.size();
+  if (xfers) {
+    if (xf.size() > xfer_cap) return fail(nullptr, MCH_EINVAL, "xfer_cap too small");
+    for (size_t i = 0; i < xf.size(); i++)
+      for (int j = 0; j < 3; j++) xfers[3 * i + j] = xf[i][j];
+  }
+  return MCH_OK;
 }

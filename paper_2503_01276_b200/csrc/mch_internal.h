@@ -44,6 +44,7 @@ struct LevelArgs {
   const double* Mc;        // level >= 2: per global level-n cell, N*2^D constraint weights
   const ProbDesc* probs;
   int nprob_mp;            // macropoints in this batch
+  int nprob_level;         // macropoints of S_level over all ranks (launch heuristics)
   // per-macropoint arrays (indexed by batch-local macropoint index)
   double* g0;              // [mp][ncon][n_rhs] original targets (Eqs. 3/4)
   double* g;               // [mp][ncon][n_rhs] targets of the solved problem (Eq. 12/13)

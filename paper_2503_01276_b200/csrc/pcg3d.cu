@@ -1138,7 +1138,7 @@ cudaError_t launch_pcg3d_l1(const LevelArgs& A, cudaStream_t st) {
     if (sms <= 0) sms = 148;
   }
   const int probs = A.nprob_mp * A.n_rhs;
-  const bool wide = probs >= 4 * sms;
+  const bool wide = A.nprob_level * A.n_rhs >= 4 * sms;  // level-global: same kernel on every rank
   auto go = [&](auto k, int nw) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
