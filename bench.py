@@ -1,14 +1,21 @@
-"""Benchmark of the hot path (Algorithm 1 lines 3-7 for every level) on the
-BASELINE workload: configs[1] (config 2: 2D 1024², ε = 1/128, contrast 1e3, L = 3, η = 2,
-33×33 macropoints, 2 continua, 6 cell problems per macropoint).
+"""Benchmark of the hot path (Algorithm 1 lines 3-7 for every level).
 
-One "step" = mch_solve_level(1..L) + mch_effective_coeffs on the device-resident medium
-(every macropoint of every level, all N(1+d) cell problems, the Eq. (7) reductions).
-value = cell-problem solves / s (whole job, all ranks).  `e2e` repeats the step through the
-C ABI with HOST buffers: mch_create from pinned host κ/ψ (H2D inside), solve, coefficients
-copied back to pinned host memory, destroy.
+Headline workload: BASELINE.json configs[4] = config 5, the largest config (3D 256³, ε = 1/32,
+contrast 1e3, L = 4, η = 2, 17³ = 4913 macropoints, 2 continua, 8 cell problems per macropoint) and
+the north star's scaling config.  BASELINE.json's metric names no config, so the largest one is
+the headline; `--config 2..4` runs the others (their per-level numbers are also printed beside the
+headline under "other_configs").
+
+One "step" = mch_solve_level(1..L) + mch_effective_coeffs on the device-resident medium: every
+macropoint of every level, all N(1+d) cell problems, the Eq. (7) reductions.
+value = cell-problem solves / s of the whole job (all ranks).  `e2e` repeats the step through the
+C ABI with HOST buffers on an already planned context: mch_set_medium from pinned host κ/ψ (H2D
+inside the timed region), the levels, mch_effective_coeffs into a pinned host buffer (D2H).
 
   python bench.py [--gpus N --steps K --warmup W --config C --impl {mch,reference}]
+
+With --gpus N > 1 outside torchrun the script re-launches itself under torch.distributed.run
+(one rank per GPU, NCCL); it fails loudly if fewer than N GPUs are visible.
 """
 from __future__ import annotations
 
@@ -16,6 +23,7 @@ import argparse
 import json
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -27,6 +35,7 @@ from mch_inputs import CONFIGS, make_medium  # noqa: E402
 
 METRIC = "cell-problem solves/sec per level (L, η, d); HBM GB/s vs B200 ~8 TB/s"
 UNIT = "cell-problem solves/s"
+HEADLINE = 5
 
 
 def _args():
@@ -34,17 +43,28 @@ def _args():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=HEADLINE)
     ap.add_argument("--impl", default="mch", choices=["mch", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-others", action="store_true", help="skip the per-level lines of the other configs")
     return ap.parse_args()
 
 
 def _peaks():
     try:
-        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured (MEASURED_PEAKS.json)"
     except Exception:
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def _device_peaks():
+    """FP64 FMA and shared-memory peaks measured on this GPU (lib/mch_peaks, DFMA / LDS loops)."""
+    exe = os.path.join(ROOT, "paper_2503_01276_b200", "lib", "mch_peaks")
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout.strip().splitlines()[-1]
+        return json.loads(out)
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
 
 
 # ------------------------------------------------------------------------------------------
@@ -99,30 +119,51 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------------
-def _oracle_sample(cfg, kap, ids, workers):
-    """Oracle (as it stands) on the vertex sub-box k ∈ [0, 2^(L-1)·2]^d of the workload, levels
-    in order with a process pool; returns (cpu-seconds per macropoint per level, sample text)."""
-    from oracle import Oracle
-    from oracle.hmh import run_parallel
-    o = Oracle.from_config(cfg, kap, ids)
-    span = 2 * cfg.eta ** (cfg.L - 1)
-    pts = [[k for k in o.plan.S(lev) if max(k) <= span] for lev in range(1, cfg.L + 1)]
-    walls, used = run_parallel(o, pts, workers=workers)
-    per = []
-    for lev, p in enumerate(pts, start=1):
-        per.append(sum(o.timings[tuple(k)] for k in p) / len(p))
-    sample = (f"oracle on vertex sub-box k∈[0,{span}]^{cfg.d} of {cfg.name} "
-              f"({'/'.join(str(len(p)) for p in pts)} macropoints at levels 1..{cfg.L}), "
-              f"per-level cpu-seconds/macropoint extrapolated to all {(cfg.M + 1) ** cfg.d}")
-    return per, sample, used, sum(walls)
+# CPU oracle sample (cpu_baseline and --impl reference).  The oracle is test infrastructure; only
+# these two legs of bench.py run it.
+def _sample_points(cfg):
+    """One macropoint per level along the x-axis edge: the corner (0,..,0) at level 1 and
+    (η^{L-n}, 0, ..) at level n >= 2 (a chain: each is a child of the previous)."""
+    d = cfg.d
+    pts = [(0,) * d]
+    for lev in range(2, cfg.L + 1):
+        pts.append((cfg.eta ** (cfg.L - lev),) + (0,) * (d - 1))
+    return pts
 
 
-def _oracle_value(cfg, per, cores):
-    from oracle.planner import Plan
-    pl = Plan(cfg.d, cfg.n, cfg.M, cfg.L, cfg.eta, cfg.l)
-    counts = [len(pl.S(l)) for l in range(1, cfg.L + 1)]
-    t = sum(c * p for c, p in zip(counts, per)) / cores
-    return sum(counts) * cfg.n_rhs / t
+class OracleSample:
+    def __init__(self, cfg, kap, ids):
+        from oracle import Oracle
+        self.cfg = cfg
+        self.o = Oracle.from_config(cfg, kap, ids)
+        self.pts = _sample_points(cfg)
+        self.warm = False
+
+    def step(self):
+        """cpu-seconds per macropoint at each level: the sampled points are re-solved with their
+        parents' solutions cached (the first call solves the whole ancestry once, untimed)."""
+        o = self.o
+        if not self.warm:
+            for k in self.pts:
+                o.solve(k)
+            self.warm = True
+        per = []
+        for k in self.pts:
+            o.cache.pop(tuple(k), None)
+            t0 = time.process_time()
+            o.solve(k)
+            per.append(time.process_time() - t0)
+        return per
+
+    def value(self, per):
+        counts = [len(self.o.plan.S(lev)) for lev in range(1, self.cfg.L + 1)]
+        cpu_s = sum(c * p for c, p in zip(counts, per))  # one core
+        return sum(counts) * self.cfg.n_rhs / cpu_s
+
+    def text(self):
+        return (f"oracle (sparse LU, one core) on one macropoint per level of {self.cfg.name} along the x-axis edge "
+                f"{self.pts} with parents cached, cpu-seconds per macropoint x |S_n|; these clipped boundary "
+                f"windows are the cheapest of each level, so the rate is an upper bound for the CPU")
 
 
 def run_reference(a):
@@ -131,65 +172,75 @@ def run_reference(a):
         return
     cfg = CONFIGS[a.config]
     kap, ids = make_medium(cfg)
-    cores = len(os.sched_getaffinity(0))
+    smp = OracleSample(cfg, kap, ids)
     vals = []
-    sample = ""
     for step in range(a.warmup + a.steps):
-        per, sample, used, wall = _oracle_sample(cfg, kap, ids, cores)
+        per = smp.step()
         if step >= a.warmup:
-            vals.append(_oracle_value(cfg, per, used))
+            vals.append(smp.value(per))
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "d": cfg.d, "fine": f"{cfg.n}^{cfg.d}", "L": cfg.L,
-                       "eta": cfg.eta, "macropoints": (cfg.M + 1) ** cfg.d, "n_rhs": cfg.n_rhs},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": "oracle", "sample": sample},
+            "config": _config_block(cfg, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": smp.text()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# ------------------------------------------------------------------------------------------
-def main():
-    a = _args()
-    if a.impl == "reference":
-        return run_reference(a)
-    import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2503_01276_b200.parallel import ShardedHomogenizer
+def _config_block(cfg, world):
+    return {"workload": cfg.name, "d": cfg.d, "fine": f"{cfg.n}^{cfg.d}", "H": f"1/{cfg.M}", "L": cfg.L,
+            "eta": cfg.eta, "N": cfg.N, "macropoints": (cfg.M + 1) ** cfg.d, "n_rhs": cfg.n_rhs,
+            "cell_problems_per_step": (cfg.M + 1) ** cfg.d * cfg.n_rhs,
+            "parallelism": f"macropoint-shard x{world}"}
 
-    cfg = CONFIGS[a.config]
-    kap, ids = make_medium(cfg)
-    kd = torch.from_numpy(kap).cuda()
-    idd = torch.from_numpy(ids).cuda()
+
+# ------------------------------------------------------------------------------------------
+def _flops_per_node_iter(d, level):
+    """algorithmic FP64 flops per (level-n node, rhs, PCG iteration): the stencil (2 per
+    coefficient: 9-point 2D, 27-point 3D levels >= 2; the 3D level-1 element form, 8 cells x 6)
+    plus 14 for the vector updates, dot products and the Jacobi scaling"""
+    if d == 2:
+        return 2 * 9 + 14
+    return (48 if level == 1 else 2 * 27) + 14
+
+
+def _level_bound(d, level):
+    """the 3D level-1/2 windows (22.4 / 4.9 MB of PCG state per macropoint) stream
+    through L2/HBM; every 2D level and the 3D levels >= 3 keep the iteration on chip (FP64 / issue
+    bound)"""
+    return "hbm" if (d == 3 and level <= 2) else "alu"
+
+
+def _plain_nodes(cfg):
+    """Σ over all macropoints of the fine window nodes: the solver DOFs of the plain (L = 1) method
+    on the same macropoints, for the cost model"""
+    c, n, w2 = cfg.n // cfg.M, cfg.n, 3 * (cfg.n // cfg.M)
+    per_dim = []
+    for k in range(cfg.M + 1):
+        lo = max(0, 2 * k * c - w2) // 2
+        hi = min(2 * n, 2 * k * c + w2) // 2
+        per_dim.append(hi - lo + 1)
+    s = sum(per_dim)
+    return s ** cfg.d
+
+
+def _run_config(cfg, kd, idd, rank, world, steps, warmup, flush, st, barrier, collect=True):
+    import torch
+    from paper_2503_01276_b200.parallel import ShardedHomogenizer
     sh = ShardedHomogenizer(cfg, kd, idd, rank, world)
-    n_cell = (cfg.M + 1) ** cfg.d * cfg.n_rhs
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
-    st = torch.cuda.current_stream()
+    Gd = torch.empty(((cfg.M + 1) ** cfg.d, cfg.n_rhs, cfg.n_rhs), dtype=torch.float64, device="cuda")
 
     def step():
         sh.reset()
         sh.solve_all()
-        return sh.effective_coeffs()
+        sh.effective_coeffs(Gd)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    for _ in range(a.warmup):
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    ms, levels, launches = [], [], 0
-    for _ in range(a.steps):
+    ms, levels = [], []
+    for _ in range(steps):
         flush.fill_(1.0)
         barrier()
         torch.cuda.synchronize()
@@ -200,48 +251,130 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ms.append(e0.elapsed_time(e1))
-        levels.append([sh.h.level_stats(l) for l in range(1, cfg.L + 1)])
-        launches += sum(s["launches"] for s in levels[-1])
+        levels.append([sh.h.level_stats(lev) for lev in range(1, cfg.L + 1)])
+    return sh, Gd, ms, levels
+
+
+def _per_level(cfg, levels, world, peaks_hbm, fp64_tf):
+    out = []
+    nsteps = len(levels)
+    for li in range(cfg.L):
+        lev = li + 1
+        avg = lambda key: sum(s[li][key] for s in levels) / nsteps  # noqa: E731
+        st = levels[-1][li]
+        bound = _level_bound(cfg.d, lev)
+        pcg_ms = avg("ms_pcg")
+        if bound == "hbm":
+            ach = avg("pcg_bytes") / (pcg_ms * 1e-3) / 1e9
+            frac, unit = ach / peaks_hbm, "GB/s"
+        else:
+            ach = avg("node_iters") * _flops_per_node_iter(cfg.d, lev) / (pcg_ms * 1e-3) / 1e12
+            frac, unit = (ach / fp64_tf if fp64_tf else None), "TFLOP/s"
+        out.append({"level": lev, "macropoints": st["macropoints"], "ms": round(avg("ms_total"), 3),
+                    "cell_solves_per_s": round(st["problems"] / (avg("ms_total") * 1e-3), 1),
+                    "macropoint_solves_per_s": round(st["macropoints"] / (avg("ms_total") * 1e-3), 1),
+                    "pcg_ms": round(pcg_ms, 3), "fine_pass_ms": round(avg("ms_setup") + avg("ms_gram"), 3),
+                    "comm_ms": round(avg("ms_comm"), 3),
+                    "avg_iters": round(st["iters_total"] / max(1, st["problems"]), 1), "max_iters": st["iters_max"],
+                    "node_iters": st["node_iters"], "unknowns_level": st["unknowns_level"],
+                    "pcg_bound": bound, "pcg_achieved": round(ach, 3), "pcg_unit": unit,
+                    "pcg_frac": (round(frac, 4) if frac is not None else None),
+                    "rank_deficient": st["rank_deficient"], "launches": st["launches"]})
+    return out
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        return run_reference(a)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.gpus > 1 and "RANK" not in os.environ:
+        import torch
+        if torch.cuda.device_count() < a.gpus:
+            print(json.dumps({"error": f"--gpus {a.gpus} but {torch.cuda.device_count()} GPU(s) visible"}), flush=True)
+            sys.exit(2)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000), __file__] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if a.gpus != world:
+        print(json.dumps({"error": f"--gpus {a.gpus} but WORLD_SIZE={world}"}), flush=True)
+        sys.exit(2)
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev_peaks = _device_peaks() if rank == 0 else {}
+    cfg = CONFIGS[a.config]
+    kap, ids = make_medium(cfg)
+    kd = torch.from_numpy(kap).cuda()
+    idd = torch.from_numpy(ids).cuda()
+    n_cell = (cfg.M + 1) ** cfg.d * cfg.n_rhs
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+    st = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    sh, Gd, ms, levels = _run_config(cfg, kd, idd, rank, world, a.steps, a.warmup, flush, st, barrier)
     clk = clocks.stop()
     t = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item())
     value = n_cell / (ms_step * 1e-3)
+    launches = sum(s["launches"] for s in levels[-1]) + 1  # + the coefficient gather / copy
 
-    # dominant kernel launch: the PCG launch of the level with the largest PCG device time (one
-    # launch per level and batch; config 2: level 2 since the level-1 Z^T r recurrence, see
-    # profiles/r01_launches_c2_final.csv).  achieved = algorithmic bytes of that launch / its device
-    # time (CUDA events on the library stream, mean over steps).
     pk, pk_src = _peaks()
-    lev = max(range(cfg.L), key=lambda l: sum(st_[l]["ms_pcg"] for st_ in levels))
-    l1_b = sum(st_[lev]["pcg_bytes"] for st_ in levels) / len(levels)
-    l1_ms = sum(st_[lev]["ms_pcg"] for st_ in levels) / len(levels)
-    achieved = l1_b / (l1_ms * 1e-3) / 1e9
-    all_b = sum(s["pcg_bytes"] for st_ in levels for s in st_) / len(levels)
-    all_ms = sum(s["ms_pcg"] for st_ in levels for s in st_) / len(levels)
+    fp64_tf = dev_peaks.get("fp64_tflops") if isinstance(dev_peaks, dict) else None
+    per_level = _per_level(cfg, levels, world, pk["hbm_gbs"], fp64_tf)
+    # dominant kernel: the PCG launch of the level with the largest PCG device time
+    dom = max(per_level, key=lambda r: r["pcg_ms"])
+    lev = dom["level"]
+    kname = ("k_pcg2d" if cfg.d == 2 else ("k_pcg3d_l1" if lev == 1 else ("k_pcg3d_w7" if lev == cfg.L and cfg.L >= 4
+                                                                          else "k_pcg3d"))) + f" level-{lev} launch"
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "pcg_dram_per_launch_r01.json")  # ncu, same launch
+    prof = os.path.join(ROOT, "profiles", "r02_dram_per_launch.json")  # ncu --set full, same launch
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(cfg.name, {}).get(f"dram_bytes_pcg_L{lev + 1}_launch")
+            traffic = json.load(open(prof)).get(cfg.name, {}).get(f"dram_bytes_pcg_L{lev}_launch")
         except Exception:
             traffic = None
-    kname = ("k_pcg2d" if cfg.d == 2 else ("k_pcg3d_l1" if lev == 0 else "k_pcg3d")) + \
-        f" level-{lev + 1} launch (on-chip projected PCG)"
-    per_level = []
-    for l in range(cfg.L):
-        s = levels[-1][l]
-        per_level.append({"level": l + 1, "macropoints": s["macropoints"], "ms": round(s["ms_total"], 3),
-                          "cell_solves_per_s": round(s["problems"] / (s["ms_total"] * 1e-3), 1),
-                          "avg_iters": round(s["iters_total"] / max(1, s["problems"]), 1),
-                          "pcg_ms": round(s["ms_pcg"], 3),
-                          "pcg_GBps": round(s["pcg_bytes"] / max(s["ms_pcg"], 1e-9) / 1e6, 1),
-                          "rank_deficient": s["rank_deficient"]})
+    li = lev - 1
+    alg_b = sum(s[li]["pcg_bytes"] for s in levels) / len(levels)
+    if dom["pcg_bound"] == "hbm":
+        roof = {"kernel": kname, "bound": "hbm", "achieved": dom["pcg_achieved"], "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": dom["pcg_frac"], "traffic": traffic,
+                "algorithmic_bytes_per_launch": alg_b, "launch_ms": dom["pcg_ms"], "peak_source": pk_src,
+                "algorithmic_bytes": "SURVEY 8(d): 8*(6*nodes*iters per problem + D_n*cells*max_iters per "
+                                     "macropoint), D_n = 1 (level 1) / 19 (3D levels >= 2)"}
+    else:
+        roof = {"kernel": kname, "bound": "alu", "achieved": dom["pcg_achieved"], "peak": fp64_tf, "unit": "TFLOP/s",
+                "frac": dom["pcg_frac"], "traffic": traffic, "launch_ms": dom["pcg_ms"],
+                "peak_source": "measured FP64 FMA loop (lib/mch_peaks)",
+                "algorithmic_flops": "node-iterations x (2 x stencil coefficients + 14)"}
+    # P10: the paper's cost model: hierarchical solver DOFs / plain-method DOFs
+    # vs the model L eta^((1-L) d)
+    uk = torch.tensor([float(s["unknowns_level"]) for s in levels[-1]], dtype=torch.float64, device="cuda")
+    ni = torch.tensor([float(s["node_iters"]) for s in levels[-1]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(uk)
+        dist.all_reduce(ni)
+    plain = _plain_nodes(cfg)
+    p10 = {"hier_nodes_per_level": [int(v) for v in uk.tolist()], "plain_nodes": plain,
+           "measured_ratio": float(uk.sum().item()) / plain,
+           "model_ratio": cfg.L * cfg.eta ** ((1 - cfg.L) * cfg.d),
+           "node_iters_per_level": [int(v) for v in ni.tolist()],
+           "note": "PAPER.md:488-498: per level (DOFs per local problem) x (macropoints); plain = every "
+                   "macropoint on the fine mesh (level 1), model L*eta^((1-L)d)"}
 
-    # e2e through the C ABI with HOST buffers: every step uploads the medium from pinned host
-    # memory into the (already planned) context with mch_set_medium, solves all levels and reads
-    # the coefficients back into pinned host memory — all inside the timed region
+    # e2e through the C ABI with HOST buffers
     kh = torch.from_numpy(kap).pin_memory()
     ih = torch.from_numpy(ids).pin_memory()
     Gh = torch.zeros(((cfg.M + 1) ** cfg.d, cfg.n_rhs, cfg.n_rhs), dtype=torch.float64).pin_memory()
@@ -252,9 +385,9 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        sh.set_medium(kh, ih)
+        sh.set_medium(kh, ih)       # mch_set_medium, host pointers: H2D + device validation
         sh.solve_all()
-        Gh.copy_(sh.effective_coeffs(), non_blocking=True)
+        sh.effective_coeffs(Gh)     # mch_effective_coeffs into pinned host memory: D2H, synchronises
         e1.record(st)
         torch.cuda.synchronize()
         if i >= a.warmup:
@@ -263,40 +396,51 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = n_cell / (float(te.item()) * 1e-3)
+    sh.close()
 
+    others = {}
+    if not a.no_others and world == 1:
+        for cid in (2, 3, 4, 5):
+            if cid == a.config:
+                continue
+            c2 = CONFIGS[cid]
+            k2, i2 = make_medium(c2)
+            sh2, _, ms2, lv2 = _run_config(c2, torch.from_numpy(k2).cuda(), torch.from_numpy(i2).cuda(), rank, world,
+                                           2, 1, flush, st, barrier)
+            sh2.close()
+            m2 = sum(ms2) / len(ms2)
+            others[c2.name] = {"ms_per_step": round(m2, 3),
+                               "cell_solves_per_s": round((c2.M + 1) ** c2.d * c2.n_rhs / (m2 * 1e-3), 1),
+                               "per_level": _per_level(c2, lv2, world, pk["hbm_gbs"], fp64_tf)}
+
+    conf = _config_block(cfg, world)
+    conf.update({"l2": "flushed between timed steps (512 MB write)",
+                 "macropoint_solves_per_s": (cfg.M + 1) ** cfg.d / (ms_step * 1e-3), "per_level": per_level,
+                 "cost_model_P10": p10})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "d": cfg.d, "fine": f"{cfg.n}^{cfg.d}", "H": f"1/{cfg.M}",
-                   "L": cfg.L, "eta": cfg.eta, "N": cfg.N, "macropoints": (cfg.M + 1) ** cfg.d,
-                   "n_rhs": cfg.n_rhs, "cell_problems_per_step": n_cell,
-                   "parallelism": f"macropoint-shard x{world}",
-                   "l2": "flushed between timed steps (512 MB write)",
-                   "macropoint_solves_per_s": (cfg.M + 1) ** cfg.d / (ms_step * 1e-3),
-                   "per_level": per_level},
-        "roofline": {"kernel": kname, "bound": "hbm",
-                     "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-                     "algorithmic_bytes_per_launch": l1_b, "launch_ms": l1_ms,
-                     "all_levels_pcg_GBps": all_b / (all_ms * 1e-3) / 1e9,
-                     "peak_source": pk_src,
-                     "algorithmic_bytes": "8*(6*nodes*iters per problem + D_n*cells*max_iters per macropoint), D_n = 1 (L1) / 5 (2D) / 19 (3D)",
-                     "note": "SURVEY 8(d) streaming bytes per PCG iteration; the kernel keeps its state on chip (DRAM traffic = 'traffic') and is issue/latency bound; the two-level preconditioner trades work per iteration for 3x fewer iterations, which lowers this per-iteration fraction while raising solves/s - DESIGN.md 6"},
-        "e2e": {"value": e2e_value, "unit": UNIT,
-                "h2d_bytes_per_step": kap.nbytes + ids.nbytes,
-                "d2h_bytes_per_step": Gh.numel() * 8},
-        "gpu_launches": launches // a.steps,
+        "config": conf,
+        "roofline": roof,
+        "device_peaks": dev_peaks,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": kap.nbytes + ids.nbytes,
+                "d2h_bytes_per_step": Gh.numel() * 8,
+                "path": "mch_set_medium (pinned host kappa/ids) + mch_solve_level 1..L + mch_effective_coeffs "
+                        "(pinned host out)"},
+        "gpu_launches": launches,
         "clocks": clk,
+        "other_configs": others,
     }
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cores = len(os.sched_getaffinity(0))
-        per, sample, used, wall = _oracle_sample(cfg, kap, ids, cores)
-        line["cpu_baseline"] = {"value": _oracle_value(cfg, per, used), "unit": UNIT, "cores": used,
-                                "kind": "oracle", "sample": sample, "wall_s": round(wall, 2)}
+        smp = OracleSample(cfg, kap, ids)
+        t0 = time.time()
+        smp.step()  # ancestry once
+        per = smp.step()
+        line["cpu_baseline"] = {"value": smp.value(per), "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": smp.text(), "wall_s": round(time.time() - t0, 1)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    sh.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -112,6 +112,8 @@ typedef struct {
                               constraints imposed in the least-squares sense) */
   double   ms_comm;        /* device time of the parent exchange after this level (world > 1) */
   double   bytes_comm;     /* bytes this rank sent + received in that exchange */
+  double   node_iters;     /* sum over problems of level-n window nodes x PCG iterations (the
+                              solver work of the paper's cost model) */
 } mch_level_stats;
 
 /* Algorithm 1 REQUIRE (macropoint set T, coarsening factor eta, fine mesh h,

@@ -21,7 +21,7 @@ FLAGS_C = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-s
 
 
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(os.path.join(os.path.dirname(LIB), "mch_peaks")):
         return True
     t = os.path.getmtime(LIB)
     for f in os.listdir(CSRC):
@@ -65,6 +65,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write("\n".join(log_parts)[-8000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     os.replace(LIB + ".tmp", LIB)
+    # measured FP64 / shared-memory peaks for the roofline (bench.py), a standalone executable
+    peaks = os.path.join(libdir, "mch_peaks")
+    res = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o", peaks,
+                          os.path.join(CSRC, "peaks.cu")], capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed for peaks.cu:\n" + res.stderr[-4000:])
     if verbose:
         print("\n".join(log_parts))
     return LIB

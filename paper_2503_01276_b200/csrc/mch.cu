@@ -883,6 +883,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
         mx = std::max(mx, it);
         S.relres_max = std::max(S.relres_max, B.h_relres[i * nr + r]);
         S.pcg_bytes += 8.0 * 6.0 * (double)ln * it;
+        S.node_iters += (double)ln * it;
       }
       S.iters_max = std::max<int64_t>(S.iters_max, mx);
       S.unknowns_level += ln;
