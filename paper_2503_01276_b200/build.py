@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libmch.so")
-SOURCES = ["mch.cu", "kernels.cu", "pcg2d.cu", "pcg3d.cu", "fine3d.cu", "macro.cu", "fine.cu", "plan.cpp", "shard.cpp", "comm.cpp"]
+SOURCES = ["mch.cu", "kernels.cu", "pcg2d.cu", "pcg3d.cu", "pcg3d_cl.cu", "fine3d.cu", "macro.cu", "fine.cu", "plan.cpp", "shard.cpp", "comm.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # dev variants: MCH_BUILD_TIMING=1 builds lib/libmch_timing.so with per-phase PCG cycle counters;
 # MCH_BUILD_TAG=t MCH_BUILD_DEFS="-DX=1 ..." builds lib/libmch_t.so with extra defines

@@ -37,6 +37,10 @@ cudaError_t launch_node_ops3d(const LevelArgs& A, int max_nodes, cudaStream_t st
 cudaError_t launch_pcg3d(const LevelArgs& A, int nxm, cudaStream_t st);
 // level 1 (windows of <= 49 fine nodes per side)
 size_t pcg3d_l1_smem(int N);
+// level 1 with a thread-block cluster of cs CTAs per problem (pcg3d_cl.cu)
+size_t pcg3d_l1c_smem(int N);
+int pcg3d_l1c_cluster(int level_problems, int sms);
+cudaError_t launch_pcg3d_l1c(const LevelArgs& A, int cs, cudaStream_t st);
 // windows of <= 7 level nodes per side, N <= 2: one CTA per macropoint, one warp per rhs
 size_t pcg3d_w7_smem(int N);
 cudaError_t launch_pcg3d_w7(const LevelArgs& A, cudaStream_t st);

@@ -94,6 +94,7 @@ struct LevelBatch {
   bool crs2d = false;   // the on-chip 2D variant was planned with the coarse space (shared memory, TMEM)
   bool fused3 = false;  // 3D level >= 2: fused fine passes (fine3d.cu), no FI/FY workspace
   int max_kp = 0;       // K_p node-box size (FK slot) of the fused path
+  int l1cs = 1;         // 3D level 1: CTAs per problem (thread-block cluster, pcg3d_cl.cu)
   bool w7 = false;      // 3D level >= 2, <= 7 level nodes per side: block PCG, one warp per rhs (k_pcg3d_w7)
   bool tsplit = false;  // 3D transport through k_pcg3d_l1<MODE 1> (fine windows <= 49 nodes per side)
   int nxm3 = 0;
@@ -385,7 +386,7 @@ struct LevelVariant {
   bool on2d = false, l1op = false, crs2d = false;
   int variant = -1, threads2 = 0, tm_cols = 32, rpt = 0;
   bool on3d = false, w7 = false, tsplit = false, fused3 = false;
-  int nxm3 = 0;
+  int nxm3 = 0, l1cs = 1;
   int th_l = 64, th_f = 64;
   int max_kp = 0;
   bool coarse = false;
@@ -491,6 +492,11 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     } else if (gmaxn <= 49 && pcg3d_l1_smem(N) <= 232448) {
       V.on3d = true;
       V.nxm3 = 49;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      V.l1cs = pcg3d_l1c_cluster((int)Sl.size() * nr, sms);  // level-global count: same on every rank
+      if (pcg3d_l1c_smem(N) > 232448 || (getenv("MCH_L1_OLD") && atoi(getenv("MCH_L1_OLD")))) V.l1cs = 0;  // 0: k_pcg3d_l1
     }
   }
   // two-level preconditioner: level 1 everywhere; level 2 on the 49-node on-chip 2D variant,
@@ -597,6 +603,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     }
     B->on3d = V.on3d;
     B->nxm3 = V.nxm3;
+    B->l1cs = V.l1cs;
     B->w7 = V.w7;
     B->tsplit = V.tsplit;
     B->fused3 = V.fused3;
@@ -790,6 +797,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       A.dbg = dbgp;
     }
     if (B.on2d) CKC(c, launch_pcg2d(A, B.variant, B.threads2, st));
+    else if (B.on3d && level == 1 && B.l1cs > 0) CKC(c, launch_pcg3d_l1c(A, B.l1cs, st));
     else if (B.on3d && level == 1) CKC(c, launch_pcg3d_l1(A, st));
     else if (B.w7) CKC(c, launch_pcg3d_w7(A, st));
     else if (B.on3d) CKC(c, launch_pcg3d(A, B.nxm3, st));

@@ -1,0 +1,744 @@
+// 3D level-1 projected PCG with a thread-block cluster per problem (sm_100a).
+//
+// Same method and arithmetic per node as k_pcg3d_l1 (pcg3d.cu): for each problem (macropoint p,
+// right-hand side r) the constrained cell problem of Eqs. (3)/(4) on the fine
+// window, projected Jacobi-PCG with the residual re-projected every iteration and the two-level
+// (inclusion coarse space) preconditioner (readings R16, R19).
+//
+// A 49^3 window does not fit on chip, and one CTA per problem leaves the
+// iteration latency-bound: config 5 has 216 problems on 148 SMs (1.46 waves) and its slowest
+// problem sets the level time.  Here a cluster of CS CTAs shares one problem: CTA c walks the
+// node planes z in [c nz / CS, (c+1) nz / CS) (each with all 98 row tasks of the plane), p, r, q, x
+// stay in global memory (L2), the p planes at the slab boundaries are read from the neighbour's
+// slab after the cluster barrier (barrier.cluster also invalidates L1, so they come from L2), and
+// every reduction — the scalars rz, pq, rr and the constraint vector c = C D^-1 r — is formed per
+// CTA, published in shared memory and summed over the cluster's CTAs in rank order through DSMEM.
+// Three cluster barriers per iteration; every CTA then holds identical scalars, so all take the same
+// branch and the projector solve (S^+ c) is done redundantly per CTA.  Fixed summation orders
+// throughout: bitwise reproducible.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "kernels.h"
+#include "pcg3d_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+struct VA { double r, p, x, d; int cm; };  // pass A loads of one node
+struct VC { double r, q, d; };             // pass C loads
+struct VX { double x, d; int cm; };        // x / D^-1 / component of one node
+}  // namespace
+
+template <int N, int NW, int CS>
+__global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1c(LevelArgs A) {
+  constexpr int NT = 98;  // at most 98 row tasks = 49 rows x 2 segments
+  constexpr int NQ = 27 * N;
+  cg::cluster_group cl = cg::this_cluster();
+  const int cr = (int)cl.block_rank();
+  const int prob = blockIdx.x / CS;
+  const int mp = prob / A.n_rhs, rhs = prob - mp * A.n_rhs;
+  const ProbDesc& P = A.probs[mp];
+  const int* ncv = P.nc;
+  const int nx = ncv[0] + 1, ny = ncv[1] + 1, nz = ncv[2] + 1, nn = nx * ny * nz;
+  const int ncx = nx - 1, ncy = ny - 1, ncz = nz - 1;
+  const int nc = A.ncon;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int z0 = (cr * nz) / CS, z1 = ((cr + 1) * nz) / CS;  // this CTA's node planes
+
+  extern __shared__ __align__(16) double smem[];
+  double* bins = smem;          // [NT task rows][NQ]
+  double* Ysh = bins + NT * NQ;  // [NQ]
+  double* csh = Ysh + NQ;        // [NQ]
+  double* slots = csh + NQ;      // [5][32]
+  double* zr = slots + 5 * 32;   // [256] coarse: E^-1 Z^T r
+  double* vv = zr + 256;         // [256] coarse: coarse part of z
+  double* red = vv + 256;        // [3][NQ + 2] cluster reduction buffers (published partials)
+  int* zsm = reinterpret_cast<int*>(red + 3 * (NQ + 2));  // [49][3]
+  __shared__ double bc[2];       // broadcast scalars
+  for (int i = threadIdx.x; i < NT * NQ + 2 * NQ + 5 * 32; i += blockDim.x) bins[i] = 0.0;
+  for (int z = threadIdx.x; z < nz; z += blockDim.x) {
+    const Sides sd = sides_of(A, P, 2, z, ncz, 1);
+    zsm[z * 3] = sd.pm;
+    zsm[z * 3 + 1] = sd.k0;
+    zsm[z * 3 + 2] = sd.k1;
+  }
+  __syncthreads();
+
+  int t = 0, y = 0, seg = 0, x = 0, kxe = 1000;
+  bool wact = false, lact = false;
+  Sides sx{0, 0, 0}, sy{0, 0, 0};
+  const int nxy = nx * ny;
+  const int64_t n2 = (int64_t)A.n * A.n;
+  unsigned pvm = 0;   // bit dy*3+dx: p neighbour (x+dx-1, y+dy-1) inside the window
+  unsigned cvm = 0;   // bit oy*2+ox: cell (x-1+ox, y-1+oy) inside the window
+  int64_t cbase = 0;  // global index of cell (x-1, y-1, -1) of the window
+  auto tside = [](int pm, int ob) { return (pm == 3) ? ob : ((pm == 2) ? 1 : 0); };
+  auto kxy = [&](int oxy) {
+    const int ox = oxy & 1, oy = oxy >> 1;
+    const int kx = ox ? ((sx.pm == 1) ? sx.k0 : sx.k1) : sx.k0;
+    const int ky = oy ? ((sy.pm == 1) ? sy.k0 : sy.k1) : sy.k0;
+    return ky * 3 + kx;
+  };
+  int kq[4];
+  // row tasks of this window: nseg x-segments of 32 lanes per node row (1 if nx <= 32), dealt
+  // round-robin to the warps so a clipped window keeps every warp busy
+  const int nseg = (nx + 31) >> 5, ntask = ny * nseg;
+  auto set_task = [&](int tt) {
+    t = tt;
+    y = t / nseg;
+    seg = t - y * nseg;
+    x = seg * 32 + lane;
+    wact = (y < ny) && (seg * 32 < nx);
+    lact = wact && x < nx;
+    sx = lact ? sides_of(A, P, 0, x, ncx, 1) : Sides{0, 0, 0};
+    sy = wact ? sides_of(A, P, 1, y, ncy, 1) : Sides{0, 0, 0};
+    kxe = (lact && x < ncx) ? slot3(A, P, 0, x, 1) : 1000;
+    pvm = 0;
+    cvm = 0;
+    if (lact) {
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+        for (int dx = 0; dx < 3; dx++) {
+          const int xx = x + dx - 1, yy = y + dy - 1;
+          if (xx >= 0 && xx < nx && yy >= 0 && yy < ny) pvm |= 1u << (dy * 3 + dx);
+        }
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        const int ex = x - 1 + (o & 1), ey = y - 1 + (o >> 1);
+        if (ex >= 0 && ex < ncx && ey >= 0 && ey < ncy) cvm |= 1u << o;
+      }
+    }
+    cbase = ((int64_t)(P.lo[2] - 1) * A.n + (P.lo[1] + y - 1)) * A.n + (P.lo[0] + x - 1);
+#pragma unroll
+    for (int o = 0; o < 4; o++) kq[o] = kxy(o);
+  };
+  auto tasks = [&](auto&& f) {
+    for (int tt = warp; tt < ntask; tt += NW) {
+      set_task(tt);
+      f();
+    }
+  };
+
+  const double* dg = A.dinv + P.node_off;
+  double* pv = A.P + P.vec_off + (int64_t)rhs * nn;
+  double* Xv = A.X + P.vec_off + (int64_t)rhs * nn;
+  double* Rv = A.R + P.vec_off + (int64_t)rhs * nn;
+  double* Qv = A.Q + P.vec_off + (int64_t)rhs * nn;
+  const double* Si = A.Sinv + (int64_t)mp * nc * nc;
+  const double hq = 0.125 * A.h * A.h * A.h, kh = A.h * (1.0 / 12.0);
+
+  // column walker over this CTA's planes z in [z0, z1): f(z, k, id[8]) with id[o] of cell octant o
+  auto walk_ids = [&](auto&& f) {
+    int idc[8];
+    const int oxy[4] = {0, 1, (int)A.n, (int)A.n + 1};
+    const uint8_t* ip = A.ids + cbase + (int64_t)(z0 + 1) * n2;  // cell layer z0
+#pragma unroll
+    for (int o = 0; o < 4; o++) {
+      idc[o] = (((cvm >> o) & 1u) && z0 >= 1) ? __ldg(ip - n2 + oxy[o]) : 0xFF;   // layer z0 - 1
+      idc[4 + o] = (((cvm >> o) & 1u) && z0 < ncz) ? __ldg(ip + oxy[o]) : 0xFF;  // layer z0
+    }
+    int k = (z0 * ny + y) * nx + x;
+    for (int z = z0; z < z1; z++) {
+      ip += n2;
+      const bool nv = z + 1 < ncz;
+      int nxt[4];
+#pragma unroll
+      for (int o = 0; o < 4; o++) nxt[o] = (((cvm >> o) & 1u) && nv) ? __ldg(ip + oxy[o]) : 0xFF;
+      f(z, k, idc);
+      k += nxy;
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        idc[o] = idc[4 + o];
+        idc[4 + o] = nxt[o];
+      }
+    }
+  };
+  auto ct_of = [&](int z, const int (&idc)[8]) -> double {
+    const int pmz = zsm[z * 3];
+    const int kz0 = zsm[z * 3 + 1] * 9, kz1 = ((pmz == 1) ? zsm[z * 3 + 1] : zsm[z * 3 + 2]) * 9;
+    double ct = 0.0;
+#pragma unroll
+    for (int o = 0; o < 8; o++)
+      if (idc[o] != 0xFF) ct += Ysh[(((o >> 2) ? kz1 : kz0) + kq[o & 3]) * N + idc[o]];
+    return ct * hq;
+  };
+
+  // walker with the loads of the next DP-1 node planes in flight: pre(k, live) -> V is issued DP-1
+  // steps ahead of f(z, k, idc, V) (the z-walk is otherwise one memory round trip per plane)
+  constexpr int DP = 3;
+  auto walk_pf = [&](auto&& pre, auto&& f) {
+    using V = decltype(pre(0, false));
+    V ring[DP];
+    int idq[DP][4];
+    const int oxy[4] = {0, 1, (int)A.n, (int)A.n + 1};
+    const uint8_t* ip0 = A.ids + cbase + (int64_t)(z0 + 1) * n2;  // cell layer z0
+    int lo4[4];
+#pragma unroll
+    for (int o = 0; o < 4; o++) lo4[o] = (((cvm >> o) & 1u) && z0 >= 1) ? __ldg(ip0 - n2 + oxy[o]) : 0xFF;
+    auto issue = [&](V& slot, int (&iq)[4], int z) {
+      const bool live = z < z1;
+      slot = pre((z * ny + y) * nx + x, live && lact);
+      const uint8_t* ip = ip0 + (int64_t)(z - z0) * n2;
+#pragma unroll
+      for (int o = 0; o < 4; o++) iq[o] = (live && ((cvm >> o) & 1u) && z < ncz) ? __ldg(ip + oxy[o]) : 0xFF;
+    };
+#pragma unroll
+    for (int d = 0; d < DP - 1; d++) issue(ring[d], idq[d], z0 + d);
+    for (int zb = z0; zb < z1; zb += DP) {
+#pragma unroll
+      for (int d = 0; d < DP; d++) {
+        const int z = zb + d;
+        if (z < z1) {
+          issue(ring[(d + DP - 1) % DP], idq[(d + DP - 1) % DP], z + DP - 1);
+          int idc[8];
+#pragma unroll
+          for (int o = 0; o < 4; o++) {
+            idc[o] = lo4[o];
+            idc[4 + o] = idq[d][o];
+            lo4[o] = idq[d][o];
+          }
+          f(z, (z * ny + y) * nx + x, idc, ring[d]);
+        }
+      }
+    }
+  };
+
+  double acc[4][N];
+  auto acc_zero = [&]() {
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int j = 0; j < N; j++) acc[a][j] = 0.0;
+  };
+  auto acc_add = [&](int zsel, int z, const int (&idc)[8], double u) {
+    const int pmz = zsm[z * 3];
+    const double w = u * hq;
+#pragma unroll
+    for (int oz = 0; oz < 2; oz++) {
+      if (tside(pmz, oz) != zsel) continue;
+#pragma unroll
+      for (int oxy = 0; oxy < 4; oxy++) {
+        const int id = idc[oz * 4 + oxy];
+#pragma unroll
+        for (int j = 0; j < N; j++) acc[oxy][j] += (id == j) ? w : 0.0;
+      }
+    }
+  };
+  auto flush = [&](int kz) {
+    double* B = bins + t * NQ;
+#pragma unroll
+    for (int ys = 0; ys < 2; ys++) {
+      if (!((sy.pm >> ys) & 1)) continue;
+      const int ky = ys ? sy.k1 : sy.k0;
+      double g[2][N];
+#pragma unroll
+      for (int xs = 0; xs < 2; xs++)
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          double a = 0.0;
+#pragma unroll
+          for (int oxy = 0; oxy < 4; oxy++)
+            if (tside(sy.pm, oxy >> 1) == ys && tside(sx.pm, oxy & 1) == xs) a += acc[oxy][j];
+          g[xs][j] = a;
+        }
+      double v[N];
+#pragma unroll
+      for (int j = 0; j < N; j++) {
+        const double tt = __shfl_down_sync(FULLMASK, g[0][j], 1);
+        v[j] = g[1][j] + ((lane < 31) ? tt : 0.0);
+      }
+      const int kup = __shfl_up_sync(FULLMASK, kxe, 1);
+      const unsigned hm = __ballot_sync(FULLMASK, lane == 0 || kxe != kup);
+      const int head = 31 - __clz(hm & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          const double tt = __shfl_up_sync(FULLMASK, v[j], d);
+          if (lane - d >= head) v[j] += tt;
+        }
+      }
+      const bool tail = (lane == 31) || ((hm >> (lane + 1)) & 1u);
+      if (tail && kxe < 1000) {
+#pragma unroll
+        for (int j = 0; j < N; j++) B[((kz * 3 + ky) * 3 + kxe) * N + j] += v[j];
+      }
+      __syncwarp();
+      if (lane == 0 && lact && x >= 1) {
+#pragma unroll
+        for (int j = 0; j < N; j++) B[((kz * 3 + ky) * 3 + sx.k0) * N + j] += g[0][j];
+      }
+      __syncwarp();
+    }
+    acc_zero();
+  };
+  // constraint sums of u over this CTA's planes into the task bins (zeroed first)
+  auto sweep_c = [&](auto&& ufun) {
+    for (int i = lane; i < NQ; i += 32) bins[t * NQ + i] = 0.0;
+    __syncwarp();
+    acc_zero();
+    int layer = -1;
+    walk_ids([&](int z, int k, const int (&idc)[8]) {
+      const double u = ufun(z, k);
+      const int pmz = zsm[z * 3];
+      if (pmz == 3) {
+        acc_add(0, z, idc, u);
+        flush(zsm[z * 3 + 1]);
+        acc_add(1, z, idc, u);
+        layer = zsm[z * 3 + 2];
+      } else {
+        acc_add((pmz == 2) ? 1 : 0, z, idc, u);
+        layer = (pmz == 2) ? zsm[z * 3 + 2] : zsm[z * 3 + 1];
+      }
+    });
+    if (layer >= 0) flush(layer);
+  };
+  // sweep_c with pipelined loads: u = ufun(z, k, V)
+  auto sweep_c_pf = [&](auto&& pre, auto&& ufun) {
+    for (int i = lane; i < NQ; i += 32) bins[t * NQ + i] = 0.0;
+    __syncwarp();
+    acc_zero();
+    int layer = -1;
+    walk_pf(pre, [&](int z, int k, const int (&idc)[8], const auto& V) {
+      const double u = ufun(z, k, V);
+      const int pmz = zsm[z * 3];
+      if (pmz == 3) {
+        acc_add(0, z, idc, u);
+        flush(zsm[z * 3 + 1]);
+        acc_add(1, z, idc, u);
+        layer = zsm[z * 3 + 2];
+      } else {
+        acc_add((pmz == 2) ? 1 : 0, z, idc, u);
+        layer = (pmz == 2) ? zsm[z * 3 + 2] : zsm[z * 3 + 1];
+      }
+    });
+    if (layer >= 0) flush(layer);
+  };
+  // (A p)_k over this CTA's planes; p planes z0 - 1 and z1 belong to the neighbours (L2 loads)
+  auto sweep_stencil = [&](auto&& f) {
+    const double* pz = pv + (int64_t)z0 * nxy + y * nx + x;
+    const double* kp = A.kappa + cbase + (int64_t)(z0 + 1) * n2;  // cells of layer z0
+    const int oxy[4] = {0, 1, (int)A.n, (int)A.n + 1};
+    int poff[9];
+#pragma unroll
+    for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+      for (int dx = 0; dx < 3; dx++) poff[dy * 3 + dx] = (dy - 1) * nx + (dx - 1);
+    double v[3][3][3];
+    double kc[2][2][2];
+#pragma unroll
+    for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+      for (int dx = 0; dx < 3; dx++) {
+        const bool in = (pvm >> (dy * 3 + dx)) & 1u;
+        v[0][dy][dx] = (in && z0 >= 1) ? __ldcg(pz - nxy + poff[dy * 3 + dx]) : 0.0;
+        v[1][dy][dx] = in ? pz[poff[dy * 3 + dx]] : 0.0;
+      }
+#pragma unroll
+    for (int o = 0; o < 4; o++) {
+      const bool in = (cvm >> o) & 1u;
+      kc[0][o >> 1][o & 1] = (in && z0 >= 1) ? __ldg(kp - n2 + oxy[o]) : 0.0;
+      kc[1][o >> 1][o & 1] = (in && z0 < ncz) ? __ldg(kp + oxy[o]) : 0.0;
+    }
+    int k = (z0 * ny + y) * nx + x;
+    for (int z = z0; z < z1; z++) {
+      pz += nxy;
+      kp += n2;
+      const bool pn = z + 1 < nz, cn = z + 1 < ncz, halo = z + 1 >= z1;
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+        for (int dx = 0; dx < 3; dx++) {
+          const bool in = ((pvm >> (dy * 3 + dx)) & 1u) && pn;
+          const double* a = pz + poff[dy * 3 + dx];
+          v[2][dy][dx] = in ? (halo ? __ldcg(a) : *a) : 0.0;
+        }
+      double kn[4];
+#pragma unroll
+      for (int o = 0; o < 4; o++) kn[o] = (((cvm >> o) & 1u) && cn) ? __ldg(kp + oxy[o]) : 0.0;
+      double Ap = 0.0;
+#pragma unroll
+      for (int o = 0; o < 8; o++) {
+        const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+        const int a = (~o) & 7;
+        auto pv_b = [&](int b) { return v[oz + ((b >> 2) & 1)][oy + ((b >> 1) & 1)][ox + (b & 1)]; };
+        Ap += kc[oz][oy][ox] * (4.0 * pv_b(a) - pv_b(a ^ 3) - pv_b(a ^ 5) - pv_b(a ^ 6) - pv_b(a ^ 7));
+      }
+      f(z, k, Ap * kh, v[1][1][1]);
+      k += nxy;
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++)
+#pragma unroll
+        for (int dx = 0; dx < 3; dx++) {
+          v[0][dy][dx] = v[1][dy][dx];
+          v[1][dy][dx] = v[2][dy][dx];
+        }
+#pragma unroll
+      for (int o = 0; o < 4; o++) {
+        kc[0][o >> 1][o & 1] = kc[1][o >> 1][o & 1];
+        kc[1][o >> 1][o & 1] = kn[o];
+      }
+    }
+  };
+
+  auto slot_put = [&](int which, double v) {
+    v = wsum0(v);
+    if (lane == 0) slots[which * 32 + warp] = v;
+  };
+  auto slot_fin = [&](int which) { return wsum0((lane < NW) ? slots[which * 32 + lane] : 0.0); };
+  // cluster reductions: CTA partials published in red[b][0..m), summed over ranks in rank order
+  auto publish = [&](int b, int i, double v) { red[b * (NQ + 2) + i] = v; };
+  auto cluster_sum = [&](int b, int i) -> double {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < CS; r++) s += *cl.map_shared_rank(red + b * (NQ + 2) + i, r);
+    return s;
+  };
+  // csh = [sub -] cluster sum of the constraint bins (publish, cluster barrier, gather)
+  auto reduce_c_pub = [&](int b) {  // per CTA: bins over task rows -> red[b][0..nc)
+    for (int i = warp; i < nc; i += NW) {
+      double s = 0.0;
+      for (int tt = lane; tt < NT; tt += 32) s += bins[tt * NQ + i];
+      s = wsum0(s);
+      if (lane == 0) publish(b, i, s);
+    }
+  };
+  auto gather_c = [&](int b, const double* sub) {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      const double s = cluster_sum(b, i);
+      csh[i] = sub ? sub[((int64_t)mp * nc + i) * A.n_rhs + rhs] - s : s;
+    }
+  };
+  auto solve_y = [&]() {
+    double cyw = 0.0;
+    for (int i = warp; i < nc; i += NW) {
+      double s = 0.0;
+      for (int j = lane; j < nc; j += 32) s += __ldg(Si + (int64_t)i * nc + j) * csh[j];
+      s = wsum0(s);
+      if (lane == 0) Ysh[i] = s;
+      cyw += s * csh[i];
+    }
+    if (lane == 0) slots[3 * 32 + warp] = cyw;
+  };
+
+  const bool crs = A.coarse && A.ncomp[mp] > 0;
+  const int nca = crs ? A.ncomp[mp] : 0;
+  const int* cmp = A.cmap + P.node_off;
+  const int* cpt = A.cptr + (int64_t)mp * (A.ncmax + 1);
+  const int* cls = A.clist + P.node_off;
+  // coarse data staged in shared memory once: CZ [nc][nca] and E^-1 [nca]
+  double* czs = reinterpret_cast<double*>(zsm + 3 * 49 + 1) ;
+  czs = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(czs) + 15) & ~uintptr_t(15));
+  double* eis = czs + (size_t)nc * nca;
+  if (crs) {
+    const double* CZm = A.CZ + (int64_t)mp * nc * A.ncmax;
+    for (int i = threadIdx.x; i < nc * nca; i += blockDim.x) {
+      const int tq = i / nca, a = i - tq * nca;
+      czs[i] = __ldg(CZm + (int64_t)tq * A.ncmax + a);
+    }
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) eis[a] = __ldg(A.Einv + (int64_t)mp * A.ncmax + a);
+    __syncthreads();
+  }
+  // zr = E^-1 Z^T R over every component (redundant per CTA; R of the whole window is complete
+  // after the preceding cluster barrier): 4 lanes per component, up to 32 node loads in flight per
+  // lane before the fixed-order sums; slot 4, then csh += (CZ) zr.  Two block barriers.
+  auto coarse_c = [&]() {
+    double part = 0.0;
+    const int sub = lane & 3, ngrp = blockDim.x >> 2;
+    for (int a0 = threadIdx.x >> 2; a0 - (int)(threadIdx.x >> 2) < nca; a0 += ngrp) {
+      const int a = a0;
+      double sv = 0.0;
+      if (a < nca) {
+        const int i0 = __ldg(cpt + a), i1 = __ldg(cpt + a + 1);
+        for (int ib = i0 + sub; ib < i1; ib += 4 * 8) {
+          double rv[8];
+#pragma unroll
+          for (int u = 0; u < 8; u++) {
+            const int i = ib + 4 * u;
+            rv[u] = (i < i1) ? __ldcg(Rv + __ldg(cls + i)) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; u++) sv += rv[u];
+        }
+      }
+      sv += __shfl_xor_sync(FULLMASK, sv, 1);
+      sv += __shfl_xor_sync(FULLMASK, sv, 2);
+      if (a < nca && sub == 0) {
+        const double ei = eis[a];
+        zr[a] = sv * ei;
+        part += sv * sv * ei;
+      }
+    }
+    part = wsum0(part);
+    if (lane == 0) slots[4 * 32 + warp] = part;
+    __syncthreads();
+    for (int tq = warp; tq < nc; tq += NW) {
+      double sv = 0.0;
+      for (int a = lane; a < nca; a += 32) sv += czs[tq * nca + a] * zr[a];
+      sv = wsum0(sv);
+      if (lane == 0) csh[tq] += sv;
+    }
+    __syncthreads();
+  };
+  // vv = s0 zr - E^-1 (CZ)^T Ysh: one warp per component, lanes over the constraint rows.  One barrier.
+  auto coarse_v = [&](double s0) {
+    for (int a = warp; a < nca; a += NW) {
+      double ac = 0.0;
+      for (int tq = lane; tq < nc; tq += 32) ac += czs[tq * nca + a] * Ysh[tq];
+      ac = wsum0(ac);
+      if (lane == 0) vv[a] = (s0 != 0.0 ? s0 * zr[a] : 0.0) - eis[a] * ac;
+    }
+    __syncthreads();
+  };
+  auto cz_at = [&](int k) -> double {
+    if (!crs) return 0.0;
+    const int a = __ldg(cmp + k);
+    return (a >= 0) ? vv[a] : 0.0;
+  };
+
+  // init: x0 = D^-1 C^T S^-1 g0, r0 = A x0, c = C D^-1 r0, yhat = S^-1 c
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) csh[i] = A.g0[((int64_t)mp * nc + i) * A.n_rhs + rhs];
+  __syncthreads();
+  solve_y();
+  __syncthreads();
+  if (crs) coarse_v(0.0);
+  tasks([&] {
+    if (!wact) return;
+    walk_ids([&](int z, int k, const int (&idc)[8]) {
+      if (!lact) return;
+      const double x0 = dg[k] * ct_of(z, idc) - cz_at(k);
+      pv[k] = x0;
+      Xv[k] = x0;
+    });
+  });
+  cl.sync();  // x0 (= p) complete over the cluster
+  tasks([&] {
+    if (wact) sweep_stencil([&](int, int k, double Ap, double) { if (lact) Rv[k] = Ap; });
+  });
+  double rr0 = 0.0;
+  tasks([&] {
+    if (wact)
+      sweep_c([&](int, int k) -> double {
+        if (!lact) return 0.0;
+        const double rk = Rv[k];
+        const double u = dg[k] * rk;
+        rr0 += rk * u;
+        return u;
+      });
+  });
+  slot_put(2, rr0);
+  __syncthreads();
+  reduce_c_pub(2);
+  if (warp == 0) {
+    const double v = slot_fin(2);
+    if (lane == 0) publish(2, NQ, v);
+  }
+  cl.sync();  // partials published; R complete (coarse_c reads it)
+  gather_c(2, nullptr);
+  if (threadIdx.x == 0) bc[0] = cluster_sum(2, NQ);
+  __syncthreads();
+  if (crs) coarse_c();
+  solve_y();
+  __syncthreads();
+  rr0 = bc[0] + (crs ? slot_fin(4) : 0.0);
+  if (crs) coarse_v(1.0);
+
+  const double tol2 = A.rtol * A.rtol;
+  const double floor2 = 1e-30 * rr0;
+  double beta = 0.0, rz = 0.0, ref = 0.0, alpha = 0.0;
+  int it = 0, breakdown = 0;
+  for (;; it++) {
+    // pass A: x += alpha_prev p_prev, r <- r - C^T yhat, z = M^-1 r, p <- -z + beta p
+    double v = 0.0;
+    const bool first = (it == 0);
+    tasks([&] {
+      if (!wact) return;
+      walk_pf(
+          [&](int k, bool live) {
+            VA a;
+            a.r = live ? Rv[k] : 0.0;
+            a.p = (live && !first) ? pv[k] : 0.0;
+            a.x = (live && !first) ? Xv[k] : 0.0;
+            a.d = live ? dg[k] : 0.0;
+            a.cm = (live && crs) ? __ldg(cmp + k) : -1;
+            return a;
+          },
+          [&](int z, int k, const int (&idc)[8], const VA& a) {
+            if (!lact) return;
+            const double rk = a.r - ct_of(z, idc);
+            const double zz = a.d * rk + ((a.cm >= 0) ? vv[a.cm] : 0.0);
+            if (!first) Xv[k] = a.x + alpha * a.p;
+            pv[k] = first ? -zz : -zz + beta * a.p;
+            Rv[k] = rk;
+            v += rk * zz;
+          });
+    });
+    slot_put(0, v);
+    __syncthreads();
+    if (warp == 0) {
+      const double s = slot_fin(0);
+      if (lane == 0) publish(0, 0, s);
+    }
+    cl.sync();  // S1: p complete over the cluster, rz partials published
+    double w = 0.0;
+    tasks([&] {
+      if (wact)
+        sweep_stencil([&](int, int k, double Ap, double pk) {
+          if (lact) {
+            Qv[k] = Ap;
+            w += pk * Ap;
+          }
+        });
+    });
+    slot_put(1, w);
+    if (threadIdx.x == 0) bc[0] = cluster_sum(0, 0);
+    __syncthreads();
+    if (warp == 0) {
+      const double s = slot_fin(1);
+      if (lane == 0) publish(1, 0, s);
+    }
+    cl.sync();  // S2: pq partials published
+    if (threadIdx.x == 0) bc[1] = cluster_sum(1, 0);
+    __syncthreads();
+    rz = bc[0];
+    const double pq = bc[1];
+    if (it == 0) ref = rz;
+    if (!(rz > fmax(tol2 * ref, floor2)) || it >= A.max_iter) break;
+    if (!(pq > 0.0) || !isfinite(pq)) {
+      breakdown = 1;
+      break;
+    }
+    alpha = rz / pq;
+    // pass C: r += alpha q, rr = r^T D^-1 r, c = C D^-1 r
+    double rr = 0.0;
+    tasks([&] {
+      if (wact)
+        sweep_c_pf(
+            [&](int k, bool live) {
+              VC c_;
+              c_.r = live ? Rv[k] : 0.0;
+              c_.q = live ? Qv[k] : 0.0;
+              c_.d = live ? dg[k] : 0.0;
+              return c_;
+            },
+            [&](int, int k, const VC& c_) -> double {
+              if (!lact) return 0.0;
+              const double rk = c_.r + alpha * c_.q;
+              Rv[k] = rk;
+              const double u = c_.d * rk;
+              rr += rk * u;
+              return u;
+            });
+    });
+    slot_put(2, rr);
+    __syncthreads();
+    reduce_c_pub(2);
+    if (warp == 0) {
+      const double s = slot_fin(2);
+      if (lane == 0) publish(2, NQ, s);
+    }
+    cl.sync();  // S3: c and rr partials published; R complete over the cluster
+    gather_c(2, nullptr);
+    if (threadIdx.x == 0) bc[0] = cluster_sum(2, NQ);
+    __syncthreads();
+    if (crs) coarse_c();
+    solve_y();
+    __syncthreads();
+    beta = (bc[0] + (crs ? slot_fin(4) : 0.0) - slot_fin(3)) / rz;
+    if (crs) coarse_v(1.0);
+  }
+
+  // feasibility restoration: x += M^-1-weighted C^T S^-1 (g - C x); parents also into the pool
+  tasks([&] {
+    if (wact) sweep_c([&](int, int k) -> double { return lact ? Xv[k] : 0.0; });
+  });
+  __syncthreads();
+  reduce_c_pub(0);
+  cl.sync();
+  gather_c(0, A.g0);
+  __syncthreads();
+  solve_y();
+  __syncthreads();
+  if (crs) coarse_v(0.0);
+  double* po = (P.pool_off >= 0) ? A.pool + P.pool_off + (int64_t)rhs * nn : nullptr;
+  tasks([&] {
+    if (!wact) return;
+    walk_ids([&](int z, int k, const int (&idc)[8]) {
+      if (!lact) return;
+      const double xf = Xv[k] + dg[k] * ct_of(z, idc) - cz_at(k);
+      Xv[k] = xf;
+      if (po) po[k] = xf;
+    });
+  });
+  if (cr == 0 && threadIdx.x == 0) {
+    A.iters[prob] = it;
+    A.relres[prob] = (ref > 0.0) ? sqrt(fmax(rz, 0.0) / ref) : 0.0;
+    double* dgo = A.diag + (int64_t)prob * 4;
+    dgo[0] = rz;
+    dgo[1] = ref;
+    dgo[2] = floor2;
+    dgo[3] = breakdown;
+  }
+  cl.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
+size_t pcg3d_l1c_smem(int N) {
+  // + the coarse data CZ [27N][255] and E^-1 [255] (two-level preconditioner), 16-byte aligned
+  return (size_t)(98 * 27 * N + 2 * 27 * N + 5 * 32 + 512 + 3 * (27 * N + 2)) * sizeof(double) +
+         (49 * 3 + 1) * sizeof(int) + 16 + (size_t)(27 * N + 1) * 255 * sizeof(double);
+}
+
+// cluster size from the level-global problem count: enough CTAs for ~3 waves of the GPU
+int pcg3d_l1c_cluster(int level_problems, int sms) {
+  const char* e = getenv("MCH_L1_CLUSTER");
+  if (e) return atoi(e);
+  int cs = 1;
+  while (cs < 8 && level_problems * cs < 3 * sms) cs *= 2;
+  return cs;
+}
+
+template <int N, int NW, int CS>
+static cudaError_t go_l1c(const LevelArgs& A, cudaStream_t st) {
+  auto k = k_pcg3d_l1c<N, NW, CS>;
+  const size_t smem = pcg3d_l1c_smem(N);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(A.nprob_mp * A.n_rhs * CS));
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, A);
+}
+
+template <int N>
+static cudaError_t go_l1c_n(const LevelArgs& A, int cs, cudaStream_t st) {
+  switch (cs) {
+    case 1: return go_l1c<N, 14, 1>(A, st);
+    case 2: return go_l1c<N, 14, 2>(A, st);
+    case 4: return go_l1c<N, 14, 4>(A, st);
+    case 8: return go_l1c<N, 14, 8>(A, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_pcg3d_l1c(const LevelArgs& A, int cs, cudaStream_t st) {
+  switch (A.N) {
+    case 1: return go_l1c_n<1>(A, cs, st);
+    case 2: return go_l1c_n<2>(A, cs, st);
+    case 3: return go_l1c_n<3>(A, cs, st);
+    case 4: return go_l1c_n<4>(A, cs, st);
+  }
+  return cudaErrorInvalidValue;
+}
