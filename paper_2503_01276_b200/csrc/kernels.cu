@@ -737,6 +737,9 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wtot, int* tot) {
   return incl - v + (wd > 0 ? wtot[wd - 1] : 0);
 }
 
+#ifndef MCH_PINV_TOL
+#define MCH_PINV_TOL 1e-34  // Jacobi stops when sum(offdiag^2) <= tol * sum(diag^2)
+#endif
 #ifndef MCH_COARSE_CONTRAST
 #define MCH_COARSE_CONTRAST 20.0  // window contrast kappa_max / kappa_min that turns the coarse space on
 #endif
@@ -1313,7 +1316,7 @@ __global__ void __launch_bounds__(256) k_pinv(LevelArgs A) {
         off += __shfl_xor_sync(FULLMASK, off, o);
         dia += __shfl_xor_sync(FULLMASK, dia, o);
       }
-      if (lane == 0) done = (off <= 1e-34 * dia);
+      if (lane == 0) done = (off <= MCH_PINV_TOL * dia);
     }
     __syncthreads();
     if (done) break;

@@ -1,5 +1,6 @@
 // C ABI (include/mch.h) and per-level orchestration of Algorithm 1.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <memory>
@@ -67,6 +68,12 @@ struct DevBuf {
   template <typename T> T* as() const { return reinterpret_cast<T*>(ptr); }
 };
 
+// NVTX range for the lifetime of a scope (Nsight timelines: per level, per kernel group)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 constexpr int kCoarseMax = 255;  // coarse components per window (two-level preconditioner; id 255 = none)
 
 int64_t ipow64(int64_t b, int e) {
@@ -95,6 +102,7 @@ struct LevelBatch {
   bool fused3 = false;  // 3D level >= 2: fused fine passes (fine3d.cu), no FI/FY workspace
   int max_kp = 0;       // K_p node-box size (FK slot) of the fused path
   int l1cs = 1;         // 3D level 1: CTAs per problem (thread-block cluster, pcg3d_cl.cu)
+  int l2cs = 1;         // 3D levels >= 2 (k_pcg3d windows): CTAs per problem (pcg3d_cl.cu)
   bool w7 = false;      // 3D level >= 2, <= 7 level nodes per side: block PCG, one warp per rhs (k_pcg3d_w7)
   bool tsplit = false;  // 3D transport through k_pcg3d_l1<MODE 1> (fine windows <= 49 nodes per side)
   int nxm3 = 0;
@@ -143,6 +151,7 @@ struct mch_ctx {
   bool events = false;
   std::vector<std::vector<std::unique_ptr<LevelBatch>>> lplans;  // per level, built on first solve
   int* h_bad = nullptr;  // mch_set_medium validation flag (pinned / device)
+  bool medium_ok = true;  // false after mch_set_medium rejected its inputs: solves return MCH_EINVAL
   int* d_bad = nullptr;
   // NEXT-2: source f (cellwise, n^D), load vectors [P][N], macro-solve workspace and results
   DevBuf fsrc, bload, mws, mG, mb, mU, mres;
@@ -386,7 +395,7 @@ struct LevelVariant {
   bool on2d = false, l1op = false, crs2d = false;
   int variant = -1, threads2 = 0, tm_cols = 32, rpt = 0;
   bool on3d = false, w7 = false, tsplit = false, fused3 = false;
-  int nxm3 = 0, l1cs = 1;
+  int nxm3 = 0, l1cs = 1, l2cs = 1;
   int th_l = 64, th_f = 64;
   int max_kp = 0;
   bool coarse = false;
@@ -486,6 +495,13 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       if (nxm > 0 && pcg3d_smem(N, nxm) <= 232448) {
         V.on3d = true;
         V.nxm3 = nxm;
+      }
+      if (V.on3d && (nxm == 25 || nxm == 13)) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        V.l2cs = pcg3dc_cluster(nxm, (int)Sl.size() * nr, sms);
+        if (pcg3dc_smem(N, nxm) > 232448) V.l2cs = 1;
       }
       const char* w7e = getenv("MCH_PCG3D_W7");
       V.w7 = V.on3d && nxm == 7 && N <= 2 && nr == 4 * N && pcg3d_w7_smem(N) <= 232448 && !(w7e && atoi(w7e) == 0);
@@ -604,6 +620,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     B->on3d = V.on3d;
     B->nxm3 = V.nxm3;
     B->l1cs = V.l1cs;
+    B->l2cs = V.l2cs;
     B->w7 = V.w7;
     B->tsplit = V.tsplit;
     B->fused3 = V.fused3;
@@ -673,8 +690,12 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
 
 extern "C" int mch_solve_level(mch_ctx* c, int level) {
   if (!c) return MCH_EINVAL;
+  if (!c->medium_ok) return fail(c, MCH_EINVAL, "the last mch_set_medium was rejected: set a valid medium first");
   if (level != c->solved + 1 || level > c->p.levels)
     return fail(c, MCH_EORDER, "levels must be solved 1..L in order");
+  char nv_name[40];
+  snprintf(nv_name, sizeof nv_name, "mch_solve_level %d", level);
+  NvtxRange nv_level(nv_name);
   const int D = c->D, N = c->N, nr = c->n_rhs, nc = c->ncon;
   const HostPlan& pl = c->plan;
   const int s = (int)ipow64(c->p.eta, level - 1);
@@ -734,6 +755,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     CKC(c, cudaMemsetAsync(c->flags.ptr, 0, sizeof(int) * nmp, st));
     cudaEventRecord(B.ev[0], st);
     S.launches += (level >= 2) ? 6 : 4;
+    nvtxRangePushA("targets + transport + projector");
     CKC(c, launch_targets(A, st));
     A.FK = B.fused3 ? c->FK.as<double>() : nullptr;
     A.nkp_max = B.max_kp;
@@ -788,6 +810,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       S.launches += 1;
     }
     cudaEventRecord(B.ev[1], st);
+    nvtxRangePop();
+    nvtxRangePushA("projected PCG");
     double* dbgp = nullptr;
     if (getenv("MCH_PCG_DEBUG") && B.on2d) {  // dev: per-iteration scalars of one problem to stderr
       A.dbg_prob = atoi(getenv("MCH_PCG_DEBUG"));
@@ -800,6 +824,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     else if (B.on3d && level == 1 && B.l1cs > 0) CKC(c, launch_pcg3d_l1c(A, B.l1cs, st));
     else if (B.on3d && level == 1) CKC(c, launch_pcg3d_l1(A, st));
     else if (B.w7) CKC(c, launch_pcg3d_w7(A, st));
+    else if (B.on3d && B.l2cs > 1) CKC(c, launch_pcg3dc(A, B.nxm3, B.l2cs, st));
     else if (B.on3d) CKC(c, launch_pcg3d(A, B.nxm3, st));
     else CKC(c, launch_pcg(A, B.th_l, st));
     if (dbgp) {
@@ -812,6 +837,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       A.dbg = nullptr;
     }
     cudaEventRecord(B.ev[2], st);
+    nvtxRangePop();
+    NvtxRange nv_gram("combine + Eq. (7)");
     if (getenv("MCH_PCG_TIMING") && B.on2d) {
       char tag[64];
       snprintf(tag, sizeof tag, "level %d variant %d", level, B.variant);
@@ -832,6 +859,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   // later levels read them (Eq. 11), grouped point-to-point NCCL transfers of whole pool slots
   cudaEventRecord(c->ev[4], st);
   if (c->comm && level < c->p.levels && !c->shard.xfer[level].empty()) {
+    NvtxRange nv_x("parent exchange (NCCL)");
     const NcclApi* nc_ = c->nccl;
     ncclResult_t nr_ = nc_->GroupStart();
     for (const auto& x : c->shard.xfer[level]) {
@@ -938,7 +966,8 @@ extern "C" int mch_set_medium(mch_ctx* c, const double* kappa, const uint8_t* id
   CKC(c, cudaMemcpyAsync(c->h_bad, c->d_bad, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   CKC(c, cudaStreamSynchronize(c->st));
   c->solved = 0;
-  if (*c->h_bad) return fail(c, MCH_EINVAL, "kappa must be positive and finite; ids < num_continua");
+  c->medium_ok = (*c->h_bad == 0);
+  if (!c->medium_ok) return fail(c, MCH_EINVAL, "kappa must be positive and finite; ids < num_continua");
   return MCH_OK;
 }
 

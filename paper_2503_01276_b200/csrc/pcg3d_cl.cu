@@ -686,6 +686,542 @@ __global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1c(LevelArg
   cl.sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
+// ------------------------------------------------------------------------------------------
+// Levels >= 2 (windows of <= 25 level nodes per side): k_pcg3d (pcg3d.cu) with a cluster of CS CTAs
+// per problem.  CTA c owns the node planes [c nz / CS, (c+1) nz / CS) of p_s; the stencil reads the
+// two boundary planes from the neighbours' shared memory (DSMEM) after the cluster barrier that
+// follows the p update; reductions as in k_pcg3d_l1c.  Config 5 level 2: the four interior windows
+// need ~280 iterations (vs ~45 elsewhere) and set the level time; the cluster shortens them.
+template <int N, int NXM, int RW, int MINB, int CS>
+__global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 8) ? 16 : 8))) * RW - 1) /
+                                        ((32 / ((NXM > 16) ? 32 : ((NXM > 8) ? 16 : 8))) * RW)),
+                                  MINB) k_pcg3dc(LevelArgs A) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int cr = (int)cl.block_rank();
+  constexpr int LPR = (NXM > 16) ? 32 : ((NXM > 8) ? 16 : 8);  // lanes per row
+  constexpr int RPW = 32 / LPR;                                 // rows per warp and round
+  constexpr int NW = (NXM + RPW * RW - 1) / (RPW * RW);
+  constexpr int PY = NXM + 2;   // p_s rows per plane (zero halo rows y = -1, ny)
+  constexpr int PZ = PY * NXM;  // p_s plane (x pitch NXM, no x halo: x-neighbours by shuffle)
+  constexpr int NQ = 27 * N;    // constraint rows of a 3x3x3-subcell window
+  const int prob = blockIdx.x / CS;
+  const int mp = prob / A.n_rhs, rhs = prob - mp * A.n_rhs;
+  const ProbDesc& P = A.probs[mp];
+  const int nx = P.nc[0] + 1, ny = P.nc[1] + 1, nz = P.nc[2] + 1, nn = nx * ny * nz;
+  const int ncx = nx - 1;
+  const int nc = A.ncon;  // == NQ (host check)
+  const int z0 = (cr * nz) / CS, z1 = ((cr + 1) * nz) / CS;  // this CTA's node planes
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int x = lane & (LPR - 1), ry = lane / LPR;
+  const bool xin = x < NXM;
+  // current row of this lane group: set by set_row
+  int y = warp;
+  bool wact = false, lact = false;  // wact warp-uniform (some row of the warp is in the window)
+
+  extern __shared__ __align__(16) double smem[];
+  double* p_s = smem;                  // [NXM+2][PY][NXM], zero halo planes / rows
+  double* bins = p_s + (NXM + 2) * PZ;  // [NXM rows][NQ]
+  double* Ysh = bins + NXM * NQ;        // [NQ] yhat
+  double* csh = Ysh + NQ;               // [NQ] c
+  double* slots = csh + NQ;             // [5][32] scalar partial sums
+  double* zr = slots + 5 * 32;          // [256] coarse: E^-1 Z^T r
+  double* vv = zr + 256;                // [256] coarse: coarse part of z
+  double* red = vv + 256;               // [3][NQ + 2] cluster reduction buffers
+  int* zsm = reinterpret_cast<int*>(red + 3 * (NQ + 2));  // [NXM][3] z sides (pm, k0, k1)
+  __shared__ double bc[2];
+
+  for (int i = threadIdx.x; i < (NXM + 2) * PZ; i += blockDim.x) p_s[i] = 0.0;
+  for (int i = threadIdx.x; i < NXM * NQ + 2 * NQ + 5 * 32; i += blockDim.x) bins[i] = 0.0;
+  for (int z = threadIdx.x; z < nz; z += blockDim.x) {
+    const Sides s = sides_of(A, P, 2, z, nz - 1);
+    zsm[z * 3] = s.pm;
+    zsm[z * 3 + 1] = s.k0;
+    zsm[z * 3 + 2] = s.k1;
+  }
+  Sides sx{0, 0, 0}, sy{0, 0, 0}, syr[RW];
+  if (x < nx) sx = sides_of(A, P, 0, x, ncx);
+#pragma unroll
+  for (int ri = 0; ri < RW; ri++) {
+    const int yy = (warp + ri * NW) * RPW + ry;
+    syr[ri] = (yy < ny) ? sides_of(A, P, 1, yy, ny - 1) : Sides{0, 0, 0};
+  }
+  const int kxe = (x < ncx) ? slot3(A, P, 0, x) : 1000;  // subcell column of element x
+  const int kseg = ry * 1024 + kxe;                      // scan key: never equal across rows
+  auto set_row = [&](int ri) {
+    const int yb = (warp + ri * NW) * RPW;
+    y = yb + ry;
+    wact = yb < ny;
+    lact = (y < ny) && x < nx;
+    sy = syr[ri];
+  };
+  __syncthreads();
+
+  const double* S27 = A.STC + P.node_off * 27;
+  const double* MW = A.MLR + P.node_off * 8 * N;
+  const double* dg = A.dinv + P.node_off;
+  double* Xv = A.X + P.vec_off + (int64_t)rhs * nn;
+  double* Rv = A.R + P.vec_off + (int64_t)rhs * nn;
+  double* Qv = A.Q + P.vec_off + (int64_t)rhs * nn;
+  const double* Si = A.Sinv + (int64_t)mp * nc * nc;
+  const double* gsrc = A.g;  // levels >= 2 only
+  const double* bvec = A.B + P.vec_off + (int64_t)rhs * nn;
+
+  auto rows = [&](auto&& f) {
+#pragma unroll
+    for (int ri = 0; ri < RW; ri++) {
+      set_row(ri);
+      f();
+    }
+  };
+  auto nidx = [&](int z) { return (z * ny + y) * nx + x; };
+  auto pidx = [&](int z) { return (z + 1) * PZ + (y + 1) * NXM + x; };
+
+  // (C^T yhat)_k over the present octants
+  auto ct_at = [&](int z, int k) -> double {
+    const int pmz = zsm[z * 3];
+    double ct = 0.0;
+#pragma unroll
+    for (int zs = 0; zs < 2; zs++) {
+      if (!((pmz >> zs) & 1)) continue;
+      const int kz = zsm[z * 3 + 1 + zs];
+#pragma unroll
+      for (int ys = 0; ys < 2; ys++) {
+        if (!((sy.pm >> ys) & 1)) continue;
+        const int ky = ys ? sy.k1 : sy.k0;
+#pragma unroll
+        for (int xs = 0; xs < 2; xs++) {
+          if (!((sx.pm >> xs) & 1)) continue;
+          const int kx = xs ? sx.k1 : sx.k0;
+          const int o = xs + 2 * ys + 4 * zs;
+          const double* yq = Ysh + ((kz * 3 + ky) * 3 + kx) * N;
+#pragma unroll
+          for (int j = 0; j < N; j++) ct += __ldg(MW + (int64_t)(o * N + j) * nn + k) * yq[j];
+        }
+      }
+    }
+    return ct;
+  };
+
+  // constraint accumulation: acc[ys][xs][j] for the current subcell layer in z
+  double acc[2][2][N];
+  auto acc_zero = [&]() {
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+      for (int b = 0; b < 2; b++)
+#pragma unroll
+        for (int j = 0; j < N; j++) acc[a][b][j] = 0.0;
+  };
+  auto acc_add = [&](int zs, int k, double u) {
+#pragma unroll
+    for (int ys = 0; ys < 2; ys++) {
+      if (!((sy.pm >> ys) & 1)) continue;
+#pragma unroll
+      for (int xs = 0; xs < 2; xs++) {
+        if (!((sx.pm >> xs) & 1)) continue;
+        const int o = xs + 2 * ys + 4 * zs;
+#pragma unroll
+        for (int j = 0; j < N; j++) acc[ys][xs][j] += __ldg(MW + (int64_t)(o * N + j) * nn + k) * u;
+      }
+    }
+  };
+  // warp-collective (wact warps): layer kz of each row -> bins[y]
+  auto flush = [&](int kz) {
+#pragma unroll
+    for (int ys = 0; ys < 2; ys++) {
+      const bool has = (sy.pm >> ys) & 1;  // per row (acc is zero where the side is absent)
+      const int ky = ys ? sy.k1 : sy.k0;
+      double v[N];
+#pragma unroll
+      for (int j = 0; j < N; j++) {
+        const double t = __shfl_down_sync(FULLMASK, acc[ys][0][j], 1);  // element x of lane x+1
+        v[j] = acc[ys][1][j] + ((x < LPR - 1) ? t : 0.0);
+      }
+      const int kup = __shfl_up_sync(FULLMASK, kseg, 1);
+      const unsigned hm = __ballot_sync(FULLMASK, lane == 0 || kseg != kup);
+      const int head = 31 - __clz(hm & (0xffffffffu >> (31 - lane)));
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+          const double t = __shfl_up_sync(FULLMASK, v[j], d);
+          if (lane - d >= head) v[j] += t;
+        }
+      }
+      const bool tail = (lane == 31) || ((hm >> (lane + 1)) & 1u);
+      if (tail && kxe < 1000 && has && y < ny) {
+        double* B = bins + y * NQ + ((kz * 3 + ky) * 3 + kxe) * N;
+#pragma unroll
+        for (int j = 0; j < N; j++) B[j] = v[j];
+      }
+    }
+    acc_zero();
+  };
+  // walk the column accumulating u(z, k) into the constraint bins (wact warps)
+  auto sweep_c = [&](auto&& ufun) {
+    acc_zero();
+    int layer = -1;
+    for (int z = z0; z < z1; z++) {
+      const int k = nidx(z);
+      const double u = ufun(z, k);
+      const int pmz = zsm[z * 3];
+      if (pmz == 3) {
+        if (lact) acc_add(0, k, u);
+        flush(zsm[z * 3 + 1]);
+        if (lact) acc_add(1, k, u);
+        layer = zsm[z * 3 + 2];
+      } else {
+        if (lact) acc_add((pmz == 2) ? 1 : 0, k, u);
+        layer = (pmz == 2) ? zsm[z * 3 + 2] : zsm[z * 3 + 1];
+      }
+    }
+    if (layer >= 0) flush(layer);
+  };
+  // p_s plane z (planes z0 - 1 and z1 live in the neighbouring CTA: DSMEM)
+  auto plane = [&](int z) -> const double* {
+    const double* base = p_s;
+    if (z >= 0 && z < nz && z < z0) base = cl.map_shared_rank(p_s, cr - 1);
+    if (z >= 0 && z < nz && z >= z1) base = cl.map_shared_rank(p_s, cr + 1);
+    return base + (z + 1) * PZ;
+  };
+  // (A p)_k from p_s: f(z, k, Ap, p_k)  (wact warps; lanes >= nx carry zeros)
+  auto sweep_stencil = [&](auto&& f) {
+    const int ro = (y + 1) * NXM + x;
+    double v[3][3];  // [dy][dz]
+    {
+      const double* pm1 = plane(z0 - 1) + ro;
+      const double* p0 = plane(z0) + ro;
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++) {
+        v[dy][0] = xin ? pm1[(dy - 1) * NXM] : 0.0;
+        v[dy][1] = xin ? p0[(dy - 1) * NXM] : 0.0;
+      }
+    }
+    for (int z = z0; z < z1; z++) {
+      const double* pn = plane(z + 1) + ro;
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++) v[dy][2] = xin ? pn[(dy - 1) * NXM] : 0.0;
+      const int k = nidx(z);
+      double cf[27];  // all 27 coefficient loads in flight before the first use
+#pragma unroll
+      for (int c = 0; c < 27; c++) cf[c] = lact ? __ldg(S27 + (int64_t)c * nn + k) : 0.0;
+      double Ap = 0.0;
+#pragma unroll
+      for (int dz = 0; dz < 3; dz++)
+#pragma unroll
+        for (int dy = 0; dy < 3; dy++) {
+          const double c0 = v[dy][dz];
+          double l = __shfl_up_sync(FULLMASK, c0, 1);
+          double r = __shfl_down_sync(FULLMASK, c0, 1);
+          if (x == 0) l = 0.0;
+          if (x == LPR - 1) r = 0.0;
+          const int cb = 9 * dz + 3 * dy;
+          Ap += cf[cb] * l + cf[cb + 1] * c0 + cf[cb + 2] * r;
+        }
+      f(z, k, Ap, v[1][1]);
+#pragma unroll
+      for (int dy = 0; dy < 3; dy++) {
+        v[dy][0] = v[dy][1];
+        v[dy][1] = v[dy][2];
+      }
+    }
+  };
+
+  auto slot_put = [&](int which, double v) {
+    v = wsum0(v);
+    if (lane == 0) slots[which * 32 + warp] = v;
+  };
+  auto slot_fin = [&](int which) { return wsum0((lane < NW) ? slots[which * 32 + lane] : 0.0); };
+  // c = sum over rows of the bins (fixed order) into csh; call between barriers
+  auto reduce_c = [&]() {  // one warp per constraint row, fixed tree over the row bins
+    for (int i = warp; i < nc; i += NW) {
+      double s = 0.0;
+      for (int yy = lane; yy < ny; yy += 32) s += bins[yy * NQ + i];
+      s = wsum0(s);
+      if (lane == 0) csh[i] = s;
+    }
+  };
+  // Ysh = S^-1 csh (rows over warps), slots[3] = per-warp partial c.yhat; call between barriers
+  auto solve_y = [&]() {
+    double cyw = 0.0;
+    for (int i = warp; i < nc; i += NW) {
+      double s = 0.0;
+      for (int j = lane; j < nc; j += 32) s += __ldg(Si + (int64_t)i * nc + j) * csh[j];
+      s = wsum0(s);
+      if (lane == 0) Ysh[i] = s;
+      cyw += s * csh[i];
+    }
+    if (lane == 0) slots[3 * 32 + warp] = cyw;
+  };
+
+  auto publish = [&](int b, int i, double v) { red[b * (NQ + 2) + i] = v; };
+  auto cluster_sum = [&](int b, int i) -> double {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < CS; r++) s += *cl.map_shared_rank(red + b * (NQ + 2) + i, r);
+    return s;
+  };
+  // per CTA: row bins -> red[b][0..nc) (one warp per constraint row, fixed tree)
+  auto reduce_c_pub = [&](int b) {
+    for (int i = warp; i < nc; i += NW) {
+      double s = 0.0;
+      for (int yy = lane; yy < ny; yy += 32) s += bins[yy * NQ + i];
+      s = wsum0(s);
+      if (lane == 0) publish(b, i, s);
+    }
+  };
+  // two-level preconditioner, as in k_pcg3d_l1
+  const bool crs = A.coarse && A.ncomp[mp] > 0;
+  const int nca = crs ? A.ncomp[mp] : 0;
+  const int* cmp = A.cmap + P.node_off;
+  const int* cpt = A.cptr + (int64_t)mp * (A.ncmax + 1);
+  const int* cls = A.clist + P.node_off;
+  const double* Eiv = A.Einv + (int64_t)mp * A.ncmax;
+  const double* CZm = A.CZ + (int64_t)mp * nc * A.ncmax;
+  auto coarse_c = [&]() {  // zr, slot 4, csh += (CZ) zr; two barriers
+    double part = 0.0;
+    const int sub = lane & 3, ngrp = blockDim.x >> 2;
+    for (int a0 = threadIdx.x >> 2; a0 - (int)(threadIdx.x >> 2) < nca; a0 += ngrp) {
+      const int a = a0;
+      double sv = 0.0;
+      if (a < nca) {
+        const int i0 = __ldg(cpt + a), i1 = __ldg(cpt + a + 1);
+        for (int i = i0 + sub; i < i1; i += 4) sv += __ldcg(Rv + __ldg(cls + i));
+      }
+      sv += __shfl_xor_sync(FULLMASK, sv, 1);
+      sv += __shfl_xor_sync(FULLMASK, sv, 2);
+      if (a < nca && sub == 0) {
+        const double ei = __ldg(Eiv + a);
+        zr[a] = sv * ei;
+        part += sv * sv * ei;
+      }
+    }
+    part = wsum0(part);
+    if (lane == 0) slots[4 * 32 + warp] = part;
+    __syncthreads();
+    for (int t = warp; t < nc; t += NW) {
+      double sv = 0.0;
+      for (int a = lane; a < nca; a += 32) sv += __ldg(CZm + (int64_t)t * A.ncmax + a) * zr[a];
+      sv = wsum0(sv);
+      if (lane == 0) csh[t] += sv;
+    }
+    __syncthreads();
+  };
+  auto coarse_v = [&](double s0) {  // vv = s0 zr - E^-1 (CZ)^T Ysh; one barrier
+    for (int a = threadIdx.x; a < nca; a += blockDim.x) {
+      double acc = 0.0;
+      for (int t = 0; t < nc; t++) acc += __ldg(CZm + (int64_t)t * A.ncmax + a) * Ysh[t];
+      vv[a] = (s0 != 0.0 ? s0 * zr[a] : 0.0) - __ldg(Eiv + a) * acc;
+    }
+    __syncthreads();
+  };
+  auto cz_at = [&](int k) -> double {
+    if (!crs) return 0.0;
+    const int a = __ldg(cmp + k);
+    return (a >= 0) ? vv[a] : 0.0;
+  };
+
+  // ---- init: x0 = D^-1 C^T S^-1 t, r0 = A x0 - b, c = C D^-1 r0, yhat = S^-1 c; returns r0^T D^-1 r0
+  auto init = [&](const double* tcol, const double* bb) -> double {
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) csh[i] = tcol[((int64_t)mp * nc + i) * A.n_rhs + rhs];
+    __syncthreads();
+    solve_y();
+    __syncthreads();
+    if (crs) coarse_v(0.0);
+    rows([&] {
+      if (lact)
+        for (int z = z0; z < z1; z++) {
+          const int k = nidx(z);
+          const double x0 = dg[k] * ct_at(z, k) - cz_at(k);
+          p_s[pidx(z)] = x0;
+          Xv[k] = x0;
+        }
+    });
+    cl.sync();  // x0 (= p_s) complete over the cluster
+    rows([&] {
+      if (wact)
+        sweep_stencil([&](int, int k, double Ap, double) {
+          if (lact) Rv[k] = Ap - (bb ? bb[k] : 0.0);
+        });
+    });
+    double rr = 0.0;
+    rows([&] {
+      if (wact)
+        sweep_c([&](int, int k) -> double {
+          if (!lact) return 0.0;
+          const double rk = Rv[k];
+          const double u = dg[k] * rk;
+          rr += rk * u;
+          return u;
+        });
+    });
+    slot_put(2, rr);
+    __syncthreads();
+    reduce_c_pub(2);
+    if (warp == 0) {
+      const double s = slot_fin(2);
+      if (lane == 0) publish(2, NQ, s);
+    }
+    cl.sync();  // partials published; R complete over the cluster
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) csh[i] = cluster_sum(2, i);
+    if (threadIdx.x == 0) bc[0] = cluster_sum(2, NQ);
+    __syncthreads();
+    if (crs) coarse_c();
+    solve_y();
+    __syncthreads();
+    const double rrt = bc[0] + (crs ? slot_fin(4) : 0.0);
+    if (crs) coarse_v(1.0);
+    cl.sync();  // red[2] free again before the next publication
+    return rrt;
+  };
+
+  // reference scale: initial projected residual of the full (non-hierarchical) problem
+  const double rr_ref = init(A.g0, nullptr);
+  double rz_ref;
+  {
+    double v = 0.0;
+    rows([&] {
+      if (lact)
+        for (int z = z0; z < z1; z++) {
+          const int k = nidx(z);
+          const double w = Rv[k] - ct_at(z, k);
+          v += dg[k] * w * w;
+        }
+    });
+    slot_put(0, v);
+    __syncthreads();
+    if (warp == 0) {
+      const double s = slot_fin(0);
+      if (lane == 0) publish(0, 0, s);
+    }
+    cl.sync();
+    rz_ref = cluster_sum(0, 0);
+    cl.sync();
+  }
+  const double rr0 = init(gsrc, bvec);
+
+  const double tol2 = A.rtol * A.rtol;
+  const double floor2 = 1e-30 * fmax(rr0, rr_ref);
+  double beta = 0.0, rz = 0.0, ref = 0.0, alpha = 0.0;
+  int it = 0, breakdown = 0;
+  for (;; it++) {
+    // pass A: x += alpha_prev p_prev (deferred), r <- r - C^T yhat, z = D^-1 r, p <- -z + beta p
+    double v = 0.0;
+    rows([&] {
+      if (!lact) return;
+      const bool first = (it == 0);
+      for (int z = z0; z < z1; z++) {
+        const int k = nidx(z);
+        const double rk = Rv[k] - ct_at(z, k);
+        const double zz = dg[k] * rk + cz_at(k);
+        double& pk = p_s[pidx(z)];
+        const double pold = pk;
+        if (!first) Xv[k] += alpha * pold;
+        pk = first ? -zz : -zz + beta * pold;
+        Rv[k] = rk;
+        v += rk * zz;
+      }
+    });
+    slot_put(0, v);
+    __syncthreads();
+    if (warp == 0) {
+      const double s = slot_fin(0);
+      if (lane == 0) publish(0, 0, s);
+    }
+    cl.sync();  // S1: p complete over the cluster, rz partials published
+    // pass B: q = A p, pq
+    double w = 0.0;
+    rows([&] {
+      if (wact)
+        sweep_stencil([&](int, int k, double Ap, double pk) {
+          if (lact) {
+            Qv[k] = Ap;
+            w += pk * Ap;
+          }
+        });
+    });
+    slot_put(1, w);
+    if (threadIdx.x == 0) bc[0] = cluster_sum(0, 0);
+    __syncthreads();
+    if (warp == 0) {
+      const double s = slot_fin(1);
+      if (lane == 0) publish(1, 0, s);
+    }
+    cl.sync();  // S2: pq partials published
+    if (threadIdx.x == 0) bc[1] = cluster_sum(1, 0);
+    __syncthreads();
+    rz = bc[0];
+    const double pq = bc[1];
+    if (it == 0) ref = fmax(rz, rz_ref);
+    if (!(rz > fmax(tol2 * ref, floor2)) || it >= A.max_iter) break;
+    if (!(pq > 0.0) || !isfinite(pq)) {
+      breakdown = 1;
+      break;
+    }
+    alpha = rz / pq;
+    // pass C: r += alpha q, rr = r^T D^-1 r, c = C D^-1 r (per row)
+    double rr = 0.0;
+    rows([&] {
+      if (wact)
+        sweep_c([&](int, int k) -> double {
+          if (!lact) return 0.0;
+          const double rk = Rv[k] + alpha * Qv[k];
+          Rv[k] = rk;
+          const double u = dg[k] * rk;
+          rr += rk * u;
+          return u;
+        });
+    });
+    slot_put(2, rr);
+    __syncthreads();
+    reduce_c_pub(2);
+    if (warp == 0) {
+      const double s = slot_fin(2);
+      if (lane == 0) publish(2, NQ, s);
+    }
+    cl.sync();  // S3: c and rr partials published; R complete over the cluster
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) csh[i] = cluster_sum(2, i);
+    if (threadIdx.x == 0) bc[0] = cluster_sum(2, NQ);
+    __syncthreads();
+    if (crs) coarse_c();
+    solve_y();
+    __syncthreads();
+    const double cy = slot_fin(3);
+    beta = (bc[0] + (crs ? slot_fin(4) : 0.0) - cy) / rz;
+    if (crs) coarse_v(1.0);
+  }
+
+  // feasibility restoration: x += D^-1 C^T S^-1 (g - C x)
+  rows([&] {
+    if (wact) sweep_c([&](int, int k) -> double { return lact ? Xv[k] : 0.0; });
+  });
+  __syncthreads();
+  reduce_c_pub(0);
+  cl.sync();
+  for (int i = threadIdx.x; i < nc; i += blockDim.x) csh[i] = gsrc[((int64_t)mp * nc + i) * A.n_rhs + rhs] - cluster_sum(0, i);
+  __syncthreads();
+  solve_y();
+  __syncthreads();
+  if (crs) coarse_v(0.0);
+  rows([&] {
+    if (lact)
+      for (int z = z0; z < z1; z++) {
+        const int k = nidx(z);
+        Xv[k] += dg[k] * ct_at(z, k) - cz_at(k);
+      }
+  });
+  if (cr == 0 && threadIdx.x == 0) {
+    A.iters[prob] = it;
+    A.relres[prob] = (ref > 0.0) ? sqrt(fmax(rz, 0.0) / ref) : 0.0;
+    double* dgo = A.diag + (int64_t)prob * 4;
+    dgo[0] = rz;
+    dgo[1] = ref;
+    dgo[2] = floor2;
+    dgo[3] = breakdown;
+  }
+  cl.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
 size_t pcg3d_l1c_smem(int N) {
   // + the coarse data CZ [27N][255] and E^-1 [255] (two-level preconditioner), 16-byte aligned
   return (size_t)(98 * 27 * N + 2 * 27 * N + 5 * 32 + 512 + 3 * (27 * N + 2)) * sizeof(double) +
@@ -697,7 +1233,7 @@ int pcg3d_l1c_cluster(int level_problems, int sms) {
   const char* e = getenv("MCH_L1_CLUSTER");
   if (e) return atoi(e);
   int cs = 1;
-  while (cs < 8 && level_problems * cs < 3 * sms) cs *= 2;
+  while (cs < 8 && level_problems * cs < 2 * sms) cs *= 2;  // config 5: 216 problems -> 2
   return cs;
 }
 
@@ -739,6 +1275,69 @@ cudaError_t launch_pcg3d_l1c(const LevelArgs& A, int cs, cudaStream_t st) {
     case 2: return go_l1c_n<2>(A, cs, st);
     case 3: return go_l1c_n<3>(A, cs, st);
     case 4: return go_l1c_n<4>(A, cs, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------------------------------
+size_t pcg3dc_smem(int N, int nxm) {
+  const size_t d = (size_t)(nxm + 2) * (nxm + 2) * nxm + (size_t)nxm * 27 * N + 2 * 27 * N + 5 * 32 + 512 +
+                   3 * (27 * N + 2);
+  return d * sizeof(double) + (size_t)nxm * 3 * sizeof(int);
+}
+
+template <int N, int NXM, int RW, int MINB, int CS>
+static cudaError_t go_3dc(const LevelArgs& A, cudaStream_t st) {
+  auto k = k_pcg3dc<N, NXM, RW, MINB, CS>;
+  const size_t smem = pcg3dc_smem(N, NXM);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  constexpr int LPR = (NXM > 16) ? 32 : ((NXM > 8) ? 16 : 8), RPW = 32 / LPR;
+  constexpr int NW = (NXM + RPW * RW - 1) / (RPW * RW);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(A.nprob_mp * A.n_rhs * CS));
+  cfg.blockDim = dim3(32 * NW);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, A);
+}
+
+template <int N>
+static cudaError_t go_3dc_n(const LevelArgs& A, int nxm, int cs, cudaStream_t st) {
+  if (nxm == 25) {
+    switch (cs) {
+      case 2: return go_3dc<N, 25, 2, 1, 2>(A, st);
+      case 4: return go_3dc<N, 25, 2, 1, 4>(A, st);
+    }
+  } else if (nxm == 13) {
+    switch (cs) {
+      case 2: return go_3dc<N, 13, 1, 2, 2>(A, st);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+int pcg3dc_cluster(int nxm, int level_problems, int sms) {
+  const char* e = getenv("MCH_L2_CLUSTER");
+  if (e) return atoi(e);
+  (void)level_problems;
+  (void)sms;
+  return (nxm == 25) ? 2 : 1;
+}
+
+cudaError_t launch_pcg3dc(const LevelArgs& A, int nxm, int cs, cudaStream_t st) {
+  switch (A.N) {
+    case 1: return go_3dc_n<1>(A, nxm, cs, st);
+    case 2: return go_3dc_n<2>(A, nxm, cs, st);
+    case 3: return go_3dc_n<3>(A, nxm, cs, st);
+    case 4: return go_3dc_n<4>(A, nxm, cs, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -621,3 +621,51 @@ def test_3d_level_paths_agree(d, n, M, L, N, seed, monkeypatch):
             assert g_err(G[i], Go[i]) < G_TOL, (name, i, g_err(G[i], Go[i]))
             ref = res["fused"][i]
             assert np.max(np.abs(G[i] - ref)) <= 1e-10 * np.abs(ref).max(), (name, i)
+
+
+@pytest.mark.parametrize("cid", [None, 5])
+def test_bitwise_reproducible(cid):
+    """Two solves of the same problem are bitwise identical (every reduction runs in a fixed
+    order; a data race or an unordered atomic would show up here).  Tiny 2D and 3D media through
+    every kernel family, and config 5 in the bench's launch configuration."""
+    H = _gpu()
+    runs = []
+    if cid is None:
+        cases = [(2, 64, 8, 3, 2), (3, 16, 4, 2, 2), (3, 32, 4, 2, 2)]
+        for d, n, M, L, N in cases:
+            kap, ids = _admissible(d, n, M, N, 90 + d)
+            out = []
+            for _ in range(2):
+                with H(d, n, N, M, L, 2, kap, ids) as h:
+                    h.solve_all()
+                    out.append(h.effective_coeffs())
+            assert np.array_equal(out[0], out[1]), (d, n, M, L, N)
+        return
+    cfg = CONFIGS[cid]
+    kap, ids = make_medium(cfg)
+    with H.from_config(cfg, kap, ids) as h:
+        h.solve_all()
+        G0 = h.effective_coeffs()
+        h.reset()
+        h.solve_all()
+        G1 = h.effective_coeffs()
+    assert np.array_equal(G0, G1)
+
+
+def test_rejected_medium_blocks_solves():
+    """mch_set_medium with invalid inputs returns MCH_EINVAL and the context refuses to solve
+    (MCH_EINVAL) until a valid medium is set"""
+    H = _gpu()
+    from paper_2503_01276_b200._native import MchError
+    d, n, M, L, N = 2, 64, 8, 3, 2
+    kap, ids = _admissible(d, n, M, N, 21)
+    with H(d, n, N, M, L, 2, kap, ids) as h:
+        bad = kap.copy()
+        bad.flat[5] = -1.0
+        with pytest.raises(MchError, match="MCH_EINVAL"):
+            h.set_medium(bad, ids)
+        with pytest.raises(MchError, match="MCH_EINVAL"):
+            h.solve_level(1)
+        h.set_medium(kap, ids)
+        h.solve_all()
+        assert np.isfinite(h.effective_coeffs()).all()
