@@ -36,7 +36,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     libdir = os.path.dirname(LIB)
-    objdir = os.path.join(libdir, "obj")
+    # objects outside the repo: the tree is pushed to the GPU box as is, the .so alone is needed
+    objdir = os.path.join(os.environ.get("TMPDIR", "/tmp"), "mch_obj")
     os.makedirs(objdir, exist_ok=True)
     procs, objs = [], []
     for src in SOURCES:

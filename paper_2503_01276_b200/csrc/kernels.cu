@@ -1319,11 +1319,17 @@ __global__ void __launch_bounds__(256) k_pinv(LevelArgs A) {
       if (lane == 0) done = (off <= MCH_PINV_TOL * dia);
     }
     __syncthreads();
+#ifdef MCH_PINV_STATS
+    if (tid == 0 && (done || sweep == 39)) atomicAdd(&A.flags[mp], (sweep + 1) << 8);
+#endif
     if (done) break;
     for (int round = 0; round < m - 1; round++) {
-      // pairs of this round: (pos[k], pos[m-1-k]), k < m/2
+      // pairs of this round: (pos(k), pos(m-1-k)), k < m/2, circle method (index 0 fixed, the
+      // others rotated by `round`)
+      const int m1 = m - 1;
+      auto posr = [&](int i) { return (i == 0) ? 0 : ((i - 1 - round) % m1 + m1) % m1 + 1; };
       if (tid < np) {
-        int p = pos[tid], q = pos[m - 1 - tid];
+        int p = posr(tid), q = posr(m - 1 - tid);
         if (p > q) { const int tt = p; p = q; q = tt; }
         const double apq = S[p * m + q];
         double c = 1.0, sn = 0.0;
@@ -1359,22 +1365,12 @@ __global__ void __launch_bounds__(256) k_pinv(LevelArgs A) {
         if (q < 0) continue;
         const double c = rc[k2], sn = rs[k2];
         const double skp = S[k * m + p], skq = S[k * m + q];
-        S[k * m + p] = c * skp - sn * skq;
-        S[k * m + q] = sn * skp + c * skq;
+        S[k * m + p] = (k == q) ? 0.0 : c * skp - sn * skq;  // the rotated-out pair entries are set to 0
+        S[k * m + q] = (k == p) ? 0.0 : sn * skp + c * skq;
         const double vkp = V[k * m + p], vkq = V[k * m + q];
         V[k * m + p] = c * vkp - sn * vkq;
         V[k * m + q] = sn * vkp + c * vkq;
       }
-      __syncthreads();
-      if (tid < np && rq[tid] >= 0) {
-        S[rp[tid] * m + rq[tid]] = 0.0;
-        S[rq[tid] * m + rp[tid]] = 0.0;
-      }
-      // rotate positions 1..m-1 (circle method)
-      int nxt = 0;
-      if (tid < m) nxt = (tid == 0) ? pos[0] : pos[(tid == 1) ? m - 1 : tid - 1];
-      __syncthreads();
-      if (tid < m) pos[tid] = nxt;
       __syncthreads();
     }
   }
@@ -1396,14 +1392,23 @@ __global__ void __launch_bounds__(256) k_pinv(LevelArgs A) {
   __syncthreads();
   const double lmax = lmax_s;
   const double* ds = A.pinv_ds + (int64_t)mp * nc;
+  // 1/lambda_k of the kept eigenvalues (0 for the truncated ones), once per window: the assembly
+  // below then has no division (r01 divided in its innermost loop, nc^3 divisions per window)
+  double* il = rc;  // rc/rs (128 doubles) are free now
+  for (int k = tid; k < nc; k += nt) {
+    const double lk = S[k * m + k];
+    il[k] = (lk > 1e-11 * lmax) ? 1.0 / lk : 0.0;
+  }
+  __syncthreads();
+  // S+ = V diag(il) V^T, symmetric: entries i <= j formed once and mirrored
   for (int idx = tid; idx < nc * nc; idx += nt) {
     const int i = idx / nc, j = idx % nc;
+    if (i > j) continue;
     double acc = 0.0;
-    for (int k = 0; k < nc; k++) {
-      const double lk = S[k * m + k];
-      if (lk > 1e-11 * lmax) acc += V[i * m + k] * V[j * m + k] / lk;
-    }
-    Sg[idx] = acc * ds[i] * ds[j];
+    for (int k = 0; k < nc; k++) acc += V[i * m + k] * V[j * m + k] * il[k];
+    const double v = acc * ds[i] * ds[j];
+    Sg[i * nc + j] = v;
+    Sg[j * nc + i] = v;
   }
 }
 
@@ -1946,6 +1951,7 @@ cudaError_t launch_pinv(const LevelArgs& A, cudaStream_t st) {
   if (A.band > 0) return cudaSuccess;  // the banded projector reports dependent rows instead (flag 8)
   const int m = (A.ncon + 1) & ~1;
   if (m > 128) return cudaErrorInvalidValue;
+
   const size_t sm = sizeof(double) * (2 * (size_t)m * m + 128) + sizeof(int) * ((size_t)m + 128);
   cudaError_t e = cudaFuncSetAttribute(k_pinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;

@@ -897,6 +897,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     for (int i = 0; i < B.nmp; i++) {
       const MacroHost& m = pl.all[B.mps[i]];
       if (B.h_flags[i] & 4) S.rank_deficient++;  // k_pinv truncated eigenvalues (reading R20)
+      if ((B.h_flags[i] >> 8) && getenv("MCH_PINV_STATS_PRINT") && i < 4)
+        fprintf(stderr, "[pinv] level %d macropoint %d sweeps %d\n", level, i, B.h_flags[i] >> 8);
       if (B.h_flags[i] & 8) {
         char buf[200];
         snprintf(buf, sizeof buf, "dependent constraint rows at macropoint (%d,%d,%d): the banded projector of "

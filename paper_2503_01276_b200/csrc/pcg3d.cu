@@ -1157,22 +1157,26 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
   const int nx = P.nc[0] + 1, ny = P.nc[1] + 1, nz = P.nc[2] + 1, nn = nx * ny * nz;
   const int lane = threadIdx.x & 31, rhs = threadIdx.x >> 5;
 
+  constexpr int EC = 729 * N;  // constraint entries: sum_nodes prod_d (element sides of the node) <= 9^3, x N
   extern __shared__ __align__(16) double smem[];
   double* st_s = smem;                  // [27][nn] stencil rows
-  double* mw_s = st_s + 27 * kW7NN;     // [8N][nn] octant-merged constraint weights
-  double* dg_s = mw_s + 8 * N * kW7NN;  // [nn] D^-1
+  double* rw_s = st_s + 27 * kW7NN;     // [EC] row-major constraint entries: weight
+  double* nw_s = rw_s + EC;             // [EC] node-major constraint entries: weight
+  double* dg_s = nw_s + EC;             // [nn] D^-1
   double* si_s = dg_s + kW7NN;          // [NQ][NQ] S^+ transposed: si_s[j*NQ + i] = S^+_ij
   double* p_all = si_s + NQ * NQ;       // [NR][PP] p with zero halo (also D^-1 r / x for C u)
   double* c_all = p_all + NR * PP;      // [NR][NQ]
   double* y_all = c_all + NR * NQ;      // [NR][NQ]
   int* sd_s = reinterpret_cast<int*>(y_all + NR * NQ);  // [3][7] sides packed pm | k0 << 4 | k1 << 8
   int* rg_s = sd_s + 3 * kW7;                             // [3][3] node range of subcell coordinate: lo | hi << 8
+  int* rs_s = rg_s + 9;                                   // [NQ + 1] row starts
+  int* ns_s = rs_s + NQ + 1;                              // [nn + 1] node starts
+  int* ri_s = ns_s + kW7NN + 1;                           // [EC] padded p index of a row entry
+  int* nr_s = ri_s + EC;                                  // [EC] constraint row of a node entry
 
   {
     const double* S27 = A.STC + P.node_off * 27;
     for (int i = threadIdx.x; i < 27 * nn; i += blockDim.x) st_s[i] = __ldg(S27 + i);
-    const double* MW = A.MLR + P.node_off * 8 * N;
-    for (int i = threadIdx.x; i < 8 * N * nn; i += blockDim.x) mw_s[i] = __ldg(MW + i);
     for (int i = threadIdx.x; i < nn; i += blockDim.x) dg_s[i] = __ldg(A.dinv + P.node_off + i);
     const double* Si = A.Sinv + (int64_t)mp * NQ * NQ;
     for (int i = threadIdx.x; i < NQ * NQ; i += blockDim.x) {
@@ -1204,6 +1208,74 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
       rg_s[threadIdx.x] = (hi >= lo) ? (lo | (hi << 8)) : (1 | (0 << 8));  // empty: lo > hi
     }
     __syncthreads();
+    // constraint weights as sparse lists, both ways: per row (q, j) its (node, weight) entries for
+    // c = C u, per node its (row, weight) entries for C^T yhat (octant-merged weights of k_node_ops3d)
+    const double* MW = A.MLR + P.node_off * 8 * N;
+    auto rng_n = [&](int r) { return max(0, (r >> 8) - (r & 255) + 1); };
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      const int z = k / (nx * ny), t = k - z * nx * ny, y = t / nx, x = t - y * nx;
+      const int px = __popc(sd_s[x] & 3), py = __popc(sd_s[kW7 + y] & 3), pz = __popc(sd_s[2 * kW7 + z] & 3);
+      ns_s[k + 1] = N * px * py * pz;
+    }
+    if (threadIdx.x < NQ) {
+      const int q = threadIdx.x / N, qz = q / 9, qy = (q / 3) % 3, qx = q % 3;
+      rs_s[threadIdx.x + 1] = rng_n(rg_s[qx]) * rng_n(rg_s[3 + qy]) * rng_n(rg_s[6 + qz]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ns_s[0] = 0;
+      for (int k = 0; k < nn; k++) ns_s[k + 1] += ns_s[k];
+    } else if (threadIdx.x == 32) {
+      rs_s[0] = 0;
+      for (int r = 0; r < NQ; r++) rs_s[r + 1] += rs_s[r];
+    }
+    __syncthreads();
+    if (ns_s[nn] > EC || rs_s[NQ] > EC) __trap();  // >= 2 level cells per subcell (reading R22) bounds both
+    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+      const int z = k / (nx * ny), t = k - z * nx * ny, y = t / nx, x = t - y * nx;
+      const int sx = sd_s[x], sy = sd_s[kW7 + y], sz = sd_s[2 * kW7 + z];
+      int e = ns_s[k];
+      for (int zs = 0; zs < 2; zs++) {
+        if (!((sz >> zs) & 1)) continue;
+        const int kz = (sz >> (4 + 4 * zs)) & 15;
+        for (int ys = 0; ys < 2; ys++) {
+          if (!((sy >> ys) & 1)) continue;
+          const int ky = (sy >> (4 + 4 * ys)) & 15;
+          for (int xs = 0; xs < 2; xs++) {
+            if (!((sx >> xs) & 1)) continue;
+            const int kx = (sx >> (4 + 4 * xs)) & 15;
+            const int o = xs + 2 * ys + 4 * zs;
+            for (int j = 0; j < N; j++, e++) {
+              nr_s[e] = ((kz * 3 + ky) * 3 + kx) * N + j;
+              nw_s[e] = __ldg(MW + (int64_t)(o * N + j) * nn + k);
+            }
+          }
+        }
+      }
+    }
+    if (threadIdx.x < NQ) {
+      const int row = threadIdx.x, q = row / N, j = row - q * N;
+      const int qz = q / 9, qy = (q / 3) % 3, qx = q % 3;
+      const int rx = rg_s[qx], ry = rg_s[3 + qy], rz = rg_s[6 + qz];
+      int e = rs_s[row];
+      for (int Z = rz & 255; Z <= (rz >> 8); Z++) {
+        const int vz = sd_s[2 * kW7 + Z];
+        const int bz = (((vz & 1) && ((vz >> 4) & 15) == qz) ? 0 : 1);
+        for (int Y = ry & 255; Y <= (ry >> 8); Y++) {
+          const int vy = sd_s[kW7 + Y];
+          const int by = (((vy & 1) && ((vy >> 4) & 15) == qy) ? 0 : 1);
+          for (int X = rx & 255; X <= (rx >> 8); X++, e++) {
+            const int vx = sd_s[X];
+            const int bx = (((vx & 1) && ((vx >> 4) & 15) == qx) ? 0 : 1);
+            const int o = bx + 2 * by + 4 * bz;
+            const int k = (Z * ny + Y) * nx + X;
+            ri_s[e] = ((Z + 1) * kW7P + (Y + 1)) * kW7P + (X + 1);
+            rw_s[e] = __ldg(MW + (int64_t)(o * N + j) * nn + k);
+          }
+        }
+      }
+    }
+    __syncthreads();
   }
   double* p_s = p_all + rhs * PP;
   double* c_s = c_all + rhs * NQ;
@@ -1229,56 +1301,19 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
     return v;
   };
-  // (C^T yhat)_k over the present octants
+  // (C^T yhat)_k from the node's constraint entries
   auto ct_at = [&](int i) -> double {
     const int k = lane + 32 * i;
-    const int v = nxy[i];
-    const int sx = sd_s[v & 15], sy = sd_s[kW7 + ((v >> 4) & 15)], sz = sd_s[2 * kW7 + (v >> 8)];
     double ct = 0.0;
-#pragma unroll
-    for (int zs = 0; zs < 2; zs++) {
-      if (!((sz >> zs) & 1)) continue;
-      const int kz = (sz >> (4 + 4 * zs)) & 15;
-#pragma unroll
-      for (int ys = 0; ys < 2; ys++) {
-        if (!((sy >> ys) & 1)) continue;
-        const int ky = (sy >> (4 + 4 * ys)) & 15;
-#pragma unroll
-        for (int xs = 0; xs < 2; xs++) {
-          if (!((sx >> xs) & 1)) continue;
-          const int kx = (sx >> (4 + 4 * xs)) & 15;
-          const int o = xs + 2 * ys + 4 * zs;
-          const double* yq = y_s + ((kz * 3 + ky) * 3 + kx) * N;
-#pragma unroll
-          for (int j = 0; j < N; j++) ct += mw_s[(o * N + j) * nn + k] * yq[j];
-        }
-      }
-    }
+    for (int e = ns_s[k], e1 = ns_s[k + 1]; e < e1; e++) ct += nw_s[e] * y_s[nr_s[e]];
     return ct;
   };
-  // c = C u with u in p_s (interior), rows over lanes; call after __syncwarp, ends with one
+  // c = C u with u in p_s (interior), rows over lanes, from the row entries; ends with __syncwarp
   auto cmul = [&]() {
     for (int row = lane; row < NQ; row += 32) {
-      const int q = row / N, j = row - q * N;
-      const int qz = q / 9, qy = (q / 3) % 3, qx = q % 3;
-      const int rx = rg_s[qx], ry = rg_s[3 + qy], rz = rg_s[6 + qz];
-      double s = 0.0;
-      for (int Z = rz & 255; Z <= (rz >> 8); Z++) {
-        const int vz = sd_s[2 * kW7 + Z];
-        const int bz = (((vz & 1) && ((vz >> 4) & 15) == qz) ? 0 : 1);
-        for (int Y = ry & 255; Y <= (ry >> 8); Y++) {
-          const int vy = sd_s[kW7 + Y];
-          const int by = (((vy & 1) && ((vy >> 4) & 15) == qy) ? 0 : 1);
-          for (int X = rx & 255; X <= (rx >> 8); X++) {
-            const int vx = sd_s[X];
-            const int bx = (((vx & 1) && ((vx >> 4) & 15) == qx) ? 0 : 1);
-            const int o = bx + 2 * by + 4 * bz;
-            const int k = (Z * ny + Y) * nx + X;
-            s += mw_s[(o * N + j) * nn + k] * p_s[((Z + 1) * kW7P + (Y + 1)) * kW7P + (X + 1)];
-          }
-        }
-      }
-      c_s[row] = s;
+      double sacc = 0.0;
+      for (int e = rs_s[row], e1 = rs_s[row + 1]; e < e1; e++) sacc += rw_s[e] * p_s[ri_s[e]];
+      c_s[row] = sacc;
     }
     __syncwarp();
   };
@@ -1442,8 +1477,9 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
 
 size_t pcg3d_w7_smem(int N) {
   const size_t NQ = 27 * (size_t)N, NR = 4 * (size_t)N;
-  const size_t d = 27 * kW7NN + 8 * N * kW7NN + kW7NN + NQ * NQ + NR * kW7P * kW7P * kW7P + 2 * NR * NQ;
-  return d * sizeof(double) + (3 * kW7 + 9) * sizeof(int);
+  const size_t EC = 729 * (size_t)N;
+  const size_t d = 27 * kW7NN + 2 * EC + kW7NN + NQ * NQ + NR * kW7P * kW7P * kW7P + 2 * NR * NQ;
+  return d * sizeof(double) + (3 * kW7 + 9 + NQ + 1 + kW7NN + 1 + 2 * EC) * sizeof(int);
 }
 
 cudaError_t launch_pcg3d_w7(const LevelArgs& A, cudaStream_t st) {
