@@ -437,3 +437,83 @@ cudaError_t launch_fine3d_combine(const LevelArgs& A, int max_fine_nodes, cudaSt
   k_fine3d_combine<<<grid, 256, 0, st>>>(A);
   return cudaGetLastError();
 }
+
+// ------------------------------------------------------------------------------------------
+// Eq. (7) on the fused 3D path (R_p = K_p, prefactor 1: reading R12):
+// G[a][b] = sum over the fine cells e of K_p of kappa_e (phi_a|_e)^T K_e (phi_b|_e), all NR
+// right-hand sides of a macropoint in one pass over the cells (k_gram re-reads every cell per a).
+// K_e is the Q1 element stiffness of a cube of side h: (K_e v)_c = h/12 (4 v_c - the four corners
+// that differ from c in >= 2 coordinates) = h/12 (5 v_c - E_{par(c)} - v_{c^7}), E_par the sum over
+// the four corners of c's parity.  Fixed-order block reduction: bitwise reproducible.
+template <int NR>
+__global__ void __launch_bounds__(256) k_gram3_kp(LevelArgs A) {
+  const int mp = blockIdx.x;
+  const ProbDesc& P = A.probs[mp];
+  __shared__ double scratch[32 * (NR * (NR + 1) / 2)];
+  __shared__ double tot[NR * (NR + 1) / 2];
+  constexpr int NP = NR * (NR + 1) / 2;
+  int lo[3], ext[3];
+  for (int i = 0; i < 3; i++) {
+    lo[i] = P.kp_lo[i] - P.lo[i];
+    ext[i] = P.kp_hi[i] - P.kp_lo[i];
+  }
+  const int kn0 = ext[0] + 1, kn1 = ext[1] + 1;
+  const int cnt = ext[0] * ext[1] * ext[2];
+  const double* F = A.FK + (int64_t)mp * NR * A.nkp_max;
+  const double kh = A.h * (1.0 / 12.0);
+  double acc[NP];
+#pragma unroll
+  for (int i = 0; i < NP; i++) acc[i] = 0.0;
+  for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+    const int ex = idx % ext[0], ey = (idx / ext[0]) % ext[1], ez = idx / (ext[0] * ext[1]);
+    const int64_t gc = ((int64_t)(P.kp_lo[2] + ez) * A.n + (P.kp_lo[1] + ey)) * A.n + (P.kp_lo[0] + ex);
+    const double w = __ldg(A.kappa + gc) * kh;
+    const int base = (ez * kn1 + ey) * kn0 + ex;
+    int nid[8];
+#pragma unroll
+    for (int c = 0; c < 8; c++) nid[c] = base + (c & 1) + ((c >> 1) & 1) * kn0 + ((c >> 2) & 1) * kn0 * kn1;
+    double ph[NR][8];
+#pragma unroll
+    for (int r = 0; r < NR; r++)
+#pragma unroll
+      for (int c = 0; c < 8; c++) ph[r][c] = F[(int64_t)r * A.nkp_max + nid[c]];
+    int pi = 0;
+#pragma unroll
+    for (int a = 0; a < NR; a++) {
+      const double ev = ph[a][0] + ph[a][3] + ph[a][5] + ph[a][6];  // even-parity corners
+      const double od = ph[a][1] + ph[a][2] + ph[a][4] + ph[a][7];
+      double y[8];
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        const bool evn = ((c ^ (c >> 1) ^ (c >> 2)) & 1) == 0;
+        y[c] = w * (5.0 * ph[a][c] - (evn ? ev : od) - ph[a][c ^ 7]);
+      }
+#pragma unroll
+      for (int b = a; b < NR; b++, pi++) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; c++) s += y[c] * ph[b][c];
+        acc[pi] += s;
+      }
+    }
+  }
+  block_sum<NP>(acc, scratch, tot);
+  if (threadIdx.x == 0) {
+    double* Gout = A.G + P.lin * NR * NR;
+    int pi = 0;
+    for (int a = 0; a < NR; a++)
+      for (int b = a; b < NR; b++, pi++) {
+        Gout[a * NR + b] = tot[pi];
+        Gout[b * NR + a] = tot[pi];
+      }
+  }
+}
+
+cudaError_t launch_gram3_kp(const LevelArgs& A, cudaStream_t st) {
+  switch (A.n_rhs) {
+    case 4: k_gram3_kp<4><<<A.nprob_mp, 256, 0, st>>>(A); break;
+    case 8: k_gram3_kp<8><<<A.nprob_mp, 256, 0, st>>>(A); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}

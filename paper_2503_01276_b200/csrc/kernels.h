@@ -73,3 +73,5 @@ cudaError_t launch_coarse_setup(const LevelArgs& A, cudaStream_t st);
 size_t fine3d_transport_smem(int N);
 cudaError_t launch_fine3d_transport(const LevelArgs& A, cudaStream_t st);
 cudaError_t launch_fine3d_combine(const LevelArgs& A, int max_fine_nodes, cudaStream_t st);
+// Eq. (7) of all rhs in one pass over the K_p cells (fused 3D path, no source term; n_rhs 4 or 8)
+cudaError_t launch_gram3_kp(const LevelArgs& A, cudaStream_t st);

@@ -846,7 +846,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     }
     if (level >= 2 && B.fused3) CKC(c, launch_fine3d_combine(A, B.max_fn, st));
     else if (level >= 2) CKC(c, launch_combine(A, B.th_f, st));
-    CKC(c, launch_gram(A, 256, st));
+    if (B.fused3 && A.f == nullptr && (nr == 4 || nr == 8)) CKC(c, launch_gram3_kp(A, st));
+    else CKC(c, launch_gram(A, 256, st));
     cudaEventRecord(B.ev[3], st);
     CKC(c, cudaMemcpyAsync(B.h_flags, c->flags.ptr, sizeof(int) * nmp, cudaMemcpyDeviceToHost, st));
     CKC(c, cudaMemcpyAsync(B.h_iters, c->iters.ptr, sizeof(int) * nmp * nr, cudaMemcpyDeviceToHost, st));
