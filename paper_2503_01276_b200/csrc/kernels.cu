@@ -666,21 +666,32 @@ __global__ void k_proj_setup(LevelArgs A) {
   __syncthreads();
   for (int p = 0; p < nc; p++) {
     const double piv = S[p * nc + p];
+    const double ip = 1.0 / piv;  // one division per pivot (r01 divided per element)
     __syncthreads();
     if (threadIdx.x == 0) minpiv = fmin(minpiv, piv);
-    for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
-      const int i = idx / nc, j = idx % nc;
-      if (i != p && j != p) S[idx] -= S[i * nc + p] * S[p * nc + j] / piv;
+    // rank-1 update of the entries off row and column p (element (i, j) stepped without div/mod)
+    {
+      int i = threadIdx.x / nc, j = threadIdx.x - (threadIdx.x / nc) * nc;
+      const int di = blockDim.x / nc, dj = blockDim.x - di * nc;
+      for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+        if (i != p && j != p) S[idx] -= S[i * nc + p] * ip * S[p * nc + j];
+        i += di;
+        j += dj;
+        if (j >= nc) {
+          j -= nc;
+          i++;
+        }
+      }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < nc; i += blockDim.x) {
       if (i != p) {
-        S[i * nc + p] = -S[i * nc + p] / piv;
-        S[p * nc + i] = S[p * nc + i] / piv;
+        S[i * nc + p] = -S[i * nc + p] * ip;
+        S[p * nc + i] = S[p * nc + i] * ip;
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) S[p * nc + p] = 1.0 / piv;
+    if (threadIdx.x == 0) S[p * nc + p] = ip;
     __syncthreads();
   }
   double* out = A.Sinv + (int64_t)mp * nc * nc;

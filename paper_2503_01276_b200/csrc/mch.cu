@@ -787,7 +787,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       CKC(c, cudaEventRecord(c->ev[6], st));
       CKC(c, cudaStreamWaitEvent(c->st2, c->ev[6], 0));
       A.psplit = 1;
-      CKC(c, launch_proj_setup(A, B.th_l, c->st2));
+      CKC(c, launch_proj_setup(A, (D == 3) ? std::max(B.th_l, 256) : B.th_l, c->st2));
       CKC(c, cudaEventRecord(c->ev[7], c->st2));
       A.psplit = 2;
       S.launches += 1;
@@ -797,7 +797,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       S.launches += 1;
     }
     if (psplit) CKC(c, cudaStreamWaitEvent(st, c->ev[7], 0));
-    CKC(c, launch_proj_setup(A, B.th_l, st));
+    CKC(c, launch_proj_setup(A, (D == 3) ? std::max(B.th_l, 256) : B.th_l, st));
     A.psplit = 0;
     CKC(c, launch_pinv(A, st));
     S.launches += 1;
