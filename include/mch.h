@@ -69,7 +69,11 @@ typedef struct {
   int      interp;         /* interpolation of preceding levels (Eq. 11): MCH_INTERP_DLINEAR (0,
                               default) = d-linear on the corners of the T_{n-1} cell (reading
                               R10); MCH_INTERP_NEAREST_S1 (1) = the single nearest S_1 point,
-                              weight 1, as in the paper's experiments */
+                              weight 1, as in the paper's experiments, shifted to
+                              the child in local coordinates (R9); MCH_INTERP_PHYSICAL_S1 (2) =
+                              the nearest S_1 point evaluated at PHYSICAL coordinates, the level-1
+                              windows enlarged by eta^(L-1)/2 layers to contain every child's
+                              window (NEXT-4; d = 2, vertex layout) */
   int      layout;         /* macropoint layout: MCH_LAYOUT_VERTEX (0, default) = x_p = H k,
                               k in {0..M}^d (reading R1); MCH_LAYOUT_BLOCK (1) = block centres
                               x_p = (k + 1/2) H, k in {0..M-1}^d, K_p the block, T_n as in the
@@ -91,6 +95,7 @@ typedef struct {
 
 #define MCH_INTERP_DLINEAR    0
 #define MCH_INTERP_NEAREST_S1 1
+#define MCH_INTERP_PHYSICAL_S1 2
 #define MCH_LAYOUT_VERTEX     0
 #define MCH_LAYOUT_BLOCK      1
 

@@ -93,7 +93,8 @@ class Oracle:
 
     def local_system(self, k):
         """Everything of steps 1-4 for macropoint k (also used by tests)."""
-        d, N, h, l, c = self.d, self.N, self.h, self.l, self.plan.c
+        d, N, h, c = self.d, self.N, self.h, self.plan.c
+        l = self.plan.l_of(k)
         lev = self.plan.level_of(k)
         lo, hi = self.plan.window(k)
         sl = self._slices(lo, hi)
@@ -110,7 +111,7 @@ class Oracle:
         A1 = assemble_stiffness(kap, h)
         C1, V = assemble_constraints(idb, sub, n_sub, N, h)
         active = V > 0
-        cen = self.plan.centre_subcell()
+        cen = self.plan.centre_subcell(k)
         # centring constants on K_p
         cm = np.zeros((d, N))
         xc = [((np.arange(lo[i], hi[i]) + 0.5) * h).reshape(self._axis_shape(i, hi[i] - lo[i]))
@@ -148,7 +149,9 @@ class Oracle:
             pt = self.solve(t)
             src = []
             for i in reversed(range(d)):
-                a = lo[i] + (t[i] - k[i]) * c - pt["lo"][i]
+                # local coordinates (R9): shift by x_t - x_p; physical (NEXT-4): none
+                shift = 0 if self.plan.interp == "physical_s1" else (t[i] - k[i]) * c
+                a = lo[i] + shift - pt["lo"][i]
                 src.append(slice(a, a + hi[i] - lo[i] + 1))
             I += wt * pt["phi"][(slice(None),) + tuple(src)]
         return I.reshape(self.n_rhs, -1)

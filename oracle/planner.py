@@ -54,8 +54,10 @@ class Plan:
         if n % M:
             raise ValueError("M must divide n (H/h integer)")
         self.d, self.n, self.M, self.L, self.eta, self.l = d, n, M, L, eta, l
-        if interp not in ("dlinear", "nearest_s1"):
-            raise ValueError("interp must be 'dlinear' or 'nearest_s1'")
+        if interp not in ("dlinear", "nearest_s1", "physical_s1"):
+            raise ValueError("interp must be 'dlinear', 'nearest_s1' or 'physical_s1'")
+        if interp == "physical_s1" and layout != "vertex":
+            raise ValueError("the physical-coordinate variant is built for the vertex layout")
         if layout not in ("vertex", "block"):
             raise ValueError("layout must be 'vertex' or 'block'")
         self.interp, self.layout = interp, layout
@@ -114,9 +116,18 @@ class Plan:
         """2 × fine-cell coordinate of x_p along one dimension (vertex k·c, block k·c + c/2)"""
         return 2 * ki * self.c + (self.c if self.layout == "block" else 0)
 
+    def l_of(self, k) -> int:
+        """oversampling layers of macropoint k's window: l, except the level-1 points of the
+        physical-coordinate variant (NEXT-4: "level-1 regions enlarged to the
+        union of R_p^+ over all assigned children"): a child assigned to its nearest S_1 point lies
+        within η^{L-1}H/2 of it per coordinate, so l + η^{L-1}/2 layers cover every child's window"""
+        if self.interp == "physical_s1" and self.level_of(k) == 1:
+            return self.l + self.eta ** (self.L - 1) // 2
+        return self.l
+
     def window(self, k):
         """fine-cell box [lo, hi) per dimension of R_p^+ = x_p ± (l+½)H, clipped"""
-        w2 = (2 * self.l + 1) * self.c  # 2 × half width
+        w2 = (2 * self.l_of(k) + 1) * self.c  # 2 × half width
         lo = tuple(max(0, (self.origin2(ki) - w2) // 2) for ki in k)
         hi = tuple(min(self.n, (self.origin2(ki) + w2) // 2) for ki in k)
         return lo, hi
@@ -130,17 +141,19 @@ class Plan:
     def subcell_of_cell(self, k, cell):
         """local subcell index q of a global fine cell inside R_p^+"""
         q = 0
-        w = 2 * self.l + 1
+        lk = self.l_of(k)
+        w = 2 * lk + 1
         for i in reversed(range(self.d)):
             v = self.subcell_coord(cell[i])
-            slot = v - k[i] + self.l
+            slot = v - k[i] + lk
             assert 0 <= slot < w
             q = q * w + slot
         return q
 
-    def centre_subcell(self) -> int:
-        w = 2 * self.l + 1
-        return sum(self.l * w ** i for i in range(self.d))
+    def centre_subcell(self, k=None) -> int:
+        lk = self.l if k is None else self.l_of(k)
+        w = 2 * lk + 1
+        return sum(lk * w ** i for i in range(self.d))
 
     # -- hierarchy -------------------------------------------------------------
     def covers(self, t_i: int, k_i: int) -> bool:
@@ -180,6 +193,18 @@ class Plan:
         lev = self.level_of(k)
         if lev == 1:
             return []
+        if self.interp == "physical_s1":
+            # NEXT-4: the nearest S_1 point (ties: the smaller coordinate), weight 1, evaluated at
+            # physical coordinates; its enlarged window contains the child's (checked)
+            t = []
+            for ki in k:
+                cands = [ti for ti, _ in self._lattice_neighbours(ki, 1)]
+                t.append(min(cands, key=lambda ti: (abs(ti - ki), ti)))
+            t = tuple(t)
+            (plo, phi), (clo, chi) = self.window(t), self.window(k)
+            if not all(plo[i] <= clo[i] and phi[i] >= chi[i] for i in range(self.d)):
+                raise ValueError(f"parent {t} does not contain the window of {k}")
+            return [(t, 1.0)]
         if self.interp == "nearest_s1":
             t = []
             for ki in k:

@@ -38,7 +38,7 @@ def _current_stream():
     return None
 
 
-INTERP = {"dlinear": 0, "nearest_s1": 1}
+INTERP = {"dlinear": 0, "nearest_s1": 1, "physical_s1": 2}
 LAYOUT = {"vertex": 0, "block": 1}
 
 
@@ -173,6 +173,7 @@ class Homogenizer:
                  world=1, keep_all=False, stream=None, interp="dlinear", layout="vertex",
                  torch_memory=False, comm=None):
         self.d, self.n, self.N, self.M, self.L, self.eta, self.l = d, n, N, M, L, eta, l
+        self.interp = interp
         self.n_rhs = N * (1 + d)
         self.mv = M + 1 if layout == "vertex" else M  # macropoints per dimension
         self.num_macropoints = self.mv ** d
@@ -279,8 +280,9 @@ class Homogenizer:
         mp = k if isinstance(k, (int, np.integer)) else self.linear_index(k)
         ext = (ctypes.c_int64 * 3)()
         cap = 1
+        lmax = self.l + (self.eta ** (self.L - 1) // 2 if self.interp == "physical_s1" else 0)
         for _ in range(self.d):
-            cap *= (2 * self.l + 1) * (self.n // self.M) + 1
+            cap *= (2 * lmax + 1) * (self.n // self.M) + 1
         out = np.zeros(cap)
         check(lib.mch_local_solution(self.ctx, mp, rhs, out.ctypes.data, cap, ext), self.ctx)
         shape = tuple(ext[i] for i in reversed(range(self.d)))

@@ -184,7 +184,7 @@ __global__ void k_transport(LevelArgs A) {
     for (int t = 0; t < P.npar; t++) {
       int64_t idx = 0;
       for (int i = D - 1; i >= 0; i--) {
-        const int xt = P.lo[i] + x[i] + (P.par_k[t][i] - P.k[i]) * A.c - P.par_lo[t][i];
+        const int xt = P.lo[i] + x[i] + (A.phys ? 0 : (P.par_k[t][i] - P.k[i]) * A.c) - P.par_lo[t][i];
         idx = idx * (P.par_ncf[t][i] + 1) + xt;
       }
       int64_t pn = 1;
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(256) k_transport2d_mr(LevelArgs A) {
     for (int t = 0; t < P.npar; t++) {
       int64_t idx = 0;
       for (int i = 1; i >= 0; i--) {
-        const int xt = P.lo[i] + x[i] + (P.par_k[t][i] - P.k[i]) * A.c - P.par_lo[t][i];
+        const int xt = P.lo[i] + x[i] + (A.phys ? 0 : (P.par_k[t][i] - P.k[i]) * A.c) - P.par_lo[t][i];
         idx = idx * (P.par_ncf[t][i] + 1) + xt;
       }
       const int64_t pn = (int64_t)(P.par_ncf[t][0] + 1) * (P.par_ncf[t][1] + 1);
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(256) k_transport3d_mr(LevelArgs A) {
       for (int t = 0; t < P.npar; t++) {
         int64_t idx = 0;
         for (int i = 2; i >= 0; i--) {
-          const int xt = P.lo[i] + x[i] + (P.par_k[t][i] - P.k[i]) * A.c - P.par_lo[t][i];
+          const int xt = P.lo[i] + x[i] + (A.phys ? 0 : (P.par_k[t][i] - P.k[i]) * A.c) - P.par_lo[t][i];
           idx = idx * (P.par_ncf[t][i] + 1) + xt;
         }
         int64_t pn = 1;

@@ -272,9 +272,21 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   c->plan.L = p.levels;
   c->plan.eta = p.eta;
   c->plan.l = p.oversample;
-  if (p.interp != 0 && p.interp != 1) {
+  if (p.interp < 0 || p.interp > 2) {
     delete c;
-    return fail(nullptr, MCH_EINVAL, "interp must be MCH_INTERP_DLINEAR or MCH_INTERP_NEAREST_S1");
+    return fail(nullptr, MCH_EINVAL, "interp must be MCH_INTERP_DLINEAR, MCH_INTERP_NEAREST_S1 or MCH_INTERP_PHYSICAL_S1");
+  }
+  if (p.interp == 2) {
+    // NEXT-4: level-1 windows of l + eta^(L-1)/2 layers; built for 2D vertex windows whose level-1
+    // constraint rows fit the dense projector of the generic PCG
+    int64_t e = 1;
+    for (int i = 1; i < p.levels; i++) e *= p.eta;
+    const int l1 = p.oversample + (int)(e / 2), w1 = 2 * l1 + 1;
+    if (p.d != 2 || p.layout != 0 || w1 * w1 * p.num_continua > 108 || c->band != 0) {
+      delete c;
+      return fail(nullptr, MCH_EINVAL,
+                  "MCH_INTERP_PHYSICAL_S1 needs d = 2, the vertex layout and <= 108 level-1 constraint rows");
+    }
   }
   c->plan.interp = p.interp;
   if (p.layout != 0 && p.layout != 1) {
@@ -401,8 +413,19 @@ struct LevelVariant {
   bool coarse = false;
 };
 
+// oversampling layers, subcells per dimension, subcells and constraint rows of a level's windows
+// (level 1 of the physical-coordinate variant has more, NEXT-4)
+static void level_geometry(const mch_ctx* c, int level, int& l, int& w, int& nsub, int& nc) {
+  l = c->plan.lwin(level);
+  w = 2 * l + 1;
+  nsub = (c->D == 2) ? w * w : w * w * w;
+  nc = nsub * c->N;
+}
+
 static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelBatch>>& out) {
-  const int D = c->D, N = c->N, nr = c->n_rhs, nc = c->ncon;
+  const int D = c->D, N = c->N, nr = c->n_rhs;
+  int lvl_l, lvl_w, lvl_nsub, nc;
+  level_geometry(c, level, lvl_l, lvl_w, lvl_nsub, nc);
   const HostPlan& pl = c->plan;
   const int s = (int)ipow64(c->p.eta, level - 1);
   const std::vector<int64_t>& Sl = pl.S[level];
@@ -462,7 +485,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       if (gmaxn > nxm || pcg2d_smem_t(N, l1op != 0, nxm, maxw, sstc != 0, smlr != 0, crs_v) > 232448) continue;
       int maxwp = 0;
       for (size_t i = 0; i < gd.size(); i++) {
-        seg_plan_2d(gd[i], s, (int)pl.c, (int)pl.coff(), c->l, rpt, tmp);
+        seg_plan_2d(gd[i], s, (int)pl.c, (int)pl.coff(), lvl_l, rpt, tmp);
         maxwp = std::max(maxwp, ((gd[i].nc[0] + 1 + 31) / 32) * (int)tmp.size());
       }
       const int rp4 = (rpt + 3) & ~3;  // TMEM: warps per lane quarter x (q, x [, component ids])
@@ -488,7 +511,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
     const char* f3e = getenv("MCH_FINE3D");
     const bool generic_t = getenv("MCH_TRANSPORT_GENERIC") != nullptr;
     V.tsplit = level >= 2 && gmaxf <= 49 && pcg3d_l1_smem(N) <= 232448 && !generic_t;
-    V.fused3 = level >= 2 && c->l == 1 && pl.c >= 4 && gmaxf <= 49 && fine3d_transport_smem(N) <= 232448 &&
+    V.fused3 = level >= 2 && lvl_l == 1 && pl.c >= 4 && gmaxf <= 49 && fine3d_transport_smem(N) <= 232448 &&
                !(f3e && atoi(f3e) == 0) && !generic_t;
     if (level >= 2) {
       const int nxm = pcg3d_nxm(gmaxn);
@@ -519,6 +542,11 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
   // whose shared memory holds the coarse data; 3D level 1 and the 25-node level-2 windows (the 13-
   // and 7-node windows of deeper levels showed no iteration change)
   V.coarse = c->coarse && c->band == 0 && (V.on2d ? V.crs2d : (level == 1 || (V.on3d && V.nxm3 == 25)));
+  // the projector setup stages S, its copy and (C Z) in shared memory: without the coarse space
+  // where that does not fit (the 98-row level-1 windows of the physical-coordinate variant)
+  if (V.coarse && sizeof(double) * (2.0 * nc * nc + 32 * 16 + 16 + (lvl_nsub * 7 + 2 + 1) / 2 + 2 +
+                                    (double)(nc + 1) * kCoarseMax) > 232448)
+    V.coarse = false;
   const double kpn = (double)V.max_kp;
 
   // ---- this rank's macropoints, batched by memory
@@ -598,7 +626,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       std::vector<std::vector<short4>> per(nmp);
       int maxseg = 0;
       for (int i = 0; i < nmp; i++) {
-        seg_plan_2d(descs[i], s, (int)pl.c, (int)pl.coff(), c->l, V.rpt, per[i]);
+        seg_plan_2d(descs[i], s, (int)pl.c, (int)pl.coff(), lvl_l, V.rpt, per[i]);
         nsegs[i] = (int)per[i].size();
         maxseg = std::max(maxseg, nsegs[i]);
       }
@@ -696,7 +724,9 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   char nv_name[40];
   snprintf(nv_name, sizeof nv_name, "mch_solve_level %d", level);
   NvtxRange nv_level(nv_name);
-  const int D = c->D, N = c->N, nr = c->n_rhs, nc = c->ncon;
+  const int D = c->D, N = c->N, nr = c->n_rhs;
+  int lvl_l, lvl_w, lvl_nsub, nc;
+  level_geometry(c, level, lvl_l, lvl_w, lvl_nsub, nc);
   const HostPlan& pl = c->plan;
   const int s = (int)ipow64(c->p.eta, level - 1);
   const int gn = (int)(pl.n / s);
@@ -715,7 +745,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   cudaEventRecord(c->ev[0], st);
 
   LevelArgs A{};
-  A.D = D; A.N = N; A.n_rhs = nr; A.l = c->l; A.w = c->w; A.nsub = c->nsub; A.ncon = nc;
+  A.D = D; A.N = N; A.n_rhs = nr; A.l = lvl_l; A.w = lvl_w; A.nsub = lvl_nsub; A.ncon = nc;
+  A.phys = (c->p.interp == 2) ? 1 : 0;  // NEXT-4: parents evaluated at physical coordinates
   A.level = level; A.s = s; A.n = (int)pl.n; A.c = (int)pl.c; A.coff = (int)pl.coff(); A.gn = gn; A.h = 1.0 / (double)pl.n; A.inv_c = 1.0f / (float)pl.c;
   A.kappa = c->kappa; A.ids = c->ids; A.pool = c->pool; A.G = c->G;
   A.f = c->has_source ? c->fsrc.as<double>() : nullptr;

@@ -78,6 +78,7 @@ struct LevelArgs {
   int* azp;                // [mp][ncmax+1] start of each component's (A z_a) list (2D on-chip kernels)
   int* azi;                // [kAzCap * nodes] node of each entry, packed x | y << 16
   double* azw;             // [kAzCap * nodes] (A z_a) at that node
+  int phys;                // 1: parents at physical coordinates (NEXT-4), 0: local coordinates (R9)
   int tphase;              // k_transport: 0 all phases; 1 only I_p; 2 only the restriction (3D split path)
   int psplit;              // k_proj_setup: 0 whole; 1 only S = C D^-1 C^T (into Sinv); 2 the rest from it
   const double* f;         // NEXT-2: cellwise source, n^D, x fastest (NULL: no load vectors)

@@ -38,8 +38,13 @@ int HostPlan::level_of(const int* k) const {
 // 2 x fine-cell coordinate of x_p along one dimension
 int64_t HostPlan::origin2(int k) const { return 2 * (int64_t)k * c + (layout == 1 ? c : 0); }
 
+// NEXT-4: with interp 2 a child is assigned to its nearest S_1 point, at most
+// eta^(L-1) H / 2 away per coordinate, and the level-1 windows are enlarged by that much so they
+// contain the windows of all their children (no extrapolation of phi_t is needed)
+int HostPlan::lwin(int level) const { return (interp == 2 && level == 1) ? l + (int)(ipow(eta, L - 1) / 2) : l; }
+
 void HostPlan::window(const int* k, int* lo, int* hi) const {
-  const int64_t w2 = (2 * l + 1) * c;
+  const int64_t w2 = (2 * lwin(level_of(k)) + 1) * c;
   for (int i = 0; i < 3; i++) {
     if (i >= D) { lo[i] = 0; hi[i] = 1; continue; }
     const int64_t a = (origin2(k[i]) - w2) / 2, b = (origin2(k[i]) + w2) / 2;
@@ -130,7 +135,7 @@ int HostPlan::build(std::string& err) {
     MacroHost& m = all[lin];
     m.npar = 0;
     if (m.level == 1) continue;
-    const int plev = (interp == 1) ? 1 : m.level - 1;
+    const int plev = (interp >= 1) ? 1 : m.level - 1;
     int cand[3][2], ncand[3];
     double wc[3][2];
     for (int i = 0; i < D; i++) {
@@ -139,8 +144,8 @@ int HostPlan::build(std::string& err) {
       const int nb = bracket(m.k[i], plev, t, w);
       int nk = 0;
       bool keep[2] = {false, false};
-      for (int j = 0; j < nb; j++) keep[j] = covers(t[j], m.k[i]);
-      if (interp == 1) {  // nearest covering point, ties: the smaller coordinate (t[0] < t[1])
+      for (int j = 0; j < nb; j++) keep[j] = (interp == 2) ? true : covers(t[j], m.k[i]);
+      if (interp >= 1) {  // nearest covering point, ties: the smaller coordinate (t[0] < t[1])
         int best = -1;
         for (int j = 0; j < nb; j++)
           if (keep[j] && (best < 0 || std::abs(t[j] - m.k[i]) < std::abs(t[best] - m.k[i]))) best = j;
@@ -158,6 +163,17 @@ int HostPlan::build(std::string& err) {
       ncand[i] = nk;
     }
     for (int i = D; i < 3; i++) { cand[i][0] = 0; wc[i][0] = 1.0; ncand[i] = 1; }
+    if (interp == 2) {  // the enlarged parent window must contain the child's (physical coordinates)
+      int t3[3] = {cand[0][0], cand[1][0], cand[2][0]}, plo[3], phi[3];
+      window(t3, plo, phi);
+      for (int i = 0; i < D; i++)
+        if (plo[i] > m.lo[i] || phi[i] < m.hi[i]) {
+          char buf[160];
+          snprintf(buf, sizeof buf, "parent window does not contain macropoint (%d,%d,%d)", m.k[0], m.k[1], m.k[2]);
+          err = buf;
+          return -8;
+        }
+    }
     for (int cz = 0; cz < ncand[2]; cz++)
       for (int cy = 0; cy < ncand[1]; cy++)
         for (int cx = 0; cx < ncand[0]; cx++) {

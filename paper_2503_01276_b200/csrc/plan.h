@@ -15,7 +15,8 @@ struct MacroHost {
 
 struct HostPlan {
   int D = 2, L = 1, eta = 2, l = 1;
-  int interp = 0;  // 0: d-linear on T_{n-1} (R10); 1: nearest covering S_1 point, weight 1
+  int interp = 0;  // 0: d-linear on T_{n-1} (R10); 1: nearest covering S_1 point, weight 1;
+                   // 2: nearest S_1 point in physical coordinates, enlarged level-1 windows (NEXT-4)
   int layout = 0;  // 0: vertex-centred (R1); 1: block-centred (paper Figs. 2-3)
   int64_t n = 0, M = 0, c = 0;
   int64_t mv = 0;          // macropoints per dimension: M+1 (vertex) or M (block)
@@ -25,6 +26,7 @@ struct HostPlan {
   int build(std::string& err);
   int level_of(const int* k) const;
   void window(const int* k, int* lo, int* hi) const;
+  int lwin(int level) const;  // oversampling layers of a level's windows (l; level 1 of interp 2: l + eta^(L-1)/2)
   bool covers(int t, int k) const;
   int64_t origin2(int k) const;
   int bracket(int k, int lev, int* t, double* w) const;

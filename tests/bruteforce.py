@@ -21,9 +21,12 @@ def _vertices(d, M):
 
 
 class BruteForce:
-    def __init__(self, d, n, M, L, eta, N, kappa, ids, l=1, layout="vertex"):
+    def __init__(self, d, n, M, L, eta, N, kappa, ids, l=1, layout="vertex", physical=False):
         self.d, self.n, self.M, self.L, self.eta, self.N, self.l = d, n, M, L, eta, N, l
         self.layout = layout
+        # NEXT-4: nearest S_1 parent in physical coordinates, level-1 regions
+        # enlarged to contain the windows of every child assigned to them
+        self.physical = physical
         self.h = 1.0 / n
         self.H = 1.0 / M
         self.kappa = kappa.reshape((n,) * d)
@@ -70,13 +73,24 @@ class BruteForce:
             if self.in_T(k, lev):
                 return lev
 
+    def lk(self, k):
+        """layers of k's window: level-1 points of the physical variant reach every assigned child,
+        i.e. the children within half the S_1 spacing, η^{L-1}H/2"""
+        if self.physical and self.level(k) == 1:
+            return self.l + self.eta ** (self.L - 1) // 2
+        return self.l
+
     def window(self, k):
         """physical box [a_i, b_i] of R_p^+ = x_p ± (l+1/2)H clipped to [0,1]"""
-        r = (self.l + 0.5) * self.H
+        r = (self.lk(k) + 0.5) * self.H
         return [(max(0.0, x - r), min(1.0, x + r)) for x in self.xp(k)]
 
     def parents(self, k):
         lev = self.level(k)
+        if self.physical:  # the S_1 point nearest to x_p (max-norm ties: smaller coordinates)
+            S1 = [t for t in self.points() if self.level(t) == 1]
+            best = min(S1, key=lambda t: (sum((t[i] - k[i]) ** 2 for i in range(self.d)), tuple(reversed(t))))
+            return [(best, 1.0)]
         s = self.eta ** (self.L - lev + 1)
         Tprev = [t for t in self.points() if self.in_T(t, lev - 1)]
         # per coordinate: candidate lattice values within distance < s, linear weights
@@ -125,7 +139,8 @@ class BruteForce:
         # quadrature over fine elements
         A1 = np.zeros((nn, nn))
         AK = np.zeros((nn, nn))
-        nsub = (2 * self.l + 1) ** d
+        lk = self.lk(k)
+        nsub = (2 * lk + 1) ** d
         C1 = np.zeros((nsub * N, nn))
         V = np.zeros(nsub * N)
         mom = np.zeros((nsub * N, d))     # ∫_{R_q} x_m ψ_j
@@ -158,7 +173,7 @@ class BruteForce:
                   for i in range(d)]
             q = 0
             for i in reversed(range(d)):
-                q = q * (2 * self.l + 1) + (vq[i] - k[i] + self.l)
+                q = q * (2 * lk + 1) + (vq[i] - k[i] + lk)
             in_kp = all(vq[i] == k[i] for i in range(d))
             Ke = kap * Kref
             A1[np.ix_(cid, cid)] += Ke
@@ -184,7 +199,7 @@ class BruteForce:
         if lev >= 2:
             for t, w in self.parents(k):
                 pt = self.solve(t)
-                shift = np.array([(t[i] - k[i]) * self.H for i in range(d)])
+                shift = np.zeros(d) if self.physical else np.array([(t[i] - k[i]) * self.H for i in range(d)])
                 Xt = X + shift
                 idx = [pt["nid"][tuple(int(round((Xt[a, i] - pt["x0"][i]) / h)) for i in range(d))]
                        for a in range(nn)]

@@ -56,7 +56,9 @@ def _create(**kw):
     (dict(ids=np.full((32, 32), 3, dtype=np.uint8), N=2), -1),  # id >= N
     (dict(d=3, n=16, M=2, N=2, l=2), -1),             # 5^3 subcells x 2 continua > 108 constraint rows
     (dict(n=64, M=4, N=4, l=6), -1),                  # 2D banded projector: 676 rows x 60 band > smem
-    (dict(interp=2), -1),                             # unknown interpolation mode
+    (dict(interp=3), -1),                             # unknown interpolation mode
+    (dict(interp=2, d=3, n=16, M=4, L=2, N=2), -1),   # physical-coordinate variant: 2D only
+    (dict(interp=2, n=64, M=8, L=3, N=3), -1),        # ... and <= 108 level-1 rows (7x7x3 = 147)
     (dict(layout=2), -1),                             # unknown macropoint layout
     (dict(n=36, M=6, L=3, layout=1), -2),             # block layout: H/(2 h eta^(L-1)) = 3/4 not integer
 ])

@@ -669,3 +669,24 @@ def test_rejected_medium_blocks_solves():
         h.set_medium(kap, ids)
         h.solve_all()
         assert np.isfinite(h.effective_coeffs()).all()
+
+
+@pytest.mark.parametrize("d,n,M,L,N", [(2, 32, 8, 2, 2), (2, 64, 8, 3, 2), (2, 64, 8, 3, 1)])
+def test_physical_transport_all_points(d, n, M, L, N):
+    """NEXT-4: nearest-S_1 parent at physical coordinates with
+    enlarged level-1 windows — every macropoint (G and φ) vs the oracle with the same reading."""
+    H = _gpu()
+    kap, ids = _admissible(d, n, M, N, 70 + d + N)
+    o = Oracle(d, n, M, L, 2, N, kap, ids, interp="physical_s1")
+    Go = o.effective_coeffs()
+    with H(d, n, N, M, L, 2, kap, ids, keep_all=True, interp="physical_s1") as h:
+        h.solve_all()
+        Gg = h.effective_coeffs()
+        for k in o.plan.all_vertices():
+            i = o.plan.linear_index(k)
+            assert g_err(Gg[i], Go[i]) < G_TOL, (k, g_err(Gg[i], Go[i]))
+            po = o.solve(k)["phi"]
+            for r in range(o.n_rhs):
+                pg = h.local_solution(k, r)
+                assert pg.shape == po[r].shape
+                assert phi_err(pg, po[r]) < PHI_TOL, (k, r, phi_err(pg, po[r]))
