@@ -1498,6 +1498,8 @@ cudaError_t launch_pcg3d_w7(const LevelArgs& A, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+
+
 // ------------------------------------------------------------------------------------------
 size_t pcg3d_smem(int N, int nxm) {
   const size_t d = (size_t)(nxm + 2) * (nxm + 2) * nxm + (size_t)nxm * 27 * N + 2 * 27 * N + 5 * 32 + 512;

@@ -599,8 +599,8 @@ def test_transport_paths_agree(d, n, M, L, N, seed, monkeypatch):
 def test_3d_level_paths_agree(d, n, M, L, N, seed, monkeypatch):
     """3D levels >= 2: the fused fine-window passes (fine3d.cu, default), the split transport
     (MCH_FINE3D=0) and the generic per-(macropoint, rhs) kernels (MCH_TRANSPORT_GENERIC=1), and the
-    block PCG of the 7³ windows (k_pcg3d_w7, default) vs the per-(macropoint, rhs) k_pcg3d
-    (MCH_PCG3D_W7=0): every path matches the oracle at every macropoint (R15 bar) and the paths
+    PCG of the 7³ windows — one warp per rhs (k_pcg3d_w7, default) vs the per-(macropoint, rhs)
+    k_pcg3d (MCH_PCG3D_W7=0): every path matches the oracle at every macropoint (R15 bar) and the paths
     agree with each other to 1e-10 of each macropoint's largest energy."""
     H = _gpu()
     kap, ids = _admissible(d, n, M, N, seed)
