@@ -340,7 +340,7 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   }
   // sharding: contiguous cost-balanced runs of each S_n per rank, parent transfers
   shard_build(c->plan, p.world, c->shard);
-  if (p.world > 1 && p.nccl_comm) {
+  if (p.nccl_comm) {  // also with world == 1 (a one-rank communicator: the collectives are copies)
     std::string nerr;
     c->nccl = nccl_api(nerr);
     if (!c->nccl) return cleanup(MCH_ENCCL, nerr);

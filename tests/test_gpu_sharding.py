@@ -82,3 +82,30 @@ def test_missing_transfer_is_detected():
     except RuntimeError:
         return  # NaN parent -> PCG breakdown reported (MCH_ENOCONV)
     assert not np.array_equal(G1, Gw) and not np.all(np.isfinite(Gw))
+
+
+def test_library_nccl_single_rank():
+    """The library's NCCL path on one GPU: mch_comm_id / mch_comm_init (NCCL resolved at run time from
+    libnccl.so.2) build a one-rank communicator; a context created with it runs the collective
+    mch_effective_coeffs (ncclAllReduce) and must return the same coefficients, bitwise, as a
+    context without one.  (The point-to-point parent exchange needs >= 2 GPUs.)"""
+    import torch
+    from paper_2503_01276_b200 import Homogenizer
+    from paper_2503_01276_b200.api import mch_comm_destroy, mch_comm_id, mch_comm_init
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    d, n, M, L, N = 2, 64, 8, 3, 2
+    kap, ids = _admissible(d, n, M, N, 81)
+    with Homogenizer(d, n, N, M, L, 2, kap, ids) as h:
+        h.solve_all()
+        G0 = h.effective_coeffs()
+    uid = mch_comm_id()
+    assert len(uid) == 128
+    comm = mch_comm_init(1, 0, uid)
+    try:
+        with Homogenizer(d, n, N, M, L, 2, kap, ids, comm=comm) as h:
+            h.solve_all()
+            G1 = h.effective_coeffs()
+    finally:
+        mch_comm_destroy(comm)
+    assert np.array_equal(G0, G1)
