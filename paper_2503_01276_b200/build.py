@@ -36,6 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     libdir = os.path.dirname(LIB)
+    os.makedirs(libdir, exist_ok=True)
     # objects outside the repo: the tree is pushed to the GPU box as is, the .so alone is needed
     objdir = os.path.join(os.environ.get("TMPDIR", "/tmp"), "mch_obj")
     os.makedirs(objdir, exist_ok=True)
