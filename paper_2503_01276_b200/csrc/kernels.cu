@@ -550,9 +550,20 @@ __global__ void k_proj_setup(LevelArgs A) {
   __shared__ int ntask;
   subcell_boxes<D>(A, P, g, eb, &ntask);  // also syncs (dinv visible to block)
   const int N = A.N;
-  // S = C D^-1 C^T over pairs of subcells that share nodes
-  for (int q1 = 0; q1 < A.nsub; q1++) {
-    for (int q2 = q1; q2 < A.nsub; q2++) {
+  // S = C D^-1 C^T over pairs of subcells that share nodes: one warp per pair (q1 <= q2), lanes over
+  // the nodes of the two subcells' common node box, warp reduction in a fixed order.  No block
+  // barrier per pair (r01/r02 reduced every pair over the CTA: two barriers each, ~190 pairs per
+  // 3x3x3 window)
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+    const int nsub = A.nsub, npairs = nsub * (nsub + 1) / 2;
+    for (int pi = wid; pi < npairs; pi += nwp) {
+      int q1 = 0, rem = pi;
+      while (rem >= nsub - q1) {
+        rem -= nsub - q1;
+        q1++;
+      }
+      const int q2 = q1 + rem;
       const int* b1 = eb + q1 * 6;
       const int* b2 = eb + q2 * 6;
       int lo[3], hi[3];
@@ -564,12 +575,12 @@ __global__ void k_proj_setup(LevelArgs A) {
         hi[i] = min(b1[i] + b1[3 + i], b2[i] + b2[3 + i]);  // node ranges are [lo, lo+ext] inclusive
         if (hi[i] < lo[i]) { empty = true; break; }
       }
-      if (empty) continue;  // uniform across the block
+      if (empty) continue;  // uniform across the warp
       const int ex = hi[0] - lo[0] + 1, ey = hi[1] - lo[1] + 1, ez = hi[2] - lo[2] + 1;
       const int cnt = ex * ey * ez;
       double v[16];
       for (int i = 0; i < 16; i++) v[i] = 0.0;
-      for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+      for (int idx = lane; idx < cnt; idx += 32) {
         const int x[3] = {lo[0] + idx % ex, lo[1] + (idx / ex) % ey, lo[2] + idx / (ex * ey)};
         const int k = node_id<D>(g, x);
         double w1[4] = {0, 0, 0, 0}, w2[4] = {0, 0, 0, 0};
@@ -594,25 +605,19 @@ __global__ void k_proj_setup(LevelArgs A) {
         for (int j1 = 0; j1 < N; j1++)
           for (int j2 = 0; j2 < N; j2++) v[j1 * 4 + j2] += w1[j1] * w2[j2] * di;
       }
-      // reduce only the N x N entries in use (N <= 2: 4 of the 16; the shuffles dominated)
-      int ts = 4;
-      if (N <= 2) {
-        double v4[4] = {v[0], v[1], v[4], v[5]};
-        block_sum<4>(v4, scratch, tot);
-        ts = 2;
-      } else {
-        block_sum<16>(v, scratch, tot);
-      }
-      if (threadIdx.x == 0) {
-        for (int j1 = 0; j1 < N; j1++)
-          for (int j2 = 0; j2 < N; j2++) {
+      for (int j1 = 0; j1 < N; j1++)
+        for (int j2 = 0; j2 < N; j2++) {
+          double t = v[j1 * 4 + j2];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULLMASK, t, o);
+          if (lane == 0) {
             const int r1 = q1 * N + j1, r2 = q2 * N + j2;
-            S[r1 * nc + r2] = tot[j1 * ts + j2];
-            S[r2 * nc + r1] = tot[j1 * ts + j2];
+            S[r1 * nc + r2] = t;
+            S[r2 * nc + r1] = t;
           }
-      }
-      __syncthreads();
+        }
     }
+    __syncthreads();
   }
   if (A.psplit == 1) {  // first half (beside k_coarse_setup): hand S over in Sinv
     double* so = A.Sinv + (int64_t)mp * nc * nc;
@@ -1286,6 +1291,150 @@ __global__ void k_proj_setup_band(LevelArgs A) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Reading R20, direct form.  S~ (unit diagonal on active rows) is factored by
+// Cholesky with diagonal pivoting, S~ = L L^T + T, stopping at rank r when every remaining pivot is
+// <= 1e-11 (T: the trailing Schur complement).  Then S~^+ = L G^-2 L^T with G = L^T L (r x r; its
+// eigenvalues are the r nonzero eigenvalues of L L^T), i.e. W W^T with W = L G^-1.  This equals
+// the eigen-truncated pseudo-inverse of the oracle (eigenvalues <= 1e-11 lambda_max dropped) when
+// both decide the same rank, which two bounds certify:
+//   (a) trace(T) <= 1e-12: by Weyl, the n - r smallest eigenvalues of S~ are <= lambda_max(T) <=
+//       trace(T) < 1e-11 <= 1e-11 lambda_max (lambda_max >= max diag = 1): all dropped by the oracle;
+//   (b) 1 / trace(G^-1) >= 1e-9 n: the r largest eigenvalues of S~ are >= those of L L^T (T is
+//       PSD) >= lambda_min(G) >= 1 / trace(G^-1) > 1e-11 n >= 1e-11 lambda_max: all kept.
+// A window that fails either bound is left to the Jacobi eigen-solver (k_pinv, flag 16).
+// Per window n pivot steps with three barriers each plus one Gauss-Jordan inverse of G, against the
+// ~10 Jacobi sweeps x (n - 1) rounds x 3 barriers of k_pinv.
+__global__ void k_pinv_all_jacobi(LevelArgs A) {  // dev switch MCH_PINV_JACOBI: skip the direct form
+  const int mp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (mp < A.nprob_mp && (A.flags[mp] & 2)) A.flags[mp] |= 16;
+}
+
+__global__ void __launch_bounds__(256) k_pinv_chol(LevelArgs A) {
+  const int mp = blockIdx.x;
+  if (!(A.flags[mp] & 2)) return;
+  const int n = A.ncon, tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
+  extern __shared__ double sm[];
+  double* Sw = sm;           // n*n working Schur complement, later W = L G^-1 (n x r)
+  double* Lc = Sw + n * n;   // column k of L at Lc[k*n + i] (i: original row index)
+  double* Gm = Lc + n * n;   // G = L^T L, inverted in place (r x r, stride n)
+  int* done = reinterpret_cast<int*>(Gm + n * n);  // n
+  __shared__ int piv_s, amb_s;
+  __shared__ double dp_s;
+  double* Sg = A.Sinv + (int64_t)mp * n * n;
+  for (int idx = tid; idx < n * n; idx += nt) Sw[idx] = Sg[idx];
+  for (int i = tid; i < n; i += nt) done[i] = 0;
+  __syncthreads();
+  int r = 0;
+  for (int k = 0; k < n; k++) {
+    if (tid < 32) {  // largest remaining pivot, ties to the smaller index
+      double best = -1.0;
+      int bi = n;
+      for (int i = lane; i < n; i += 32) {
+        const double d = Sw[i * n + i];
+        if (!done[i] && d > best) { best = d; bi = i; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(FULLMASK, best, o);
+        const int oi = __shfl_xor_sync(FULLMASK, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) { piv_s = bi; dp_s = best; }
+    }
+    __syncthreads();
+    if (!(dp_s > 1e-11)) break;  // uniform
+    const int p = piv_s;
+    const double lp = sqrt(dp_s), ilp = 1.0 / lp;
+    for (int i = tid; i < n; i += nt) Lc[k * n + i] = done[i] ? 0.0 : ((i == p) ? lp : Sw[i * n + p] * ilp);
+    __syncthreads();
+    if (tid == 0) done[p] = 1;
+    const double* lk = Lc + k * n;
+    for (int idx = tid; idx < n * n; idx += nt) {
+      const int i = idx / n, j = idx - (idx / n) * n;
+      if (!done[i] && !done[j] && i != p && j != p) Sw[idx] -= lk[i] * lk[j];
+    }
+    r = k + 1;
+    __syncthreads();
+  }
+  // (a) trace of the trailing Schur complement
+  if (tid < 32) {
+    double tr = 0.0;
+    for (int i = lane; i < n; i += 32)
+      if (!done[i]) tr += fmax(Sw[i * n + i], 0.0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(FULLMASK, tr, o);
+    if (lane == 0) amb_s = !(tr <= 1e-12);
+  }
+  __syncthreads();
+  if (amb_s) {
+    if (tid == 0) atomicOr(&A.flags[mp], 16);
+    return;
+  }
+  // G = L^T L
+  for (int idx = tid; idx < r * r; idx += nt) {
+    const int a = idx / r, b = idx - (idx / r) * r;
+    if (a > b) continue;
+    double acc = 0.0;
+    for (int i = 0; i < n; i++) acc += Lc[a * n + i] * Lc[b * n + i];
+    Gm[a * n + b] = acc;
+    Gm[b * n + a] = acc;
+  }
+  __syncthreads();
+  // G^-1 in place (Gauss-Jordan, SPD: no pivoting)
+  for (int q = 0; q < r; q++) {
+    const double ip = 1.0 / Gm[q * n + q];
+    __syncthreads();
+    for (int idx = tid; idx < r * r; idx += nt) {
+      const int i = idx / r, j = idx - (idx / r) * r;
+      if (i != q && j != q) Gm[i * n + j] -= Gm[i * n + q] * ip * Gm[q * n + j];
+    }
+    __syncthreads();
+    for (int i = tid; i < r; i += nt) {
+      if (i != q) {
+        Gm[i * n + q] = -Gm[i * n + q] * ip;
+        Gm[q * n + i] = Gm[q * n + i] * ip;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) Gm[q * n + q] = ip;
+    __syncthreads();
+  }
+  // (b) trace(G^-1)
+  if (tid < 32) {
+    double tr = 0.0;
+    for (int a = lane; a < r; a += 32) tr += Gm[a * n + a];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(FULLMASK, tr, o);
+    if (lane == 0) amb_s = !(tr > 0.0 && tr * 1e-9 * n <= 1.0);
+  }
+  __syncthreads();
+  if (amb_s) {
+    if (tid == 0) atomicOr(&A.flags[mp], 16);
+    return;
+  }
+  if (tid == 0 && r < n) atomicOr(&A.flags[mp], 4);  // rows were dependent
+  // W = L G^-1 (n x r) into Sw
+  for (int idx = tid; idx < n * r; idx += nt) {
+    const int i = idx / r, a = idx - (idx / r) * r;
+    double acc = 0.0;
+    for (int b = 0; b < r; b++) acc += Lc[b * n + i] * Gm[b * n + a];
+    Sw[i * n + a] = acc;
+  }
+  __syncthreads();
+  // S^+ = Lambda W W^T Lambda, symmetric
+  const double* ds = A.pinv_ds + (int64_t)mp * n;
+  for (int idx = tid; idx < n * n; idx += nt) {
+    const int i = idx / n, j = idx - (idx / n) * n;
+    if (i > j) continue;
+    double acc = 0.0;
+    for (int a = 0; a < r; a++) acc += Sw[i * n + a] * Sw[j * n + a];
+    const double v = acc * ds[i] * ds[j];
+    Sg[i * n + j] = v;
+    Sg[j * n + i] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // Reading R20: S^+ = Lambda S~^+ Lambda with S~ = V diag(lambda) V^T, eigenvalues
 // below 1e-11 lambda_max dropped.  One CTA per flagged window: parallel cyclic Jacobi with the
 // round-robin ordering (each round rotates nc/2 disjoint pairs at once; the row and column updates
@@ -1293,7 +1442,7 @@ __global__ void k_proj_setup_band(LevelArgs A) {
 // diagonal's (at most 40 sweeps).
 __global__ void __launch_bounds__(256) k_pinv(LevelArgs A) {
   const int mp = blockIdx.x;
-  if (!(A.flags[mp] & 2)) return;
+  if (!(A.flags[mp] & 16)) return;  // only the windows k_pinv_chol could not certify
   const int nc = A.ncon, tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
   extern __shared__ double sm[];
   double* S = sm;            // nc*nc (padded to even m)
@@ -1966,6 +2115,11 @@ cudaError_t launch_pinv(const LevelArgs& A, cudaStream_t st) {
   const size_t sm = sizeof(double) * (2 * (size_t)m * m + 128) + sizeof(int) * ((size_t)m + 128);
   cudaError_t e = cudaFuncSetAttribute(k_pinv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
+  const size_t smc = sizeof(double) * 3 * (size_t)A.ncon * A.ncon + sizeof(int) * (size_t)A.ncon;
+  e = cudaFuncSetAttribute(k_pinv_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+  if (e != cudaSuccess) return e;
+  if (getenv("MCH_PINV_JACOBI")) k_pinv_all_jacobi<<<(A.nprob_mp + 255) / 256, 256, 0, st>>>(A);  // dev A/B
+  else k_pinv_chol<<<A.nprob_mp, 256, smc, st>>>(A);
   k_pinv<<<A.nprob_mp, 256, sm, st>>>(A);
   return cudaGetLastError();
 }

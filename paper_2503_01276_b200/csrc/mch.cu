@@ -92,6 +92,7 @@ struct LevelBatch {
   int nmp = 0;
   int64_t node_off = 0, vec_off = 0, fine_off = 0;
   int max_ln = 0, max_fn = 0, th_l = 64, th_f = 64;
+  int max_comb = 0;     // fine3d combine: nodes written per macropoint (whole window if stored, else K_p box)
   std::vector<int64_t> mps, ln, lc;
   std::vector<int> lexpos;  // position of each batch macropoint in the lexicographic list of this rank
   DevBuf descs, segs, nseg;
@@ -604,6 +605,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       if (level >= 2) B->fine_off += fnn * nr;
       B->max_ln = std::max<int>(B->max_ln, (int)ln);
       B->max_fn = std::max<int>(B->max_fn, (int)fnn);
+      B->max_comb = std::max<int>(B->max_comb, P.pool_off >= 0 ? (int)fnn : V.max_kp);
       P.npar = m.npar;
       for (int t = 0; t < m.npar; t++) {
         const MacroHost& pm = pl.all[m.par_lin[t]];
@@ -875,7 +877,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       snprintf(tag, sizeof tag, "level %d variant %d", level, B.variant);
       pcg2d_phase_dump(tag);
     }
-    if (level >= 2 && B.fused3) CKC(c, launch_fine3d_combine(A, B.max_fn, st));
+    if (level >= 2 && B.fused3) CKC(c, launch_fine3d_combine(A, B.max_comb, st));
     else if (level >= 2) CKC(c, launch_combine(A, B.th_f, st));
     if (B.fused3 && A.f == nullptr && (nr == 4 || nr == 8)) CKC(c, launch_gram3_kp(A, st));
     else CKC(c, launch_gram(A, 256, st));
@@ -929,6 +931,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     for (int i = 0; i < B.nmp; i++) {
       const MacroHost& m = pl.all[B.mps[i]];
       if (B.h_flags[i] & 4) S.rank_deficient++;  // k_pinv truncated eigenvalues (reading R20)
+      if ((B.h_flags[i] & 16) && getenv("MCH_PINV_STATS_PRINT"))
+        fprintf(stderr, "[pinv] level %d macropoint %d: Jacobi eigen-solver (rank not certified by the direct form)\n", level, i);
       if ((B.h_flags[i] >> 8) && getenv("MCH_PINV_STATS_PRINT") && i < 4)
         fprintf(stderr, "[pinv] level %d macropoint %d sweeps %d\n", level, i, B.h_flags[i] >> 8);
       if (B.h_flags[i] & 8) {

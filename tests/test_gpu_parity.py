@@ -100,6 +100,37 @@ def test_rank_deficient_level():
                 assert phi_err(h.local_solution(k, r), o.solve(k)["phi"][r]) < PHI_TOL
 
 
+
+def test_pinv_paths_agree(monkeypatch):
+    """Reading R20, two ways to the pseudo-inverse of S~: the certified direct form (pivoted
+    Cholesky + G = LᵀL, `k_pinv_chol`, default) and the Jacobi eigen-solver (`k_pinv`,
+    MCH_PINV_JACOBI=1).  Both vs the oracle at every macropoint of the 2D rank-deficient level,
+    and against each other on config 5, whose 4184 level-4 windows are all rank-deficient."""
+    H = _gpu()
+    kap, ids = periodic_medium(2, 64, 4, 0.3, 1.0, 30.0)
+    o = Oracle(2, 64, 8, 3, 2, 2, kap, ids)
+    Go = o.effective_coeffs()
+    cfg = CONFIGS[5]
+    k5, i5 = make_medium(cfg)
+    res = {}
+    for name, env in (("direct", None), ("jacobi", "1")):
+        monkeypatch.delenv("MCH_PINV_JACOBI", raising=False)
+        if env:
+            monkeypatch.setenv("MCH_PINV_JACOBI", env)
+        with H(2, 64, 2, 8, 3, 2, kap, ids) as h:
+            h.solve_all()
+            assert h.level_stats(3)["rank_deficient"] > 0
+            Gg = h.effective_coeffs()
+        for i in range(Go.shape[0]):
+            assert g_err(Gg[i], Go[i]) < G_TOL, (name, i, g_err(Gg[i], Go[i]))
+        with H.from_config(cfg, k5, i5) as h:
+            h.solve_all()
+            assert h.level_stats(4)["rank_deficient"] == 4184
+            res[name] = h.effective_coeffs()
+    a, b = res["direct"], res["jacobi"]
+    scale = np.abs(b).reshape(len(b), -1).max(axis=1)
+    assert np.max(np.abs(a - b).reshape(len(b), -1).max(axis=1) / scale) < 1e-10
+
 def test_config1_full():
     """BASELINE config 1 (2D 256², 81 macropoints, L = 1): every G entry, φ at sampled points"""
     H = _gpu()
