@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <type_traits>
 
 #include "device_common.cuh"
 #include "kernels.h"
@@ -38,9 +39,9 @@ __device__ __forceinline__ int slot_f(const LevelArgs& A, const ProbDesc& P, int
 }  // namespace
 
 size_t fine3d_transport_smem(int N) {
-  // I ring 4 x 49^2, kappa ring 3 x 48^2, ids ring 3 x 48^2 (bytes), Y plane 49^2, Yx 49 x 25,
-  // level planes 2 x 25^2, constraint partials, constraint sums
-  const size_t d = 4 * kIP * kIP + 3 * kKP * kKP + kFX * kFX + kFX * 25 + 2 * 25 * 25 + (size_t)kFThreads * 3 * N + 27 * N;
+  // I ring 4 x 51^2, kappa ring 3 x 50^2, ids ring 3 x 48^2 (bytes), z-restricted accumulators
+  // 2 x 49^2, Yx 49 x 25, constraint partials, constraint sums
+  const size_t d = 4 * kIP * kIP + 3 * kKP * kKP + 2 * kFX * kFX + kFX * 25 + (size_t)kFThreads * 3 * N + 27 * N;
   return d * sizeof(double) + 3 * kFC * kFC;
 }
 
@@ -57,19 +58,19 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
   const int x = tid % kFX, strip = tid / kFX;
   const int y0 = strip * kStrip;
   const bool act = tid < kFThreads && x < nx && y0 < ny;
+  const bool full_strip = act && y0 + kStrip <= ny;  // no row of the strip outside the window
 
   extern __shared__ __align__(16) double smem[];
   double* Ir = smem;                    // [4][51*51] I_p planes (slot = plane & 3), zero halo
   double* Kr = Ir + 4 * kIP * kIP;      // [3][50*50] kappa of cell layers (slot = (layer + 3) % 3), 0 outside
-  double* Yp = Kr + 3 * kKP * kKP;      // [49*49] A_1 I_p on the current plane
-  double* Yx = Yp + kFX * kFX;          // [ny][nlx]
-  double* La = Yx + kFX * 25;           // [2][nly * nlx]
-  double* cb = La + 2 * 25 * 25;        // [kFThreads][3][N] constraint partials
+  double* Za = Kr + 3 * kKP * kKP;      // [2][49*49] A_1 I_p restricted in z to level plane Z (slot Z & 1)
+  double* Yx = Za + 2 * kFX * kFX;      // [ny][nlx]
+  double* cb = Yx + kFX * 25;           // [kFThreads][3][N] constraint partials
   double* cs = cb + kFThreads * 3 * N;  // [27][N] constraint sums
   uint8_t* Dr = reinterpret_cast<uint8_t*>(cs + 27 * N);  // [3][48*48] ids of cell layers
   for (int i = tid; i < 4 * kIP * kIP; i += blockDim.x) Ir[i] = 0.0;
   for (int i = tid; i < 3 * kKP * kKP; i += blockDim.x) Kr[i] = 0.0;
-  for (int i = tid; i < 2 * 25 * 25; i += blockDim.x) La[i] = 0.0;
+  for (int i = tid; i < 2 * kFX * kFX; i += blockDim.x) Za[i] = 0.0;
   for (int i = tid; i < 27 * N; i += blockDim.x) cs[i] = 0.0;
 
   // parents: per thread base of column (x, y0) at plane 0, and strides
@@ -95,34 +96,55 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
   }
   // global cell (x-1, y-1, z-1) of the window
   const int64_t cbase = ((int64_t)(P.lo[2] - 1) * n + (P.lo[1] - 1)) * n + (P.lo[0] - 1);
-  // stage I_p on plane p (all parents' loads of the strip in flight together)
-  auto stage_I = [&](int p) {
-    if (!act || p >= nz) return;
+  // stage I_p on plane p: all loads of a group of up to four parents in flight before the first
+  // use; the parent count is a compile-time constant per CTA (dispatch below), so no load slot is
+  // predicated off
+  auto stage_np = [&](auto npc, int p) {
+    constexpr int NP = decltype(npc)::value;
     double* dst = Ir + (p & 3) * kIP * kIP + (y0 + 1) * kIP + (x + 1);
     double v[kStrip];
 #pragma unroll
-    for (int i = 0; i < kStrip; i++) v[i] = 0.0;
-    // parents in groups of four: every load of a group in flight before the first use
+    for (int t0 = 0; t0 < NP; t0 += 4) {
+      constexpr int G0 = 4;
+      double raw[G0][kStrip];
 #pragma unroll
-    for (int t0 = 0; t0 < MCH_MAXPAR; t0 += 4) {
-      if (t0 >= npar) break;
-      double raw[4][kStrip];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < G0; u++) {
         const int t = t0 + u;
-        const double* src = pb[t] + (int64_t)p * psz[t];
+        if (t >= NP) break;
+        const double* src = pb[t] + p * psz[t];
+        if (full_strip) {
 #pragma unroll
-        for (int i = 0; i < kStrip; i++) raw[u][i] = (t < npar && y0 + i < ny) ? __ldg(src + (int64_t)i * psy[t]) : 0.0;
+          for (int i = 0; i < kStrip; i++) raw[u][i] = __ldg(src + i * psy[t]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < kStrip; i++) raw[u][i] = (y0 + i < ny) ? __ldg(src + i * psy[t]) : 0.0;
+        }
       }
 #pragma unroll
       for (int i = 0; i < kStrip; i++)
 #pragma unroll
-        for (int u = 0; u < 4; u++)
-          if (t0 + u < npar) v[i] += pw[t0 + u] * raw[u][i];
+        for (int u = 0; u < G0; u++) {
+          const int t = t0 + u;
+          if (t >= NP) break;
+          v[i] = (t == 0) ? pw[0] * raw[0][i] : v[i] + pw[t] * raw[u][i];
+        }
     }
 #pragma unroll
     for (int i = 0; i < kStrip; i++)
       if (y0 + i < ny) dst[i * kIP] = v[i];
+  };
+  auto stage_I = [&](int p) {
+    if (!act || p >= nz) return;
+    switch (npar) {
+      case 1: stage_np(std::integral_constant<int, 1>{}, p); break;
+      case 2: stage_np(std::integral_constant<int, 2>{}, p); break;
+      case 3: stage_np(std::integral_constant<int, 3>{}, p); break;
+      case 4: stage_np(std::integral_constant<int, 4>{}, p); break;
+      case 5: stage_np(std::integral_constant<int, 5>{}, p); break;
+      case 6: stage_np(std::integral_constant<int, 6>{}, p); break;
+      case 7: stage_np(std::integral_constant<int, 7>{}, p); break;
+      default: stage_np(std::integral_constant<int, 8>{}, p); break;
+    }
   };
   // kappa and ids of cell layer cz (0 / 0xFF outside the window): loads into registers first, the
   // shared-memory stores after the stencil of the current plane (latency hidden behind it)
@@ -166,6 +188,10 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
   for (int a = 0; a < 3; a++)
 #pragma unroll
     for (int j = 0; j < N; j++) acc[a][j] = 0.0;
+  // subcell slots of the cell columns and of the strips' first rows (-1: no cells), for flush()
+  __shared__ int sxs[kFX], sys[kFX / kStrip];
+  for (int u = tid; u < kFX; u += blockDim.x) sxs[u] = (u < ncx) ? slot_f(A, P, 0, u) : -1;
+  for (int u = tid; u < kFX / kStrip; u += blockDim.x) sys[u] = (u * kStrip < ncy) ? slot_f(A, P, 1, u * kStrip) : -100;
   auto flush = [&](int kz) {
     double* mine = cb + tid * 3 * N;
     if (tid < kFThreads) {
@@ -184,9 +210,9 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
       const int j = tg % N, q2 = tg / N, qy = q2 / 3, qx = q2 % 3;
       double sum = 0.0;
       for (int u = lane; u < kFThreads; u += 32) {
-        const int ux = u % kFX, ust = u / kFX, uy0 = ust * kStrip;
-        if (ux >= ncx || uy0 >= ncy || slot_f(A, P, 0, ux) != qx) continue;
-        const int a = qy - slot_f(A, P, 1, uy0);
+        const int ust = u / kFX, ux = u - ust * kFX;
+        if (sxs[ux] != qx) continue;
+        const int a = qy - sys[ust];
         if (a >= 0 && a < 3) sum += cb[(u * 3 + a) * N + j];
       }
 #pragma unroll
@@ -205,15 +231,19 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
   const double kh = A.h * (1.0 / 12.0);
   const double inv_s = 1.0 / (double)s;
   double* bvec = A.B + P.vec_off + (int64_t)r * nlx * nly * (P.nc[2] + 1);
-  for (int z = 0; z < nz; z++) {
+  int Z0 = 0, rem = 0;  // level plane below z and z's offset above it (z = Z0 s + rem)
+  for (int z = 0; z < nz; z++, rem = (rem + 1 == s) ? 0 : rem + 1, Z0 += (rem == 0) ? 1 : 0) {
     // stage plane z+2 and cell layer z+1 (slots not read in this iteration) while the stencil of
     // plane z runs: no barrier between the two
     load_K(z + 1);
     stage_I(z + 2);
+    const double wlo = 1.0 - rem * inv_s, whi = rem * inv_s;
     if (act) {
       const double* pl[3] = {Ir + ((z + 3) & 3) * kIP * kIP, Ir + (z & 3) * kIP * kIP, Ir + ((z + 1) & 3) * kIP * kIP};
       const double* kl[2] = {Kr + ((z + 2) % 3) * kKP * kKP, Kr + (z % 3) * kKP * kKP};  // layers z-1, z
       const uint8_t* dl = Dr + (z % 3) * kFC * kFC;
+      double* zlo = Za + (Z0 & 1) * kFX * kFX + x;        // level plane Z0
+      double* zhi = Za + ((Z0 + 1) & 1) * kFX * kFX + x;  // level plane Z0 + 1
       double v[3][3][3];   // [dz][dy][dx]
       double kc[2][2][2];  // [oz][oy][ox]
       auto ld_row = [&](int yy, int slot) {
@@ -242,27 +272,35 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
         if (y >= ny) break;
         ld_row(y + 1, 2);
         ld_kap(y, 1);
-        double Ap = 0.0;
+        // (A_1 I)_node = h/12 sum over the 8 cells o around the node of kappa_o (4 v_node - the
+        // node's two face-diagonal and one body-diagonal partners in o ... as 4 terms a^3, a^5, a^6,
+        // a^7 of the cell-local corner a): octant terms formed independently, summed as a tree
+        const double c4 = 4.0 * v[1][1][1];
+        double t[8];
 #pragma unroll
         for (int o = 0; o < 8; o++) {
           const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
           const int a = (~o) & 7;
           auto vb = [&](int b) { return v[oz + ((b >> 2) & 1)][oy + ((b >> 1) & 1)][ox + (b & 1)]; };
-          Ap += kc[oz][oy][ox] * (4.0 * vb(a) - vb(a ^ 3) - vb(a ^ 5) - vb(a ^ 6) - vb(a ^ 7));
+          t[o] = kc[oz][oy][ox] * ((c4 - (vb(a ^ 3) + vb(a ^ 5))) - (vb(a ^ 6) + vb(a ^ 7)));
         }
-        Yp[y * kFX + x] = Ap * kh;
+        const double Ap = (((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]))) * kh;
+        // z restriction (1D hat of level plane Z0 and Z0 + 1) into the accumulators; x and y once
+        // per completed level plane below
+        zlo[y * kFX] += wlo * Ap;
+        if (rem > 0) zhi[y * kFX] += whi * Ap;
         // cell (x, y, z): corners on planes z, z+1, rows y, y+1, columns x, x+1
         if (cl && y < ncy) {
-          const double sig = v[1][1][1] + v[1][1][2] + v[1][2][1] + v[1][2][2] + v[2][1][1] + v[2][1][2] +
-                             v[2][2][1] + v[2][2][2];
+          const double sig = ((v[1][1][1] + v[1][1][2]) + (v[1][2][1] + v[1][2][2])) +
+                             ((v[2][1][1] + v[2][1][2]) + (v[2][2][1] + v[2][2][2]));
           const int id = dl[y * kFC + x];
           const int a = (i < i1) ? 0 : ((i < i2) ? 1 : 2);
 #pragma unroll
           for (int j = 0; j < N; j++) {
-            const double t = (id == j) ? sig : 0.0;
-            if (a == 0) acc[0][j] += t;
-            else if (a == 1) acc[1][j] += t;
-            else acc[2][j] += t;
+            const double tj = (id == j) ? sig : 0.0;
+            if (a == 0) acc[0][j] += tj;
+            else if (a == 1) acc[1][j] += tj;
+            else acc[2][j] += tj;
           }
         }
 #pragma unroll
@@ -284,40 +322,38 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
       const int kz = slot_f(A, P, 2, z);
       if (z + 1 == ncz || slot_f(A, P, 2, z + 1) != kz) flush(kz);
     }
-    __syncthreads();  // Y plane complete; staged plane z+2 / layer z+1 visible from here on
-    // x restriction: Yx[y][X] = sum_d (1 - |d|/s) Y[y][X s + d]
-    for (int u = tid; u < ny * nlx; u += blockDim.x) {
-      const int y = u / nlx, X = u - y * nlx, c0 = X * s;
-      const double* row = Yp + y * kFX;
-      double a = row[c0];
-      for (int d = 1; d < s; d++) {
-        const double w = 1.0 - d * inv_s;
-        if (c0 - d >= 0) a += w * row[c0 - d];
-        if (c0 + d < nx) a += w * row[c0 + d];
+    // level plane Z0 complete: restrict it in x, then y, into b; its accumulator slot is zeroed for
+    // level plane Z0 + 2 (first written at plane (Z0 + 1) s + 1, after the barriers below)
+    if (rem == s - 1 || z == nz - 1) {
+      __syncthreads();
+      const double* zp = Za + (Z0 & 1) * kFX * kFX;
+      for (int u = tid; u < ny * nlx; u += blockDim.x) {
+        const int y = u / nlx, X = u - y * nlx, c0 = X * s;
+        const double* row = zp + y * kFX;
+        double a = row[c0];
+        for (int d = 1; d < s; d++) {
+          const double w = 1.0 - d * inv_s;
+          if (c0 - d >= 0) a += w * row[c0 - d];
+          if (c0 + d < nx) a += w * row[c0 + d];
+        }
+        Yx[y * nlx + X] = a;
       }
-      Yx[y * nlx + X] = a;
+      __syncthreads();
+      for (int u = tid; u < nly * nlx; u += blockDim.x) {
+        const int Yl = u / nlx, X = u - Yl * nlx, c0 = Yl * s;
+        double a = Yx[c0 * nlx + X];
+        for (int d = 1; d < s; d++) {
+          const double w = 1.0 - d * inv_s;
+          if (c0 - d >= 0) a += w * Yx[(c0 - d) * nlx + X];
+          if (c0 + d < ny) a += w * Yx[(c0 + d) * nlx + X];
+        }
+        bvec[((int64_t)Z0 * nly + Yl) * nlx + X] = -a;
+      }
+      double* zw = Za + (Z0 & 1) * kFX * kFX;
+      for (int u = tid; u < kFX * kFX; u += blockDim.x) zw[u] = 0.0;
     }
-    __syncthreads();
-    // y restriction and z accumulation into the level planes; complete planes go to b
-    const int Z0 = z / s, rem = z - Z0 * s;
-    for (int u = tid; u < nly * nlx; u += blockDim.x) {
-      const int Yl = u / nlx, X = u - Yl * nlx, c0 = Yl * s;
-      double a = Yx[c0 * nlx + X];
-      for (int d = 1; d < s; d++) {
-        const double w = 1.0 - d * inv_s;
-        if (c0 - d >= 0) a += w * Yx[(c0 - d) * nlx + X];
-        if (c0 + d < ny) a += w * Yx[(c0 + d) * nlx + X];
-      }
-      double* L0 = La + (Z0 & 1) * nly * nlx;
-      L0[u] += (rem == 0) ? a : (1.0 - rem * inv_s) * a;
-      if (rem > 0) La[((Z0 + 1) & 1) * nly * nlx + u] += rem * inv_s * a;
-      if (rem == s - 1 || z == nz - 1) {
-        bvec[((int64_t)Z0 * nly + Yl) * nlx + X] = -L0[u];
-        L0[u] = 0.0;
-      }
-    }
+    __syncthreads();  // staged plane z+2 / layer z+1 visible from here on
   }
-  __syncthreads();
   const double hq = 0.125 * A.h * A.h * A.h;
   for (int i = tid; i < 27 * N; i += blockDim.x) {
     const int64_t gi = ((int64_t)mp * A.ncon + i) * A.n_rhs + r;
@@ -348,7 +384,7 @@ cudaError_t launch_fine3d_transport(const LevelArgs& A, cudaStream_t st) {
 // into FK (read by k_gram for Eq. 7), and on the whole window into the parent pool if p is
 // stored (parents of later levels, or keep_all).  I_p is formed again from the parents (the
 // transport kept it on chip); per value the arithmetic is k_combine's.
-__global__ void __launch_bounds__(256) k_fine3d_combine(LevelArgs A) {
+__global__ void __launch_bounds__(256, 2) k_fine3d_combine(LevelArgs A) {
   const int mp = blockIdx.y;
   const ProbDesc& P = A.probs[mp];
   const Geo<3> gf = fine_geo<3>(P);
@@ -402,33 +438,42 @@ __global__ void __launch_bounds__(256) k_fine3d_combine(LevelArgs A) {
     wgt[a] = w;
     nid[a] = node_id<3>(gl, xc);
   }
-  int64_t pidx[MCH_MAXPAR], pn[MCH_MAXPAR];
+  // right-hand sides in chunks of eight: per parent (runtime loop, index formed in place) the
+  // loads of all eight rhs are in flight together, I accumulated in registers (one rhs at a time
+  // left the loop long-scoreboard bound); the coarse-node values (L1-resident) are read at use
+  constexpr int RC = 8;
+  for (int r0 = 0; r0 < nr; r0 += RC) {
+    double Iv[RC];
 #pragma unroll
-  for (int q = 0; q < MCH_MAXPAR; q++) {
-    pidx[q] = 0;
-    pn[q] = 0;
-    if (q >= P.npar) continue;
-    int64_t idx = 0;
-    for (int i = 2; i >= 0; i--) {
-      const int xt = P.lo[i] + xf[i] + (P.par_k[q][i] - P.k[i]) * A.c - P.par_lo[q][i];
-      idx = idx * (P.par_ncf[q][i] + 1) + xt;
+    for (int u = 0; u < RC; u++) Iv[u] = 0.0;
+    for (int q = 0; q < P.npar; q++) {
+      int64_t idx = 0;
+      for (int i = 2; i >= 0; i--) {
+        const int xt = P.lo[i] + xf[i] + (P.par_k[q][i] - P.k[i]) * A.c - P.par_lo[q][i];
+        idx = idx * (P.par_ncf[q][i] + 1) + xt;
+      }
+      const int pn = (P.par_ncf[q][0] + 1) * (P.par_ncf[q][1] + 1) * (P.par_ncf[q][2] + 1);
+      const double* src = A.pool + P.par_pool[q] + idx + (int64_t)r0 * pn;
+      const double w = P.par_w[q];
+      double pv[RC];
+#pragma unroll
+      for (int u = 0; u < RC; u++) pv[u] = (r0 + u < nr) ? __ldg(src + (int64_t)u * pn) : 0.0;
+#pragma unroll
+      for (int u = 0; u < RC; u++) Iv[u] += w * pv[u];
     }
-    pidx[q] = idx;
-    pn[q] = (int64_t)(P.par_ncf[q][0] + 1) * (P.par_ncf[q][1] + 1) * (P.par_ncf[q][2] + 1);
-  }
-  for (int r = 0; r < nr; r++) {
-    double I = 0.0;
 #pragma unroll
-    for (int q = 0; q < MCH_MAXPAR; q++)
-      if (q < P.npar) I += P.par_w[q] * __ldg(A.pool + P.par_pool[q] + (int64_t)r * pn[q] + pidx[q]);
-    const double* xi = A.X + P.vec_off + (int64_t)r * nnl;
-    double v = 0.0;
+    for (int u = 0; u < RC; u++) {
+      const int r = r0 + u;
+      if (r >= nr) break;
+      const double* xi = A.X + P.vec_off + (int64_t)r * nnl;
+      double v = 0.0;
 #pragma unroll
-    for (int a = 0; a < 8; a++)
-      if (wgt[a] != 0.0) v += wgt[a] * xi[nid[a]];
-    const double phi = I + v;
-    if (kk >= 0) A.FK[((int64_t)mp * nr + r) * A.nkp_max + kk] = phi;
-    if (full) A.pool[P.pool_off + (int64_t)r * nnf + kf] = phi;
+      for (int a = 0; a < 8; a++)
+        if (wgt[a] != 0.0) v += wgt[a] * xi[nid[a]];
+      const double phi = Iv[u] + v;
+      if (kk >= 0) A.FK[((int64_t)mp * nr + r) * A.nkp_max + kk] = phi;
+      if (full) A.pool[P.pool_off + (int64_t)r * nnf + kf] = phi;
+    }
   }
 }
 

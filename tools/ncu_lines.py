@@ -3,8 +3,12 @@ import collections, csv, io, subprocess, sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".csv.gz"):  # an exported source page (ncu -i ... --page source --csv | gzip)
+    import gzip
+    src = gzip.open(rep, "rt").read()
+else:
+    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
 cur = None
 per_i, per_s, text, ops = collections.Counter(), collections.Counter(), {}, collections.Counter()
 for r in csv.reader(io.StringIO(src)):
