@@ -1173,11 +1173,10 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
   int* ns_s = rs_s + NQ + 1;                              // [nn + 1] node starts
   int* ri_s = ns_s + kW7NN + 1;                           // [EC] padded p index of a row entry
   int* nr_s = ri_s + EC;                                  // [EC] constraint row of a node entry
+  int* pm_s = nr_s + EC;                                  // [nn] node of slot s (slots sorted by entry count)
 
   {
     const double* S27 = A.STC + P.node_off * 27;
-    for (int i = threadIdx.x; i < 27 * nn; i += blockDim.x) st_s[i] = __ldg(S27 + i);
-    for (int i = threadIdx.x; i < nn; i += blockDim.x) dg_s[i] = __ldg(A.dinv + P.node_off + i);
     const double* Si = A.Sinv + (int64_t)mp * NQ * NQ;
     for (int i = threadIdx.x; i < NQ * NQ; i += blockDim.x) {
       const int r = i / NQ, c = i - r * NQ;
@@ -1212,15 +1211,40 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
     // c = C u, per node its (row, weight) entries for C^T yhat (octant-merged weights of k_node_ops3d)
     const double* MW = A.MLR + P.node_off * 8 * N;
     auto rng_n = [&](int r) { return max(0, (r >> 8) - (r & 255) + 1); };
+    // entries per node (N x the subcells around it: 1 to 8); nodes are dealt to the lanes in slots
+    // sorted by that count (s = lane + 32 i, node pm_s[s]), so the 32 lanes of a slot walk lists of
+    // (nearly) equal length in C^T yhat: in node order a warp's 32 nodes mixed 2- to 16-entry lists
+    // and every lane waited for the longest (the loop was over half of the kernel's instructions)
+    int* cnt_s = nr_s;  // temporary, overwritten by the node entries below
     for (int k = threadIdx.x; k < nn; k += blockDim.x) {
       const int z = k / (nx * ny), t = k - z * nx * ny, y = t / nx, x = t - y * nx;
       const int px = __popc(sd_s[x] & 3), py = __popc(sd_s[kW7 + y] & 3), pz = __popc(sd_s[2 * kW7 + z] & 3);
-      ns_s[k + 1] = N * px * py * pz;
+      cnt_s[k] = px * py * pz;
     }
     if (threadIdx.x < NQ) {
       const int q = threadIdx.x / N, qz = q / 9, qy = (q / 3) % 3, qx = q % 3;
       rs_s[threadIdx.x + 1] = rng_n(rg_s[qx]) * rng_n(rg_s[3 + qy]) * rng_n(rg_s[6 + qz]);
     }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // stable counting sort by ballots, classes 1, 2, 4, 8 subcells
+      int pos = 0;
+      for (int cls = 1; cls <= 8; cls <<= 1)
+        for (int k0 = 0; k0 < nn; k0 += 32) {
+          const int k = k0 + lane;
+          const bool hit = k < nn && cnt_s[k] == cls;
+          const unsigned b = __ballot_sync(FULLMASK, hit);
+          if (hit) pm_s[pos + __popc(b & ((1u << lane) - 1u))] = k;
+          pos += __popc(b);
+        }
+    }
+    __syncthreads();
+    for (int sl = threadIdx.x; sl < nn; sl += blockDim.x) ns_s[sl + 1] = N * cnt_s[pm_s[sl]];
+    // stencil rows and D^-1 in slot order (lane-contiguous reads in the solve)
+    for (int i = threadIdx.x; i < 27 * nn; i += blockDim.x) {
+      const int c = i / nn, sl = i - c * nn;
+      st_s[i] = __ldg(S27 + c * nn + pm_s[sl]);
+    }
+    for (int sl = threadIdx.x; sl < nn; sl += blockDim.x) dg_s[sl] = __ldg(A.dinv + P.node_off + pm_s[sl]);
     __syncthreads();
     if (threadIdx.x == 0) {
       ns_s[0] = 0;
@@ -1231,10 +1255,11 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
     }
     __syncthreads();
     if (ns_s[nn] > EC || rs_s[NQ] > EC) __trap();  // >= 2 level cells per subcell (reading R22) bounds both
-    for (int k = threadIdx.x; k < nn; k += blockDim.x) {
+    for (int sl = threadIdx.x; sl < nn; sl += blockDim.x) {
+      const int k = pm_s[sl];
       const int z = k / (nx * ny), t = k - z * nx * ny, y = t / nx, x = t - y * nx;
       const int sx = sd_s[x], sy = sd_s[kW7 + y], sz = sd_s[2 * kW7 + z];
-      int e = ns_s[k];
+      int e = ns_s[sl];
       for (int zs = 0; zs < 2; zs++) {
         if (!((sz >> zs) & 1)) continue;
         const int kz = (sz >> (4 + 4 * zs)) & 15;
@@ -1281,19 +1306,17 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
   double* c_s = c_all + rhs * NQ;
   double* y_s = y_all + rhs * NQ;
 
-  // owned nodes: k = lane + 32 i
+  // owned nodes: slot lane + 32 i, node pm_s[slot]
   int pix[kW7KPL];  // padded index of the node, -1 if absent
-  int nxy[kW7KPL];  // x | y << 4 | z << 8
 #pragma unroll
   for (int i = 0; i < kW7KPL; i++) {
-    const int k = lane + 32 * i;
-    if (k < nn) {
+    const int sl = lane + 32 * i;
+    if (sl < nn) {
+      const int k = pm_s[sl];
       const int z = k / (nx * ny), t = k - z * nx * ny, y = t / nx, x = t - y * nx;
       pix[i] = ((z + 1) * kW7P + (y + 1)) * kW7P + (x + 1);
-      nxy[i] = x | (y << 4) | (z << 8);
     } else {
       pix[i] = -1;
-      nxy[i] = 0;
     }
   }
   auto wsum = [](double v) {
@@ -1305,6 +1328,7 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
   auto ct_at = [&](int i) -> double {
     const int k = lane + 32 * i;
     double ct = 0.0;
+#pragma unroll 2
     for (int e = ns_s[k], e1 = ns_s[k + 1]; e < e1; e++) ct += nw_s[e] * y_s[nr_s[e]];
     return ct;
   };
@@ -1333,7 +1357,7 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
   auto apply = [&](int i) -> double {
     const int k = lane + 32 * i;
     const double* pb = p_s + pix[i];
-    double a = 0.0;
+    double a[3] = {0.0, 0.0, 0.0};  // one chain per plane dz (three independent FMA chains)
 #pragma unroll
     for (int dz = -1; dz <= 1; dz++)
 #pragma unroll
@@ -1341,9 +1365,9 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
 #pragma unroll
         for (int dx = -1; dx <= 1; dx++) {
           const int c = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
-          a += st_s[c * nn + k] * pb[(dz * kW7P + dy) * kW7P + dx];
+          a[dz + 1] += st_s[c * nn + k] * pb[(dz * kW7P + dy) * kW7P + dx];
         }
-    return a;
+    return (a[0] + a[1]) + a[2];
   };
 
   double xr[kW7KPL], rr_[kW7KPL], pr[kW7KPL], qr[kW7KPL];
@@ -1366,7 +1390,7 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
     double rr = 0.0;
 #pragma unroll
     for (int i = 0; i < kW7KPL; i++)
-      if (pix[i] >= 0) rr_[i] = apply(i) - (bb ? bb[lane + 32 * i] : 0.0);
+      if (pix[i] >= 0) rr_[i] = apply(i) - (bb ? bb[pm_s[lane + 32 * i]] : 0.0);
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < kW7KPL; i++)
@@ -1462,7 +1486,7 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
   double* Xv = A.X + P.vec_off + (int64_t)rhs * nn;
 #pragma unroll
   for (int i = 0; i < kW7KPL; i++)
-    if (pix[i] >= 0) Xv[lane + 32 * i] = xr[i] + dg_s[lane + 32 * i] * ct_at(i);
+    if (pix[i] >= 0) Xv[pm_s[lane + 32 * i]] = xr[i] + dg_s[lane + 32 * i] * ct_at(i);
   if (lane == 0) {
     const int prob = mp * A.n_rhs + rhs;
     A.iters[prob] = it;
@@ -1479,7 +1503,7 @@ size_t pcg3d_w7_smem(int N) {
   const size_t NQ = 27 * (size_t)N, NR = 4 * (size_t)N;
   const size_t EC = 729 * (size_t)N;
   const size_t d = 27 * kW7NN + 2 * EC + kW7NN + NQ * NQ + NR * kW7P * kW7P * kW7P + 2 * NR * NQ;
-  return d * sizeof(double) + (3 * kW7 + 9 + NQ + 1 + kW7NN + 1 + 2 * EC) * sizeof(int);
+  return d * sizeof(double) + (3 * kW7 + 9 + NQ + 1 + kW7NN + 1 + 2 * EC + kW7NN) * sizeof(int);
 }
 
 cudaError_t launch_pcg3d_w7(const LevelArgs& A, cudaStream_t st) {
