@@ -280,6 +280,12 @@ def _per_level(cfg, levels, world, peaks_hbm, fp64_tf):
                     "pcg_bound": bound, "pcg_achieved": round(ach, 3), "pcg_unit": unit,
                     "pcg_frac": (round(frac, 4) if frac is not None else None),
                     "rank_deficient": st["rank_deficient"], "launches": st["launches"]})
+        tms = avg("ms_transport")
+        if lev >= 2 and tms > 0:  # the transport launch (Eqs. 11-13), FP64 / issue bound
+            tach = avg("transport_flops") / (tms * 1e-3) / 1e12
+            out[-1].update({"transport_ms": round(tms, 3), "transport_units": st["transport_units"],
+                            "transport_achieved": round(tach, 3), "transport_unit": "TFLOP/s",
+                            "transport_frac": (round(tach / fp64_tf, 4) if fp64_tf else None)})
     return out
 
 
@@ -334,8 +340,9 @@ def main():
     pk, pk_src = _peaks()
     fp64_tf = dev_peaks.get("fp64_tflops") if isinstance(dev_peaks, dict) else None
     per_level = _per_level(cfg, levels, world, pk["hbm_gbs"], fp64_tf)
-    # dominant kernel: the PCG launch of the level with the largest PCG device time
+    # dominant kernel: the longest single launch of the step, a level's PCG or its transport
     dom = max(per_level, key=lambda r: r["pcg_ms"])
+    domt = max(per_level, key=lambda r: r.get("transport_ms", 0.0))
     lev = dom["level"]
     kname = ("k_pcg2d" if cfg.d == 2 else ("k_pcg3d_l1" if lev == 1 else ("k_pcg3d_w7" if lev == cfg.L and cfg.L >= 4
                                                                           else "k_pcg3d"))) + f" level-{lev} launch"
@@ -359,6 +366,22 @@ def main():
                 "frac": dom["pcg_frac"], "traffic": traffic, "launch_ms": dom["pcg_ms"],
                 "peak_source": "measured FP64 FMA loop (lib/mch_peaks)",
                 "algorithmic_flops": "node-iterations x (2 x stencil coefficients + 14)"}
+    if domt.get("transport_ms", 0.0) > dom["pcg_ms"]:
+        lt = domt["level"]
+        ttraffic = None
+        if os.path.exists(prof):
+            try:
+                ttraffic = json.load(open(prof)).get(cfg.name, {}).get(f"dram_bytes_transport_L{lt}_launch")
+            except Exception:
+                ttraffic = None
+        roof = {"kernel": f"k_fine3d_transport level-{lt} launch" if cfg.d == 3 else f"transport level-{lt} launch",
+                "bound": "alu", "achieved": domt["transport_achieved"], "peak": fp64_tf, "unit": "TFLOP/s",
+                "frac": domt["transport_frac"], "traffic": ttraffic, "launch_ms": domt["transport_ms"],
+                "peak_source": "measured FP64 FMA loop (lib/mch_peaks)",
+                "algorithmic_flops": "fine window nodes x rhs x (2 npar + 60): I_p from the parents, the "
+                                     "kappa-weighted Q1 rows of A_1 I_p, z restriction, constraint sums (DESIGN.md §6)",
+                "pcg_dominant": {"kernel": kname, "bound": roof["bound"], "frac": roof["frac"],
+                                 "launch_ms": roof["launch_ms"], "traffic": roof["traffic"]}}
     # P10: the paper's cost model: hierarchical solver DOFs / plain-method DOFs
     # vs the model L eta^((1-L) d)
     uk = torch.tensor([float(s["unknowns_level"]) for s in levels[-1]], dtype=torch.float64, device="cuda")

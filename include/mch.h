@@ -119,6 +119,10 @@ typedef struct {
   double   bytes_comm;     /* bytes this rank sent + received in that exchange */
   double   node_iters;     /* sum over problems of level-n window nodes x PCG iterations (the
                               solver work of the paper's cost model) */
+  double   ms_transport;   /* device time of the transport (Eqs. 11-13: I_p, b, g), part of ms_setup */
+  double   transport_units;/* fine window nodes x right-hand sides the transport processed */
+  double   transport_flops;/* its algorithmic FP64 flops: per unit 2 npar (I_p) + 60 (the kappa-
+                              weighted Q1 rows, z restriction, constraint sums) */
 } mch_level_stats;
 
 /* Algorithm 1 REQUIRE (macropoint set T, coarsening factor eta, fine mesh h,

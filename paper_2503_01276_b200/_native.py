@@ -62,7 +62,9 @@ class MchLevelStats(ctypes.Structure):
                 ("ms_pcg", ctypes.c_double), ("ms_setup", ctypes.c_double),
                 ("ms_gram", ctypes.c_double), ("pcg_bytes", ctypes.c_double),
                 ("launches", ctypes.c_int64), ("rank_deficient", ctypes.c_int64),
-                ("ms_comm", ctypes.c_double), ("bytes_comm", ctypes.c_double), ("node_iters", ctypes.c_double)]
+                ("ms_comm", ctypes.c_double), ("bytes_comm", ctypes.c_double), ("node_iters", ctypes.c_double),
+                ("ms_transport", ctypes.c_double), ("transport_units", ctypes.c_double),
+                ("transport_flops", ctypes.c_double)]
 
 
 class MchError(RuntimeError):

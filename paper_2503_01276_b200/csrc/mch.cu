@@ -112,7 +112,8 @@ struct LevelBatch {
   int* h_iters = nullptr;
   double* h_relres = nullptr;
   double* h_diag = nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // 4, 5: around the transport
+  double tr_units = 0, tr_flops = 0;  // fine window nodes x rhs of the transport, its algorithmic flops
   ~LevelBatch() {
     descs.release();
     segs.release();
@@ -606,6 +607,10 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       B->max_ln = std::max<int>(B->max_ln, (int)ln);
       B->max_fn = std::max<int>(B->max_fn, (int)fnn);
       B->max_comb = std::max<int>(B->max_comb, P.pool_off >= 0 ? (int)fnn : V.max_kp);
+      if (level >= 2) {  // transport work: per fine node and rhs 2 npar (I_p) + 60
+        B->tr_units += (double)fnn * nr;
+        B->tr_flops += (double)fnn * nr * (2.0 * m.npar + 60.0);
+      }
       P.npar = m.npar;
       for (int t = 0; t < m.npar; t++) {
         const MacroHost& pm = pl.all[m.par_lin[t]];
@@ -704,8 +709,10 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
       }
     }
     if (B->on3d && level >= 2) {
-      CKC(c, c->STC.ensure(sizeof(double) * 27 * B->node_off));
-      CKC(c, c->MLR.ensure(sizeof(double) * 8 * N * B->node_off));
+      const int64_t pad = B->w7 ? 0 : (int64_t)B->nxm3 * B->nxm3 * B->nxm3;
+      const int64_t nodes = std::max<int64_t>(B->node_off, pad * nmp);
+      CKC(c, c->STC.ensure(sizeof(double) * 27 * nodes));
+      CKC(c, c->MLR.ensure(sizeof(double) * 8 * N * nodes));
     }
     CKC(c, cudaMallocHost(&B->h_flags, sizeof(int) * nmp));
     CKC(c, cudaMallocHost(&B->h_iters, sizeof(int) * nmp * nr));
@@ -792,6 +799,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     CKC(c, launch_targets(A, st));
     A.FK = B.fused3 ? c->FK.as<double>() : nullptr;
     A.nkp_max = B.max_kp;
+    A.stc_pad = (B.on3d && level >= 2 && !B.w7) ? B.nxm3 * B.nxm3 * B.nxm3 : 0;
+    cudaEventRecord(B.ev[4], st);
     if (level >= 2 && B.fused3) {  // 3D: I_p, A_1 I_p, C_1 I_p and P_n^T in one pass (fine3d.cu)
       CKC(c, launch_fine3d_transport(A, st));
     } else if (level >= 2 && B.tsplit) {  // 3D: I_p, then the column-walking apply, then P_n^T
@@ -805,6 +814,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     } else if (level >= 2) {
       CKC(c, launch_transport(A, B.th_f, st));
     }
+    cudaEventRecord(B.ev[5], st);
     A.coarse = B.coarse ? 1 : 0;
     A.ncmax = kCoarseMax;
     A.cmap = c->cmap.as<int>(); A.ncomp = c->ncomp.as<int>(); A.cbox = c->cbox.as<int>();
@@ -920,7 +930,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     cudaEventElapsedTime(&tc, c->ev[4], c->ev[5]);
     S.ms_comm = tc;
   }
-  float ms_setup = 0, ms_pcg = 0, ms_gram = 0;
+  float ms_setup = 0, ms_pcg = 0, ms_gram = 0, ms_tr = 0;
   for (size_t bi = 0; bi < batches.size(); bi++) {
     LevelBatch& B = *batches[bi];
     float t1 = 0, t2 = 0, t3 = 0;
@@ -928,6 +938,11 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     cudaEventElapsedTime(&t2, B.ev[1], B.ev[2]);
     cudaEventElapsedTime(&t3, B.ev[2], B.ev[3]);
     ms_setup += t1; ms_pcg += t2; ms_gram += t3;
+    float t4 = 0;
+    cudaEventElapsedTime(&t4, B.ev[4], B.ev[5]);
+    ms_tr += t4;
+    S.transport_units += B.tr_units;
+    S.transport_flops += B.tr_flops;
     for (int i = 0; i < B.nmp; i++) {
       const MacroHost& m = pl.all[B.mps[i]];
       if (B.h_flags[i] & 4) S.rank_deficient++;  // k_pinv truncated eigenvalues (reading R20)
@@ -984,6 +999,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
   S.ms_setup = ms_setup;
   S.ms_pcg = ms_pcg;
   S.ms_gram = ms_gram;
+  S.ms_transport = ms_tr;
   c->solved = level;
   return MCH_OK;
 }

@@ -756,8 +756,9 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
   };
   __syncthreads();
 
-  const double* S27 = A.STC + P.node_off * 27;
-  const double* MW = A.MLR + P.node_off * 8 * N;
+  constexpr int PAD = NXM * NXM * NXM;  // fixed node stride of STC / MLR (A.stc_pad): offsets c PAD are immediates
+  const double* S27 = A.STC + (int64_t)mp * 27 * PAD;
+  const double* MW = A.MLR + (int64_t)mp * 8 * N * PAD;
   const double* dg = A.dinv + P.node_off;
   double* Xv = A.X + P.vec_off + (int64_t)rhs * nn;
   double* Rv = A.R + P.vec_off + (int64_t)rhs * nn;
@@ -795,7 +796,7 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
           const int o = xs + 2 * ys + 4 * zs;
           const double* yq = Ysh + ((kz * 3 + ky) * 3 + kx) * N;
 #pragma unroll
-          for (int j = 0; j < N; j++) ct += __ldg(MW + (int64_t)(o * N + j) * nn + k) * yq[j];
+          for (int j = 0; j < N; j++) ct += __ldg(MW + (o * N + j) * PAD + k) * yq[j];
         }
       }
     }
@@ -821,7 +822,7 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
         if (!((sx.pm >> xs) & 1)) continue;
         const int o = xs + 2 * ys + 4 * zs;
 #pragma unroll
-        for (int j = 0; j < N; j++) acc[ys][xs][j] += __ldg(MW + (int64_t)(o * N + j) * nn + k) * u;
+        for (int j = 0; j < N; j++) acc[ys][xs][j] += __ldg(MW + (o * N + j) * PAD + k) * u;
       }
     }
   };
@@ -904,7 +905,7 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
       const int k = nidx(z);
       double cf[27];  // all 27 coefficient loads in flight before the first use
 #pragma unroll
-      for (int c = 0; c < 27; c++) cf[c] = lact ? __ldg(S27 + (int64_t)c * nn + k) : 0.0;
+      for (int c = 0; c < 27; c++) cf[c] = lact ? __ldg(S27 + c * PAD + k) : 0.0;
       double Ap = 0.0;
 #pragma unroll
       for (int dz = 0; dz < 3; dz++)
