@@ -73,26 +73,23 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
   for (int i = tid; i < 2 * kFX * kFX; i += blockDim.x) Za[i] = 0.0;
   for (int i = tid; i < 27 * N; i += blockDim.x) cs[i] = 0.0;
 
-  // parents: per thread base of column (x, y0) at plane 0, and strides
+  // parents: per CTA table in shared memory (window origin's element in parent t at plane 0, row and
+  // plane strides, weight); a thread adds its column offset y0 px + x at use (kept out of registers:
+  // eight 64-bit bases, strides and weights per thread cost ~48 registers)
   const int npar = P.npar;
-  const double* pb[MCH_MAXPAR];
-  int psy[MCH_MAXPAR], psz[MCH_MAXPAR];
-  double pw[MCH_MAXPAR];
-#pragma unroll
-  for (int t = 0; t < MCH_MAXPAR; t++) {
-    pb[t] = A.pool;
-    psy[t] = psz[t] = 0;
-    pw[t] = 0.0;
-    if (t < npar) {
-      const int px = P.par_ncf[t][0] + 1, py = P.par_ncf[t][1] + 1, pz = P.par_ncf[t][2] + 1;
-      const int xt = P.lo[0] + x + (P.par_k[t][0] - P.k[0]) * A.c - P.par_lo[t][0];
-      const int yt = P.lo[1] + y0 + (P.par_k[t][1] - P.k[1]) * A.c - P.par_lo[t][1];
-      const int zt = P.lo[2] + (P.par_k[t][2] - P.k[2]) * A.c - P.par_lo[t][2];
-      psy[t] = px;
-      psz[t] = px * py;
-      pb[t] = A.pool + P.par_pool[t] + (int64_t)r * px * py * pz + ((int64_t)zt * py + yt) * px + xt;
-      pw[t] = P.par_w[t];
-    }
+  __shared__ long long pbs[MCH_MAXPAR];
+  __shared__ int pxs[MCH_MAXPAR], pxys[MCH_MAXPAR];
+  __shared__ double pws[MCH_MAXPAR];
+  if (tid < npar) {
+    const int t = tid;
+    const int px = P.par_ncf[t][0] + 1, py = P.par_ncf[t][1] + 1, pz = P.par_ncf[t][2] + 1;
+    const int xt = P.lo[0] + (P.par_k[t][0] - P.k[0]) * A.c - P.par_lo[t][0];
+    const int yt = P.lo[1] + (P.par_k[t][1] - P.k[1]) * A.c - P.par_lo[t][1];
+    const int zt = P.lo[2] + (P.par_k[t][2] - P.k[2]) * A.c - P.par_lo[t][2];
+    pxs[t] = px;
+    pxys[t] = px * py;
+    pbs[t] = P.par_pool[t] + (int64_t)r * px * py * pz + ((int64_t)zt * py + yt) * px + xt;
+    pws[t] = P.par_w[t];
   }
   // global cell (x-1, y-1, z-1) of the window
   const int64_t cbase = ((int64_t)(P.lo[2] - 1) * n + (P.lo[1] - 1)) * n + (P.lo[0] - 1);
@@ -111,13 +108,14 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
       for (int u = 0; u < G0; u++) {
         const int t = t0 + u;
         if (t >= NP) break;
-        const double* src = pb[t] + p * psz[t];
+        const int px = pxs[t];
+        const double* src = A.pool + pbs[t] + (p * pxys[t] + y0 * px + x);
         if (full_strip) {
 #pragma unroll
-          for (int i = 0; i < kStrip; i++) raw[u][i] = __ldg(src + i * psy[t]);
+          for (int i = 0; i < kStrip; i++) raw[u][i] = __ldg(src + i * px);
         } else {
 #pragma unroll
-          for (int i = 0; i < kStrip; i++) raw[u][i] = (y0 + i < ny) ? __ldg(src + i * psy[t]) : 0.0;
+          for (int i = 0; i < kStrip; i++) raw[u][i] = (y0 + i < ny) ? __ldg(src + i * px) : 0.0;
         }
       }
 #pragma unroll
@@ -126,7 +124,7 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
         for (int u = 0; u < G0; u++) {
           const int t = t0 + u;
           if (t >= NP) break;
-          v[i] = (t == 0) ? pw[0] * raw[0][i] : v[i] + pw[t] * raw[u][i];
+          v[i] = (t == 0) ? pws[0] * raw[0][i] : v[i] + pws[t] * raw[u][i];
         }
     }
 #pragma unroll
@@ -246,6 +244,9 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
       double* zhi = Za + ((Z0 + 1) & 1) * kFX * kFX + x;  // level plane Z0 + 1
       double v[3][3][3];   // [dz][dy][dx]
       double kc[2][2][2];  // [oz][oy][ox]
+      double apr[kStrip];  // A_1 I_p of the strip's nodes: the z-restriction read-modify-writes of the
+                           // shared accumulators after the row loop, so no shared store sits between
+                           // the rows' shared loads (the compiler cannot prove they do not alias)
       auto ld_row = [&](int yy, int slot) {
 #pragma unroll
         for (int dz = 0; dz < 3; dz++)
@@ -285,10 +286,7 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
           t[o] = kc[oz][oy][ox] * ((c4 - (vb(a ^ 3) + vb(a ^ 5))) - (vb(a ^ 6) + vb(a ^ 7)));
         }
         const double Ap = (((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]))) * kh;
-        // z restriction (1D hat of level plane Z0 and Z0 + 1) into the accumulators; x and y once
-        // per completed level plane below
-        zlo[y * kFX] += wlo * Ap;
-        if (rem > 0) zhi[y * kFX] += whi * Ap;
+        apr[i] = Ap;
         // cell (x, y, z): corners on planes z, z+1, rows y, y+1, columns x, x+1
         if (cl && y < ncy) {
           const double sig = ((v[1][1][1] + v[1][1][2]) + (v[1][2][1] + v[1][2][2])) +
@@ -314,6 +312,15 @@ __global__ void __launch_bounds__(kFBlock, 1) k_fine3d_transport(LevelArgs A) {
         for (int oz = 0; oz < 2; oz++)
 #pragma unroll
           for (int ox = 0; ox < 2; ox++) kc[oz][0][ox] = kc[oz][1][ox];
+      }
+      // z restriction (1D hat of level plane Z0 and Z0 + 1) into the accumulators; x and y once per
+      // completed level plane below
+#pragma unroll
+      for (int i = 0; i < kStrip; i++) {
+        const int y = y0 + i;
+        if (y >= ny) break;
+        zlo[y * kFX] += wlo * apr[i];
+        if (rem > 0) zhi[y * kFX] += whi * apr[i];
       }
     }
     store_K(z + 1);
