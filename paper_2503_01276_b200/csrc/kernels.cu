@@ -110,10 +110,14 @@ __global__ void k_targets(LevelArgs A) {
     double v[16];
     for (int i = 0; i < 16; i++) v[i] = 0.0;
     if (present) {
-      const int64_t cnt = (int64_t)ext[0] * ext[1] * ext[2];
-      for (int64_t idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
-        const int f[3] = {lo[0] + (int)(idx % ext[0]), lo[1] + (int)((idx / ext[0]) % ext[1]),
-                          lo[2] + (int)(idx / ((int64_t)ext[0] * ext[1]))};
+      // plane by plane (z), threads over the plane's cells: 32-bit index arithmetic with the
+      // float-reciprocal division of fdiv (exact below 2^22; r02 divided 64-bit per cell)
+      const int pc = ext[0] * ext[1];
+      const float inv0 = 1.0f / (float)ext[0];
+      for (int zz = 0; zz < ext[2]; zz++)
+      for (int t = threadIdx.x; t < pc; t += blockDim.x) {
+        const int yy = fdiv(t, inv0);
+        const int f[3] = {lo[0] + t - yy * ext[0], lo[1] + yy, lo[2] + zz};
         int64_t fi = 0;
         for (int i = D - 1; i >= 0; i--) fi = fi * A.n + f[i];
         const int id = A.ids[fi];
