@@ -1150,7 +1150,7 @@ constexpr int kW7P = kW7 + 2;               // padded p pitch
 constexpr int kW7NN = kW7 * kW7 * kW7;      // 343
 constexpr int kW7KPL = (kW7NN + 31) / 32;   // nodes per lane (11)
 
-template <int N>
+template <int N, bool LOCK>
 __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
   constexpr int NR = 4 * N;   // right-hand sides = warps
   constexpr int NQ = 27 * N;  // constraint rows
@@ -1167,10 +1167,11 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
   double* nw_s = rw_s + EC;             // [EC] node-major constraint entries: weight
   double* dg_s = nw_s + EC;             // [nn] D^-1
   double* si_s = dg_s + kW7NN;          // [NQ][NQ] S^+ transposed: si_s[j*NQ + i] = S^+_ij
-  double* p_all = si_s + NQ * NQ;       // [NR][PP] p with zero halo (also D^-1 r / x for C u)
-  double* c_all = p_all + NR * PP;      // [NR][NQ]
-  double* y_all = c_all + NR * NQ;      // [NR][NQ]
-  int* sd_s = reinterpret_cast<int*>(y_all + NR * NQ);  // [3][7] sides packed pm | k0 << 4 | k1 << 8
+  double* p_all = si_s + ((NQ * NQ + 1) & ~1);  // [NR][PP] p with zero halo (also D^-1 r / x for C u);
+                                        // 16-byte aligned (double2 accesses of the lockstep form)
+  double* c_all = p_all + (NR + 2) * PP;  // [NR][NQ] (lockstep form: [NQ][NR + 2], p_all [PP][NR + 2])
+  double* y_all = c_all + (NR + 2) * NQ;  // as c_all
+  int* sd_s = reinterpret_cast<int*>(y_all + (NR + 2) * NQ);  // [3][7] sides packed pm | k0 << 4 | k1 << 8
   int* rg_s = sd_s + 3 * kW7;                             // [3][3] node range of subcell coordinate: lo | hi << 8
   int* rs_s = rg_s + 9;                                   // [NQ + 1] row starts
   int* ns_s = rs_s + NQ + 1;                              // [nn + 1] node starts
@@ -1185,7 +1186,7 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
       const int r = i / NQ, c = i - r * NQ;
       si_s[c * NQ + r] = __ldg(Si + i);
     }
-    for (int i = threadIdx.x; i < NR * PP; i += blockDim.x) p_all[i] = 0.0;
+    for (int i = threadIdx.x; i < (NR + 2) * PP; i += blockDim.x) p_all[i] = 0.0;  // zero halo (either layout)
     if (threadIdx.x < 3 * kW7) {
       const int d = threadIdx.x / kW7, X = threadIdx.x - d * kW7;
       const int ncd = P.nc[d];
@@ -1304,6 +1305,371 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
       }
     }
     __syncthreads();
+  }
+  if constexpr (LOCK) {
+    // ---- lockstep form: the n_rhs = 4N right-hand sides iterate together.  A task is (node slot s,
+    // half h of four right-hand sides); thread t owns tasks t + 128N i (i < 3), all of half t & 1, and
+    // keeps x, r, p, q of its tasks' four right-hand sides in registers.  The vectors the operator
+    // reads are interleaved by rhs in shared memory (p_all[padded node][NR], c_all / y_all[row][NR]),
+    // so each stencil coefficient, constraint weight and S^+ entry is read once for four right-hand
+    // sides (the warp-per-rhs form re-read them per rhs and was shared-memory bound).  Per-rhs
+    // scalars come from fixed-order block reductions; a right-hand side that meets its stopping
+    // test is frozen (x, r, p no longer updated) while the others continue, so every rhs takes
+    // the same iterates as in the per-rhs form (up to the reduction order).
+    constexpr int HV = NR / 4;        // halves
+    constexpr int NRP = NR + 2;       // padded node / row stride of the interleaved vectors: 80 B for
+                                      // NR = 8 spreads the scattered slots' 16-byte loads over the banks
+                                      // (a 64 B stride put every other slot on the same 16 banks)
+    constexpr int TPT = 3;            // HV * nn <= 3 * 128 N for nn <= 343
+    const int tid = threadIdx.x, nt = blockDim.x, nwp = nt >> 5;
+    const int h = (HV == 2) ? (tid & 1) : 0, r0 = 4 * h;
+    __shared__ double redw[4 * N][2 * NR];
+    __shared__ double tot_s[2 * NR];
+    __shared__ double sc_alpha[NR], sc_beta[NR], sc_rz[NR], sc_ref[NR], sc_fl[NR], sc_rzref[NR];
+    __shared__ int sc_act[NR], sc_it[NR], sc_bd[NR], sc_any;
+    int tpx[TPT], tsl[TPT];  // padded p index (-1: no task) and slot of each task
+#pragma unroll
+    for (int i = 0; i < TPT; i++) {
+      const int tau = tid + nt * i, sl = tau / HV;
+      tsl[i] = sl;
+      tpx[i] = -1;
+      if (sl < nn) {
+        const int k = pm_s[sl];
+        const int z = k / (nx * ny), t = k - z * nx * ny, y = t / nx, x = t - y * nx;
+        tpx[i] = ((z + 1) * kW7P + (y + 1)) * kW7P + (x + 1);
+      }
+    }
+    auto ld4 = [](const double* a, double (&v)[4]) {
+      const double2 u0 = *reinterpret_cast<const double2*>(a), u1 = *reinterpret_cast<const double2*>(a + 2);
+      v[0] = u0.x; v[1] = u0.y; v[2] = u1.x; v[3] = u1.y;
+    };
+    auto st4 = [](double* a, const double (&v)[4]) {
+      *reinterpret_cast<double2*>(a) = make_double2(v[0], v[1]);
+      *reinterpret_cast<double2*>(a + 2) = make_double2(v[2], v[3]);
+    };
+    // block sums of two per-rhs quantities (this thread's four) into tot_s[0..NR), tot_s[NR..2NR)
+    auto bsum2 = [&](const double (&a)[4], const double (&b)[4]) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 4; u++) { v[u] = a[u]; v[4 + u] = b[u]; }
+#pragma unroll
+      for (int o = 16; o >= HV; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < 8; u++) v[u] += __shfl_xor_sync(FULLMASK, v[u], o);
+      if ((tid & 31) < HV) {
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          redw[tid >> 5][r0 + u] = v[u];
+          redw[tid >> 5][NR + r0 + u] = v[4 + u];
+        }
+      }
+      __syncthreads();
+      if (tid < 2 * NR) {
+        double sacc = 0.0;
+        for (int w = 0; w < nwp; w++) sacc += redw[w][tid];
+        tot_s[tid] = sacc;
+      }
+      __syncthreads();
+    };
+    // (C^T yhat) of task i for its four right-hand sides
+    auto ct4 = [&](int i, double (&ct)[4]) {
+#pragma unroll
+      for (int u = 0; u < 4; u++) ct[u] = 0.0;
+      const int sl = tsl[i];
+      for (int e = ns_s[sl], e1 = ns_s[sl + 1]; e < e1; e++) {
+        const double w = nw_s[e];
+        double yv[4];
+        ld4(y_all + nr_s[e] * NRP + r0, yv);
+#pragma unroll
+        for (int u = 0; u < 4; u++) ct[u] += w * yv[u];
+      }
+    };
+    // (A p) of task i from p_all
+    auto apply4 = [&](int i, double (&a)[4]) {
+#pragma unroll
+      for (int u = 0; u < 4; u++) a[u] = 0.0;
+      const int sl = tsl[i];
+      const double* pb = p_all + tpx[i] * NRP + r0;
+#pragma unroll
+      for (int dz = -1; dz <= 1; dz++)
+#pragma unroll
+        for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+          for (int dx = -1; dx <= 1; dx++) {
+            const int c = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+            const double cf = st_s[c * nn + sl];
+            double pv[4];
+            ld4(pb + ((dz * kW7P + dy) * kW7P + dx) * NRP, pv);
+#pragma unroll
+            for (int u = 0; u < 4; u++) a[u] += cf * pv[u];
+          }
+    };
+    // c = C u (u in p_all): tasks (row, half, part) = tid < 2 NQ HV, each part half of the row's
+    // entries, the two parts summed through the partner lane (tid ^ 1); ends with a barrier
+    auto cmul4 = [&]() {
+      if (tid < 2 * NQ * HV) {
+        const int q = tid & 1, hh = (tid >> 1) % HV, row = (tid >> 1) / HV;
+        const int e0 = rs_s[row], e1 = rs_s[row + 1], em = (e0 + e1) >> 1;
+        double cv[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int e = q ? em : e0, ee = q ? e1 : em; e < ee; e++) {
+          const double w = rw_s[e];
+          double uv[4];
+          ld4(p_all + ri_s[e] * NRP + 4 * hh, uv);
+#pragma unroll
+          for (int u = 0; u < 4; u++) cv[u] += w * uv[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) cv[u] += __shfl_xor_sync(0xffffffffu >> (32 - min(32, 2 * NQ * HV - (tid & ~31))), cv[u], 1);
+        if (q == 0) st4(c_all + row * NRP + 4 * hh, cv);
+      }
+      __syncthreads();
+    };
+    // y = S^+ c, tasks as cmul4 (parts: j < NQ/2, j >= NQ/2); ends with a barrier.  cy partials
+    // (this thread's half, rows tid / HV) into cy[] after that barrier
+    auto smul4 = [&](double (&cy)[4]) {
+      if (tid < 2 * NQ * HV) {
+        const int q = tid & 1, hh = (tid >> 1) % HV, row = (tid >> 1) / HV;
+        double yv[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int j = q ? NQ / 2 : 0, je = q ? NQ : NQ / 2; j < je; j++) {
+          const double sv = si_s[j * NQ + row];
+          double cv[4];
+          ld4(c_all + j * NRP + 4 * hh, cv);
+#pragma unroll
+          for (int u = 0; u < 4; u++) yv[u] += sv * cv[u];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) yv[u] += __shfl_xor_sync(0xffffffffu >> (32 - min(32, 2 * NQ * HV - (tid & ~31))), yv[u], 1);
+        if (q == 0) st4(y_all + row * NRP + 4 * hh, yv);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 4; u++) cy[u] = 0.0;
+      if (tid < NQ * HV) {
+        const int row = tid / HV;
+        double yv[4], cr[4];
+        ld4(y_all + row * NRP + r0, yv);
+        ld4(c_all + row * NRP + r0, cr);
+#pragma unroll
+        for (int u = 0; u < 4; u++) cy[u] = yv[u] * cr[u];
+      }
+    };
+
+    double xr[TPT][4], rv[TPT][4], pr[TPT][4], qr[TPT][4];
+#pragma unroll
+    for (int i = 0; i < TPT; i++)
+#pragma unroll
+      for (int u = 0; u < 4; u++) xr[i][u] = rv[i][u] = pr[i][u] = qr[i][u] = 0.0;
+    const double* bbase = A.B + P.vec_off;
+    const double zero4[4] = {0.0, 0.0, 0.0, 0.0};
+    // init: x0 = D^-1 C^T S^+ t, r0 = A x0 - b, c = C D^-1 r0, yhat = S^+ c; tot_s[0..NR) = r0^T D^-1 r0
+    auto init = [&](const double* tcol, bool withb) {
+      for (int idx = tid; idx < NQ * NR; idx += nt) {
+        const int row = idx / NR, rr = idx - row * NR;
+        c_all[row * NRP + rr] = tcol[((int64_t)mp * NQ + row) * A.n_rhs + rr];
+      }
+      __syncthreads();
+      double cyd[4];
+      smul4(cyd);
+#pragma unroll
+      for (int i = 0; i < TPT; i++)
+        if (tpx[i] >= 0) {
+          double ct[4];
+          ct4(i, ct);
+          const double dgv = dg_s[tsl[i]];
+#pragma unroll
+          for (int u = 0; u < 4; u++) xr[i][u] = dgv * ct[u];
+          st4(p_all + tpx[i] * NRP + r0, xr[i]);
+        }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < TPT; i++)
+        if (tpx[i] >= 0) {
+          double ap[4];
+          apply4(i, ap);
+          const int k = pm_s[tsl[i]];
+#pragma unroll
+          for (int u = 0; u < 4; u++) rv[i][u] = ap[u] - (withb ? bbase[(int64_t)(r0 + u) * nn + k] : 0.0);
+        }
+      __syncthreads();
+      double rr[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < TPT; i++)
+        if (tpx[i] >= 0) {
+          const double dgv = dg_s[tsl[i]];
+          double uv[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            uv[u] = dgv * rv[i][u];
+            rr[u] += rv[i][u] * uv[u];
+          }
+          st4(p_all + tpx[i] * NRP + r0, uv);
+        }
+      __syncthreads();
+      cmul4();
+      smul4(cyd);
+      bsum2(rr, zero4);
+    };
+
+    init(A.g0, false);
+    {
+      double rz[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < TPT; i++)
+        if (tpx[i] >= 0) {
+          double ct[4];
+          ct4(i, ct);
+          const double dgv = dg_s[tsl[i]];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const double w = rv[i][u] - ct[u];
+            rz[u] += dgv * w * w;
+          }
+        }
+      if (tid < NR) sc_fl[tid] = tot_s[tid];  // rr_ref (stash)
+      __syncthreads();
+      bsum2(rz, zero4);
+      if (tid < NR) sc_rzref[tid] = tot_s[tid];
+      __syncthreads();
+    }
+    init(A.g, true);
+    const double tol2 = A.rtol * A.rtol;
+    if (tid < NR) {
+      sc_fl[tid] = 1e-30 * fmax(tot_s[tid], sc_fl[tid]);  // floor2 = 1e-30 max(rr0, rr_ref)
+      sc_act[tid] = 1;
+      sc_it[tid] = 0;
+      sc_bd[tid] = 0;
+      sc_alpha[tid] = 0.0;
+      sc_beta[tid] = 0.0;
+    }
+    __syncthreads();
+    for (int it = 0;; it++) {
+      // pass A: x += alpha_prev p_prev (deferred), r <- r - C^T yhat, z = D^-1 r, p <- -z + beta p
+      double v[4] = {0.0, 0.0, 0.0, 0.0};
+      bool act[4];
+      double al[4], be[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        act[u] = sc_act[r0 + u] != 0;
+        al[u] = sc_alpha[r0 + u];
+        be[u] = sc_beta[r0 + u];
+      }
+#pragma unroll
+      for (int i = 0; i < TPT; i++)
+        if (tpx[i] >= 0) {
+          double ct[4];
+          ct4(i, ct);
+          const double dgv = dg_s[tsl[i]];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            if (!act[u]) continue;
+            const double rk = rv[i][u] - ct[u];
+            const double zz = dgv * rk;
+            const double pold = pr[i][u];
+            if (it > 0) xr[i][u] += al[u] * pold;
+            pr[i][u] = (it == 0) ? -zz : -zz + be[u] * pold;
+            rv[i][u] = rk;
+            v[u] += rk * zz;
+          }
+          st4(p_all + tpx[i] * NRP + r0, pr[i]);
+        }
+      __syncthreads();
+      // pass B: q = A p, pq
+      double w[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < TPT; i++)
+        if (tpx[i] >= 0) {
+          apply4(i, qr[i]);
+#pragma unroll
+          for (int u = 0; u < 4; u++) w[u] += pr[i][u] * qr[i][u];
+        }
+      bsum2(v, w);
+      if (tid < NR && sc_act[tid]) {
+        const double rz = tot_s[tid], pq = tot_s[NR + tid];
+        if (it == 0) sc_ref[tid] = fmax(rz, sc_rzref[tid]);
+        sc_rz[tid] = rz;
+        if (!(rz > fmax(tol2 * sc_ref[tid], sc_fl[tid])) || it >= A.max_iter) {
+          sc_act[tid] = 0;
+          sc_it[tid] = it;
+        } else if (!(pq > 0.0) || !isfinite(pq)) {
+          sc_act[tid] = 0;
+          sc_it[tid] = it;
+          sc_bd[tid] = 1;
+        } else {
+          sc_alpha[tid] = rz / pq;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int any = 0;
+        for (int q = 0; q < NR; q++) any |= sc_act[q];
+        sc_any = any;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        act[u] = sc_act[r0 + u] != 0;
+        al[u] = sc_alpha[r0 + u];
+      }
+      __syncthreads();
+      if (!sc_any) break;
+      // pass C: r += alpha q, rr = r^T D^-1 r, u = D^-1 r -> p_all (p stays in registers)
+      double rr[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < TPT; i++)
+        if (tpx[i] >= 0) {
+          const double dgv = dg_s[tsl[i]];
+          double uv[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            if (act[u]) rv[i][u] += al[u] * qr[i][u];
+            uv[u] = dgv * rv[i][u];
+            rr[u] += rv[i][u] * uv[u];
+          }
+          st4(p_all + tpx[i] * NRP + r0, uv);
+        }
+      __syncthreads();
+      cmul4();
+      double cy[4];
+      smul4(cy);
+      bsum2(rr, cy);
+      if (tid < NR && sc_act[tid]) sc_beta[tid] = (tot_s[tid] - tot_s[NR + tid]) / sc_rz[tid];
+      __syncthreads();
+    }
+    // feasibility restoration: x += D^-1 C^T S^+ (g - C x)
+#pragma unroll
+    for (int i = 0; i < TPT; i++)
+      if (tpx[i] >= 0) st4(p_all + tpx[i] * NRP + r0, xr[i]);
+    __syncthreads();
+    cmul4();
+    for (int idx = tid; idx < NQ * NR; idx += nt) {
+      const int row = idx / NR, rr = idx - row * NR;
+      c_all[row * NRP + rr] = A.g[((int64_t)mp * NQ + row) * A.n_rhs + rr] - c_all[row * NRP + rr];
+    }
+    __syncthreads();
+    double cyd[4];
+    smul4(cyd);
+    double* Xb = A.X + P.vec_off;
+#pragma unroll
+    for (int i = 0; i < TPT; i++)
+      if (tpx[i] >= 0) {
+        double ct[4];
+        ct4(i, ct);
+        const double dgv = dg_s[tsl[i]];
+        const int k = pm_s[tsl[i]];
+#pragma unroll
+        for (int u = 0; u < 4; u++) Xb[(int64_t)(r0 + u) * nn + k] = xr[i][u] + dgv * ct[u];
+      }
+    if (tid < NR) {
+      const int prob = mp * A.n_rhs + tid;
+      A.iters[prob] = sc_it[tid];
+      const double ref = sc_ref[tid], rz = sc_rz[tid];
+      A.relres[prob] = (ref > 0.0) ? sqrt(fmax(rz, 0.0) / ref) : 0.0;
+      double* dgo = A.diag + (int64_t)prob * 4;
+      dgo[0] = rz;
+      dgo[1] = ref;
+      dgo[2] = sc_fl[tid];
+      dgo[3] = sc_bd[tid];
+    }
+    return;
   }
   double* p_s = p_all + rhs * PP;
   double* c_s = c_all + rhs * NQ;
@@ -1505,12 +1871,15 @@ __global__ void __launch_bounds__(128 * N, 1) k_pcg3d_w7(LevelArgs A) {
 size_t pcg3d_w7_smem(int N) {
   const size_t NQ = 27 * (size_t)N, NR = 4 * (size_t)N;
   const size_t EC = 729 * (size_t)N;
-  const size_t d = 27 * kW7NN + 2 * EC + kW7NN + NQ * NQ + NR * kW7P * kW7P * kW7P + 2 * NR * NQ;
+  const size_t d = 27 * kW7NN + 2 * EC + kW7NN + ((NQ * NQ + 1) & ~(size_t)1) + (NR + 2) * kW7P * kW7P * kW7P + 2 * (NR + 2) * NQ;
   return d * sizeof(double) + (3 * kW7 + 9 + NQ + 1 + kW7NN + 1 + 2 * EC + kW7NN) * sizeof(int);
 }
 
 cudaError_t launch_pcg3d_w7(const LevelArgs& A, cudaStream_t st) {
   const size_t smem = pcg3d_w7_smem(A.N);
+  // lockstep form by default; MCH_PCG3D_W7_WARP=1: one warp per rhs (A/B and path cross-check)
+  const char* we = getenv("MCH_PCG3D_W7_WARP");
+  const bool lock = !(we && atoi(we) != 0);
   auto go = [&](auto k, int N) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1519,8 +1888,8 @@ cudaError_t launch_pcg3d_w7(const LevelArgs& A, cudaStream_t st) {
   };
   if (A.n_rhs != 4 * A.N) return cudaErrorInvalidValue;
   switch (A.N) {
-    case 1: return go(k_pcg3d_w7<1>, 1);
-    case 2: return go(k_pcg3d_w7<2>, 2);
+    case 1: return lock ? go(k_pcg3d_w7<1, true>, 1) : go(k_pcg3d_w7<1, false>, 1);
+    case 2: return lock ? go(k_pcg3d_w7<2, true>, 2) : go(k_pcg3d_w7<2, false>, 2);
   }
   return cudaErrorInvalidValue;
 }

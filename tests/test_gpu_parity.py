@@ -630,8 +630,8 @@ def test_transport_paths_agree(d, n, M, L, N, seed, monkeypatch):
 def test_3d_level_paths_agree(d, n, M, L, N, seed, monkeypatch):
     """3D levels >= 2: the fused fine-window passes (fine3d.cu, default), the split transport
     (MCH_FINE3D=0) and the generic per-(macropoint, rhs) kernels (MCH_TRANSPORT_GENERIC=1), and the
-    PCG of the 7³ windows — one warp per rhs (k_pcg3d_w7, default) vs the per-(macropoint, rhs)
-    k_pcg3d (MCH_PCG3D_W7=0): every path matches the oracle at every macropoint (R15 bar) and the paths
+    PCG of the 7³ windows — all rhs in lockstep (k_pcg3d_w7, default), one warp per rhs
+    (MCH_PCG3D_W7_WARP=1) and the per-(macropoint, rhs) k_pcg3d (MCH_PCG3D_W7=0): every path matches the oracle at every macropoint (R15 bar) and the paths
     agree with each other to 1e-10 of each macropoint's largest energy."""
     H = _gpu()
     kap, ids = _admissible(d, n, M, N, seed)
@@ -639,8 +639,8 @@ def test_3d_level_paths_agree(d, n, M, L, N, seed, monkeypatch):
     Go = o.effective_coeffs()
     res = {}
     for name, env in (("fused", {}), ("split", {"MCH_FINE3D": "0"}), ("generic", {"MCH_TRANSPORT_GENERIC": "1"}),
-                      ("pcg_old", {"MCH_PCG3D_W7": "0"})):
-        for k in ("MCH_FINE3D", "MCH_TRANSPORT_GENERIC", "MCH_PCG3D_W7"):
+                      ("pcg_old", {"MCH_PCG3D_W7": "0"}), ("w7_warp", {"MCH_PCG3D_W7_WARP": "1"})):
+        for k in ("MCH_FINE3D", "MCH_TRANSPORT_GENERIC", "MCH_PCG3D_W7", "MCH_PCG3D_W7_WARP"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
