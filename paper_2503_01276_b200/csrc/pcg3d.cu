@@ -64,10 +64,16 @@ __global__ void k_node_ops3d(LevelArgs A) {
     elem_W<3>(A, P, g, e, W);
     const int a = (~o) & 7;  // corner of the node in element e
     for (int b = 0; b < 8; b++) {
-      double c[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-      c[b] = 1.0;
+      // (K_E)_ab = elem_row(W, e_b, a) written out: per direction k one weight, sign + if a_k = 1,
+      // times + if b_k = 1 (the pair partner b ^ (1 << k) has b_k = 0)
+      double kab = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 3; kk++) {
+        const double w = W[kk * DimC<3>::NT + pair_type<3>(kk, a, b)];
+        kab += ((((a ^ b) >> kk) & 1) ? -w : w);
+      }
       const int dx = e[0] + (b & 1) - X[0], dy = e[1] + ((b >> 1) & 1) - X[1], dz = e[2] + ((b >> 2) & 1) - X[2];
-      st[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)] += elem_row<3>(W, c, a);
+      st[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)] += kab;
     }
     for (int j = 0; j < N; j++) mw[t][j] += elem_m<3>(A, P, g, e, j, a);
   }
