@@ -531,9 +531,10 @@ __global__ void k_proj_setup(LevelArgs A) {
     const double dv = 1.0 / diag_node<D>(A, P, g, k);
     dinv[k] = (D == 2) ? (double)(float)dv : dv;
   }
-  // nw[j][k] = sum over the elements around node k of m_{E,j,a} (used for subcell-interior nodes)
+  // nw[j][k] = sum over the elements around node k of m_{E,j,a} (used for subcell-interior nodes by
+  // the generic k_pcg only: the specialised solvers form their own constraint weights)
   double* nwt = A.NWt + P.node_off * A.N;
-  for (int k = threadIdx.x; k < g.nnodes; k += blockDim.x) {
+  for (int k = threadIdx.x; A.need_nwt && k < g.nnodes; k += blockDim.x) {
     int x[3];
     node_xyz<D>(g, k, x);
     double w[4] = {0.0, 0.0, 0.0, 0.0};

@@ -800,6 +800,7 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
     A.FK = B.fused3 ? c->FK.as<double>() : nullptr;
     A.nkp_max = B.max_kp;
     A.stc_pad = (B.on3d && level >= 2 && !B.w7) ? B.nxm3 * B.nxm3 * B.nxm3 : 0;
+    A.need_nwt = (B.on2d || B.on3d) ? 0 : 1;  // see the PCG dispatch below
     cudaEventRecord(B.ev[4], st);
     if (level >= 2 && B.fused3) {  // 3D: I_p, A_1 I_p, C_1 I_p and P_n^T in one pass (fine3d.cu)
       CKC(c, launch_fine3d_transport(A, st));

@@ -95,6 +95,7 @@ struct LevelArgs {
   double* STC;             // levels >= 2: per window node 9 stencil coefficients, SoA [9][nodes]
   double* dbg;             // debug: per-iteration scalars of problem dbg_prob (NULL: off)
   int dbg_prob, dbg_cap;
+  int need_nwt;            // k_proj_setup fills NWt (generic k_pcg only)
   int stc_pad;             // 3D levels >= 2 on k_pcg3d / k_pcg3dc: STC / MLR per window at a fixed node
                            // stride NXM^3 (window i at i * 27 * NXM^3), so the solvers address them
                            // with compile-time offsets; 0: node_off layout with stride nn
