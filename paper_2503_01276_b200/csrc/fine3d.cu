@@ -391,7 +391,7 @@ cudaError_t launch_fine3d_transport(const LevelArgs& A, cudaStream_t st) {
 // into FK (read by k_gram for Eq. 7), and on the whole window into the parent pool if p is
 // stored (parents of later levels, or keep_all).  I_p is formed again from the parents (the
 // transport kept it on chip); per value the arithmetic is k_combine's.
-__global__ void __launch_bounds__(256, 2) k_fine3d_combine(LevelArgs A) {
+__global__ void __launch_bounds__(256, 3) k_fine3d_combine(LevelArgs A) {
   const int mp = blockIdx.y;
   const ProbDesc& P = A.probs[mp];
   const Geo<3> gf = fine_geo<3>(P);
@@ -445,10 +445,10 @@ __global__ void __launch_bounds__(256, 2) k_fine3d_combine(LevelArgs A) {
     wgt[a] = w;
     nid[a] = node_id<3>(gl, xc);
   }
-  // right-hand sides in chunks of eight: per parent (runtime loop, index formed in place) the
+  // right-hand sides in chunks of four (80 registers: three CTAs per SM): per parent (runtime loop, index formed in place) the
   // loads of all eight rhs are in flight together, I accumulated in registers (one rhs at a time
   // left the loop long-scoreboard bound); the coarse-node values (L1-resident) are read at use
-  constexpr int RC = 8;
+  constexpr int RC = 4;
   for (int r0 = 0; r0 < nr; r0 += RC) {
     double Iv[RC];
 #pragma unroll
