@@ -902,10 +902,10 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
       const double* pn = plane(z + 1) + ro;
 #pragma unroll
       for (int dy = 0; dy < 3; dy++) v[dy][2] = xin ? pn[(dy - 1) * NXM] : 0.0;
-      const int k = nidx(z), kl = lact ? k : 0;
+      const int k = nidx(z);
       double cf[27];  // all 27 coefficient loads in flight before the first use
 #pragma unroll
-      for (int c = 0; c < 27; c++) cf[c] = __ldg(S27 + c * PAD + kl);  // kl: k, or node 0 on inactive lanes
+      for (int c = 0; c < 27; c++) cf[c] = lact ? __ldg(S27 + c * PAD + k) : 0.0;
       double Ap = 0.0;
 #pragma unroll
       for (int dz = 0; dz < 3; dz++)
@@ -919,7 +919,7 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
           const int cb = 9 * dz + 3 * dy;
           Ap += cf[cb] * l + cf[cb + 1] * c0 + cf[cb + 2] * r;
         }
-      f(z, k, lact ? Ap : 0.0, v[1][1]);
+      f(z, k, Ap, v[1][1]);
 #pragma unroll
       for (int dy = 0; dy < 3; dy++) {
         v[dy][0] = v[dy][1];
