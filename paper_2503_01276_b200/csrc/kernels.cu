@@ -77,7 +77,9 @@ __global__ void k_level_ops(LevelArgs A) {
 }
 
 // ---------------------------------------------------------------------------------------
-// targets: one CTA per macropoint
+// targets: one CTA per macropoint.  K_p first (the whole CTA: its centroids c_mj enter every
+// subcell's targets), then one warp per subcell with warp reductions (r02 reduced every subcell
+// over the CTA: two barriers and a serial thread-0 section per subcell)
 template <int D>
 __global__ void k_targets(LevelArgs A) {
   const int mp = blockIdx.x;
@@ -86,16 +88,13 @@ __global__ void k_targets(LevelArgs A) {
   __shared__ double tot[16];
   __shared__ double cm[3][4];
   const int N = A.N;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwp = blockDim.x >> 5;
   const double hd = (D == 2) ? A.h * A.h : A.h * A.h * A.h;
-  // process K_p first (subcell index of slot l in every dim), then all subcells
-  int qc = 0;
-  for (int i = D - 1; i >= 0; i--) qc = qc * A.w + A.l;
-  for (int pass = 0; pass <= A.nsub; pass++) {
-    const int q = (pass == 0) ? qc : pass - 1;
-    // fine-cell box of subcell q
-    int lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
+  // fine-cell box of subcell q
+  auto box = [&](int q, int (&lo)[3], int (&ext)[3]) -> bool {
     bool present = true;
     int rem = q;
+    for (int i = 0; i < 3; i++) { lo[i] = 0; ext[i] = 1; }
     for (int i = 0; i < D; i++) {
       const int slot = rem % A.w;
       rem /= A.w;
@@ -107,30 +106,41 @@ __global__ void k_targets(LevelArgs A) {
       lo[i] = flo;
       ext[i] = fhi - flo;
     }
-    double v[16];
-    for (int i = 0; i < 16; i++) v[i] = 0.0;
-    if (present) {
-      // plane by plane (z), threads over the plane's cells: 32-bit index arithmetic with the
-      // float-reciprocal division of fdiv (exact below 2^22; r02 divided 64-bit per cell)
-      const int pc = ext[0] * ext[1];
-      const float inv0 = 1.0f / (float)ext[0];
-      for (int zz = 0; zz < ext[2]; zz++)
-      for (int t = threadIdx.x; t < pc; t += blockDim.x) {
+    return present;
+  };
+  // v[j*4] = count, v[j*4+1+m] = sum (f_m + 1/2) over the box's cells of continuum j (N <= 4 x 4
+  // entries: per thread, cells t0, t0 + stride, ... of the box plane by plane, 32-bit index
+  // arithmetic with the float-reciprocal division of fdiv, exact below 2^22)
+  auto accum = [&](const int (&lo)[3], const int (&ext)[3], int t0, int stride, double (&v)[16]) {
+    const int pc = ext[0] * ext[1];
+    const float inv0 = 1.0f / (float)ext[0];
+    for (int zz = 0; zz < ext[2]; zz++)
+      for (int t = t0; t < pc; t += stride) {
         const int yy = fdiv(t, inv0);
         const int f[3] = {lo[0] + t - yy * ext[0], lo[1] + yy, lo[2] + zz};
         int64_t fi = 0;
         for (int i = D - 1; i >= 0; i--) fi = fi * A.n + f[i];
         const int id = A.ids[fi];
-        // v[j*(1+D)] = count, v[j*(1+D)+1+m] = sum (f_m + 1/2)
+#pragma unroll
         for (int j = 0; j < 4; j++) {
           if (j == id) {
             v[j * 4] += 1.0;
+#pragma unroll
             for (int m = 0; m < D; m++) v[j * 4 + 1 + m] += f[m] + 0.5;
           }
         }
       }
-    }
-    if (N <= 2) {  // entries j*4 + (0..D) with j < N all lie in the first 8: reduce only those
+  };
+  {  // K_p (subcell index of slot l in every dim): centroids c_mj
+    int qc = 0;
+    for (int i = D - 1; i >= 0; i--) qc = qc * A.w + A.l;
+    int lo[3], ext[3];
+    const bool present = box(qc, lo, ext);
+    double v[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = 0.0;
+    if (present) accum(lo, ext, threadIdx.x, blockDim.x, v);
+    if (N <= 2) {
       double v8[8];
 #pragma unroll
       for (int i = 0; i < 8; i++) v8[i] = v[i];
@@ -138,31 +148,41 @@ __global__ void k_targets(LevelArgs A) {
     } else {
       block_sum<16>(v, scratch, tot);
     }
-    if (pass == 0) {
-      if (threadIdx.x == 0) {
-        for (int j = 0; j < N; j++) {
-          const double cnt = tot[j * 4];
-          if (cnt == 0.0) atomicOr(&A.flags[mp], 1);
-          for (int m = 0; m < D; m++) cm[m][j] = (cnt > 0) ? (tot[j * 4 + 1 + m] * A.h) / cnt : 0.0;
-        }
-        for (int m = 0; m < D; m++)
-          for (int j = 0; j < N; j++) A.cm[(mp * 3 + m) * 4 + j] = cm[m][j];
+    const int ts = (N <= 2) ? 4 : 4;
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < N; j++) {
+        const double cnt = tot[j * ts];
+        if (cnt == 0.0) atomicOr(&A.flags[mp], 1);
+        for (int m = 0; m < D; m++) cm[m][j] = (cnt > 0) ? (tot[j * ts + 1 + m] * A.h) / cnt : 0.0;
       }
-      __syncthreads();
-    } else {
-      if (threadIdx.x == 0) {
-        for (int j = 0; j < N; j++) {
-          const int row = q * N + j;
-          const double cnt = present ? tot[j * 4] : 0.0;
-          A.meas[(int64_t)mp * A.ncon + row] = cnt * hd;
-          double* gr = A.g0 + ((int64_t)mp * A.ncon + row) * A.n_rhs;
-          for (int a = 0; a < A.n_rhs; a++) gr[a] = 0.0;
-          gr[j] = cnt * hd;
-          for (int m = 0; m < D; m++)
-            gr[N + j * D + m] = (cnt > 0) ? hd * (tot[j * 4 + 1 + m] * A.h - cm[m][j] * cnt) : 0.0;
-        }
-      }
-      __syncthreads();
+      for (int m = 0; m < D; m++)
+        for (int j = 0; j < N; j++) A.cm[(mp * 3 + m) * 4 + j] = cm[m][j];
+    }
+    __syncthreads();
+  }
+  for (int q = wid; q < A.nsub; q += nwp) {
+    int lo[3], ext[3];
+    const bool present = box(q, lo, ext);
+    double v[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) v[i] = 0.0;
+    if (present) accum(lo, ext, lane, 32, v);
+#pragma unroll
+    for (int i = 0; i < 16; i++)
+      if (i < 4 * N)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(FULLMASK, v[i], o);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {  // lane j writes continuum j's rows
+      if (j >= N || lane != j) continue;
+      const int row = q * N + j;
+      const double cnt = present ? v[j * 4] : 0.0;
+      A.meas[(int64_t)mp * A.ncon + row] = cnt * hd;
+      double* gr = A.g0 + ((int64_t)mp * A.ncon + row) * A.n_rhs;
+      for (int a = 0; a < A.n_rhs; a++) gr[a] = 0.0;
+      gr[j] = cnt * hd;
+      for (int m = 0; m < D; m++)
+        gr[N + j * D + m] = (cnt > 0) ? hd * (v[j * 4 + 1 + m] * A.h - cm[m][j] * cnt) : 0.0;
     }
   }
 }
