@@ -27,6 +27,10 @@
 
 #include "pcg3d_common.cuh"
 
+#ifndef MCH_P13_MINB
+#define MCH_P13_MINB 3  // CTAs per SM of the 13-node windows: 3 (80 registers, some spills) beat 2 (128): c5 level-3 PCG 31.0 -> 28.1 ms
+#endif
+
 // ------------------------------------------------------------------------------------------
 // per-node stencil rows STC[27][nodes] (offset (dx+1) + 3(dy+1) + 9(dz+1)) and octant-merged
 // constraint weights MW[8][N][nodes] (octant o = xs + 2 ys + 4 zs, sides as in Sides) of every
@@ -1936,7 +1940,7 @@ template <int N>
 static cudaError_t launch3n(const LevelArgs& A, int nxm, cudaStream_t st) {
   switch (nxm) {
     case 7: return launch3<N, 7, 1, 8>(A, st);
-    case 13: return launch3<N, 13, 1, 2>(A, st);
+    case 13: return launch3<N, 13, 1, MCH_P13_MINB>(A, st);
     case 25: return launch3<N, 25, 2, 1>(A, st);
   }
   return cudaErrorInvalidValue;
