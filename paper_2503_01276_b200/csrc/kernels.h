@@ -42,7 +42,7 @@ size_t pcg3d_l1c_smem(int N);
 int pcg3d_l1c_cluster(int level_problems, int sms);
 cudaError_t launch_pcg3d_l1c(const LevelArgs& A, int cs, cudaStream_t st);
 // levels >= 2 (windows of 13 / 25 level nodes per side) with a cluster of cs CTAs per problem
-size_t pcg3dc_smem(int N, int nxm);
+size_t pcg3dc_smem(int N, int nxm, int cs);
 int pcg3dc_cluster(int nxm, int level_problems, int sms);
 cudaError_t launch_pcg3dc(const LevelArgs& A, int nxm, int cs, cudaStream_t st);
 // windows of <= 7 level nodes per side, N <= 2: one CTA per macropoint, one warp per rhs

@@ -526,7 +526,7 @@ static int build_level(mch_ctx* c, int level, std::vector<std::unique_ptr<LevelB
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         V.l2cs = pcg3dc_cluster(nxm, (int)Sl.size() * nr, sms);
-        if (pcg3dc_smem(N, nxm) > 232448) V.l2cs = 1;
+        if (pcg3dc_smem(N, nxm, V.l2cs) > 232448) V.l2cs = 1;
       }
       const char* w7e = getenv("MCH_PCG3D_W7");
       V.w7 = V.on3d && nxm == 7 && N <= 2 && nr == 4 * N && pcg3d_w7_smem(N) <= 232448 && !(w7e && atoi(w7e) == 0);

@@ -24,6 +24,10 @@
 #include "kernels.h"
 #include "pcg3d_common.cuh"
 
+#ifndef MCH_P25_MINB
+#define MCH_P25_MINB 1  // CTAs per SM of the 25-node cluster kernel (2: 72 registers, 968 B spills, 44 -> 69 ms)
+#endif
+
 namespace cg = cooperative_groups;
 
 namespace {
@@ -719,8 +723,9 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
   bool wact = false, lact = false;  // wact warp-uniform (some row of the warp is in the window)
 
   extern __shared__ __align__(16) double smem[];
-  double* p_s = smem;                  // [NXM+2][PY][NXM], zero halo planes / rows
-  double* bins = p_s + (NXM + 2) * PZ;  // [NXM rows][NQ]
+  constexpr int SL = (NXM + CS - 1) / CS + 2;  // p planes held per CTA: its slab + a zero halo plane each side
+  double* p_s = smem;                  // [SL][PY][NXM]: plane z of the slab at z - z0 + 1, zero halo rows
+  double* bins = p_s + SL * PZ;        // [NXM rows][NQ]
   double* Ysh = bins + NXM * NQ;        // [NQ] yhat
   double* csh = Ysh + NQ;               // [NQ] c
   double* slots = csh + NQ;             // [5][32] scalar partial sums
@@ -730,7 +735,7 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
   int* zsm = reinterpret_cast<int*>(red + 3 * (NQ + 2));  // [NXM][3] z sides (pm, k0, k1)
   __shared__ double bc[2];
 
-  for (int i = threadIdx.x; i < (NXM + 2) * PZ; i += blockDim.x) p_s[i] = 0.0;
+  for (int i = threadIdx.x; i < SL * PZ; i += blockDim.x) p_s[i] = 0.0;
   for (int i = threadIdx.x; i < NXM * NQ + 2 * NQ + 5 * 32; i += blockDim.x) bins[i] = 0.0;
   for (int z = threadIdx.x; z < nz; z += blockDim.x) {
     const Sides s = sides_of(A, P, 2, z, nz - 1);
@@ -775,7 +780,7 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
     }
   };
   auto nidx = [&](int z) { return (z * ny + y) * nx + x; };
-  auto pidx = [&](int z) { return (z + 1) * PZ + (y + 1) * NXM + x; };
+  auto pidx = [&](int z) { return (z - z0 + 1) * PZ + (y + 1) * NXM + x; };
 
   // (C^T yhat)_k over the present octants
   auto ct_at = [&](int z, int k) -> double {
@@ -880,10 +885,11 @@ __global__ void __launch_bounds__(32 * ((NXM + (32 / ((NXM > 16) ? 32 : ((NXM > 
   };
   // p_s plane z (planes z0 - 1 and z1 live in the neighbouring CTA: DSMEM)
   auto plane = [&](int z) -> const double* {
-    const double* base = p_s;
-    if (z >= 0 && z < nz && z < z0) base = cl.map_shared_rank(p_s, cr - 1);
-    if (z >= 0 && z < nz && z >= z1) base = cl.map_shared_rank(p_s, cr + 1);
-    return base + (z + 1) * PZ;
+    // own slab and the window's zero halo planes -1 / nz: local plane z - z0 + 1; a neighbour's
+    // boundary plane: its local index from its slab start
+    if (z >= 0 && z < nz && z < z0) return cl.map_shared_rank(p_s, cr - 1) + (z - ((cr - 1) * nz) / CS + 1) * PZ;
+    if (z >= 0 && z < nz && z >= z1) return cl.map_shared_rank(p_s, cr + 1) + (z - z1 + 1) * PZ;
+    return p_s + (z - z0 + 1) * PZ;
   };
   // (A p)_k from p_s: f(z, k, Ap, p_k)  (wact warps; lanes >= nx carry zeros)
   auto sweep_stencil = [&](auto&& f) {
@@ -1281,8 +1287,8 @@ cudaError_t launch_pcg3d_l1c(const LevelArgs& A, int cs, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------------
-size_t pcg3dc_smem(int N, int nxm) {
-  const size_t d = (size_t)(nxm + 2) * (nxm + 2) * nxm + (size_t)nxm * 27 * N + 2 * 27 * N + 5 * 32 + 512 +
+size_t pcg3dc_smem(int N, int nxm, int cs) {
+  const size_t d = (size_t)((nxm + cs - 1) / cs + 2) * (nxm + 2) * nxm + (size_t)nxm * 27 * N + 2 * 27 * N + 5 * 32 + 512 +
                    3 * (27 * N + 2);
   return d * sizeof(double) + (size_t)nxm * 3 * sizeof(int);
 }
@@ -1290,7 +1296,7 @@ size_t pcg3dc_smem(int N, int nxm) {
 template <int N, int NXM, int RW, int MINB, int CS>
 static cudaError_t go_3dc(const LevelArgs& A, cudaStream_t st) {
   auto k = k_pcg3dc<N, NXM, RW, MINB, CS>;
-  const size_t smem = pcg3dc_smem(N, NXM);
+  const size_t smem = pcg3dc_smem(N, NXM, CS);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   constexpr int LPR = (NXM > 16) ? 32 : ((NXM > 8) ? 16 : 8), RPW = 32 / LPR;
@@ -1314,7 +1320,7 @@ template <int N>
 static cudaError_t go_3dc_n(const LevelArgs& A, int nxm, int cs, cudaStream_t st) {
   if (nxm == 25) {
     switch (cs) {
-      case 2: return go_3dc<N, 25, 2, 1, 2>(A, st);
+      case 2: return go_3dc<N, 25, 2, MCH_P25_MINB, 2>(A, st);
       case 4: return go_3dc<N, 25, 2, 1, 4>(A, st);
     }
   } else if (nxm == 13) {
