@@ -7,6 +7,8 @@ arrays or CUDA torch tensors; PyTorch is only used for device memory and the str
 from __future__ import annotations
 
 import ctypes
+import json
+import os
 
 import numpy as np
 
@@ -174,6 +176,7 @@ class Homogenizer:
                  torch_memory=False, comm=None):
         self.d, self.n, self.N, self.M, self.L, self.eta, self.l = d, n, N, M, L, eta, l
         self.interp = interp
+        self.rank, self.world = rank, world
         self.n_rhs = N * (1 + d)
         self.mv = M + 1 if layout == "vertex" else M  # macropoints per dimension
         self.num_macropoints = self.mv ** d
@@ -201,9 +204,19 @@ class Homogenizer:
         mch_set_medium(self.ctx, kappa, ids)
         self.solved = 0
 
-    def solve_all(self):
+    def solve_all(self, log=None):
+        """Solve the remaining levels in order.  `log`: path of a JSON-lines
+        file that gets one record per level (mch_get_level_stats of that solve: macropoints,
+        iterations, per-phase device times, bytes, launches), or the MCH_LEVEL_LOG environment
+        variable; appended, one line per level."""
+        log = log or os.environ.get("MCH_LEVEL_LOG")
         for lev in range(self.solved + 1, self.L + 1):
             self.solve_level(lev)
+            if log:
+                rec = {"level": lev, "d": self.d, "n_rhs": self.n_rhs, "rank": self.rank, "world": self.world}
+                rec.update(self.level_stats(lev))
+                with open(log, "a") as f:
+                    f.write(json.dumps(rec) + "\n")
 
     def effective_coeffs(self, out=None):
         if out is None:

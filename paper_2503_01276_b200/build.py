@@ -48,6 +48,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
         defs = (["-DPCG2D_TIMING"] if timing else []) + os.environ.get("MCH_BUILD_DEFS", "").split()
         cmd = [NVCC, *FLAGS_C, *defs, "-c", "-o", obj, os.path.join(CSRC, src)]
+        # incremental: an object newer than its source and every header is kept (dev speed-up;
+        # force=True or a removed object directory rebuilds everything)
+        hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+        hdrs.append(os.path.join(os.path.dirname(HERE), "include", "mch.h"))
+        deps = [os.path.join(CSRC, src), *hdrs, os.path.abspath(__file__)]
+        if not force and os.path.exists(obj) and all(os.path.getmtime(obj) > os.path.getmtime(d) for d in deps):
+            continue
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     log_parts, failed = [], False
     for cmd, pr in procs:

@@ -834,12 +834,32 @@ __global__ void k_coarse_setup(LevelArgs A) {
   for (int w = 0; w < nw; w++) { kmin = fmin(kmin, red[w]); kmax = fmax(kmax, red[32 + w]); }
   const bool use = kmax >= MCH_COARSE_CONTRAST * kmin;
   const double thr = sqrt(kmin * kmax);
+  const double thr1 = 0.5 * (kmin + kmax);  // pass 1: cells mostly made of the high phase
+  const int erode_mode = (A.coarse >> 2) & 3;  // dev A/B: 1 = all-cells-high erosion instead
+  __shared__ int csize[1024];
+  __shared__ int cnew[1024];
+  __shared__ int redo;
+  __shared__ int wtot[32];
+  int nall = 0;
+  // Two passes at most.  Pass 0: high nodes = nodes touching a cell with kappa > thr.  On a coarse
+  // level mesh the cell means widen every inclusion by up to a cell, so close inclusions fuse into
+  // one component above kCompNodes, which the selection below would drop (config 5, level 2: the
+  // four windows around the largest spheres then iterate on Jacobi alone, 220-286 iterations
+  // instead of ~45).  Pass 1 (MCH_COARSE_ERODE, default on) relabels the nodes of such components
+  // only: a node stays high when ALL its cells in the window are high, which splits the fused
+  // inclusions again.  Nodes of different components still never share a cell (a cell shared by
+  // two kept nodes makes them neighbours), so E stays diagonal.
+  for (int pass = 0; pass < 2; pass++) {
   // 2. high nodes: label = own index
   for (int k = threadIdx.x; k < nn; k += blockDim.x) {
     int lab = -1;
-    if (use) {
+    const int prev = (pass == 0) ? 0 : cm[k];  // pass 1: component id of pass 0 (or -1)
+    const bool big = pass == 1 && prev >= 0 && prev < nall && csize[prev] > kCompNodes;
+    if (pass == 1 && prev >= 0 && !big) lab = k;
+    if (use && (pass == 0 || big)) {
       int x[3];
       node_xyz<D>(g, k, x);
+      bool any = false, all = true, maj = false;
       for (int o = 0; o < (1 << D); o++) {
         int e[3] = {0, 0, 0};
         bool ok = true;
@@ -847,8 +867,14 @@ __global__ void k_coarse_setup(LevelArgs A) {
           e[i] = x[i] - 1 + ((o >> i) & 1);
           ok = ok && e[i] >= 0 && e[i] < g.nc[i];
         }
-        if (ok && kcell(e) > thr) lab = k;
+        if (ok) {
+          const double kc = kcell(e);
+          any = any || kc > thr;
+          all = all && kc > thr;
+          maj = maj || kc > thr1;
+        }
       }
+      if (pass == 0 ? any : (erode_mode == 1 ? (any && all) : maj)) lab = k;
     }
     cm[k] = lab;
   }
@@ -896,7 +922,6 @@ __global__ void k_coarse_setup(LevelArgs A) {
   const int k0 = threadIdx.x * chunk, k1 = min(nn, k0 + chunk);
   int mine = 0;
   for (int k = k0; k < k1; k++) mine += (cm[k] == k);
-  __shared__ int wtot[32];
   cnt[threadIdx.x] = block_excl_scan(mine, wtot, &total);
   __syncthreads();
   {
@@ -918,14 +943,19 @@ __global__ void k_coarse_setup(LevelArgs A) {
   // keep components of at most kCompNodes nodes (long ones, e.g. channels across the window,
   // would make the per-component sums of every iteration a long serial chain), renumbered in
   // order; at most ncmax of them
-  __shared__ int csize[1024];
-  __shared__ int cnew[1024];
-  const int nall = min(total, 1024);
+  nall = min(total, 1024);
+  if (threadIdx.x == 0) redo = 0;
   for (int a = threadIdx.x; a < nall; a += blockDim.x) csize[a] = 0;
   __syncthreads();
   for (int k = threadIdx.x; k < nn; k += blockDim.x)
     if (cm[k] >= 0 && cm[k] < nall) atomicAdd(&csize[cm[k]], 1);
   __syncthreads();
+  if (pass == 0 && (A.coarse & 2) && total <= 1024)
+    for (int a = threadIdx.x; a < nall; a += blockDim.x)
+      if (csize[a] > kCompNodes) redo = 1;
+  __syncthreads();
+  if (!redo) break;
+  }  // pass
   if (threadIdx.x == 0) {
     int next = 0;
     for (int a = 0; a < nall; a++) cnew[a] = (csize[a] <= kCompNodes && next < A.ncmax) ? next++ : -1;

@@ -161,6 +161,7 @@ struct mch_ctx {
   DevBuf cmap, ncomp, cbox, einv, cz, cptr, clist;  // two-level preconditioner (level 1)
   DevBuf azp, azi, azw;                               // (A z_a) lists of the 2D on-chip kernels
   bool coarse = false;
+  int coarse_erode = 1;  // MCH_COARSE_ERODE=0: one labelling pass only (oversized components dropped)
   DevAlloc al;
   std::vector<DevBuf*> bufs() {
     return {&FK, &STC, &MLR, &pinv_ds, &W, &Mc, &g0, &g, &meas, &cm, &flags, &dinv, &nwt, &Sinv, &X, &R, &P, &Q, &B,
@@ -264,6 +265,7 @@ extern "C" int mch_create(const mch_params* prm, const double* kappa, const uint
   c->st = reinterpret_cast<cudaStream_t>(p.stream);
   // two-level preconditioner at level 1: on unless MCH_COARSE=0
   c->coarse = !(getenv("MCH_COARSE") != nullptr && atoi(getenv("MCH_COARSE")) == 0);
+  c->coarse_erode = getenv("MCH_COARSE_ERODE") != nullptr ? atoi(getenv("MCH_COARSE_ERODE")) : 1;
   if (const char* pm = getenv("MCH_PCG")) {
     if (!strcmp(pm, "old")) c->pcg_mode = 1;
     else if (!strcmp(pm, "gn")) c->pcg_mode = 2;
@@ -816,7 +818,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       CKC(c, launch_transport(A, B.th_f, st));
     }
     cudaEventRecord(B.ev[5], st);
-    A.coarse = B.coarse ? 1 : 0;
+    // bit 1: second labelling pass that erodes oversized components (k_coarse_setup)
+    A.coarse = B.coarse ? (c->coarse_erode ? 3 | (c->coarse_erode == 2 ? 4 : 0) : 1) : 0;
     A.ncmax = kCoarseMax;
     A.cmap = c->cmap.as<int>(); A.ncomp = c->ncomp.as<int>(); A.cbox = c->cbox.as<int>();
     A.Einv = c->einv.as<double>(); A.CZ = c->cz.as<double>();

@@ -597,6 +597,49 @@ def test_coarse_space_preconditioner(monkeypatch):
         assert g_err(G1[i], G0[i]) < G_TOL, (i, g_err(G1[i], G0[i]))
 
 
+def test_coarse_space_second_pass_config5_level2(monkeypatch):
+    """Second labelling pass of the coarse space (`MCH_COARSE_ERODE`): the four
+    config-5 level-2 windows around the largest spheres fuse every inclusion into one oversized
+    component on the 2h mesh (dropped: Jacobi alone, > 200 iterations); relabelling that component
+    with the majority-cell threshold brings them to the other windows' counts, and the coefficients
+    stay within the R15 bar of the one-pass run (same constrained problems, same tolerance)."""
+    import torch
+    from mch_inputs import CONFIGS, make_medium
+    H = _gpu()
+    cfg = CONFIGS[5]
+    kap, ids = make_medium(cfg)
+    kd, idd = torch.from_numpy(kap).cuda(), torch.from_numpy(ids).cuda()
+    res = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("MCH_COARSE_ERODE", flag)
+        with H.from_config(cfg, kd, idd) as h:
+            h.solve_level(1)
+            h.solve_level(2)
+            res[flag] = (h.level_iterations(2), h.level_macropoints(2), h.effective_coeffs())
+    it0, it1 = res["0"][0], res["1"][0]
+    assert it0.max() > 200 and it1.max() * 3 < it0.max(), (it0.max(), it1.max())
+    assert it1.sum() < it0.sum()
+    G0, G1 = res["0"][2], res["1"][2]
+    for i in res["0"][1]:
+        assert g_err(G1[int(i)], G0[int(i)]) < G_TOL, (int(i), g_err(G1[int(i)], G0[int(i)]))
+
+
+def test_level_log_jsonl(tmp_path):
+    """solve_all(log=...) appends one JSON record per level with the library's level stats."""
+    import json
+    H = _gpu()
+    kap, ids = _admissible(2, 32, 4, 2, 5)
+    path = tmp_path / "levels.jsonl"
+    with H(2, 32, 2, 4, 2, 2, kap, ids) as h:
+        h.solve_all(log=str(path))
+        stats = [h.level_stats(l) for l in (1, 2)]
+    recs = [json.loads(x) for x in path.read_text().splitlines()]
+    assert [r["level"] for r in recs] == [1, 2]
+    for r, s in zip(recs, stats):
+        assert r["macropoints"] == s["macropoints"] and r["iters_total"] == s["iters_total"]
+        assert r["ms_pcg"] > 0 and r["launches"] > 0
+
+
 @pytest.mark.parametrize("d,n,M,L,N,seed", [(3, 16, 4, 2, 2, 970), (2, 64, 8, 3, 1, 41), (2, 64, 8, 3, 2, 7),
                                              (2, 32, 4, 2, 3, 23)])
 def test_transport_paths_agree(d, n, M, L, N, seed, monkeypatch):
