@@ -835,7 +835,6 @@ __global__ void k_coarse_setup(LevelArgs A) {
   const bool use = kmax >= MCH_COARSE_CONTRAST * kmin;
   const double thr = sqrt(kmin * kmax);
   const double thr1 = 0.5 * (kmin + kmax);  // pass 1: cells mostly made of the high phase
-  const int erode_mode = (A.coarse >> 2) & 3;  // dev A/B: 1 = all-cells-high erosion instead
   __shared__ int csize[1024];
   __shared__ int cnew[1024];
   __shared__ int redo;
@@ -845,10 +844,11 @@ __global__ void k_coarse_setup(LevelArgs A) {
   // level mesh the cell means widen every inclusion by up to a cell, so close inclusions fuse into
   // one component above kCompNodes, which the selection below would drop (config 5, level 2: the
   // four windows around the largest spheres then iterate on Jacobi alone, 220-286 iterations
-  // instead of ~45).  Pass 1 (MCH_COARSE_ERODE, default on) relabels the nodes of such components
-  // only: a node stays high when ALL its cells in the window are high, which splits the fused
-  // inclusions again.  Nodes of different components still never share a cell (a cell shared by
-  // two kept nodes makes them neighbours), so E stays diagonal.
+  // instead of ~45).  Pass 1 (MCH_COARSE_ERODE=0 turns it off) relabels the nodes of such
+  // components only: a node stays high when it touches a cell whose mean is above the midpoint
+  // thr1, i.e. a cell mostly made of the high phase, which separates the fused inclusions again.
+  // The kept nodes are a subset of one pass-0 component, and two of them sharing a cell are
+  // neighbours, so nodes of different components still never share a cell and E stays diagonal.
   for (int pass = 0; pass < 2; pass++) {
   // 2. high nodes: label = own index
   for (int k = threadIdx.x; k < nn; k += blockDim.x) {
@@ -859,7 +859,7 @@ __global__ void k_coarse_setup(LevelArgs A) {
     if (use && (pass == 0 || big)) {
       int x[3];
       node_xyz<D>(g, k, x);
-      bool any = false, all = true, maj = false;
+      bool any = false, maj = false;
       for (int o = 0; o < (1 << D); o++) {
         int e[3] = {0, 0, 0};
         bool ok = true;
@@ -870,11 +870,10 @@ __global__ void k_coarse_setup(LevelArgs A) {
         if (ok) {
           const double kc = kcell(e);
           any = any || kc > thr;
-          all = all && kc > thr;
           maj = maj || kc > thr1;
         }
       }
-      if (pass == 0 ? any : (erode_mode == 1 ? (any && all) : maj)) lab = k;
+      if (pass == 0 ? any : maj) lab = k;
     }
     cm[k] = lab;
   }

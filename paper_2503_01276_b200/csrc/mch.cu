@@ -818,8 +818,8 @@ extern "C" int mch_solve_level(mch_ctx* c, int level) {
       CKC(c, launch_transport(A, B.th_f, st));
     }
     cudaEventRecord(B.ev[5], st);
-    // bit 1: second labelling pass that erodes oversized components (k_coarse_setup)
-    A.coarse = B.coarse ? (c->coarse_erode ? 3 | (c->coarse_erode == 2 ? 4 : 0) : 1) : 0;
+    // bit 1: second labelling pass that splits oversized components (k_coarse_setup)
+    A.coarse = B.coarse ? (c->coarse_erode ? 3 : 1) : 0;
     A.ncmax = kCoarseMax;
     A.cmap = c->cmap.as<int>(); A.ncomp = c->ncomp.as<int>(); A.cbox = c->cbox.as<int>();
     A.Einv = c->einv.as<double>(); A.CZ = c->cz.as<double>();

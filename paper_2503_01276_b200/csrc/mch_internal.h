@@ -66,7 +66,7 @@ struct LevelArgs {
                            //  equilibrated S (half-bandwidth band, 2D large l), Sinv[mp][nc][band+1]
   // two-level preconditioner (generic k_pcg, level 1, dense projector): M^-1 = D^-1 + Z E^-1 Z^T with
   // Z = indicators of the 8- (26-) connected components of nodes touching a high-kappa cell
-  int coarse;              // 1: build and use the coarse space
+  int coarse;              // bit 0: build and use the coarse space; bit 1: second labelling pass (k_coarse_setup)
   int ncmax;               // components per window capacity (more: the window runs without)
   int* cmap;               // [nodes] component of each level-1 node, -1 none (node_off based)
   int* ncomp;              // [mp]
