@@ -247,6 +247,22 @@ int mch_pool_slot(const mch_ctx* ctx, int64_t macropoint, int64_t* offset, int64
 /* device pointer of the [(M+1)^d][n_rhs][n_rhs] coefficient array */
 int mch_coeffs_device(const mch_ctx* ctx, double** G);
 
+/* ---- checkpoint / resume between levels (SURVEY.md §5 auxiliaries) ----
+ * The levels are solved in order and level n reads only what levels < n left behind
+ * (Algorithm 1: "for n = 1..L"): the pool of stored fine local solutions
+ * (the parents' phi, Eq. 11), the coefficient array G (Eq. 7) and, with a source set, the load
+ * vectors.  mch_checkpoint_save writes those arrays of this rank, the number of solved levels and
+ * the parameters that fix their layout (d, n, N, M, L, eta, l, interp, layout, keep_all, rank,
+ * world) to `path` (host file, little-endian, raw fp64: bitwise).  mch_checkpoint_load restores
+ * them into a context created with the same parameters and the same medium (the medium is NOT in
+ * the file; a fingerprint of kappa / ids taken on the device is, and must match) and marks
+ * those levels solved (their count in *solved_levels if not NULL), so mch_solve_level continues
+ * at the next one with bitwise the same result as an uninterrupted run.  Level statistics of the restored levels are not kept.
+ * Errors: MCH_EINVAL (NULL, file unreadable / not a checkpoint / parameters or medium differ),
+ * MCH_ECUDA, MCH_ENOMEM. */
+int mch_checkpoint_save(mch_ctx* ctx, const char* path);
+int mch_checkpoint_load(mch_ctx* ctx, const char* path, int* solved_levels);
+
 /* ---- multi-GPU plumbing; NCCL is loaded at run time (libnccl.so.2) ----
  * mch_comm_id: a new NCCL unique id (id_len >= 128 bytes) on one rank, to be broadcast to the
  * others by the caller (e.g. torch.distributed).  mch_comm_init: ncclCommInitRank(world, id, rank)

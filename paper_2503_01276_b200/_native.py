@@ -20,7 +20,7 @@ SYMBOLS = ["mch_create", "mch_set_medium", "mch_reset", "mch_solve_level", "mch_
            "mch_local_solution", "mch_get_level_stats", "mch_level_iterations", "mch_pool_info", "mch_pool_slot",
            "mch_coeffs_device", "mch_set_source", "mch_load_vectors", "mch_macro_solve", "mch_fine_solve",
            "mch_fine_block_averages", "mch_comm_id", "mch_comm_init", "mch_comm_destroy", "mch_shard_plan",
-           "mch_last_error", "mch_destroy"]
+           "mch_checkpoint_save", "mch_checkpoint_load", "mch_last_error", "mch_destroy"]
 
 
 class MchParams(ctypes.Structure):
@@ -93,6 +93,8 @@ def _load():
     lib.mch_pool_info.argtypes = [vp, P(vp), P(i64)]
     lib.mch_pool_slot.argtypes = [vp, i64, P(i64), P(i64)]
     lib.mch_coeffs_device.argtypes = [vp, P(vp)]
+    lib.mch_checkpoint_save.argtypes = [vp, ctypes.c_char_p]
+    lib.mch_checkpoint_load.argtypes = [vp, ctypes.c_char_p, P(i32)]
     lib.mch_set_source.argtypes = [vp, vp, i32]
     lib.mch_load_vectors.argtypes = [vp, vp, ctypes.c_size_t, i32]
     lib.mch_macro_solve.argtypes = [vp, vp, vp, i32, vp, ctypes.c_size_t, i32, dbl, i32, P(i32)]

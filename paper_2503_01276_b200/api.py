@@ -265,6 +265,17 @@ class Homogenizer:
         check(lib.mch_fine_block_averages(self.ctx, up, udev, op, n, odev), self.ctx)
         return out
 
+    def save_checkpoint(self, path):
+        """mch_checkpoint_save: parent pool, coefficients, loads and the solved level to `path`."""
+        check(lib.mch_checkpoint_save(self.ctx, os.fsencode(path)), self.ctx)
+
+    def load_checkpoint(self, path):
+        """mch_checkpoint_load into a context of the same parameters and medium; solve_all()
+        then continues at the next level."""
+        solved = ctypes.c_int32()
+        check(lib.mch_checkpoint_load(self.ctx, os.fsencode(path), ctypes.byref(solved)), self.ctx)
+        self.solved = solved.value
+
     def coeffs_device_ptr(self):
         p = ctypes.c_void_p()
         check(lib.mch_coeffs_device(self.ctx, ctypes.byref(p)), self.ctx)

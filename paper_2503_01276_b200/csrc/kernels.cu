@@ -2077,6 +2077,30 @@ __global__ void k_validate(const double* kappa, const uint8_t* ids, int64_t cnt,
   }
 }
 
+// 64-bit fingerprint of the medium (checkpoints: the file does not hold kappa / ids): wrapping sum of
+// per-cell mixed words, order-independent and so reproducible for any grid
+__global__ void k_fingerprint(const double* kappa, const uint8_t* ids, int64_t cnt, unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long v = (unsigned long long)__double_as_longlong(kappa[i]);
+    v ^= ((unsigned long long)ids[i] + 1ull) * 0x9E3779B97F4A7C15ull;
+    v += (unsigned long long)i * 0xD6E8FEB86659FD93ull;
+    v ^= v >> 32;
+    v *= 0xD6E8FEB86659FD93ull;
+    v ^= v >> 29;
+    acc += v;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+cudaError_t launch_fingerprint(const double* kappa, const uint8_t* ids, int64_t cnt, unsigned long long* out,
+                               cudaStream_t st) {
+  const unsigned grid = (unsigned)std::min<int64_t>((cnt + 255) / 256, 148 * 8);
+  k_fingerprint<<<grid, 256, 0, st>>>(kappa, ids, cnt, out);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------------------
 // host launchers
 size_t pcg_smem(const LevelArgs& A) {

@@ -10,6 +10,8 @@ cudaError_t launch_pinv(const LevelArgs& A, cudaStream_t st);  // R20 windows fl
 cudaError_t launch_pcg(const LevelArgs& A, int threads, cudaStream_t st);
 cudaError_t launch_combine(const LevelArgs& A, int threads, cudaStream_t st);
 cudaError_t launch_gram(const LevelArgs& A, int threads, cudaStream_t st);
+cudaError_t launch_fingerprint(const double* kappa, const uint8_t* ids, int64_t cnt, unsigned long long* out,
+                               cudaStream_t st);
 cudaError_t launch_validate(const double* kappa, const uint8_t* ids, int64_t cnt, int N, int* bad,
                             cudaStream_t st);
 

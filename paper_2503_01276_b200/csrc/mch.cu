@@ -1285,6 +1285,108 @@ extern "C" int mch_level_iterations(const mch_ctx* c, int level, int32_t* out, s
   return MCH_OK;
 }
 
+// ---- checkpoint / resume (include/mch.h) ------------------------------------------------------
+namespace {
+struct CkptHeader {
+  char magic[8];  // "MCHCKPT1"
+  int32_t d, num_continua, levels, eta, oversample, interp, layout, keep_all, rank, world, solved, has_source;
+  int64_t n, M, pool_len, g_len, b_len;
+  uint64_t medium;
+};
+
+int medium_fingerprint(mch_ctx* c, uint64_t* out) {
+  const int64_t n = c->p.n, cells = (c->D == 2) ? n * n : n * n * n;
+  unsigned long long* d = nullptr;
+  CKC(c, dev_alloc(&c->al, (void**)&d, sizeof(unsigned long long)));
+  cudaError_t e = cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->st);
+  if (e == cudaSuccess) e = launch_fingerprint(c->kappa, c->ids, cells, d, c->st);
+  unsigned long long h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, c->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+  dev_free(&c->al, d);
+  CKC(c, e);
+  *out = h;
+  return MCH_OK;
+}
+
+CkptHeader ckpt_header(const mch_ctx* c) {
+  CkptHeader h{};
+  memcpy(h.magic, "MCHCKPT1", 8);
+  h.d = c->p.d; h.num_continua = c->p.num_continua; h.levels = c->p.levels; h.eta = c->p.eta;
+  h.oversample = c->p.oversample; h.interp = c->p.interp; h.layout = c->p.layout; h.keep_all = c->p.keep_all;
+  h.rank = c->p.rank; h.world = c->p.world; h.solved = c->solved; h.has_source = c->has_source ? 1 : 0;
+  h.n = c->p.n; h.M = c->p.M; h.pool_len = c->pool_len;
+  h.g_len = (int64_t)c->plan.all.size() * c->n_rhs * c->n_rhs;
+  h.b_len = c->has_source ? (int64_t)c->plan.all.size() * c->N : 0;
+  return h;
+}
+
+// device array <-> file through a pinned staging buffer (64 MB pieces)
+int ckpt_stream(mch_ctx* c, FILE* f, double* dev, int64_t len, bool save, double* stage, int64_t cap) {
+  for (int64_t o = 0; o < len; o += cap) {
+    const int64_t m = std::min(cap, len - o);
+    if (save) {
+      CKC(c, cudaMemcpyAsync(stage, dev + o, m * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+      CKC(c, cudaStreamSynchronize(c->st));
+      if (fwrite(stage, sizeof(double), (size_t)m, f) != (size_t)m) return fail(c, MCH_EINVAL, "checkpoint: write failed");
+    } else {
+      if (fread(stage, sizeof(double), (size_t)m, f) != (size_t)m) return fail(c, MCH_EINVAL, "checkpoint: file truncated");
+      CKC(c, cudaMemcpyAsync(dev + o, stage, m * sizeof(double), cudaMemcpyHostToDevice, c->st));
+      CKC(c, cudaStreamSynchronize(c->st));
+    }
+  }
+  return MCH_OK;
+}
+
+int ckpt_run(mch_ctx* c, const char* path, bool save) {
+  if (!c || !path) return MCH_EINVAL;
+  if (!c->medium_ok) return fail(c, MCH_EINVAL, "checkpoint: the context holds no valid medium");
+  uint64_t fp = 0;
+  if (int rc = medium_fingerprint(c, &fp)) return rc;
+  FILE* f = fopen(path, save ? "wb" : "rb");
+  if (!f) return fail(c, MCH_EINVAL, std::string("checkpoint: cannot open ") + path);
+  CkptHeader h = ckpt_header(c);
+  h.medium = fp;
+  int rc = MCH_OK;
+  if (save) {
+    if (fwrite(&h, sizeof(h), 1, f) != 1) rc = fail(c, MCH_EINVAL, "checkpoint: write failed");
+  } else {
+    CkptHeader g{};
+    if (fread(&g, sizeof(g), 1, f) != 1 || memcmp(g.magic, "MCHCKPT1", 8) != 0) {
+      rc = fail(c, MCH_EINVAL, "checkpoint: not a checkpoint file");
+    } else {
+      const int solved = g.solved, src = g.has_source;
+      const int64_t bl = g.b_len;
+      g.solved = h.solved; g.has_source = h.has_source; g.b_len = h.b_len;  // state, not layout
+      if (memcmp(&g, &h, sizeof(h)) != 0)
+        rc = fail(c, MCH_EINVAL, (g.medium != h.medium) ? "checkpoint: the medium differs from the one it was taken on"
+                                                        : "checkpoint: parameters differ from the context's");
+      else if (solved < 0 || solved > c->p.levels || (src != 0) != c->has_source)
+        rc = fail(c, MCH_EINVAL, "checkpoint: solved level out of range, or source set on one side only");
+      h.solved = solved;
+      h.b_len = bl;
+    }
+  }
+  double* stage = nullptr;
+  const int64_t cap = (int64_t)8 << 20;
+  if (rc == MCH_OK && cudaMallocHost(&stage, cap * sizeof(double)) != cudaSuccess) rc = fail(c, MCH_ENOMEM, "checkpoint: staging buffer");
+  if (rc == MCH_OK) rc = ckpt_stream(c, f, c->pool, h.pool_len, save, stage, cap);
+  if (rc == MCH_OK) rc = ckpt_stream(c, f, c->G, h.g_len, save, stage, cap);
+  if (rc == MCH_OK && h.b_len > 0) rc = ckpt_stream(c, f, c->bload.as<double>(), h.b_len, save, stage, cap);
+  if (stage) cudaFreeHost(stage);
+  if (fclose(f) != 0 && rc == MCH_OK && save) rc = fail(c, MCH_EINVAL, "checkpoint: close failed");
+  if (rc == MCH_OK && !save) c->solved = h.solved;
+  return rc;
+}
+}  // namespace
+
+extern "C" int mch_checkpoint_save(mch_ctx* c, const char* path) { return ckpt_run(c, path, true); }
+extern "C" int mch_checkpoint_load(mch_ctx* c, const char* path, int* solved_levels) {
+  const int rc = ckpt_run(c, path, false);
+  if (rc == MCH_OK && solved_levels) *solved_levels = c->solved;
+  return rc;
+}
+
 extern "C" int mch_pool_info(const mch_ctx* c, double** pool, int64_t* len) {
   if (!c) return MCH_EINVAL;
   if (pool) *pool = c->pool;

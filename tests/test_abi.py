@@ -79,3 +79,5 @@ def test_null_context_is_rejected():
     assert lib.mch_solve_level(None, 1) == -1
     assert lib.mch_effective_coeffs(None, buf.ctypes.data, 16, 0) == -1
     assert lib.mch_set_medium(None, buf.ctypes.data, buf.ctypes.data, 0) == -1
+    assert lib.mch_checkpoint_save(None, b"/tmp/x.mchckpt") == -1
+    assert lib.mch_checkpoint_load(None, b"/tmp/x.mchckpt", None) == -1

@@ -623,6 +623,43 @@ def test_coarse_space_second_pass_config5_level2(monkeypatch):
         assert g_err(G1[i], G0[i]) < G_TOL, (i, g_err(G1[i], G0[i]))
 
 
+@pytest.mark.parametrize("d,n,M,L,N", [(2, 64, 8, 3, 2), (3, 16, 4, 2, 2)])
+def test_checkpoint_resume_bitwise(d, n, M, L, N, tmp_path):
+    """mch_checkpoint_save after level L-1, mch_checkpoint_load into a fresh context, last level
+    solved there: coefficients and local solutions bitwise equal to the uninterrupted run (which
+    the parity tests compare with the oracle); a different medium or hierarchy is refused."""
+    from paper_2503_01276_b200._native import MchError
+    H = _gpu()
+    kap, ids = _admissible(d, n, M, N, 300 + d)
+    path = str(tmp_path / "levels.mchckpt")
+    with H(d, n, N, M, L, 2, kap, ids, keep_all=True) as h:
+        for lev in range(1, L):
+            h.solve_level(lev)
+        h.save_checkpoint(path)
+        h.solve_all()
+        G0 = h.effective_coeffs()
+        pts = h.level_macropoints(L)
+        k0 = [int(m) for m in pts[:3]]  # linear macropoint indices
+        phi0 = [h.local_solution(k, r) for k in k0 for r in (0, N * (1 + d) - 1)]
+    with H(d, n, N, M, L, 2, kap, ids, keep_all=True) as h:
+        h.load_checkpoint(path)
+        assert h.solved == L - 1
+        h.solve_all()
+        G1 = h.effective_coeffs()
+        phi1 = [h.local_solution(k, r) for k in k0 for r in (0, N * (1 + d) - 1)]
+    assert np.array_equal(G0, G1)
+    for a, b in zip(phi0, phi1):
+        assert np.array_equal(a, b)
+    kap2 = kap.copy()
+    kap2.flat[7] *= 1.5
+    with H(d, n, N, M, L, 2, kap2, ids, keep_all=True) as h:
+        with pytest.raises(MchError, match="medium differs"):
+            h.load_checkpoint(path)
+    with H(d, n, N, M, L, 2, kap, ids, keep_all=False) as h:
+        with pytest.raises(MchError, match="parameters differ"):
+            h.load_checkpoint(path)
+
+
 def test_level_log_jsonl(tmp_path):
     """solve_all(log=...) appends one JSON record per level with the library's level stats."""
     import json
