@@ -131,6 +131,17 @@ def _sample_points(cfg):
     return pts
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 class OracleSample:
     def __init__(self, cfg, kap, ids):
         from oracle import Oracle
@@ -183,7 +194,8 @@ def run_reference(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config_block(cfg, 1),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": smp.text()},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": smp.text(),
+                             "cpu_model": _cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -461,7 +473,8 @@ def main():
         smp.step()  # ancestry once
         per = smp.step()
         line["cpu_baseline"] = {"value": smp.value(per), "unit": UNIT, "cores": 1, "kind": "oracle",
-                                "sample": smp.text(), "wall_s": round(time.time() - t0, 1)}
+                                "sample": smp.text(), "wall_s": round(time.time() - t0, 1),
+                                "cpu_model": _cpu_model()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
