@@ -24,6 +24,15 @@
 #include "kernels.h"
 #include "pcg3d_common.cuh"
 
+#ifndef MCH_L1_NW
+#define MCH_L1_NW 14  // warps per CTA of the level-1 cluster kernel (98 row tasks of a 49-node window: 7 per warp)
+#endif
+#ifndef MCH_L1_NW2
+#define MCH_L1_NW2 20  // the same for a cluster of two (half the planes per CTA): 20 warps at 96 registers, c5 level-1 PCG 44.5 -> 42.6 ms (25 warps at 72 registers: 52 ms; one CTA per problem, config 4: 14 warps 373 ms, 20 warps 386 ms)
+#endif
+#ifndef MCH_P25_RW
+#define MCH_P25_RW 1  // node rows per warp of the 25-node cluster kernel (1: 25 warps at 72 registers, c5 level-2 PCG 35.4 -> 33.1 ms)
+#endif
 #ifndef MCH_P25_MINB
 #define MCH_P25_MINB 1  // CTAs per SM of the 25-node cluster kernel (2: 72 registers, 968 B spills, 44 -> 69 ms)
 #endif
@@ -37,7 +46,7 @@ struct VX { double x, d; int cm; };        // x / D^-1 / component of one node
 }  // namespace
 
 template <int N, int NW, int CS>
-__global__ void __launch_bounds__(NW * 32, 448 / (NW * 32)) k_pcg3d_l1c(LevelArgs A) {
+__global__ void __launch_bounds__(NW * 32, (NW * 32 <= 448) ? 448 / (NW * 32) : 1) k_pcg3d_l1c(LevelArgs A) {
   constexpr int NT = 98;  // at most 98 row tasks = 49 rows x 2 segments
   constexpr int NQ = 27 * N;
   cg::cluster_group cl = cg::this_cluster();
@@ -1268,10 +1277,10 @@ static cudaError_t go_l1c(const LevelArgs& A, cudaStream_t st) {
 template <int N>
 static cudaError_t go_l1c_n(const LevelArgs& A, int cs, cudaStream_t st) {
   switch (cs) {
-    case 1: return go_l1c<N, 14, 1>(A, st);
-    case 2: return go_l1c<N, 14, 2>(A, st);
-    case 4: return go_l1c<N, 14, 4>(A, st);
-    case 8: return go_l1c<N, 14, 8>(A, st);
+    case 1: return go_l1c<N, MCH_L1_NW, 1>(A, st);
+    case 2: return go_l1c<N, MCH_L1_NW2, 2>(A, st);
+    case 4: return go_l1c<N, MCH_L1_NW, 4>(A, st);
+    case 8: return go_l1c<N, MCH_L1_NW, 8>(A, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -1320,7 +1329,7 @@ template <int N>
 static cudaError_t go_3dc_n(const LevelArgs& A, int nxm, int cs, cudaStream_t st) {
   if (nxm == 25) {
     switch (cs) {
-      case 2: return go_3dc<N, 25, 2, MCH_P25_MINB, 2>(A, st);
+      case 2: return go_3dc<N, 25, MCH_P25_RW, MCH_P25_MINB, 2>(A, st);
       case 4: return go_3dc<N, 25, 2, 1, 4>(A, st);
     }
   } else if (nxm == 13) {
